@@ -1,0 +1,81 @@
+"""Seeded synthetic inputs for the MoE block -- shared by tests/ and bench.py.
+
+This module holds NONE of the method's arithmetic: it only draws random
+numbers and rounds them to the storage dtype. Both the CUDA path and the
+oracle consume the exact bytes it returns (the oracle decodes bf16 itself).
+
+Recipe (PAPER.md is silent, Sec. 5 used real
+Mixtral weights and OpenOrca prompts, which are out of scope):
+  x   ~ N(0, 1)          [T, d]
+  W_g ~ N(0, 1/d)        [E, d]
+  W1  ~ N(0, 1/d)        [E, f, d]   (HF nn.Linear [out, in])
+  W3  ~ N(0, 1/d)        [E, f, d]
+  W2  ~ N(0, 1/f)        [E, d, f]
+all rounded to bf16 with round-to-nearest-even (torch's `.to(torch.bfloat16)`),
+or kept fp32 for the tiny config's fp32 self-tests (BASELINE.json configs[0]).
+This gives router logits with std ~1, i.e. real top-2 competition, and an
+expert output rms ~0.6.
+
+Seeds: tensor i of layer L draws from torch.Generator(device).manual_seed(
+seed * 1000 + 100 * L + i) with i = 0 (x), 1 (W_g), 2 (W1), 3 (W3), 4 (W2).
+Large configs may be drawn on a CUDA generator (fast); the bytes are then
+copied to the host for the oracle, which is allowed because torch's RNG is
+plumbing, not the CUDA path under test.
+"""
+from __future__ import annotations
+
+import dataclasses
+import math
+
+import torch
+
+
+@dataclasses.dataclass(frozen=True)
+class MoEShape:
+    T: int
+    d: int
+    f: int
+    E: int
+    k: int
+
+
+# BASELINE.json configs (numbered from 0 here): 0 tiny, 1 decode, 2 prefill.
+TINY = MoEShape(T=16, d=64, f=128, E=4, k=2)
+DECODE = MoEShape(T=64, d=4096, f=14336, E=8, k=2)
+PREFILL = MoEShape(T=64 * 512, d=4096, f=14336, E=8, k=2)
+
+
+def _randn(shape, std, seed, device, dtype):
+    g = torch.Generator(device=device)
+    g.manual_seed(int(seed))
+    t = torch.randn(shape, generator=g, device=device, dtype=torch.float32)
+    if std != 1.0:
+        t.mul_(std)
+    return t.to(dtype)
+
+
+def make_tokens(T, d, seed, layer=0, device="cpu", dtype=torch.bfloat16):
+    return _randn((T, d), 1.0, seed * 1000 + 100 * layer + 0, device, dtype)
+
+
+def make_weights(d, f, E, seed, layer=0, device="cpu", dtype=torch.bfloat16):
+    """Return dict wg [E,d], w1 [E,f,d], w3 [E,f,d], w2 [E,d,f] (HF layout)."""
+    base = seed * 1000 + 100 * layer
+    return {
+        "wg": _randn((E, d), 1.0 / math.sqrt(d), base + 1, device, dtype),
+        "w1": _randn((E, f, d), 1.0 / math.sqrt(d), base + 2, device, dtype),
+        "w3": _randn((E, f, d), 1.0 / math.sqrt(d), base + 3, device, dtype),
+        "w2": _randn((E, d, f), 1.0 / math.sqrt(f), base + 4, device, dtype),
+    }
+
+
+def make_inputs(shape: MoEShape, seed, layer=0, device="cpu", dtype=torch.bfloat16):
+    w = make_weights(shape.d, shape.f, shape.E, seed, layer, device, dtype)
+    w["x"] = make_tokens(shape.T, shape.d, seed, layer, device, dtype)
+    return w
+
+
+def bf16_bits(t: torch.Tensor):
+    """bf16 tensor -> numpy uint16 view of the same bytes (host)."""
+    assert t.dtype == torch.bfloat16
+    return t.detach().cpu().contiguous().view(torch.int16).numpy().view("uint16")
