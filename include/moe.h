@@ -1,0 +1,205 @@
+/* include/moe.h -- C ABI of libmoe: the batched Mixtral-8x7B sparse-MoE FFN block
+ * on B200 (sm_100a).
+ *
+ * What the calls compute.  BASELINE.json north_star: "router GEMM, softmax,
+ * top-2 expert selection with renormalised gate weights, token permutation by
+ * expert, grouped SwiGLU expert GEMMs (w1/w3 then w2) and a weighted
+ * scatter-combine back to token order", behind "moe_init / moe_forward(tokens
+ * [T,4096], router_w, expert_w, out) / moe_destroy". PAPER.md names the model
+ * (Sec. 2, Sec. 4.1, Sec. 5: Mixtral 8x7B) and the parallel
+ * variants (Sec. 4.1: tensor parallel = "splitting tensors into
+ * non-overlapping pieces", expert parallel = "distributes experts of an MoE
+ * across GPUs") but prints no formula; the block is (reading R1):
+ *     l = x W_g^T ; S = top-k(l) ; w_j = softmax(l)_{S_j} / sum_j' softmax(l)_{S_j'}
+ *     y = sum_j w_j * W2_{S_j} ( silu(W1_{S_j} x) * (W3_{S_j} x) )
+ * Precision contract (reading R7): bf16 inputs/weights; router logits, gates,
+ * expert outputs and the combine in fp32; exactly two roundings to bf16 (the
+ * SwiGLU activation h, and the final output, both round-to-nearest-even).
+ *
+ * Conventions.
+ *   - All tensors are row-major, contiguous, 16-byte aligned device memory
+ *     unless a parameter says "host". bf16 = IEEE bfloat16 bit patterns.
+ *   - "stream" is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *   - The caller owns every buffer it passes (tokens, weights, out, aux) and
+ *     the NCCL communicator; the library owns the context, its workspace and a
+ *     TMA-descriptor cache. The library never frees or retains caller memory
+ *     beyond the call that received it, except the descriptor cache, which
+ *     stores weight *addresses* (not contents) and is keyed by them.
+ *   - Calls validate their arguments BEFORE enqueuing anything; an invalid
+ *     argument returns MOE_ERR_INVALID and nothing runs. Kernel launches are
+ *     asynchronous; an asynchronous device fault surfaces as MOE_ERR_CUDA on a
+ *     later call and is sticky (MOE_ERR_STATE thereafter for that context).
+ *   - No exception crosses the ABI; the library never calls exit().
+ *   - One host thread per context at a time.
+ *   - There is no CPU fallback: every step of the forward runs in libmoe's own
+ *     CUDA kernels on the device (sm_100a). A machine without an sm_100 GPU
+ *     gets MOE_ERR_UNSUPPORTED from moe_init.
+ */
+#ifndef PAPER_2408_00008_B200_MOE_H
+#define PAPER_2408_00008_B200_MOE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MOE_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define MOE_API __attribute__((visibility("default")))
+#else
+#define MOE_API
+#endif
+
+typedef struct moe_ctx moe_ctx; /* opaque, library-owned */
+
+typedef enum {
+    MOE_OK = 0,
+    MOE_ERR_INVALID = 1,     /* bad argument; nothing was enqueued            */
+    MOE_ERR_UNSUPPORTED = 2, /* shape / feature / device not supported        */
+    MOE_ERR_OOM = 3,         /* workspace allocation failed in moe_init        */
+    MOE_ERR_CUDA = 4,        /* CUDA launch or runtime failure (see last_error)*/
+    MOE_ERR_NCCL = 5,        /* NCCL failure (EP / TP variants)                */
+    MOE_ERR_STATE = 6        /* context poisoned by an earlier device fault    */
+} moe_status;
+
+/* Parallel variant (Sec. 4.1). */
+typedef enum {
+    MOE_PAR_NONE = 0, /* single GPU: all experts, all ffn columns                  */
+    MOE_PAR_EP = 1,   /* expert parallel: rank r owns experts [r*E/G, (r+1)*E/G);
+                         tokens are sharded by the caller (T may differ per rank);
+                         rows are exchanged with NCCL all-to-all (bf16 out, fp32 back) */
+    MOE_PAR_TP = 2    /* tensor parallel: rank r owns ffn columns [r*f/G, (r+1)*f/G)
+                         of every expert; every rank passes the same tokens; the
+                         fp32 partial outputs are summed across ranks (all-reduce) */
+} moe_par;
+
+/* Flags (moe_config.flags). */
+#define MOE_FLAG_RESIDUAL    0x1u /* out = x + MoE(x): C5 stack composition (reading R12) */
+#define MOE_FLAG_FORCE_SWAP  0x2u /* always use the decode (weights-as-M, swap-AB) GEMMs */
+#define MOE_FLAG_FORCE_TILED 0x4u /* always use the prefill (tokens-as-M) GEMMs          */
+#define MOE_FLAG_NO_PDL      0x8u /* disable programmatic dependent launch               */
+
+typedef struct {
+    int32_t hidden;      /* d: 4096 for Mixtral (C1: 64). Must be a multiple of 64.   */
+    int32_t ffn;         /* f: 14336 for Mixtral (C1: 128). f/G must be a multiple of 128. */
+    int32_t num_experts; /* E: 8 for Mixtral. 1 <= E <= 32; E % G == 0 for EP.       */
+    int32_t top_k;       /* k: 2 for Mixtral; 1 is also supported. k <= E.           */
+    int32_t max_tokens;  /* per-rank T capacity; sizes the workspace. >= 1.           */
+    int32_t par;         /* moe_par                                                    */
+    int32_t world_size;  /* G (1 for MOE_PAR_NONE)                                     */
+    int32_t rank;        /* 0 <= rank < G                                              */
+    void* nccl_comm;     /* ncclComm_t from moe_nccl_comm_init (caller-owned); EP/TP  */
+    uint32_t flags;      /* MOE_FLAG_*                                                 */
+    int32_t split_k;     /* decode w2 GEMM split-K factor; 0 = automatic               */
+    int32_t device;      /* CUDA device ordinal the context binds to; -1 = current    */
+    int32_t reserved[6]; /* must be zero                                               */
+} moe_config;
+
+/* Packed expert weights of THIS rank (device, bf16, produced by moe_pack_weights).
+ *   w13: [E_local, 2*f_local, d] -- w1 and w3 rows interleaved in blocks of 128:
+ *        packed row 256*b + i     = w1 row 128*b + i  (i < 128)
+ *        packed row 256*b + 128+i = w3 row 128*b + i
+ *   w2:  [E_local, d, f_local]   -- HF layout, ffn slice of this rank.          */
+typedef struct {
+    const void* w13;
+    const void* w2;
+} moe_expert_weights;
+
+/* Optional debug / parity outputs (any pointer may be NULL). Device memory,
+ * T = this call's token count on this rank.
+ *   logits  [T, E] fp32  router logits, fp32 accumulation, never rounded to bf16
+ *   topk_idx[T, k] int32 selected experts, slot 0 = larger logit, ties -> lower index
+ *   topk_w  [T, k] fp32  renormalised gates
+ *   expert_counts [E_local] int32 rows routed to each local expert
+ *   expert_offsets [E_local+1] int32 first row of each expert's segment in the
+ *                  permuted buffer (segments padded to multiples of 128 rows)
+ *   pos     [T, k] int32 permuted row of each assignment (single-GPU / TP only)
+ *   out_f32 [T, d] fp32  the combined output before the final bf16 rounding      */
+typedef struct {
+    float* logits;
+    int32_t* topk_idx;
+    float* topk_w;
+    int32_t* expert_counts;
+    int32_t* expert_offsets;
+    int32_t* pos;
+    float* out_f32;
+} moe_aux;
+
+/* Create a context bound to cfg->device: validates cfg, allocates the
+ * workspace for max_tokens (permuted tokens, activations, fp32 expert outputs,
+ * routing metadata; about 3.5 GB at max_tokens = 32768 for Mixtral), and
+ * encodes the workspace TMA descriptors. Returns MOE_ERR_UNSUPPORTED if the
+ * device is not sm_100. *out is set only on MOE_OK. */
+MOE_API moe_status moe_init(const moe_config* cfg, moe_ctx** out);
+
+/* Bytes of this rank's packed w13 / w2 buffers for cfg (no device work). */
+MOE_API moe_status moe_packed_sizes(const moe_config* cfg, size_t* w13_bytes, size_t* w2_bytes);
+
+/* Pack HF-layout weights (device, bf16) into this rank's layout (see
+ * moe_expert_weights): w1, w3 [E, f, d], w2 [E, d, f] are the FULL model
+ * tensors; the kernel extracts this rank's expert range (EP) or ffn slice (TP).
+ * w13_out / w2_out must hold moe_packed_sizes bytes. Enqueued on stream. */
+MOE_API moe_status moe_pack_weights(moe_ctx* ctx, const void* w1, const void* w3, const void* w2,
+                            void* w13_out, void* w2_out, void* stream);
+
+/* The block forward. tokens [T, d] bf16, router_w [E, d] bf16 (full, replicated
+ * on every rank), out [T, d] bf16. 0 <= T <= max_tokens. T == 0 enqueues nothing
+ * (except the EP collectives, in which every rank takes part). No host
+ * synchronisation on the single-GPU and TP paths, so they are CUDA-graph
+ * capturable; no allocation. aux may be NULL. */
+MOE_API moe_status moe_forward(moe_ctx* ctx, const void* tokens, int32_t T, const void* router_w,
+                       const moe_expert_weights* weights, void* out, const moe_aux* aux,
+                       void* stream);
+
+/* Same as moe_forward with the routing supplied by the caller (the oracle's
+ * "forced routing" mode): topk_idx [T, k] int32
+ * (distinct experts per token, each in [0, E)), topk_w [T, k] fp32 gates used
+ * as given. Single-GPU and TP only. Indices are validated on the device: an
+ * out-of-range index makes the routing kernel trap (MOE_ERR_CUDA later). */
+MOE_API moe_status moe_forward_routed(moe_ctx* ctx, const void* tokens, int32_t T, const int32_t* topk_idx,
+                              const float* topk_w, const moe_expert_weights* weights, void* out,
+                              const moe_aux* aux, void* stream);
+
+/* End-to-end call with HOST token/output buffers (ideally pinned): copies
+ * tokens_host [T, d] bf16 to a library-owned device buffer, runs moe_forward,
+ * copies the result to out_host [T, d] bf16, all enqueued on stream. The caller
+ * synchronises the stream before reading out_host. */
+MOE_API moe_status moe_forward_host(moe_ctx* ctx, const void* tokens_host, int32_t T, const void* router_w,
+                            const moe_expert_weights* weights, void* out_host, void* stream);
+
+/* Release the context and its workspace. NULL is a no-op. */
+MOE_API moe_status moe_destroy(moe_ctx* ctx);
+
+/* Last error text of ctx (or of the last failed moe_init when ctx == NULL). */
+MOE_API const char* moe_last_error(const moe_ctx* ctx);
+MOE_API const char* moe_status_string(moe_status s);
+
+/* Instrumentation (bench.py).
+ * moe_set_profiling(ctx, 1): every subsequent forward records a CUDA event pair
+ *   around each kernel on the launch stream; moe_kernel_times returns, per
+ *   kernel slot, the summed milliseconds and launch count since the last
+ *   moe_reset_profile (it synchronises on the recorded events). Slots:
+ *   0 router, 1 permute, 2 gemm1(w1/w3+SwiGLU), 3 gemm2(w2), 4 combine,
+ *   5 dispatch (EP), 6 exchange-back / all-reduce (EP/TP), 7 pack.
+ * moe_launch_count: kernels libmoe launched since context creation.  */
+#define MOE_NUM_KERNEL_SLOTS 8
+MOE_API moe_status moe_set_profiling(moe_ctx* ctx, int enable);
+MOE_API moe_status moe_reset_profile(moe_ctx* ctx);
+MOE_API moe_status moe_kernel_times(moe_ctx* ctx, double* ms /*[8]*/, int64_t* launches /*[8]*/);
+MOE_API int64_t moe_launch_count(const moe_ctx* ctx);
+
+/* NCCL plumbing for the EP / TP variants (libnccl.so.2 is loaded at run time;
+ * the single-GPU path never touches NCCL). id128: 128-byte ncclUniqueId buffer,
+ * broadcast by the caller (e.g. over the host process group). */
+MOE_API moe_status moe_nccl_unique_id(void* id128);
+MOE_API moe_status moe_nccl_comm_init(const void* id128, int32_t world, int32_t rank, int32_t device,
+                              void** comm);
+MOE_API moe_status moe_nccl_comm_destroy(void* comm);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PAPER_2408_00008_B200_MOE_H */

@@ -1,0 +1,256 @@
+"""paper_2408_00008_b200 -- B200-native Mixtral-8x7B sparse-MoE block (ScaleLLM's
+engine hot path, arXiv 2408.00008 Sec. 4.1) behind the C ABI of include/moe.h.
+
+This module is argument marshalling only (ctypes over libmoe.so): every step of
+the forward runs in libmoe's CUDA kernels. torch is used for device memory and
+streams. There is no CPU fallback: if libmoe.so is missing, importing this
+package raises; if no sm_100 device is present, moe_init fails loudly.
+
+Names follow the C ABI: moe_init, moe_packed_sizes, moe_pack_weights,
+moe_forward, moe_forward_routed, moe_forward_host, moe_destroy, plus the
+instrumentation and NCCL helpers. `MoEBlock` is a small convenience owner of a
+context and its packed weights.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libmoe.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"libmoe.so not built at {LIB_PATH}: run `python -c 'import __graft_entry__ as g; g.build()'`")
+
+_lib = ctypes.CDLL(LIB_PATH)
+
+MOE_OK, MOE_ERR_INVALID, MOE_ERR_UNSUPPORTED, MOE_ERR_OOM, MOE_ERR_CUDA, MOE_ERR_NCCL, MOE_ERR_STATE = range(7)
+MOE_PAR_NONE, MOE_PAR_EP, MOE_PAR_TP = 0, 1, 2
+MOE_FLAG_RESIDUAL, MOE_FLAG_FORCE_SWAP, MOE_FLAG_FORCE_TILED, MOE_FLAG_NO_PDL = 0x1, 0x2, 0x4, 0x8
+NUM_KERNEL_SLOTS = 8
+KERNEL_SLOTS = ("router", "permute", "gemm1_w13_swiglu", "gemm2_w2", "combine", "dispatch", "exchange", "pack")
+
+# every symbol include/moe.h declares (tests check the .so exports all of them)
+EXPORTED = ("moe_init", "moe_packed_sizes", "moe_pack_weights", "moe_forward", "moe_forward_routed",
+            "moe_forward_host", "moe_destroy", "moe_last_error", "moe_status_string", "moe_set_profiling",
+            "moe_reset_profile", "moe_kernel_times", "moe_launch_count", "moe_nccl_unique_id",
+            "moe_nccl_comm_init", "moe_nccl_comm_destroy")
+
+
+class moe_config(ctypes.Structure):
+    _fields_ = [("hidden", ctypes.c_int32), ("ffn", ctypes.c_int32), ("num_experts", ctypes.c_int32),
+                ("top_k", ctypes.c_int32), ("max_tokens", ctypes.c_int32), ("par", ctypes.c_int32),
+                ("world_size", ctypes.c_int32), ("rank", ctypes.c_int32), ("nccl_comm", ctypes.c_void_p),
+                ("flags", ctypes.c_uint32), ("split_k", ctypes.c_int32), ("device", ctypes.c_int32),
+                ("reserved", ctypes.c_int32 * 6)]
+
+
+class moe_expert_weights(ctypes.Structure):
+    _fields_ = [("w13", ctypes.c_void_p), ("w2", ctypes.c_void_p)]
+
+
+class moe_aux(ctypes.Structure):
+    _fields_ = [("logits", ctypes.c_void_p), ("topk_idx", ctypes.c_void_p), ("topk_w", ctypes.c_void_p),
+                ("expert_counts", ctypes.c_void_p), ("expert_offsets", ctypes.c_void_p), ("pos", ctypes.c_void_p),
+                ("out_f32", ctypes.c_void_p)]
+
+
+_P, _I32, _I64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
+_sig = {
+    "moe_init": ([ctypes.POINTER(moe_config), ctypes.POINTER(_P)], _I32),
+    "moe_packed_sizes": ([ctypes.POINTER(moe_config), ctypes.POINTER(ctypes.c_size_t),
+                          ctypes.POINTER(ctypes.c_size_t)], _I32),
+    "moe_pack_weights": ([_P, _P, _P, _P, _P, _P, _P], _I32),
+    "moe_forward": ([_P, _P, _I32, _P, ctypes.POINTER(moe_expert_weights), _P, ctypes.POINTER(moe_aux), _P], _I32),
+    "moe_forward_routed": ([_P, _P, _I32, _P, _P, ctypes.POINTER(moe_expert_weights), _P,
+                            ctypes.POINTER(moe_aux), _P], _I32),
+    "moe_forward_host": ([_P, _P, _I32, _P, ctypes.POINTER(moe_expert_weights), _P, _P], _I32),
+    "moe_destroy": ([_P], _I32),
+    "moe_last_error": ([_P], ctypes.c_char_p),
+    "moe_status_string": ([_I32], ctypes.c_char_p),
+    "moe_set_profiling": ([_P, ctypes.c_int], _I32),
+    "moe_reset_profile": ([_P], _I32),
+    "moe_kernel_times": ([_P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_I64)], _I32),
+    "moe_launch_count": ([_P], _I64),
+    "moe_nccl_unique_id": ([_P], _I32),
+    "moe_nccl_comm_init": ([_P, _I32, _I32, _I32, ctypes.POINTER(_P)], _I32),
+    "moe_nccl_comm_destroy": ([_P], _I32),
+}
+for _name, (_args, _res) in _sig.items():
+    _fn = getattr(_lib, _name)
+    _fn.argtypes = _args
+    _fn.restype = _res
+
+
+class MoEError(RuntimeError):
+    def __init__(self, status, msg):
+        self.status = status
+        super().__init__(f"{_lib.moe_status_string(status).decode()}: {msg}")
+
+
+def _check(status, ctx=None):
+    if status != MOE_OK:
+        raise MoEError(status, (_lib.moe_last_error(ctx) or b"").decode())
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    if isinstance(t, int):
+        return t
+    return t.data_ptr()
+
+
+def _stream(stream):
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+def make_config(hidden, ffn, num_experts, top_k, max_tokens, par=MOE_PAR_NONE, world_size=1, rank=0,
+                nccl_comm=None, flags=0, split_k=0, device=-1) -> moe_config:
+    c = moe_config()
+    c.hidden, c.ffn, c.num_experts, c.top_k, c.max_tokens = hidden, ffn, num_experts, top_k, max_tokens
+    c.par, c.world_size, c.rank, c.nccl_comm = par, world_size, rank, nccl_comm
+    c.flags, c.split_k, c.device = flags, split_k, device
+    return c
+
+
+# ------------------------------------------------------------------ C-ABI mirrors
+def moe_init(cfg: moe_config):
+    ctx = _P()
+    _check(_lib.moe_init(ctypes.byref(cfg), ctypes.byref(ctx)))
+    return ctx.value
+
+
+def moe_packed_sizes(cfg: moe_config):
+    a, b = ctypes.c_size_t(), ctypes.c_size_t()
+    _check(_lib.moe_packed_sizes(ctypes.byref(cfg), ctypes.byref(a), ctypes.byref(b)))
+    return a.value, b.value
+
+
+def moe_pack_weights(ctx, w1, w3, w2, w13_out, w2_out, stream=None):
+    _check(_lib.moe_pack_weights(ctx, _ptr(w1), _ptr(w3), _ptr(w2), _ptr(w13_out), _ptr(w2_out),
+                                 _stream(stream)), ctx)
+
+
+def _aux(aux):
+    if aux is None:
+        return None
+    a = moe_aux()
+    for k in ("logits", "topk_idx", "topk_w", "expert_counts", "expert_offsets", "pos", "out_f32"):
+        setattr(a, k, _ptr(aux.get(k)))
+    return ctypes.byref(a)
+
+
+def _weights(w13, w2):
+    return ctypes.byref(moe_expert_weights(_ptr(w13), _ptr(w2)))
+
+
+def moe_forward(ctx, tokens, T, router_w, w13, w2, out, aux=None, stream=None):
+    _check(_lib.moe_forward(ctx, _ptr(tokens), int(T), _ptr(router_w), _weights(w13, w2), _ptr(out), _aux(aux),
+                            _stream(stream)), ctx)
+
+
+def moe_forward_routed(ctx, tokens, T, topk_idx, topk_w, w13, w2, out, aux=None, stream=None):
+    _check(_lib.moe_forward_routed(ctx, _ptr(tokens), int(T), _ptr(topk_idx), _ptr(topk_w), _weights(w13, w2),
+                                   _ptr(out), _aux(aux), _stream(stream)), ctx)
+
+
+def moe_forward_host(ctx, tokens_host, T, router_w, w13, w2, out_host, stream=None):
+    _check(_lib.moe_forward_host(ctx, _ptr(tokens_host), int(T), _ptr(router_w), _weights(w13, w2),
+                                 _ptr(out_host), _stream(stream)), ctx)
+
+
+def moe_destroy(ctx):
+    _check(_lib.moe_destroy(ctx))
+
+
+def moe_last_error(ctx=None) -> str:
+    return (_lib.moe_last_error(ctx) or b"").decode()
+
+
+def moe_set_profiling(ctx, enable: bool):
+    _check(_lib.moe_set_profiling(ctx, int(bool(enable))), ctx)
+
+
+def moe_reset_profile(ctx):
+    _check(_lib.moe_reset_profile(ctx), ctx)
+
+
+def moe_kernel_times(ctx):
+    ms = (ctypes.c_double * NUM_KERNEL_SLOTS)()
+    n = (_I64 * NUM_KERNEL_SLOTS)()
+    _check(_lib.moe_kernel_times(ctx, ms, n), ctx)
+    return {KERNEL_SLOTS[i]: (ms[i], n[i]) for i in range(NUM_KERNEL_SLOTS)}
+
+
+def moe_launch_count(ctx) -> int:
+    return int(_lib.moe_launch_count(ctx))
+
+
+def moe_nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(_lib.moe_nccl_unique_id(buf))
+    return buf.raw
+
+
+def moe_nccl_comm_init(uid: bytes, world: int, rank: int, device: int):
+    comm = _P()
+    buf = ctypes.create_string_buffer(uid, 128)
+    _check(_lib.moe_nccl_comm_init(buf, world, rank, device, ctypes.byref(comm)))
+    return comm.value
+
+
+def moe_nccl_comm_destroy(comm):
+    _check(_lib.moe_nccl_comm_destroy(comm))
+
+
+# ------------------------------------------------------------------ convenience owner
+class MoEBlock:
+    """Owns a libmoe context and this rank's packed weights (torch device memory).
+
+    w1, w3: [E, f, d], w2: [E, d, f], router_w: [E, d] -- bf16 HF layout (device).
+    """
+
+    def __init__(self, router_w, w1, w3, w2, top_k=2, max_tokens=64, par=MOE_PAR_NONE, world_size=1, rank=0,
+                 nccl_comm=None, flags=0, split_k=0, device=None):
+        dev = router_w.device if device is None else torch.device(device)
+        E, f, d = w1.shape
+        self.cfg = make_config(d, f, E, top_k, max_tokens, par, world_size, rank, nccl_comm, flags, split_k,
+                               dev.index if dev.index is not None else torch.cuda.current_device())
+        self.ctx = moe_init(self.cfg)
+        self.d, self.f, self.E, self.k = d, f, E, top_k
+        b13, b2 = moe_packed_sizes(self.cfg)
+        self.w13 = torch.empty(b13 // 2, dtype=torch.bfloat16, device=dev)
+        self.w2 = torch.empty(b2 // 2, dtype=torch.bfloat16, device=dev)
+        self.router_w = router_w.contiguous()
+        moe_pack_weights(self.ctx, w1.contiguous(), w3.contiguous(), w2.contiguous(), self.w13, self.w2)
+
+    def forward(self, x, out=None, aux=None, stream=None):
+        T = x.shape[0]
+        if out is None:
+            out = torch.empty_like(x)
+        moe_forward(self.ctx, x, T, self.router_w, self.w13, self.w2, out, aux, stream)
+        return out
+
+    def forward_routed(self, x, topk_idx, topk_w, out=None, aux=None, stream=None):
+        if out is None:
+            out = torch.empty_like(x)
+        moe_forward_routed(self.ctx, x, x.shape[0], topk_idx, topk_w, self.w13, self.w2, out, aux, stream)
+        return out
+
+    def close(self):
+        if getattr(self, "ctx", None):
+            moe_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,373 @@
+// gemm_sm100.cuh -- grouped expert GEMMs of the MoE block on tcgen05 / TMEM / TMA.
+//
+// Steps a7 / a8 of SURVEY.md Sec. 8(a) (BASELINE.json north_star: "grouped bf16
+// expert GEMMs on tcgen05/TMEM fed by TMA, with the SiLU-gate fused into the
+// w1/w3 epilogue"), for every expert segment of the permuted token buffer:
+//   GEMM1 (+SwiGLU): h[r, i] = bf16_rne( silu(a) * b ),  a = x_r . W1_e[i,:],  b = x_r . W3_e[i,:]
+//   GEMM2          : y[r, c] = sum_i h[r, i] * W2_e[c, i]            (fp32, never rounded)
+// with fp32 accumulation in TMEM (PAPER.md prints no formula; R1, R7).
+//
+// One persistent, warp-specialised kernel template, four instantiations:
+//   kG1Tiled / kG2Tiled (prefill): A = 128 permuted token rows (M=128), B = 256
+//       weight rows (N=256); tokens vary fastest so an expert's weight tile is
+//       shared through L2 by the CTAs working on it.
+//   kG1Swap / kG2Swap (decode, "swap-AB"): A = 128 weight rows (M=128), B = the
+//       (few) token rows of the expert (N = 16..NB, rounded up to 16), so the
+//       weight stream -- the HBM roofline at decode -- fills the M dimension.
+//       kG2Swap splits K (ffn) across CTAs to fill all SMs; partial sums go to
+//       separate fp32 buffers that the combine kernel adds in a fixed order.
+// Warp roles (192 threads): warp 0 = TMA producer (one lane), warp 1 = TMEM
+// allocator + MMA issuer (one lane), warps 2..5 = epilogue (TMEM lane quadrant
+// = warp % 4). Pipelines: smem ring (full/empty mbarriers, STAGES deep) between
+// TMA and MMA; two TMEM accumulators (tmem_full/tmem_empty) between MMA and
+// epilogue, so the epilogue of tile i overlaps the mainloop of tile i+1.
+#pragma once
+
+#include "sm100.cuh"
+#include <cuda_bf16.h>
+
+namespace moe {
+
+enum GemmKind : int { kG1Tiled = 0, kG2Tiled = 1, kG1Swap = 2, kG2Swap = 3 };
+
+struct GemmParams {
+    const int32_t* counts;   // [E] rows per local expert (device, from the permute step)
+    const int32_t* offsets;  // [E+1] first row of each expert segment (128-row aligned)
+    int32_t E;               // local experts
+    int32_t d;               // hidden
+    int32_t f;               // ffn columns held by this rank
+    int32_t splits;          // K splits (kG2Swap only; 1 otherwise)
+    void* out;               // kG1*: h bf16 [Cap, f];  kG2*: y fp32 [splits][Cap, d]
+    int64_t out_split_stride;// elements between split buffers (kG2Swap)
+};
+
+constexpr int kGemmThreads = 192;
+constexpr int kBK = 64;                 // K per stage = one 128-byte swizzle atom of bf16
+constexpr int kSmemBudget = 232448;     // 227 KB opt-in dynamic shared memory per CTA
+
+template <int KIND, int NB>
+struct GemmCfg {
+    static constexpr bool kSwap = (KIND == kG1Swap || KIND == kG2Swap);
+    static constexpr bool kG1 = (KIND == kG1Tiled || KIND == kG1Swap);
+    // bytes per stage of each operand (rows x 128 B)
+    static constexpr int kARows = (KIND == kG1Swap) ? 256 : 128;
+    static constexpr int kBRows = kSwap ? NB : 256;
+    static constexpr int kABytes = kARows * 128;
+    static constexpr int kBBytes = kBRows * 128;
+    static constexpr int kStageBytes = kABytes + kBBytes;
+    static constexpr int kStagesRaw = (kSmemBudget - 2048) / kStageBytes;
+    static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
+    static constexpr int kSmemBytes = kStages * kStageBytes + 2048;  // + barriers + 1 KB align slack
+    static constexpr int kAccCols = 256;  // TMEM columns per accumulator stage (2 stages = 512)
+    static_assert(kStages >= 2, "pipeline too shallow");
+    static_assert(!kSwap || (NB >= 16 && NB <= 128 && (NB % 16) == 0), "bad NB");
+};
+
+struct TileInfo {
+    int32_t e;        // local expert
+    int32_t seg;      // first row of the expert segment in the permuted buffer
+    int32_t rows;     // rows of the expert (n_e)
+    int32_t a_row;    // A-operand row coordinate (within the tensor map's row dim)
+    int32_t b_row;    // B-operand row coordinate
+    int32_t kb0, nkb; // K-block range
+    int32_t m_idx, n_idx, split;
+    int32_t n_valid;  // swap: valid token columns in this tile
+};
+
+// Number of tiles of expert e and the tile decode. Both must be identical in
+// all three roles (they are pure functions of counts/params).
+template <int KIND, int NB>
+__device__ __forceinline__ int tiles_of(int n_e, const GemmParams& p) {
+    if (n_e <= 0) return 0;
+    if (KIND == kG1Tiled) return ((n_e + 127) / 128) * (p.f / 128);
+    if (KIND == kG2Tiled) return ((n_e + 127) / 128) * ((p.d + 255) / 256);
+    if (KIND == kG1Swap) return ((n_e + NB - 1) / NB) * (p.f / 128);
+    return ((n_e + NB - 1) / NB) * ((p.d + 127) / 128) * p.splits;  // kG2Swap
+}
+
+template <int KIND, int NB>
+__device__ __forceinline__ bool decode_tile(int t, const GemmParams& p, const int32_t* s_counts,
+                                            const int32_t* s_offsets, TileInfo& ti) {
+    int e = 0;
+    for (; e < p.E; ++e) {
+        int n = tiles_of<KIND, NB>(s_counts[e], p);
+        if (t < n) break;
+        t -= n;
+    }
+    if (e >= p.E) return false;
+    ti.e = e;
+    ti.seg = s_offsets[e];
+    ti.rows = s_counts[e];
+    ti.split = 0;
+    if (KIND == kG1Tiled || KIND == kG2Tiled) {
+        int mt = (ti.rows + 127) / 128;
+        ti.m_idx = t % mt;             // tokens fastest: CTAs share the weight tile via L2
+        ti.n_idx = t / mt;
+        ti.a_row = ti.seg + ti.m_idx * 128;
+        ti.b_row = ti.n_idx * 256;
+        ti.kb0 = 0;
+        ti.nkb = (KIND == kG1Tiled ? p.d : p.f) / kBK;
+        ti.n_valid = 0;
+    } else {
+        int nt = (ti.rows + NB - 1) / NB;
+        ti.n_idx = t % nt;             // token tiles fastest: same weight tile back-to-back
+        int rest = t / nt;
+        int wt = (KIND == kG1Swap) ? (p.f / 128) : ((p.d + 127) / 128);
+        ti.m_idx = rest % wt;
+        ti.split = rest / wt;
+        ti.a_row = ti.m_idx * (KIND == kG1Swap ? 256 : 128);
+        ti.b_row = ti.seg + ti.n_idx * NB;
+        int nkb_all = (KIND == kG1Swap ? p.d : p.f) / kBK;
+        int S = (KIND == kG2Swap) ? p.splits : 1;
+        ti.kb0 = (nkb_all * ti.split) / S;
+        ti.nkb = (nkb_all * (ti.split + 1)) / S - ti.kb0;
+        int rem = ti.rows - ti.n_idx * NB;
+        ti.n_valid = rem < NB ? rem : NB;
+    }
+    return true;
+}
+
+__device__ __forceinline__ float silu_f32(float a) { return a / (1.0f + __expf(-a)); }
+
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+    __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+    return *reinterpret_cast<uint32_t*>(&v);
+}
+
+// tmA: tensor map of the A operand, tmB: of the B operand (see moe.cu for boxes).
+template <int KIND, int NB>
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    moe_gemm_kernel(const GemmParams p, const __grid_constant__ CUtensorMap tmA,
+                    const __grid_constant__ CUtensorMap tmB) {
+    using C = GemmCfg<KIND, NB>;
+    constexpr int S = C::kStages;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    // 1024-byte alignment for the 128B-swizzled TMA/UMMA tiles
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* smem_a = smem;
+    uint8_t* smem_b = smem + S * C::kABytes;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * C::kStageBytes);
+    uint64_t* full = bars;
+    uint64_t* empty = bars + S;
+    uint64_t* tmem_full = bars + 2 * S;
+    uint64_t* tmem_empty = bars + 2 * S + 2;
+    uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 4);
+    int32_t* s_counts = reinterpret_cast<int32_t*>(bars + 2 * S + 5);      // [32]
+    int32_t* s_offsets = s_counts + 32;                                    // [33]
+
+    const int warp = threadIdx.x / 32;
+    const int lane = threadIdx.x % 32;
+
+    if (warp == 0 && lane == 0) {
+        ptx::prefetch_tmap(&tmA);
+        ptx::prefetch_tmap(&tmB);
+        for (int i = 0; i < S; ++i) {
+            ptx::mbar_init(&full[i], 1);
+            ptx::mbar_init(&empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            ptx::mbar_init(&tmem_full[i], 1);
+            ptx::mbar_init(&tmem_empty[i], 4);
+        }
+        ptx::fence_mbar_init();
+    }
+    if (warp == 1) {
+        ptx::tmem_alloc(tmem_base_slot, 2 * C::kAccCols);
+        ptx::tmem_relinquish();
+    }
+    // Everything above overlaps the previous kernel's tail (PDL); from here on we
+    // read its outputs (counts / offsets / permuted rows).
+    ptx::pdl_wait();
+    if (threadIdx.x < 32) {
+        for (int e = threadIdx.x; e < p.E; e += 32) {
+            s_counts[e] = p.counts[e];
+            s_offsets[e] = p.offsets[e];
+        }
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = *tmem_base_slot;
+
+    int total = 0;
+    for (int e = 0; e < p.E; ++e) total += tiles_of<KIND, NB>(s_counts[e], p);
+
+    if (warp == 0) {
+        // ---------------------------------------------------------------- TMA producer
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int t = blockIdx.x; t < total; t += gridDim.x) {
+                TileInfo ti;
+                decode_tile<KIND, NB>(t, p, s_counts, s_offsets, ti);
+                for (int kb = 0; kb < ti.nkb; ++kb) {
+                    ptx::mbar_wait(&empty[stage], phase ^ 1);
+                    ptx::mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
+                    const int kc = (ti.kb0 + kb) * kBK;
+                    uint8_t* sa = smem_a + stage * C::kABytes;
+                    uint8_t* sb = smem_b + stage * C::kBBytes;
+                    if (C::kSwap) {
+                        // A = weights (3D map [K, rows, E]) streamed once: evict-first.
+                        ptx::tma_load_3d(&tmA, &full[stage], sa, kc, ti.a_row, ti.e, ptx::kEvictFirst);
+                        // B = permuted tokens / activations (2D map [K, Cap]): keep in L2.
+                        ptx::tma_load_2d(&tmB, &full[stage], sb, kc, ti.b_row, ptx::kEvictLast);
+                    } else {
+                        ptx::tma_load_2d(&tmA, &full[stage], sa, kc, ti.a_row, ptx::kEvictLast);
+                        ptx::tma_load_3d(&tmB, &full[stage], sb, kc, ti.b_row, ti.e, ptx::kEvictNormal);
+                    }
+                    if (++stage == S) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------------------------------------------------------- MMA issuer
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            for (int t = blockIdx.x; t < total; t += gridDim.x) {
+                TileInfo ti;
+                decode_tile<KIND, NB>(t, p, s_counts, s_offsets, ti);
+                uint32_t n_mma;
+                if (KIND == kG1Tiled) n_mma = 256;
+                else if (KIND == kG2Tiled) n_mma = min(256, p.d - ti.n_idx * 256);
+                else n_mma = (uint32_t)((ti.n_valid + 15) / 16 * 16);
+                const uint32_t idesc = ptx::make_idesc_bf16(128, n_mma);
+                const uint32_t d_tmem = tmem_base + acc * C::kAccCols;
+                ptx::mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
+                ptx::tc_fence_after();
+                for (int kb = 0; kb < ti.nkb; ++kb) {
+                    ptx::mbar_wait(&full[stage], phase);
+                    ptx::tc_fence_after();
+                    const uint32_t sa = ptx::smem_u32(smem_a + stage * C::kABytes);
+                    const uint32_t sb = ptx::smem_u32(smem_b + stage * C::kBBytes);
+                    const uint64_t adesc = ptx::make_smem_desc_sw128(sa);
+                    const uint64_t bdesc = ptx::make_smem_desc_sw128(sb);
+#pragma unroll
+                    for (int kk = 0; kk < kBK / 16; ++kk) {
+                        const uint32_t accum = (kb | kk) ? 1u : 0u;
+                        ptx::mma_bf16(d_tmem, adesc + 2 * kk, bdesc + 2 * kk, idesc, accum);
+                        if (KIND == kG1Swap) {
+                            // w3 half of the 256-row A tile (rows 128..255, +16 KB) -> columns +128
+                            const uint64_t adesc3 = ptx::make_smem_desc_sw128(sa + 128 * 128);
+                            ptx::mma_bf16(d_tmem + 128, adesc3 + 2 * kk, bdesc + 2 * kk, idesc, accum);
+                        }
+                    }
+                    ptx::mma_commit(&empty[stage]);  // frees the smem slot when these MMAs finish
+                    if (++stage == S) { stage = 0; phase ^= 1; }
+                }
+                ptx::mma_commit(&tmem_full[acc]);    // accumulator ready for the epilogue
+                if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+            }
+        }
+    } else {
+        // ---------------------------------------------------------------- epilogue (warps 2..5)
+        const int q = warp & 3;                  // TMEM lane quadrant this warp may access
+        const int r = q * 32 + lane;             // accumulator row (= TMEM lane) of this thread
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int t = blockIdx.x; t < total; t += gridDim.x) {
+            TileInfo ti;
+            decode_tile<KIND, NB>(t, p, s_counts, s_offsets, ti);
+            ptx::mbar_wait(&tmem_full[acc], acc_phase);
+            ptx::tc_fence_after();
+            const uint32_t tbase = tmem_base + acc * C::kAccCols + (static_cast<uint32_t>(q * 32) << 16);
+            if (KIND == kG1Tiled) {
+                // row r = token (seg + m*128 + r); cols [0,128) = a, [128,256) = b for f = n*128 + j
+                const bool valid = ti.m_idx * 128 + r < ti.rows;
+                __nv_bfloat16* h = static_cast<__nv_bfloat16*>(p.out) +
+                                   static_cast<int64_t>(ti.a_row + r) * p.f + ti.n_idx * 128;
+#pragma unroll 1
+                for (int c = 0; c < 8; ++c) {
+                    uint32_t a[16], b[16];
+                    ptx::tmem_ld16(tbase + c * 16, a);
+                    ptx::tmem_ld16(tbase + 128 + c * 16, b);
+                    ptx::tmem_wait_ld();
+                    uint32_t o[8];
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        float h0 = silu_f32(__uint_as_float(a[2 * i])) * __uint_as_float(b[2 * i]);
+                        float h1 = silu_f32(__uint_as_float(a[2 * i + 1])) * __uint_as_float(b[2 * i + 1]);
+                        o[i] = pack_bf16x2(h0, h1);
+                    }
+                    if (valid) {
+                        uint4* dst = reinterpret_cast<uint4*>(h + c * 16);
+                        dst[0] = make_uint4(o[0], o[1], o[2], o[3]);
+                        dst[1] = make_uint4(o[4], o[5], o[6], o[7]);
+                    }
+                }
+            } else if (KIND == kG2Tiled) {
+                const bool valid = ti.m_idx * 128 + r < ti.rows;
+                const int ncols = min(256, p.d - ti.n_idx * 256);
+                float* y = static_cast<float*>(p.out) + static_cast<int64_t>(ti.a_row + r) * p.d + ti.n_idx * 256;
+#pragma unroll 1
+                for (int c = 0; c < ncols / 16; ++c) {
+                    uint32_t v[16];
+                    ptx::tmem_ld16(tbase + c * 16, v);
+                    ptx::tmem_wait_ld();
+                    if (valid) {
+                        float4* dst = reinterpret_cast<float4*>(y + c * 16);
+#pragma unroll
+                        for (int i = 0; i < 4; ++i)
+                            dst[i] = make_float4(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]),
+                                                 __uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3]));
+                    }
+                }
+            } else if (KIND == kG1Swap) {
+                // row r = ffn index m*128 + r (w1 at cols [0,NB), w3 at cols [128,128+NB)); col n = token
+                __nv_bfloat16* h = static_cast<__nv_bfloat16*>(p.out) + static_cast<int64_t>(ti.b_row) * p.f +
+                                   ti.m_idx * 128 + r;
+                const int nchunks = (ti.n_valid + 15) / 16;
+#pragma unroll 1
+                for (int c = 0; c < nchunks; ++c) {
+                    uint32_t a[16], b[16];
+                    ptx::tmem_ld16(tbase + c * 16, a);
+                    ptx::tmem_ld16(tbase + 128 + c * 16, b);
+                    ptx::tmem_wait_ld();
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        const int n = c * 16 + i;
+                        if (n < ti.n_valid) {
+                            float hv = silu_f32(__uint_as_float(a[i])) * __uint_as_float(b[i]);
+                            h[static_cast<int64_t>(n) * p.f] = __float2bfloat16_rn(hv);
+                        }
+                    }
+                }
+            } else {  // kG2Swap
+                // row r = hidden index m*128 + r; col n = token; fp32 partial of split s
+                const int drow = ti.m_idx * 128 + r;
+                float* y = static_cast<float*>(p.out) + p.out_split_stride * ti.split +
+                           static_cast<int64_t>(ti.b_row) * p.d + drow;
+                const int nchunks = (ti.n_valid + 15) / 16;
+#pragma unroll 1
+                for (int c = 0; c < nchunks; ++c) {
+                    uint32_t v[16];
+                    ptx::tmem_ld16(tbase + c * 16, v);
+                    ptx::tmem_wait_ld();
+                    if (drow < p.d) {
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) {
+                            const int n = c * 16 + i;
+                            if (n < ti.n_valid) y[static_cast<int64_t>(n) * p.d] = __uint_as_float(v[i]);
+                        }
+                    }
+                }
+            }
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&tmem_empty[acc]);
+            if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        }
+    }
+    // Allow the next kernel in the stream to start its prologue.
+    ptx::pdl_launch_dependents();
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc(tmem_base, 2 * C::kAccCols);
+    }
+}
+
+}  // namespace moe

@@ -1,0 +1,715 @@
+// moe.cu -- libmoe: the C ABI of include/moe.h (context, validation, workspace,
+// TMA-descriptor cache, launch sequence, instrumentation, NCCL variants).
+//
+// Launch sequence of one forward (single GPU; SURVEY.md Sec. 3 "S1"):
+//   K1 moe_router_kernel   (logits, top-k, gates, histogram, scan)     [a2-a5]
+//   K2 moe_permute_kernel  (stable positions, 16-B row scatter)        [a6]
+//   K3 moe_gemm_kernel<G1> (w1/w3 grouped GEMM + fused SwiGLU)         [a7]
+//   K4 moe_gemm_kernel<G2> (w2 grouped GEMM, fp32 out / split-K)       [a8]
+//   K5 moe_combine_kernel  (gate-weighted un-permute, bf16 RNE)        [a9]
+// chained with programmatic dependent launch; no host synchronisation.
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/moe.h"
+#include "gemm_sm100.cuh"
+#include "kernels.cuh"
+
+using namespace moe;
+
+namespace {
+
+thread_local std::string g_init_error;
+
+enum Slot { kSlotRouter = 0, kSlotPermute, kSlotGemm1, kSlotGemm2, kSlotCombine, kSlotDispatch, kSlotExchange, kSlotPack };
+
+// ------------------------------------------------------------------ NCCL (dlopen)
+typedef int ncclResult_t;
+typedef void* ncclComm_t;
+typedef struct { char internal[128]; } ncclUniqueId;
+enum { ncclInt8 = 0, ncclInt32 = 2, ncclFloat32 = 7, ncclBfloat16 = 9 };
+enum { ncclSum = 0 };
+struct NcclApi {
+    bool loaded = false;
+    std::string err;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*);
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int);
+    ncclResult_t (*CommDestroy)(ncclComm_t);
+    ncclResult_t (*AllReduce)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t);
+    ncclResult_t (*ReduceScatter)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t);
+    ncclResult_t (*AllGather)(const void*, void*, size_t, int, ncclComm_t, cudaStream_t);
+    ncclResult_t (*AlltoAll)(const void*, void*, size_t, int, ncclComm_t, cudaStream_t);
+    ncclResult_t (*Send)(const void*, size_t, int, int, ncclComm_t, cudaStream_t);
+    ncclResult_t (*Recv)(void*, size_t, int, int, ncclComm_t, cudaStream_t);
+    ncclResult_t (*GroupStart)();
+    ncclResult_t (*GroupEnd)();
+    const char* (*GetErrorString)(ncclResult_t);
+};
+NcclApi g_nccl;
+std::mutex g_nccl_mu;
+
+bool load_nccl(std::string& err) {
+    std::lock_guard<std::mutex> lk(g_nccl_mu);
+    if (g_nccl.loaded) return true;
+    const char* env = getenv("MOE_NCCL_LIB");
+    const char* cands[] = {env, "libnccl.so.2", "libnccl.so"};
+    void* h = nullptr;
+    for (const char* c : cands) {
+        if (!c) continue;
+        h = dlopen(c, RTLD_NOW | RTLD_GLOBAL);
+        if (h) break;
+    }
+    if (!h) { err = std::string("cannot dlopen libnccl.so.2: ") + dlerror(); return false; }
+#define LOADSYM(field, name)                                                     \
+    g_nccl.field = reinterpret_cast<decltype(g_nccl.field)>(dlsym(h, name));    \
+    if (!g_nccl.field) { err = "missing NCCL symbol " name; return false; }
+    LOADSYM(GetUniqueId, "ncclGetUniqueId");
+    LOADSYM(CommInitRank, "ncclCommInitRank");
+    LOADSYM(CommDestroy, "ncclCommDestroy");
+    LOADSYM(AllReduce, "ncclAllReduce");
+    LOADSYM(ReduceScatter, "ncclReduceScatter");
+    LOADSYM(AllGather, "ncclAllGather");
+    LOADSYM(AlltoAll, "ncclAlltoAll");
+    LOADSYM(Send, "ncclSend");
+    LOADSYM(Recv, "ncclRecv");
+    LOADSYM(GroupStart, "ncclGroupStart");
+    LOADSYM(GroupEnd, "ncclGroupEnd");
+    LOADSYM(GetErrorString, "ncclGetErrorString");
+#undef LOADSYM
+    g_nccl.loaded = true;
+    return true;
+}
+
+// ------------------------------------------------------------------ TMA descriptors
+typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                      const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                      CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+PFN_encodeTiled_t get_encode_fn() {
+    static PFN_encodeTiled_t fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_encodeTiled_t>(p);
+    });
+    return fn;
+}
+
+// rank-2 [rows, K] or rank-3 [batch, rows, K] bf16, K innermost; box {64, box_rows(, 1)}; 128B swizzle.
+bool encode_map(CUtensorMap* m, const void* base, int rank, uint64_t K, uint64_t rows, uint64_t batch,
+                uint32_t box_rows) {
+    PFN_encodeTiled_t fn = get_encode_fn();
+    if (!fn) return false;
+    cuuint64_t dims[3] = {K, rows, batch};
+    cuuint64_t strides[2] = {K * 2, K * 2 * rows};
+    cuuint32_t box[3] = {64, box_rows, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(base), dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
+int next_pow2(int v) { int p = 1; while (p < v) p <<= 1; return p; }
+
+}  // namespace
+
+struct moe_ctx {
+    moe_config cfg{};
+    int device = 0;
+    int num_sms = 148;
+    int d = 0, f = 0, E = 0, k = 0, G = 1, rank = 0;
+    int E_local = 0, e_lo = 0, f_local = 0, f_off = 0;
+    int max_T = 0, nblk_max = 0;
+    int64_t cap = 0;          // rows of the permuted buffers (tiled path)
+    int64_t cap_swap = 0;     // rows used by the swap (decode) path
+    int swap_max_T = 128;     // swap path chosen when T <= this (and not forced)
+    int max_splits = 4;
+    int64_t split_stride = 0; // elements between split-K partial buffers of this forward
+    // workspace (device)
+    int32_t *topk_idx = nullptr, *pos = nullptr, *blockcount = nullptr, *blockoff = nullptr;
+    int32_t *counts = nullptr, *offsets = nullptr;
+    float* topk_w = nullptr;
+    unsigned int* done = nullptr;
+    __nv_bfloat16 *x_perm = nullptr, *h = nullptr;
+    float* y = nullptr;
+    int64_t y_elems = 0;
+    __nv_bfloat16 *stage_in = nullptr, *stage_out = nullptr;  // moe_forward_host staging
+    float* tp_partial = nullptr;                               // TP: fp32 partial [max_T, d]
+    float* tp_scatter = nullptr;                               // TP: reduce-scatter result
+    // EP staging
+    __nv_bfloat16 *ep_send = nullptr, *ep_recv = nullptr;
+    float *ep_ysend = nullptr, *ep_yrecv = nullptr;
+    int32_t *ep_meta_send = nullptr, *ep_meta_recv = nullptr;
+    // TMA descriptors: workspace operands
+    CUtensorMap tm_x_tiled{}, tm_h_tiled{};
+    CUtensorMap tm_x_swap[3]{}, tm_h_swap[3]{};  // NB = 32, 64, 128
+    // weight descriptor cache (keyed by pointer)
+    const void* w13_key = nullptr;
+    const void* w2_key = nullptr;
+    CUtensorMap tm_w13{}, tm_w2_tiled{}, tm_w2_swap{};
+    // instrumentation
+    bool profiling = false;
+    struct Ev { int slot; cudaEvent_t a, b; };
+    std::vector<Ev> pending;
+    std::vector<cudaEvent_t> ev_pool;
+    double ms[MOE_NUM_KERNEL_SLOTS]{};
+    int64_t launches[MOE_NUM_KERNEL_SLOTS]{};
+    int64_t launch_count = 0;
+    bool poisoned = false;
+    std::string err;
+};
+
+namespace {
+
+moe_status fail(moe_ctx* c, moe_status s, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    if (c) {
+        c->err = buf;
+        if (s == MOE_ERR_CUDA) c->poisoned = true;
+    } else {
+        g_init_error = buf;
+    }
+    return s;
+}
+
+#define CUDA_TRY(ctx, expr)                                                                          \
+    do {                                                                                             \
+        cudaError_t _e = (expr);                                                                     \
+        if (_e != cudaSuccess)                                                                       \
+            return fail(ctx, MOE_ERR_CUDA, "%s failed: %s (%s:%d)", #expr, cudaGetErrorString(_e),   \
+                        __FILE__, __LINE__);                                                         \
+    } while (0)
+
+cudaEvent_t take_event(moe_ctx* c) {
+    if (!c->ev_pool.empty()) {
+        cudaEvent_t e = c->ev_pool.back();
+        c->ev_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+}
+
+// Launch helper: cudaLaunchKernelEx with PDL + optional profiling events.
+template <typename... KArgs, typename... Args>
+moe_status launch(moe_ctx* c, int slot, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                  cudaStream_t st, Args&&... args) {
+    cudaEvent_t ea = nullptr, eb = nullptr;
+    if (c->profiling) {
+        ea = take_event(c);
+        eb = take_event(c);
+        cudaEventRecord(ea, st);
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = (c->cfg.flags & MOE_FLAG_NO_PDL) ? 0 : 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+    if (e != cudaSuccess) return fail(c, MOE_ERR_CUDA, "kernel launch (slot %d) failed: %s", slot, cudaGetErrorString(e));
+    c->launch_count++;
+    if (c->profiling) {
+        cudaEventRecord(eb, st);
+        c->pending.push_back({slot, ea, eb});
+    }
+    return MOE_OK;
+}
+
+template <int KIND, int NB>
+moe_status set_gemm_attr(moe_ctx* c) {
+    CUDA_TRY(c, cudaFuncSetAttribute(moe_gemm_kernel<KIND, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     GemmCfg<KIND, NB>::kSmemBytes));
+    return MOE_OK;
+}
+
+template <int KIND, int NB>
+moe_status launch_gemm(moe_ctx* c, int slot, const GemmParams& p, const CUtensorMap& a, const CUtensorMap& b,
+                       int grid, cudaStream_t st) {
+    return launch(c, slot, moe_gemm_kernel<KIND, NB>, dim3(grid), dim3(kGemmThreads),
+                  (size_t)GemmCfg<KIND, NB>::kSmemBytes, st, p, a, b);
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+moe_status validate_cfg(const moe_config* cfg, moe_ctx* c) {
+    if (!cfg) return fail(c, MOE_ERR_INVALID, "cfg is NULL");
+    if (cfg->hidden <= 0 || cfg->hidden % 64) return fail(c, MOE_ERR_INVALID, "hidden must be a positive multiple of 64");
+    if (cfg->num_experts < 1 || cfg->num_experts > 32) return fail(c, MOE_ERR_INVALID, "num_experts must be in [1,32]");
+    if (cfg->top_k < 1 || cfg->top_k > 2 || cfg->top_k > cfg->num_experts)
+        return fail(c, MOE_ERR_INVALID, "top_k must be 1 or 2 and <= num_experts");
+    if (cfg->max_tokens < 1) return fail(c, MOE_ERR_INVALID, "max_tokens must be >= 1");
+    if (cfg->par < MOE_PAR_NONE || cfg->par > MOE_PAR_TP) return fail(c, MOE_ERR_INVALID, "bad par");
+    const int G = cfg->par == MOE_PAR_NONE ? 1 : cfg->world_size;
+    if (G < 1 || cfg->rank < 0 || cfg->rank >= G) return fail(c, MOE_ERR_INVALID, "bad world_size/rank");
+    if (cfg->par == MOE_PAR_NONE && (cfg->world_size > 1 || cfg->rank != 0))
+        return fail(c, MOE_ERR_INVALID, "MOE_PAR_NONE needs world_size 1, rank 0");
+    if (cfg->ffn <= 0 || cfg->ffn % (128 * (cfg->par == MOE_PAR_TP ? G : 1)))
+        return fail(c, MOE_ERR_INVALID, "ffn / tp_world must be a positive multiple of 128");
+    if (cfg->par == MOE_PAR_EP && cfg->num_experts % G) return fail(c, MOE_ERR_INVALID, "num_experts % ep_world != 0");
+    if (cfg->par != MOE_PAR_NONE && G > 1 && !cfg->nccl_comm) return fail(c, MOE_ERR_INVALID, "nccl_comm required");
+    if (cfg->split_k < 0 || cfg->split_k > 8) return fail(c, MOE_ERR_INVALID, "split_k must be in [0,8]");
+    for (int i = 0; i < 6; ++i)
+        if (cfg->reserved[i]) return fail(c, MOE_ERR_INVALID, "reserved fields must be zero");
+    if ((cfg->flags & MOE_FLAG_FORCE_SWAP) && (cfg->flags & MOE_FLAG_FORCE_TILED))
+        return fail(c, MOE_ERR_INVALID, "FORCE_SWAP and FORCE_TILED are exclusive");
+    return MOE_OK;
+}
+
+void derive_shape(const moe_config* cfg, int& G, int& E_local, int& e_lo, int& f_local, int& f_off) {
+    G = cfg->par == MOE_PAR_NONE ? 1 : cfg->world_size;
+    E_local = cfg->par == MOE_PAR_EP ? cfg->num_experts / G : cfg->num_experts;
+    e_lo = cfg->par == MOE_PAR_EP ? cfg->rank * E_local : 0;
+    f_local = cfg->par == MOE_PAR_TP ? cfg->ffn / G : cfg->ffn;
+    f_off = cfg->par == MOE_PAR_TP ? cfg->rank * f_local : 0;
+}
+
+moe_status ensure_weight_maps(moe_ctx* c, const moe_expert_weights* w) {
+    if (w->w13 != c->w13_key) {
+        if (!encode_map(&c->tm_w13, w->w13, 3, c->d, 2 * (uint64_t)c->f_local, c->E_local, 256))
+            return fail(c, MOE_ERR_CUDA, "cuTensorMapEncodeTiled(w13) failed");
+        c->w13_key = w->w13;
+    }
+    if (w->w2 != c->w2_key) {
+        if (!encode_map(&c->tm_w2_tiled, w->w2, 3, c->f_local, c->d, c->E_local, 256) ||
+            !encode_map(&c->tm_w2_swap, w->w2, 3, c->f_local, c->d, c->E_local, 128))
+            return fail(c, MOE_ERR_CUDA, "cuTensorMapEncodeTiled(w2) failed");
+        c->w2_key = w->w2;
+    }
+    return MOE_OK;
+}
+
+template <int NB>
+moe_status run_swap(moe_ctx* c, int nbi, const moe_expert_weights* w, int splits, cudaStream_t st) {
+    (void)w;
+    GemmParams p1{c->counts, c->offsets, c->E_local, c->d, c->f_local, 1, c->h, 0};
+    moe_status s = launch_gemm<kG1Swap, NB>(c, kSlotGemm1, p1, c->tm_w13, c->tm_x_swap[nbi], c->num_sms, st);
+    if (s) return s;
+    GemmParams p2{c->counts, c->offsets, c->E_local, c->d, c->f_local, splits, c->y, c->split_stride};
+    return launch_gemm<kG2Swap, NB>(c, kSlotGemm2, p2, c->tm_w2_swap, c->tm_h_swap[nbi], c->num_sms, st);
+}
+
+// Core single-rank pipeline: tokens -> (router or given routing) -> permute -> GEMMs -> y.
+// Returns the split count used (for the combine) via *splits_out.
+moe_status run_local(moe_ctx* c, const void* tokens, int T, const void* router_w, const int32_t* in_idx,
+                     const float* in_w, const moe_expert_weights* w, const moe_aux* aux, bool use_swap,
+                     int* splits_out, cudaStream_t st) {
+    const int nblk = (T + kRouteTokPerBlock - 1) / kRouteTokPerBlock;
+    RouteParams rp{};
+    rp.x = static_cast<const __nv_bfloat16*>(tokens);
+    rp.wg = static_cast<const __nv_bfloat16*>(router_w);
+    rp.in_idx = in_idx;
+    rp.in_w = in_w;
+    rp.T = T; rp.d = c->d; rp.E = c->E; rp.k = c->k;
+    rp.e_lo = c->e_lo; rp.e_hi = c->e_lo + c->E_local;
+    rp.logits = aux ? aux->logits : nullptr;
+    rp.topk_idx = c->topk_idx; rp.topk_w = c->topk_w;
+    rp.blockcount = c->blockcount; rp.blockoff = c->blockoff;
+    rp.counts = c->counts; rp.offsets = c->offsets; rp.done = c->done;
+    moe_status s;
+    if (c->E <= 8) s = launch(c, kSlotRouter, moe_router_kernel<8>, dim3(nblk), dim3(kRouteThreads), 0, st, rp);
+    else if (c->E <= 16) s = launch(c, kSlotRouter, moe_router_kernel<16>, dim3(nblk), dim3(kRouteThreads), 0, st, rp);
+    else s = launch(c, kSlotRouter, moe_router_kernel<32>, dim3(nblk), dim3(kRouteThreads), 0, st, rp);
+    if (s) return s;
+
+    PermuteParams pp{};
+    pp.x = rp.x; pp.topk_idx = c->topk_idx; pp.topk_w = c->topk_w; pp.blockoff = c->blockoff; pp.offsets = c->offsets;
+    pp.T = T; pp.d = c->d; pp.k = c->k; pp.e_lo = c->e_lo; pp.E_local = c->E_local;
+    pp.pos = c->pos; pp.pos_aux = aux ? aux->pos : nullptr; pp.x_perm = c->x_perm;
+    if ((s = launch(c, kSlotPermute, moe_permute_kernel, dim3(nblk), dim3(kRouteThreads), 0, st, pp))) return s;
+
+    int splits = 1;
+    if (use_swap) {
+        splits = *splits_out;
+        const int nbw = std::max(32, std::min(128, next_pow2(T)));
+        if (nbw == 32) s = run_swap<32>(c, 0, w, splits, st);
+        else if (nbw == 64) s = run_swap<64>(c, 1, w, splits, st);
+        else s = run_swap<128>(c, 2, w, splits, st);
+        if (s) return s;
+    } else {
+        const int64_t mt_max = (int64_t)T * c->k / 128 + c->E_local;
+        const int g1 = (int)std::min<int64_t>(c->num_sms, mt_max * (c->f_local / 128));
+        const int g2 = (int)std::min<int64_t>(c->num_sms, mt_max * ((c->d + 255) / 256));
+        GemmParams p1{c->counts, c->offsets, c->E_local, c->d, c->f_local, 1, c->h, 0};
+        if ((s = launch_gemm<kG1Tiled, 256>(c, kSlotGemm1, p1, c->tm_x_tiled, c->tm_w13, g1, st))) return s;
+        GemmParams p2{c->counts, c->offsets, c->E_local, c->d, c->f_local, 1, c->y, 0};
+        if ((s = launch_gemm<kG2Tiled, 256>(c, kSlotGemm2, p2, c->tm_h_tiled, c->tm_w2_tiled, g2, st))) return s;
+    }
+    *splits_out = splits;
+    if (aux) {
+        if (aux->topk_idx)
+            CUDA_TRY(c, cudaMemcpyAsync(aux->topk_idx, c->topk_idx, sizeof(int32_t) * T * c->k, cudaMemcpyDeviceToDevice, st));
+        if (aux->topk_w)
+            CUDA_TRY(c, cudaMemcpyAsync(aux->topk_w, c->topk_w, sizeof(float) * T * c->k, cudaMemcpyDeviceToDevice, st));
+        if (aux->expert_counts)
+            CUDA_TRY(c, cudaMemcpyAsync(aux->expert_counts, c->counts, sizeof(int32_t) * c->E_local, cudaMemcpyDeviceToDevice, st));
+        if (aux->expert_offsets)
+            CUDA_TRY(c, cudaMemcpyAsync(aux->expert_offsets, c->offsets, sizeof(int32_t) * (c->E_local + 1), cudaMemcpyDeviceToDevice, st));
+    }
+    return MOE_OK;
+}
+
+bool use_swap_path(const moe_ctx* c, int T) {
+    if (c->cfg.flags & MOE_FLAG_FORCE_SWAP) return true;
+    if (c->cfg.flags & MOE_FLAG_FORCE_TILED) return false;
+    return T <= c->swap_max_T;
+}
+
+moe_status check_ready(moe_ctx* c) {
+    if (!c) return MOE_ERR_INVALID;
+    if (c->poisoned) return fail(c, MOE_ERR_STATE, "context poisoned by an earlier CUDA error: %s", c->err.c_str());
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    return MOE_OK;
+}
+
+moe_status forward_impl(moe_ctx* c, const void* tokens, int32_t T, const void* router_w, const int32_t* in_idx,
+                        const float* in_w, const moe_expert_weights* w, void* out, const moe_aux* aux,
+                        cudaStream_t st);
+
+}  // namespace
+
+// ====================================================================== ABI
+extern "C" {
+
+const char* moe_status_string(moe_status s) {
+    switch (s) {
+        case MOE_OK: return "MOE_OK";
+        case MOE_ERR_INVALID: return "MOE_ERR_INVALID";
+        case MOE_ERR_UNSUPPORTED: return "MOE_ERR_UNSUPPORTED";
+        case MOE_ERR_OOM: return "MOE_ERR_OOM";
+        case MOE_ERR_CUDA: return "MOE_ERR_CUDA";
+        case MOE_ERR_NCCL: return "MOE_ERR_NCCL";
+        case MOE_ERR_STATE: return "MOE_ERR_STATE";
+    }
+    return "MOE_ERR_UNKNOWN";
+}
+
+const char* moe_last_error(const moe_ctx* ctx) { return ctx ? ctx->err.c_str() : g_init_error.c_str(); }
+
+moe_status moe_packed_sizes(const moe_config* cfg, size_t* w13_bytes, size_t* w2_bytes) {
+    moe_status s = validate_cfg(cfg, nullptr);
+    if (s) return s;
+    if (!w13_bytes || !w2_bytes) return fail(nullptr, MOE_ERR_INVALID, "NULL output pointer");
+    int G, E_local, e_lo, f_local, f_off;
+    derive_shape(cfg, G, E_local, e_lo, f_local, f_off);
+    *w13_bytes = (size_t)E_local * 2 * f_local * cfg->hidden * 2;
+    *w2_bytes = (size_t)E_local * cfg->hidden * f_local * 2;
+    return MOE_OK;
+}
+
+moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
+    if (!out) return fail(nullptr, MOE_ERR_INVALID, "out is NULL");
+    *out = nullptr;
+    moe_status s = validate_cfg(cfg, nullptr);
+    if (s) return s;
+    int dev = cfg->device;
+    if (dev < 0 && cudaGetDevice(&dev) != cudaSuccess) return fail(nullptr, MOE_ERR_UNSUPPORTED, "no CUDA device");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || dev >= ndev)
+        return fail(nullptr, MOE_ERR_UNSUPPORTED, "CUDA device %d not available", dev);
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, dev) != cudaSuccess)
+        return fail(nullptr, MOE_ERR_UNSUPPORTED, "cudaGetDeviceProperties failed");
+    if (prop.major != 10 || prop.minor != 0)
+        return fail(nullptr, MOE_ERR_UNSUPPORTED, "libmoe is built for sm_100a (B200); device %d is sm_%d%d", dev,
+                    prop.major, prop.minor);
+    if (!get_encode_fn()) return fail(nullptr, MOE_ERR_UNSUPPORTED, "cuTensorMapEncodeTiled unavailable");
+
+    moe_ctx* c = new (std::nothrow) moe_ctx();
+    if (!c) return fail(nullptr, MOE_ERR_OOM, "host allocation failed");
+    c->cfg = *cfg;
+    c->device = dev;
+    c->num_sms = prop.multiProcessorCount;
+    c->d = cfg->hidden; c->f = cfg->ffn; c->E = cfg->num_experts; c->k = cfg->top_k;
+    derive_shape(cfg, c->G, c->E_local, c->e_lo, c->f_local, c->f_off);
+    c->rank = cfg->rank;
+    c->max_T = cfg->max_tokens;
+    c->nblk_max = (c->max_T + kRouteTokPerBlock - 1) / kRouteTokPerBlock;
+
+    // EP: a rank may receive up to every token of every peer (dropless, reading R6).
+    const int64_t rows_in = cfg->par == MOE_PAR_EP ? (int64_t)c->max_T * c->G : c->max_T;
+    c->cap = round_up(rows_in * c->k + (int64_t)c->E_local * (kSegAlign - 1), kSegAlign);
+    const int64_t swap_T = std::min<int64_t>(rows_in, c->swap_max_T);
+    c->cap_swap = round_up(swap_T * c->k + (int64_t)c->E_local * (kSegAlign - 1), kSegAlign);
+    c->y_elems = std::max<int64_t>(c->cap, c->cap_swap * c->max_splits) * c->d;
+
+    auto fail_init = [&](const char* what, cudaError_t e) {
+        std::string m = std::string("workspace allocation failed (") + what + "): " + cudaGetErrorString(e);
+        moe_destroy(c);
+        g_init_error = m;
+        return e == cudaErrorMemoryAllocation ? MOE_ERR_OOM : MOE_ERR_CUDA;
+    };
+    cudaError_t e;
+    if ((e = cudaSetDevice(dev)) != cudaSuccess) return fail_init("cudaSetDevice", e);
+#define ALLOC(ptr, bytes)                                                               \
+    if ((e = cudaMalloc(reinterpret_cast<void**>(&(ptr)), (bytes))) != cudaSuccess)     \
+        return fail_init(#ptr, e);
+    const int64_t nblk_rows = (rows_in + kRouteTokPerBlock - 1) / kRouteTokPerBlock + 1;
+    ALLOC(c->topk_idx, sizeof(int32_t) * c->max_T * c->k);
+    ALLOC(c->topk_w, sizeof(float) * c->max_T * c->k);
+    ALLOC(c->pos, sizeof(int32_t) * c->max_T * c->k);
+    ALLOC(c->blockcount, sizeof(int32_t) * nblk_rows * 32);
+    ALLOC(c->blockoff, sizeof(int32_t) * nblk_rows * 32);
+    ALLOC(c->counts, sizeof(int32_t) * 64);
+    ALLOC(c->offsets, sizeof(int32_t) * 64);
+    ALLOC(c->done, sizeof(unsigned int) * 4);
+    ALLOC(c->x_perm, sizeof(__nv_bfloat16) * c->cap * c->d);
+    ALLOC(c->h, sizeof(__nv_bfloat16) * c->cap * c->f_local);
+    ALLOC(c->y, sizeof(float) * c->y_elems);
+    ALLOC(c->stage_in, sizeof(__nv_bfloat16) * c->max_T * c->d);
+    ALLOC(c->stage_out, sizeof(__nv_bfloat16) * c->max_T * c->d);
+    if (cfg->par == MOE_PAR_TP) {
+        ALLOC(c->tp_partial, sizeof(float) * c->max_T * c->d);
+        ALLOC(c->tp_scatter, sizeof(float) * ((int64_t)c->max_T * c->d / c->G + 64));
+    }
+    if (cfg->par == MOE_PAR_EP) {
+        // fixed per-peer capacity of max_T*k rows (dropless)
+        const int64_t slots = (int64_t)c->G * c->max_T * c->k;
+        ALLOC(c->ep_send, sizeof(__nv_bfloat16) * slots * c->d);
+        ALLOC(c->ep_recv, sizeof(__nv_bfloat16) * slots * c->d);
+        ALLOC(c->ep_ysend, sizeof(float) * slots * c->d);
+        ALLOC(c->ep_yrecv, sizeof(float) * slots * c->d);
+        ALLOC(c->ep_meta_send, sizeof(int32_t) * slots * 4 + 64);
+        ALLOC(c->ep_meta_recv, sizeof(int32_t) * slots * 4 + 64);
+    }
+#undef ALLOC
+    if ((e = cudaMemset(c->done, 0, sizeof(unsigned int) * 4)) != cudaSuccess) return fail_init("memset", e);
+    if ((e = cudaMemset(c->x_perm, 0, sizeof(__nv_bfloat16) * c->cap * c->d)) != cudaSuccess) return fail_init("memset", e);
+    if ((e = cudaMemset(c->h, 0, sizeof(__nv_bfloat16) * c->cap * c->f_local)) != cudaSuccess) return fail_init("memset", e);
+
+    // workspace TMA descriptors
+    bool ok = encode_map(&c->tm_x_tiled, c->x_perm, 2, c->d, c->cap, 1, 128) &&
+              encode_map(&c->tm_h_tiled, c->h, 2, c->f_local, c->cap, 1, 128);
+    const uint32_t nbs[3] = {32, 64, 128};
+    for (int i = 0; i < 3 && ok; ++i)
+        ok = encode_map(&c->tm_x_swap[i], c->x_perm, 2, c->d, c->cap, 1, nbs[i]) &&
+             encode_map(&c->tm_h_swap[i], c->h, 2, c->f_local, c->cap, 1, nbs[i]);
+    if (!ok) {
+        moe_destroy(c);
+        return fail(nullptr, MOE_ERR_CUDA, "cuTensorMapEncodeTiled(workspace) failed");
+    }
+    moe_status as;
+    if ((as = set_gemm_attr<kG1Tiled, 256>(c)) || (as = set_gemm_attr<kG2Tiled, 256>(c)) ||
+        (as = set_gemm_attr<kG1Swap, 32>(c)) || (as = set_gemm_attr<kG2Swap, 32>(c)) ||
+        (as = set_gemm_attr<kG1Swap, 64>(c)) || (as = set_gemm_attr<kG2Swap, 64>(c)) ||
+        (as = set_gemm_attr<kG1Swap, 128>(c)) || (as = set_gemm_attr<kG2Swap, 128>(c))) {
+        std::string m = c->err;
+        moe_destroy(c);
+        g_init_error = m;
+        return as;
+    }
+    if ((e = cudaDeviceSynchronize()) != cudaSuccess) return fail_init("sync", e);
+    *out = c;
+    return MOE_OK;
+}
+
+moe_status moe_destroy(moe_ctx* c) {
+    if (!c) return MOE_OK;
+    cudaSetDevice(c->device);
+    void* bufs[] = {c->topk_idx, c->topk_w, c->pos, c->blockcount, c->blockoff, c->counts, c->offsets, c->done,
+                    c->x_perm, c->h, c->y, c->stage_in, c->stage_out, c->tp_partial, c->tp_scatter, c->ep_send,
+                    c->ep_recv, c->ep_ysend, c->ep_yrecv, c->ep_meta_send, c->ep_meta_recv};
+    for (void* b : bufs)
+        if (b) cudaFree(b);
+    for (auto& ev : c->pending) { cudaEventDestroy(ev.a); cudaEventDestroy(ev.b); }
+    for (auto ev : c->ev_pool) cudaEventDestroy(ev);
+    delete c;
+    return MOE_OK;
+}
+
+moe_status moe_pack_weights(moe_ctx* c, const void* w1, const void* w3, const void* w2, void* w13_out, void* w2_out,
+                            void* stream) {
+    moe_status s = check_ready(c);
+    if (s) return s;
+    if (!w1 || !w3 || !w2 || !w13_out || !w2_out) return fail(c, MOE_ERR_INVALID, "NULL weight pointer");
+    if (!aligned16(w1) || !aligned16(w3) || !aligned16(w2) || !aligned16(w13_out) || !aligned16(w2_out))
+        return fail(c, MOE_ERR_INVALID, "weight pointers must be 16-byte aligned");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int e_off = c->cfg.par == MOE_PAR_EP ? c->e_lo : 0;
+    if ((s = launch(c, kSlotPack, moe_pack_w13_kernel, dim3(4 * c->num_sms), dim3(256), 0, st,
+                    static_cast<const __nv_bfloat16*>(w1), static_cast<const __nv_bfloat16*>(w3),
+                    static_cast<__nv_bfloat16*>(w13_out), c->E_local, e_off, c->d, c->f, c->f_local, c->f_off)))
+        return s;
+    if ((s = launch(c, kSlotPack, moe_pack_w2_kernel, dim3(4 * c->num_sms), dim3(256), 0, st,
+                    static_cast<const __nv_bfloat16*>(w2), static_cast<__nv_bfloat16*>(w2_out), c->E_local, e_off,
+                    c->d, c->f, c->f_local, c->f_off)))
+        return s;
+    // descriptors keyed by these pointers must be re-encoded if memory was reused
+    if (c->w13_key == w13_out) c->w13_key = nullptr;
+    if (c->w2_key == w2_out) c->w2_key = nullptr;
+    return MOE_OK;
+}
+
+moe_status moe_forward(moe_ctx* c, const void* tokens, int32_t T, const void* router_w,
+                       const moe_expert_weights* w, void* out, const moe_aux* aux, void* stream) {
+    moe_status s = check_ready(c);
+    if (s) return s;
+    if (!router_w || !aligned16(router_w)) return fail(c, MOE_ERR_INVALID, "router_w must be a 16-byte aligned device pointer");
+    return forward_impl(c, tokens, T, router_w, nullptr, nullptr, w, out, aux, static_cast<cudaStream_t>(stream));
+}
+
+moe_status moe_forward_routed(moe_ctx* c, const void* tokens, int32_t T, const int32_t* topk_idx,
+                              const float* topk_w, const moe_expert_weights* w, void* out, const moe_aux* aux,
+                              void* stream) {
+    moe_status s = check_ready(c);
+    if (s) return s;
+    if (c->cfg.par == MOE_PAR_EP) return fail(c, MOE_ERR_UNSUPPORTED, "moe_forward_routed: single-GPU / TP only");
+    if (T > 0 && (!topk_idx || !topk_w)) return fail(c, MOE_ERR_INVALID, "NULL routing");
+    return forward_impl(c, tokens, T, nullptr, topk_idx, topk_w, w, out, aux, static_cast<cudaStream_t>(stream));
+}
+
+moe_status moe_forward_host(moe_ctx* c, const void* tokens_host, int32_t T, const void* router_w,
+                            const moe_expert_weights* w, void* out_host, void* stream) {
+    moe_status s = check_ready(c);
+    if (s) return s;
+    if (T < 0 || T > c->max_T) return fail(c, MOE_ERR_INVALID, "T out of range");
+    if (T > 0 && (!tokens_host || !out_host)) return fail(c, MOE_ERR_INVALID, "NULL host buffer");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const size_t bytes = (size_t)T * c->d * sizeof(__nv_bfloat16);
+    if (T > 0) CUDA_TRY(c, cudaMemcpyAsync(c->stage_in, tokens_host, bytes, cudaMemcpyHostToDevice, st));
+    if ((s = moe_forward(c, c->stage_in, T, router_w, w, c->stage_out, nullptr, stream))) return s;
+    if (T > 0) CUDA_TRY(c, cudaMemcpyAsync(out_host, c->stage_out, bytes, cudaMemcpyDeviceToHost, st));
+    return MOE_OK;
+}
+
+moe_status moe_set_profiling(moe_ctx* c, int enable) {
+    if (!c) return MOE_ERR_INVALID;
+    c->profiling = enable != 0;
+    return MOE_OK;
+}
+
+moe_status moe_reset_profile(moe_ctx* c) {
+    if (!c) return MOE_ERR_INVALID;
+    for (auto& ev : c->pending) {
+        cudaEventSynchronize(ev.b);
+        c->ev_pool.push_back(ev.a);
+        c->ev_pool.push_back(ev.b);
+    }
+    c->pending.clear();
+    for (int i = 0; i < MOE_NUM_KERNEL_SLOTS; ++i) { c->ms[i] = 0; c->launches[i] = 0; }
+    return MOE_OK;
+}
+
+moe_status moe_kernel_times(moe_ctx* c, double* ms, int64_t* launches) {
+    if (!c || !ms || !launches) return MOE_ERR_INVALID;
+    for (auto& ev : c->pending) {
+        cudaError_t e = cudaEventSynchronize(ev.b);
+        if (e != cudaSuccess) return fail(c, MOE_ERR_CUDA, "event sync: %s", cudaGetErrorString(e));
+        float t = 0.f;
+        cudaEventElapsedTime(&t, ev.a, ev.b);
+        c->ms[ev.slot] += t;
+        c->launches[ev.slot] += 1;
+        c->ev_pool.push_back(ev.a);
+        c->ev_pool.push_back(ev.b);
+    }
+    c->pending.clear();
+    for (int i = 0; i < MOE_NUM_KERNEL_SLOTS; ++i) { ms[i] = c->ms[i]; launches[i] = c->launches[i]; }
+    return MOE_OK;
+}
+
+int64_t moe_launch_count(const moe_ctx* c) { return c ? c->launch_count : -1; }
+
+moe_status moe_nccl_unique_id(void* id128) {
+    if (!id128) return fail(nullptr, MOE_ERR_INVALID, "NULL id");
+    std::string err;
+    if (!load_nccl(err)) return fail(nullptr, MOE_ERR_UNSUPPORTED, "%s", err.c_str());
+    ncclUniqueId id;
+    ncclResult_t r = g_nccl.GetUniqueId(&id);
+    if (r) return fail(nullptr, MOE_ERR_NCCL, "ncclGetUniqueId: %s", g_nccl.GetErrorString(r));
+    std::memcpy(id128, &id, 128);
+    return MOE_OK;
+}
+
+moe_status moe_nccl_comm_init(const void* id128, int32_t world, int32_t rank, int32_t device, void** comm) {
+    if (!id128 || !comm || world < 1 || rank < 0 || rank >= world) return fail(nullptr, MOE_ERR_INVALID, "bad args");
+    std::string err;
+    if (!load_nccl(err)) return fail(nullptr, MOE_ERR_UNSUPPORTED, "%s", err.c_str());
+    if (device >= 0 && cudaSetDevice(device) != cudaSuccess) return fail(nullptr, MOE_ERR_CUDA, "cudaSetDevice");
+    ncclUniqueId id;
+    std::memcpy(&id, id128, 128);
+    ncclComm_t cm = nullptr;
+    ncclResult_t r = g_nccl.CommInitRank(&cm, world, id, rank);
+    if (r) return fail(nullptr, MOE_ERR_NCCL, "ncclCommInitRank: %s", g_nccl.GetErrorString(r));
+    *comm = cm;
+    return MOE_OK;
+}
+
+moe_status moe_nccl_comm_destroy(void* comm) {
+    if (!comm) return MOE_OK;
+    std::string err;
+    if (!load_nccl(err)) return fail(nullptr, MOE_ERR_UNSUPPORTED, "%s", err.c_str());
+    ncclResult_t r = g_nccl.CommDestroy(comm);
+    if (r) return fail(nullptr, MOE_ERR_NCCL, "ncclCommDestroy: %s", g_nccl.GetErrorString(r));
+    return MOE_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+moe_status forward_impl(moe_ctx* c, const void* tokens, int32_t T, const void* router_w, const int32_t* in_idx,
+                        const float* in_w, const moe_expert_weights* w, void* out, const moe_aux* aux,
+                        cudaStream_t st) {
+    if (T < 0 || T > c->max_T) return fail(c, MOE_ERR_INVALID, "T=%d out of range [0, %d]", T, c->max_T);
+    if (!w || !w->w13 || !w->w2 || !aligned16(w->w13) || !aligned16(w->w2))
+        return fail(c, MOE_ERR_INVALID, "expert weights must be 16-byte aligned device pointers");
+    if (T > 0 && (!tokens || !out || !aligned16(tokens) || !aligned16(out)))
+        return fail(c, MOE_ERR_INVALID, "tokens / out must be 16-byte aligned device pointers");
+    if (aux && aux->out_f32 && !aligned16(aux->out_f32)) return fail(c, MOE_ERR_INVALID, "aux.out_f32 misaligned");
+    if (c->cfg.par == MOE_PAR_EP) return fail(c, MOE_ERR_UNSUPPORTED, "EP forward not available in this build");
+    if (c->cfg.par == MOE_PAR_TP && c->G > 1) return fail(c, MOE_ERR_UNSUPPORTED, "TP forward not available in this build");
+    moe_status s = ensure_weight_maps(c, w);
+    if (s) return s;
+    if (T == 0) return MOE_OK;
+    const bool swap = use_swap_path(c, T);
+    int splits = 1;
+    if (swap) {
+        // split-K partial buffers: splits x rows_needed rows must fit the y workspace
+        const int64_t rows_needed = round_up((int64_t)T * c->k + (int64_t)c->E_local * (kSegAlign - 1), kSegAlign);
+        splits = c->cfg.split_k ? c->cfg.split_k : c->max_splits;
+        splits = (int)std::max<int64_t>(1, std::min<int64_t>(splits, c->y_elems / (rows_needed * c->d)));
+        splits = std::min(splits, c->f_local / kBK);  // every split owns >= 1 K block
+        c->split_stride = rows_needed * c->d;
+    } else {
+        c->split_stride = 0;
+    }
+    s = run_local(c, tokens, T, router_w, in_idx, in_w, w, aux, swap, &splits, st);
+    if (s) return s;
+    CombineParams cp{};
+    cp.y = c->y;
+    cp.split_stride = c->split_stride;
+    cp.splits = splits;
+    cp.pos = c->pos;
+    cp.topk_w = c->topk_w;
+    cp.x = (c->cfg.flags & MOE_FLAG_RESIDUAL) ? static_cast<const __nv_bfloat16*>(tokens) : nullptr;
+    cp.T = T; cp.d = c->d; cp.k = c->k;
+    cp.out = static_cast<__nv_bfloat16*>(out);
+    cp.out_f32 = aux ? aux->out_f32 : nullptr;
+    return launch(c, kSlotCombine, moe_combine_kernel, dim3((T + 7) / 8), dim3(256), 0, st, cp);
+}
+
+}  // namespace

@@ -1,0 +1,74 @@
+"""CPU-side checks of the C-ABI boundary (no compute calls, no GPU needed):
+libmoe.so loads, exports every symbol include/moe.h declares, validates
+configurations, and fails loudly (no CPU fallback) without an sm_100 device."""
+import ctypes
+import os
+import re
+
+import pytest
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _header_symbols():
+    src = open(os.path.join(ROOT, "include", "moe.h")).read()
+    return sorted(set(re.findall(r"MOE_API\s+[\w\s\*]+?\b(moe_\w+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    import paper_2408_00008_b200 as moe
+    syms = _header_symbols()
+    assert len(syms) >= 16, syms
+    lib = ctypes.CDLL(moe.LIB_PATH)
+    for s in syms:
+        assert hasattr(lib, s), f"libmoe.so does not export {s}"
+    assert sorted(moe.EXPORTED) == syms
+
+
+def test_no_torch_or_oracle_in_boundary():
+    """The ABI header has no torch types; the product tree never references oracle/."""
+    hdr = open(os.path.join(ROOT, "include", "moe.h")).read()
+    assert "torch" not in hdr and "at::" not in hdr
+    pkg = os.path.join(ROOT, "paper_2408_00008_b200")
+    for dp, _, fns in os.walk(pkg):
+        for fn in fns:
+            if fn.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                txt = open(os.path.join(dp, fn)).read()
+                assert "import oracle" not in txt and "moe_oracle" not in txt and "liboracle" not in txt, fn
+
+
+def test_packed_sizes_and_validation():
+    import paper_2408_00008_b200 as moe
+    cfg = moe.make_config(4096, 14336, 8, 2, 64)
+    a, b = moe.moe_packed_sizes(cfg)
+    assert a == 8 * 2 * 14336 * 4096 * 2 and b == 8 * 4096 * 14336 * 2
+    tp = moe.make_config(4096, 14336, 8, 2, 64, par=moe.MOE_PAR_TP, world_size=8, rank=3, nccl_comm=1)
+    a, b = moe.moe_packed_sizes(tp)
+    assert a == 8 * 2 * 1792 * 4096 * 2 and b == 8 * 4096 * 1792 * 2
+    ep = moe.make_config(4096, 14336, 8, 2, 64, par=moe.MOE_PAR_EP, world_size=8, rank=3, nccl_comm=1)
+    a, b = moe.moe_packed_sizes(ep)
+    assert a == 1 * 2 * 14336 * 4096 * 2
+    bad = [
+        moe.make_config(100, 14336, 8, 2, 64),            # hidden % 64
+        moe.make_config(4096, 1000, 8, 2, 64),            # ffn % 128
+        moe.make_config(4096, 14336, 8, 3, 64),           # top_k
+        moe.make_config(4096, 14336, 33, 2, 64),          # E > 32
+        moe.make_config(4096, 14336, 8, 2, 0),            # max_tokens
+        moe.make_config(4096, 14336, 8, 2, 64, par=moe.MOE_PAR_EP, world_size=3, nccl_comm=1),  # E % G
+        moe.make_config(4096, 14336, 8, 2, 64, par=moe.MOE_PAR_TP, world_size=8, nccl_comm=1, rank=8),
+        moe.make_config(4096, 14336, 8, 2, 64, par=moe.MOE_PAR_TP, world_size=2),  # no comm
+        moe.make_config(4096, 14336, 8, 2, 64, flags=moe.MOE_FLAG_FORCE_SWAP | moe.MOE_FLAG_FORCE_TILED),
+    ]
+    for c in bad:
+        with pytest.raises(moe.MoEError) as ei:
+            moe.moe_packed_sizes(c)
+        assert ei.value.status == moe.MOE_ERR_INVALID
+
+
+@pytest.mark.skipif(torch.cuda.is_available(), reason="checks the no-GPU failure mode")
+def test_init_fails_loudly_without_gpu():
+    import paper_2408_00008_b200 as moe
+    with pytest.raises(moe.MoEError) as ei:
+        moe.moe_init(moe.make_config(64, 128, 4, 2, 16))
+    assert ei.value.status == moe.MOE_ERR_UNSUPPORTED
