@@ -18,8 +18,8 @@
 
 namespace moe {
 
-constexpr int kRouteTokPerBlock = 64;   // tokens per router / permute block
-constexpr int kRouteThreads = 256;      // 8 warps
+constexpr int kRouteThreads = 128;      // router block: 4 warps split the hidden dim
+constexpr int kPermuteThreads = 256;    // permute block: 8 warps
 constexpr int kSegAlign = 128;          // expert segments padded to the GEMM M tile
 
 struct RouteParams {
@@ -49,162 +49,146 @@ __device__ __forceinline__ void bf16x8_to_f32(const uint4& v, float (&f)[8]) {
     }
 }
 
-// Per-warp, stable (by token index) rank of each of the warp's 32 tokens inside
-// each local expert: rank = #{lanes l' < l whose token is routed to that expert}.
-// Writes wcnt[e] = #tokens of this warp routed to local expert e.
-template <int KMAX>
-__device__ __forceinline__ void warp_expert_ranks(const int32_t (&le)[KMAX], int k, int E_local, bool valid,
-                                                  int32_t (&rank)[KMAX], int32_t* wcnt, int lane) {
-    const uint32_t lt = (1u << lane) - 1u;
-    for (int e = 0; e < E_local; ++e) {
-        bool mine = false;
-#pragma unroll
-        for (int j = 0; j < KMAX; ++j) mine |= (j < k) && (le[j] == e);
-        const uint32_t m = __ballot_sync(0xffffffffu, valid && mine);
-#pragma unroll
-        for (int j = 0; j < KMAX; ++j)
-            if (j < k && le[j] == e) rank[j] = __popc(m & lt);
-        if (lane == 0) wcnt[e] = __popc(m);
-    }
-}
-
-// K1: router + histogram + (last block) scan.  E_MAX bounds E (register arrays).
-template <int E_MAX>
+// K1: router (a2, a3) + per-block histogram (a4) + last-block exclusive scan (a5).
+// A block owns TB consecutive tokens; its 128 threads split the hidden dimension
+// in 8-element (16-byte) chunks, each thread accumulating TB x E partial dot
+// products in fp32 (bf16*bf16 products are exact in fp32). W_g chunks are loaded
+// once per thread and reused for the TB tokens. Partial sums are reduced with
+// warp shuffles, then across the 4 warps in a fixed order (deterministic).
+template <int E_MAX, int TB>
 __global__ void __launch_bounds__(kRouteThreads) moe_router_kernel(const RouteParams p) {
-    __shared__ int32_t s_idx[kRouteTokPerBlock][2];
-    __shared__ int32_t s_wcnt[2][32];
+    __shared__ float s_part[4][TB][E_MAX];
+    __shared__ int32_t s_idx[TB][2];
     __shared__ int s_last;
+    __shared__ int32_t s_tot[32];
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-    const int tok0 = blockIdx.x * kRouteTokPerBlock;
+    const int tok0 = blockIdx.x * TB;
+    const int ntok = min(TB, p.T - tok0);
     const int E_local = p.e_hi - p.e_lo;
 
     ptx::pdl_wait();
 
     if (p.in_idx == nullptr) {
-        // ---- a2/a3: logits by warp-cooperative dot products, 2 tokens per pass.
-        // Lane owns 8 consecutive hidden elements per 256-element slab (16-byte loads).
-        for (int pass = 0; pass < kRouteTokPerBlock / 16; ++pass) {
-            const int tl0 = warp * (kRouteTokPerBlock / 8) + 2 * pass;
-            const int t0 = tok0 + tl0, t1 = t0 + 1;
-            float acc0[E_MAX], acc1[E_MAX];
+        float acc[TB][E_MAX];
 #pragma unroll
-            for (int e = 0; e < E_MAX; ++e) { acc0[e] = 0.f; acc1[e] = 0.f; }
-            if (t0 < p.T) {
-                const bool has1 = t1 < p.T;
-                for (int c = lane * 8; c < p.d; c += 256) {
-                    float x0[8], x1[8];
-                    bf16x8_to_f32(__ldg(reinterpret_cast<const uint4*>(p.x + (int64_t)t0 * p.d + c)), x0);
-                    if (has1) bf16x8_to_f32(__ldg(reinterpret_cast<const uint4*>(p.x + (int64_t)t1 * p.d + c)), x1);
-                    else {
+        for (int t = 0; t < TB; ++t)
 #pragma unroll
-                        for (int i = 0; i < 8; ++i) x1[i] = 0.f;
-                    }
+            for (int e = 0; e < E_MAX; ++e) acc[t][e] = 0.f;
+        // All loads of one chunk are issued before any use (rows / experts past the
+        // end are clamped to a valid address and their sums ignored), so a thread
+        // keeps TB + E 16-byte loads in flight instead of serialising on each.
+        const int nchunk = p.d / 8;
+        const uint4* xrow[TB];
 #pragma unroll
-                    for (int e = 0; e < E_MAX; ++e) {
-                        if (e < p.E) {
-                            float w[8];
-                            bf16x8_to_f32(__ldg(reinterpret_cast<const uint4*>(p.wg + (int64_t)e * p.d + c)), w);
+        for (int t = 0; t < TB; ++t)
+            xrow[t] = reinterpret_cast<const uint4*>(p.x + (int64_t)(tok0 + min(t, ntok - 1)) * p.d);
+#pragma unroll 2
+        for (int ci = threadIdx.x; ci < nchunk; ci += kRouteThreads) {
+            uint4 xr[TB], wr[E_MAX];
 #pragma unroll
-                            for (int i = 0; i < 8; ++i) {
-                                acc0[e] = fmaf(x0[i], w[i], acc0[e]);  // bf16*bf16 is exact in fp32
-                                acc1[e] = fmaf(x1[i], w[i], acc1[e]);
-                            }
-                        }
-                    }
+            for (int t = 0; t < TB; ++t) xr[t] = __ldg(xrow[t] + ci);
+#pragma unroll
+            for (int e = 0; e < E_MAX; ++e)
+                wr[e] = __ldg(reinterpret_cast<const uint4*>(p.wg + (int64_t)min(e, p.E - 1) * p.d) + ci);
+#pragma unroll
+            for (int t = 0; t < TB; ++t) {
+                float xv[8];
+                bf16x8_to_f32(xr[t], xv);
+#pragma unroll
+                for (int e = 0; e < E_MAX; ++e) {
+                    float w[8];
+                    bf16x8_to_f32(wr[e], w);
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) acc[t][e] = fmaf(xv[i], w[i], acc[t][e]);
                 }
             }
+        }
+#pragma unroll
+        for (int t = 0; t < TB; ++t)
 #pragma unroll
             for (int e = 0; e < E_MAX; ++e) {
+                float v = acc[t][e];
 #pragma unroll
-                for (int o = 16; o > 0; o >>= 1) {
-                    acc0[e] += __shfl_xor_sync(0xffffffffu, acc0[e], o);
-                    acc1[e] += __shfl_xor_sync(0xffffffffu, acc1[e], o);
-                }
+                for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                if (lane == 0) s_part[warp][t][e] = v;
             }
-            // lane 0 finalises token t0, lane 1 token t1 (each from its own, fixed-order sums)
-            if (lane < 2) {
-                const int t = lane == 0 ? t0 : t1;
-                if (t < p.T) {
-                    float l[E_MAX];
+        __syncthreads();
+        if (threadIdx.x < ntok) {
+            const int tb = threadIdx.x, t = tok0 + tb;
+            float l[E_MAX];
 #pragma unroll
-                    for (int e = 0; e < E_MAX; ++e) l[e] = lane == 0 ? acc0[e] : acc1[e];
-                    if (p.logits) {
+            for (int e = 0; e < E_MAX; ++e)
+                l[e] = ((s_part[0][tb][e] + s_part[1][tb][e]) + s_part[2][tb][e]) + s_part[3][tb][e];
+            if (p.logits) {
 #pragma unroll
-                        for (int e = 0; e < E_MAX; ++e)
-                            if (e < p.E) p.logits[(int64_t)t * p.E + e] = l[e];
-                    }
-                    // top-k by (logit desc, index asc): strict '>' keeps the lower index on ties
-                    int i0 = 0;
-                    float b0 = l[0];
-#pragma unroll
-                    for (int e = 1; e < E_MAX; ++e)
-                        if (e < p.E && l[e] > b0) { b0 = l[e]; i0 = e; }
-                    int i1 = -1;
-                    float b1 = 0.f;
-                    if (p.k > 1) {
-#pragma unroll
-                        for (int e = 0; e < E_MAX; ++e)
-                            if (e < p.E && e != i0 && (i1 < 0 || l[e] > b1)) { b1 = l[e]; i1 = e; }
-                    }
-                    // softmax over all E renormalised over the selected k: the partition
-                    // function cancels, w_j = exp(l_j - l_max) / sum_sel exp(l - l_max)
-                    float w0 = 1.f, w1 = 0.f;
-                    if (p.k > 1) {
-                        const float e1 = expf(b1 - b0);
-                        const float den = 1.f + e1;
-                        w0 = 1.f / den;
-                        w1 = e1 / den;
-                    }
-                    p.topk_idx[(int64_t)t * p.k] = i0;
-                    p.topk_w[(int64_t)t * p.k] = w0;
-                    if (p.k > 1) {
-                        p.topk_idx[(int64_t)t * p.k + 1] = i1;
-                        p.topk_w[(int64_t)t * p.k + 1] = w1;
-                    }
-                    s_idx[t - tok0][0] = i0;
-                    s_idx[t - tok0][1] = i1;
-                }
+                for (int e = 0; e < E_MAX; ++e)
+                    if (e < p.E) p.logits[(int64_t)t * p.E + e] = l[e];
             }
+            // top-k by (logit desc, index asc): strict '>' keeps the lower index on ties (R3)
+            int i0 = 0;
+            float b0 = l[0];
+#pragma unroll
+            for (int e = 1; e < E_MAX; ++e)
+                if (e < p.E && l[e] > b0) { b0 = l[e]; i0 = e; }
+            int i1 = -1;
+            float b1 = 0.f;
+            if (p.k > 1) {
+#pragma unroll
+                for (int e = 0; e < E_MAX; ++e)
+                    if (e < p.E && e != i0 && (i1 < 0 || l[e] > b1)) { b1 = l[e]; i1 = e; }
+            }
+            // softmax over all E renormalised over the selected k (R2): the partition
+            // function cancels, w_j = exp(l_j - l_max) / sum_sel exp(l - l_max)
+            float w0 = 1.f, w1 = 0.f;
+            if (p.k > 1) {
+                const float e1 = expf(b1 - b0);
+                const float den = 1.f + e1;
+                w0 = 1.f / den;
+                w1 = e1 / den;
+            }
+            p.topk_idx[(int64_t)t * p.k] = i0;
+            p.topk_w[(int64_t)t * p.k] = w0;
+            if (p.k > 1) {
+                p.topk_idx[(int64_t)t * p.k + 1] = i1;
+                p.topk_w[(int64_t)t * p.k + 1] = w1;
+            }
+            s_idx[tb][0] = i0;
+            s_idx[tb][1] = i1;
         }
     } else {
         // routed mode (caller supplied routing): validate and copy into the workspace
-        for (int i = threadIdx.x; i < kRouteTokPerBlock * p.k; i += blockDim.x) {
-            const int tl = i / p.k, j = i % p.k;
-            const int t = tok0 + tl;
-            if (t < p.T) {
-                const int e = p.in_idx[(int64_t)t * p.k + j];
-                if (e < 0 || e >= p.E) __trap();
-                p.topk_idx[(int64_t)t * p.k + j] = e;
-                p.topk_w[(int64_t)t * p.k + j] = p.in_w[(int64_t)t * p.k + j];
-                s_idx[tl][j] = e;
-            }
+        for (int i = threadIdx.x; i < ntok * p.k; i += kRouteThreads) {
+            const int tb = i / p.k, j = i % p.k;
+            const int64_t o = (int64_t)(tok0 + tb) * p.k + j;
+            const int e = p.in_idx[o];
+            if (e < 0 || e >= p.E) __trap();
+            p.topk_idx[o] = e;
+            p.topk_w[o] = p.in_w[o];
+            s_idx[tb][j] = e;
         }
     }
     __syncthreads();
 
-    // ---- a4: per-block histogram over local experts (warps 0,1 x 32 tokens)
-    if (warp < 2) {
-        const int tl = warp * 32 + lane;
-        const bool valid = tok0 + tl < p.T;
-        int32_t le[2], rank[2];
-#pragma unroll
-        for (int j = 0; j < 2; ++j) le[j] = valid && j < p.k ? s_idx[tl][j] - p.e_lo : -1;
-        if (valid && p.k > 1 && le[0] == le[1]) __trap();  // duplicate expert in a routing
-        warp_expert_ranks<2>(le, p.k, E_local, valid, rank, s_wcnt[warp], lane);
+    // ---- a4: per-block histogram over local experts
+    if (threadIdx.x < E_local) {
+        const int e = threadIdx.x + p.e_lo;
+        int32_t cnt = 0;
+        for (int tb = 0; tb < ntok; ++tb) {
+            const bool a = s_idx[tb][0] == e, b = p.k > 1 && s_idx[tb][1] == e;
+            if (a && b) __trap();  // duplicate expert in a routing
+            cnt += (a || b) ? 1 : 0;
+        }
+        p.blockcount[(int64_t)blockIdx.x * E_local + threadIdx.x] = cnt;
     }
-    __syncthreads();
-    for (int e = threadIdx.x; e < E_local; e += blockDim.x)
-        p.blockcount[(int64_t)blockIdx.x * E_local + e] = s_wcnt[0][e] + s_wcnt[1][e];
 
-    // ---- a5: the last block to finish runs the exclusive scan (deterministic: one
-    // block, fixed order). Classic threadfence-reduction handshake.
+    // ---- a5: the last block to finish runs the exclusive scan (one block, fixed
+    // order: deterministic). Classic threadfence-reduction handshake.
     __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) s_last = (atomicAdd(p.done, 1u) == gridDim.x - 1);
     __syncthreads();
     if (!s_last) return;
     __threadfence();
-    __shared__ int32_t s_tot[32];
     const int nblk = gridDim.x;
     for (int e = warp; e < E_local; e += kRouteThreads / 32) {
         int32_t running = 0;
@@ -238,79 +222,65 @@ __global__ void __launch_bounds__(kRouteThreads) moe_router_kernel(const RoutePa
 struct PermuteParams {
     const __nv_bfloat16* x;   // [T, d]
     const int32_t* topk_idx;  // [T, k]
-    const float* topk_w;      // [T, k]
-    const int32_t* blockoff;  // [nblk, E_local]
+    const int32_t* blockoff;  // [nblk, E_local] (router blocks of TB tokens)
     const int32_t* offsets;   // [E_local + 1]
     int32_t T, d, k, e_lo, E_local;
+    int32_t TB;               // router block size (tokens)
+    int32_t PT;               // tokens per permute block (1, 2, 4 or 8)
     int32_t* pos;             // [T, k] permuted row per assignment (-1: not local)
     int32_t* pos_aux;         // optional copy for the caller
     __nv_bfloat16* x_perm;    // [Cap, d]
 };
 
-// K2: stable rank -> position, then copy each token row to its k segments with
-// 16-byte vectors (one warp per token row; all loads of a row in flight first).
-__global__ void __launch_bounds__(kRouteThreads) moe_permute_kernel(const PermuteParams p) {
-    __shared__ int32_t s_wcnt[2][32];
-    __shared__ int32_t s_pos[kRouteTokPerBlock][2];
+// K2 (a6): position of each assignment = segment start + rank of its router block
+// + stable rank inside the block (#earlier tokens of the block routed to the same
+// expert), then a 16-byte-vector copy of the token row to each of its k
+// positions (8/PT warps per row, all loads of a row in flight before the stores).
+__global__ void __launch_bounds__(kPermuteThreads) moe_permute_kernel(const PermuteParams p) {
+    __shared__ int32_t s_pos[8][2];
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-    const int tok0 = blockIdx.x * kRouteTokPerBlock;
+    const int tok0 = blockIdx.x * p.PT;
     ptx::pdl_wait();
-    int32_t le[2] = {-1, -1}, rank[2] = {0, 0};
-    const int tl = warp * 32 + lane;
-    const bool valid = warp < 2 && tok0 + tl < p.T;
-    if (warp < 2) {
-        if (valid) {
-#pragma unroll
-            for (int j = 0; j < 2; ++j)
-                if (j < p.k) {
-                    const int e = p.topk_idx[(int64_t)(tok0 + tl) * p.k + j] - p.e_lo;
-                    le[j] = (e >= 0 && e < p.E_local) ? e : -1;
-                }
-        }
-        warp_expert_ranks<2>(le, p.k, p.E_local, valid, rank, s_wcnt[warp], lane);
-    }
-    __syncthreads();
-    if (valid) {
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-            if (j >= p.k) break;
+    if (threadIdx.x < p.PT * p.k) {
+        const int tl = threadIdx.x / p.k, j = threadIdx.x % p.k;
+        const int t = tok0 + tl;
+        if (t < p.T) {
+            const int e = p.topk_idx[(int64_t)t * p.k + j] - p.e_lo;
             int32_t ps = -1;
-            if (le[j] >= 0) {
-                const int e = le[j];
-                ps = p.offsets[e] + p.blockoff[(int64_t)blockIdx.x * p.E_local + e] +
-                     (warp == 1 ? s_wcnt[0][e] : 0) + rank[j];
+            if (e >= 0 && e < p.E_local) {
+                const int b = t / p.TB;
+                int32_t rank = 0;
+                for (int t2 = b * p.TB; t2 < t; ++t2)
+                    for (int j2 = 0; j2 < p.k; ++j2) rank += (p.topk_idx[(int64_t)t2 * p.k + j2] - p.e_lo == e);
+                ps = p.offsets[e] + p.blockoff[(int64_t)b * p.E_local + e] + rank;
             }
-            p.pos[(int64_t)(tok0 + tl) * p.k + j] = ps;
-            if (p.pos_aux) p.pos_aux[(int64_t)(tok0 + tl) * p.k + j] = ps;
+            p.pos[(int64_t)t * p.k + j] = ps;
+            if (p.pos_aux) p.pos_aux[(int64_t)t * p.k + j] = ps;
             s_pos[tl][j] = ps;
         }
     }
     __syncthreads();
-    // row copies: warp w handles tokens [w*8, w*8+8) of the block
-    const int nvec = p.d / 8;  // uint4 per row
-    for (int i = 0; i < kRouteTokPerBlock / 8; ++i) {
-        const int tl2 = warp * (kRouteTokPerBlock / 8) + i;
-        const int t = tok0 + tl2;
-        if (t >= p.T) break;
+    const int wpt = 8 / p.PT;            // warps per token row
+    const int tl = warp / wpt, sw = warp % wpt;
+    const int t = tok0 + tl;
+    if (t < p.T) {
+        const int nvec = p.d / 8;
         const uint4* src = reinterpret_cast<const uint4*>(p.x + (int64_t)t * p.d);
-        int32_t dst_row[2] = {s_pos[tl2][0], p.k > 1 ? s_pos[tl2][1] : -1};
-        for (int v0 = 0; v0 < nvec; v0 += 32 * 8) {
-            uint4 buf[8];
+        const int32_t d0 = s_pos[tl][0], d1 = p.k > 1 ? s_pos[tl][1] : -1;
+        uint4* dst0 = d0 >= 0 ? reinterpret_cast<uint4*>(p.x_perm + (int64_t)d0 * p.d) : nullptr;
+        uint4* dst1 = d1 >= 0 ? reinterpret_cast<uint4*>(p.x_perm + (int64_t)d1 * p.d) : nullptr;
+        const int stride = 32 * wpt;
+        for (int v0 = sw * 32 + lane; v0 < nvec; v0 += 4 * stride) {
+            uint4 buf[4];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const int v = v0 + u * 32 + lane;
-                if (v < nvec) buf[u] = __ldg(src + v);
-            }
+            for (int u = 0; u < 4; ++u)
+                if (v0 + u * stride < nvec) buf[u] = __ldg(src + v0 + u * stride);
 #pragma unroll
-            for (int j = 0; j < 2; ++j) {
-                if (dst_row[j] < 0) continue;
-                uint4* dst = reinterpret_cast<uint4*>(p.x_perm + (int64_t)dst_row[j] * p.d);
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    const int v = v0 + u * 32 + lane;
-                    if (v < nvec) dst[v] = buf[u];
+            for (int u = 0; u < 4; ++u)
+                if (v0 + u * stride < nvec) {
+                    if (dst0) dst0[v0 + u * stride] = buf[u];
+                    if (dst1) dst1[v0 + u * stride] = buf[u];
                 }
-            }
         }
     }
     ptx::pdl_launch_dependents();
@@ -328,13 +298,14 @@ struct CombineParams {
     float* out_f32;           // [T, d] optional (fp32 before rounding)
 };
 
-// K5: out[t] = bf16_rne( sum_j w_j * (sum_s y_s[pos_j]) (+ x[t]) ), fixed order:
+// K5 (a9): out[t] = bf16_rne( sum_j w_j * (sum_s y_s[pos_j]) (+ x[t]) ), fixed order:
 // splits ascending, then r = w_0*s_0, r = fma(w_1, s_1, r), then + x.
+// grid = (ceil(d/1024), T): each thread owns 4 consecutive columns of one token.
 __global__ void __launch_bounds__(256) moe_combine_kernel(const CombineParams p) {
-    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-    const int t = blockIdx.x * 8 + warp;
+    const int t = blockIdx.y;
+    const int c = blockIdx.x * 1024 + threadIdx.x * 4;
     ptx::pdl_wait();
-    if (t < p.T) {
+    if (c < p.d) {
         int32_t pr[2];
         float w[2];
 #pragma unroll
@@ -342,38 +313,35 @@ __global__ void __launch_bounds__(256) moe_combine_kernel(const CombineParams p)
             pr[j] = j < p.k ? p.pos[(int64_t)t * p.k + j] : -1;
             w[j] = j < p.k ? p.topk_w[(int64_t)t * p.k + j] : 0.f;
         }
-        for (int c = lane * 4; c < p.d; c += 128) {
-            float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
+        float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-            for (int j = 0; j < 2; ++j) {
-                if (pr[j] < 0) continue;
-                const float* yr = p.y + (int64_t)pr[j] * p.d + c;
-                float4 s = __ldcs(reinterpret_cast<const float4*>(yr));
-                for (int sp = 1; sp < p.splits; ++sp) {
-                    const float4 u = __ldcs(reinterpret_cast<const float4*>(yr + sp * p.split_stride));
-                    s.x += u.x; s.y += u.y; s.z += u.z; s.w += u.w;
-                }
-                if (j == 0) {
-                    r = make_float4(w[0] * s.x, w[0] * s.y, w[0] * s.z, w[0] * s.w);
-                } else {
-                    r.x = fmaf(w[j], s.x, r.x); r.y = fmaf(w[j], s.y, r.y);
-                    r.z = fmaf(w[j], s.z, r.z); r.w = fmaf(w[j], s.w, r.w);
-                }
+        for (int j = 0; j < 2; ++j) {
+            if (pr[j] < 0) continue;
+            const float* yr = p.y + (int64_t)pr[j] * p.d + c;
+            float4 s = __ldcs(reinterpret_cast<const float4*>(yr));
+#pragma unroll 8
+            for (int sp = 1; sp < p.splits; ++sp) {
+                const float4 u = __ldcs(reinterpret_cast<const float4*>(yr + sp * p.split_stride));
+                s.x += u.x; s.y += u.y; s.z += u.z; s.w += u.w;
             }
-            if (p.x) {
-                float xv[4];
-                const __nv_bfloat162* xs = reinterpret_cast<const __nv_bfloat162*>(p.x + (int64_t)t * p.d + c);
-                float2 a = __bfloat1622float2(xs[0]), b = __bfloat1622float2(xs[1]);
-                xv[0] = a.x; xv[1] = a.y; xv[2] = b.x; xv[3] = b.y;
-                r.x += xv[0]; r.y += xv[1]; r.z += xv[2]; r.w += xv[3];
+            if (j == 0) {
+                r = make_float4(w[0] * s.x, w[0] * s.y, w[0] * s.z, w[0] * s.w);
+            } else {
+                r.x = fmaf(w[j], s.x, r.x); r.y = fmaf(w[j], s.y, r.y);
+                r.z = fmaf(w[j], s.z, r.z); r.w = fmaf(w[j], s.w, r.w);
             }
-            if (p.out_f32) *reinterpret_cast<float4*>(p.out_f32 + (int64_t)t * p.d + c) = r;
-            __nv_bfloat162 o0 = __floats2bfloat162_rn(r.x, r.y), o1 = __floats2bfloat162_rn(r.z, r.w);
-            uint2 ov;
-            ov.x = *reinterpret_cast<uint32_t*>(&o0);
-            ov.y = *reinterpret_cast<uint32_t*>(&o1);
-            *reinterpret_cast<uint2*>(p.out + (int64_t)t * p.d + c) = ov;
         }
+        if (p.x) {
+            const __nv_bfloat162* xs = reinterpret_cast<const __nv_bfloat162*>(p.x + (int64_t)t * p.d + c);
+            const float2 a = __bfloat1622float2(xs[0]), b = __bfloat1622float2(xs[1]);
+            r.x += a.x; r.y += a.y; r.z += b.x; r.w += b.y;
+        }
+        if (p.out_f32) __stcs(reinterpret_cast<float4*>(p.out_f32 + (int64_t)t * p.d + c), r);
+        __nv_bfloat162 o0 = __floats2bfloat162_rn(r.x, r.y), o1 = __floats2bfloat162_rn(r.z, r.w);
+        uint2 ov;
+        ov.x = *reinterpret_cast<uint32_t*>(&o0);
+        ov.y = *reinterpret_cast<uint32_t*>(&o1);
+        *reinterpret_cast<uint2*>(p.out + (int64_t)t * p.d + c) = ov;
     }
     ptx::pdl_launch_dependents();
 }

@@ -318,7 +318,10 @@ moe_status run_swap(moe_ctx* c, int nbi, const moe_expert_weights* w, int splits
 moe_status run_local(moe_ctx* c, const void* tokens, int T, const void* router_w, const int32_t* in_idx,
                      const float* in_w, const moe_expert_weights* w, const moe_aux* aux, bool use_swap,
                      int* splits_out, cudaStream_t st) {
-    const int nblk = (T + kRouteTokPerBlock - 1) / kRouteTokPerBlock;
+    // router block size: 2 tokens (many blocks, low latency) for small batches,
+    // 8 tokens (W_g chunks reused from registers) for large E<=8 batches
+    const int TB = (c->E <= 8 && T >= 2048) ? 8 : 2;
+    const int nblk = (T + TB - 1) / TB;
     RouteParams rp{};
     rp.x = static_cast<const __nv_bfloat16*>(tokens);
     rp.wg = static_cast<const __nv_bfloat16*>(router_w);
@@ -331,16 +334,22 @@ moe_status run_local(moe_ctx* c, const void* tokens, int T, const void* router_w
     rp.blockcount = c->blockcount; rp.blockoff = c->blockoff;
     rp.counts = c->counts; rp.offsets = c->offsets; rp.done = c->done;
     moe_status s;
-    if (c->E <= 8) s = launch(c, kSlotRouter, moe_router_kernel<8>, dim3(nblk), dim3(kRouteThreads), 0, st, rp);
-    else if (c->E <= 16) s = launch(c, kSlotRouter, moe_router_kernel<16>, dim3(nblk), dim3(kRouteThreads), 0, st, rp);
-    else s = launch(c, kSlotRouter, moe_router_kernel<32>, dim3(nblk), dim3(kRouteThreads), 0, st, rp);
+    const dim3 rg(nblk), rb(kRouteThreads);
+    if (TB == 8) s = launch(c, kSlotRouter, moe_router_kernel<8, 8>, rg, rb, 0, st, rp);
+    else if (c->E <= 8) s = launch(c, kSlotRouter, moe_router_kernel<8, 2>, rg, rb, 0, st, rp);
+    else if (c->E <= 16) s = launch(c, kSlotRouter, moe_router_kernel<16, 2>, rg, rb, 0, st, rp);
+    else s = launch(c, kSlotRouter, moe_router_kernel<32, 2>, rg, rb, 0, st, rp);
     if (s) return s;
 
     PermuteParams pp{};
-    pp.x = rp.x; pp.topk_idx = c->topk_idx; pp.topk_w = c->topk_w; pp.blockoff = c->blockoff; pp.offsets = c->offsets;
+    pp.x = rp.x; pp.topk_idx = c->topk_idx; pp.blockoff = c->blockoff; pp.offsets = c->offsets;
     pp.T = T; pp.d = c->d; pp.k = c->k; pp.e_lo = c->e_lo; pp.E_local = c->E_local;
+    pp.TB = TB;
+    pp.PT = T <= 1024 ? 2 : 8;
     pp.pos = c->pos; pp.pos_aux = aux ? aux->pos : nullptr; pp.x_perm = c->x_perm;
-    if ((s = launch(c, kSlotPermute, moe_permute_kernel, dim3(nblk), dim3(kRouteThreads), 0, st, pp))) return s;
+    if ((s = launch(c, kSlotPermute, moe_permute_kernel, dim3((T + pp.PT - 1) / pp.PT), dim3(kPermuteThreads), 0,
+                    st, pp)))
+        return s;
 
     int splits = 1;
     if (use_swap) {
@@ -448,7 +457,7 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
     derive_shape(cfg, c->G, c->E_local, c->e_lo, c->f_local, c->f_off);
     c->rank = cfg->rank;
     c->max_T = cfg->max_tokens;
-    c->nblk_max = (c->max_T + kRouteTokPerBlock - 1) / kRouteTokPerBlock;
+    c->nblk_max = (int)(((int64_t)c->max_T * (cfg->par == MOE_PAR_EP ? c->G : 1) + 1) / 2 + 1);
 
     // EP: a rank may receive up to every token of every peer (dropless, reading R6).
     const int64_t rows_in = cfg->par == MOE_PAR_EP ? (int64_t)c->max_T * c->G : c->max_T;
@@ -468,7 +477,7 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
 #define ALLOC(ptr, bytes)                                                               \
     if ((e = cudaMalloc(reinterpret_cast<void**>(&(ptr)), (bytes))) != cudaSuccess)     \
         return fail_init(#ptr, e);
-    const int64_t nblk_rows = (rows_in + kRouteTokPerBlock - 1) / kRouteTokPerBlock + 1;
+    const int64_t nblk_rows = c->nblk_max;
     ALLOC(c->topk_idx, sizeof(int32_t) * c->max_T * c->k);
     ALLOC(c->topk_w, sizeof(float) * c->max_T * c->k);
     ALLOC(c->pos, sizeof(int32_t) * c->max_T * c->k);
@@ -709,7 +718,7 @@ moe_status forward_impl(moe_ctx* c, const void* tokens, int32_t T, const void* r
     cp.T = T; cp.d = c->d; cp.k = c->k;
     cp.out = static_cast<__nv_bfloat16*>(out);
     cp.out_f32 = aux ? aux->out_f32 : nullptr;
-    return launch(c, kSlotCombine, moe_combine_kernel, dim3((T + 7) / 8), dim3(256), 0, st, cp);
+    return launch(c, kSlotCombine, moe_combine_kernel, dim3((c->d + 1023) / 1024, T), dim3(256), 0, st, cp);
 }
 
 }  // namespace
