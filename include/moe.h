@@ -199,6 +199,19 @@ MOE_API moe_status moe_nccl_comm_init(const void* id128, int32_t world, int32_t 
                               void** comm);
 MOE_API moe_status moe_nccl_comm_destroy(void* comm);
 
+/* TEST TRANSPORT. A loopback "communicator" that emulates a G-rank group inside
+ * ONE process on ONE device: G contexts (par EP/TP, world G, rank r, nccl_comm =
+ * the rank handle) are driven by G host threads; each collective synchronises
+ * the caller's stream, meets the other ranks at a host barrier and moves data
+ * with device copies (fp32 sums in ascending rank order). It runs the exact EP /
+ * TP device path so parity can be tested at G = 2..8 without G GPUs; it is not
+ * a production transport (no overlap, host-synchronous, not graph-capturable).
+ *   moe_loopback_comm_create(world, &group); moe_loopback_comm_rank(group, r, &comm_r);
+ *   moe_loopback_comm_destroy(comm_r) for every rank handle, then (group).      */
+MOE_API moe_status moe_loopback_comm_create(int32_t world, void** group);
+MOE_API moe_status moe_loopback_comm_rank(void* group, int32_t rank, void** comm);
+MOE_API moe_status moe_loopback_comm_destroy(void* group_or_rank);
+
 #ifdef __cplusplus
 }
 #endif

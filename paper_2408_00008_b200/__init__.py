@@ -36,7 +36,8 @@ KERNEL_SLOTS = ("router", "permute", "gemm1_w13_swiglu", "gemm2_w2", "combine", 
 EXPORTED = ("moe_init", "moe_packed_sizes", "moe_pack_weights", "moe_forward", "moe_forward_routed",
             "moe_forward_host", "moe_destroy", "moe_last_error", "moe_status_string", "moe_set_profiling",
             "moe_reset_profile", "moe_kernel_times", "moe_launch_count", "moe_nccl_unique_id",
-            "moe_nccl_comm_init", "moe_nccl_comm_destroy")
+            "moe_nccl_comm_init", "moe_nccl_comm_destroy", "moe_loopback_comm_create", "moe_loopback_comm_rank",
+            "moe_loopback_comm_destroy")
 
 
 class moe_config(ctypes.Structure):
@@ -77,6 +78,9 @@ _sig = {
     "moe_nccl_unique_id": ([_P], _I32),
     "moe_nccl_comm_init": ([_P, _I32, _I32, _I32, ctypes.POINTER(_P)], _I32),
     "moe_nccl_comm_destroy": ([_P], _I32),
+    "moe_loopback_comm_create": ([_I32, ctypes.POINTER(_P)], _I32),
+    "moe_loopback_comm_rank": ([_P, _I32, ctypes.POINTER(_P)], _I32),
+    "moe_loopback_comm_destroy": ([_P], _I32),
 }
 for _name, (_args, _res) in _sig.items():
     _fn = getattr(_lib, _name)
@@ -208,6 +212,31 @@ def moe_nccl_comm_init(uid: bytes, world: int, rank: int, device: int):
 
 def moe_nccl_comm_destroy(comm):
     _check(_lib.moe_nccl_comm_destroy(comm))
+
+
+def moe_loopback_comm_create(world: int):
+    g = _P()
+    _check(_lib.moe_loopback_comm_create(world, ctypes.byref(g)))
+    return g.value
+
+
+def moe_loopback_comm_rank(group, rank: int):
+    c = _P()
+    _check(_lib.moe_loopback_comm_rank(group, rank, ctypes.byref(c)))
+    return c.value
+
+
+def moe_loopback_comm_destroy(handle):
+    _check(_lib.moe_loopback_comm_destroy(handle))
+
+
+def nccl_comm_from_process_group(world: int, rank: int, device: int):
+    """Create libmoe's NCCL communicator for the current torch.distributed group:
+    rank 0 draws the ncclUniqueId, the host process group broadcasts it."""
+    import torch.distributed as dist
+    obj = [moe_nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    return moe_nccl_comm_init(obj[0], world, rank, device)
 
 
 # ------------------------------------------------------------------ convenience owner

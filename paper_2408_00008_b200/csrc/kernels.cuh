@@ -28,16 +28,27 @@ struct RouteParams {
     const int32_t* in_idx;    // routed mode: caller's [T, k] (else nullptr)
     const float* in_w;        // routed mode: caller's gates [T, k]
     int32_t T, d, E, k;
-    int32_t e_lo, e_hi;       // experts owned by this rank: [e_lo, e_hi) (all for NONE/TP)
+    // histogram key of an assignment to expert e: (e - key_lo) / key_div, counted
+    // when 0 <= key < nkeys. Local experts: key_lo = e_lo, key_div = 1, nkeys = E_local.
+    // EP dispatch: key = destination rank (key_lo = 0, key_div = E/G, nkeys = G).
+    int32_t key_lo, key_div, nkeys;
+    int32_t seg_align;        // segment padding of the scan (128: GEMM M tile; 1: none)
+    int32_t allow_neg;        // routed mode: negative expert index = empty slot (EP receive)
     float* logits;            // [T, E] optional debug output
     int32_t* topk_idx;        // [T, k] workspace
     float* topk_w;            // [T, k] workspace
-    int32_t* blockcount;      // [nblk, E_local]
-    int32_t* blockoff;        // [nblk, E_local]
-    int32_t* counts;          // [E_local]
-    int32_t* offsets;         // [E_local + 1]
+    int32_t* blockcount;      // [nblk, nkeys]
+    int32_t* blockoff;        // [nblk, nkeys]
+    int32_t* counts;          // [nkeys]
+    int32_t* offsets;         // [nkeys + 1]
     unsigned int* done;       // block-completion counter (zero between launches)
 };
+
+__device__ __forceinline__ int hist_key(int e, int key_lo, int key_div, int nkeys) {
+    if (e < key_lo) return -1;
+    const int q = (e - key_lo) / key_div;
+    return q < nkeys ? q : -1;
+}
 
 __device__ __forceinline__ void bf16x8_to_f32(const uint4& v, float (&f)[8]) {
     const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
@@ -64,7 +75,7 @@ __global__ void __launch_bounds__(kRouteThreads) moe_router_kernel(const RoutePa
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int tok0 = blockIdx.x * TB;
     const int ntok = min(TB, p.T - tok0);
-    const int E_local = p.e_hi - p.e_lo;
+    const int NK = p.nkeys;
 
     ptx::pdl_wait();
 
@@ -161,24 +172,24 @@ __global__ void __launch_bounds__(kRouteThreads) moe_router_kernel(const RoutePa
             const int tb = i / p.k, j = i % p.k;
             const int64_t o = (int64_t)(tok0 + tb) * p.k + j;
             const int e = p.in_idx[o];
-            if (e < 0 || e >= p.E) __trap();
+            if (e >= p.E || (e < 0 && !p.allow_neg)) __trap();
             p.topk_idx[o] = e;
-            p.topk_w[o] = p.in_w[o];
+            p.topk_w[o] = p.in_w ? p.in_w[o] : 1.f;
             s_idx[tb][j] = e;
         }
     }
     __syncthreads();
 
-    // ---- a4: per-block histogram over local experts
-    if (threadIdx.x < E_local) {
-        const int e = threadIdx.x + p.e_lo;
+    // ---- a4: per-block histogram over the keys (local experts / destination ranks)
+    if (threadIdx.x < NK) {
         int32_t cnt = 0;
         for (int tb = 0; tb < ntok; ++tb) {
-            const bool a = s_idx[tb][0] == e, b = p.k > 1 && s_idx[tb][1] == e;
-            if (a && b) __trap();  // duplicate expert in a routing
-            cnt += (a || b) ? 1 : 0;
+            const int e0 = s_idx[tb][0], e1 = p.k > 1 ? s_idx[tb][1] : -1;
+            if (p.k > 1 && e0 == e1 && e0 >= 0) __trap();  // duplicate expert in a routing
+            cnt += (e0 >= 0 && hist_key(e0, p.key_lo, p.key_div, NK) == (int)threadIdx.x) ? 1 : 0;
+            cnt += (e1 >= 0 && hist_key(e1, p.key_lo, p.key_div, NK) == (int)threadIdx.x) ? 1 : 0;
         }
-        p.blockcount[(int64_t)blockIdx.x * E_local + threadIdx.x] = cnt;
+        p.blockcount[(int64_t)blockIdx.x * NK + threadIdx.x] = cnt;
     }
 
     // ---- a5: the last block to finish runs the exclusive scan (one block, fixed
@@ -190,18 +201,18 @@ __global__ void __launch_bounds__(kRouteThreads) moe_router_kernel(const RoutePa
     if (!s_last) return;
     __threadfence();
     const int nblk = gridDim.x;
-    for (int e = warp; e < E_local; e += kRouteThreads / 32) {
+    for (int e = warp; e < NK; e += kRouteThreads / 32) {
         int32_t running = 0;
         for (int base = 0; base < nblk; base += 32) {
             const int b = base + lane;
-            const int32_t v = b < nblk ? __ldcg(&p.blockcount[(int64_t)b * E_local + e]) : 0;
+            const int32_t v = b < nblk ? __ldcg(&p.blockcount[(int64_t)b * NK + e]) : 0;
             int32_t inc = v;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const int32_t u = __shfl_up_sync(0xffffffffu, inc, o);
                 if (lane >= o) inc += u;
             }
-            if (b < nblk) p.blockoff[(int64_t)b * E_local + e] = running + inc - v;
+            if (b < nblk) p.blockoff[(int64_t)b * NK + e] = running + inc - v;
             running += __shfl_sync(0xffffffffu, inc, 31);
         }
         if (lane == 0) s_tot[e] = running;
@@ -210,9 +221,9 @@ __global__ void __launch_bounds__(kRouteThreads) moe_router_kernel(const RoutePa
     if (threadIdx.x == 0) {
         int32_t off = 0;
         p.offsets[0] = 0;
-        for (int e = 0; e < E_local; ++e) {
+        for (int e = 0; e < NK; ++e) {
             p.counts[e] = s_tot[e];
-            off += (s_tot[e] + kSegAlign - 1) / kSegAlign * kSegAlign;
+            off += (s_tot[e] + p.seg_align - 1) / p.seg_align * p.seg_align;
             p.offsets[e + 1] = off;
         }
         *p.done = 0u;  // ready for the next forward (kernel boundary orders it)
@@ -222,9 +233,12 @@ __global__ void __launch_bounds__(kRouteThreads) moe_router_kernel(const RoutePa
 struct PermuteParams {
     const __nv_bfloat16* x;   // [T, d]
     const int32_t* topk_idx;  // [T, k]
-    const int32_t* blockoff;  // [nblk, E_local] (router blocks of TB tokens)
-    const int32_t* offsets;   // [E_local + 1]
-    int32_t T, d, k, e_lo, E_local;
+    const int32_t* blockoff;  // [nblk, nkeys] (router blocks of TB tokens)
+    const int32_t* offsets;   // [nkeys + 1] (normal mode)
+    int32_t T, d, k;
+    int32_t key_lo, key_div, nkeys;  // as RouteParams
+    int32_t cap;              // EP dispatch mode: rows per destination bucket (0 = normal mode)
+    int32_t* meta;            // EP dispatch mode: [nkeys * cap] local expert id at the destination
     int32_t TB;               // router block size (tokens)
     int32_t PT;               // tokens per permute block (1, 2, 4 or 8)
     int32_t* pos;             // [T, k] permuted row per assignment (-1: not local)
@@ -245,14 +259,26 @@ __global__ void __launch_bounds__(kPermuteThreads) moe_permute_kernel(const Perm
         const int tl = threadIdx.x / p.k, j = threadIdx.x % p.k;
         const int t = tok0 + tl;
         if (t < p.T) {
-            const int e = p.topk_idx[(int64_t)t * p.k + j] - p.e_lo;
+            const int ex = p.topk_idx[(int64_t)t * p.k + j];
+            const int e = ex >= 0 ? hist_key(ex, p.key_lo, p.key_div, p.nkeys) : -1;
             int32_t ps = -1;
-            if (e >= 0 && e < p.E_local) {
+            if (e >= 0) {
                 const int b = t / p.TB;
                 int32_t rank = 0;
-                for (int t2 = b * p.TB; t2 < t; ++t2)
-                    for (int j2 = 0; j2 < p.k; ++j2) rank += (p.topk_idx[(int64_t)t2 * p.k + j2] - p.e_lo == e);
-                ps = p.offsets[e] + p.blockoff[(int64_t)b * p.E_local + e] + rank;
+                // stable order = (token, slot): count earlier assignments with the same key.
+                // (A token may put both its rows in one EP destination bucket.)
+                for (int t2 = b * p.TB; t2 <= t; ++t2)
+                    for (int j2 = 0; j2 < (t2 == t ? j : p.k); ++j2) {
+                        const int e2 = p.topk_idx[(int64_t)t2 * p.k + j2];
+                        rank += (e2 >= 0 && hist_key(e2, p.key_lo, p.key_div, p.nkeys) == e);
+                    }
+                const int32_t r = p.blockoff[(int64_t)b * p.nkeys + e] + rank;
+                if (p.cap > 0) {  // EP dispatch: bucket of destination rank e
+                    ps = e * p.cap + r;
+                    p.meta[ps] = ex - e * p.key_div;  // expert index local to the destination
+                } else {
+                    ps = p.offsets[e] + r;
+                }
             }
             p.pos[(int64_t)t * p.k + j] = ps;
             if (p.pos_aux) p.pos_aux[(int64_t)t * p.k + j] = ps;
@@ -337,11 +363,60 @@ __global__ void __launch_bounds__(256) moe_combine_kernel(const CombineParams p)
             r.x += a.x; r.y += a.y; r.z += b.x; r.w += b.y;
         }
         if (p.out_f32) __stcs(reinterpret_cast<float4*>(p.out_f32 + (int64_t)t * p.d + c), r);
+        if (p.out == nullptr) return;
         __nv_bfloat162 o0 = __floats2bfloat162_rn(r.x, r.y), o1 = __floats2bfloat162_rn(r.z, r.w);
         uint2 ov;
         ov.x = *reinterpret_cast<uint32_t*>(&o0);
         ov.y = *reinterpret_cast<uint32_t*>(&o1);
         *reinterpret_cast<uint2*>(p.out + (int64_t)t * p.d + c) = ov;
+    }
+    ptx::pdl_launch_dependents();
+}
+
+// EP return path: ysend[slot] = sum_s y_s[pos[slot]] for every occupied receive
+// slot (fp32 rows; splits summed in ascending order, as in the combine).
+__global__ void __launch_bounds__(256) moe_ep_gather_kernel(const float* y, int64_t split_stride, int splits,
+                                                            const int32_t* pos, int nslots, int d, float* ysend) {
+    const int slot = blockIdx.y;
+    const int c = blockIdx.x * 1024 + threadIdx.x * 4;
+    ptx::pdl_wait();
+    if (slot < nslots && c < d) {
+        const int32_t pr = pos[slot];
+        if (pr >= 0) {
+            const float* yr = y + (int64_t)pr * d + c;
+            float4 s = __ldcs(reinterpret_cast<const float4*>(yr));
+#pragma unroll 8
+            for (int sp = 1; sp < splits; ++sp) {
+                const float4 u = __ldcs(reinterpret_cast<const float4*>(yr + sp * split_stride));
+                s.x += u.x; s.y += u.y; s.z += u.z; s.w += u.w;
+            }
+            *reinterpret_cast<float4*>(ysend + (int64_t)slot * d + c) = s;
+        }
+    }
+    ptx::pdl_launch_dependents();
+}
+
+// TP epilogue after the fp32 reduce-scatter: this rank's shard of the summed
+// output (+ residual) -> one bf16 RNE rounding, written in place into its slice of
+// `out` (all-gathered afterwards); optional fp32 copy into its slice of out_f32.
+__global__ void __launch_bounds__(256) moe_tp_finish_kernel(const float* shard, int64_t n, int64_t base,
+                                                            const __nv_bfloat16* x, __nv_bfloat16* out,
+                                                            float* out_f32) {
+    ptx::pdl_wait();
+    for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * 4; i < n;
+         i += (int64_t)gridDim.x * blockDim.x * 4) {
+        float4 r = *reinterpret_cast<const float4*>(shard + i);
+        if (x) {
+            const __nv_bfloat162* xs = reinterpret_cast<const __nv_bfloat162*>(x + base + i);
+            const float2 a = __bfloat1622float2(xs[0]), b = __bfloat1622float2(xs[1]);
+            r.x += a.x; r.y += a.y; r.z += b.x; r.w += b.y;
+        }
+        if (out_f32) *reinterpret_cast<float4*>(out_f32 + base + i) = r;
+        __nv_bfloat162 o0 = __floats2bfloat162_rn(r.x, r.y), o1 = __floats2bfloat162_rn(r.z, r.w);
+        uint2 ov;
+        ov.x = *reinterpret_cast<uint32_t*>(&o0);
+        ov.y = *reinterpret_cast<uint32_t*>(&o1);
+        *reinterpret_cast<uint2*>(out + base + i) = ov;
     }
     ptx::pdl_launch_dependents();
 }

@@ -17,6 +17,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <condition_variable>
 #include <mutex>
 #include <new>
 #include <string>
@@ -155,6 +156,8 @@ struct moe_ctx {
     __nv_bfloat16 *ep_send = nullptr, *ep_recv = nullptr;
     float *ep_ysend = nullptr, *ep_yrecv = nullptr;
     int32_t *ep_meta_send = nullptr, *ep_meta_recv = nullptr;
+    int32_t *ep_ridx = nullptr, *ep_rpos = nullptr;
+    float* ep_rw = nullptr;
     // TMA descriptors: workspace operands
     CUtensorMap tm_x_tiled{}, tm_h_tiled{};
     CUtensorMap tm_x_swap[3]{}, tm_h_swap[3]{};  // NB = 32, 64, 128
@@ -271,6 +274,8 @@ moe_status validate_cfg(const moe_config* cfg, moe_ctx* c) {
     if (cfg->ffn <= 0 || cfg->ffn % (128 * (cfg->par == MOE_PAR_TP ? G : 1)))
         return fail(c, MOE_ERR_INVALID, "ffn / tp_world must be a positive multiple of 128");
     if (cfg->par == MOE_PAR_EP && cfg->num_experts % G) return fail(c, MOE_ERR_INVALID, "num_experts % ep_world != 0");
+    if (cfg->par == MOE_PAR_TP && cfg->hidden % (4 * G))
+        return fail(c, MOE_ERR_INVALID, "TP needs hidden % (4*world) == 0 (reduce-scatter shards)");
     if (cfg->par != MOE_PAR_NONE && G > 1 && !cfg->nccl_comm) return fail(c, MOE_ERR_INVALID, "nccl_comm required");
     if (cfg->split_k < 0 || cfg->split_k > 8) return fail(c, MOE_ERR_INVALID, "split_k must be in [0,8]");
     for (int i = 0; i < 6; ++i)
@@ -313,24 +318,40 @@ moe_status run_swap(moe_ctx* c, int nbi, const moe_expert_weights* w, int splits
     return launch_gemm<kG2Swap, NB>(c, kSlotGemm2, p2, c->tm_w2_swap, c->tm_h_swap[nbi], c->num_sms, st);
 }
 
-// Core single-rank pipeline: tokens -> (router or given routing) -> permute -> GEMMs -> y.
-// Returns the split count used (for the combine) via *splits_out.
-moe_status run_local(moe_ctx* c, const void* tokens, int T, const void* router_w, const int32_t* in_idx,
-                     const float* in_w, const moe_expert_weights* w, const moe_aux* aux, bool use_swap,
-                     int* splits_out, cudaStream_t st) {
+// One routing + permutation pass (K1 + K2) over `T` rows of `x`.
+struct RouteSpec {
+    const void* x = nullptr;     // [T, d] bf16 rows
+    int T = 0, k = 0;
+    const void* router_w = nullptr;       // router mode
+    const int32_t* in_idx = nullptr;      // routed mode
+    const float* in_w = nullptr;
+    int allow_neg = 0;
+    int key_lo = 0, key_div = 1, nkeys = 0, seg_align = kSegAlign;
+    float* logits = nullptr;
+    int32_t* topk_idx = nullptr;
+    float* topk_w = nullptr;
+    int32_t* pos = nullptr;
+    int32_t* pos_aux = nullptr;
+    void* dst_rows = nullptr;    // x_perm (normal) or EP send buffer (dispatch)
+    int cap = 0;                 // > 0: EP dispatch buckets of `cap` rows per key
+    int32_t* meta = nullptr;
+};
+
+moe_status route_and_permute(moe_ctx* c, const RouteSpec& r, cudaStream_t st) {
     // router block size: 2 tokens (many blocks, low latency) for small batches,
     // 8 tokens (W_g chunks reused from registers) for large E<=8 batches
-    const int TB = (c->E <= 8 && T >= 2048) ? 8 : 2;
-    const int nblk = (T + TB - 1) / TB;
+    const int TB = (r.in_idx == nullptr && c->E <= 8 && r.T >= 2048) ? 8 : 2;
+    const int nblk = (r.T + TB - 1) / TB;
     RouteParams rp{};
-    rp.x = static_cast<const __nv_bfloat16*>(tokens);
-    rp.wg = static_cast<const __nv_bfloat16*>(router_w);
-    rp.in_idx = in_idx;
-    rp.in_w = in_w;
-    rp.T = T; rp.d = c->d; rp.E = c->E; rp.k = c->k;
-    rp.e_lo = c->e_lo; rp.e_hi = c->e_lo + c->E_local;
-    rp.logits = aux ? aux->logits : nullptr;
-    rp.topk_idx = c->topk_idx; rp.topk_w = c->topk_w;
+    rp.x = static_cast<const __nv_bfloat16*>(r.x);
+    rp.wg = static_cast<const __nv_bfloat16*>(r.router_w);
+    rp.in_idx = r.in_idx;
+    rp.in_w = r.in_w;
+    rp.T = r.T; rp.d = c->d; rp.E = c->E; rp.k = r.k;
+    rp.key_lo = r.key_lo; rp.key_div = r.key_div; rp.nkeys = r.nkeys; rp.seg_align = r.seg_align;
+    rp.allow_neg = r.allow_neg;
+    rp.logits = r.logits;
+    rp.topk_idx = r.topk_idx; rp.topk_w = r.topk_w;
     rp.blockcount = c->blockcount; rp.blockoff = c->blockoff;
     rp.counts = c->counts; rp.offsets = c->offsets; rp.done = c->done;
     moe_status s;
@@ -342,25 +363,39 @@ moe_status run_local(moe_ctx* c, const void* tokens, int T, const void* router_w
     if (s) return s;
 
     PermuteParams pp{};
-    pp.x = rp.x; pp.topk_idx = c->topk_idx; pp.blockoff = c->blockoff; pp.offsets = c->offsets;
-    pp.T = T; pp.d = c->d; pp.k = c->k; pp.e_lo = c->e_lo; pp.E_local = c->E_local;
+    pp.x = rp.x; pp.topk_idx = r.topk_idx; pp.blockoff = c->blockoff; pp.offsets = c->offsets;
+    pp.T = r.T; pp.d = c->d; pp.k = r.k;
+    pp.key_lo = r.key_lo; pp.key_div = r.key_div; pp.nkeys = r.nkeys;
+    pp.cap = r.cap; pp.meta = r.meta;
     pp.TB = TB;
-    pp.PT = T <= 1024 ? 2 : 8;
-    pp.pos = c->pos; pp.pos_aux = aux ? aux->pos : nullptr; pp.x_perm = c->x_perm;
-    if ((s = launch(c, kSlotPermute, moe_permute_kernel, dim3((T + pp.PT - 1) / pp.PT), dim3(kPermuteThreads), 0,
-                    st, pp)))
-        return s;
+    pp.PT = r.T <= 1024 ? 2 : 8;
+    pp.pos = r.pos; pp.pos_aux = r.pos_aux; pp.x_perm = static_cast<__nv_bfloat16*>(r.dst_rows);
+    return launch(c, kSlotPermute, moe_permute_kernel, dim3((r.T + pp.PT - 1) / pp.PT), dim3(kPermuteThreads), 0,
+                  st, pp);
+}
 
+// K3 + K4 over the expert segments described by the device-side counts/offsets.
+// rows_bound: upper bound of the rows of any one local expert (picks the swap-path
+// token tile NB so one tile covers the whole expert at decode); rows_total: bound
+// of all permuted rows (sizes the split-K partial buffers).
+moe_status run_gemms(moe_ctx* c, bool swap, int64_t rows_bound, int64_t rows_total, int* splits_out,
+                     cudaStream_t st) {
+    moe_status s;
     int splits = 1;
-    if (use_swap) {
-        splits = *splits_out;
-        const int nbw = std::max(32, std::min(128, next_pow2(T)));
-        if (nbw == 32) s = run_swap<32>(c, 0, w, splits, st);
-        else if (nbw == 64) s = run_swap<64>(c, 1, w, splits, st);
-        else s = run_swap<128>(c, 2, w, splits, st);
+    c->split_stride = 0;
+    if (swap) {
+        const int64_t rows_needed = round_up(rows_total + (int64_t)c->E_local * (kSegAlign - 1), kSegAlign);
+        splits = c->cfg.split_k ? c->cfg.split_k : c->max_splits;
+        splits = (int)std::max<int64_t>(1, std::min<int64_t>(splits, c->y_elems / (rows_needed * c->d)));
+        splits = std::min(splits, c->f_local / kBK);  // every split owns >= 1 K block
+        c->split_stride = rows_needed * c->d;
+        const int nbw = (int)std::max<int64_t>(32, std::min<int64_t>(128, next_pow2((int)std::min<int64_t>(rows_bound, 1 << 20))));
+        if (nbw == 32) s = run_swap<32>(c, 0, nullptr, splits, st);
+        else if (nbw == 64) s = run_swap<64>(c, 1, nullptr, splits, st);
+        else s = run_swap<128>(c, 2, nullptr, splits, st);
         if (s) return s;
     } else {
-        const int64_t mt_max = (int64_t)T * c->k / 128 + c->E_local;
+        const int64_t mt_max = rows_total / 128 + c->E_local;
         const int g1 = (int)std::min<int64_t>(c->num_sms, mt_max * (c->f_local / 128));
         const int g2 = (int)std::min<int64_t>(c->num_sms, mt_max * ((c->d + 255) / 256));
         GemmParams p1{c->counts, c->offsets, c->E_local, c->d, c->f_local, 1, c->h, 0};
@@ -369,18 +404,158 @@ moe_status run_local(moe_ctx* c, const void* tokens, int T, const void* router_w
         if ((s = launch_gemm<kG2Tiled, 256>(c, kSlotGemm2, p2, c->tm_h_tiled, c->tm_w2_tiled, g2, st))) return s;
     }
     *splits_out = splits;
-    if (aux) {
-        if (aux->topk_idx)
-            CUDA_TRY(c, cudaMemcpyAsync(aux->topk_idx, c->topk_idx, sizeof(int32_t) * T * c->k, cudaMemcpyDeviceToDevice, st));
-        if (aux->topk_w)
-            CUDA_TRY(c, cudaMemcpyAsync(aux->topk_w, c->topk_w, sizeof(float) * T * c->k, cudaMemcpyDeviceToDevice, st));
-        if (aux->expert_counts)
-            CUDA_TRY(c, cudaMemcpyAsync(aux->expert_counts, c->counts, sizeof(int32_t) * c->E_local, cudaMemcpyDeviceToDevice, st));
-        if (aux->expert_offsets)
-            CUDA_TRY(c, cudaMemcpyAsync(aux->expert_offsets, c->offsets, sizeof(int32_t) * (c->E_local + 1), cudaMemcpyDeviceToDevice, st));
-    }
     return MOE_OK;
 }
+
+moe_status copy_aux(moe_ctx* c, const moe_aux* aux, int T, cudaStream_t st) {
+    if (!aux || T <= 0) return MOE_OK;
+    if (aux->topk_idx)
+        CUDA_TRY(c, cudaMemcpyAsync(aux->topk_idx, c->topk_idx, sizeof(int32_t) * T * c->k, cudaMemcpyDeviceToDevice, st));
+    if (aux->topk_w)
+        CUDA_TRY(c, cudaMemcpyAsync(aux->topk_w, c->topk_w, sizeof(float) * T * c->k, cudaMemcpyDeviceToDevice, st));
+    return MOE_OK;
+}
+
+moe_status copy_aux_segments(moe_ctx* c, const moe_aux* aux, cudaStream_t st) {
+    if (!aux) return MOE_OK;
+    if (aux->expert_counts)
+        CUDA_TRY(c, cudaMemcpyAsync(aux->expert_counts, c->counts, sizeof(int32_t) * c->E_local, cudaMemcpyDeviceToDevice, st));
+    if (aux->expert_offsets)
+        CUDA_TRY(c, cudaMemcpyAsync(aux->expert_offsets, c->offsets, sizeof(int32_t) * (c->E_local + 1), cudaMemcpyDeviceToDevice, st));
+    return MOE_OK;
+}
+
+// profiling of non-kernel steps (NCCL) on the launch stream
+struct StepTimer {
+    moe_ctx* c; int slot; cudaStream_t st; cudaEvent_t a = nullptr;
+    StepTimer(moe_ctx* c_, int slot_, cudaStream_t st_) : c(c_), slot(slot_), st(st_) {
+        if (c->profiling) { a = take_event(c); cudaEventRecord(a, st); }
+    }
+    void done() {
+        if (c->profiling && a) {
+            cudaEvent_t b = take_event(c);
+            cudaEventRecord(b, st);
+            c->pending.push_back({slot, a, b});
+            a = nullptr;
+        }
+    }
+};
+
+#define NCCL_TRY(ctx, expr)                                                                          \
+    do {                                                                                             \
+        ncclResult_t _r = (expr);                                                                    \
+        if (_r != 0) return fail(ctx, MOE_ERR_NCCL, "%s failed: %s", #expr, g_nccl.GetErrorString(_r)); \
+    } while (0)
+
+// ------------------------------------------------------------------ collectives
+// Two transports behind the same three collectives: NCCL (production; one process
+// per GPU) and a loopback group (TEST ONLY: G contexts in one process on one
+// device, each driven by its own host thread; host barrier + device copies),
+// which lets the EP/TP device path be parity-tested at G = 2..8 on one GPU.
+__global__ void moe_loopback_add_kernel(float* dst, const float* src, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] += src[i];
+}
+
+struct LoopbackGroup {
+    int world = 0;
+    std::mutex mu;
+    std::condition_variable cv;
+    int arrived = 0;
+    int64_t generation = 0;
+    std::vector<const void*> ptr;
+    void barrier() {
+        std::unique_lock<std::mutex> lk(mu);
+        const int64_t gen = generation;
+        if (++arrived == world) {
+            arrived = 0;
+            ++generation;
+            cv.notify_all();
+        } else {
+            cv.wait(lk, [&] { return generation != gen; });
+        }
+    }
+};
+struct LoopbackRank {
+    uint32_t magic = 0x4C4F4F50u;  // "LOOP"
+    LoopbackGroup* g = nullptr;
+    int rank = 0;
+};
+
+LoopbackRank* as_loopback(void* comm) {
+    LoopbackRank* r = static_cast<LoopbackRank*>(comm);
+    return (r && r->magic == 0x4C4F4F50u) ? r : nullptr;
+}
+
+moe_status lb_sync(moe_ctx* c, cudaStream_t st) {
+    CUDA_TRY(c, cudaStreamSynchronize(st));
+    return MOE_OK;
+}
+
+// all-to-all: peer p's block `rank` -> my block p (bytes per peer)
+moe_status comm_alltoall(moe_ctx* c, const void* send, void* recv, size_t count, int nccl_type, size_t esize,
+                         cudaStream_t st) {
+    if (LoopbackRank* lr = as_loopback(c->cfg.nccl_comm)) {
+        moe_status s;
+        if ((s = lb_sync(c, st))) return s;
+        LoopbackGroup* g = lr->g;
+        g->ptr[lr->rank] = send;
+        g->barrier();
+        const size_t b = count * esize;
+        for (int p = 0; p < g->world; ++p)
+            CUDA_TRY(c, cudaMemcpyAsync(static_cast<char*>(recv) + p * b,
+                                        static_cast<const char*>(g->ptr[p]) + lr->rank * b, b,
+                                        cudaMemcpyDeviceToDevice, st));
+        if ((s = lb_sync(c, st))) return s;
+        g->barrier();
+        return MOE_OK;
+    }
+    NCCL_TRY(c, g_nccl.AlltoAll(send, recv, count, nccl_type, c->cfg.nccl_comm, st));
+    return MOE_OK;
+}
+
+moe_status comm_reduce_scatter_f32(moe_ctx* c, const float* send, float* recv, size_t cnt, cudaStream_t st) {
+    if (LoopbackRank* lr = as_loopback(c->cfg.nccl_comm)) {
+        moe_status s;
+        if ((s = lb_sync(c, st))) return s;
+        LoopbackGroup* g = lr->g;
+        g->ptr[lr->rank] = send;
+        g->barrier();
+        for (int p = 0; p < g->world; ++p) {
+            const float* src = static_cast<const float*>(g->ptr[p]) + lr->rank * cnt;
+            if (p == 0) CUDA_TRY(c, cudaMemcpyAsync(recv, src, cnt * 4, cudaMemcpyDeviceToDevice, st));
+            else moe_loopback_add_kernel<<<c->num_sms, 256, 0, st>>>(recv, src, (int64_t)cnt);
+        }
+        if ((s = lb_sync(c, st))) return s;
+        g->barrier();
+        return MOE_OK;
+    }
+    NCCL_TRY(c, g_nccl.ReduceScatter(send, recv, cnt, ncclFloat32, ncclSum, c->cfg.nccl_comm, st));
+    return MOE_OK;
+}
+
+// in-place all-gather: my block lives at recv + rank*cnt
+moe_status comm_allgather_inplace(moe_ctx* c, void* recv, size_t cnt, int nccl_type, size_t esize, cudaStream_t st) {
+    const size_t b = cnt * esize;
+    if (LoopbackRank* lr = as_loopback(c->cfg.nccl_comm)) {
+        moe_status s;
+        if ((s = lb_sync(c, st))) return s;
+        LoopbackGroup* g = lr->g;
+        g->ptr[lr->rank] = recv;
+        g->barrier();
+        for (int p = 0; p < g->world; ++p)
+            if (p != lr->rank)
+                CUDA_TRY(c, cudaMemcpyAsync(static_cast<char*>(recv) + p * b,
+                                            static_cast<const char*>(g->ptr[p]) + p * b, b, cudaMemcpyDeviceToDevice,
+                                            st));
+        if ((s = lb_sync(c, st))) return s;
+        g->barrier();
+        return MOE_OK;
+    }
+    NCCL_TRY(c, g_nccl.AllGather(static_cast<char*>(recv) + c->rank * b, recv, cnt, nccl_type, c->cfg.nccl_comm, st));
+    return MOE_OK;
+}
+
 
 bool use_swap_path(const moe_ctx* c, int T) {
     if (c->cfg.flags & MOE_FLAG_FORCE_SWAP) return true;
@@ -398,6 +573,8 @@ moe_status check_ready(moe_ctx* c) {
 moe_status forward_impl(moe_ctx* c, const void* tokens, int32_t T, const void* router_w, const int32_t* in_idx,
                         const float* in_w, const moe_expert_weights* w, void* out, const moe_aux* aux,
                         cudaStream_t st);
+moe_status forward_ep(moe_ctx* c, const void* tokens, int32_t T, const void* router_w, void* out,
+                      const moe_aux* aux, cudaStream_t st);
 
 }  // namespace
 
@@ -457,7 +634,8 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
     derive_shape(cfg, c->G, c->E_local, c->e_lo, c->f_local, c->f_off);
     c->rank = cfg->rank;
     c->max_T = cfg->max_tokens;
-    c->nblk_max = (int)(((int64_t)c->max_T * (cfg->par == MOE_PAR_EP ? c->G : 1) + 1) / 2 + 1);
+    // router blocks of >= 2 rows; EP also routes the G*max_T*k receive slots
+    c->nblk_max = (int)(((int64_t)c->max_T * (cfg->par == MOE_PAR_EP ? c->G * c->k : 1) + 1) / 2 + 1);
 
     // EP: a rank may receive up to every token of every peer (dropless, reading R6).
     const int64_t rows_in = cfg->par == MOE_PAR_EP ? (int64_t)c->max_T * c->G : c->max_T;
@@ -474,6 +652,18 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
     };
     cudaError_t e;
     if ((e = cudaSetDevice(dev)) != cudaSuccess) return fail_init("cudaSetDevice", e);
+    if (LoopbackRank* lr = as_loopback(cfg->nccl_comm)) {
+        if (lr->rank != cfg->rank || lr->g->world != c->G) {
+            moe_destroy(c);
+            return fail(nullptr, MOE_ERR_INVALID, "loopback comm rank/world does not match cfg");
+        }
+    } else if (cfg->par != MOE_PAR_NONE && c->G > 1) {
+        std::string lerr;
+        if (!load_nccl(lerr)) {
+            moe_destroy(c);
+            return fail(nullptr, MOE_ERR_UNSUPPORTED, "%s", lerr.c_str());
+        }
+    }
 #define ALLOC(ptr, bytes)                                                               \
     if ((e = cudaMalloc(reinterpret_cast<void**>(&(ptr)), (bytes))) != cudaSuccess)     \
         return fail_init(#ptr, e);
@@ -502,8 +692,11 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
         ALLOC(c->ep_recv, sizeof(__nv_bfloat16) * slots * c->d);
         ALLOC(c->ep_ysend, sizeof(float) * slots * c->d);
         ALLOC(c->ep_yrecv, sizeof(float) * slots * c->d);
-        ALLOC(c->ep_meta_send, sizeof(int32_t) * slots * 4 + 64);
-        ALLOC(c->ep_meta_recv, sizeof(int32_t) * slots * 4 + 64);
+        ALLOC(c->ep_meta_send, sizeof(int32_t) * slots + 64);
+        ALLOC(c->ep_meta_recv, sizeof(int32_t) * slots + 64);
+        ALLOC(c->ep_ridx, sizeof(int32_t) * slots + 64);
+        ALLOC(c->ep_rpos, sizeof(int32_t) * slots + 64);
+        ALLOC(c->ep_rw, sizeof(float) * slots + 64);
     }
 #undef ALLOC
     if ((e = cudaMemset(c->done, 0, sizeof(unsigned int) * 4)) != cudaSuccess) return fail_init("memset", e);
@@ -541,7 +734,8 @@ moe_status moe_destroy(moe_ctx* c) {
     cudaSetDevice(c->device);
     void* bufs[] = {c->topk_idx, c->topk_w, c->pos, c->blockcount, c->blockoff, c->counts, c->offsets, c->done,
                     c->x_perm, c->h, c->y, c->stage_in, c->stage_out, c->tp_partial, c->tp_scatter, c->ep_send,
-                    c->ep_recv, c->ep_ysend, c->ep_yrecv, c->ep_meta_send, c->ep_meta_recv};
+                    c->ep_recv, c->ep_ysend, c->ep_yrecv, c->ep_meta_send, c->ep_meta_recv,
+                    c->ep_ridx, c->ep_rpos, c->ep_rw};
     for (void* b : bufs)
         if (b) cudaFree(b);
     for (auto& ev : c->pending) { cudaEventDestroy(ev.a); cudaEventDestroy(ev.b); }
@@ -667,6 +861,38 @@ moe_status moe_nccl_comm_init(const void* id128, int32_t world, int32_t rank, in
     return MOE_OK;
 }
 
+moe_status moe_loopback_comm_create(int32_t world, void** group) {
+    if (world < 1 || world > 64 || !group) return fail(nullptr, MOE_ERR_INVALID, "bad loopback world/group");
+    LoopbackGroup* g = new (std::nothrow) LoopbackGroup();
+    if (!g) return fail(nullptr, MOE_ERR_OOM, "host allocation failed");
+    g->world = world;
+    g->ptr.assign(world, nullptr);
+    *group = g;
+    return MOE_OK;
+}
+
+moe_status moe_loopback_comm_rank(void* group, int32_t rank, void** comm) {
+    LoopbackGroup* g = static_cast<LoopbackGroup*>(group);
+    if (!g || !comm || rank < 0 || rank >= g->world) return fail(nullptr, MOE_ERR_INVALID, "bad loopback rank");
+    LoopbackRank* r = new (std::nothrow) LoopbackRank();
+    if (!r) return fail(nullptr, MOE_ERR_OOM, "host allocation failed");
+    r->g = g;
+    r->rank = rank;
+    *comm = r;
+    return MOE_OK;
+}
+
+moe_status moe_loopback_comm_destroy(void* group_or_rank) {
+    if (!group_or_rank) return MOE_OK;
+    if (LoopbackRank* r = as_loopback(group_or_rank)) {
+        r->magic = 0;
+        delete r;
+    } else {
+        delete static_cast<LoopbackGroup*>(group_or_rank);
+    }
+    return MOE_OK;
+}
+
 moe_status moe_nccl_comm_destroy(void* comm) {
     if (!comm) return MOE_OK;
     std::string err;
@@ -689,29 +915,128 @@ moe_status forward_impl(moe_ctx* c, const void* tokens, int32_t T, const void* r
     if (T > 0 && (!tokens || !out || !aligned16(tokens) || !aligned16(out)))
         return fail(c, MOE_ERR_INVALID, "tokens / out must be 16-byte aligned device pointers");
     if (aux && aux->out_f32 && !aligned16(aux->out_f32)) return fail(c, MOE_ERR_INVALID, "aux.out_f32 misaligned");
-    if (c->cfg.par == MOE_PAR_EP) return fail(c, MOE_ERR_UNSUPPORTED, "EP forward not available in this build");
-    if (c->cfg.par == MOE_PAR_TP && c->G > 1) return fail(c, MOE_ERR_UNSUPPORTED, "TP forward not available in this build");
     moe_status s = ensure_weight_maps(c, w);
     if (s) return s;
-    if (T == 0) return MOE_OK;
+    if (c->cfg.par == MOE_PAR_EP) return forward_ep(c, tokens, T, router_w, out, aux, st);
+    if (T == 0) return MOE_OK;  // TP: every rank passes the same T, so all skip together
+
+    const bool tp = c->cfg.par == MOE_PAR_TP && c->G > 1;
+    RouteSpec r;
+    r.x = tokens; r.T = T; r.k = c->k;
+    r.router_w = router_w; r.in_idx = in_idx; r.in_w = in_w;
+    r.key_lo = c->e_lo; r.key_div = 1; r.nkeys = c->E_local; r.seg_align = kSegAlign;
+    r.logits = aux ? aux->logits : nullptr;
+    r.topk_idx = c->topk_idx; r.topk_w = c->topk_w;
+    r.pos = c->pos; r.pos_aux = aux ? aux->pos : nullptr;
+    r.dst_rows = c->x_perm;
+    if ((s = route_and_permute(c, r, st))) return s;
     const bool swap = use_swap_path(c, T);
     int splits = 1;
-    if (swap) {
-        // split-K partial buffers: splits x rows_needed rows must fit the y workspace
-        const int64_t rows_needed = round_up((int64_t)T * c->k + (int64_t)c->E_local * (kSegAlign - 1), kSegAlign);
-        splits = c->cfg.split_k ? c->cfg.split_k : c->max_splits;
-        splits = (int)std::max<int64_t>(1, std::min<int64_t>(splits, c->y_elems / (rows_needed * c->d)));
-        splits = std::min(splits, c->f_local / kBK);  // every split owns >= 1 K block
-        c->split_stride = rows_needed * c->d;
-    } else {
-        c->split_stride = 0;
-    }
-    s = run_local(c, tokens, T, router_w, in_idx, in_w, w, aux, swap, &splits, st);
-    if (s) return s;
+    if ((s = run_gemms(c, swap, T, (int64_t)T * c->k, &splits, st))) return s;
+    if ((s = copy_aux(c, aux, T, st)) || (s = copy_aux_segments(c, aux, st))) return s;
+
     CombineParams cp{};
     cp.y = c->y;
     cp.split_stride = c->split_stride;
     cp.splits = splits;
+    cp.pos = c->pos;
+    cp.topk_w = c->topk_w;
+    cp.T = T; cp.d = c->d; cp.k = c->k;
+    const bool residual = (c->cfg.flags & MOE_FLAG_RESIDUAL) != 0;
+    if (!tp) {
+        cp.x = residual ? static_cast<const __nv_bfloat16*>(tokens) : nullptr;
+        cp.out = static_cast<__nv_bfloat16*>(out);
+        cp.out_f32 = aux ? aux->out_f32 : nullptr;
+        return launch(c, kSlotCombine, moe_combine_kernel, dim3((c->d + 1023) / 1024, T), dim3(256), 0, st, cp);
+    }
+    // ---- TP: fp32 partial of this rank's ffn slice -> fp32 reduce-scatter ->
+    // one bf16 rounding (+ residual) -> bf16 all-gather (R7: single rounding)
+    cp.x = nullptr;
+    cp.out = nullptr;
+    cp.out_f32 = c->tp_partial;
+    if ((s = launch(c, kSlotCombine, moe_combine_kernel, dim3((c->d + 1023) / 1024, T), dim3(256), 0, st, cp)))
+        return s;
+    const int64_t n = (int64_t)T * c->d, cnt = n / c->G, base = cnt * c->rank;
+    ncclComm_t comm = c->cfg.nccl_comm;
+    StepTimer t1(c, kSlotExchange, st);
+    if ((s = comm_reduce_scatter_f32(c, c->tp_partial, c->tp_scatter, (size_t)cnt, st))) return s;
+    t1.done();
+    float* of32 = aux ? aux->out_f32 : nullptr;
+    const int blocks = (int)std::min<int64_t>(4 * c->num_sms, (cnt / 4 + 255) / 256 + 1);
+    if ((s = launch(c, kSlotCombine, moe_tp_finish_kernel, dim3(blocks), dim3(256), 0, st,
+                    static_cast<const float*>(c->tp_scatter), cnt, base,
+                    residual ? static_cast<const __nv_bfloat16*>(tokens) : nullptr, static_cast<__nv_bfloat16*>(out),
+                    of32)))
+        return s;
+    StepTimer t2(c, kSlotExchange, st);
+    const bool nccl = as_loopback(comm) == nullptr;
+    if (nccl) NCCL_TRY(c, g_nccl.GroupStart());
+    if ((s = comm_allgather_inplace(c, out, (size_t)cnt, ncclBfloat16, 2, st))) return s;
+    if (of32 && (s = comm_allgather_inplace(c, of32, (size_t)cnt, ncclFloat32, 4, st))) return s;
+    if (nccl) NCCL_TRY(c, g_nccl.GroupEnd());
+    t2.done();
+    return MOE_OK;
+}
+
+// ---- EP ("distributes experts of an MoE across GPUs"):
+// route local tokens over all E experts -> bucket rows by destination rank into
+// fixed-capacity send slots (dropless: cap = max_tokens*k per peer) -> NCCL
+// all-to-all (bf16 rows + local-expert ids, -1 = empty slot) -> group the received
+// rows by local expert (same K1/K2 machinery, k = 1) -> K3/K4 -> fp32 rows back to
+// their slots -> NCCL all-to-all -> K5 combine at the source rank.
+moe_status forward_ep(moe_ctx* c, const void* tokens, int32_t T, const void* router_w, void* out,
+                      const moe_aux* aux, cudaStream_t st) {
+    moe_status s;
+    const int G = c->G;
+    const int64_t cap = (int64_t)c->max_T * c->k;
+    const int64_t R = cap * G;
+    ncclComm_t comm = c->cfg.nccl_comm;
+    CUDA_TRY(c, cudaMemsetAsync(c->ep_meta_send, 0xFF, sizeof(int32_t) * R, st));  // all slots empty (-1)
+    if (T > 0) {
+        RouteSpec r;
+        r.x = tokens; r.T = T; r.k = c->k; r.router_w = router_w;
+        r.key_lo = 0; r.key_div = c->E_local; r.nkeys = G; r.seg_align = 1;
+        r.logits = aux ? aux->logits : nullptr;
+        r.topk_idx = c->topk_idx; r.topk_w = c->topk_w;
+        r.pos = c->pos; r.pos_aux = aux ? aux->pos : nullptr;
+        r.dst_rows = c->ep_send; r.cap = (int)cap; r.meta = c->ep_meta_send;
+        if ((s = route_and_permute(c, r, st))) return s;
+        if ((s = copy_aux(c, aux, T, st))) return s;
+    }
+    StepTimer t1(c, kSlotDispatch, st);
+    const bool nccl = as_loopback(comm) == nullptr;
+    if (nccl) NCCL_TRY(c, g_nccl.GroupStart());
+    if ((s = comm_alltoall(c, c->ep_meta_send, c->ep_meta_recv, (size_t)cap, ncclInt32, 4, st))) return s;
+    if ((s = comm_alltoall(c, c->ep_send, c->ep_recv, (size_t)(cap * c->d), ncclBfloat16, 2, st))) return s;
+    if (nccl) NCCL_TRY(c, g_nccl.GroupEnd());
+    t1.done();
+    // receive side: R slots (peer-major), k = 1, expert = meta (local index, -1 empty)
+    RouteSpec r2;
+    r2.x = c->ep_recv; r2.T = (int)R; r2.k = 1;
+    r2.in_idx = c->ep_meta_recv; r2.in_w = nullptr; r2.allow_neg = 1;
+    r2.key_lo = 0; r2.key_div = 1; r2.nkeys = c->E_local; r2.seg_align = kSegAlign;
+    r2.topk_idx = c->ep_ridx; r2.topk_w = c->ep_rw; r2.pos = c->ep_rpos;
+    r2.dst_rows = c->x_perm;
+    if ((s = route_and_permute(c, r2, st))) return s;
+    if ((s = copy_aux_segments(c, aux, st))) return s;
+    // expected rows per rank ~ T*k (balanced routing); an expert gets at most G*max_T rows
+    const bool swap = (c->cfg.flags & MOE_FLAG_FORCE_SWAP) ? true
+                    : (c->cfg.flags & MOE_FLAG_FORCE_TILED) ? false
+                    : (int64_t)T * c->k <= 2 * c->swap_max_T;
+    int splits = 1;
+    if ((s = run_gemms(c, swap, std::min<int64_t>(R, (int64_t)G * c->max_T), R, &splits, st))) return s;
+    if ((s = launch(c, kSlotExchange, moe_ep_gather_kernel, dim3((c->d + 1023) / 1024, (unsigned)R), dim3(256), 0,
+                    st, static_cast<const float*>(c->y), c->split_stride, splits,
+                    static_cast<const int32_t*>(c->ep_rpos), (int)R, c->d, c->ep_ysend)))
+        return s;
+    StepTimer t2(c, kSlotExchange, st);
+    if ((s = comm_alltoall(c, c->ep_ysend, c->ep_yrecv, (size_t)(cap * c->d), ncclFloat32, 4, st))) return s;
+    t2.done();
+    if (T == 0) return MOE_OK;
+    CombineParams cp{};
+    cp.y = c->ep_yrecv;
+    cp.split_stride = 0;
+    cp.splits = 1;
     cp.pos = c->pos;
     cp.topk_w = c->topk_w;
     cp.x = (c->cfg.flags & MOE_FLAG_RESIDUAL) ? static_cast<const __nv_bfloat16*>(tokens) : nullptr;
