@@ -6,10 +6,13 @@ f=14336, E=8, top-2, bf16), 64-token decode batch, 1 B200. A "step" is one full
 pass of the hot path (router, permute, w1/w3+SwiGLU, w2, combine) over one batch.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config decode|prefill]
-                  [--impl ours|reference]
+                  [--impl ours|reference] [--par ep|tp|none]
 
-N>1 is launched by torchrun (one process per GPU); the single-GPU variant then
-runs as N independent replicas.
+N>1 is launched by torchrun (one process per GPU). The default multi-GPU variant
+is expert parallel (BASELINE.json configs[3]): the global batch (64 decode tokens
+or 32k prefill tokens) is sharded across the N ranks, each rank owns E/N experts,
+rows travel by NCCL all-to-all; `--par tp` runs the ffn-sharded variant
+(configs[4] shape, one layer). Both are strong scaling of a fixed global batch.
 
 Timing: CUDA events on the launch stream, W warm-up steps, barrier + synchronize
 on both sides of exactly K steps, max over ranks. The expert weights (2.8 GB)
@@ -35,6 +38,24 @@ CONFIGS = {
 }
 
 
+METRIC = "MoE-block tokens/sec (Mixtral-8x7B shape, 64-req decode) + % HBM / tensor-pipe peak"
+
+
+def workload_config(args, world):
+    """The `config` object both arms print (same workload, same keys)."""
+    Tg, d, f, E, k, ci = CONFIGS[args.config]
+    par = args.par or ("ep" if world > 1 else "none")
+    T = Tg // world if par == "ep" else Tg
+    return par, T, {
+        "workload": f"BASELINE.json configs[{3 if world > 1 else ci}]: Mixtral-8x7B single MoE layer, "
+                    f"{'64-request decode' if args.config == 'decode' else '32k-token prefill'}, "
+                    f"global batch T={Tg}, d={d}, f={f}, E={E}, top-{k}, bf16",
+        "global_tokens": Tg, "tokens_per_gpu": T,
+        "parallelism": {"none": "single" if world == 1 else f"replicas{world}", "ep": f"ep{world}",
+                        "tp": f"tp{world}"}[par],
+        "l2": "weights (2.8 GB) > L2 (126 MB): streamed from HBM every step, no flush"}
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -44,6 +65,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--par", default=None, choices=["ep", "tp", "none"],
+                    help="multi-GPU variant (default: ep when N > 1)")
     return ap.parse_args()
 
 
@@ -121,9 +144,11 @@ def dist_setup(args):
 
 
 def algorithmic(T, d, f, E, k, counts):
-    """SURVEY.md Sec. 8(d) work formulas for one forward, from the actual routing."""
+    """SURVEY.md Sec. 8(d) work formulas for one forward on one rank, from the actual
+    routing: T = tokens routed on this rank, f = ffn columns held by this rank,
+    counts = rows of each LOCAL expert (their sum = A assignments computed here)."""
     touched = int(sum(1 for c in counts if c > 0))
-    A = T * k
+    A = int(sum(counts))
     b_w13 = touched * 2 * f * d * 2                 # w1+w3 of touched experts (bf16)
     b_w2 = touched * d * f * 2
     bytes_total = b_w13 + b_w2 + E * d * 2 + 2 * T * d * 2
@@ -178,14 +203,18 @@ def run_reference(args):
             break
     dt = float(np.median(times))
     val = sample / dt
-    line = {"impl": "reference", "metric": "MoE-block tokens/sec (Mixtral-8x7B shape, 64-req decode)",
-            "value": val, "unit": "tokens/s", "n_gpus": args.gpus, "steps": len(times), "warmup": args.warmup,
-            "ms_per_step": dt * 1000, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"BASELINE.json configs[{ci}]: Mixtral-8x7B MoE layer, T={T}, d={d}, f={f}, "
-                                   f"E={E}, top-{k}", "sample_tokens_per_step": sample},
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    par, _, cfg = workload_config(args, world)
+    line = {"impl": "reference", "metric": METRIC,
+            "value": val, "unit": "tokens/s", "n_gpus": world, "steps": len(times), "warmup": args.warmup,
+            "ms_per_step": dt * 1000, "higher_is_better": True,
+            "scaling": "strong" if par in ("ep", "tp") else "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (same seeded workload; the oracle processes a bounded token sample "
+                                    "of it per step)",
+            "config": cfg,
             "cpu_baseline": {"value": val, "unit": "tokens/s", "cores": min(ncores, sample), "kind": "oracle",
-                             "sample": f"{sample} of {T} tokens per step"},
+                             "sample": f"{sample} of {T} tokens of the batch per step, full Mixtral layer weights, "
+                                       f"fp64 C++ (OpenMP over tokens), median of {len(times)} steps"},
             "e2e": {"value": val, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -201,16 +230,29 @@ def main():
     world, rank, local = dist_setup(args)
     import paper_2408_00008_b200 as moe
 
-    T, d, f, E, k, ci = CONFIGS[args.config]
+    Tg, d, f, E, k, ci = CONFIGS[args.config]
     dev = torch.device("cuda", local)
+    par = args.par or ("ep" if world > 1 else "none")
+    pmap = {"none": moe.MOE_PAR_NONE, "ep": moe.MOE_PAR_EP, "tp": moe.MOE_PAR_TP}
+    comm = None
+    if par != "none":
+        comm = moe.nccl_comm_from_process_group(world, rank, local) if world > 1 else \
+            moe.moe_nccl_comm_init(moe.moe_nccl_unique_id(), 1, 0, local)
+    # EP: the global batch is sharded across ranks (strong scaling of the batch);
+    # TP / single GPU: every rank processes the whole batch.
+    T = Tg // world if par == "ep" else Tg
     w = synth.make_weights(d, f, E, seed=args.seed, device=dev)
     nbuf = 4  # distinct token batches cycled through the steps
-    xs = [synth.make_tokens(T, d, seed=args.seed + 1 + i, layer=rank, device=dev) for i in range(nbuf)]
-    blk = moe.MoEBlock(w["wg"], w["w1"], w["w3"], w["w2"], top_k=k, max_tokens=T)
+    xs = [synth.make_tokens(Tg, d, seed=args.seed + 1 + i, device=dev)[rank * T:(rank + 1) * T] if par == "ep"
+          else synth.make_tokens(Tg, d, seed=args.seed + 1 + i, device=dev) for i in range(nbuf)]
+    blk = moe.MoEBlock(w["wg"], w["w1"], w["w3"], w["w2"], top_k=k, max_tokens=T, par=pmap[par],
+                       world_size=world if par != "none" else 1, rank=rank if par != "none" else 0, nccl_comm=comm)
     del w["w1"], w["w3"], w["w2"]
     torch.cuda.empty_cache()
     out = torch.empty(T, d, dtype=torch.bfloat16, device=dev)
-    counts = torch.empty(E, dtype=torch.int32, device=dev)
+    E_local = E // world if par == "ep" else E
+    f_local = f // world if par == "tp" else f
+    counts = torch.empty(E_local, dtype=torch.int32, device=dev)
     stream = torch.cuda.current_stream()
 
     def step(i, aux=None):
@@ -287,7 +329,7 @@ def main():
     aux = {"expert_counts": counts}
     step(0, aux)
     torch.cuda.synchronize()
-    alg = algorithmic(T, d, f, E, k, counts.cpu().tolist())
+    alg = algorithmic(T, d, f_local, E, k, counts.cpu().tolist())
     peaks = load_peaks()
     per = {name: (v[0] / v[1] if v[1] else 0.0) for name, v in ktimes.items()}
     decode = args.config == "decode"
@@ -306,18 +348,16 @@ def main():
                 "traffic": None, "kernel": "moe_gemm_kernel<kG1Tiled> (w1/w3 + SwiGLU)",
                 "peak_src": peaks["src"] + " (MEASURED_PEAKS.json bf16_tflops_sustained)"}
         step_frac = alg["flops"] / (ms * 1e-3) / 1e12 / pk
-    tok_s = T * world / (ms * 1e-3)
+    tok_s = Tg / (ms * 1e-3) if par in ("ep", "tp") else T * world / (ms * 1e-3)
     kernel_share = {n: round(per[n] / ms_prof, 4) for n in per if ktimes[n][1]}
 
     line = {
-        "metric": "MoE-block tokens/sec (Mixtral-8x7B shape, 64-req decode) + % HBM / tensor-pipe peak",
+        "metric": METRIC,
         "value": tok_s, "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": max(3, args.warmup),
-        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong" if par in ("ep", "tp") else "weak", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (seeded Gaussian tokens, random-init Mixtral-shaped weights; DESIGN.md input recipe)",
-        "config": {"workload": f"BASELINE.json configs[{ci}]: Mixtral-8x7B single MoE layer, T={T} tokens/GPU, "
-                               f"d={d}, f={f}, E={E}, top-{k}, bf16",
-                   "tokens_per_gpu": T, "parallelism": "replicas" if world > 1 else "single",
-                   "l2": "weights (2.8 GB) > L2 (126 MB): streamed from HBM every step, no flush"},
+        "config": workload_config(args, world)[2],
         "roofline": roof,
         "step_roofline_frac": step_frac,
         "kernel_ms": {n: round(per[n], 5) for n in per if ktimes[n][1]},
@@ -325,7 +365,8 @@ def main():
         "ms_per_step_profiled": ms_prof,
         "gpu_launches": launches,
         "clocks": clk,
-        "e2e": {"value": T * world / (ms_e2e * 1e-3), "unit": "tokens/s", "ms_per_step": ms_e2e,
+        "e2e": {"value": (Tg if par in ("ep", "tp") else T * world) / (ms_e2e * 1e-3), "unit": "tokens/s",
+                "ms_per_step": ms_e2e,
                 "h2d_bytes_per_step": T * d * 2, "d2h_bytes_per_step": T * d * 2,
                 "api": "moe_forward_host (pinned host tokens -> device -> host output)"},
     }
@@ -337,6 +378,8 @@ def main():
     if rank == 0:
         print(json.dumps(line), flush=True)
     blk.close()
+    if comm is not None:
+        moe.moe_nccl_comm_destroy(comm)
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
