@@ -81,6 +81,7 @@ typedef enum {
 #define MOE_FLAG_FORCE_SWAP  0x2u /* always use the decode (weights-as-M, swap-AB) GEMMs */
 #define MOE_FLAG_FORCE_TILED 0x4u /* always use the prefill (tokens-as-M) GEMMs          */
 #define MOE_FLAG_NO_PDL      0x8u /* disable programmatic dependent launch               */
+#define MOE_FLAG_NO_PAIR     0x10u /* prefill GEMMs on single CTAs (M=128) instead of CTA pairs (M=256) */
 
 typedef struct {
     int32_t hidden;      /* d: 4096 for Mixtral (C1: 64). Must be a multiple of 64.   */

@@ -28,7 +28,7 @@ _lib = ctypes.CDLL(LIB_PATH)
 
 MOE_OK, MOE_ERR_INVALID, MOE_ERR_UNSUPPORTED, MOE_ERR_OOM, MOE_ERR_CUDA, MOE_ERR_NCCL, MOE_ERR_STATE = range(7)
 MOE_PAR_NONE, MOE_PAR_EP, MOE_PAR_TP = 0, 1, 2
-MOE_FLAG_RESIDUAL, MOE_FLAG_FORCE_SWAP, MOE_FLAG_FORCE_TILED, MOE_FLAG_NO_PDL = 0x1, 0x2, 0x4, 0x8
+MOE_FLAG_RESIDUAL, MOE_FLAG_FORCE_SWAP, MOE_FLAG_FORCE_TILED, MOE_FLAG_NO_PDL, MOE_FLAG_NO_PAIR = 0x1, 0x2, 0x4, 0x8, 0x10
 NUM_KERNEL_SLOTS = 8
 KERNEL_SLOTS = ("router", "permute", "gemm1_w13_swiglu", "gemm2_w2", "combine", "dispatch", "exchange", "pack")
 

@@ -28,7 +28,7 @@
 
 namespace moe {
 
-enum GemmKind : int { kG1Tiled = 0, kG2Tiled = 1, kG1Swap = 2, kG2Swap = 3 };
+enum GemmKind : int { kG1Tiled = 0, kG2Tiled = 1, kG1Swap = 2, kG2Swap = 3, kG1Pair = 4, kG2Pair = 5 };
 
 struct GemmParams {
     const int32_t* counts;   // [E] rows per local expert (device, from the permute step)
@@ -367,6 +367,229 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     if (warp == 1) {
         ptx::tc_fence_after();
         ptx::tmem_dealloc(tmem_base, 2 * C::kAccCols);
+    }
+}
+
+// ============================================================================
+// CTA-pair (cta_group::2) variant of the prefill GEMMs: a cluster of 2 CTAs on
+// one TPC computes a 256-token x 256-column tile with tcgen05.mma.cta_group::2
+// (M = 256). CTA r stages token rows [128r, 128r+128) of the tile (A half) and
+// weight rows [r*N/2, (r+1)*N/2) (B half); each CTA's TMEM receives its 128 token
+// rows x all N columns, so the epilogue is the single-CTA one. Compared with the
+// 1-CTA M=128 x N=256 tile, each SM reads half of B from its own shared memory
+// per MMA (the pair shares operands), halving the smem and L2 traffic per FLOP.
+// Roles: warp 0 = TMA producer in both CTAs (completing bytes on the LEADER's
+// full barrier), warp 1 of the leader = MMA issuer (commits multicast to both
+// CTAs' empty / tmem_full barriers), warps 2..5 of both CTAs = epilogue (arrive
+// on the leader's tmem_empty barrier; 8 arrivals per accumulator).
+constexpr int kPairStageBytes = 2 * 128 * 128;  // A half 16 KB + B half 16 KB
+constexpr int kPairStages = (kSmemBudget - 2048) / kPairStageBytes > 8 ? 8 : (kSmemBudget - 2048) / kPairStageBytes;
+constexpr int kPairSmemBytes = kPairStages * kPairStageBytes + 2048;
+
+template <int KIND>
+__device__ __forceinline__ int pair_tiles_of(int n_e, const GemmParams& p) {
+    if (n_e <= 0) return 0;
+    const int mt = (n_e + 255) / 256;
+    return KIND == kG1Pair ? mt * (p.f / 128) : mt * ((p.d + 255) / 256);
+}
+
+template <int KIND>
+__device__ __forceinline__ void pair_decode(int t, const GemmParams& p, const int32_t* s_counts,
+                                            const int32_t* s_offsets, TileInfo& ti) {
+    int e = 0;
+    for (; e < p.E; ++e) {
+        const int n = pair_tiles_of<KIND>(s_counts[e], p);
+        if (t < n) break;
+        t -= n;
+    }
+    ti.e = e;
+    ti.seg = s_offsets[e];
+    ti.rows = s_counts[e];
+    const int mt = (ti.rows + 255) / 256;
+    ti.m_idx = t % mt;   // tokens fastest (weight tile shared through L2)
+    ti.n_idx = t / mt;
+    ti.kb0 = 0;
+    ti.nkb = (KIND == kG1Pair ? p.d : p.f) / kBK;
+    ti.split = 0;
+    ti.n_valid = 0;
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    moe_gemm_pair_kernel(const GemmParams p, const __grid_constant__ CUtensorMap tmA,
+                         const __grid_constant__ CUtensorMap tmB) {
+    constexpr int S = kPairStages;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* smem_a = smem;
+    uint8_t* smem_b = smem + S * 16384;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * kPairStageBytes);
+    uint64_t* full = bars;
+    uint64_t* empty = bars + S;
+    uint64_t* tmem_full = bars + 2 * S;
+    uint64_t* tmem_empty = bars + 2 * S + 2;
+    uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 4);
+    int32_t* s_counts = reinterpret_cast<int32_t*>(bars + 2 * S + 5);
+    int32_t* s_offsets = s_counts + 32;
+
+    const int warp = threadIdx.x / 32;
+    const int lane = threadIdx.x % 32;
+    const uint32_t crank = ptx::cluster_ctarank();
+    const bool leader = crank == 0;
+
+    if (warp == 0 && lane == 0) {
+        ptx::prefetch_tmap(&tmA);
+        ptx::prefetch_tmap(&tmB);
+        for (int i = 0; i < S; ++i) {
+            ptx::mbar_init(&full[i], 1);
+            ptx::mbar_init(&empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            ptx::mbar_init(&tmem_full[i], 1);
+            ptx::mbar_init(&tmem_empty[i], 8);
+        }
+        ptx::fence_mbar_init();
+    }
+    if (warp == 1) {
+        ptx::tmem_alloc_pair(tmem_base_slot, 512);
+        ptx::tmem_relinquish_pair();
+    }
+    ptx::pdl_wait();
+    if (threadIdx.x < 32) {
+        for (int e = threadIdx.x; e < p.E; e += 32) {
+            s_counts[e] = p.counts[e];
+            s_offsets[e] = p.offsets[e];
+        }
+    }
+    ptx::tc_fence_before();
+    ptx::cluster_sync();  // barriers of both CTAs initialised, TMEM allocated
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = *tmem_base_slot;
+
+    int total = 0;
+    for (int e = 0; e < p.E; ++e) total += pair_tiles_of<KIND>(s_counts[e], p);
+    const int cid = blockIdx.x / 2, ncl = gridDim.x / 2;
+
+    if (warp == 0) {
+        // ---------------------------------------------------------------- TMA producer (both CTAs)
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int t = cid; t < total; t += ncl) {
+                TileInfo ti;
+                pair_decode<KIND>(t, p, s_counts, s_offsets, ti);
+                const int n_mma = KIND == kG1Pair ? 256 : min(256, p.d - ti.n_idx * 256);
+                const int a_row = ti.seg + ti.m_idx * 256 + (int)crank * 128;
+                const int b_row = ti.n_idx * 256 + (int)crank * (n_mma / 2);
+                for (int kb = 0; kb < ti.nkb; ++kb) {
+                    ptx::mbar_wait(&empty[stage], phase ^ 1);
+                    const uint32_t fb = ptx::map_cluster(&full[stage], 0);
+                    if (leader) ptx::mbar_arrive_expect_tx(&full[stage], 2 * kPairStageBytes);
+                    const int kc = kb * kBK;
+                    ptx::tma_load_2d_pair(&tmA, fb, smem_a + stage * 16384, kc, a_row, ptx::kEvictLast);
+                    ptx::tma_load_3d_pair(&tmB, fb, smem_b + stage * 16384, kc, b_row, ti.e, ptx::kEvictNormal);
+                    if (++stage == S) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------------------------------------------------------- MMA issuer (leader CTA)
+        if (leader && lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            for (int t = cid; t < total; t += ncl) {
+                TileInfo ti;
+                pair_decode<KIND>(t, p, s_counts, s_offsets, ti);
+                const uint32_t n_mma = KIND == kG1Pair ? 256u : (uint32_t)min(256, p.d - ti.n_idx * 256);
+                const uint32_t idesc = ptx::make_idesc_bf16(256, n_mma);
+                const uint32_t d_tmem = tmem_base + acc * 256;
+                ptx::mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
+                ptx::tc_fence_after();
+                for (int kb = 0; kb < ti.nkb; ++kb) {
+                    ptx::mbar_wait(&full[stage], phase);
+                    ptx::tc_fence_after();
+                    const uint64_t adesc = ptx::make_smem_desc_sw128(ptx::smem_u32(smem_a + stage * 16384));
+                    const uint64_t bdesc = ptx::make_smem_desc_sw128(ptx::smem_u32(smem_b + stage * 16384));
+#pragma unroll
+                    for (int kk = 0; kk < kBK / 16; ++kk)
+                        ptx::mma_bf16_pair(d_tmem, adesc + 2 * kk, bdesc + 2 * kk, idesc, (kb | kk) ? 1u : 0u);
+                    ptx::mma_commit_pair(&empty[stage], 0x3);
+                    if (++stage == S) { stage = 0; phase ^= 1; }
+                }
+                ptx::mma_commit_pair(&tmem_full[acc], 0x3);
+                if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+            }
+        }
+    } else {
+        // ---------------------------------------------------------------- epilogue (warps 2..5, both CTAs)
+        const int q = warp & 3;
+        const int r = q * 32 + lane;
+        const uint32_t leader_empty0 = ptx::map_cluster(&tmem_empty[0], 0);
+        const uint32_t leader_empty1 = ptx::map_cluster(&tmem_empty[1], 0);
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int t = cid; t < total; t += ncl) {
+            TileInfo ti;
+            pair_decode<KIND>(t, p, s_counts, s_offsets, ti);
+            ptx::mbar_wait(&tmem_full[acc], acc_phase);
+            ptx::tc_fence_after();
+            const uint32_t tbase = tmem_base + acc * 256 + (static_cast<uint32_t>(q * 32) << 16);
+            const int mrow = ti.m_idx * 256 + (int)crank * 128 + r;  // row within the expert segment
+            const bool valid = mrow < ti.rows;
+            if (KIND == kG1Pair) {
+                __nv_bfloat16* h = static_cast<__nv_bfloat16*>(p.out) + static_cast<int64_t>(ti.seg + mrow) * p.f +
+                                   ti.n_idx * 128;
+#pragma unroll 1
+                for (int c = 0; c < 8; ++c) {
+                    uint32_t a[16], b[16];
+                    ptx::tmem_ld16(tbase + c * 16, a);
+                    ptx::tmem_ld16(tbase + 128 + c * 16, b);
+                    ptx::tmem_wait_ld();
+                    uint32_t o[8];
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        float h0 = silu_f32(__uint_as_float(a[2 * i])) * __uint_as_float(b[2 * i]);
+                        float h1 = silu_f32(__uint_as_float(a[2 * i + 1])) * __uint_as_float(b[2 * i + 1]);
+                        o[i] = pack_bf16x2(h0, h1);
+                    }
+                    if (valid) {
+                        uint4* dst = reinterpret_cast<uint4*>(h + c * 16);
+                        dst[0] = make_uint4(o[0], o[1], o[2], o[3]);
+                        dst[1] = make_uint4(o[4], o[5], o[6], o[7]);
+                    }
+                }
+            } else {
+                const int ncols = min(256, p.d - ti.n_idx * 256);
+                float* y = static_cast<float*>(p.out) + static_cast<int64_t>(ti.seg + mrow) * p.d + ti.n_idx * 256;
+#pragma unroll 1
+                for (int c = 0; c < ncols / 16; ++c) {
+                    uint32_t v[16];
+                    ptx::tmem_ld16(tbase + c * 16, v);
+                    ptx::tmem_wait_ld();
+                    if (valid) {
+                        float4* dst = reinterpret_cast<float4*>(y + c * 16);
+#pragma unroll
+                        for (int i = 0; i < 4; ++i)
+                            dst[i] = make_float4(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]),
+                                                 __uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3]));
+                    }
+                }
+            }
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive_cluster(acc == 0 ? leader_empty0 : leader_empty1);
+            if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        }
+    }
+    ptx::pdl_launch_dependents();
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::cluster_sync();  // the peer's epilogue may still read TMEM columns the pair shares
+    if (warp == 1) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc_pair(tmem_base, 512);
     }
 }
 

@@ -164,7 +164,7 @@ struct moe_ctx {
     // weight descriptor cache (keyed by pointer)
     const void* w13_key = nullptr;
     const void* w2_key = nullptr;
-    CUtensorMap tm_w13{}, tm_w2_tiled{}, tm_w2_swap{};
+    CUtensorMap tm_w13{}, tm_w13_pair{}, tm_w2_tiled{}, tm_w2_swap{};
     // instrumentation
     bool profiling = false;
     struct Ev { int slot; cudaEvent_t a, b; };
@@ -243,10 +243,50 @@ moe_status launch(moe_ctx* c, int slot, void (*kern)(KArgs...), dim3 grid, dim3 
     return MOE_OK;
 }
 
+template <int KIND>
+moe_status set_pair_attr(moe_ctx* c) {
+    CUDA_TRY(c, cudaFuncSetAttribute(moe_gemm_pair_kernel<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     kPairSmemBytes));
+    return MOE_OK;
+}
+
 template <int KIND, int NB>
 moe_status set_gemm_attr(moe_ctx* c) {
     CUDA_TRY(c, cudaFuncSetAttribute(moe_gemm_kernel<KIND, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      GemmCfg<KIND, NB>::kSmemBytes));
+    return MOE_OK;
+}
+
+template <int KIND>
+moe_status launch_gemm_pair(moe_ctx* c, int slot, const GemmParams& p, const CUtensorMap& a, const CUtensorMap& b,
+                            int nclusters, cudaStream_t st) {
+    cudaEvent_t ea = nullptr, eb = nullptr;
+    if (c->profiling) {
+        ea = take_event(c);
+        eb = take_event(c);
+        cudaEventRecord(ea, st);
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(2 * nclusters);
+    cfg.blockDim = dim3(kGemmThreads);
+    cfg.dynamicSmemBytes = kPairSmemBytes;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = (c->cfg.flags & MOE_FLAG_NO_PDL) ? 0 : 1;
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = 2;
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 2;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, moe_gemm_pair_kernel<KIND>, p, a, b);
+    if (e != cudaSuccess) return fail(c, MOE_ERR_CUDA, "pair kernel launch (slot %d) failed: %s", slot, cudaGetErrorString(e));
+    c->launch_count++;
+    if (c->profiling) {
+        cudaEventRecord(eb, st);
+        c->pending.push_back({slot, ea, eb});
+    }
     return MOE_OK;
 }
 
@@ -295,7 +335,8 @@ void derive_shape(const moe_config* cfg, int& G, int& E_local, int& e_lo, int& f
 
 moe_status ensure_weight_maps(moe_ctx* c, const moe_expert_weights* w) {
     if (w->w13 != c->w13_key) {
-        if (!encode_map(&c->tm_w13, w->w13, 3, c->d, 2 * (uint64_t)c->f_local, c->E_local, 256))
+        if (!encode_map(&c->tm_w13, w->w13, 3, c->d, 2 * (uint64_t)c->f_local, c->E_local, 256) ||
+            !encode_map(&c->tm_w13_pair, w->w13, 3, c->d, 2 * (uint64_t)c->f_local, c->E_local, 128))
             return fail(c, MOE_ERR_CUDA, "cuTensorMapEncodeTiled(w13) failed");
         c->w13_key = w->w13;
     }
@@ -394,6 +435,16 @@ moe_status run_gemms(moe_ctx* c, bool swap, int64_t rows_bound, int64_t rows_tot
         else if (nbw == 64) s = run_swap<64>(c, 1, nullptr, splits, st);
         else s = run_swap<128>(c, 2, nullptr, splits, st);
         if (s) return s;
+    } else if (!(c->cfg.flags & MOE_FLAG_NO_PAIR)) {
+        // CTA-pair (cta_group::2) 256x256 tiles, one cluster of 2 CTAs per TPC
+        const int64_t mt_max = rows_total / 256 + c->E_local;
+        const int ncl = c->num_sms / 2;
+        const int g1 = (int)std::min<int64_t>(ncl, mt_max * (c->f_local / 128));
+        const int g2 = (int)std::min<int64_t>(ncl, mt_max * ((c->d + 255) / 256));
+        GemmParams p1{c->counts, c->offsets, c->E_local, c->d, c->f_local, 1, c->h, 0};
+        if ((s = launch_gemm_pair<kG1Pair>(c, kSlotGemm1, p1, c->tm_x_tiled, c->tm_w13_pair, g1, st))) return s;
+        GemmParams p2{c->counts, c->offsets, c->E_local, c->d, c->f_local, 1, c->y, 0};
+        if ((s = launch_gemm_pair<kG2Pair>(c, kSlotGemm2, p2, c->tm_h_tiled, c->tm_w2_swap, g2, st))) return s;
     } else {
         const int64_t mt_max = rows_total / 128 + c->E_local;
         const int g1 = (int)std::min<int64_t>(c->num_sms, mt_max * (c->f_local / 128));
@@ -718,7 +769,8 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
     if ((as = set_gemm_attr<kG1Tiled, 256>(c)) || (as = set_gemm_attr<kG2Tiled, 256>(c)) ||
         (as = set_gemm_attr<kG1Swap, 32>(c)) || (as = set_gemm_attr<kG2Swap, 32>(c)) ||
         (as = set_gemm_attr<kG1Swap, 64>(c)) || (as = set_gemm_attr<kG2Swap, 64>(c)) ||
-        (as = set_gemm_attr<kG1Swap, 128>(c)) || (as = set_gemm_attr<kG2Swap, 128>(c))) {
+        (as = set_gemm_attr<kG1Swap, 128>(c)) || (as = set_gemm_attr<kG2Swap, 128>(c)) ||
+        (as = set_pair_attr<kG1Pair>(c)) || (as = set_pair_attr<kG2Pair>(c))) {
         std::string m = c->err;
         moe_destroy(c);
         g_init_error = m;

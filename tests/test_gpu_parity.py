@@ -38,7 +38,7 @@ def _inputs(shape, seed, device="cuda"):
     return synth.make_inputs(shape, seed, device=device)
 
 
-MODES = {"auto": 0, "swap": 0x2, "tiled": 0x4}
+MODES = {"auto": 0, "swap": 0x2, "tiled": 0x4, "tiled1cta": 0x4 | 0x10}
 
 
 # ---------------------------------------------------------------- worked example
@@ -97,7 +97,7 @@ def test_ragged_shapes(moe, T, d, f, E, k, mode):
     blk.close()
 
 
-@pytest.mark.parametrize("mode", ["swap", "tiled"])
+@pytest.mark.parametrize("mode", ["swap", "tiled", "tiled1cta"])
 def test_multi_tile_mid_size(moe, mode):
     """Several M/N/K tiles per expert plus ragged tails (d=512, f=1024, E=8, T=1000)."""
     shape = synth.MoEShape(T=1000, d=512, f=1024, E=8, k=2)
