@@ -39,6 +39,8 @@ struct GemmParams {
     int32_t splits;          // K splits (kG2Swap only; 1 otherwise)
     void* out;               // kG1*: h bf16 [Cap, f];  kG2*: y fp32 [splits][Cap, d]
     int64_t out_split_stride;// elements between split buffers (kG2Swap)
+    int32_t raster;          // pair kernels: 0 = token tiles fastest, 1 = weight tiles fastest
+    uint64_t hint_a, hint_b; // pair kernels: L2 cache-policy operands of the A / B TMA loads
 };
 
 constexpr int kGemmThreads = 192;
@@ -406,8 +408,14 @@ __device__ __forceinline__ void pair_decode(int t, const GemmParams& p, const in
     ti.seg = s_offsets[e];
     ti.rows = s_counts[e];
     const int mt = (ti.rows + 255) / 256;
-    ti.m_idx = t % mt;   // tokens fastest (weight tile shared through L2)
-    ti.n_idx = t / mt;
+    const int nt = KIND == kG1Pair ? p.f / 128 : (p.d + 255) / 256;
+    if (p.raster == 0) {  // tokens fastest: a weight tile is shared through L2 by the clusters of one wave
+        ti.m_idx = t % mt;
+        ti.n_idx = t / mt;
+    } else {              // weights fastest: a token tile is shared through L2
+        ti.n_idx = t % nt;
+        ti.m_idx = t / nt;
+    }
     ti.kb0 = 0;
     ti.nkb = (KIND == kG1Pair ? p.d : p.f) / kBK;
     ti.split = 0;
@@ -486,8 +494,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                     const uint32_t fb = ptx::map_cluster(&full[stage], 0);
                     if (leader) ptx::mbar_arrive_expect_tx(&full[stage], 2 * kPairStageBytes);
                     const int kc = kb * kBK;
-                    ptx::tma_load_2d_pair(&tmA, fb, smem_a + stage * 16384, kc, a_row, ptx::kEvictLast);
-                    ptx::tma_load_3d_pair(&tmB, fb, smem_b + stage * 16384, kc, b_row, ti.e, ptx::kEvictNormal);
+                    ptx::tma_load_2d_pair(&tmA, fb, smem_a + stage * 16384, kc, a_row, p.hint_a);
+                    ptx::tma_load_3d_pair(&tmB, fb, smem_b + stage * 16384, kc, b_row, ti.e, p.hint_b);
                     if (++stage == S) { stage = 0; phase ^= 1; }
                 }
             }

@@ -37,6 +37,7 @@ struct RouteParams {
     float* logits;            // [T, E] optional debug output
     int32_t* topk_idx;        // [T, k] workspace
     float* topk_w;            // [T, k] workspace
+    int32_t* rank;            // [T, k] stable rank of each assignment among same-key ones of its block
     int32_t* blockcount;      // [nblk, nkeys]
     int32_t* blockoff;        // [nblk, nkeys]
     int32_t* counts;          // [nkeys]
@@ -60,7 +61,114 @@ __device__ __forceinline__ void bf16x8_to_f32(const uint4& v, float (&f)[8]) {
     }
 }
 
-// K1: router (a2, a3) + per-block histogram (a4) + last-block exclusive scan (a5).
+// a4 + a5 for one router block whose routing sits in s_idx[ntok][2] (shared):
+//   rank[t][j]      = #{(t', j') < (t, j) in this block with the same key} (stable order)
+//   blockcount[b][] = assignments of this block per key
+// then the last block to finish runs the exclusive scan over blocks (one block,
+// fixed order: deterministic; classic threadfence-reduction handshake):
+//   blockoff[b][key], counts[key], offsets[key] (segments padded to seg_align).
+template <int NTHREADS>
+__device__ __forceinline__ void route_block_finish(const RouteParams& p, const int32_t (*s_idx)[2], int ntok,
+                                                   int tok0) {
+    constexpr int NW = NTHREADS / 32;
+    __shared__ int s_last;
+    __shared__ int32_t s_wk[NW][32];    // per-warp assignment count of every key
+    __shared__ int32_t s_tot[32];
+    __shared__ int32_t s_base[NW][32];  // scan: per-warp partial sums of every key
+    const int NK = p.nkeys;
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    // thread i <-> assignment i = (token i / k, slot i % k); NTHREADS >= TB * k
+    const int i = threadIdx.x;
+    const bool valid = i < ntok * p.k;
+    int key = -1;
+    if (valid) {
+        const int e = s_idx[i / p.k][i % p.k];
+        if (p.k > 1 && (i % p.k) == 1 && e >= 0 && e == s_idx[i / p.k][0]) __trap();  // duplicate expert
+        key = e >= 0 ? hist_key(e, p.key_lo, p.key_div, NK) : -1;
+    }
+    const uint32_t lt = (1u << lane) - 1u;
+    int32_t lrank = 0;
+    for (int e = 0; e < NK; ++e) {
+        const uint32_t m = __ballot_sync(0xffffffffu, key == e);
+        if (key == e) lrank = __popc(m & lt);
+        if (lane == 0) s_wk[warp][e] = __popc(m);
+    }
+    __syncthreads();
+    if (key >= 0) {
+        int32_t r = lrank;
+        for (int w = 0; w < warp; ++w) r += s_wk[w][key];
+        p.rank[(int64_t)tok0 * p.k + i] = r;
+    } else if (valid) {
+        p.rank[(int64_t)tok0 * p.k + i] = 0;
+    }
+    if (threadIdx.x < NK) {
+        int32_t cnt = 0;
+        for (int w = 0; w < NW; ++w) cnt += s_wk[w][threadIdx.x];
+        p.blockcount[(int64_t)blockIdx.x * NK + threadIdx.x] = cnt;
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = (atomicAdd(p.done, 1u) == gridDim.x - 1);
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    // Exclusive scan over blocks for every key. Thread t owns the contiguous run of
+    // blocks [t*per, (t+1)*per): pass 1 sums the run for all keys (independent
+    // loads, in flight together), a block-wide scan in shared memory gives each
+    // run's base, pass 2 writes the per-block offsets. Fixed order: deterministic.
+    const int nblk = gridDim.x;
+    const int per = (nblk + NTHREADS - 1) / NTHREADS;
+    const int b0 = min(nblk, threadIdx.x * per), b1 = min(nblk, b0 + per);
+    int32_t sum[32];
+#pragma unroll
+    for (int e = 0; e < 32; ++e) sum[e] = 0;
+    for (int bb = b0; bb < b1; ++bb)
+#pragma unroll
+        for (int e = 0; e < 32; ++e)
+            if (e < NK) sum[e] += __ldcg(&p.blockcount[(int64_t)bb * NK + e]);
+    int32_t excl[32];
+#pragma unroll
+    for (int e = 0; e < 32; ++e) {
+        if (e >= NK) break;
+        int32_t inc = sum[e];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int32_t u = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += u;
+        }
+        excl[e] = inc - sum[e];
+        if (lane == 31) s_base[warp][e] = inc;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < 32; ++e) {
+        if (e >= NK) break;
+        int32_t base = 0;
+        for (int w = 0; w < warp; ++w) base += s_base[w][e];
+        excl[e] += base;
+        if (threadIdx.x == NTHREADS - 1) s_tot[e] = excl[e] + sum[e];
+    }
+    for (int bb = b0; bb < b1; ++bb)
+#pragma unroll
+        for (int e = 0; e < 32; ++e)
+            if (e < NK) {
+                p.blockoff[(int64_t)bb * NK + e] = excl[e];
+                excl[e] += __ldcg(&p.blockcount[(int64_t)bb * NK + e]);
+            }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int32_t off = 0;
+        p.offsets[0] = 0;
+        for (int e = 0; e < NK; ++e) {
+            p.counts[e] = s_tot[e];
+            off += (s_tot[e] + p.seg_align - 1) / p.seg_align * p.seg_align;
+            p.offsets[e + 1] = off;
+        }
+        *p.done = 0u;  // ready for the next forward (kernel boundary orders it)
+    }
+}
+
+// K1: router (a2, a3) + histogram / ranks (a4) + last-block exclusive scan (a5).
 // A block owns TB consecutive tokens; its 128 threads split the hidden dimension
 // in 8-element (16-byte) chunks, each thread accumulating TB x E partial dot
 // products in fp32 (bf16*bf16 products are exact in fp32). W_g chunks are loaded
@@ -70,12 +178,9 @@ template <int E_MAX, int TB>
 __global__ void __launch_bounds__(kRouteThreads) moe_router_kernel(const RouteParams p) {
     __shared__ float s_part[4][TB][E_MAX];
     __shared__ int32_t s_idx[TB][2];
-    __shared__ int s_last;
-    __shared__ int32_t s_tot[32];
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int tok0 = blockIdx.x * TB;
     const int ntok = min(TB, p.T - tok0);
-    const int NK = p.nkeys;
 
     ptx::pdl_wait();
 
@@ -101,17 +206,17 @@ __global__ void __launch_bounds__(kRouteThreads) moe_router_kernel(const RoutePa
 #pragma unroll
             for (int e = 0; e < E_MAX; ++e)
                 wr[e] = __ldg(reinterpret_cast<const uint4*>(p.wg + (int64_t)min(e, p.E - 1) * p.d) + ci);
+            float xv[TB][8];
 #pragma unroll
-            for (int t = 0; t < TB; ++t) {
-                float xv[8];
-                bf16x8_to_f32(xr[t], xv);
+            for (int t = 0; t < TB; ++t) bf16x8_to_f32(xr[t], xv[t]);
 #pragma unroll
-                for (int e = 0; e < E_MAX; ++e) {
-                    float w[8];
-                    bf16x8_to_f32(wr[e], w);
+            for (int e = 0; e < E_MAX; ++e) {
+                float w[8];
+                bf16x8_to_f32(wr[e], w);
 #pragma unroll
-                    for (int i = 0; i < 8; ++i) acc[t][e] = fmaf(xv[i], w[i], acc[t][e]);
-                }
+                for (int t = 0; t < TB; ++t)
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) acc[t][e] = fmaf(xv[t][i], w[i], acc[t][e]);
             }
         }
 #pragma unroll
@@ -179,55 +284,126 @@ __global__ void __launch_bounds__(kRouteThreads) moe_router_kernel(const RoutePa
         }
     }
     __syncthreads();
+    route_block_finish<kRouteThreads>(p, s_idx, ntok, tok0);
+}
 
-    // ---- a4: per-block histogram over the keys (local experts / destination ranks)
-    if (threadIdx.x < NK) {
-        int32_t cnt = 0;
-        for (int tb = 0; tb < ntok; ++tb) {
-            const int e0 = s_idx[tb][0], e1 = p.k > 1 ? s_idx[tb][1] : -1;
-            if (p.k > 1 && e0 == e1 && e0 >= 0) __trap();  // duplicate expert in a routing
-            cnt += (e0 >= 0 && hist_key(e0, p.key_lo, p.key_div, NK) == (int)threadIdx.x) ? 1 : 0;
-            cnt += (e1 >= 0 && hist_key(e1, p.key_lo, p.key_div, NK) == (int)threadIdx.x) ? 1 : 0;
-        }
-        p.blockcount[(int64_t)blockIdx.x * NK + threadIdx.x] = cnt;
-    }
 
-    // ---- a5: the last block to finish runs the exclusive scan (one block, fixed
-    // order: deterministic). Classic threadfence-reduction handshake.
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) s_last = (atomicAdd(p.done, 1u) == gridDim.x - 1);
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    const int nblk = gridDim.x;
-    for (int e = warp; e < NK; e += kRouteThreads / 32) {
-        int32_t running = 0;
-        for (int base = 0; base < nblk; base += 32) {
-            const int b = base + lane;
-            const int32_t v = b < nblk ? __ldcg(&p.blockcount[(int64_t)b * NK + e]) : 0;
-            int32_t inc = v;
+// K1 on the legacy tensor-core path (mma.sync m16n8k16, bf16 in, fp32 accumulate)
+// for E <= 8: the router GEMM has N = E = 8, exactly one n8 fragment. Each warp
+// owns 16 tokens x a 1/KS slice of K. A lane loads 16 contiguous bytes (8 bf16)
+// of each of its two token rows and of its expert's W_g row at the same k, and
+// feeds them as the fragments of two MMAs: the k order inside the MMA is a
+// permutation applied identically to A and B, which leaves the dot products
+// unchanged. Products of bf16 are exact in fp32; accumulation is fp32 (R5).
+// Tokens per block = 16 * (8 / KS): KS = 8 splits K over all 8 warps (decode:
+// many short warps), KS = 1 gives each warp its own 16 tokens (prefill).
+__device__ __forceinline__ void mma_bf16_16816(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                               uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+template <int KS>
+__global__ void __launch_bounds__(256) moe_router_mma_kernel(const RouteParams p) {
+    constexpr int TOK = 16 * (8 / KS);
+    __shared__ float s_log[8 / KS][KS][16][8];
+    __shared__ int32_t s_idx[TOK][2];
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int tok0 = blockIdx.x * TOK;
+    const int ntok = min(TOK, p.T - tok0);
+    const int g = warp / KS, kp = warp % KS;
+    const int gid = lane >> 2, q = lane & 3;
+
+    ptx::pdl_wait();
+
+    const int r0 = min(tok0 + g * 16 + gid, p.T - 1), r1 = min(tok0 + g * 16 + gid + 8, p.T - 1);
+    const uint4* xa = reinterpret_cast<const uint4*>(p.x + (int64_t)r0 * p.d);
+    const uint4* xb = reinterpret_cast<const uint4*>(p.x + (int64_t)r1 * p.d);
+    const bool has_e = gid < p.E;
+    const uint4* wr = reinterpret_cast<const uint4*>(p.wg + (int64_t)min(gid, p.E - 1) * p.d);
+    const int ksl = p.d / KS;                  // K slice of this warp (multiple of 32: d % 256 == 0 or KS small)
+    const int cb = (kp * ksl) / 8, ce = ((kp + 1) * ksl) / 8;  // 16-byte chunks of this warp's K slice
+    float c[4] = {0.f, 0.f, 0.f, 0.f};
+    // warp-uniform trip count (mma.sync is .aligned); lanes past the slice feed zeros.
+    // Software-pipelined by hand: DEPTH iterations of loads are issued before their
+    // MMAs, so each lane keeps 3*DEPTH 16-byte loads in flight (HBM-bound at prefill,
+    // latency-bound at decode).
+    constexpr int DEPTH = 8;
+    for (int g0 = cb; g0 < ce; g0 += 4 * DEPTH) {
+        uint4 a[DEPTH], b[DEPTH], w[DEPTH];
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int32_t u = __shfl_up_sync(0xffffffffu, inc, o);
-                if (lane >= o) inc += u;
+        for (int u = 0; u < DEPTH; ++u) {
+            const int ci = g0 + 4 * u + q;
+            a[u] = make_uint4(0u, 0u, 0u, 0u);
+            b[u] = a[u];
+            w[u] = a[u];
+            if (ci < ce) {
+                a[u] = __ldg(xa + ci);
+                b[u] = __ldg(xb + ci);
+                if (has_e) w[u] = __ldg(wr + ci);
             }
-            if (b < nblk) p.blockoff[(int64_t)b * NK + e] = running + inc - v;
-            running += __shfl_sync(0xffffffffu, inc, 31);
         }
-        if (lane == 0) s_tot[e] = running;
+#pragma unroll
+        for (int u = 0; u < DEPTH; ++u) {
+            mma_bf16_16816(c, a[u].x, b[u].x, a[u].y, b[u].y, w[u].x, w[u].y);
+            mma_bf16_16816(c, a[u].z, b[u].z, a[u].w, b[u].w, w[u].z, w[u].w);
+        }
+    }
+    // c0,c1: token row gid, experts 2q, 2q+1; c2,c3: row gid+8
+    s_log[g][kp][gid][2 * q] = c[0];
+    s_log[g][kp][gid][2 * q + 1] = c[1];
+    s_log[g][kp][gid + 8][2 * q] = c[2];
+    s_log[g][kp][gid + 8][2 * q + 1] = c[3];
+    __syncthreads();
+    if (threadIdx.x < ntok) {
+        const int tb = threadIdx.x, t = tok0 + tb;
+        const int gg = tb / 16, rr = tb % 16;
+        float l[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            float v = s_log[gg][0][rr][e];
+#pragma unroll
+            for (int s2 = 1; s2 < KS; ++s2) v += s_log[gg][s2][rr][e];  // fixed order over K slices
+            l[e] = v;
+        }
+        if (p.logits) {
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+                if (e < p.E) p.logits[(int64_t)t * p.E + e] = l[e];
+        }
+        int i0 = 0;
+        float b0 = l[0];
+#pragma unroll
+        for (int e = 1; e < 8; ++e)
+            if (e < p.E && l[e] > b0) { b0 = l[e]; i0 = e; }
+        int i1 = -1;
+        float b1 = 0.f;
+        if (p.k > 1) {
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+                if (e < p.E && e != i0 && (i1 < 0 || l[e] > b1)) { b1 = l[e]; i1 = e; }
+        }
+        float w0 = 1.f, w1 = 0.f;
+        if (p.k > 1) {
+            const float e1 = expf(b1 - b0);
+            const float den = 1.f + e1;
+            w0 = 1.f / den;
+            w1 = e1 / den;
+        }
+        p.topk_idx[(int64_t)t * p.k] = i0;
+        p.topk_w[(int64_t)t * p.k] = w0;
+        if (p.k > 1) {
+            p.topk_idx[(int64_t)t * p.k + 1] = i1;
+            p.topk_w[(int64_t)t * p.k + 1] = w1;
+        }
+        s_idx[tb][0] = i0;
+        s_idx[tb][1] = i1;
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        int32_t off = 0;
-        p.offsets[0] = 0;
-        for (int e = 0; e < NK; ++e) {
-            p.counts[e] = s_tot[e];
-            off += (s_tot[e] + p.seg_align - 1) / p.seg_align * p.seg_align;
-            p.offsets[e + 1] = off;
-        }
-        *p.done = 0u;  // ready for the next forward (kernel boundary orders it)
-    }
+    route_block_finish<256>(p, s_idx, ntok, tok0);
 }
 
 struct PermuteParams {
@@ -241,7 +417,7 @@ struct PermuteParams {
     int32_t* meta;            // EP dispatch mode: [nkeys * cap] local expert id at the destination
     int32_t TB;               // router block size (tokens)
     int32_t PT;               // tokens per permute block (1, 2, 4 or 8)
-    int32_t* pos;             // [T, k] permuted row per assignment (-1: not local)
+    int32_t* pos;             // [T, k] in: in-block rank (router); out: permuted row (-1: not local)
     int32_t* pos_aux;         // optional copy for the caller
     __nv_bfloat16* x_perm;    // [Cap, d]
 };
@@ -264,15 +440,7 @@ __global__ void __launch_bounds__(kPermuteThreads) moe_permute_kernel(const Perm
             int32_t ps = -1;
             if (e >= 0) {
                 const int b = t / p.TB;
-                int32_t rank = 0;
-                // stable order = (token, slot): count earlier assignments with the same key.
-                // (A token may put both its rows in one EP destination bucket.)
-                for (int t2 = b * p.TB; t2 <= t; ++t2)
-                    for (int j2 = 0; j2 < (t2 == t ? j : p.k); ++j2) {
-                        const int e2 = p.topk_idx[(int64_t)t2 * p.k + j2];
-                        rank += (e2 >= 0 && hist_key(e2, p.key_lo, p.key_div, p.nkeys) == e);
-                    }
-                const int32_t r = p.blockoff[(int64_t)b * p.nkeys + e] + rank;
+                const int32_t r = p.blockoff[(int64_t)b * p.nkeys + e] + p.pos[(int64_t)t * p.k + j];
                 if (p.cap > 0) {  // EP dispatch: bucket of destination rank e
                     ps = e * p.cap + r;
                     p.meta[ps] = ex - e * p.key_div;  // expert index local to the destination
@@ -326,36 +494,50 @@ struct CombineParams {
 
 // K5 (a9): out[t] = bf16_rne( sum_j w_j * (sum_s y_s[pos_j]) (+ x[t]) ), fixed order:
 // splits ascending, then r = w_0*s_0, r = fma(w_1, s_1, r), then + x.
-// grid = (ceil(d/1024), T): each thread owns 4 consecutive columns of one token.
+// grid = (ceil(d/4096), T): each thread owns 4 float4 column groups of one token
+// (strided by 1024 columns), so 8 independent 16-byte loads per thread are in flight.
+constexpr int kCombineVec = 4;
 __global__ void __launch_bounds__(256) moe_combine_kernel(const CombineParams p) {
     const int t = blockIdx.y;
-    const int c = blockIdx.x * 1024 + threadIdx.x * 4;
+    const int c0 = blockIdx.x * 1024 * kCombineVec + threadIdx.x * 4;
     ptx::pdl_wait();
-    if (c < p.d) {
-        int32_t pr[2];
-        float w[2];
+    int32_t pr[2];
+    float w[2];
 #pragma unroll
-        for (int j = 0; j < 2; ++j) {
-            pr[j] = j < p.k ? p.pos[(int64_t)t * p.k + j] : -1;
-            w[j] = j < p.k ? p.topk_w[(int64_t)t * p.k + j] : 0.f;
+    for (int j = 0; j < 2; ++j) {
+        pr[j] = j < p.k ? p.pos[(int64_t)t * p.k + j] : -1;
+        w[j] = j < p.k ? p.topk_w[(int64_t)t * p.k + j] : 0.f;
+    }
+    float4 s[2][kCombineVec];
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int v = 0; v < kCombineVec; ++v) {
+            const int c = c0 + v * 1024;
+            s[j][v] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (pr[j] >= 0 && c < p.d) s[j][v] = __ldcs(reinterpret_cast<const float4*>(p.y + (int64_t)pr[j] * p.d + c));
         }
-        float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int sp = 1; sp < p.splits; ++sp)
 #pragma unroll
-        for (int j = 0; j < 2; ++j) {
-            if (pr[j] < 0) continue;
-            const float* yr = p.y + (int64_t)pr[j] * p.d + c;
-            float4 s = __ldcs(reinterpret_cast<const float4*>(yr));
-#pragma unroll 8
-            for (int sp = 1; sp < p.splits; ++sp) {
-                const float4 u = __ldcs(reinterpret_cast<const float4*>(yr + sp * p.split_stride));
-                s.x += u.x; s.y += u.y; s.z += u.z; s.w += u.w;
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int v = 0; v < kCombineVec; ++v) {
+                const int c = c0 + v * 1024;
+                if (pr[j] >= 0 && c < p.d) {
+                    const float4 u = __ldcs(reinterpret_cast<const float4*>(p.y + sp * p.split_stride +
+                                                                            (int64_t)pr[j] * p.d + c));
+                    s[j][v].x += u.x; s[j][v].y += u.y; s[j][v].z += u.z; s[j][v].w += u.w;
+                }
             }
-            if (j == 0) {
-                r = make_float4(w[0] * s.x, w[0] * s.y, w[0] * s.z, w[0] * s.w);
-            } else {
-                r.x = fmaf(w[j], s.x, r.x); r.y = fmaf(w[j], s.y, r.y);
-                r.z = fmaf(w[j], s.z, r.z); r.w = fmaf(w[j], s.w, r.w);
-            }
+#pragma unroll
+    for (int v = 0; v < kCombineVec; ++v) {
+        const int c = c0 + v * 1024;
+        if (c >= p.d) break;
+        float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (pr[0] >= 0) r = make_float4(w[0] * s[0][v].x, w[0] * s[0][v].y, w[0] * s[0][v].z, w[0] * s[0][v].w);
+        if (pr[1] >= 0) {
+            r.x = fmaf(w[1], s[1][v].x, r.x); r.y = fmaf(w[1], s[1][v].y, r.y);
+            r.z = fmaf(w[1], s[1][v].z, r.z); r.w = fmaf(w[1], s[1][v].w, r.w);
         }
         if (p.x) {
             const __nv_bfloat162* xs = reinterpret_cast<const __nv_bfloat162*>(p.x + (int64_t)t * p.d + c);
@@ -363,12 +545,13 @@ __global__ void __launch_bounds__(256) moe_combine_kernel(const CombineParams p)
             r.x += a.x; r.y += a.y; r.z += b.x; r.w += b.y;
         }
         if (p.out_f32) __stcs(reinterpret_cast<float4*>(p.out_f32 + (int64_t)t * p.d + c), r);
-        if (p.out == nullptr) return;
-        __nv_bfloat162 o0 = __floats2bfloat162_rn(r.x, r.y), o1 = __floats2bfloat162_rn(r.z, r.w);
-        uint2 ov;
-        ov.x = *reinterpret_cast<uint32_t*>(&o0);
-        ov.y = *reinterpret_cast<uint32_t*>(&o1);
-        *reinterpret_cast<uint2*>(p.out + (int64_t)t * p.d + c) = ov;
+        if (p.out) {
+            __nv_bfloat162 o0 = __floats2bfloat162_rn(r.x, r.y), o1 = __floats2bfloat162_rn(r.z, r.w);
+            uint2 ov;
+            ov.x = *reinterpret_cast<uint32_t*>(&o0);
+            ov.y = *reinterpret_cast<uint32_t*>(&o1);
+            *reinterpret_cast<uint2*>(p.out + (int64_t)t * p.d + c) = ov;
+        }
     }
     ptx::pdl_launch_dependents();
 }

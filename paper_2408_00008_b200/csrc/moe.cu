@@ -141,6 +141,7 @@ struct moe_ctx {
     int swap_max_T = 128;     // swap path chosen when T <= this (and not forced)
     int max_splits = 4;
     int64_t split_stride = 0; // elements between split-K partial buffers of this forward
+    int pair_tune = 0;        // bits: 0 G1 raster, 1 G2 raster, 2-3 G1 A hint, 4-5 G1 B hint, 6-7 G2 A, 8-9 G2 B
     // workspace (device)
     int32_t *topk_idx = nullptr, *pos = nullptr, *blockcount = nullptr, *blockoff = nullptr;
     int32_t *counts = nullptr, *offsets = nullptr;
@@ -379,9 +380,13 @@ struct RouteSpec {
 };
 
 moe_status route_and_permute(moe_ctx* c, const RouteSpec& r, cudaStream_t st) {
-    // router block size: 2 tokens (many blocks, low latency) for small batches,
-    // 8 tokens (W_g chunks reused from registers) for large E<=8 batches
-    const int TB = (r.in_idx == nullptr && c->E <= 8 && r.T >= 2048) ? 8 : 2;
+    // Router variant: E <= 8 -> tensor-core router (mma.sync, N = E = 8); 16 tokens
+    // per block with K split over 8 warps for small batches (latency), 128 tokens
+    // per block for large ones (throughput). Routed mode / E > 8 -> CUDA-core
+    // router, 2 tokens per block.
+    const bool mma = r.in_idx == nullptr && c->E <= 8;
+    const int KS = r.T >= 2048 ? 1 : 8;
+    const int TB = mma ? 16 * (8 / KS) : 2;
     const int nblk = (r.T + TB - 1) / TB;
     RouteParams rp{};
     rp.x = static_cast<const __nv_bfloat16*>(r.x);
@@ -393,14 +398,16 @@ moe_status route_and_permute(moe_ctx* c, const RouteSpec& r, cudaStream_t st) {
     rp.allow_neg = r.allow_neg;
     rp.logits = r.logits;
     rp.topk_idx = r.topk_idx; rp.topk_w = r.topk_w;
+    rp.rank = r.pos;
     rp.blockcount = c->blockcount; rp.blockoff = c->blockoff;
     rp.counts = c->counts; rp.offsets = c->offsets; rp.done = c->done;
     moe_status s;
-    const dim3 rg(nblk), rb(kRouteThreads);
-    if (TB == 8) s = launch(c, kSlotRouter, moe_router_kernel<8, 8>, rg, rb, 0, st, rp);
-    else if (c->E <= 8) s = launch(c, kSlotRouter, moe_router_kernel<8, 2>, rg, rb, 0, st, rp);
-    else if (c->E <= 16) s = launch(c, kSlotRouter, moe_router_kernel<16, 2>, rg, rb, 0, st, rp);
-    else s = launch(c, kSlotRouter, moe_router_kernel<32, 2>, rg, rb, 0, st, rp);
+    const dim3 rg(nblk);
+    if (mma && KS == 1) s = launch(c, kSlotRouter, moe_router_mma_kernel<1>, rg, dim3(256), 0, st, rp);
+    else if (mma) s = launch(c, kSlotRouter, moe_router_mma_kernel<8>, rg, dim3(256), 0, st, rp);
+    else if (c->E <= 8) s = launch(c, kSlotRouter, moe_router_kernel<8, 2>, rg, dim3(kRouteThreads), 0, st, rp);
+    else if (c->E <= 16) s = launch(c, kSlotRouter, moe_router_kernel<16, 2>, rg, dim3(kRouteThreads), 0, st, rp);
+    else s = launch(c, kSlotRouter, moe_router_kernel<32, 2>, rg, dim3(kRouteThreads), 0, st, rp);
     if (s) return s;
 
     PermuteParams pp{};
@@ -441,9 +448,13 @@ moe_status run_gemms(moe_ctx* c, bool swap, int64_t rows_bound, int64_t rows_tot
         const int ncl = c->num_sms / 2;
         const int g1 = (int)std::min<int64_t>(ncl, mt_max * (c->f_local / 128));
         const int g2 = (int)std::min<int64_t>(ncl, mt_max * ((c->d + 255) / 256));
-        GemmParams p1{c->counts, c->offsets, c->E_local, c->d, c->f_local, 1, c->h, 0};
+        const uint64_t hints[3] = {ptx::kEvictNormal, ptx::kEvictFirst, ptx::kEvictLast};
+        const int tune = c->pair_tune;  // raster/hint selection (env MOE_PAIR_TUNE, for experiments)
+        GemmParams p1{c->counts, c->offsets, c->E_local, c->d, c->f_local, 1, c->h, 0, (tune >> 0) & 1,
+                      hints[((tune >> 2) & 3) % 3], hints[((tune >> 4) & 3) % 3]};
         if ((s = launch_gemm_pair<kG1Pair>(c, kSlotGemm1, p1, c->tm_x_tiled, c->tm_w13_pair, g1, st))) return s;
-        GemmParams p2{c->counts, c->offsets, c->E_local, c->d, c->f_local, 1, c->y, 0};
+        GemmParams p2{c->counts, c->offsets, c->E_local, c->d, c->f_local, 1, c->y, 0, (tune >> 1) & 1,
+                      hints[((tune >> 6) & 3) % 3], hints[((tune >> 8) & 3) % 3]};
         if ((s = launch_gemm_pair<kG2Pair>(c, kSlotGemm2, p2, c->tm_h_tiled, c->tm_w2_swap, g2, st))) return s;
     } else {
         const int64_t mt_max = rows_total / 128 + c->E_local;
@@ -685,6 +696,7 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
     derive_shape(cfg, c->G, c->E_local, c->e_lo, c->f_local, c->f_off);
     c->rank = cfg->rank;
     c->max_T = cfg->max_tokens;
+    if (const char* pt = getenv("MOE_PAIR_TUNE")) c->pair_tune = atoi(pt);
     // router blocks of >= 2 rows; EP also routes the G*max_T*k receive slots
     c->nblk_max = (int)(((int64_t)c->max_T * (cfg->par == MOE_PAR_EP ? c->G * c->k : 1) + 1) / 2 + 1);
 
@@ -999,14 +1011,14 @@ moe_status forward_impl(moe_ctx* c, const void* tokens, int32_t T, const void* r
         cp.x = residual ? static_cast<const __nv_bfloat16*>(tokens) : nullptr;
         cp.out = static_cast<__nv_bfloat16*>(out);
         cp.out_f32 = aux ? aux->out_f32 : nullptr;
-        return launch(c, kSlotCombine, moe_combine_kernel, dim3((c->d + 1023) / 1024, T), dim3(256), 0, st, cp);
+        return launch(c, kSlotCombine, moe_combine_kernel, dim3((c->d + 4095) / 4096, T), dim3(256), 0, st, cp);
     }
     // ---- TP: fp32 partial of this rank's ffn slice -> fp32 reduce-scatter ->
     // one bf16 rounding (+ residual) -> bf16 all-gather (R7: single rounding)
     cp.x = nullptr;
     cp.out = nullptr;
     cp.out_f32 = c->tp_partial;
-    if ((s = launch(c, kSlotCombine, moe_combine_kernel, dim3((c->d + 1023) / 1024, T), dim3(256), 0, st, cp)))
+    if ((s = launch(c, kSlotCombine, moe_combine_kernel, dim3((c->d + 4095) / 4096, T), dim3(256), 0, st, cp)))
         return s;
     const int64_t n = (int64_t)T * c->d, cnt = n / c->G, base = cnt * c->rank;
     ncclComm_t comm = c->cfg.nccl_comm;
@@ -1095,7 +1107,7 @@ moe_status forward_ep(moe_ctx* c, const void* tokens, int32_t T, const void* rou
     cp.T = T; cp.d = c->d; cp.k = c->k;
     cp.out = static_cast<__nv_bfloat16*>(out);
     cp.out_f32 = aux ? aux->out_f32 : nullptr;
-    return launch(c, kSlotCombine, moe_combine_kernel, dim3((c->d + 1023) / 1024, T), dim3(256), 0, st, cp);
+    return launch(c, kSlotCombine, moe_combine_kernel, dim3((c->d + 4095) / 4096, T), dim3(256), 0, st, cp);
 }
 
 }  // namespace
