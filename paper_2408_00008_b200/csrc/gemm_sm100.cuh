@@ -39,7 +39,8 @@ struct GemmParams {
     int32_t splits;          // K splits (kG2Swap only; 1 otherwise)
     void* out;               // kG1*: h bf16 [Cap, f];  kG2*: y fp32 [splits][Cap, d]
     int64_t out_split_stride;// elements between split buffers (kG2Swap)
-    int32_t raster;          // pair kernels: 0 = token tiles fastest, 1 = weight tiles fastest
+    int32_t raster;          // pair kernels: tile order, see pair_decode
+    int32_t band;            // pair kernels: band width (tiles) of the banded orders
     uint64_t hint_a, hint_b; // pair kernels: L2 cache-policy operands of the A / B TMA loads
 };
 
@@ -409,12 +410,30 @@ __device__ __forceinline__ void pair_decode(int t, const GemmParams& p, const in
     ti.rows = s_counts[e];
     const int mt = (ti.rows + 255) / 256;
     const int nt = KIND == kG1Pair ? p.f / 128 : (p.d + 255) / 256;
-    if (p.raster == 0) {  // tokens fastest: a weight tile is shared through L2 by the clusters of one wave
+    // Tile orders (the ~74 clusters of one wave work on consecutive tiles):
+    //   0: token tiles fastest        1: weight tiles fastest
+    //   2: bands of `band` token tiles; inside a band token tiles fastest -- the
+    //      band's token rows stay L2-resident while the expert's weights stream once
+    //      per band (GEMM1: weights are 3.7x the expert's tokens)
+    //   3: bands of `band` weight tiles; inside a band weight tiles fastest -- the
+    //      band's weight rows stay L2-resident while the activations stream once per
+    //      band (GEMM2: the expert's activations are 2x its weights)
+    if (p.raster == 0) {
         ti.m_idx = t % mt;
         ti.n_idx = t / mt;
-    } else {              // weights fastest: a token tile is shared through L2
+    } else if (p.raster == 1) {
         ti.n_idx = t % nt;
         ti.m_idx = t / nt;
+    } else if (p.raster == 2) {
+        const int bw = p.band, b = t / (bw * nt), r = t % (bw * nt);
+        const int w = min(bw, mt - b * bw);
+        ti.m_idx = b * bw + r % w;
+        ti.n_idx = r / w;
+    } else {
+        const int bw = p.band, b = t / (bw * mt), r = t % (bw * mt);
+        const int w = min(bw, nt - b * bw);
+        ti.n_idx = b * bw + r % w;
+        ti.m_idx = r / w;
     }
     ti.kb0 = 0;
     ti.nkb = (KIND == kG1Pair ? p.d : p.f) / kBK;

@@ -141,7 +141,8 @@ struct moe_ctx {
     int swap_max_T = 128;     // swap path chosen when T <= this (and not forced)
     int max_splits = 4;
     int64_t split_stride = 0; // elements between split-K partial buffers of this forward
-    int pair_tune = 0;        // bits: 0 G1 raster, 1 G2 raster, 2-3 G1 A hint, 4-5 G1 B hint, 6-7 G2 A, 8-9 G2 B
+    int pair_tune = 0;        // experiment override of the prefill tile orders (env MOE_PAIR_TUNE)
+    int g1_raster = 2, g1_band = 16, g2_raster = 1, g2_band = 1;  // prefill tile orders (pair_decode; ncu DRAM sweep r01)
     // workspace (device)
     int32_t *topk_idx = nullptr, *pos = nullptr, *blockcount = nullptr, *blockoff = nullptr;
     int32_t *counts = nullptr, *offsets = nullptr;
@@ -448,13 +449,18 @@ moe_status run_gemms(moe_ctx* c, bool swap, int64_t rows_bound, int64_t rows_tot
         const int ncl = c->num_sms / 2;
         const int g1 = (int)std::min<int64_t>(ncl, mt_max * (c->f_local / 128));
         const int g2 = (int)std::min<int64_t>(ncl, mt_max * ((c->d + 255) / 256));
-        const uint64_t hints[3] = {ptx::kEvictNormal, ptx::kEvictFirst, ptx::kEvictLast};
-        const int tune = c->pair_tune;  // raster/hint selection (env MOE_PAIR_TUNE, for experiments)
-        GemmParams p1{c->counts, c->offsets, c->E_local, c->d, c->f_local, 1, c->h, 0, (tune >> 0) & 1,
-                      hints[((tune >> 2) & 3) % 3], hints[((tune >> 4) & 3) % 3]};
+        // tile order per GEMM (see pair_decode); env MOE_PAIR_TUNE overrides for experiments:
+        // bits 0-1 G1 order, 2-3 G2 order, 4-9 G1 band, 10-15 G2 band
+        int r1 = c->g1_raster, r2 = c->g2_raster, b1 = c->g1_band, b2 = c->g2_band;
+        if (c->pair_tune) {
+            r1 = c->pair_tune & 3; r2 = (c->pair_tune >> 2) & 3;
+            b1 = std::max(1, (c->pair_tune >> 4) & 63); b2 = std::max(1, (c->pair_tune >> 10) & 63);
+        }
+        GemmParams p1{c->counts, c->offsets, c->E_local, c->d, c->f_local, 1, c->h, 0, r1, b1,
+                      ptx::kEvictNormal, ptx::kEvictNormal};
         if ((s = launch_gemm_pair<kG1Pair>(c, kSlotGemm1, p1, c->tm_x_tiled, c->tm_w13_pair, g1, st))) return s;
-        GemmParams p2{c->counts, c->offsets, c->E_local, c->d, c->f_local, 1, c->y, 0, (tune >> 1) & 1,
-                      hints[((tune >> 6) & 3) % 3], hints[((tune >> 8) & 3) % 3]};
+        GemmParams p2{c->counts, c->offsets, c->E_local, c->d, c->f_local, 1, c->y, 0, r2, b2,
+                      ptx::kEvictNormal, ptx::kEvictNormal};
         if ((s = launch_gemm_pair<kG2Pair>(c, kSlotGemm2, p2, c->tm_h_tiled, c->tm_w2_swap, g2, st))) return s;
     } else {
         const int64_t mt_max = rows_total / 128 + c->E_local;
