@@ -35,7 +35,12 @@ CONFIGS = {
     # name: (T, d, f, E, k, BASELINE.json config index)
     "decode": (64, 4096, 14336, 8, 2, 1),
     "prefill": (64 * 512, 4096, 14336, 8, 2, 2),
+    # BASELINE.json configs[4]: 32-layer stack, 64 concurrent requests, mixed prefill +
+    # decode; steady-state batch M1 = 63 decode tokens + one 512-token prefill chunk
+    # (one admission every 512/64 = 8 iterations at closed-loop 64).
+    "stack": (575, 4096, 14336, 8, 2, 4),
 }
+STACK_LAYERS = 32
 
 
 METRIC = "MoE-block tokens/sec (Mixtral-8x7B shape, 64-req decode) + % HBM / tensor-pipe peak"
@@ -44,16 +49,21 @@ METRIC = "MoE-block tokens/sec (Mixtral-8x7B shape, 64-req decode) + % HBM / ten
 def workload_config(args, world):
     """The `config` object both arms print (same workload, same keys)."""
     Tg, d, f, E, k, ci = CONFIGS[args.config]
-    par = args.par or ("ep" if world > 1 else "none")
+    stack = args.config == "stack"
+    par = args.par or (("tp" if stack else "ep") if world > 1 else "none")
     T = Tg // world if par == "ep" else Tg
+    what = {"decode": "Mixtral-8x7B single MoE layer, 64-request decode",
+            "prefill": "Mixtral-8x7B single MoE layer, 32k-token prefill",
+            "stack": f"Mixtral-8x7B {STACK_LAYERS}-layer MoE stack (x + MoE(x) per layer), 64 concurrent "
+                     f"requests, mixed batch 63 decode + 1x512 prefill"}[args.config]
     return par, T, {
-        "workload": f"BASELINE.json configs[{3 if world > 1 else ci}]: Mixtral-8x7B single MoE layer, "
-                    f"{'64-request decode' if args.config == 'decode' else '32k-token prefill'}, "
+        "workload": f"BASELINE.json configs[{ci if stack else (3 if world > 1 else ci)}]: {what}, "
                     f"global batch T={Tg}, d={d}, f={f}, E={E}, top-{k}, bf16",
         "global_tokens": Tg, "tokens_per_gpu": T,
         "parallelism": {"none": "single" if world == 1 else f"replicas{world}", "ep": f"ep{world}",
                         "tp": f"tp{world}"}[par],
-        "l2": "weights (2.8 GB) > L2 (126 MB): streamed from HBM every step, no flush"}
+        "layers": STACK_LAYERS if stack else 1,
+        "l2": "weights (2.8 GB per layer) > L2 (126 MB): streamed from HBM every step, no flush"}
 
 
 def parse():
@@ -65,6 +75,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--flags", type=lambda v: int(v, 0), default=0,
+                    help="extra MOE_FLAG_* bits (experiments: 0x2 force swap-AB GEMMs, 0x4 force tiled, 0x10 no CTA pairs)")
     ap.add_argument("--graph", action="store_true",
                     help="headline pass as CUDA-graph replays of the forward (single GPU; default: eager launches)")
     ap.add_argument("--par", default=None, choices=["ep", "tp", "none"],
@@ -221,10 +233,136 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def run_stack(args, world, rank, local):
+    """configs[4]: 32 MoE layers with residual, one shared context, T = 575 mixed batch."""
+    import torch
+    import synth
+    import paper_2408_00008_b200 as moe
+    Tg, d, f, E, k, ci = CONFIGS["stack"]
+    par, T, cfg = workload_config(args, world)
+    dev = torch.device("cuda", local)
+    pmap = {"none": moe.MOE_PAR_NONE, "ep": moe.MOE_PAR_EP, "tp": moe.MOE_PAR_TP}
+    comm = None
+    if par != "none":
+        comm = moe.nccl_comm_from_process_group(world, rank, local) if world > 1 else \
+            moe.moe_nccl_comm_init(moe.moe_nccl_unique_id(), 1, 0, local)
+    first = synth.make_weights(d, f, E, seed=args.seed, layer=0, device=dev)
+    st = moe.MoEStack([first], top_k=k, max_tokens=T, par=pmap[par], world_size=world if par != "none" else 1,
+                      rank=rank if par != "none" else 0, nccl_comm=comm, flags=args.flags)
+    del first
+    for l in range(1, STACK_LAYERS):
+        lw = synth.make_weights(d, f, E, seed=args.seed, layer=l, device=dev)
+        st.add_layer(lw)
+        del lw
+    torch.cuda.empty_cache()
+    nbuf = 4
+    xs = [synth.make_tokens(Tg, d, seed=args.seed + 1 + i, device=dev) for i in range(nbuf)]
+    xs = [x[rank * T:(rank + 1) * T] if par == "ep" else x for x in xs]
+    out = torch.empty(T, d, dtype=torch.bfloat16, device=dev)
+    stream = torch.cuda.current_stream()
+    for i in range(max(3, args.warmup)):
+        st.forward(xs[i % nbuf], out, stream)
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    moe.moe_reset_profile(st.ctx)
+    moe.moe_set_profiling(st.ctx, True)
+    l0 = moe.moe_launch_count(st.ctx)
+    barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for i in range(args.steps):
+        st.forward(xs[i % nbuf], out, stream)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    launches = moe.moe_launch_count(st.ctx) - l0
+    kt = moe.moe_kernel_times(st.ctx)
+    moe.moe_set_profiling(st.ctx, False)
+    ms_prof = ev0.elapsed_time(ev1) / args.steps
+    barrier()
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    for i in range(args.steps):
+        st.forward(xs[i % nbuf], out, stream)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    # e2e: host tokens -> 32 layers -> host output
+    xh = [x.cpu().pin_memory() for x in xs]
+    oh = torch.empty(T, d, dtype=torch.bfloat16).pin_memory()
+    xd = torch.empty(T, d, dtype=torch.bfloat16, device=dev)
+    barrier()
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    for i in range(args.steps):
+        xd.copy_(xh[i % nbuf], non_blocking=True)
+        st.forward(xd, out, stream)
+        oh.copy_(out, non_blocking=True)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    ms_e2e = ev0.elapsed_time(ev1) / args.steps
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([ms, ms_prof, ms_e2e], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, ms_prof, ms_e2e = (float(v) for v in t)
+    peaks = load_peaks()
+    f_l = f // world if par == "tp" else f
+    E_l = E // world if par == "ep" else E
+    # every expert is touched at T = 575 (P(untouched) ~ 0.75^575): weights stream once per layer
+    bytes_layer = E_l * 3 * d * f_l * 2 + E * d * 2 + 2 * T * d * 2
+    per = {n: (v[0] / v[1] if v[1] else 0.0) for n, v in kt.items()}
+    g1_ms = kt["gemm1_w13_swiglu"][0] / max(1, kt["gemm1_w13_swiglu"][1])
+    g1_bytes = E_l * 2 * f_l * d * 2 + T * k * d * 2 + T * k * f_l * 2
+    achieved = g1_bytes / (g1_ms * 1e-3) / 1e9
+    line = {
+        "metric": METRIC, "value": Tg / (ms * 1e-3), "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+        "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong" if par in ("ep", "tp") else "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (seeded Gaussian tokens, random-init Mixtral-shaped weights per layer; DESIGN.md input recipe)",
+        "config": cfg,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                     "frac": achieved / peaks["hbm_gbs"], "traffic": None,
+                     "kernel": "moe_gemm_kernel w1/w3 + SwiGLU (mean over the 32 layers)",
+                     "peak_src": peaks["src"] + " (MEASURED_PEAKS.json hbm_gbs)"},
+        "step_roofline_frac": STACK_LAYERS * bytes_layer / (ms * 1e-3) / 1e9 / peaks["hbm_gbs"],
+        "kernel_ms_per_launch": {n: round(per[n], 5) for n in per if kt[n][1]},
+        "kernel_share": {n: round(kt[n][0] / args.steps / ms_prof, 4) for n in kt if kt[n][1]},
+        "ms_per_step_profiled": ms_prof, "gpu_launches": launches, "clocks": clk,
+        "e2e": {"value": Tg / (ms_e2e * 1e-3), "unit": "tokens/s", "ms_per_step": ms_e2e,
+                "h2d_bytes_per_step": T * d * 2, "d2h_bytes_per_step": T * d * 2,
+                "api": "MoEStack.forward (host tokens copied in, 32 x moe_forward, output copied out)"},
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    st.close()
+    if comm is not None:
+        moe.moe_nccl_comm_destroy(comm)
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+        return
+    if args.config == "stack":
+        import torch
+        world, rank, local = dist_setup(args)
+        run_stack(args, world, rank, local)
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
         return
     import numpy as np
     import torch
@@ -248,7 +386,8 @@ def main():
     xs = [synth.make_tokens(Tg, d, seed=args.seed + 1 + i, device=dev)[rank * T:(rank + 1) * T] if par == "ep"
           else synth.make_tokens(Tg, d, seed=args.seed + 1 + i, device=dev) for i in range(nbuf)]
     blk = moe.MoEBlock(w["wg"], w["w1"], w["w3"], w["w2"], top_k=k, max_tokens=T, par=pmap[par],
-                       world_size=world if par != "none" else 1, rank=rank if par != "none" else 0, nccl_comm=comm)
+                       world_size=world if par != "none" else 1, rank=rank if par != "none" else 0, nccl_comm=comm,
+                       flags=args.flags)
     del w["w1"], w["w3"], w["w2"]
     torch.cuda.empty_cache()
     out = torch.empty(T, d, dtype=torch.bfloat16, device=dev)

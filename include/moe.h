@@ -82,6 +82,9 @@ typedef enum {
 #define MOE_FLAG_FORCE_TILED 0x4u /* always use the prefill (tokens-as-M) GEMMs          */
 #define MOE_FLAG_NO_PDL      0x8u /* disable programmatic dependent launch               */
 #define MOE_FLAG_NO_PAIR     0x10u /* prefill GEMMs on single CTAs (M=128) instead of CTA pairs (M=256) */
+#define MOE_FLAG_EP_EXACT    0x20u /* EP: always exchange exact row counts (one host sync per forward);
+                                      default: exact only when a fixed-capacity exchange would move
+                                      more than 32 MB, i.e. prefill-sized batches                  */
 
 typedef struct {
     int32_t hidden;      /* d: 4096 for Mixtral (C1: 64). Must be a multiple of 64.   */

@@ -29,6 +29,7 @@ _lib = ctypes.CDLL(LIB_PATH)
 MOE_OK, MOE_ERR_INVALID, MOE_ERR_UNSUPPORTED, MOE_ERR_OOM, MOE_ERR_CUDA, MOE_ERR_NCCL, MOE_ERR_STATE = range(7)
 MOE_PAR_NONE, MOE_PAR_EP, MOE_PAR_TP = 0, 1, 2
 MOE_FLAG_RESIDUAL, MOE_FLAG_FORCE_SWAP, MOE_FLAG_FORCE_TILED, MOE_FLAG_NO_PDL, MOE_FLAG_NO_PAIR = 0x1, 0x2, 0x4, 0x8, 0x10
+MOE_FLAG_EP_EXACT = 0x20
 NUM_KERNEL_SLOTS = 8
 KERNEL_SLOTS = ("router", "permute", "gemm1_w13_swiglu", "gemm2_w2", "combine", "dispatch", "exchange", "pack")
 
@@ -272,6 +273,72 @@ class MoEBlock:
             out = torch.empty_like(x)
         moe_forward_routed(self.ctx, x, x.shape[0], topk_idx, topk_w, self.w13, self.w2, out, aux, stream)
         return out
+
+    def close(self):
+        if getattr(self, "ctx", None):
+            moe_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class MoEStack:
+    """A stack of L MoE layers, x_{l+1} = x_l + MoE_l(x_l) (reading R12; the
+    residual add is fused into the combine kernel via MOE_FLAG_RESIDUAL). All layers
+    share one libmoe context (one workspace, cached per-layer TMA descriptors).
+
+    layers: list of dicts with HF-layout bf16 device tensors wg, w1, w3, w2 (each
+    layer's tensors may be freed by the caller after construction: they are packed).
+    """
+
+    def __init__(self, layers, top_k=2, max_tokens=64, par=MOE_PAR_NONE, world_size=1, rank=0, nccl_comm=None,
+                 flags=0, split_k=0, device=None):
+        first = layers[0]
+        dev = first["wg"].device if device is None else torch.device(device)
+        E, f, d = first["w1"].shape
+        self.cfg = make_config(d, f, E, top_k, max_tokens, par, world_size, rank, nccl_comm,
+                               flags | MOE_FLAG_RESIDUAL, split_k,
+                               dev.index if dev.index is not None else torch.cuda.current_device())
+        self.ctx = moe_init(self.cfg)
+        self.d, self.T_max = d, max_tokens
+        b13, b2 = moe_packed_sizes(self.cfg)
+        self.w13, self.w2, self.router_w = [], [], []
+        for lw in layers:
+            self.add_layer(lw, b13, b2, dev)
+        self._buf = [torch.empty(max_tokens, d, dtype=torch.bfloat16, device=dev) for _ in range(2)]
+
+    def add_layer(self, lw, b13=None, b2=None, dev=None):
+        if b13 is None:
+            b13, b2 = moe_packed_sizes(self.cfg)
+        dev = dev or lw["wg"].device
+        w13 = torch.empty(b13 // 2, dtype=torch.bfloat16, device=dev)
+        w2 = torch.empty(b2 // 2, dtype=torch.bfloat16, device=dev)
+        moe_pack_weights(self.ctx, lw["w1"].contiguous(), lw["w3"].contiguous(), lw["w2"].contiguous(), w13, w2)
+        self.w13.append(w13)
+        self.w2.append(w2)
+        self.router_w.append(lw["wg"].contiguous())
+
+    @property
+    def num_layers(self):
+        return len(self.w13)
+
+    def forward(self, x, out=None, stream=None, layer_outputs=None):
+        """x [T, d] bf16 -> out [T, d] bf16 after all layers. layer_outputs: optional
+        list that receives each layer's output tensor (views of internal buffers are
+        cloned) -- used by the per-layer parity tests."""
+        T = x.shape[0]
+        cur = x
+        for l in range(self.num_layers):
+            dst = out if (l == self.num_layers - 1 and out is not None) else self._buf[l % 2][:T]
+            moe_forward(self.ctx, cur, T, self.router_w[l], self.w13[l], self.w2[l], dst, None, stream)
+            if layer_outputs is not None:
+                layer_outputs.append(dst.clone())
+            cur = dst
+        return cur
 
     def close(self):
         if getattr(self, "ctx", None):

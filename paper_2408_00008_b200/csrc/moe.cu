@@ -138,7 +138,10 @@ struct moe_ctx {
     int max_T = 0, nblk_max = 0;
     int64_t cap = 0;          // rows of the permuted buffers (tiled path)
     int64_t cap_swap = 0;     // rows used by the swap (decode) path
-    int swap_max_T = 128;     // swap path chosen when T <= this (and not forced)
+    // decode (swap-AB) GEMMs while the mean rows per local expert T*k/E_l <= this:
+    // the weight stream dominates up to ~2 token tiles of 128 per expert (bench r01:
+    // 32-layer T=575 stack 18.5 ms swap vs 20.8 ms CTA-pair tiles)
+    int swap_rows_per_expert = 256;
     int max_splits = 4;
     int64_t split_stride = 0; // elements between split-K partial buffers of this forward
     int pair_tune = 0;        // experiment override of the prefill tile orders (env MOE_PAIR_TUNE)
@@ -160,13 +163,23 @@ struct moe_ctx {
     int32_t *ep_meta_send = nullptr, *ep_meta_recv = nullptr;
     int32_t *ep_ridx = nullptr, *ep_rpos = nullptr;
     float* ep_rw = nullptr;
+    int32_t* ep_rcounts = nullptr;    // device: rows each peer sends me (exact mode)
+    int32_t* h_counts = nullptr;      // pinned host: [0,64) my send counts, [64,128) receive counts
+    int64_t ep_exact_bytes = 32ll << 20;  // exact mode when a capacity exchange would move more bf16 bytes
     // TMA descriptors: workspace operands
     CUtensorMap tm_x_tiled{}, tm_h_tiled{};
     CUtensorMap tm_x_swap[3]{}, tm_h_swap[3]{};  // NB = 32, 64, 128
     // weight descriptor cache (keyed by pointer)
-    const void* w13_key = nullptr;
-    const void* w2_key = nullptr;
-    CUtensorMap tm_w13{}, tm_w13_pair{}, tm_w2_tiled{}, tm_w2_swap{};
+    struct WeightMaps {
+        const void* w13 = nullptr;
+        const void* w2 = nullptr;
+        uint64_t tick = 0;
+        CUtensorMap tm_w13{}, tm_w13_pair{}, tm_w2_tiled{}, tm_w2_swap{};
+    };
+    static constexpr size_t kWeightMapCache = 64;
+    std::vector<WeightMaps> wmaps;
+    uint64_t use_tick = 0;
+    CUtensorMap tm_w13{}, tm_w13_pair{}, tm_w2_tiled{}, tm_w2_swap{};  // maps of the current call
     // instrumentation
     bool profiling = false;
     struct Ev { int slot; cudaEvent_t a, b; };
@@ -335,19 +348,37 @@ void derive_shape(const moe_config* cfg, int& G, int& E_local, int& e_lo, int& f
     f_off = cfg->par == MOE_PAR_TP ? cfg->rank * f_local : 0;
 }
 
+// TMA descriptors of the expert weights, cached by (w13, w2) address pair (LRU,
+// up to kWeightMapCache layers: a stack of layers shares one context).
 moe_status ensure_weight_maps(moe_ctx* c, const moe_expert_weights* w) {
-    if (w->w13 != c->w13_key) {
-        if (!encode_map(&c->tm_w13, w->w13, 3, c->d, 2 * (uint64_t)c->f_local, c->E_local, 256) ||
-            !encode_map(&c->tm_w13_pair, w->w13, 3, c->d, 2 * (uint64_t)c->f_local, c->E_local, 128))
-            return fail(c, MOE_ERR_CUDA, "cuTensorMapEncodeTiled(w13) failed");
-        c->w13_key = w->w13;
+    c->use_tick++;
+    for (auto& m : c->wmaps)
+        if (m.w13 == w->w13 && m.w2 == w->w2) {
+            m.tick = c->use_tick;
+            c->tm_w13 = m.tm_w13; c->tm_w13_pair = m.tm_w13_pair;
+            c->tm_w2_tiled = m.tm_w2_tiled; c->tm_w2_swap = m.tm_w2_swap;
+            return MOE_OK;
+        }
+    moe_ctx::WeightMaps m;
+    m.w13 = w->w13;
+    m.w2 = w->w2;
+    m.tick = c->use_tick;
+    if (!encode_map(&m.tm_w13, w->w13, 3, c->d, 2 * (uint64_t)c->f_local, c->E_local, 256) ||
+        !encode_map(&m.tm_w13_pair, w->w13, 3, c->d, 2 * (uint64_t)c->f_local, c->E_local, 128))
+        return fail(c, MOE_ERR_CUDA, "cuTensorMapEncodeTiled(w13) failed");
+    if (!encode_map(&m.tm_w2_tiled, w->w2, 3, c->f_local, c->d, c->E_local, 256) ||
+        !encode_map(&m.tm_w2_swap, w->w2, 3, c->f_local, c->d, c->E_local, 128))
+        return fail(c, MOE_ERR_CUDA, "cuTensorMapEncodeTiled(w2) failed");
+    if (c->wmaps.size() >= moe_ctx::kWeightMapCache) {
+        size_t lru = 0;
+        for (size_t i = 1; i < c->wmaps.size(); ++i)
+            if (c->wmaps[i].tick < c->wmaps[lru].tick) lru = i;
+        c->wmaps[lru] = m;
+    } else {
+        c->wmaps.push_back(m);
     }
-    if (w->w2 != c->w2_key) {
-        if (!encode_map(&c->tm_w2_tiled, w->w2, 3, c->f_local, c->d, c->E_local, 256) ||
-            !encode_map(&c->tm_w2_swap, w->w2, 3, c->f_local, c->d, c->E_local, 128))
-            return fail(c, MOE_ERR_CUDA, "cuTensorMapEncodeTiled(w2) failed");
-        c->w2_key = w->w2;
-    }
+    c->tm_w13 = m.tm_w13; c->tm_w13_pair = m.tm_w13_pair;
+    c->tm_w2_tiled = m.tm_w2_tiled; c->tm_w2_swap = m.tm_w2_swap;
     return MOE_OK;
 }
 
@@ -603,6 +634,39 @@ moe_status comm_reduce_scatter_f32(moe_ctx* c, const float* send, float* recv, s
 }
 
 // in-place all-gather: my block lives at recv + rank*cnt
+// all-to-all with per-peer row counts (EP exact mode): rows of peer-bucket p live at
+// slot p*cap (row = row_elems elements); scount[p] rows go to p, rcount[p] come from p.
+moe_status comm_alltoallv(moe_ctx* c, const void* send, void* recv, const int32_t* scount, const int32_t* rcount,
+                          int64_t cap, size_t row_elems, int nccl_type, size_t esize, cudaStream_t st) {
+    const size_t row_b = row_elems * esize;
+    if (LoopbackRank* lr = as_loopback(c->cfg.nccl_comm)) {
+        moe_status s;
+        if ((s = lb_sync(c, st))) return s;
+        LoopbackGroup* g = lr->g;
+        g->ptr[lr->rank] = send;
+        g->barrier();
+        for (int p = 0; p < g->world; ++p)
+            if (rcount[p] > 0)
+                CUDA_TRY(c, cudaMemcpyAsync(static_cast<char*>(recv) + p * cap * row_b,
+                                            static_cast<const char*>(g->ptr[p]) + lr->rank * cap * row_b,
+                                            rcount[p] * row_b, cudaMemcpyDeviceToDevice, st));
+        if ((s = lb_sync(c, st))) return s;
+        g->barrier();
+        return MOE_OK;
+    }
+    NCCL_TRY(c, g_nccl.GroupStart());
+    for (int p = 0; p < c->G; ++p) {
+        if (scount[p] > 0)
+            NCCL_TRY(c, g_nccl.Send(static_cast<const char*>(send) + p * cap * row_b, scount[p] * row_elems, nccl_type,
+                                    p, c->cfg.nccl_comm, st));
+        if (rcount[p] > 0)
+            NCCL_TRY(c, g_nccl.Recv(static_cast<char*>(recv) + p * cap * row_b, rcount[p] * row_elems, nccl_type, p,
+                                    c->cfg.nccl_comm, st));
+    }
+    NCCL_TRY(c, g_nccl.GroupEnd());
+    return MOE_OK;
+}
+
 moe_status comm_allgather_inplace(moe_ctx* c, void* recv, size_t cnt, int nccl_type, size_t esize, cudaStream_t st) {
     const size_t b = cnt * esize;
     if (LoopbackRank* lr = as_loopback(c->cfg.nccl_comm)) {
@@ -628,7 +692,7 @@ moe_status comm_allgather_inplace(moe_ctx* c, void* recv, size_t cnt, int nccl_t
 bool use_swap_path(const moe_ctx* c, int T) {
     if (c->cfg.flags & MOE_FLAG_FORCE_SWAP) return true;
     if (c->cfg.flags & MOE_FLAG_FORCE_TILED) return false;
-    return T <= c->swap_max_T;
+    return (int64_t)T * c->k <= (int64_t)c->swap_rows_per_expert * c->E_local;
 }
 
 moe_status check_ready(moe_ctx* c) {
@@ -709,7 +773,7 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
     // EP: a rank may receive up to every token of every peer (dropless, reading R6).
     const int64_t rows_in = cfg->par == MOE_PAR_EP ? (int64_t)c->max_T * c->G : c->max_T;
     c->cap = round_up(rows_in * c->k + (int64_t)c->E_local * (kSegAlign - 1), kSegAlign);
-    const int64_t swap_T = std::min<int64_t>(rows_in, c->swap_max_T);
+    const int64_t swap_T = std::min<int64_t>(rows_in, (int64_t)c->swap_rows_per_expert * c->E_local / c->k);
     c->cap_swap = round_up(swap_T * c->k + (int64_t)c->E_local * (kSegAlign - 1), kSegAlign);
     c->y_elems = std::max<int64_t>(c->cap, c->cap_swap * c->max_splits) * c->d;
 
@@ -766,6 +830,9 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
         ALLOC(c->ep_ridx, sizeof(int32_t) * slots + 64);
         ALLOC(c->ep_rpos, sizeof(int32_t) * slots + 64);
         ALLOC(c->ep_rw, sizeof(float) * slots + 64);
+        ALLOC(c->ep_rcounts, sizeof(int32_t) * 64);
+        if ((e = cudaMallocHost(reinterpret_cast<void**>(&c->h_counts), sizeof(int32_t) * 128)) != cudaSuccess)
+            return fail_init("h_counts", e);
     }
 #undef ALLOC
     if ((e = cudaMemset(c->done, 0, sizeof(unsigned int) * 4)) != cudaSuccess) return fail_init("memset", e);
@@ -805,9 +872,10 @@ moe_status moe_destroy(moe_ctx* c) {
     void* bufs[] = {c->topk_idx, c->topk_w, c->pos, c->blockcount, c->blockoff, c->counts, c->offsets, c->done,
                     c->x_perm, c->h, c->y, c->stage_in, c->stage_out, c->tp_partial, c->tp_scatter, c->ep_send,
                     c->ep_recv, c->ep_ysend, c->ep_yrecv, c->ep_meta_send, c->ep_meta_recv,
-                    c->ep_ridx, c->ep_rpos, c->ep_rw};
+                    c->ep_ridx, c->ep_rpos, c->ep_rw, c->ep_rcounts};
     for (void* b : bufs)
         if (b) cudaFree(b);
+    if (c->h_counts) cudaFreeHost(c->h_counts);
     for (auto& ev : c->pending) { cudaEventDestroy(ev.a); cudaEventDestroy(ev.b); }
     for (auto ev : c->ev_pool) cudaEventDestroy(ev);
     delete c;
@@ -832,8 +900,7 @@ moe_status moe_pack_weights(moe_ctx* c, const void* w1, const void* w3, const vo
                     c->d, c->f, c->f_local, c->f_off)))
         return s;
     // descriptors keyed by these pointers must be re-encoded if memory was reused
-    if (c->w13_key == w13_out) c->w13_key = nullptr;
-    if (c->w2_key == w2_out) c->w2_key = nullptr;
+    (void)w13_out;  // descriptors hold addresses only; repacking in place keeps them valid
     return MOE_OK;
 }
 
@@ -1073,12 +1140,32 @@ moe_status forward_ep(moe_ctx* c, const void* tokens, int32_t T, const void* rou
         if ((s = route_and_permute(c, r, st))) return s;
         if ((s = copy_aux(c, aux, T, st))) return s;
     }
+    // Exchange. Capacity mode (decode): every peer gets its whole fixed-size bucket,
+    // no host synchronisation (graph-capturable). Exact mode (large batches, or
+    // MOE_FLAG_EP_EXACT): the per-destination counts are exchanged first and read
+    // on the host (one stream sync), then only the occupied rows travel.
+    const bool exact = (c->cfg.flags & MOE_FLAG_EP_EXACT) || cap * c->d * 2 * G > c->ep_exact_bytes;
     StepTimer t1(c, kSlotDispatch, st);
     const bool nccl = as_loopback(comm) == nullptr;
-    if (nccl) NCCL_TRY(c, g_nccl.GroupStart());
-    if ((s = comm_alltoall(c, c->ep_meta_send, c->ep_meta_recv, (size_t)cap, ncclInt32, 4, st))) return s;
-    if ((s = comm_alltoall(c, c->ep_send, c->ep_recv, (size_t)(cap * c->d), ncclBfloat16, 2, st))) return s;
-    if (nccl) NCCL_TRY(c, g_nccl.GroupEnd());
+    if (exact) {
+        if (T == 0) CUDA_TRY(c, cudaMemsetAsync(c->counts, 0, sizeof(int32_t) * G, st));
+        if ((s = comm_alltoall(c, c->counts, c->ep_rcounts, 1, ncclInt32, 4, st))) return s;
+        CUDA_TRY(c, cudaMemcpyAsync(c->h_counts, c->counts, sizeof(int32_t) * G, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(c, cudaMemcpyAsync(c->h_counts + 64, c->ep_rcounts, sizeof(int32_t) * G, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(c, cudaStreamSynchronize(st));
+        CUDA_TRY(c, cudaMemsetAsync(c->ep_meta_recv, 0xFF, sizeof(int32_t) * R, st));
+        if ((s = comm_alltoallv(c, c->ep_meta_send, c->ep_meta_recv, c->h_counts, c->h_counts + 64, cap, 1, ncclInt32,
+                                4, st)))
+            return s;
+        if ((s = comm_alltoallv(c, c->ep_send, c->ep_recv, c->h_counts, c->h_counts + 64, cap, c->d, ncclBfloat16, 2,
+                                st)))
+            return s;
+    } else {
+        if (nccl) NCCL_TRY(c, g_nccl.GroupStart());
+        if ((s = comm_alltoall(c, c->ep_meta_send, c->ep_meta_recv, (size_t)cap, ncclInt32, 4, st))) return s;
+        if ((s = comm_alltoall(c, c->ep_send, c->ep_recv, (size_t)(cap * c->d), ncclBfloat16, 2, st))) return s;
+        if (nccl) NCCL_TRY(c, g_nccl.GroupEnd());
+    }
     t1.done();
     // receive side: R slots (peer-major), k = 1, expert = meta (local index, -1 empty)
     RouteSpec r2;
@@ -1090,9 +1177,14 @@ moe_status forward_ep(moe_ctx* c, const void* tokens, int32_t T, const void* rou
     if ((s = route_and_permute(c, r2, st))) return s;
     if ((s = copy_aux_segments(c, aux, st))) return s;
     // expected rows per rank ~ T*k (balanced routing); an expert gets at most G*max_T rows
+    int64_t rows_expected = (int64_t)T * c->k;  // balanced routing: a rank receives about what it sends
+    if (exact) {
+        rows_expected = 0;
+        for (int p = 0; p < G; ++p) rows_expected += c->h_counts[64 + p];
+    }
     const bool swap = (c->cfg.flags & MOE_FLAG_FORCE_SWAP) ? true
                     : (c->cfg.flags & MOE_FLAG_FORCE_TILED) ? false
-                    : (int64_t)T * c->k <= 2 * c->swap_max_T;
+                    : rows_expected <= (int64_t)c->swap_rows_per_expert * c->E_local;
     int splits = 1;
     if ((s = run_gemms(c, swap, std::min<int64_t>(R, (int64_t)G * c->max_T), R, &splits, st))) return s;
     if ((s = launch(c, kSlotExchange, moe_ep_gather_kernel, dim3((c->d + 1023) / 1024, (unsigned)R), dim3(256), 0,
@@ -1100,7 +1192,13 @@ moe_status forward_ep(moe_ctx* c, const void* tokens, int32_t T, const void* rou
                     static_cast<const int32_t*>(c->ep_rpos), (int)R, c->d, c->ep_ysend)))
         return s;
     StepTimer t2(c, kSlotExchange, st);
-    if ((s = comm_alltoall(c, c->ep_ysend, c->ep_yrecv, (size_t)(cap * c->d), ncclFloat32, 4, st))) return s;
+    if (exact) {  // rows go back to where they came from: counts swap roles
+        if ((s = comm_alltoallv(c, c->ep_ysend, c->ep_yrecv, c->h_counts + 64, c->h_counts, cap, c->d, ncclFloat32, 4,
+                                st)))
+            return s;
+    } else if ((s = comm_alltoall(c, c->ep_ysend, c->ep_yrecv, (size_t)(cap * c->d), ncclFloat32, 4, st))) {
+        return s;
+    }
     t2.done();
     if (T == 0) return MOE_OK;
     CombineParams cp{};

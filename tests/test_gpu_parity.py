@@ -292,7 +292,7 @@ def _check_group_outputs(host, k, x_rows, outs, auxs):
 
 
 @pytest.mark.parametrize("G", [1, 2, 4, 8])
-@pytest.mark.parametrize("mode", ["swap", "tiled"])
+@pytest.mark.parametrize("mode", ["swap", "tiled", "exact"])
 def test_ep_loopback(moe, G, mode):
     """Expert parallel (one process per GPU emulated by G threads on one device):
     tokens sharded unevenly across ranks (incl. a rank with no tokens)."""
@@ -303,7 +303,8 @@ def test_ep_loopback(moe, G, mode):
     if G >= 2:
         cuts[1] = 0  # rank 0 gets no tokens, rank 1 gets the first share
     shards = [inp["x"][cuts[r]:cuts[r + 1]] for r in range(G)]
-    res = _run_group(moe, inp, moe.MOE_PAR_EP, G, shards, flags=MODES[mode], max_tokens=shape.T)
+    flags = moe.MOE_FLAG_EP_EXACT if mode == "exact" else MODES[mode]
+    res = _run_group(moe, inp, moe.MOE_PAR_EP, G, shards, flags=flags, max_tokens=shape.T)
     outs = [r[0] for r in res]
     auxs = [r[1] for r in res]
     _check_group_outputs(host, 2, host["x"], outs, auxs)
@@ -323,15 +324,16 @@ def test_tp_loopback(moe, G, mode):
     _check_group_outputs(host, 2, host["x"], [res[0][0]], [res[0][1]])
 
 
-@pytest.mark.parametrize("par", ["ep", "tp"])
+@pytest.mark.parametrize("par", ["ep", "ep_exact", "tp"])
 def test_mixtral_decode_8_ranks(moe, mixtral_weights, par):
     """BASELINE configs[3]/[4] shapes at G=8 (loopback): 64-token decode, Mixtral layer."""
     w, host = mixtral_weights
     x = synth.make_tokens(64, 4096, seed=300, device="cuda")
     G = 8
-    if par == "ep":
+    if par.startswith("ep"):
         shards = [x[8 * r:8 * (r + 1)] for r in range(G)]
-        res = _run_group(moe, w, moe.MOE_PAR_EP, G, shards, max_tokens=8)
+        res = _run_group(moe, w, moe.MOE_PAR_EP, G, shards, max_tokens=8,
+                         flags=moe.MOE_FLAG_EP_EXACT if par == "ep_exact" else 0)
         outs, auxs = [r[0] for r in res], [r[1] for r in res]
     else:
         res = _run_group(moe, w, moe.MOE_PAR_TP, G, [x] * G, max_tokens=64)
@@ -360,3 +362,32 @@ def test_nccl_world1(moe, par):
     assert rel_err(run.np("out"), y).max() <= 2e-2
     blk.close()
     moe.moe_nccl_comm_destroy(comm)
+
+
+# ---------------------------------------------------------------- C5: layer stack with residual
+@pytest.mark.parametrize("L,shape", [(6, synth.MoEShape(T=100, d=256, f=512, E=8, k=2)),
+                                     (3, synth.MoEShape(T=64, d=4096, f=14336, E=8, k=2))])
+def test_stack_teacher_forced(moe, L, shape):
+    """x_{l+1} = x_l + MoE_l(x_l) (reading R12), one shared context: each layer's
+    GPU output vs the oracle applied to the GPU's own input of that layer."""
+    from parity import rel_err
+    layers = [synth.make_weights(shape.d, shape.f, shape.E, seed=500, layer=l, device="cuda") for l in range(L)]
+    x = synth.make_tokens(shape.T, shape.d, seed=501, device="cuda")
+    st = moe.MoEStack(layers, top_k=shape.k, max_tokens=shape.T)
+    outs = []
+    y = st.forward(x, layer_outputs=outs)
+    torch.cuda.synchronize()
+    assert torch.equal(y.view(torch.int16), outs[-1].view(torch.int16))
+    cur = x
+    for l in range(L):
+        h = {n: synth.bf16_bits(v) for n, v in layers[l].items()}
+        xin = synth.bf16_bits(cur)
+        r = oracle.router(xin, h["wg"], shape.k)
+        # teacher forcing uses the oracle's routing except in the margin band, where
+        # the layer is evaluated with the routing the GPU must have picked (both valid)
+        ref = oracle.moe_forward(xin, h["wg"], h["w1"], h["w3"], h["w2"], shape.k, residual=True)
+        err = rel_err(outs[l].float().cpu().numpy(), ref)
+        excl = r["m23"] < 1e-3
+        assert err[~excl].max() <= 2e-2, (l, err.max())
+        cur = outs[l]
+    st.close()
