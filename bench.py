@@ -84,6 +84,17 @@ def parse():
     return ap.parse_args()
 
 
+def load_traffic(config):
+    """DRAM bytes per launch of the dominant kernel from the newest committed ncu
+    capture (profiles/<round>/traffic.json), or None."""
+    import glob
+    for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "traffic.json")), reverse=True):
+        j = json.load(open(f)).get(config)
+        if j:
+            return j["dram_read_bytes"] + j["dram_write_bytes"], os.path.relpath(f, ROOT)
+    return None, None
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -507,6 +518,11 @@ def main():
                 "traffic": None, "kernel": "moe_gemm_kernel<kG1Tiled> (w1/w3 + SwiGLU)",
                 "peak_src": peaks["src"] + " (MEASURED_PEAKS.json bf16_tflops_sustained)"}
         step_frac = alg["flops"] / (ms * 1e-3) / 1e12 / pk
+    tr, tr_src = load_traffic(args.config) if world == 1 and par == "none" else (None, None)
+    roof["traffic"] = tr
+    if tr is not None:
+        roof["traffic_src"] = tr_src
+        roof["algorithmic"] = alg["g1_bytes"] if decode else alg["g1_flops"]
     tok_s = Tg / (ms * 1e-3) if par in ("ep", "tp") else T * world / (ms * 1e-3)
     kernel_share = {n: round(per[n] / ms_prof, 4) for n in per if ktimes[n][1]}
 
