@@ -51,7 +51,7 @@ def workload_config(args, world):
     Tg, d, f, E, k, ci = CONFIGS[args.config]
     stack = args.config == "stack"
     par = args.par or (("tp" if stack else "ep") if world > 1 else "none")
-    T = Tg // world if par == "ep" else Tg
+    T = Tg // world if par == "ep" else (Tg // (world // args.tp) if par == "hybrid" else Tg)
     what = {"decode": "Mixtral-8x7B single MoE layer, 64-request decode",
             "prefill": "Mixtral-8x7B single MoE layer, 32k-token prefill",
             "stack": f"Mixtral-8x7B {STACK_LAYERS}-layer MoE stack (x + MoE(x) per layer), 64 concurrent "
@@ -61,7 +61,7 @@ def workload_config(args, world):
                     f"global batch T={Tg}, d={d}, f={f}, E={E}, top-{k}, bf16",
         "global_tokens": Tg, "tokens_per_gpu": T,
         "parallelism": {"none": "single" if world == 1 else f"replicas{world}", "ep": f"ep{world}",
-                        "tp": f"tp{world}"}[par],
+                        "tp": f"tp{world}", "hybrid": f"ep{world // args.tp}xtp{args.tp}"}[par],
         "layers": STACK_LAYERS if stack else 1,
         "l2": "weights (2.8 GB per layer) > L2 (126 MB): streamed from HBM every step, no flush"}
 
@@ -79,8 +79,9 @@ def parse():
                     help="extra MOE_FLAG_* bits (experiments: 0x2 force swap-AB GEMMs, 0x4 force tiled, 0x10 no CTA pairs)")
     ap.add_argument("--graph", action="store_true",
                     help="headline pass as CUDA-graph replays of the forward (single GPU; default: eager launches)")
-    ap.add_argument("--par", default=None, choices=["ep", "tp", "none"],
+    ap.add_argument("--par", default=None, choices=["ep", "tp", "hybrid", "none"],
                     help="multi-GPU variant (default: ep when N > 1)")
+    ap.add_argument("--tp", type=int, default=2, help="TP degree of --par hybrid (EP degree = N / tp)")
     return ap.parse_args()
 
 
@@ -233,7 +234,7 @@ def run_reference(args):
     line = {"impl": "reference", "metric": METRIC,
             "value": val, "unit": "tokens/s", "n_gpus": world, "steps": len(times), "warmup": args.warmup,
             "ms_per_step": dt * 1000, "higher_is_better": True,
-            "scaling": "strong" if par in ("ep", "tp") else "weak", "vs_baseline": None,
+            "scaling": "strong" if par in ("ep", "tp", "hybrid") else "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic (same seeded workload; the oracle processes a bounded token sample "
                                     "of it per step)",
             "config": cfg,
@@ -340,7 +341,7 @@ def run_stack(args, world, rank, local):
     line = {
         "metric": METRIC, "value": Tg / (ms * 1e-3), "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
         "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "strong" if par in ("ep", "tp") else "weak", "vs_baseline": None, "dtype": "bf16",
+        "scaling": "strong" if par in ("ep", "tp", "hybrid") else "weak", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (seeded Gaussian tokens, random-init Mixtral-shaped weights per layer; DESIGN.md input recipe)",
         "config": cfg,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
@@ -383,27 +384,29 @@ def main():
 
     Tg, d, f, E, k, ci = CONFIGS[args.config]
     dev = torch.device("cuda", local)
-    par = args.par or ("ep" if world > 1 else "none")
-    pmap = {"none": moe.MOE_PAR_NONE, "ep": moe.MOE_PAR_EP, "tp": moe.MOE_PAR_TP}
-    comm = None
-    if par != "none":
+    par, T, _ = workload_config(args, world)
+    pmap = {"none": moe.MOE_PAR_NONE, "ep": moe.MOE_PAR_EP, "tp": moe.MOE_PAR_TP, "hybrid": moe.MOE_PAR_HYBRID}
+    comm, tp_comm, tp_size = None, None, 0
+    if par == "hybrid":
+        tp_size = args.tp
+        comm, tp_comm = moe.nccl_hybrid_comms(world, rank, tp_size, local)
+    elif par != "none":
         comm = moe.nccl_comm_from_process_group(world, rank, local) if world > 1 else \
             moe.moe_nccl_comm_init(moe.moe_nccl_unique_id(), 1, 0, local)
-    # EP: the global batch is sharded across ranks (strong scaling of the batch);
-    # TP / single GPU: every rank processes the whole batch.
-    T = Tg // world if par == "ep" else Tg
+    # EP / hybrid: the global batch is sharded across the EP groups (strong scaling of
+    # the batch); TP / single GPU: every rank processes the whole batch.
+    shard = rank if par == "ep" else (rank // args.tp if par == "hybrid" else 0)
     w = synth.make_weights(d, f, E, seed=args.seed, device=dev)
     nbuf = 4  # distinct token batches cycled through the steps
-    xs = [synth.make_tokens(Tg, d, seed=args.seed + 1 + i, device=dev)[rank * T:(rank + 1) * T] if par == "ep"
-          else synth.make_tokens(Tg, d, seed=args.seed + 1 + i, device=dev) for i in range(nbuf)]
+    xs = [synth.make_tokens(Tg, d, seed=args.seed + 1 + i, device=dev)[shard * T:(shard + 1) * T] for i in range(nbuf)]
     blk = moe.MoEBlock(w["wg"], w["w1"], w["w3"], w["w2"], top_k=k, max_tokens=T, par=pmap[par],
                        world_size=world if par != "none" else 1, rank=rank if par != "none" else 0, nccl_comm=comm,
-                       flags=args.flags)
+                       flags=args.flags, tp_size=tp_size, tp_comm=tp_comm)
     del w["w1"], w["w3"], w["w2"]
     torch.cuda.empty_cache()
     out = torch.empty(T, d, dtype=torch.bfloat16, device=dev)
-    E_local = E // world if par == "ep" else E
-    f_local = f // world if par == "tp" else f
+    E_local = E // world if par == "ep" else (E // (world // args.tp) if par == "hybrid" else E)
+    f_local = f // world if par == "tp" else (f // args.tp if par == "hybrid" else f)
     counts = torch.empty(E_local, dtype=torch.int32, device=dev)
     stream = torch.cuda.current_stream()
 
@@ -523,14 +526,14 @@ def main():
     if tr is not None:
         roof["traffic_src"] = tr_src
         roof["algorithmic"] = alg["g1_bytes"] if decode else alg["g1_flops"]
-    tok_s = Tg / (ms * 1e-3) if par in ("ep", "tp") else T * world / (ms * 1e-3)
+    tok_s = Tg / (ms * 1e-3) if par in ("ep", "tp", "hybrid") else T * world / (ms * 1e-3)
     kernel_share = {n: round(per[n] / ms_prof, 4) for n in per if ktimes[n][1]}
 
     line = {
         "metric": METRIC,
         "value": tok_s, "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": max(3, args.warmup),
         "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "strong" if par in ("ep", "tp") else "weak", "vs_baseline": None, "dtype": "bf16",
+        "scaling": "strong" if par in ("ep", "tp", "hybrid") else "weak", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (seeded Gaussian tokens, random-init Mixtral-shaped weights; DESIGN.md input recipe)",
         "config": workload_config(args, world)[2],
         "roofline": roof,
@@ -541,7 +544,7 @@ def main():
         "gpu_launches": launches,
         "graph_replay": use_graph,
         "clocks": clk,
-        "e2e": {"value": (Tg if par in ("ep", "tp") else T * world) / (ms_e2e * 1e-3), "unit": "tokens/s",
+        "e2e": {"value": (Tg if par in ("ep", "tp", "hybrid") else T * world) / (ms_e2e * 1e-3), "unit": "tokens/s",
                 "ms_per_step": ms_e2e,
                 "h2d_bytes_per_step": T * d * 2, "d2h_bytes_per_step": T * d * 2,
                 "api": "moe_forward_host (pinned host tokens -> device -> host output)"},
@@ -554,8 +557,9 @@ def main():
     if rank == 0:
         print(json.dumps(line), flush=True)
     blk.close()
-    if comm is not None:
-        moe.moe_nccl_comm_destroy(comm)
+    for cm in (comm, tp_comm):
+        if cm is not None:
+            moe.moe_nccl_comm_destroy(cm)
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()

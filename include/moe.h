@@ -71,9 +71,16 @@ typedef enum {
     MOE_PAR_EP = 1,   /* expert parallel: rank r owns experts [r*E/G, (r+1)*E/G);
                          tokens are sharded by the caller (T may differ per rank);
                          rows are exchanged with NCCL all-to-all (bf16 out, fp32 back) */
-    MOE_PAR_TP = 2    /* tensor parallel: rank r owns ffn columns [r*f/G, (r+1)*f/G)
+    MOE_PAR_TP = 2,   /* tensor parallel: rank r owns ffn columns [r*f/G, (r+1)*f/G)
                          of every expert; every rank passes the same tokens; the
                          fp32 partial outputs are summed across ranks (all-reduce) */
+    MOE_PAR_HYBRID = 3 /* EP x TP ("a hybrid of the two", P:337-349 EP2TP4 / EP4TP2):
+                         G = ep * tp ranks, rank = ep_rank * tp + tp_rank (tp = tp_size).
+                         EP group ep_rank owns experts [ep_rank*E/ep, ...) and each of
+                         its tp ranks an ffn slice [tp_rank*f/tp, ...); the tp ranks of
+                         an EP group pass the same tokens (the group's shard). Rows
+                         travel over nccl_comm (the ep ranks with my tp_rank); expert
+                         outputs are summed over tp_comm (the tp ranks of my group) */
 } moe_par;
 
 /* Flags (moe_config.flags). */
@@ -99,14 +106,17 @@ typedef struct {
     uint32_t flags;      /* MOE_FLAG_*                                                 */
     int32_t split_k;     /* decode w2 GEMM split-K factor; 0 = automatic               */
     int32_t device;      /* CUDA device ordinal the context binds to; -1 = current    */
-    int32_t reserved[6]; /* must be zero                                               */
+    int32_t tp_size;     /* MOE_PAR_HYBRID: TP degree (world_size = ep * tp_size); else 0 */
+    void* tp_comm;       /* MOE_PAR_HYBRID: communicator of my TP group; else NULL      */
+    int32_t reserved[3]; /* must be zero                                               */
 } moe_config;
 
 /* Packed expert weights of THIS rank (device, bf16, produced by moe_pack_weights).
  *   w13: [E_local, 2*f_local, d] -- w1 and w3 rows interleaved in blocks of 128:
  *        packed row 256*b + i     = w1 row 128*b + i  (i < 128)
  *        packed row 256*b + 128+i = w3 row 128*b + i
- *   w2:  [E_local, d, f_local]   -- HF layout, ffn slice of this rank.          */
+ *   w2:  [E_local, d, f_local]   -- HF layout, ffn slice of this rank.
+ * (E_local = E/ep, f_local = f/tp: EP ep = G, TP tp = G, hybrid ep * tp = G.)   */
 typedef struct {
     const void* w13;
     const void* w2;

@@ -27,7 +27,7 @@ if not os.path.exists(LIB_PATH):
 _lib = ctypes.CDLL(LIB_PATH)
 
 MOE_OK, MOE_ERR_INVALID, MOE_ERR_UNSUPPORTED, MOE_ERR_OOM, MOE_ERR_CUDA, MOE_ERR_NCCL, MOE_ERR_STATE = range(7)
-MOE_PAR_NONE, MOE_PAR_EP, MOE_PAR_TP = 0, 1, 2
+MOE_PAR_NONE, MOE_PAR_EP, MOE_PAR_TP, MOE_PAR_HYBRID = 0, 1, 2, 3
 MOE_FLAG_RESIDUAL, MOE_FLAG_FORCE_SWAP, MOE_FLAG_FORCE_TILED, MOE_FLAG_NO_PDL, MOE_FLAG_NO_PAIR = 0x1, 0x2, 0x4, 0x8, 0x10
 MOE_FLAG_EP_EXACT = 0x20
 NUM_KERNEL_SLOTS = 8
@@ -46,7 +46,7 @@ class moe_config(ctypes.Structure):
                 ("top_k", ctypes.c_int32), ("max_tokens", ctypes.c_int32), ("par", ctypes.c_int32),
                 ("world_size", ctypes.c_int32), ("rank", ctypes.c_int32), ("nccl_comm", ctypes.c_void_p),
                 ("flags", ctypes.c_uint32), ("split_k", ctypes.c_int32), ("device", ctypes.c_int32),
-                ("reserved", ctypes.c_int32 * 6)]
+                ("tp_size", ctypes.c_int32), ("tp_comm", ctypes.c_void_p), ("reserved", ctypes.c_int32 * 3)]
 
 
 class moe_expert_weights(ctypes.Structure):
@@ -117,11 +117,12 @@ def _stream(stream):
 
 
 def make_config(hidden, ffn, num_experts, top_k, max_tokens, par=MOE_PAR_NONE, world_size=1, rank=0,
-                nccl_comm=None, flags=0, split_k=0, device=-1) -> moe_config:
+                nccl_comm=None, flags=0, split_k=0, device=-1, tp_size=0, tp_comm=None) -> moe_config:
     c = moe_config()
     c.hidden, c.ffn, c.num_experts, c.top_k, c.max_tokens = hidden, ffn, num_experts, top_k, max_tokens
     c.par, c.world_size, c.rank, c.nccl_comm = par, world_size, rank, nccl_comm
     c.flags, c.split_k, c.device = flags, split_k, device
+    c.tp_size, c.tp_comm = tp_size, tp_comm
     return c
 
 
@@ -240,6 +241,22 @@ def nccl_comm_from_process_group(world: int, rank: int, device: int):
     return moe_nccl_comm_init(obj[0], world, rank, device)
 
 
+def nccl_hybrid_comms(world: int, rank: int, tp: int, device: int):
+    """EP x TP communicators for MOE_PAR_HYBRID: rank = ep_rank * tp + tp_rank.
+    Returns (ep_comm over the ranks sharing my tp_rank, tp_comm over my EP group).
+    Rank 0 draws every group's ncclUniqueId; the host process group broadcasts them."""
+    ep = world // tp
+    obj = [[moe_nccl_unique_id() for _ in range(tp + ep)] if rank == 0 else None]
+    if world > 1:
+        import torch.distributed as dist
+        dist.broadcast_object_list(obj, src=0)
+    ids = obj[0]
+    e, t = rank // tp, rank % tp
+    ep_comm = moe_nccl_comm_init(ids[t], ep, e, device)
+    tp_comm = moe_nccl_comm_init(ids[tp + e], tp, t, device)
+    return ep_comm, tp_comm
+
+
 # ------------------------------------------------------------------ convenience owner
 class MoEBlock:
     """Owns a libmoe context and this rank's packed weights (torch device memory).
@@ -248,11 +265,11 @@ class MoEBlock:
     """
 
     def __init__(self, router_w, w1, w3, w2, top_k=2, max_tokens=64, par=MOE_PAR_NONE, world_size=1, rank=0,
-                 nccl_comm=None, flags=0, split_k=0, device=None):
+                 nccl_comm=None, flags=0, split_k=0, device=None, tp_size=0, tp_comm=None):
         dev = router_w.device if device is None else torch.device(device)
         E, f, d = w1.shape
         self.cfg = make_config(d, f, E, top_k, max_tokens, par, world_size, rank, nccl_comm, flags, split_k,
-                               dev.index if dev.index is not None else torch.cuda.current_device())
+                               dev.index if dev.index is not None else torch.cuda.current_device(), tp_size, tp_comm)
         self.ctx = moe_init(self.cfg)
         self.d, self.f, self.E, self.k = d, f, E, top_k
         b13, b2 = moe_packed_sizes(self.cfg)

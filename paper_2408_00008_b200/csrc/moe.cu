@@ -135,6 +135,9 @@ struct moe_ctx {
     int num_sms = 148;
     int d = 0, f = 0, E = 0, k = 0, G = 1, rank = 0;
     int E_local = 0, e_lo = 0, f_local = 0, f_off = 0;
+    int ep_world = 1, ep_rank = 0, tp_world = 1, tp_rank = 0;  // G = ep_world * tp_world
+    float* lb_scratch = nullptr;  // loopback all-reduce scratch (test transport)
+    size_t lb_scratch_elems = 0;
     int max_T = 0, nblk_max = 0;
     int64_t cap = 0;          // rows of the permuted buffers (tiled path)
     int64_t cap_swap = 0;     // rows used by the swap (decode) path
@@ -314,6 +317,30 @@ moe_status launch_gemm(moe_ctx* c, int slot, const GemmParams& p, const CUtensor
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
+// Parallel layout of a config: G ranks = ep_world x tp_world; rank = ep_rank * tp_world + tp_rank.
+struct ParShape {
+    int G = 1, ep_world = 1, tp_world = 1, ep_rank = 0, tp_rank = 0;
+    int E_local = 0, e_lo = 0, f_local = 0, f_off = 0;
+};
+
+ParShape par_shape(const moe_config* cfg) {
+    ParShape ps;
+    ps.G = cfg->par == MOE_PAR_NONE ? 1 : cfg->world_size;
+    if (cfg->par == MOE_PAR_EP) { ps.ep_world = ps.G; ps.ep_rank = cfg->rank; }
+    if (cfg->par == MOE_PAR_TP) { ps.tp_world = ps.G; ps.tp_rank = cfg->rank; }
+    if (cfg->par == MOE_PAR_HYBRID) {
+        ps.tp_world = cfg->tp_size > 0 ? cfg->tp_size : 1;
+        ps.ep_world = ps.G / ps.tp_world;
+        ps.ep_rank = cfg->rank / ps.tp_world;
+        ps.tp_rank = cfg->rank % ps.tp_world;
+    }
+    ps.E_local = cfg->num_experts / ps.ep_world;
+    ps.e_lo = ps.ep_rank * ps.E_local;
+    ps.f_local = cfg->ffn / ps.tp_world;
+    ps.f_off = ps.tp_rank * ps.f_local;
+    return ps;
+}
+
 moe_status validate_cfg(const moe_config* cfg, moe_ctx* c) {
     if (!cfg) return fail(c, MOE_ERR_INVALID, "cfg is NULL");
     if (cfg->hidden <= 0 || cfg->hidden % 64) return fail(c, MOE_ERR_INVALID, "hidden must be a positive multiple of 64");
@@ -321,35 +348,34 @@ moe_status validate_cfg(const moe_config* cfg, moe_ctx* c) {
     if (cfg->top_k < 1 || cfg->top_k > 2 || cfg->top_k > cfg->num_experts)
         return fail(c, MOE_ERR_INVALID, "top_k must be 1 or 2 and <= num_experts");
     if (cfg->max_tokens < 1) return fail(c, MOE_ERR_INVALID, "max_tokens must be >= 1");
-    if (cfg->par < MOE_PAR_NONE || cfg->par > MOE_PAR_TP) return fail(c, MOE_ERR_INVALID, "bad par");
+    if (cfg->par < MOE_PAR_NONE || cfg->par > MOE_PAR_HYBRID) return fail(c, MOE_ERR_INVALID, "bad par");
     const int G = cfg->par == MOE_PAR_NONE ? 1 : cfg->world_size;
     if (G < 1 || cfg->rank < 0 || cfg->rank >= G) return fail(c, MOE_ERR_INVALID, "bad world_size/rank");
     if (cfg->par == MOE_PAR_NONE && (cfg->world_size > 1 || cfg->rank != 0))
         return fail(c, MOE_ERR_INVALID, "MOE_PAR_NONE needs world_size 1, rank 0");
-    if (cfg->ffn <= 0 || cfg->ffn % (128 * (cfg->par == MOE_PAR_TP ? G : 1)))
+    if (cfg->par == MOE_PAR_HYBRID && (cfg->tp_size < 1 || G % cfg->tp_size))
+        return fail(c, MOE_ERR_INVALID, "MOE_PAR_HYBRID needs tp_size >= 1 dividing world_size");
+    if (cfg->par != MOE_PAR_HYBRID && (cfg->tp_size != 0 || cfg->tp_comm))
+        return fail(c, MOE_ERR_INVALID, "tp_size / tp_comm are for MOE_PAR_HYBRID only");
+    const ParShape ps = par_shape(cfg);
+    if (cfg->ffn <= 0 || cfg->ffn % (128 * ps.tp_world))
         return fail(c, MOE_ERR_INVALID, "ffn / tp_world must be a positive multiple of 128");
-    if (cfg->par == MOE_PAR_EP && cfg->num_experts % G) return fail(c, MOE_ERR_INVALID, "num_experts % ep_world != 0");
+    if (cfg->num_experts % ps.ep_world) return fail(c, MOE_ERR_INVALID, "num_experts % ep_world != 0");
     if (cfg->par == MOE_PAR_TP && cfg->hidden % (4 * G))
         return fail(c, MOE_ERR_INVALID, "TP needs hidden % (4*world) == 0 (reduce-scatter shards)");
-    if (cfg->par != MOE_PAR_NONE && G > 1 && !cfg->nccl_comm) return fail(c, MOE_ERR_INVALID, "nccl_comm required");
+    if ((cfg->par == MOE_PAR_EP || cfg->par == MOE_PAR_HYBRID) && !cfg->nccl_comm)
+        return fail(c, MOE_ERR_INVALID, "nccl_comm (EP group) required");
+    if (cfg->par == MOE_PAR_TP && G > 1 && !cfg->nccl_comm) return fail(c, MOE_ERR_INVALID, "nccl_comm required");
+    if (cfg->par == MOE_PAR_HYBRID && ps.tp_world > 1 && !cfg->tp_comm)
+        return fail(c, MOE_ERR_INVALID, "tp_comm (TP group) required");
     if (cfg->split_k < 0 || cfg->split_k > 8) return fail(c, MOE_ERR_INVALID, "split_k must be in [0,8]");
-    for (int i = 0; i < 6; ++i)
+    for (int i = 0; i < 3; ++i)
         if (cfg->reserved[i]) return fail(c, MOE_ERR_INVALID, "reserved fields must be zero");
     if ((cfg->flags & MOE_FLAG_FORCE_SWAP) && (cfg->flags & MOE_FLAG_FORCE_TILED))
         return fail(c, MOE_ERR_INVALID, "FORCE_SWAP and FORCE_TILED are exclusive");
     return MOE_OK;
 }
 
-void derive_shape(const moe_config* cfg, int& G, int& E_local, int& e_lo, int& f_local, int& f_off) {
-    G = cfg->par == MOE_PAR_NONE ? 1 : cfg->world_size;
-    E_local = cfg->par == MOE_PAR_EP ? cfg->num_experts / G : cfg->num_experts;
-    e_lo = cfg->par == MOE_PAR_EP ? cfg->rank * E_local : 0;
-    f_local = cfg->par == MOE_PAR_TP ? cfg->ffn / G : cfg->ffn;
-    f_off = cfg->par == MOE_PAR_TP ? cfg->rank * f_local : 0;
-}
-
-// TMA descriptors of the expert weights, cached by (w13, w2) address pair (LRU,
-// up to kWeightMapCache layers: a stack of layers shares one context).
 moe_status ensure_weight_maps(moe_ctx* c, const moe_expert_weights* w) {
     c->use_tick++;
     for (auto& m : c->wmaps)
@@ -591,10 +617,17 @@ moe_status lb_sync(moe_ctx* c, cudaStream_t st) {
     return MOE_OK;
 }
 
-// all-to-all: peer p's block `rank` -> my block p (bytes per peer)
-moe_status comm_alltoall(moe_ctx* c, const void* send, void* recv, size_t count, int nccl_type, size_t esize,
-                         cudaStream_t st) {
-    if (LoopbackRank* lr = as_loopback(c->cfg.nccl_comm)) {
+// A communicator of the context: NCCL handle or loopback rank handle, its size and
+// this process's rank in it (EP group, TP group).
+struct CommRef {
+    void* comm;
+    int world, rank;
+};
+
+// all-to-all: peer p's block `rank` -> my block p (count elements per peer)
+moe_status comm_alltoall(moe_ctx* c, CommRef cm, const void* send, void* recv, size_t count, int nccl_type,
+                         size_t esize, cudaStream_t st) {
+    if (LoopbackRank* lr = as_loopback(cm.comm)) {
         moe_status s;
         if ((s = lb_sync(c, st))) return s;
         LoopbackGroup* g = lr->g;
@@ -609,12 +642,13 @@ moe_status comm_alltoall(moe_ctx* c, const void* send, void* recv, size_t count,
         g->barrier();
         return MOE_OK;
     }
-    NCCL_TRY(c, g_nccl.AlltoAll(send, recv, count, nccl_type, c->cfg.nccl_comm, st));
+    NCCL_TRY(c, g_nccl.AlltoAll(send, recv, count, nccl_type, cm.comm, st));
     return MOE_OK;
 }
 
-moe_status comm_reduce_scatter_f32(moe_ctx* c, const float* send, float* recv, size_t cnt, cudaStream_t st) {
-    if (LoopbackRank* lr = as_loopback(c->cfg.nccl_comm)) {
+moe_status comm_reduce_scatter_f32(moe_ctx* c, CommRef cm, const float* send, float* recv, size_t cnt,
+                                   cudaStream_t st) {
+    if (LoopbackRank* lr = as_loopback(cm.comm)) {
         moe_status s;
         if ((s = lb_sync(c, st))) return s;
         LoopbackGroup* g = lr->g;
@@ -629,17 +663,50 @@ moe_status comm_reduce_scatter_f32(moe_ctx* c, const float* send, float* recv, s
         g->barrier();
         return MOE_OK;
     }
-    NCCL_TRY(c, g_nccl.ReduceScatter(send, recv, cnt, ncclFloat32, ncclSum, c->cfg.nccl_comm, st));
+    NCCL_TRY(c, g_nccl.ReduceScatter(send, recv, cnt, ncclFloat32, ncclSum, cm.comm, st));
     return MOE_OK;
 }
 
-// in-place all-gather: my block lives at recv + rank*cnt
+// in-place fp32 sum over the group (hybrid EP x TP: the expert outputs of the ffn slices)
+moe_status comm_allreduce_f32(moe_ctx* c, CommRef cm, float* buf, size_t cnt, cudaStream_t st) {
+    if (LoopbackRank* lr = as_loopback(cm.comm)) {
+        moe_status s;
+        if ((s = lb_sync(c, st))) return s;
+        LoopbackGroup* g = lr->g;
+        g->ptr[lr->rank] = buf;
+        g->barrier();
+        // every rank forms the same ascending-rank sum in a scratch copy, then all
+        // ranks meet again before anyone overwrites its buffer
+        float* tmp = c->lb_scratch;
+        if (!tmp || c->lb_scratch_elems < cnt) {
+            if (tmp) cudaFree(tmp);
+            CUDA_TRY(c, cudaMalloc(reinterpret_cast<void**>(&c->lb_scratch), cnt * 4));
+            c->lb_scratch_elems = cnt;
+            tmp = c->lb_scratch;
+        }
+        for (int p = 0; p < g->world; ++p) {
+            const float* src = static_cast<const float*>(g->ptr[p]);
+            if (p == 0) CUDA_TRY(c, cudaMemcpyAsync(tmp, src, cnt * 4, cudaMemcpyDeviceToDevice, st));
+            else moe_loopback_add_kernel<<<c->num_sms, 256, 0, st>>>(tmp, src, (int64_t)cnt);
+        }
+        if ((s = lb_sync(c, st))) return s;
+        g->barrier();
+        CUDA_TRY(c, cudaMemcpyAsync(buf, tmp, cnt * 4, cudaMemcpyDeviceToDevice, st));
+        if ((s = lb_sync(c, st))) return s;
+        g->barrier();
+        return MOE_OK;
+    }
+    NCCL_TRY(c, g_nccl.AllReduce(buf, buf, cnt, ncclFloat32, ncclSum, cm.comm, st));
+    return MOE_OK;
+}
+
 // all-to-all with per-peer row counts (EP exact mode): rows of peer-bucket p live at
 // slot p*cap (row = row_elems elements); scount[p] rows go to p, rcount[p] come from p.
-moe_status comm_alltoallv(moe_ctx* c, const void* send, void* recv, const int32_t* scount, const int32_t* rcount,
-                          int64_t cap, size_t row_elems, int nccl_type, size_t esize, cudaStream_t st) {
+moe_status comm_alltoallv(moe_ctx* c, CommRef cm, const void* send, void* recv, const int32_t* scount,
+                          const int32_t* rcount, int64_t cap, size_t row_elems, int nccl_type, size_t esize,
+                          cudaStream_t st) {
     const size_t row_b = row_elems * esize;
-    if (LoopbackRank* lr = as_loopback(c->cfg.nccl_comm)) {
+    if (LoopbackRank* lr = as_loopback(cm.comm)) {
         moe_status s;
         if ((s = lb_sync(c, st))) return s;
         LoopbackGroup* g = lr->g;
@@ -655,21 +722,23 @@ moe_status comm_alltoallv(moe_ctx* c, const void* send, void* recv, const int32_
         return MOE_OK;
     }
     NCCL_TRY(c, g_nccl.GroupStart());
-    for (int p = 0; p < c->G; ++p) {
+    for (int p = 0; p < cm.world; ++p) {
         if (scount[p] > 0)
             NCCL_TRY(c, g_nccl.Send(static_cast<const char*>(send) + p * cap * row_b, scount[p] * row_elems, nccl_type,
-                                    p, c->cfg.nccl_comm, st));
+                                    p, cm.comm, st));
         if (rcount[p] > 0)
             NCCL_TRY(c, g_nccl.Recv(static_cast<char*>(recv) + p * cap * row_b, rcount[p] * row_elems, nccl_type, p,
-                                    c->cfg.nccl_comm, st));
+                                    cm.comm, st));
     }
     NCCL_TRY(c, g_nccl.GroupEnd());
     return MOE_OK;
 }
 
-moe_status comm_allgather_inplace(moe_ctx* c, void* recv, size_t cnt, int nccl_type, size_t esize, cudaStream_t st) {
+// in-place all-gather: my block lives at recv + rank*cnt
+moe_status comm_allgather_inplace(moe_ctx* c, CommRef cm, void* recv, size_t cnt, int nccl_type, size_t esize,
+                                  cudaStream_t st) {
     const size_t b = cnt * esize;
-    if (LoopbackRank* lr = as_loopback(c->cfg.nccl_comm)) {
+    if (LoopbackRank* lr = as_loopback(cm.comm)) {
         moe_status s;
         if ((s = lb_sync(c, st))) return s;
         LoopbackGroup* g = lr->g;
@@ -684,10 +753,14 @@ moe_status comm_allgather_inplace(moe_ctx* c, void* recv, size_t cnt, int nccl_t
         g->barrier();
         return MOE_OK;
     }
-    NCCL_TRY(c, g_nccl.AllGather(static_cast<char*>(recv) + c->rank * b, recv, cnt, nccl_type, c->cfg.nccl_comm, st));
+    NCCL_TRY(c, g_nccl.AllGather(static_cast<char*>(recv) + cm.rank * b, recv, cnt, nccl_type, cm.comm, st));
     return MOE_OK;
 }
 
+CommRef ep_comm(const moe_ctx* c) { return {c->cfg.nccl_comm, c->ep_world, c->ep_rank}; }
+CommRef tp_comm(const moe_ctx* c) {
+    return {c->cfg.par == MOE_PAR_HYBRID ? c->cfg.tp_comm : c->cfg.nccl_comm, c->tp_world, c->tp_rank};
+}
 
 bool use_swap_path(const moe_ctx* c, int T) {
     if (c->cfg.flags & MOE_FLAG_FORCE_SWAP) return true;
@@ -732,10 +805,9 @@ moe_status moe_packed_sizes(const moe_config* cfg, size_t* w13_bytes, size_t* w2
     moe_status s = validate_cfg(cfg, nullptr);
     if (s) return s;
     if (!w13_bytes || !w2_bytes) return fail(nullptr, MOE_ERR_INVALID, "NULL output pointer");
-    int G, E_local, e_lo, f_local, f_off;
-    derive_shape(cfg, G, E_local, e_lo, f_local, f_off);
-    *w13_bytes = (size_t)E_local * 2 * f_local * cfg->hidden * 2;
-    *w2_bytes = (size_t)E_local * cfg->hidden * f_local * 2;
+    const ParShape ps = par_shape(cfg);
+    *w13_bytes = (size_t)ps.E_local * 2 * ps.f_local * cfg->hidden * 2;
+    *w2_bytes = (size_t)ps.E_local * cfg->hidden * ps.f_local * 2;
     return MOE_OK;
 }
 
@@ -763,15 +835,20 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
     c->device = dev;
     c->num_sms = prop.multiProcessorCount;
     c->d = cfg->hidden; c->f = cfg->ffn; c->E = cfg->num_experts; c->k = cfg->top_k;
-    derive_shape(cfg, c->G, c->E_local, c->e_lo, c->f_local, c->f_off);
+    {
+        const ParShape ps = par_shape(cfg);
+        c->G = ps.G; c->E_local = ps.E_local; c->e_lo = ps.e_lo; c->f_local = ps.f_local; c->f_off = ps.f_off;
+        c->ep_world = ps.ep_world; c->ep_rank = ps.ep_rank; c->tp_world = ps.tp_world; c->tp_rank = ps.tp_rank;
+    }
     c->rank = cfg->rank;
     c->max_T = cfg->max_tokens;
     if (const char* pt = getenv("MOE_PAIR_TUNE")) c->pair_tune = atoi(pt);
     // router blocks of >= 2 rows; EP also routes the G*max_T*k receive slots
-    c->nblk_max = (int)(((int64_t)c->max_T * (cfg->par == MOE_PAR_EP ? c->G * c->k : 1) + 1) / 2 + 1);
+    c->nblk_max = (int)(((int64_t)c->max_T * (c->ep_world > 1 ? c->ep_world * c->k : 1) + 1) / 2 + 1);
 
     // EP: a rank may receive up to every token of every peer (dropless, reading R6).
-    const int64_t rows_in = cfg->par == MOE_PAR_EP ? (int64_t)c->max_T * c->G : c->max_T;
+    const bool ep_like = cfg->par == MOE_PAR_EP || cfg->par == MOE_PAR_HYBRID;
+    const int64_t rows_in = ep_like ? (int64_t)c->max_T * c->ep_world : c->max_T;
     c->cap = round_up(rows_in * c->k + (int64_t)c->E_local * (kSegAlign - 1), kSegAlign);
     const int64_t swap_T = std::min<int64_t>(rows_in, (int64_t)c->swap_rows_per_expert * c->E_local / c->k);
     c->cap_swap = round_up(swap_T * c->k + (int64_t)c->E_local * (kSegAlign - 1), kSegAlign);
@@ -785,12 +862,18 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
     };
     cudaError_t e;
     if ((e = cudaSetDevice(dev)) != cudaSuccess) return fail_init("cudaSetDevice", e);
-    if (LoopbackRank* lr = as_loopback(cfg->nccl_comm)) {
-        if (lr->rank != cfg->rank || lr->g->world != c->G) {
-            moe_destroy(c);
-            return fail(nullptr, MOE_ERR_INVALID, "loopback comm rank/world does not match cfg");
-        }
-    } else if (cfg->par != MOE_PAR_NONE && c->G > 1) {
+    {
+        const int want_world[2] = {cfg->par == MOE_PAR_TP ? c->tp_world : c->ep_world, c->tp_world};
+        const int want_rank[2] = {cfg->par == MOE_PAR_TP ? c->tp_rank : c->ep_rank, c->tp_rank};
+        void* comms[2] = {cfg->nccl_comm, cfg->par == MOE_PAR_HYBRID ? cfg->tp_comm : nullptr};
+        for (int i = 0; i < 2; ++i)
+            if (LoopbackRank* lr = as_loopback(comms[i]))
+                if (lr->rank != want_rank[i] || lr->g->world != want_world[i]) {
+                    moe_destroy(c);
+                    return fail(nullptr, MOE_ERR_INVALID, "loopback comm rank/world does not match cfg");
+                }
+    }
+    if (!as_loopback(cfg->nccl_comm) && cfg->par != MOE_PAR_NONE && c->G > 1) {
         std::string lerr;
         if (!load_nccl(lerr)) {
             moe_destroy(c);
@@ -818,9 +901,9 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
         ALLOC(c->tp_partial, sizeof(float) * c->max_T * c->d);
         ALLOC(c->tp_scatter, sizeof(float) * ((int64_t)c->max_T * c->d / c->G + 64));
     }
-    if (cfg->par == MOE_PAR_EP) {
+    if (ep_like) {
         // fixed per-peer capacity of max_T*k rows (dropless)
-        const int64_t slots = (int64_t)c->G * c->max_T * c->k;
+        const int64_t slots = (int64_t)c->ep_world * c->max_T * c->k;
         ALLOC(c->ep_send, sizeof(__nv_bfloat16) * slots * c->d);
         ALLOC(c->ep_recv, sizeof(__nv_bfloat16) * slots * c->d);
         ALLOC(c->ep_ysend, sizeof(float) * slots * c->d);
@@ -872,7 +955,7 @@ moe_status moe_destroy(moe_ctx* c) {
     void* bufs[] = {c->topk_idx, c->topk_w, c->pos, c->blockcount, c->blockoff, c->counts, c->offsets, c->done,
                     c->x_perm, c->h, c->y, c->stage_in, c->stage_out, c->tp_partial, c->tp_scatter, c->ep_send,
                     c->ep_recv, c->ep_ysend, c->ep_yrecv, c->ep_meta_send, c->ep_meta_recv,
-                    c->ep_ridx, c->ep_rpos, c->ep_rw, c->ep_rcounts};
+                    c->ep_ridx, c->ep_rpos, c->ep_rw, c->ep_rcounts, c->lb_scratch};
     for (void* b : bufs)
         if (b) cudaFree(b);
     if (c->h_counts) cudaFreeHost(c->h_counts);
@@ -890,7 +973,7 @@ moe_status moe_pack_weights(moe_ctx* c, const void* w1, const void* w3, const vo
     if (!aligned16(w1) || !aligned16(w3) || !aligned16(w2) || !aligned16(w13_out) || !aligned16(w2_out))
         return fail(c, MOE_ERR_INVALID, "weight pointers must be 16-byte aligned");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    const int e_off = c->cfg.par == MOE_PAR_EP ? c->e_lo : 0;
+    const int e_off = c->e_lo;  // 0 unless experts are sharded (EP, hybrid)
     if ((s = launch(c, kSlotPack, moe_pack_w13_kernel, dim3(4 * c->num_sms), dim3(256), 0, st,
                     static_cast<const __nv_bfloat16*>(w1), static_cast<const __nv_bfloat16*>(w3),
                     static_cast<__nv_bfloat16*>(w13_out), c->E_local, e_off, c->d, c->f, c->f_local, c->f_off)))
@@ -917,7 +1000,8 @@ moe_status moe_forward_routed(moe_ctx* c, const void* tokens, int32_t T, const i
                               void* stream) {
     moe_status s = check_ready(c);
     if (s) return s;
-    if (c->cfg.par == MOE_PAR_EP) return fail(c, MOE_ERR_UNSUPPORTED, "moe_forward_routed: single-GPU / TP only");
+    if (c->cfg.par == MOE_PAR_EP || c->cfg.par == MOE_PAR_HYBRID)
+        return fail(c, MOE_ERR_UNSUPPORTED, "moe_forward_routed: single-GPU / TP only");
     if (T > 0 && (!topk_idx || !topk_w)) return fail(c, MOE_ERR_INVALID, "NULL routing");
     return forward_impl(c, tokens, T, nullptr, topk_idx, topk_w, w, out, aux, static_cast<cudaStream_t>(stream));
 }
@@ -1054,7 +1138,7 @@ moe_status forward_impl(moe_ctx* c, const void* tokens, int32_t T, const void* r
     if (aux && aux->out_f32 && !aligned16(aux->out_f32)) return fail(c, MOE_ERR_INVALID, "aux.out_f32 misaligned");
     moe_status s = ensure_weight_maps(c, w);
     if (s) return s;
-    if (c->cfg.par == MOE_PAR_EP) return forward_ep(c, tokens, T, router_w, out, aux, st);
+    if (c->cfg.par == MOE_PAR_EP || c->cfg.par == MOE_PAR_HYBRID) return forward_ep(c, tokens, T, router_w, out, aux, st);
     if (T == 0) return MOE_OK;  // TP: every rank passes the same T, so all skip together
 
     const bool tp = c->cfg.par == MOE_PAR_TP && c->G > 1;
@@ -1094,9 +1178,10 @@ moe_status forward_impl(moe_ctx* c, const void* tokens, int32_t T, const void* r
     if ((s = launch(c, kSlotCombine, moe_combine_kernel, dim3((c->d + 4095) / 4096, T), dim3(256), 0, st, cp)))
         return s;
     const int64_t n = (int64_t)T * c->d, cnt = n / c->G, base = cnt * c->rank;
+    const CommRef tpc = tp_comm(c);
     ncclComm_t comm = c->cfg.nccl_comm;
     StepTimer t1(c, kSlotExchange, st);
-    if ((s = comm_reduce_scatter_f32(c, c->tp_partial, c->tp_scatter, (size_t)cnt, st))) return s;
+    if ((s = comm_reduce_scatter_f32(c, tpc, c->tp_partial, c->tp_scatter, (size_t)cnt, st))) return s;
     t1.done();
     float* of32 = aux ? aux->out_f32 : nullptr;
     const int blocks = (int)std::min<int64_t>(4 * c->num_sms, (cnt / 4 + 255) / 256 + 1);
@@ -1108,8 +1193,8 @@ moe_status forward_impl(moe_ctx* c, const void* tokens, int32_t T, const void* r
     StepTimer t2(c, kSlotExchange, st);
     const bool nccl = as_loopback(comm) == nullptr;
     if (nccl) NCCL_TRY(c, g_nccl.GroupStart());
-    if ((s = comm_allgather_inplace(c, out, (size_t)cnt, ncclBfloat16, 2, st))) return s;
-    if (of32 && (s = comm_allgather_inplace(c, of32, (size_t)cnt, ncclFloat32, 4, st))) return s;
+    if ((s = comm_allgather_inplace(c, tpc, out, (size_t)cnt, ncclBfloat16, 2, st))) return s;
+    if (of32 && (s = comm_allgather_inplace(c, tpc, of32, (size_t)cnt, ncclFloat32, 4, st))) return s;
     if (nccl) NCCL_TRY(c, g_nccl.GroupEnd());
     t2.done();
     return MOE_OK;
@@ -1124,7 +1209,8 @@ moe_status forward_impl(moe_ctx* c, const void* tokens, int32_t T, const void* r
 moe_status forward_ep(moe_ctx* c, const void* tokens, int32_t T, const void* router_w, void* out,
                       const moe_aux* aux, cudaStream_t st) {
     moe_status s;
-    const int G = c->G;
+    const int G = c->ep_world;
+    const CommRef epc = ep_comm(c);
     const int64_t cap = (int64_t)c->max_T * c->k;
     const int64_t R = cap * G;
     ncclComm_t comm = c->cfg.nccl_comm;
@@ -1149,21 +1235,21 @@ moe_status forward_ep(moe_ctx* c, const void* tokens, int32_t T, const void* rou
     const bool nccl = as_loopback(comm) == nullptr;
     if (exact) {
         if (T == 0) CUDA_TRY(c, cudaMemsetAsync(c->counts, 0, sizeof(int32_t) * G, st));
-        if ((s = comm_alltoall(c, c->counts, c->ep_rcounts, 1, ncclInt32, 4, st))) return s;
+        if ((s = comm_alltoall(c, epc, c->counts, c->ep_rcounts, 1, ncclInt32, 4, st))) return s;
         CUDA_TRY(c, cudaMemcpyAsync(c->h_counts, c->counts, sizeof(int32_t) * G, cudaMemcpyDeviceToHost, st));
         CUDA_TRY(c, cudaMemcpyAsync(c->h_counts + 64, c->ep_rcounts, sizeof(int32_t) * G, cudaMemcpyDeviceToHost, st));
         CUDA_TRY(c, cudaStreamSynchronize(st));
         CUDA_TRY(c, cudaMemsetAsync(c->ep_meta_recv, 0xFF, sizeof(int32_t) * R, st));
-        if ((s = comm_alltoallv(c, c->ep_meta_send, c->ep_meta_recv, c->h_counts, c->h_counts + 64, cap, 1, ncclInt32,
+        if ((s = comm_alltoallv(c, epc, c->ep_meta_send, c->ep_meta_recv, c->h_counts, c->h_counts + 64, cap, 1, ncclInt32,
                                 4, st)))
             return s;
-        if ((s = comm_alltoallv(c, c->ep_send, c->ep_recv, c->h_counts, c->h_counts + 64, cap, c->d, ncclBfloat16, 2,
+        if ((s = comm_alltoallv(c, epc, c->ep_send, c->ep_recv, c->h_counts, c->h_counts + 64, cap, c->d, ncclBfloat16, 2,
                                 st)))
             return s;
     } else {
         if (nccl) NCCL_TRY(c, g_nccl.GroupStart());
-        if ((s = comm_alltoall(c, c->ep_meta_send, c->ep_meta_recv, (size_t)cap, ncclInt32, 4, st))) return s;
-        if ((s = comm_alltoall(c, c->ep_send, c->ep_recv, (size_t)(cap * c->d), ncclBfloat16, 2, st))) return s;
+        if ((s = comm_alltoall(c, epc, c->ep_meta_send, c->ep_meta_recv, (size_t)cap, ncclInt32, 4, st))) return s;
+        if ((s = comm_alltoall(c, epc, c->ep_send, c->ep_recv, (size_t)(cap * c->d), ncclBfloat16, 2, st))) return s;
         if (nccl) NCCL_TRY(c, g_nccl.GroupEnd());
     }
     t1.done();
@@ -1192,11 +1278,25 @@ moe_status forward_ep(moe_ctx* c, const void* tokens, int32_t T, const void* rou
                     static_cast<const int32_t*>(c->ep_rpos), (int)R, c->d, c->ep_ysend)))
         return s;
     StepTimer t2(c, kSlotExchange, st);
+    if (c->tp_world > 1) {
+        // hybrid EP x TP: the rows' expert outputs are partial sums over this rank's
+        // ffn slice; the TP group (same experts, same received rows) sums them in fp32
+        const CommRef tpc = tp_comm(c);
+        if (exact) {
+            for (int p = 0; p < G; ++p)
+                if (c->h_counts[64 + p] > 0 &&
+                    (s = comm_allreduce_f32(c, tpc, c->ep_ysend + p * cap * c->d, (size_t)c->h_counts[64 + p] * c->d,
+                                            st)))
+                    return s;
+        } else if ((s = comm_allreduce_f32(c, tpc, c->ep_ysend, (size_t)(R * c->d), st))) {
+            return s;
+        }
+    }
     if (exact) {  // rows go back to where they came from: counts swap roles
-        if ((s = comm_alltoallv(c, c->ep_ysend, c->ep_yrecv, c->h_counts + 64, c->h_counts, cap, c->d, ncclFloat32, 4,
+        if ((s = comm_alltoallv(c, epc, c->ep_ysend, c->ep_yrecv, c->h_counts + 64, c->h_counts, cap, c->d, ncclFloat32, 4,
                                 st)))
             return s;
-    } else if ((s = comm_alltoall(c, c->ep_ysend, c->ep_yrecv, (size_t)(cap * c->d), ncclFloat32, 4, st))) {
+    } else if ((s = comm_alltoall(c, epc, c->ep_ysend, c->ep_yrecv, (size_t)(cap * c->d), ncclFloat32, 4, st))) {
         return s;
     }
     t2.done();

@@ -391,3 +391,91 @@ def test_stack_teacher_forced(moe, L, shape):
         assert err[~excl].max() <= 2e-2, (l, err.max())
         cur = outs[l]
     st.close()
+
+
+# ---------------------------------------------------------------- hybrid EP x TP
+def _run_hybrid(moe, inp, ep, tp, shards, flags=0, max_tokens=None):
+    """G = ep*tp ranks (threads) on one GPU; rank (e, t) = e*tp + t; EP groups =
+    ranks with the same t, TP groups = ranks with the same e; rank (e, t) gets the
+    token shard e."""
+    import threading
+    G = ep * tp
+    ep_groups = [moe.moe_loopback_comm_create(ep) for _ in range(tp)]
+    tp_groups = [moe.moe_loopback_comm_create(tp) for _ in range(ep)]
+    handles = []
+    blocks = []
+    mt = max_tokens or max(1, max(s.shape[0] for s in shards))
+    for e in range(ep):
+        for t in range(tp):
+            ce = moe.moe_loopback_comm_rank(ep_groups[t], e)
+            ct = moe.moe_loopback_comm_rank(tp_groups[e], t)
+            handles += [ce, ct]
+            blocks.append(moe.MoEBlock(inp["wg"], inp["w1"], inp["w3"], inp["w2"], top_k=2, max_tokens=mt,
+                                       par=moe.MOE_PAR_HYBRID, world_size=G, rank=e * tp + t, nccl_comm=ce,
+                                       tp_size=tp, tp_comm=ct, flags=flags))
+    torch.cuda.synchronize()
+    d = inp["wg"].shape[1]
+    res = [None] * G
+    errs = []
+
+    def work(r):
+        try:
+            st = torch.cuda.Stream()
+            x = shards[r // tp]
+            T = x.shape[0]
+            aux = {"topk_idx": torch.empty(max(T, 1), 2, dtype=torch.int32, device="cuda"),
+                   "out_f32": torch.empty(max(T, 1), d, dtype=torch.float32, device="cuda")}
+            out = torch.empty(max(T, 1), d, dtype=torch.bfloat16, device="cuda")
+            with torch.cuda.stream(st):
+                moe.moe_forward(blocks[r].ctx, x if T else out, T, blocks[r].router_w, blocks[r].w13, blocks[r].w2,
+                                out, aux, st)
+            st.synchronize()
+            res[r] = (out[:T].clone(), {n: v[:T].clone() for n, v in aux.items()})
+        except Exception as ex:  # pragma: no cover
+            errs.append((r, ex))
+
+    ths = [threading.Thread(target=work, args=(r,)) for r in range(G)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join(timeout=600)
+    for b in blocks:
+        b.close()
+    for h in handles:
+        moe.moe_loopback_comm_destroy(h)
+    for g in ep_groups + tp_groups:
+        moe.moe_loopback_comm_destroy(g)
+    assert not errs, errs
+    return res
+
+
+@pytest.mark.parametrize("ep,tp", [(2, 2), (2, 4), (4, 2), (1, 2), (2, 1)])
+@pytest.mark.parametrize("mode", ["capacity", "exact"])
+def test_hybrid_loopback(moe, ep, tp, mode):
+    shape = synth.MoEShape(T=72, d=256, f=1024, E=8, k=2)
+    inp = _inputs(shape, 70 + ep * 10 + tp)
+    host = to_host_inputs(inp)
+    cuts = np.linspace(0, shape.T, ep + 1).astype(int)
+    shards = [inp["x"][cuts[e]:cuts[e + 1]] for e in range(ep)]
+    res = _run_hybrid(moe, inp, ep, tp, shards, flags=moe.MOE_FLAG_EP_EXACT if mode == "exact" else 0,
+                      max_tokens=shape.T)
+    for e in range(ep):
+        for t in range(1, tp):
+            assert torch.equal(res[e * tp + t][0].view(torch.int16), res[e * tp][0].view(torch.int16))
+    outs = [res[e * tp][0] for e in range(ep)]
+    auxs = [res[e * tp][1] for e in range(ep)]
+    _check_group_outputs(host, 2, host["x"], outs, auxs)
+
+
+@pytest.mark.parametrize("ep,tp", [(2, 4), (4, 2)])
+def test_mixtral_decode_hybrid(moe, mixtral_weights, ep, tp):
+    """The paper's Exp4 hybrids (EP2xTP4, EP4xTP2) at Mixtral size, 64-token decode."""
+    w, host = mixtral_weights
+    x = synth.make_tokens(64, 4096, seed=301, device="cuda")
+    per = 64 // ep
+    shards = [x[per * e:per * (e + 1)] for e in range(ep)]
+    res = _run_hybrid(moe, w, ep, tp, shards, max_tokens=per)
+    outs = [res[e * tp][0] for e in range(ep)]
+    auxs = [res[e * tp][1] for e in range(ep)]
+    e32, e16 = _check_group_outputs(host, 2, synth.bf16_bits(x), outs, auxs)
+    print(f"EP{ep}xTP{tp}", e32, e16)
