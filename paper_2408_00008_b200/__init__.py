@@ -19,7 +19,8 @@ import os
 import torch
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libmoe.so")
+# MOE_LIB selects an experiment build of the same sources (scripts/ab_*.sh); default in-tree
+LIB_PATH = os.environ.get("MOE_LIB") or os.path.join(_PKG, "libmoe.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"libmoe.so not built at {LIB_PATH}: run `python -c 'import __graft_entry__ as g; g.build()'`")

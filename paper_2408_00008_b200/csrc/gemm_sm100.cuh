@@ -178,9 +178,20 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         ptx::tmem_alloc(tmem_base_slot, 2 * C::kAccCols);
         ptx::tmem_relinquish();
     }
-    // Everything above overlaps the previous kernel's tail (PDL); from here on we
-    // read its outputs (counts / offsets / permuted rows).
-    ptx::pdl_wait();
+// MOE_PDL_PREFETCH=0 disables the pre-wait weight stages (A/B experiments, scripts/ab_decode.sh:
+// r01 decode 0.4543 ms without, 0.4522 ms with; an extra L2 prefetch of the next stages measured
+// worse, 0.4596 ms, and was dropped).
+#ifndef MOE_PDL_PREFETCH
+#define MOE_PDL_PREFETCH 1
+#endif
+    // Everything above overlaps the previous kernel's tail (PDL). The tiled kinds
+    // wait here for the previous kernel's outputs. The swap (decode) kinds only read
+    // the routing counts before waiting -- they come from the router, which has
+    // completed by the time this grid can start (the permute kernel triggers its
+    // dependents after its own griddepcontrol.wait, and the w1/w3 GEMM after its
+    // wait) -- and their producer issues the first weight stages before waiting for
+    // the permuted tokens / activations of the previous kernel.
+    if (!C::kSwap || MOE_PDL_PREFETCH == 0) ptx::pdl_wait();
     if (threadIdx.x < 32) {
         for (int e = threadIdx.x; e < p.E; e += 32) {
             s_counts[e] = p.counts[e];
@@ -200,15 +211,36 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
+            int pre = 0;  // k-blocks of the first tile whose weight loads precede the wait
+            if (C::kSwap && MOE_PDL_PREFETCH > 0) {
+                if ((int)blockIdx.x < total) {
+                    TileInfo t0;
+                    decode_tile<KIND, NB>(blockIdx.x, p, s_counts, s_offsets, t0);
+                    pre = min(S, t0.nkb);
+                    for (int kb = 0; kb < pre; ++kb) {  // fresh stages: no empty-wait needed
+                        ptx::mbar_arrive_expect_tx(&full[kb], C::kStageBytes);
+                        ptx::tma_load_3d(&tmA, &full[kb], smem_a + kb * C::kABytes, (t0.kb0 + kb) * kBK, t0.a_row,
+                                         t0.e, ptx::kEvictFirst);
+                    }
+                }
+                ptx::pdl_wait();
+            }
+            bool first = true;
             for (int t = blockIdx.x; t < total; t += gridDim.x) {
                 TileInfo ti;
                 decode_tile<KIND, NB>(t, p, s_counts, s_offsets, ti);
                 for (int kb = 0; kb < ti.nkb; ++kb) {
-                    ptx::mbar_wait(&empty[stage], phase ^ 1);
-                    ptx::mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
                     const int kc = (ti.kb0 + kb) * kBK;
                     uint8_t* sa = smem_a + stage * C::kABytes;
                     uint8_t* sb = smem_b + stage * C::kBBytes;
+                    if (first && kb < pre) {
+                        // weights already in flight on this armed stage: add the token operand
+                        ptx::tma_load_2d(&tmB, &full[stage], sb, kc, ti.b_row, ptx::kEvictLast);
+                        if (++stage == S) { stage = 0; phase ^= 1; }
+                        continue;
+                    }
+                    ptx::mbar_wait(&empty[stage], phase ^ 1);
+                    ptx::mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
                     if (C::kSwap) {
                         // A = weights (3D map [K, rows, E]) streamed once: evict-first.
                         ptx::tma_load_3d(&tmA, &full[stage], sa, kc, ti.a_row, ti.e, ptx::kEvictFirst);
@@ -220,6 +252,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                     }
                     if (++stage == S) { stage = 0; phase ^= 1; }
                 }
+                first = false;
             }
         }
     } else if (warp == 1) {
