@@ -38,8 +38,10 @@ def build(force: bool = False) -> str:
 def _load():
     global _lib
     if _lib is None:
-        build()
-        lib = ctypes.CDLL(_LIB_PATH)
+        override = os.environ.get("ORACLE_LIB")  # tests/test_oracle_mutations.py: a mutated build
+        if not override:
+            build()
+        lib = ctypes.CDLL(override or _LIB_PATH)
         P = ctypes.c_void_p
         I, L = ctypes.c_int, ctypes.c_int64
         lib.oracle_router.argtypes = [I, P, P, L, I, I, I, P, P, P, P, P]
