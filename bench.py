@@ -77,6 +77,9 @@ def parse():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--flags", type=lambda v: int(v, 0), default=0,
                     help="extra MOE_FLAG_* bits (experiments: 0x2 force swap-AB GEMMs, 0x4 force tiled, 0x10 no CTA pairs)")
+    ap.add_argument("--fp8", action="store_true",
+                    help="FP8 E4M3 expert weights with per-row power-of-two scales (SURVEY 8(f) NEXT #2); "
+                         "not the BASELINE bf16 headline")
     ap.add_argument("--graph", action="store_true",
                     help="headline pass as CUDA-graph replays of the forward (single GPU; default: eager launches)")
     ap.add_argument("--par", default=None, choices=["ep", "tp", "hybrid", "none"],
@@ -169,14 +172,17 @@ def dist_setup(args):
     return world, rank, local
 
 
-def algorithmic(T, d, f, E, k, counts):
+def algorithmic(T, d, f, E, k, counts, wbytes=2):
     """SURVEY.md Sec. 8(d) work formulas for one forward on one rank, from the actual
     routing: T = tokens routed on this rank, f = ffn columns held by this rank,
     counts = rows of each LOCAL expert (their sum = A assignments computed here)."""
     touched = int(sum(1 for c in counts if c > 0))
     A = int(sum(counts))
-    b_w13 = touched * 2 * f * d * 2                 # w1+w3 of touched experts (bf16)
-    b_w2 = touched * d * f * 2
+    b_w13 = touched * 2 * f * d * wbytes            # w1+w3 of touched experts (bf16: 2 B, fp8: 1 B)
+    b_w2 = touched * d * f * wbytes
+    if wbytes == 1:                                 # + fp32 per-row scales
+        b_w13 += touched * 2 * f * 4
+        b_w2 += touched * d * 4
     bytes_total = b_w13 + b_w2 + E * d * 2 + 2 * T * d * 2
     flops_total = 2 * A * 3 * d * f + 2 * T * d * E
     # per-kernel algorithmic traffic (DESIGN.md "Kernels")
@@ -399,9 +405,14 @@ def main():
     w = synth.make_weights(d, f, E, seed=args.seed, device=dev)
     nbuf = 4  # distinct token batches cycled through the steps
     xs = [synth.make_tokens(Tg, d, seed=args.seed + 1 + i, device=dev)[shard * T:(shard + 1) * T] for i in range(nbuf)]
+    flags = args.flags
+    if args.fp8:
+        flags |= moe.MOE_FLAG_FP8_WEIGHTS
+        for n in ("w1", "w3", "w2"):
+            w[n] = synth.quantize_fp8_rows(w[n])
     blk = moe.MoEBlock(w["wg"], w["w1"], w["w3"], w["w2"], top_k=k, max_tokens=T, par=pmap[par],
                        world_size=world if par != "none" else 1, rank=rank if par != "none" else 0, nccl_comm=comm,
-                       flags=args.flags, tp_size=tp_size, tp_comm=tp_comm)
+                       flags=flags, tp_size=tp_size, tp_comm=tp_comm)
     del w["w1"], w["w3"], w["w2"]
     torch.cuda.empty_cache()
     out = torch.empty(T, d, dtype=torch.bfloat16, device=dev)
@@ -411,7 +422,7 @@ def main():
     stream = torch.cuda.current_stream()
 
     def step(i, aux=None):
-        moe.moe_forward(blk.ctx, xs[i % nbuf], T, blk.router_w, blk.w13, blk.w2, out, aux, stream)
+        moe.moe_forward(blk.ctx, xs[i % nbuf], T, blk.router_w, blk.w13, blk.w2, out, aux, stream, blk.s13, blk.s2)
 
     for i in range(max(3, args.warmup)):
         step(i)
@@ -453,7 +464,7 @@ def main():
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g):
                 moe.moe_forward(blk.ctx, xs[i], T, blk.router_w, blk.w13, blk.w2, out, None,
-                                torch.cuda.current_stream())
+                                torch.cuda.current_stream(), blk.s13, blk.s2)
             graphs.append(g)
         for i in range(2 * nbuf):
             graphs[i % nbuf].replay()
@@ -481,13 +492,13 @@ def main():
     xh = [x.cpu().pin_memory() for x in xs]
     oh = torch.empty(T, d, dtype=torch.bfloat16).pin_memory()
     for i in range(3):
-        moe.moe_forward_host(blk.ctx, xh[i % nbuf], T, blk.router_w, blk.w13, blk.w2, oh, stream)
+        moe.moe_forward_host(blk.ctx, xh[i % nbuf], T, blk.router_w, blk.w13, blk.w2, oh, stream, blk.s13, blk.s2)
     torch.cuda.synchronize()
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for i in range(args.steps):
-        moe.moe_forward_host(blk.ctx, xh[i % nbuf], T, blk.router_w, blk.w13, blk.w2, oh, stream)
+        moe.moe_forward_host(blk.ctx, xh[i % nbuf], T, blk.router_w, blk.w13, blk.w2, oh, stream, blk.s13, blk.s2)
     e1.record(stream)
     torch.cuda.synchronize()
     barrier()
@@ -502,7 +513,7 @@ def main():
     aux = {"expert_counts": counts}
     step(0, aux)
     torch.cuda.synchronize()
-    alg = algorithmic(T, d, f_local, E, k, counts.cpu().tolist())
+    alg = algorithmic(T, d, f_local, E, k, counts.cpu().tolist(), wbytes=1 if args.fp8 else 2)
     peaks = load_peaks()
     per = {name: (v[0] / v[1] if v[1] else 0.0) for name, v in ktimes.items()}
     decode = args.config == "decode"
@@ -521,7 +532,7 @@ def main():
                 "traffic": None, "kernel": "moe_gemm_kernel<kG1Tiled> (w1/w3 + SwiGLU)",
                 "peak_src": peaks["src"] + " (MEASURED_PEAKS.json bf16_tflops_sustained)"}
         step_frac = alg["flops"] / (ms * 1e-3) / 1e12 / pk
-    tr, tr_src = load_traffic(args.config) if world == 1 and par == "none" else (None, None)
+    tr, tr_src = load_traffic(args.config) if world == 1 and par == "none" and not args.fp8 else (None, None)
     roof["traffic"] = tr
     if tr is not None:
         roof["traffic_src"] = tr_src
@@ -533,7 +544,8 @@ def main():
         "metric": METRIC,
         "value": tok_s, "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": max(3, args.warmup),
         "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "strong" if par in ("ep", "tp", "hybrid") else "weak", "vs_baseline": None, "dtype": "bf16",
+        "scaling": "strong" if par in ("ep", "tp", "hybrid") else "weak", "vs_baseline": None,
+        "dtype": "fp8-e4m3 weights (per-row pow2 scales), fp16 GEMM activations, bf16 in/out" if args.fp8 else "bf16",
         "data": "synthetic (seeded Gaussian tokens, random-init Mixtral-shaped weights; DESIGN.md input recipe)",
         "config": workload_config(args, world)[2],
         "roofline": roof,

@@ -89,6 +89,9 @@ typedef enum {
 #define MOE_FLAG_FORCE_TILED 0x4u /* always use the prefill (tokens-as-M) GEMMs          */
 #define MOE_FLAG_NO_PDL      0x8u /* disable programmatic dependent launch               */
 #define MOE_FLAG_NO_PAIR     0x10u /* prefill GEMMs on single CTAs (M=128) instead of CTA pairs (M=256) */
+#define MOE_FLAG_FP8_WEIGHTS 0x40u /* expert weights are FP8 E4M3 with per-row power-of-two scales
+                                      (moe_pack_weights_fp8); tokens / activations on the GEMMs are
+                                      fp16; decode (swap-AB) GEMMs at any T */
 #define MOE_FLAG_EP_EXACT    0x20u /* EP: always exchange exact row counts (one host sync per forward);
                                       default: exact only when a fixed-capacity exchange would move
                                       more than 32 MB, i.e. prefill-sized batches                  */
@@ -120,6 +123,8 @@ typedef struct {
 typedef struct {
     const void* w13;
     const void* w2;
+    const float* w13_scale; /* MOE_FLAG_FP8_WEIGHTS: [E_local, 2*f_local] fp32, packed row order */
+    const float* w2_scale;  /* MOE_FLAG_FP8_WEIGHTS: [E_local, d] fp32; both NULL for bf16     */
 } moe_expert_weights;
 
 /* Optional debug / parity outputs (any pointer may be NULL). Device memory,
@@ -158,6 +163,18 @@ MOE_API moe_status moe_packed_sizes(const moe_config* cfg, size_t* w13_bytes, si
  * w13_out / w2_out must hold moe_packed_sizes bytes. Enqueued on stream. */
 MOE_API moe_status moe_pack_weights(moe_ctx* ctx, const void* w1, const void* w3, const void* w2,
                             void* w13_out, void* w2_out, void* stream);
+
+/* FP8 weights ("applying quantization techniques using ... 8-bit (fp8)").
+ * q1, q3 [E, f, d] and q2 [E, d, f] are FP8 E4M3 bytes (HF layout, FULL model);
+ * s1, s3 [E, f] and s2 [E, d] are fp32 per-output-row scales, each a power of two,
+ * so that w = q * s exactly (the caller quantises; the library never rounds a
+ * weight). Packs this rank's share like moe_pack_weights, plus the scales. The
+ * context must have MOE_FLAG_FP8_WEIGHTS. Sizes from moe_packed_sizes_fp8.     */
+MOE_API moe_status moe_packed_sizes_fp8(const moe_config* cfg, size_t* w13_bytes, size_t* w2_bytes,
+                                        size_t* w13_scale_bytes, size_t* w2_scale_bytes);
+MOE_API moe_status moe_pack_weights_fp8(moe_ctx* ctx, const void* q1, const void* q3, const void* q2,
+                                        const float* s1, const float* s3, const float* s2, void* w13_out,
+                                        void* w2_out, float* w13_scale_out, float* w2_scale_out, void* stream);
 
 /* The block forward. tokens [T, d] bf16, router_w [E, d] bf16 (full, replicated
  * on every rank), out [T, d] bf16. 0 <= T <= max_tokens. T == 0 enqueues nothing

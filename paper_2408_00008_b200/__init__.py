@@ -31,6 +31,7 @@ MOE_OK, MOE_ERR_INVALID, MOE_ERR_UNSUPPORTED, MOE_ERR_OOM, MOE_ERR_CUDA, MOE_ERR
 MOE_PAR_NONE, MOE_PAR_EP, MOE_PAR_TP, MOE_PAR_HYBRID = 0, 1, 2, 3
 MOE_FLAG_RESIDUAL, MOE_FLAG_FORCE_SWAP, MOE_FLAG_FORCE_TILED, MOE_FLAG_NO_PDL, MOE_FLAG_NO_PAIR = 0x1, 0x2, 0x4, 0x8, 0x10
 MOE_FLAG_EP_EXACT = 0x20
+MOE_FLAG_FP8_WEIGHTS = 0x40
 NUM_KERNEL_SLOTS = 8
 KERNEL_SLOTS = ("router", "permute", "gemm1_w13_swiglu", "gemm2_w2", "combine", "dispatch", "exchange", "pack")
 
@@ -39,7 +40,7 @@ EXPORTED = ("moe_init", "moe_packed_sizes", "moe_pack_weights", "moe_forward", "
             "moe_forward_host", "moe_destroy", "moe_last_error", "moe_status_string", "moe_set_profiling",
             "moe_reset_profile", "moe_kernel_times", "moe_launch_count", "moe_nccl_unique_id",
             "moe_nccl_comm_init", "moe_nccl_comm_destroy", "moe_loopback_comm_create", "moe_loopback_comm_rank",
-            "moe_loopback_comm_destroy")
+            "moe_loopback_comm_destroy", "moe_packed_sizes_fp8", "moe_pack_weights_fp8")
 
 
 class moe_config(ctypes.Structure):
@@ -51,7 +52,8 @@ class moe_config(ctypes.Structure):
 
 
 class moe_expert_weights(ctypes.Structure):
-    _fields_ = [("w13", ctypes.c_void_p), ("w2", ctypes.c_void_p)]
+    _fields_ = [("w13", ctypes.c_void_p), ("w2", ctypes.c_void_p), ("w13_scale", ctypes.c_void_p),
+                ("w2_scale", ctypes.c_void_p)]
 
 
 class moe_aux(ctypes.Structure):
@@ -81,6 +83,8 @@ _sig = {
     "moe_nccl_comm_init": ([_P, _I32, _I32, _I32, ctypes.POINTER(_P)], _I32),
     "moe_nccl_comm_destroy": ([_P], _I32),
     "moe_loopback_comm_create": ([_I32, ctypes.POINTER(_P)], _I32),
+    "moe_packed_sizes_fp8": ([ctypes.POINTER(moe_config)] + [ctypes.POINTER(ctypes.c_size_t)] * 4, _I32),
+    "moe_pack_weights_fp8": ([_P] * 12, _I32),
     "moe_loopback_comm_rank": ([_P, _I32, ctypes.POINTER(_P)], _I32),
     "moe_loopback_comm_destroy": ([_P], _I32),
 }
@@ -154,13 +158,24 @@ def _aux(aux):
     return ctypes.byref(a)
 
 
-def _weights(w13, w2):
-    return ctypes.byref(moe_expert_weights(_ptr(w13), _ptr(w2)))
+def _weights(w13, w2, w13_scale=None, w2_scale=None):
+    return ctypes.byref(moe_expert_weights(_ptr(w13), _ptr(w2), _ptr(w13_scale), _ptr(w2_scale)))
 
 
-def moe_forward(ctx, tokens, T, router_w, w13, w2, out, aux=None, stream=None):
-    _check(_lib.moe_forward(ctx, _ptr(tokens), int(T), _ptr(router_w), _weights(w13, w2), _ptr(out), _aux(aux),
-                            _stream(stream)), ctx)
+def moe_forward(ctx, tokens, T, router_w, w13, w2, out, aux=None, stream=None, w13_scale=None, w2_scale=None):
+    _check(_lib.moe_forward(ctx, _ptr(tokens), int(T), _ptr(router_w), _weights(w13, w2, w13_scale, w2_scale),
+                            _ptr(out), _aux(aux), _stream(stream)), ctx)
+
+
+def moe_packed_sizes_fp8(cfg: moe_config):
+    v = [ctypes.c_size_t() for _ in range(4)]
+    _check(_lib.moe_packed_sizes_fp8(ctypes.byref(cfg), *[ctypes.byref(x) for x in v]))
+    return tuple(x.value for x in v)
+
+
+def moe_pack_weights_fp8(ctx, q1, q3, q2, s1, s3, s2, w13_out, w2_out, s13_out, s2_out, stream=None):
+    _check(_lib.moe_pack_weights_fp8(ctx, *[_ptr(t) for t in (q1, q3, q2, s1, s3, s2, w13_out, w2_out, s13_out,
+                                                               s2_out)], _stream(stream)), ctx)
 
 
 def moe_forward_routed(ctx, tokens, T, topk_idx, topk_w, w13, w2, out, aux=None, stream=None):
@@ -168,9 +183,9 @@ def moe_forward_routed(ctx, tokens, T, topk_idx, topk_w, w13, w2, out, aux=None,
                                    _ptr(out), _aux(aux), _stream(stream)), ctx)
 
 
-def moe_forward_host(ctx, tokens_host, T, router_w, w13, w2, out_host, stream=None):
-    _check(_lib.moe_forward_host(ctx, _ptr(tokens_host), int(T), _ptr(router_w), _weights(w13, w2),
-                                 _ptr(out_host), _stream(stream)), ctx)
+def moe_forward_host(ctx, tokens_host, T, router_w, w13, w2, out_host, stream=None, w13_scale=None, w2_scale=None):
+    _check(_lib.moe_forward_host(ctx, _ptr(tokens_host), int(T), _ptr(router_w),
+                                 _weights(w13, w2, w13_scale, w2_scale), _ptr(out_host), _stream(stream)), ctx)
 
 
 def moe_destroy(ctx):
@@ -267,29 +282,46 @@ class MoEBlock:
 
     def __init__(self, router_w, w1, w3, w2, top_k=2, max_tokens=64, par=MOE_PAR_NONE, world_size=1, rank=0,
                  nccl_comm=None, flags=0, split_k=0, device=None, tp_size=0, tp_comm=None):
+        """FP8 weights: pass flags |= MOE_FLAG_FP8_WEIGHTS and w1/w3/w2 as (q, scale) pairs
+        (synth.quantize_fp8_rows)."""
         dev = router_w.device if device is None else torch.device(device)
-        E, f, d = w1.shape
+        w1_fp8 = (w1, w3, w2) if flags & MOE_FLAG_FP8_WEIGHTS else None
+        E, f, d = (w1[0] if w1_fp8 else w1).shape
         self.cfg = make_config(d, f, E, top_k, max_tokens, par, world_size, rank, nccl_comm, flags, split_k,
                                dev.index if dev.index is not None else torch.cuda.current_device(), tp_size, tp_comm)
         self.ctx = moe_init(self.cfg)
         self.d, self.f, self.E, self.k = d, f, E, top_k
-        b13, b2 = moe_packed_sizes(self.cfg)
-        self.w13 = torch.empty(b13 // 2, dtype=torch.bfloat16, device=dev)
-        self.w2 = torch.empty(b2 // 2, dtype=torch.bfloat16, device=dev)
         self.router_w = router_w.contiguous()
-        moe_pack_weights(self.ctx, w1.contiguous(), w3.contiguous(), w2.contiguous(), self.w13, self.w2)
+        self.s13 = self.s2 = None
+        if flags & MOE_FLAG_FP8_WEIGHTS:
+            # w1, w3, w2 are (q uint8 E4M3 bytes, s fp32 per-row power-of-two scale) pairs
+            (q1, s1), (q3, s3), (q2, s2) = w1_fp8
+            b13, b2, bs13, bs2 = moe_packed_sizes_fp8(self.cfg)
+            self.w13 = torch.empty(b13, dtype=torch.uint8, device=dev)
+            self.w2 = torch.empty(b2, dtype=torch.uint8, device=dev)
+            self.s13 = torch.empty(bs13 // 4, dtype=torch.float32, device=dev)
+            self.s2 = torch.empty(bs2 // 4, dtype=torch.float32, device=dev)
+            moe_pack_weights_fp8(self.ctx, q1.contiguous(), q3.contiguous(), q2.contiguous(), s1.contiguous(),
+                                 s3.contiguous(), s2.contiguous(), self.w13, self.w2, self.s13, self.s2)
+        else:
+            b13, b2 = moe_packed_sizes(self.cfg)
+            self.w13 = torch.empty(b13 // 2, dtype=torch.bfloat16, device=dev)
+            self.w2 = torch.empty(b2 // 2, dtype=torch.bfloat16, device=dev)
+            moe_pack_weights(self.ctx, w1.contiguous(), w3.contiguous(), w2.contiguous(), self.w13, self.w2)
 
     def forward(self, x, out=None, aux=None, stream=None):
         T = x.shape[0]
         if out is None:
             out = torch.empty_like(x)
-        moe_forward(self.ctx, x, T, self.router_w, self.w13, self.w2, out, aux, stream)
+        moe_forward(self.ctx, x, T, self.router_w, self.w13, self.w2, out, aux, stream, self.s13, self.s2)
         return out
 
     def forward_routed(self, x, topk_idx, topk_w, out=None, aux=None, stream=None):
         if out is None:
             out = torch.empty_like(x)
-        moe_forward_routed(self.ctx, x, x.shape[0], topk_idx, topk_w, self.w13, self.w2, out, aux, stream)
+        _check(_lib.moe_forward_routed(self.ctx, _ptr(x), int(x.shape[0]), _ptr(topk_idx), _ptr(topk_w),
+                                       _weights(self.w13, self.w2, self.s13, self.s2), _ptr(out), _aux(aux),
+                                       _stream(stream)), self.ctx)
         return out
 
     def close(self):

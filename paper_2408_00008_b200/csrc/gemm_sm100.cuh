@@ -25,6 +25,7 @@
 
 #include "sm100.cuh"
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 
 namespace moe {
 
@@ -88,7 +89,7 @@ __device__ __forceinline__ int tiles_of(int n_e, const GemmParams& p) {
     return ((n_e + NB - 1) / NB) * ((p.d + 127) / 128) * p.splits;  // kG2Swap
 }
 
-template <int KIND, int NB>
+template <int KIND, int NB, int KBLK = kBK>
 __device__ __forceinline__ bool decode_tile(int t, const GemmParams& p, const int32_t* s_counts,
                                             const int32_t* s_offsets, TileInfo& ti) {
     int e = 0;
@@ -109,7 +110,7 @@ __device__ __forceinline__ bool decode_tile(int t, const GemmParams& p, const in
         ti.a_row = ti.seg + ti.m_idx * 128;
         ti.b_row = ti.n_idx * 256;
         ti.kb0 = 0;
-        ti.nkb = (KIND == kG1Tiled ? p.d : p.f) / kBK;
+        ti.nkb = (KIND == kG1Tiled ? p.d : p.f) / KBLK;
         ti.n_valid = 0;
     } else {
         int nt = (ti.rows + NB - 1) / NB;
@@ -120,7 +121,7 @@ __device__ __forceinline__ bool decode_tile(int t, const GemmParams& p, const in
         ti.split = rest / wt;
         ti.a_row = ti.m_idx * (KIND == kG1Swap ? 256 : 128);
         ti.b_row = ti.seg + ti.n_idx * NB;
-        int nkb_all = (KIND == kG1Swap ? p.d : p.f) / kBK;
+        int nkb_all = (KIND == kG1Swap ? p.d : p.f) / KBLK;
         int S = (KIND == kG2Swap) ? p.splits : 1;
         ti.kb0 = (nkb_all * ti.split) / S;
         ti.nkb = (nkb_all * (ti.split + 1)) / S - ti.kb0;
@@ -269,7 +270,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 if (KIND == kG1Tiled) n_mma = 256;
                 else if (KIND == kG2Tiled) n_mma = min(256, p.d - ti.n_idx * 256);
                 else n_mma = (uint32_t)((ti.n_valid + 15) / 16 * 16);
-                const uint32_t idesc = ptx::make_idesc_bf16(128, n_mma);
+                uint32_t idesc = ptx::make_idesc_bf16(128, n_mma);
+#if defined(MOE_EXP_A_F16)
+                if (C::kSwap) idesc &= ~(7u << 7);  // experiment: A operand read as fp16 (B stays bf16)
+#endif
                 const uint32_t d_tmem = tmem_base + acc * C::kAccCols;
                 ptx::mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
                 ptx::tc_fence_after();
@@ -650,6 +654,550 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     if (warp == 1) {
         ptx::tc_fence_after();
         ptx::tmem_dealloc_pair(tmem_base, 512);
+    }
+}
+
+// ============================================================================
+// FP8-weight decode GEMMs ("8-bit (fp8) floating point").
+// Expert weights are E4M3 with one power-of-two scale per output row; tokens and
+// activations are fp16. tcgen05 kind::f16 needs A and B of the same 16-bit type
+// (a bf16 x fp16 descriptor traps), so the weight tile is widened in shared memory:
+//   TMA (fp8 box, 64-byte swizzle) -> converter warps (cvt.rn.f16x2.e4m3x2, exact)
+//   -> fp16 tile in the 128-byte-swizzled K-major layout -> tcgen05.mma (fp32 acc)
+// and the epilogue multiplies by the row scale (a power of two: exact). HBM sees one
+// byte per weight, so the weight stream -- the decode roofline -- halves.
+// Two rings: the load ring (fp8 A + fp16 B, deep, keeps HBM busy) and the fp16 ring
+// (shallow). Warps: 0 TMA, 1 MMA + TMEM, 2..5 epilogue, 6..9 converters.
+constexpr int kFp8Threads = 320;
+
+template <int KIND, int NB>
+struct Fp8Cfg {
+    static_assert(KIND == kG1Swap || KIND == kG2Swap, "fp8 weights: decode (swap-AB) GEMMs only");
+    static constexpr int kARows = KIND == kG1Swap ? 256 : 128;
+    static constexpr int kA8Bytes = kARows * 64;    // fp8 rows x 64 B (one 64-element K block)
+    static constexpr int kA16Bytes = kARows * 128;  // fp16 rows x 128 B
+    static constexpr int kBBytes = NB * 128;        // fp16 tokens
+    static constexpr int kS2 = KIND == kG1Swap ? 2 : 3;
+    static constexpr int kLoadBytes = kA8Bytes + kBBytes;
+    static constexpr int kS1Raw = (kSmemBudget - 2048 - kS2 * kA16Bytes) / kLoadBytes;
+    static constexpr int kS1 = kS1Raw > 8 ? 8 : kS1Raw;
+    static constexpr int kSmemBytes = kS1 * kLoadBytes + kS2 * kA16Bytes + 2048;
+    static_assert(kS1 >= 3, "fp8 load ring too shallow");
+};
+
+__device__ __forceinline__ uint32_t cvt_e4m3x2_f16x2(uint32_t two_fp8) {
+    uint32_t r;
+    const uint16_t v = static_cast<uint16_t>(two_fp8);
+    asm("cvt.rn.f16x2.e4m3x2 %0, %1;" : "=r"(r) : "h"(v));
+    return r;
+}
+
+__device__ __forceinline__ uint32_t pack_f16x2(float lo, float hi) {
+    __half2 v = __floats2half2_rn(lo, hi);
+    return *reinterpret_cast<uint32_t*>(&v);
+}
+
+// scales: kG1Swap -> per packed w13 row [E][2f]; kG2Swap -> per w2 row [E][d]
+template <int KIND, int NB>
+__global__ void __launch_bounds__(kFp8Threads, 1)
+    moe_gemm_fp8_kernel(const GemmParams p, const float* __restrict__ scales,
+                        const __grid_constant__ CUtensorMap tmA8, const __grid_constant__ CUtensorMap tmB) {
+    using C = Fp8Cfg<KIND, NB>;
+    constexpr int S1 = C::kS1, S2 = C::kS2;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* ring16 = smem;                              // S2 x fp16 A tiles (1024-aligned)
+    uint8_t* ring_b = ring16 + S2 * C::kA16Bytes;        // S1 x fp16 B tiles (1024-aligned: NB*128)
+    uint8_t* ring8 = ring_b + S1 * C::kBBytes;           // S1 x fp8 A tiles (512-aligned)
+    uint64_t* bars = reinterpret_cast<uint64_t*>(ring8 + S1 * C::kA8Bytes);
+    uint64_t* full1 = bars;                 // TMA -> converters (fp8 A + B bytes)
+    uint64_t* empty1 = bars + S1;           // converters (4) + MMA commit (1) -> TMA
+    uint64_t* full2 = bars + 2 * S1;        // converters (4 warps) -> MMA
+    uint64_t* empty2 = full2 + S2;          // MMA commit -> converters
+    uint64_t* tmem_full = empty2 + S2;
+    uint64_t* tmem_empty = tmem_full + 2;
+    uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+    int32_t* s_counts = reinterpret_cast<int32_t*>(tmem_empty + 3);
+    int32_t* s_offsets = s_counts + 32;
+
+    const int warp = threadIdx.x / 32;
+    const int lane = threadIdx.x % 32;
+    if (warp == 0 && lane == 0) {
+        ptx::prefetch_tmap(&tmA8);
+        ptx::prefetch_tmap(&tmB);
+        for (int i = 0; i < S1; ++i) {
+            ptx::mbar_init(&full1[i], 1);
+            ptx::mbar_init(&empty1[i], 5);
+        }
+        for (int i = 0; i < S2; ++i) {
+            ptx::mbar_init(&full2[i], 4);
+            ptx::mbar_init(&empty2[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            ptx::mbar_init(&tmem_full[i], 1);
+            ptx::mbar_init(&tmem_empty[i], 4);
+        }
+        ptx::fence_mbar_init();
+    }
+    if (warp == 1) {
+        ptx::tmem_alloc(tmem_base_slot, 512);
+        ptx::tmem_relinquish();
+    }
+    ptx::pdl_wait();
+    if (threadIdx.x < 32)
+        for (int e = threadIdx.x; e < p.E; e += 32) {
+            s_counts[e] = p.counts[e];
+            s_offsets[e] = p.offsets[e];
+        }
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = *tmem_base_slot;
+    int total = 0;
+    for (int e = 0; e < p.E; ++e) total += tiles_of<KIND, NB>(s_counts[e], p);
+
+    if (warp == 0) {
+        // ---------------------------------------------------------------- TMA producer
+        if (lane == 0) {
+            int st = 0;
+            uint32_t ph = 0;
+            for (int t = blockIdx.x; t < total; t += gridDim.x) {
+                TileInfo ti;
+                decode_tile<KIND, NB>(t, p, s_counts, s_offsets, ti);
+                for (int kb = 0; kb < ti.nkb; ++kb) {
+                    ptx::mbar_wait(&empty1[st], ph ^ 1);
+                    ptx::mbar_arrive_expect_tx(&full1[st], C::kLoadBytes);
+                    const int kc = (ti.kb0 + kb) * kBK;
+                    ptx::tma_load_3d(&tmA8, &full1[st], ring8 + st * C::kA8Bytes, kc, ti.a_row, ti.e,
+                                     ptx::kEvictFirst);
+                    ptx::tma_load_2d(&tmB, &full1[st], ring_b + st * C::kBBytes, kc, ti.b_row, ptx::kEvictLast);
+                    if (++st == S1) { st = 0; ph ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------------------------------------------------------- MMA issuer
+        if (lane == 0) {
+            int s1 = 0, s2 = 0;
+            uint32_t ph1 = 0, ph2 = 0;
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            for (int t = blockIdx.x; t < total; t += gridDim.x) {
+                TileInfo ti;
+                decode_tile<KIND, NB>(t, p, s_counts, s_offsets, ti);
+                const uint32_t n_mma = (uint32_t)((ti.n_valid + 15) / 16 * 16);
+                const uint32_t idesc = (1u << 4) | ((n_mma >> 3) << 17) | ((128u >> 4) << 24);  // f16 x f16 -> f32
+                const uint32_t d_tmem = tmem_base + acc * 256;
+                ptx::mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
+                ptx::tc_fence_after();
+                for (int kb = 0; kb < ti.nkb; ++kb) {
+                    ptx::mbar_wait(&full2[s2], ph2);
+                    ptx::tc_fence_after();
+                    const uint32_t sa = ptx::smem_u32(ring16 + s2 * C::kA16Bytes);
+                    const uint64_t adesc = ptx::make_smem_desc_sw128(sa);
+                    const uint64_t bdesc = ptx::make_smem_desc_sw128(ptx::smem_u32(ring_b + s1 * C::kBBytes));
+#pragma unroll
+                    for (int kk = 0; kk < kBK / 16; ++kk) {
+                        const uint32_t accum = (kb | kk) ? 1u : 0u;
+                        ptx::mma_bf16(d_tmem, adesc + 2 * kk, bdesc + 2 * kk, idesc, accum);
+                        if (KIND == kG1Swap) {
+                            const uint64_t adesc3 = ptx::make_smem_desc_sw128(sa + 128 * 128);
+                            ptx::mma_bf16(d_tmem + 128, adesc3 + 2 * kk, bdesc + 2 * kk, idesc, accum);
+                        }
+                    }
+                    ptx::mma_commit(&empty2[s2]);
+                    ptx::mma_commit(&empty1[s1]);
+                    if (++s2 == S2) { s2 = 0; ph2 ^= 1; }
+                    if (++s1 == S1) { s1 = 0; ph1 ^= 1; }
+                }
+                ptx::mma_commit(&tmem_full[acc]);
+                if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+            }
+        }
+    } else if (warp >= 6) {
+        // ---------------------------------------------------------------- converters (warps 6..9)
+        // thread c owns A rows c (and c + 128 for the 256-row w1|w3 tile)
+        const int c = threadIdx.x - 6 * 32;
+        int s1 = 0, s2 = 0;
+        uint32_t ph1 = 0, ph2 = 0;
+        for (int t = blockIdx.x; t < total; t += gridDim.x) {
+            TileInfo ti;
+            decode_tile<KIND, NB>(t, p, s_counts, s_offsets, ti);
+            for (int kb = 0; kb < ti.nkb; ++kb) {
+                ptx::mbar_wait(&full1[s1], ph1);
+                ptx::mbar_wait(&empty2[s2], ph2 ^ 1);
+                const uint8_t* src = ring8 + s1 * C::kA8Bytes;
+                uint8_t* dst = ring16 + s2 * C::kA16Bytes;
+#pragma unroll
+                for (int h = 0; h < C::kARows / 128; ++h) {
+                    const int r = c + h * 128;
+                    const uint4* srow = reinterpret_cast<const uint4*>(src + r * 64);
+                    uint4* drow = reinterpret_cast<uint4*>(dst + r * 128);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {            // 16 fp8 of logical chunk q
+                        const uint4 v = srow[q ^ ((r >> 1) & 3)];  // 64-byte swizzle
+                        uint4 lo, hi;
+                        lo.x = cvt_e4m3x2_f16x2(v.x);       lo.y = cvt_e4m3x2_f16x2(v.x >> 16);
+                        lo.z = cvt_e4m3x2_f16x2(v.y);       lo.w = cvt_e4m3x2_f16x2(v.y >> 16);
+                        hi.x = cvt_e4m3x2_f16x2(v.z);       hi.y = cvt_e4m3x2_f16x2(v.z >> 16);
+                        hi.z = cvt_e4m3x2_f16x2(v.w);       hi.w = cvt_e4m3x2_f16x2(v.w >> 16);
+                        drow[(2 * q) ^ (r & 7)] = lo;       // 128-byte swizzle (UMMA SW128 K-major)
+                        drow[(2 * q + 1) ^ (r & 7)] = hi;
+                    }
+                }
+                ptx::fence_proxy_async();  // generic-proxy smem writes -> visible to tcgen05.mma
+                __syncwarp();
+                if (lane == 0) {
+                    ptx::mbar_arrive(&full2[s2]);
+                    ptx::mbar_arrive(&empty1[s1]);  // fp8 bytes consumed (B still owned by the MMA)
+                }
+                if (++s2 == S2) { s2 = 0; ph2 ^= 1; }
+                if (++s1 == S1) { s1 = 0; ph1 ^= 1; }
+            }
+        }
+    } else {
+        // ---------------------------------------------------------------- epilogue (warps 2..5)
+        const int q = warp & 3;
+        const int r = q * 32 + lane;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int t = blockIdx.x; t < total; t += gridDim.x) {
+            TileInfo ti;
+            decode_tile<KIND, NB>(t, p, s_counts, s_offsets, ti);
+            ptx::mbar_wait(&tmem_full[acc], acc_phase);
+            ptx::tc_fence_after();
+            const uint32_t tbase = tmem_base + acc * 256 + (static_cast<uint32_t>(q * 32) << 16);
+            const int nchunks = (ti.n_valid + 15) / 16;
+            if (KIND == kG1Swap) {
+                // row r: ffn index m*128 + r; w1 scale at packed row 256m + r, w3 at 256m + 128 + r
+                const float* sc = scales + (int64_t)ti.e * 2 * p.f + ti.m_idx * 256;
+                const float s1v = sc[r], s3v = sc[128 + r];
+                __half* hp = static_cast<__half*>(p.out) + static_cast<int64_t>(ti.b_row) * p.f + ti.m_idx * 128 + r;
+#pragma unroll 1
+                for (int cc = 0; cc < nchunks; ++cc) {
+                    uint32_t a[16], b[16];
+                    ptx::tmem_ld16(tbase + cc * 16, a);
+                    ptx::tmem_ld16(tbase + 128 + cc * 16, b);
+                    ptx::tmem_wait_ld();
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        const int n = cc * 16 + i;
+                        if (n < ti.n_valid) {
+                            const float hv = silu_f32(__uint_as_float(a[i]) * s1v) * (__uint_as_float(b[i]) * s3v);
+                            hp[static_cast<int64_t>(n) * p.f] = __float2half_rn(hv);
+                        }
+                    }
+                }
+            } else {
+                const int drow = ti.m_idx * 128 + r;
+                const float s2v = drow < p.d ? scales[(int64_t)ti.e * p.d + drow] : 0.f;
+                float* y = static_cast<float*>(p.out) + p.out_split_stride * ti.split +
+                           static_cast<int64_t>(ti.b_row) * p.d + drow;
+#pragma unroll 1
+                for (int cc = 0; cc < nchunks; ++cc) {
+                    uint32_t v[16];
+                    ptx::tmem_ld16(tbase + cc * 16, v);
+                    ptx::tmem_wait_ld();
+                    if (drow < p.d) {
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) {
+                            const int n = cc * 16 + i;
+                            if (n < ti.n_valid) y[static_cast<int64_t>(n) * p.d] = __uint_as_float(v[i]) * s2v;
+                        }
+                    }
+                }
+            }
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&tmem_empty[acc]);
+            if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        }
+    }
+    ptx::pdl_launch_dependents();
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc(tmem_base, 512);
+    }
+}
+
+// ----------------------------------------------------------------------------
+// FP8-weight decode GEMM, A widened straight into TENSOR memory (NB <= 64). The
+// smem-staged variant above needs ~180 B/cycle/SM of shared-memory traffic at the
+// HBM rate (fp8 in, fp16 out, fp16 read by the MMA, plus the token tile) -- over
+// the ~128 B/cycle an SM has, so it runs at ~60 % of the fp8 roofline. Here the
+// converter warps tcgen05.st their fp16 rows into TMEM and tcgen05.mma reads A from
+// TMEM ([a_tmem] operand), leaving shared memory with the fp8 tile and the tokens.
+// TMEM columns: accumulators [0, 2*ACC) (ACC = 2*NB for w1|w3, NB for w2), A ring
+// after them (32 columns per 128 fp16 rows x 64 K per stage).
+template <int KIND, int NB, int KB>
+struct Fp8TmemCfg {
+    static_assert(NB <= 64, "TMEM-A fp8 variant: NB <= 64");
+    static_assert(KB == 64 || KB == 128, "K per stage");
+    static constexpr int kHalves = KIND == kG1Swap ? 2 : 1;
+    static constexpr int kARows = 128 * kHalves;
+    static constexpr int kA8Bytes = kARows * KB;              // fp8 rows x KB bytes
+    static constexpr int kBSub = NB * 128;                    // one 64-element fp16 token atom
+    static constexpr int kBBytes = kBSub * (KB / 64);
+    static constexpr int kAcc = kHalves * NB;                 // TMEM columns per accumulator stage
+    static constexpr int kACols = (KB / 2) * kHalves;         // TMEM columns per A stage (2 fp16 / column)
+    static constexpr int kS2Raw = (512 - 2 * kAcc) / kACols;
+    static constexpr int kS2 = kS2Raw > 6 ? 6 : kS2Raw;
+    static constexpr int kLoadBytes = kA8Bytes + kBBytes;
+    static constexpr int kS1Raw = (kSmemBudget - 2048) / kLoadBytes;
+    static constexpr int kS1 = kS1Raw > 10 ? 10 : kS1Raw;
+    static constexpr int kSmemBytes = kS1 * kLoadBytes + 2048;
+    static_assert(kS2 >= 2 && kS1 >= 4, "bad fp8 pipeline");
+};
+
+// Two converter groups (warps 6..9 and 10..13) take alternate k-blocks so that one
+// group's shared-memory / TMEM-store latency overlaps the other's.
+constexpr int kFp8tGroups = 1;  // r01: 2 groups measured slower (0.3466 vs 0.3388 ms per decode step)
+constexpr int kFp8tThreads = (6 + 4 * kFp8tGroups) * 32;
+
+template <int KIND, int NB, int KB>
+__global__ void __launch_bounds__(kFp8tThreads, 1)
+    moe_gemm_fp8t_kernel(const GemmParams p, const float* __restrict__ scales,
+                         const __grid_constant__ CUtensorMap tmA8, const __grid_constant__ CUtensorMap tmB) {
+    using C = Fp8TmemCfg<KIND, NB, KB>;
+    constexpr int S1 = C::kS1, S2 = C::kS2;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* ring_b = smem;                      // S1 x fp16 token tiles (NB*128 B, 1024-aligned)
+    uint8_t* ring8 = ring_b + S1 * C::kBBytes;   // S1 x fp8 weight tiles (64-byte swizzle)
+    uint64_t* bars = reinterpret_cast<uint64_t*>(ring8 + S1 * C::kA8Bytes);
+    uint64_t* full1 = bars;
+    uint64_t* empty1 = bars + S1;
+    uint64_t* full2 = bars + 2 * S1;
+    uint64_t* empty2 = full2 + S2;
+    uint64_t* tmem_full = empty2 + S2;
+    uint64_t* tmem_empty = tmem_full + 2;
+    uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+    int32_t* s_counts = reinterpret_cast<int32_t*>(tmem_empty + 3);
+    int32_t* s_offsets = s_counts + 32;
+
+    const int warp = threadIdx.x / 32;
+    const int lane = threadIdx.x % 32;
+    if (warp == 0 && lane == 0) {
+        ptx::prefetch_tmap(&tmA8);
+        ptx::prefetch_tmap(&tmB);
+        for (int i = 0; i < S1; ++i) {
+            ptx::mbar_init(&full1[i], 1);
+            ptx::mbar_init(&empty1[i], 5);
+        }
+        for (int i = 0; i < S2; ++i) {
+            ptx::mbar_init(&full2[i], 4);
+            ptx::mbar_init(&empty2[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            ptx::mbar_init(&tmem_full[i], 1);
+            ptx::mbar_init(&tmem_empty[i], 4);
+        }
+        ptx::fence_mbar_init();
+    }
+    if (warp == 1) {
+        ptx::tmem_alloc(tmem_base_slot, 512);
+        ptx::tmem_relinquish();
+    }
+    ptx::pdl_wait();
+    if (threadIdx.x < 32)
+        for (int e = threadIdx.x; e < p.E; e += 32) {
+            s_counts[e] = p.counts[e];
+            s_offsets[e] = p.offsets[e];
+        }
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = *tmem_base_slot;
+    const uint32_t a_base = tmem_base + 2 * C::kAcc;
+    int total = 0;
+    for (int e = 0; e < p.E; ++e) total += tiles_of<KIND, NB>(s_counts[e], p);
+
+    if (warp == 0) {
+        if (lane == 0) {  // ------------------------------------------------ TMA producer
+            int st = 0;
+            uint32_t ph = 0;
+            for (int t = blockIdx.x; t < total; t += gridDim.x) {
+                TileInfo ti;
+                decode_tile<KIND, NB, KB>(t, p, s_counts, s_offsets, ti);
+                for (int kb = 0; kb < ti.nkb; ++kb) {
+                    ptx::mbar_wait(&empty1[st], ph ^ 1);
+                    ptx::mbar_arrive_expect_tx(&full1[st], C::kLoadBytes);
+                    const int kc = (ti.kb0 + kb) * KB;
+                    ptx::tma_load_3d(&tmA8, &full1[st], ring8 + st * C::kA8Bytes, kc, ti.a_row, ti.e,
+                                     ptx::kEvictFirst);
+#pragma unroll
+                    for (int sub = 0; sub < KB / 64; ++sub)
+                        ptx::tma_load_2d(&tmB, &full1[st], ring_b + st * C::kBBytes + sub * C::kBSub, kc + 64 * sub,
+                                         ti.b_row, ptx::kEvictLast);
+                    if (++st == S1) { st = 0; ph ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // ------------------------------------------------ MMA issuer
+            int s1 = 0, s2 = 0;
+            uint32_t ph1 = 0, ph2 = 0;
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            for (int t = blockIdx.x; t < total; t += gridDim.x) {
+                TileInfo ti;
+                decode_tile<KIND, NB, KB>(t, p, s_counts, s_offsets, ti);
+                const uint32_t n_mma = (uint32_t)((ti.n_valid + 15) / 16 * 16);
+                const uint32_t idesc = (1u << 4) | ((n_mma >> 3) << 17) | ((128u >> 4) << 24);  // f16 x f16 -> f32
+                const uint32_t d_tmem = tmem_base + acc * C::kAcc;
+                ptx::mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
+                ptx::tc_fence_after();
+                for (int kb = 0; kb < ti.nkb; ++kb) {
+                    ptx::mbar_wait(&full2[s2], ph2);
+                    ptx::tc_fence_after();
+                    const uint32_t a_t = a_base + s2 * C::kACols;
+#pragma unroll
+                    for (int kk = 0; kk < KB / 16; ++kk) {
+                        const uint64_t bdesc = ptx::make_smem_desc_sw128(
+                            ptx::smem_u32(ring_b + s1 * C::kBBytes + (kk / 4) * C::kBSub));
+                        const uint32_t accum = (kb | kk) ? 1u : 0u;
+                        ptx::mma_f16_tmem_a(d_tmem, a_t + 8 * kk, bdesc + 2 * (kk % 4), idesc, accum);
+                        if (KIND == kG1Swap)
+                            ptx::mma_f16_tmem_a(d_tmem + NB, a_t + KB / 2 + 8 * kk, bdesc + 2 * (kk % 4), idesc,
+                                                accum);
+                    }
+                    ptx::mma_commit(&empty2[s2]);
+                    ptx::mma_commit(&empty1[s1]);
+                    if (++s2 == S2) { s2 = 0; ph2 ^= 1; }
+                    if (++s1 == S1) { s1 = 0; ph1 ^= 1; }
+                }
+                ptx::mma_commit(&tmem_full[acc]);
+                if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+            }
+        }
+    } else if (warp >= 6) {
+        // ---------------------------------------------------------------- converters (warps 6..)
+        const int q = warp & 3;                 // TMEM lane quadrant of this warp
+        const int r = q * 32 + lane;            // A row (= TMEM lane) of this thread
+        const int grp = (warp - 6) / 4;         // converter group: takes k-blocks seq % kFp8tGroups == grp
+        int s1 = 0, s2 = 0;
+        uint32_t ph1 = 0, ph2 = 0;
+        int seq = 0;
+        for (int t = blockIdx.x; t < total; t += gridDim.x) {
+            TileInfo ti;
+            decode_tile<KIND, NB, KB>(t, p, s_counts, s_offsets, ti);
+            for (int kb = 0; kb < ti.nkb; ++kb, ++seq) {
+                if (seq % kFp8tGroups != grp) {
+                    if (++s2 == S2) { s2 = 0; ph2 ^= 1; }
+                    if (++s1 == S1) { s1 = 0; ph1 ^= 1; }
+                    continue;
+                }
+                ptx::mbar_wait(&full1[s1], ph1);
+                ptx::mbar_wait(&empty2[s2], ph2 ^ 1);
+                ptx::tc_fence_after();
+                const uint8_t* src = ring8 + s1 * C::kA8Bytes;
+#pragma unroll
+                for (int h = 0; h < C::kHalves; ++h) {
+                    const int rr = r + 128 * h;
+                    const uint32_t srow = ptx::smem_u32(src + rr * KB);
+#pragma unroll
+                    for (int half = 0; half < KB / 64; ++half) {   // 64 K elements -> 32 TMEM columns
+                        uint4 vv[4];
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) {  // all shared loads issued first
+                            const int lc = 4 * half + c;  // logical 16-byte chunk of the row
+                            const int pc = KB == 64 ? (lc ^ ((rr >> 1) & 3)) : (lc ^ (rr & 7));  // 64B / 128B swizzle
+                            vv[c] = ptx::lds128(srow + 16 * pc);
+                        }
+                        uint32_t o[32];
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) {
+                            const uint4 v = vv[c];
+                            o[8 * c + 0] = cvt_e4m3x2_f16x2(v.x);
+                            o[8 * c + 1] = cvt_e4m3x2_f16x2(v.x >> 16);
+                            o[8 * c + 2] = cvt_e4m3x2_f16x2(v.y);
+                            o[8 * c + 3] = cvt_e4m3x2_f16x2(v.y >> 16);
+                            o[8 * c + 4] = cvt_e4m3x2_f16x2(v.z);
+                            o[8 * c + 5] = cvt_e4m3x2_f16x2(v.z >> 16);
+                            o[8 * c + 6] = cvt_e4m3x2_f16x2(v.w);
+                            o[8 * c + 7] = cvt_e4m3x2_f16x2(v.w >> 16);
+                        }
+                        ptx::tmem_st32(a_base + s2 * C::kACols + (KB / 2) * h + 32 * half +
+                                           (static_cast<uint32_t>(q * 32) << 16),
+                                       o);
+                    }
+                }
+                ptx::tmem_wait_st();
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) {
+                    ptx::mbar_arrive(&full2[s2]);
+                    ptx::mbar_arrive(&empty1[s1]);
+                }
+                if (++s2 == S2) { s2 = 0; ph2 ^= 1; }
+                if (++s1 == S1) { s1 = 0; ph1 ^= 1; }
+            }
+        }
+    } else {
+        // ---------------------------------------------------------------- epilogue (warps 2..5)
+        const int q = warp & 3;
+        const int r = q * 32 + lane;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int t = blockIdx.x; t < total; t += gridDim.x) {
+            TileInfo ti;
+            decode_tile<KIND, NB, KB>(t, p, s_counts, s_offsets, ti);
+            ptx::mbar_wait(&tmem_full[acc], acc_phase);
+            ptx::tc_fence_after();
+            const uint32_t tbase = tmem_base + acc * C::kAcc + (static_cast<uint32_t>(q * 32) << 16);
+            const int nchunks = (ti.n_valid + 15) / 16;
+            if (KIND == kG1Swap) {
+                const float* sc = scales + (int64_t)ti.e * 2 * p.f + ti.m_idx * 256;
+                const float s1v = sc[r], s3v = sc[128 + r];
+                __half* hp = static_cast<__half*>(p.out) + static_cast<int64_t>(ti.b_row) * p.f + ti.m_idx * 128 + r;
+#pragma unroll 1
+                for (int cc = 0; cc < nchunks; ++cc) {
+                    uint32_t a[16], b[16];
+                    ptx::tmem_ld16(tbase + cc * 16, a);
+                    ptx::tmem_ld16(tbase + NB + cc * 16, b);
+                    ptx::tmem_wait_ld();
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        const int n = cc * 16 + i;
+                        if (n < ti.n_valid) {
+                            const float hv = silu_f32(__uint_as_float(a[i]) * s1v) * (__uint_as_float(b[i]) * s3v);
+                            hp[static_cast<int64_t>(n) * p.f] = __float2half_rn(hv);
+                        }
+                    }
+                }
+            } else {
+                const int drow = ti.m_idx * 128 + r;
+                const float s2v = drow < p.d ? scales[(int64_t)ti.e * p.d + drow] : 0.f;
+                float* y = static_cast<float*>(p.out) + p.out_split_stride * ti.split +
+                           static_cast<int64_t>(ti.b_row) * p.d + drow;
+#pragma unroll 1
+                for (int cc = 0; cc < nchunks; ++cc) {
+                    uint32_t v[16];
+                    ptx::tmem_ld16(tbase + cc * 16, v);
+                    ptx::tmem_wait_ld();
+                    if (drow < p.d) {
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) {
+                            const int n = cc * 16 + i;
+                            if (n < ti.n_valid) y[static_cast<int64_t>(n) * p.d] = __uint_as_float(v[i]) * s2v;
+                        }
+                    }
+                }
+            }
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&tmem_empty[acc]);
+            if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        }
+    }
+    ptx::pdl_launch_dependents();
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc(tmem_base, 512);
     }
 }
 

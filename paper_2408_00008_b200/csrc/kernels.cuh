@@ -13,6 +13,7 @@
 #pragma once
 
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <stdint.h>
 #include "sm100.cuh"
 
@@ -420,7 +421,21 @@ struct PermuteParams {
     int32_t* pos;             // [T, k] in: in-block rank (router); out: permuted row (-1: not local)
     int32_t* pos_aux;         // optional copy for the caller
     __nv_bfloat16* x_perm;    // [Cap, d]
+    int32_t to_f16;           // store rows as fp16 (fp8-weight GEMMs) instead of copying bf16
 };
+
+__device__ __forceinline__ uint4 bf16x8_to_f16x8(const uint4& v) {
+    float f[8];
+    bf16x8_to_f32(v, f);
+    uint4 r;
+    __half2 h0 = __floats2half2_rn(f[0], f[1]), h1 = __floats2half2_rn(f[2], f[3]);
+    __half2 h2 = __floats2half2_rn(f[4], f[5]), h3 = __floats2half2_rn(f[6], f[7]);
+    r.x = *reinterpret_cast<uint32_t*>(&h0);
+    r.y = *reinterpret_cast<uint32_t*>(&h1);
+    r.z = *reinterpret_cast<uint32_t*>(&h2);
+    r.w = *reinterpret_cast<uint32_t*>(&h3);
+    return r;
+}
 
 // K2 (a6): position of each assignment = segment start + rank of its router block
 // + stable rank inside the block (#earlier tokens of the block routed to the same
@@ -478,6 +493,10 @@ __global__ void __launch_bounds__(kPermuteThreads) moe_permute_kernel(const Perm
 #pragma unroll
             for (int u = 0; u < 4; ++u)
                 if (v0 + u * stride < nvec) buf[u] = __ldg(src + v0 + u * stride);
+            if (p.to_f16) {
+#pragma unroll
+                for (int u = 0; u < 4; ++u) buf[u] = bf16x8_to_f16x8(buf[u]);
+            }
 #pragma unroll
             for (int u = 0; u < 4; ++u)
                 if (v0 + u * stride < nvec) {
@@ -639,6 +658,23 @@ __global__ void moe_pack_w2_kernel(const __nv_bfloat16* w2, __nv_bfloat16* w2p, 
         const int64_t e = row / d, r = row % d;
         const __nv_bfloat16* src = w2 + ((e_off + e) * (int64_t)d + r) * f + f_off;
         reinterpret_cast<uint4*>(w2p)[v] = reinterpret_cast<const uint4*>(src)[cv];
+    }
+}
+
+// FP8 weight scales (one fp32 power of two per output row) in the packed row order:
+// s13[e][256*b + i] = s1[eg][f_off + 128*b + i] (i < 128), s3[...][... + i - 128] (i >= 128)
+__global__ void moe_pack_scales_kernel(const float* s1, const float* s3, const float* s2, float* s13p, float* s2p,
+                                       int E_local, int e_off, int d, int f, int f_local, int f_off) {
+    const int64_t n13 = (int64_t)E_local * 2 * f_local, n2 = (int64_t)E_local * d;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n13 + n2; i += (int64_t)gridDim.x * blockDim.x) {
+        if (i < n13) {
+            const int64_t e = i / (2 * f_local), pr = i % (2 * f_local), b = pr / 256, j = pr % 256;
+            const float* src = j < 128 ? s1 : s3;
+            s13p[i] = src[(e_off + e) * (int64_t)f + f_off + b * 128 + (j % 128)];
+        } else {
+            const int64_t k = i - n13, e = k / d, r = k % d;
+            s2p[k] = s2[(e_off + e) * (int64_t)d + r];
+        }
     }
 }
 

@@ -124,6 +124,21 @@ bool encode_map(CUtensorMap* m, const void* base, int rank, uint64_t K, uint64_t
     return r == CUDA_SUCCESS;
 }
 
+// rank-3 [batch, rows, K] fp8 (1 byte), box {64, box_rows, 1}, 64-byte swizzle (FP8 weights)
+bool encode_map_fp8(CUtensorMap* m, const void* base, uint64_t K, uint64_t rows, uint64_t batch, uint32_t box_rows,
+                    uint32_t box_k = 64) {
+    PFN_encodeTiled_t fn = get_encode_fn();
+    if (!fn) return false;
+    cuuint64_t dims[3] = {K, rows, batch};
+    cuuint64_t strides[2] = {K, K * rows};
+    cuuint32_t box[3] = {box_k, box_rows, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(base), dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, box_k == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
 int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
 int next_pow2(int v) { int p = 1; while (p < v) p <<= 1; return p; }
 
@@ -147,6 +162,11 @@ struct moe_ctx {
     int swap_rows_per_expert = 256;
     int max_splits = 4;
     int64_t split_stride = 0; // elements between split-K partial buffers of this forward
+    bool fp8 = false;             // MOE_FLAG_FP8_WEIGHTS
+    bool fp8_smem_a = false;
+    bool fp8_kb128 = false;       // fp8 TMEM-A GEMMs with 128-element K blocks (d % 128 == 0); env
+                                  // MOE_FP8_KB=64 selects 64 (r01: 0.3304 ms vs 0.2975 ms per step)      // env MOE_FP8_SMEM_A=1: widen fp8 weights in smem (not TMEM) at NB <= 64
+    moe_expert_weights cur_w{};   // weights of the current forward
     int pair_tune = 0;        // experiment override of the prefill tile orders (env MOE_PAIR_TUNE)
     int g1_raster = 2, g1_band = 16, g2_raster = 1, g2_band = 1;  // prefill tile orders (pair_decode; ncu DRAM sweep r01)
     // workspace (device)
@@ -178,11 +198,13 @@ struct moe_ctx {
         const void* w2 = nullptr;
         uint64_t tick = 0;
         CUtensorMap tm_w13{}, tm_w13_pair{}, tm_w2_tiled{}, tm_w2_swap{};
+        CUtensorMap tm8_w13_64{}, tm8_w2_64{};  // fp8 weights, 64-byte boxes (smem-widening variant)
     };
     static constexpr size_t kWeightMapCache = 64;
     std::vector<WeightMaps> wmaps;
     uint64_t use_tick = 0;
     CUtensorMap tm_w13{}, tm_w13_pair{}, tm_w2_tiled{}, tm_w2_swap{};  // maps of the current call
+    CUtensorMap tm8_w13_64{}, tm8_w2_64{};
     // instrumentation
     bool profiling = false;
     struct Ev { int slot; cudaEvent_t a, b; };
@@ -258,6 +280,22 @@ moe_status launch(moe_ctx* c, int slot, void (*kern)(KArgs...), dim3 grid, dim3 
         cudaEventRecord(eb, st);
         c->pending.push_back({slot, ea, eb});
     }
+    return MOE_OK;
+}
+
+template <int KIND, int NB>
+moe_status set_fp8t_attr(moe_ctx* c) {
+    CUDA_TRY(c, cudaFuncSetAttribute(moe_gemm_fp8t_kernel<KIND, NB, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     Fp8TmemCfg<KIND, NB, 64>::kSmemBytes));
+    CUDA_TRY(c, cudaFuncSetAttribute(moe_gemm_fp8t_kernel<KIND, NB, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     Fp8TmemCfg<KIND, NB, 128>::kSmemBytes));
+    return MOE_OK;
+}
+
+template <int KIND, int NB>
+moe_status set_fp8_attr(moe_ctx* c) {
+    CUDA_TRY(c, cudaFuncSetAttribute(moe_gemm_fp8_kernel<KIND, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     Fp8Cfg<KIND, NB>::kSmemBytes));
     return MOE_OK;
 }
 
@@ -383,18 +421,28 @@ moe_status ensure_weight_maps(moe_ctx* c, const moe_expert_weights* w) {
             m.tick = c->use_tick;
             c->tm_w13 = m.tm_w13; c->tm_w13_pair = m.tm_w13_pair;
             c->tm_w2_tiled = m.tm_w2_tiled; c->tm_w2_swap = m.tm_w2_swap;
+            c->tm8_w13_64 = m.tm8_w13_64; c->tm8_w2_64 = m.tm8_w2_64;
             return MOE_OK;
         }
     moe_ctx::WeightMaps m;
     m.w13 = w->w13;
     m.w2 = w->w2;
     m.tick = c->use_tick;
-    if (!encode_map(&m.tm_w13, w->w13, 3, c->d, 2 * (uint64_t)c->f_local, c->E_local, 256) ||
-        !encode_map(&m.tm_w13_pair, w->w13, 3, c->d, 2 * (uint64_t)c->f_local, c->E_local, 128))
-        return fail(c, MOE_ERR_CUDA, "cuTensorMapEncodeTiled(w13) failed");
-    if (!encode_map(&m.tm_w2_tiled, w->w2, 3, c->f_local, c->d, c->E_local, 256) ||
-        !encode_map(&m.tm_w2_swap, w->w2, 3, c->f_local, c->d, c->E_local, 128))
-        return fail(c, MOE_ERR_CUDA, "cuTensorMapEncodeTiled(w2) failed");
+    if (c->fp8) {  // E4M3 weights: only the decode (swap-AB) maps exist
+        const uint32_t bk = c->fp8_kb128 ? 128 : 64;
+        if (!encode_map_fp8(&m.tm_w13, w->w13, c->d, 2 * (uint64_t)c->f_local, c->E_local, 256, bk) ||
+            !encode_map_fp8(&m.tm_w2_swap, w->w2, c->f_local, c->d, c->E_local, 128, bk) ||
+            !encode_map_fp8(&m.tm8_w13_64, w->w13, c->d, 2 * (uint64_t)c->f_local, c->E_local, 256, 64) ||
+            !encode_map_fp8(&m.tm8_w2_64, w->w2, c->f_local, c->d, c->E_local, 128, 64))
+            return fail(c, MOE_ERR_CUDA, "cuTensorMapEncodeTiled(fp8 weights) failed");
+    } else {
+        if (!encode_map(&m.tm_w13, w->w13, 3, c->d, 2 * (uint64_t)c->f_local, c->E_local, 256) ||
+            !encode_map(&m.tm_w13_pair, w->w13, 3, c->d, 2 * (uint64_t)c->f_local, c->E_local, 128))
+            return fail(c, MOE_ERR_CUDA, "cuTensorMapEncodeTiled(w13) failed");
+        if (!encode_map(&m.tm_w2_tiled, w->w2, 3, c->f_local, c->d, c->E_local, 256) ||
+            !encode_map(&m.tm_w2_swap, w->w2, 3, c->f_local, c->d, c->E_local, 128))
+            return fail(c, MOE_ERR_CUDA, "cuTensorMapEncodeTiled(w2) failed");
+    }
     if (c->wmaps.size() >= moe_ctx::kWeightMapCache) {
         size_t lru = 0;
         for (size_t i = 1; i < c->wmaps.size(); ++i)
@@ -405,12 +453,50 @@ moe_status ensure_weight_maps(moe_ctx* c, const moe_expert_weights* w) {
     }
     c->tm_w13 = m.tm_w13; c->tm_w13_pair = m.tm_w13_pair;
     c->tm_w2_tiled = m.tm_w2_tiled; c->tm_w2_swap = m.tm_w2_swap;
+    c->tm8_w13_64 = m.tm8_w13_64; c->tm8_w2_64 = m.tm8_w2_64;
     return MOE_OK;
+}
+
+template <int KIND, int NB>
+moe_status launch_gemm_fp8(moe_ctx* c, int slot, const GemmParams& p, const float* scales, const CUtensorMap& a8,
+                           const CUtensorMap& b, int grid, cudaStream_t st) {
+    return launch(c, slot, moe_gemm_fp8_kernel<KIND, NB>, dim3(grid), dim3(kFp8Threads),
+                  (size_t)Fp8Cfg<KIND, NB>::kSmemBytes, st, p, scales, a8, b);
+}
+
+template <int KIND, int NB>
+moe_status launch_gemm_fp8t(moe_ctx* c, int slot, const GemmParams& p, const float* scales, const CUtensorMap& a8,
+                            const CUtensorMap& b, int grid, cudaStream_t st) {
+    if (c->fp8_kb128)  // 128-element K blocks (maps encoded with a 128-byte fp8 box)
+        return launch(c, slot, moe_gemm_fp8t_kernel<KIND, NB, 128>, dim3(grid), dim3(kFp8tThreads),
+                      (size_t)Fp8TmemCfg<KIND, NB, 128>::kSmemBytes, st, p, scales, a8, b);
+    return launch(c, slot, moe_gemm_fp8t_kernel<KIND, NB, 64>, dim3(grid), dim3(kFp8tThreads),
+                  (size_t)Fp8TmemCfg<KIND, NB, 64>::kSmemBytes, st, p, scales, a8, b);
 }
 
 template <int NB>
 moe_status run_swap(moe_ctx* c, int nbi, const moe_expert_weights* w, int splits, cudaStream_t st) {
-    (void)w;
+    if constexpr (NB <= 64) {
+        if (c->fp8 && !c->fp8_smem_a) {  // weights widened into TMEM
+            GemmParams p1{c->counts, c->offsets, c->E_local, c->d, c->f_local, 1, c->h, 0};
+            moe_status s = launch_gemm_fp8t<kG1Swap, NB>(c, kSlotGemm1, p1, w->w13_scale, c->tm_w13,
+                                                         c->tm_x_swap[nbi], c->num_sms, st);
+            if (s) return s;
+            GemmParams p2{c->counts, c->offsets, c->E_local, c->d, c->f_local, splits, c->y, c->split_stride};
+            return launch_gemm_fp8t<kG2Swap, NB>(c, kSlotGemm2, p2, w->w2_scale, c->tm_w2_swap, c->tm_h_swap[nbi],
+                                                 c->num_sms, st);
+        }
+    }
+    if (c->fp8) {  // weights widened in shared memory (64-element K blocks)
+        const int sp = std::min(splits, c->f_local / kBK);
+        GemmParams p1{c->counts, c->offsets, c->E_local, c->d, c->f_local, 1, c->h, 0};
+        moe_status s = launch_gemm_fp8<kG1Swap, NB>(c, kSlotGemm1, p1, w->w13_scale, c->tm8_w13_64,
+                                                    c->tm_x_swap[nbi], c->num_sms, st);
+        if (s) return s;
+        GemmParams p2{c->counts, c->offsets, c->E_local, c->d, c->f_local, sp, c->y, c->split_stride};
+        return launch_gemm_fp8<kG2Swap, NB>(c, kSlotGemm2, p2, w->w2_scale, c->tm8_w2_64, c->tm_h_swap[nbi],
+                                            c->num_sms, st);
+    }
     GemmParams p1{c->counts, c->offsets, c->E_local, c->d, c->f_local, 1, c->h, 0};
     moe_status s = launch_gemm<kG1Swap, NB>(c, kSlotGemm1, p1, c->tm_w13, c->tm_x_swap[nbi], c->num_sms, st);
     if (s) return s;
@@ -476,6 +562,7 @@ moe_status route_and_permute(moe_ctx* c, const RouteSpec& r, cudaStream_t st) {
     pp.TB = TB;
     pp.PT = r.T <= 1024 ? 2 : 8;
     pp.pos = r.pos; pp.pos_aux = r.pos_aux; pp.x_perm = static_cast<__nv_bfloat16*>(r.dst_rows);
+    pp.to_f16 = c->fp8 && r.cap == 0;  // fp8-weight GEMMs take fp16 tokens
     return launch(c, kSlotPermute, moe_permute_kernel, dim3((r.T + pp.PT - 1) / pp.PT), dim3(kPermuteThreads), 0,
                   st, pp);
 }
@@ -493,12 +580,12 @@ moe_status run_gemms(moe_ctx* c, bool swap, int64_t rows_bound, int64_t rows_tot
         const int64_t rows_needed = round_up(rows_total + (int64_t)c->E_local * (kSegAlign - 1), kSegAlign);
         splits = c->cfg.split_k ? c->cfg.split_k : c->max_splits;
         splits = (int)std::max<int64_t>(1, std::min<int64_t>(splits, c->y_elems / (rows_needed * c->d)));
-        splits = std::min(splits, c->f_local / kBK);  // every split owns >= 1 K block
+        splits = std::min(splits, c->f_local / (c->fp8_kb128 ? 128 : kBK));  // every split owns >= 1 K block
         c->split_stride = rows_needed * c->d;
         const int nbw = (int)std::max<int64_t>(32, std::min<int64_t>(128, next_pow2((int)std::min<int64_t>(rows_bound, 1 << 20))));
-        if (nbw == 32) s = run_swap<32>(c, 0, nullptr, splits, st);
-        else if (nbw == 64) s = run_swap<64>(c, 1, nullptr, splits, st);
-        else s = run_swap<128>(c, 2, nullptr, splits, st);
+        if (nbw == 32) s = run_swap<32>(c, 0, &c->cur_w, splits, st);
+        else if (nbw == 64) s = run_swap<64>(c, 1, &c->cur_w, splits, st);
+        else s = run_swap<128>(c, 2, &c->cur_w, splits, st);
         if (s) return s;
     } else if (!(c->cfg.flags & MOE_FLAG_NO_PAIR)) {
         // CTA-pair (cta_group::2) 256x256 tiles, one cluster of 2 CTAs per TPC
@@ -763,7 +850,7 @@ CommRef tp_comm(const moe_ctx* c) {
 }
 
 bool use_swap_path(const moe_ctx* c, int T) {
-    if (c->cfg.flags & MOE_FLAG_FORCE_SWAP) return true;
+    if ((c->cfg.flags & MOE_FLAG_FORCE_SWAP) || c->fp8) return true;  // fp8 weights: decode GEMMs only
     if (c->cfg.flags & MOE_FLAG_FORCE_TILED) return false;
     return (int64_t)T * c->k <= (int64_t)c->swap_rows_per_expert * c->E_local;
 }
@@ -811,6 +898,20 @@ moe_status moe_packed_sizes(const moe_config* cfg, size_t* w13_bytes, size_t* w2
     return MOE_OK;
 }
 
+moe_status moe_packed_sizes_fp8(const moe_config* cfg, size_t* w13_bytes, size_t* w2_bytes, size_t* w13_scale_bytes,
+                                size_t* w2_scale_bytes) {
+    moe_status s = validate_cfg(cfg, nullptr);
+    if (s) return s;
+    if (!w13_bytes || !w2_bytes || !w13_scale_bytes || !w2_scale_bytes)
+        return fail(nullptr, MOE_ERR_INVALID, "NULL output pointer");
+    const ParShape ps = par_shape(cfg);
+    *w13_bytes = (size_t)ps.E_local * 2 * ps.f_local * cfg->hidden;
+    *w2_bytes = (size_t)ps.E_local * cfg->hidden * ps.f_local;
+    *w13_scale_bytes = (size_t)ps.E_local * 2 * ps.f_local * 4;
+    *w2_scale_bytes = (size_t)ps.E_local * cfg->hidden * 4;
+    return MOE_OK;
+}
+
 moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
     if (!out) return fail(nullptr, MOE_ERR_INVALID, "out is NULL");
     *out = nullptr;
@@ -842,6 +943,10 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
     }
     c->rank = cfg->rank;
     c->max_T = cfg->max_tokens;
+    c->fp8 = (cfg->flags & MOE_FLAG_FP8_WEIGHTS) != 0;
+    if (const char* v = getenv("MOE_FP8_SMEM_A")) c->fp8_smem_a = atoi(v) != 0;
+    c->fp8_kb128 = c->fp8 && c->d % 128 == 0 && c->f_local % 128 == 0;
+    if (const char* v = getenv("MOE_FP8_KB")) c->fp8_kb128 = c->fp8_kb128 && atoi(v) == 128;
     if (const char* pt = getenv("MOE_PAIR_TUNE")) c->pair_tune = atoi(pt);
     // router blocks of >= 2 rows; EP also routes the G*max_T*k receive slots
     c->nblk_max = (int)(((int64_t)c->max_T * (c->ep_world > 1 ? c->ep_world * c->k : 1) + 1) / 2 + 1);
@@ -938,7 +1043,12 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
         (as = set_gemm_attr<kG1Swap, 32>(c)) || (as = set_gemm_attr<kG2Swap, 32>(c)) ||
         (as = set_gemm_attr<kG1Swap, 64>(c)) || (as = set_gemm_attr<kG2Swap, 64>(c)) ||
         (as = set_gemm_attr<kG1Swap, 128>(c)) || (as = set_gemm_attr<kG2Swap, 128>(c)) ||
-        (as = set_pair_attr<kG1Pair>(c)) || (as = set_pair_attr<kG2Pair>(c))) {
+        (as = set_pair_attr<kG1Pair>(c)) || (as = set_pair_attr<kG2Pair>(c)) ||
+        (as = set_fp8_attr<kG1Swap, 32>(c)) || (as = set_fp8_attr<kG2Swap, 32>(c)) ||
+        (as = set_fp8_attr<kG1Swap, 64>(c)) || (as = set_fp8_attr<kG2Swap, 64>(c)) ||
+        (as = set_fp8_attr<kG1Swap, 128>(c)) || (as = set_fp8_attr<kG2Swap, 128>(c)) ||
+        (as = set_fp8t_attr<kG1Swap, 32>(c)) || (as = set_fp8t_attr<kG2Swap, 32>(c)) ||
+        (as = set_fp8t_attr<kG1Swap, 64>(c)) || (as = set_fp8t_attr<kG2Swap, 64>(c))) {
         std::string m = c->err;
         moe_destroy(c);
         g_init_error = m;
@@ -984,6 +1094,34 @@ moe_status moe_pack_weights(moe_ctx* c, const void* w1, const void* w3, const vo
         return s;
     // descriptors keyed by these pointers must be re-encoded if memory was reused
     (void)w13_out;  // descriptors hold addresses only; repacking in place keeps them valid
+    return MOE_OK;
+}
+
+moe_status moe_pack_weights_fp8(moe_ctx* c, const void* q1, const void* q3, const void* q2, const float* s1,
+                                const float* s3, const float* s2, void* w13_out, void* w2_out, float* w13_scale_out,
+                                float* w2_scale_out, void* stream) {
+    moe_status s = check_ready(c);
+    if (s) return s;
+    if (!c->fp8) return fail(c, MOE_ERR_INVALID, "context was not created with MOE_FLAG_FP8_WEIGHTS");
+    if (!q1 || !q3 || !q2 || !s1 || !s3 || !s2 || !w13_out || !w2_out || !w13_scale_out || !w2_scale_out)
+        return fail(c, MOE_ERR_INVALID, "NULL pointer");
+    if (!aligned16(q1) || !aligned16(q3) || !aligned16(q2) || !aligned16(w13_out) || !aligned16(w2_out))
+        return fail(c, MOE_ERR_INVALID, "fp8 weight pointers must be 16-byte aligned");
+    if (c->d % 16) return fail(c, MOE_ERR_UNSUPPORTED, "fp8 packing needs hidden % 16 == 0");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int e_off = c->e_lo;
+    // one byte per weight: pack pairs of fp8 as 2-byte units with the bf16 packers
+    if ((s = launch(c, kSlotPack, moe_pack_w13_kernel, dim3(4 * c->num_sms), dim3(256), 0, st,
+                    static_cast<const __nv_bfloat16*>(q1), static_cast<const __nv_bfloat16*>(q3),
+                    static_cast<__nv_bfloat16*>(w13_out), c->E_local, e_off, c->d / 2, c->f, c->f_local, c->f_off)))
+        return s;
+    if ((s = launch(c, kSlotPack, moe_pack_w2_kernel, dim3(4 * c->num_sms), dim3(256), 0, st,
+                    static_cast<const __nv_bfloat16*>(q2), static_cast<__nv_bfloat16*>(w2_out), c->E_local, e_off,
+                    c->d, c->f / 2, c->f_local / 2, c->f_off / 2)))
+        return s;
+    if ((s = launch(c, kSlotPack, moe_pack_scales_kernel, dim3(c->num_sms), dim3(256), 0, st, s1, s3, s2,
+                    w13_scale_out, w2_scale_out, c->E_local, e_off, c->d, c->f, c->f_local, c->f_off)))
+        return s;
     return MOE_OK;
 }
 
@@ -1136,6 +1274,9 @@ moe_status forward_impl(moe_ctx* c, const void* tokens, int32_t T, const void* r
     if (T > 0 && (!tokens || !out || !aligned16(tokens) || !aligned16(out)))
         return fail(c, MOE_ERR_INVALID, "tokens / out must be 16-byte aligned device pointers");
     if (aux && aux->out_f32 && !aligned16(aux->out_f32)) return fail(c, MOE_ERR_INVALID, "aux.out_f32 misaligned");
+    if (c->fp8 && (!w->w13_scale || !w->w2_scale))
+        return fail(c, MOE_ERR_INVALID, "MOE_FLAG_FP8_WEIGHTS needs w13_scale and w2_scale");
+    c->cur_w = *w;
     moe_status s = ensure_weight_maps(c, w);
     if (s) return s;
     if (c->cfg.par == MOE_PAR_EP || c->cfg.par == MOE_PAR_HYBRID) return forward_ep(c, tokens, T, router_w, out, aux, st);
@@ -1268,7 +1409,7 @@ moe_status forward_ep(moe_ctx* c, const void* tokens, int32_t T, const void* rou
         rows_expected = 0;
         for (int p = 0; p < G; ++p) rows_expected += c->h_counts[64 + p];
     }
-    const bool swap = (c->cfg.flags & MOE_FLAG_FORCE_SWAP) ? true
+    const bool swap = (c->cfg.flags & MOE_FLAG_FORCE_SWAP) || c->fp8 ? true
                     : (c->cfg.flags & MOE_FLAG_FORCE_TILED) ? false
                     : rows_expected <= (int64_t)c->swap_rows_per_expert * c->E_local;
     int splits = 1;

@@ -79,3 +79,20 @@ def bf16_bits(t: torch.Tensor):
     """bf16 tensor -> numpy uint16 view of the same bytes (host)."""
     assert t.dtype == torch.bfloat16
     return t.detach().cpu().contiguous().view(torch.int16).numpy().view("uint16")
+
+
+def quantize_fp8_rows(w: torch.Tensor):
+    """Input preparation for the FP8-weight variant: for every output row
+    of the HF [out, in] matrix a power-of-two scale s = 2^ceil(log2(max|w| / 448))
+    (448 = largest E4M3 value) and q = E4M3(w / s) with torch's RNE conversion.
+    Returns (q as uint8 bytes, s fp32 [..., out]); the exact weight is q * s."""
+    wf = w.float()
+    amax = wf.abs().amax(dim=-1).clamp_min(1e-30)
+    s = torch.exp2(torch.ceil(torch.log2(amax / 448.0)))
+    q = (wf / s.unsqueeze(-1)).to(torch.float8_e4m3fn)
+    return q.view(torch.uint8), s.contiguous()
+
+
+def dequantize_fp8_rows(q: torch.Tensor, s: torch.Tensor):
+    """Exact fp32 value of q * s (E4M3 -> fp32 is exact; s is a power of two)."""
+    return q.view(torch.float8_e4m3fn).float() * s.unsqueeze(-1)

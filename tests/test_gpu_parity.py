@@ -479,3 +479,43 @@ def test_mixtral_decode_hybrid(moe, mixtral_weights, ep, tp):
     auxs = [res[e * tp][1] for e in range(ep)]
     e32, e16 = _check_group_outputs(host, 2, synth.bf16_bits(x), outs, auxs)
     print(f"EP{ep}xTP{tp}", e32, e16)
+
+
+# ---------------------------------------------------------------- FP8 weights
+def _fp8_inputs(shape, seed):
+    inp = _inputs(shape, seed)
+    qs = {n: synth.quantize_fp8_rows(inp[n]) for n in ("w1", "w3", "w2")}
+    # oracle inputs: the exact dequantised weights (fp32) and the bf16 tokens / router (exact in fp32)
+    host = {n: synth.dequantize_fp8_rows(*qs[n]).cpu().numpy() for n in qs}
+    host["x"] = inp["x"].float().cpu().numpy()
+    host["wg"] = inp["wg"].float().cpu().numpy()
+    return inp, qs, host
+
+
+@pytest.mark.parametrize("T,d,f,E", [(16, 64, 128, 4), (64, 512, 1024, 8), (300, 256, 512, 8), (7, 128, 256, 2)])
+def test_fp8_weights(moe, T, d, f, E):
+    """FP8 E4M3 weights with per-row power-of-two scales: the GPU must match the oracle
+    evaluated on the exact dequantised weights (same tolerance as bf16)."""
+    inp, qs, host = _fp8_inputs(synth.MoEShape(T=T, d=d, f=f, E=E, k=2), 800 + T)
+    blk = moe.MoEBlock(inp["wg"], qs["w1"], qs["w3"], qs["w2"], top_k=2, max_tokens=T,
+                       flags=moe.MOE_FLAG_FP8_WEIGHTS)
+    run = GpuRun(blk, inp["x"])
+    st = check_forward(run, host, 2)
+    print("fp8", T, d, f, E, st)
+    blk.close()
+
+
+def test_fp8_mixtral_decode(moe):
+    """64-token decode at Mixtral size with FP8 weights, all tokens vs the oracle."""
+    w = synth.make_weights(4096, 14336, 8, seed=43, device="cuda")
+    qs = {n: synth.quantize_fp8_rows(w[n]) for n in ("w1", "w3", "w2")}
+    host = {n: synth.dequantize_fp8_rows(*qs[n]).cpu().numpy() for n in qs}
+    x = synth.make_tokens(64, 4096, seed=44, device="cuda")
+    host["x"] = x.float().cpu().numpy()
+    host["wg"] = w["wg"].float().cpu().numpy()
+    blk = moe.MoEBlock(w["wg"], qs["w1"], qs["w3"], qs["w2"], top_k=2, max_tokens=64,
+                       flags=moe.MOE_FLAG_FP8_WEIGHTS)
+    run = GpuRun(blk, x)
+    st = check_forward(run, host, 2)
+    print("fp8 C2", st)
+    blk.close()
