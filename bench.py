@@ -532,7 +532,8 @@ def main():
                 "traffic": None, "kernel": "moe_gemm_kernel<kG1Tiled> (w1/w3 + SwiGLU)",
                 "peak_src": peaks["src"] + " (MEASURED_PEAKS.json bf16_tflops_sustained)"}
         step_frac = alg["flops"] / (ms * 1e-3) / 1e12 / pk
-    tr, tr_src = load_traffic(args.config) if world == 1 and par == "none" and not args.fp8 else (None, None)
+    tr, tr_src = load_traffic(args.config + ("_fp8" if args.fp8 else "")) if world == 1 and par == "none" \
+        else (None, None)
     roof["traffic"] = tr
     if tr is not None:
         roof["traffic_src"] = tr_src
