@@ -692,6 +692,18 @@ __device__ __forceinline__ uint32_t cvt_e4m3x2_f16x2(uint32_t two_fp8) {
     return r;
 }
 
+// 4 E4M3 bytes -> 4 fp16 equal to (e4m3 value) * 2^-8, EXACTLY, with integer ops only:
+// fp16 = sign << 15 | (e4m3 & 0x7F) << 7. E4M3 (bias 7) and fp16 (bias 15) differ by
+// 8 in the exponent bias, and E4M3 subnormals land on fp16 subnormals, so the bit
+// move is an exact scaling by 2^-8 for every finite code (the row scale absorbs 2^8).
+// Integer-ALU alternative to cvt.rn.f16x2.e4m3x2 (MOE_FP8_CVT_INSN=0); measured slower.
+__device__ __forceinline__ void e4m3x4_to_f16x4_scaled(uint32_t w, uint32_t& lo, uint32_t& hi) {
+    const uint32_t t0 = __byte_perm(w, 0u, 0x1404);  // b1 << 24 | b0 << 8
+    const uint32_t t1 = __byte_perm(w, 0u, 0x3424);  // b3 << 24 | b2 << 8
+    lo = (t0 & 0x80008000u) | ((t0 >> 1) & 0x3F803F80u);
+    hi = (t1 & 0x80008000u) | ((t1 >> 1) & 0x3F803F80u);
+}
+
 __device__ __forceinline__ uint32_t pack_f16x2(float lo, float hi) {
     __half2 v = __floats2half2_rn(lo, hi);
     return *reinterpret_cast<uint32_t*>(&v);
@@ -951,6 +963,13 @@ struct Fp8TmemCfg {
     static_assert(kS2 >= 2 && kS1 >= 4, "bad fp8 pipeline");
 };
 
+#ifndef MOE_FP8_CVT_INSN
+// 1: cvt.rn.f16x2.e4m3x2 (exact values); 0: integer bit move (values * 2^-8, also exact).
+// r01 A/B on one box: cvt 0.2987 ms vs bit move 0.3586 ms per decode step.
+#define MOE_FP8_CVT_INSN 1
+#endif
+constexpr float kFp8Rescale = MOE_FP8_CVT_INSN ? 1.0f : 256.0f;  // undoes the bit move's 2^-8 (exact)
+
 // Two converter groups (warps 6..9 and 10..13) take alternate k-blocks so that one
 // group's shared-memory / TMEM-store latency overlaps the other's.
 constexpr int kFp8tGroups = 1;  // r01: 2 groups measured slower (0.3466 vs 0.3388 ms per decode step)
@@ -1110,6 +1129,7 @@ __global__ void __launch_bounds__(kFp8tThreads, 1)
 #pragma unroll
                         for (int c = 0; c < 4; ++c) {
                             const uint4 v = vv[c];
+#if MOE_FP8_CVT_INSN
                             o[8 * c + 0] = cvt_e4m3x2_f16x2(v.x);
                             o[8 * c + 1] = cvt_e4m3x2_f16x2(v.x >> 16);
                             o[8 * c + 2] = cvt_e4m3x2_f16x2(v.y);
@@ -1118,6 +1138,12 @@ __global__ void __launch_bounds__(kFp8tThreads, 1)
                             o[8 * c + 5] = cvt_e4m3x2_f16x2(v.z >> 16);
                             o[8 * c + 6] = cvt_e4m3x2_f16x2(v.w);
                             o[8 * c + 7] = cvt_e4m3x2_f16x2(v.w >> 16);
+#else
+                            e4m3x4_to_f16x4_scaled(v.x, o[8 * c + 0], o[8 * c + 1]);
+                            e4m3x4_to_f16x4_scaled(v.y, o[8 * c + 2], o[8 * c + 3]);
+                            e4m3x4_to_f16x4_scaled(v.z, o[8 * c + 4], o[8 * c + 5]);
+                            e4m3x4_to_f16x4_scaled(v.w, o[8 * c + 6], o[8 * c + 7]);
+#endif
                         }
                         ptx::tmem_st32(a_base + s2 * C::kACols + (KB / 2) * h + 32 * half +
                                            (static_cast<uint32_t>(q * 32) << 16),
@@ -1150,7 +1176,7 @@ __global__ void __launch_bounds__(kFp8tThreads, 1)
             const int nchunks = (ti.n_valid + 15) / 16;
             if (KIND == kG1Swap) {
                 const float* sc = scales + (int64_t)ti.e * 2 * p.f + ti.m_idx * 256;
-                const float s1v = sc[r], s3v = sc[128 + r];
+                const float s1v = sc[r] * kFp8Rescale, s3v = sc[128 + r] * kFp8Rescale;
                 __half* hp = static_cast<__half*>(p.out) + static_cast<int64_t>(ti.b_row) * p.f + ti.m_idx * 128 + r;
 #pragma unroll 1
                 for (int cc = 0; cc < nchunks; ++cc) {
@@ -1169,7 +1195,7 @@ __global__ void __launch_bounds__(kFp8tThreads, 1)
                 }
             } else {
                 const int drow = ti.m_idx * 128 + r;
-                const float s2v = drow < p.d ? scales[(int64_t)ti.e * p.d + drow] : 0.f;
+                const float s2v = drow < p.d ? scales[(int64_t)ti.e * p.d + drow] * kFp8Rescale : 0.f;
                 float* y = static_cast<float*>(p.out) + p.out_split_stride * ti.split +
                            static_cast<int64_t>(ti.b_row) * p.d + drow;
 #pragma unroll 1

@@ -519,3 +519,25 @@ def test_fp8_mixtral_decode(moe):
     st = check_forward(run, host, 2)
     print("fp8 C2", st)
     blk.close()
+
+
+def test_cuda_graph_capture(moe):
+    """The single-GPU forward has no host synchronisation: it can be captured into a
+    CUDA graph (PDL edges included) and replayed with bit-identical results."""
+    for shape, flags in ((synth.MoEShape(T=64, d=256, f=512, E=8, k=2), 0),
+                         (synth.MoEShape(T=600, d=256, f=512, E=8, k=2), moe.MOE_FLAG_FORCE_TILED)):
+        inp = _inputs(shape, 900 + shape.T)
+        blk = _block(moe, inp, 2, shape.T, flags)
+        ref = blk.forward(inp["x"]).clone()
+        out = torch.empty_like(ref)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            moe.moe_forward(blk.ctx, inp["x"], shape.T, blk.router_w, blk.w13, blk.w2, out, None,
+                            torch.cuda.current_stream())
+        for _ in range(3):
+            out.zero_()
+            g.replay()
+            torch.cuda.synchronize()
+            assert torch.equal(out.view(torch.int16), ref.view(torch.int16))
+        blk.close()
