@@ -177,7 +177,10 @@ struct moe_ctx {
     __nv_bfloat16 *x_perm = nullptr, *h = nullptr;
     float* y = nullptr;
     int64_t y_elems = 0;
-    __nv_bfloat16 *stage_in = nullptr, *stage_out = nullptr;  // moe_forward_host staging
+    __nv_bfloat16 *stage_in = nullptr, *stage_out = nullptr;  // moe_forward_host staging (2 input slots)
+    cudaStream_t copy_stream = nullptr;                        // moe_forward_host uploads
+    cudaEvent_t slot_free[2]{}, slot_loaded[2]{};
+    int host_slot = 0;
     float* tp_partial = nullptr;                               // TP: fp32 partial [max_T, d]
     float* tp_scatter = nullptr;                               // TP: reduce-scatter result
     // EP staging
@@ -1000,7 +1003,13 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
     ALLOC(c->x_perm, sizeof(__nv_bfloat16) * c->cap * c->d);
     ALLOC(c->h, sizeof(__nv_bfloat16) * c->cap * c->f_local);
     ALLOC(c->y, sizeof(float) * c->y_elems);
-    ALLOC(c->stage_in, sizeof(__nv_bfloat16) * c->max_T * c->d);
+    ALLOC(c->stage_in, 2 * sizeof(__nv_bfloat16) * c->max_T * c->d);
+    if ((e = cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking)) != cudaSuccess)
+        return fail_init("copy stream", e);
+    for (int i = 0; i < 2; ++i)
+        if ((e = cudaEventCreateWithFlags(&c->slot_free[i], cudaEventDisableTiming)) != cudaSuccess ||
+            (e = cudaEventCreateWithFlags(&c->slot_loaded[i], cudaEventDisableTiming)) != cudaSuccess)
+            return fail_init("staging events", e);
     ALLOC(c->stage_out, sizeof(__nv_bfloat16) * c->max_T * c->d);
     if (cfg->par == MOE_PAR_TP) {
         ALLOC(c->tp_partial, sizeof(float) * c->max_T * c->d);
@@ -1069,6 +1078,11 @@ moe_status moe_destroy(moe_ctx* c) {
     for (void* b : bufs)
         if (b) cudaFree(b);
     if (c->h_counts) cudaFreeHost(c->h_counts);
+    for (int i = 0; i < 2; ++i) {
+        if (c->slot_free[i]) cudaEventDestroy(c->slot_free[i]);
+        if (c->slot_loaded[i]) cudaEventDestroy(c->slot_loaded[i]);
+    }
+    if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
     for (auto& ev : c->pending) { cudaEventDestroy(ev.a); cudaEventDestroy(ev.b); }
     for (auto ev : c->ev_pool) cudaEventDestroy(ev);
     delete c;
@@ -1152,9 +1166,25 @@ moe_status moe_forward_host(moe_ctx* c, const void* tokens_host, int32_t T, cons
     if (T > 0 && (!tokens_host || !out_host)) return fail(c, MOE_ERR_INVALID, "NULL host buffer");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const size_t bytes = (size_t)T * c->d * sizeof(__nv_bfloat16);
-    if (T > 0) CUDA_TRY(c, cudaMemcpyAsync(c->stage_in, tokens_host, bytes, cudaMemcpyHostToDevice, st));
-    if ((s = moe_forward(c, c->stage_in, T, router_w, w, c->stage_out, nullptr, stream))) return s;
-    if (T > 0) CUDA_TRY(c, cudaMemcpyAsync(out_host, c->stage_out, bytes, cudaMemcpyDeviceToHost, st));
+    // Double-buffered token staging: the host->device copy runs on the context's copy
+    // stream as soon as its slot's previous forward has finished, so consecutive calls
+    // overlap this call's upload with the previous call's forward; the forward waits
+    // for the upload, the result is copied back on `stream` (ready once the caller
+    // synchronises `stream`).
+    const int slot = c->host_slot;
+    c->host_slot ^= 1;
+    __nv_bfloat16* in = c->stage_in + (size_t)slot * c->max_T * c->d;
+    if (T > 0) {
+        CUDA_TRY(c, cudaStreamWaitEvent(c->copy_stream, c->slot_free[slot], 0));
+        CUDA_TRY(c, cudaMemcpyAsync(in, tokens_host, bytes, cudaMemcpyHostToDevice, c->copy_stream));
+        CUDA_TRY(c, cudaEventRecord(c->slot_loaded[slot], c->copy_stream));
+        CUDA_TRY(c, cudaStreamWaitEvent(st, c->slot_loaded[slot], 0));
+    }
+    if ((s = moe_forward(c, in, T, router_w, w, c->stage_out, nullptr, stream))) return s;
+    if (T > 0) {
+        CUDA_TRY(c, cudaEventRecord(c->slot_free[slot], st));
+        CUDA_TRY(c, cudaMemcpyAsync(out_host, c->stage_out, bytes, cudaMemcpyDeviceToHost, st));
+    }
     return MOE_OK;
 }
 
