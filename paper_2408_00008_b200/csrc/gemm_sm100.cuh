@@ -62,9 +62,14 @@ struct GemmCfg {
     static constexpr int kStagesRaw = (kSmemBudget - 2048) / kStageBytes;
     static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
     static constexpr int kSmemBytes = kStages * kStageBytes + 2048;  // + barriers + 1 KB align slack
-    static constexpr int kAccCols = 256;  // TMEM columns per accumulator stage (2 stages = 512)
+    // TMEM: 512 columns = kAccStages x kAccCols. The w1|w3 swap tile with NB = 256 token
+    // columns needs a 256-column accumulator for each of a and b -> one stage only.
+    static constexpr bool kWide = (KIND == kG1Swap && NB > 128);
+    static constexpr int kAccStages = kWide ? 1 : 2;
+    static constexpr int kAccCols = kWide ? 512 : 256;
+    static constexpr int kBOff = kWide ? 256 : 128;  // column of the w3 (b) accumulator in a stage
     static_assert(kStages >= 2, "pipeline too shallow");
-    static_assert(!kSwap || (NB >= 16 && NB <= 128 && (NB % 16) == 0), "bad NB");
+    static_assert(!kSwap || (NB >= 16 && NB <= 256 && (NB % 16) == 0), "bad NB");
 };
 
 struct TileInfo {
@@ -176,7 +181,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         ptx::fence_mbar_init();
     }
     if (warp == 1) {
-        ptx::tmem_alloc(tmem_base_slot, 2 * C::kAccCols);
+        ptx::tmem_alloc(tmem_base_slot, C::kAccStages * C::kAccCols);
         ptx::tmem_relinquish();
     }
 // MOE_PDL_PREFETCH=0 disables the pre-wait weight stages (A/B experiments, scripts/ab_decode.sh:
@@ -291,14 +296,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                         if (KIND == kG1Swap) {
                             // w3 half of the 256-row A tile (rows 128..255, +16 KB) -> columns +128
                             const uint64_t adesc3 = ptx::make_smem_desc_sw128(sa + 128 * 128);
-                            ptx::mma_bf16(d_tmem + 128, adesc3 + 2 * kk, bdesc + 2 * kk, idesc, accum);
+                            ptx::mma_bf16(d_tmem + C::kBOff, adesc3 + 2 * kk, bdesc + 2 * kk, idesc, accum);
                         }
                     }
                     ptx::mma_commit(&empty[stage]);  // frees the smem slot when these MMAs finish
                     if (++stage == S) { stage = 0; phase ^= 1; }
                 }
                 ptx::mma_commit(&tmem_full[acc]);    // accumulator ready for the epilogue
-                if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+                if (++acc == C::kAccStages) { acc = 0; acc_phase ^= 1; }
             }
         }
     } else {
@@ -363,7 +368,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 for (int c = 0; c < nchunks; ++c) {
                     uint32_t a[16], b[16];
                     ptx::tmem_ld16(tbase + c * 16, a);
-                    ptx::tmem_ld16(tbase + 128 + c * 16, b);
+                    ptx::tmem_ld16(tbase + C::kBOff + c * 16, b);
                     ptx::tmem_wait_ld();
 #pragma unroll
                     for (int i = 0; i < 16; ++i) {
@@ -397,7 +402,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(&tmem_empty[acc]);
-            if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+            if (++acc == C::kAccStages) { acc = 0; acc_phase ^= 1; }
         }
     }
     // Allow the next kernel in the stream to start its prologue.
@@ -406,7 +411,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     __syncthreads();
     if (warp == 1) {
         ptx::tc_fence_after();
-        ptx::tmem_dealloc(tmem_base, 2 * C::kAccCols);
+        ptx::tmem_dealloc(tmem_base, C::kAccStages * C::kAccCols);
     }
 }
 

@@ -194,7 +194,7 @@ struct moe_ctx {
     int64_t ep_exact_bytes = 32ll << 20;  // exact mode when a capacity exchange would move more bf16 bytes
     // TMA descriptors: workspace operands
     CUtensorMap tm_x_tiled{}, tm_h_tiled{};
-    CUtensorMap tm_x_swap[3]{}, tm_h_swap[3]{};  // NB = 32, 64, 128
+    CUtensorMap tm_x_swap[4]{}, tm_h_swap[4]{};  // NB = 32, 64, 128, 256
     // weight descriptor cache (keyed by pointer)
     struct WeightMaps {
         const void* w13 = nullptr;
@@ -477,33 +477,35 @@ moe_status launch_gemm_fp8t(moe_ctx* c, int slot, const GemmParams& p, const flo
                   (size_t)Fp8TmemCfg<KIND, NB, 64>::kSmemBytes, st, p, scales, a8, b);
 }
 
+// Decode (swap-AB) GEMM1 with token tile NB: bf16 weights, or FP8 weights widened in
+// TMEM (NB <= 64) / in shared memory (NB = 128).
 template <int NB>
-moe_status run_swap(moe_ctx* c, int nbi, const moe_expert_weights* w, int splits, cudaStream_t st) {
-    if constexpr (NB <= 64) {
-        if (c->fp8 && !c->fp8_smem_a) {  // weights widened into TMEM
-            GemmParams p1{c->counts, c->offsets, c->E_local, c->d, c->f_local, 1, c->h, 0};
-            moe_status s = launch_gemm_fp8t<kG1Swap, NB>(c, kSlotGemm1, p1, w->w13_scale, c->tm_w13,
-                                                         c->tm_x_swap[nbi], c->num_sms, st);
-            if (s) return s;
-            GemmParams p2{c->counts, c->offsets, c->E_local, c->d, c->f_local, splits, c->y, c->split_stride};
+moe_status run_swap_g1(moe_ctx* c, int nbi, const moe_expert_weights* w, cudaStream_t st) {
+    GemmParams p1{c->counts, c->offsets, c->E_local, c->d, c->f_local, 1, c->h, 0};
+    if constexpr (NB <= 64)
+        if (c->fp8 && !c->fp8_smem_a)
+            return launch_gemm_fp8t<kG1Swap, NB>(c, kSlotGemm1, p1, w->w13_scale, c->tm_w13, c->tm_x_swap[nbi],
+                                                 c->num_sms, st);
+    if constexpr (NB <= 128)
+        if (c->fp8)
+            return launch_gemm_fp8<kG1Swap, NB>(c, kSlotGemm1, p1, w->w13_scale, c->tm8_w13_64, c->tm_x_swap[nbi],
+                                                c->num_sms, st);
+    return launch_gemm<kG1Swap, NB>(c, kSlotGemm1, p1, c->tm_w13, c->tm_x_swap[nbi], c->num_sms, st);
+}
+
+template <int NB>
+moe_status run_swap_g2(moe_ctx* c, int nbi, const moe_expert_weights* w, int splits, cudaStream_t st) {
+    GemmParams p2{c->counts, c->offsets, c->E_local, c->d, c->f_local, splits, c->y, c->split_stride};
+    if constexpr (NB <= 64)
+        if (c->fp8 && !c->fp8_smem_a)
             return launch_gemm_fp8t<kG2Swap, NB>(c, kSlotGemm2, p2, w->w2_scale, c->tm_w2_swap, c->tm_h_swap[nbi],
                                                  c->num_sms, st);
+    if constexpr (NB <= 128)
+        if (c->fp8) {
+            p2.splits = std::min(splits, c->f_local / kBK);
+            return launch_gemm_fp8<kG2Swap, NB>(c, kSlotGemm2, p2, w->w2_scale, c->tm8_w2_64, c->tm_h_swap[nbi],
+                                                c->num_sms, st);
         }
-    }
-    if (c->fp8) {  // weights widened in shared memory (64-element K blocks)
-        const int sp = std::min(splits, c->f_local / kBK);
-        GemmParams p1{c->counts, c->offsets, c->E_local, c->d, c->f_local, 1, c->h, 0};
-        moe_status s = launch_gemm_fp8<kG1Swap, NB>(c, kSlotGemm1, p1, w->w13_scale, c->tm8_w13_64,
-                                                    c->tm_x_swap[nbi], c->num_sms, st);
-        if (s) return s;
-        GemmParams p2{c->counts, c->offsets, c->E_local, c->d, c->f_local, sp, c->y, c->split_stride};
-        return launch_gemm_fp8<kG2Swap, NB>(c, kSlotGemm2, p2, w->w2_scale, c->tm8_w2_64, c->tm_h_swap[nbi],
-                                            c->num_sms, st);
-    }
-    GemmParams p1{c->counts, c->offsets, c->E_local, c->d, c->f_local, 1, c->h, 0};
-    moe_status s = launch_gemm<kG1Swap, NB>(c, kSlotGemm1, p1, c->tm_w13, c->tm_x_swap[nbi], c->num_sms, st);
-    if (s) return s;
-    GemmParams p2{c->counts, c->offsets, c->E_local, c->d, c->f_local, splits, c->y, c->split_stride};
     return launch_gemm<kG2Swap, NB>(c, kSlotGemm2, p2, c->tm_w2_swap, c->tm_h_swap[nbi], c->num_sms, st);
 }
 
@@ -585,10 +587,21 @@ moe_status run_gemms(moe_ctx* c, bool swap, int64_t rows_bound, int64_t rows_tot
         splits = (int)std::max<int64_t>(1, std::min<int64_t>(splits, c->y_elems / (rows_needed * c->d)));
         splits = std::min(splits, c->f_local / (c->fp8_kb128 ? 128 : kBK));  // every split owns >= 1 K block
         c->split_stride = rows_needed * c->d;
-        const int nbw = (int)std::max<int64_t>(32, std::min<int64_t>(128, next_pow2((int)std::min<int64_t>(rows_bound, 1 << 20))));
-        if (nbw == 32) s = run_swap<32>(c, 0, &c->cur_w, splits, st);
-        else if (nbw == 64) s = run_swap<64>(c, 1, &c->cur_w, splits, st);
-        else s = run_swap<128>(c, 2, &c->cur_w, splits, st);
+        // Token tile NB: one tile covers an expert's rows when possible (the weight tile
+        // then streams once). GEMM1 stops at 128 (NB = 256 leaves its w1|w3 accumulators
+        // single-buffered: measured slower, 32-layer stack r01), GEMM2 goes to 256;
+        // FP8 kernels stop at 128.
+        const int nbw = (int)std::max<int64_t>(32, std::min<int64_t>(256, next_pow2((int)std::min<int64_t>(rows_bound, 1 << 20))));
+        const int nb1 = std::min(nbw, 128), nb2 = c->fp8 ? nb1 : nbw;
+        const int i1 = nb1 == 32 ? 0 : nb1 == 64 ? 1 : 2;
+        if (nb1 == 32) s = run_swap_g1<32>(c, i1, &c->cur_w, st);
+        else if (nb1 == 64) s = run_swap_g1<64>(c, i1, &c->cur_w, st);
+        else s = run_swap_g1<128>(c, i1, &c->cur_w, st);
+        if (s) return s;
+        if (nb2 == 32) s = run_swap_g2<32>(c, 0, &c->cur_w, splits, st);
+        else if (nb2 == 64) s = run_swap_g2<64>(c, 1, &c->cur_w, splits, st);
+        else if (nb2 == 128) s = run_swap_g2<128>(c, 2, &c->cur_w, splits, st);
+        else s = run_swap_g2<256>(c, 3, &c->cur_w, splits, st);
         if (s) return s;
     } else if (!(c->cfg.flags & MOE_FLAG_NO_PAIR)) {
         // CTA-pair (cta_group::2) 256x256 tiles, one cluster of 2 CTAs per TPC
@@ -1039,8 +1052,8 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
     // workspace TMA descriptors
     bool ok = encode_map(&c->tm_x_tiled, c->x_perm, 2, c->d, c->cap, 1, 128) &&
               encode_map(&c->tm_h_tiled, c->h, 2, c->f_local, c->cap, 1, 128);
-    const uint32_t nbs[3] = {32, 64, 128};
-    for (int i = 0; i < 3 && ok; ++i)
+    const uint32_t nbs[4] = {32, 64, 128, 256};
+    for (int i = 0; i < 4 && ok; ++i)
         ok = encode_map(&c->tm_x_swap[i], c->x_perm, 2, c->d, c->cap, 1, nbs[i]) &&
              encode_map(&c->tm_h_swap[i], c->h, 2, c->f_local, c->cap, 1, nbs[i]);
     if (!ok) {
@@ -1052,6 +1065,7 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
         (as = set_gemm_attr<kG1Swap, 32>(c)) || (as = set_gemm_attr<kG2Swap, 32>(c)) ||
         (as = set_gemm_attr<kG1Swap, 64>(c)) || (as = set_gemm_attr<kG2Swap, 64>(c)) ||
         (as = set_gemm_attr<kG1Swap, 128>(c)) || (as = set_gemm_attr<kG2Swap, 128>(c)) ||
+        (as = set_gemm_attr<kG2Swap, 256>(c)) ||
         (as = set_pair_attr<kG1Pair>(c)) || (as = set_pair_attr<kG2Pair>(c)) ||
         (as = set_fp8_attr<kG1Swap, 32>(c)) || (as = set_fp8_attr<kG2Swap, 32>(c)) ||
         (as = set_fp8_attr<kG1Swap, 64>(c)) || (as = set_fp8_attr<kG2Swap, 64>(c)) ||
