@@ -522,12 +522,14 @@ struct CombineParams {
 
 // K5 (a9): out[t] = bf16_rne( sum_j w_j * (sum_s y_s[pos_j]) (+ x[t]) ), fixed order:
 // splits ascending, then r = w_0*s_0, r = fma(w_1, s_1, r), then + x.
-// grid = (ceil(d/4096), T): each thread owns 4 float4 column groups of one token
+// grid = T * ceil(d/4096) blocks: each thread owns 4 float4 column groups of one token
 // (strided by 1024 columns), so 8 independent 16-byte loads per thread are in flight.
 constexpr int kCombineVec = 4;
 __global__ void __launch_bounds__(256) moe_combine_kernel(const CombineParams p) {
-    const int t = blockIdx.y;
-    const int c0 = blockIdx.x * 1024 * kCombineVec + threadIdx.x * 4;
+    // 1-D grid (T may exceed the 65535 limit of gridDim.y): block b -> token b / nxb
+    const int nxb = (p.d + 1024 * kCombineVec - 1) / (1024 * kCombineVec);
+    const int t = blockIdx.x / nxb;
+    const int c0 = (blockIdx.x % nxb) * 1024 * kCombineVec + threadIdx.x * 4;
     ptx::pdl_wait();
     int32_t pr[2];
     float w[2];
@@ -588,8 +590,9 @@ __global__ void __launch_bounds__(256) moe_combine_kernel(const CombineParams p)
 // slot (fp32 rows; splits summed in ascending order, as in the combine).
 __global__ void __launch_bounds__(256) moe_ep_gather_kernel(const float* y, int64_t split_stride, int splits,
                                                             const int32_t* pos, int nslots, int d, float* ysend) {
-    const int slot = blockIdx.y;
-    const int c = blockIdx.x * 1024 + threadIdx.x * 4;
+    const int nxb = (d + 1023) / 1024;  // 1-D grid: block b -> slot b / nxb
+    const int slot = blockIdx.x / nxb;
+    const int c = (blockIdx.x % nxb) * 1024 + threadIdx.x * 4;
     ptx::pdl_wait();
     if (slot < nslots && c < d) {
         const int32_t pr = pos[slot];

@@ -1353,14 +1353,14 @@ moe_status forward_impl(moe_ctx* c, const void* tokens, int32_t T, const void* r
         cp.x = residual ? static_cast<const __nv_bfloat16*>(tokens) : nullptr;
         cp.out = static_cast<__nv_bfloat16*>(out);
         cp.out_f32 = aux ? aux->out_f32 : nullptr;
-        return launch(c, kSlotCombine, moe_combine_kernel, dim3((c->d + 4095) / 4096, T), dim3(256), 0, st, cp);
+        return launch(c, kSlotCombine, moe_combine_kernel, dim3((unsigned)((c->d + 4095) / 4096 * (int64_t)T)), dim3(256), 0, st, cp);
     }
     // ---- TP: fp32 partial of this rank's ffn slice -> fp32 reduce-scatter ->
     // one bf16 rounding (+ residual) -> bf16 all-gather (R7: single rounding)
     cp.x = nullptr;
     cp.out = nullptr;
     cp.out_f32 = c->tp_partial;
-    if ((s = launch(c, kSlotCombine, moe_combine_kernel, dim3((c->d + 4095) / 4096, T), dim3(256), 0, st, cp)))
+    if ((s = launch(c, kSlotCombine, moe_combine_kernel, dim3((unsigned)((c->d + 4095) / 4096 * (int64_t)T)), dim3(256), 0, st, cp)))
         return s;
     const int64_t n = (int64_t)T * c->d, cnt = n / c->G, base = cnt * c->rank;
     const CommRef tpc = tp_comm(c);
@@ -1458,7 +1458,7 @@ moe_status forward_ep(moe_ctx* c, const void* tokens, int32_t T, const void* rou
                     : rows_expected <= (int64_t)c->swap_rows_per_expert * c->E_local;
     int splits = 1;
     if ((s = run_gemms(c, swap, std::min<int64_t>(R, (int64_t)G * c->max_T), R, &splits, st))) return s;
-    if ((s = launch(c, kSlotExchange, moe_ep_gather_kernel, dim3((c->d + 1023) / 1024, (unsigned)R), dim3(256), 0,
+    if ((s = launch(c, kSlotExchange, moe_ep_gather_kernel, dim3((unsigned)((c->d + 1023) / 1024 * R)), dim3(256), 0,
                     st, static_cast<const float*>(c->y), c->split_stride, splits,
                     static_cast<const int32_t*>(c->ep_rpos), (int)R, c->d, c->ep_ysend)))
         return s;
@@ -1496,7 +1496,7 @@ moe_status forward_ep(moe_ctx* c, const void* tokens, int32_t T, const void* rou
     cp.T = T; cp.d = c->d; cp.k = c->k;
     cp.out = static_cast<__nv_bfloat16*>(out);
     cp.out_f32 = aux ? aux->out_f32 : nullptr;
-    return launch(c, kSlotCombine, moe_combine_kernel, dim3((c->d + 4095) / 4096, T), dim3(256), 0, st, cp);
+    return launch(c, kSlotCombine, moe_combine_kernel, dim3((unsigned)((c->d + 4095) / 4096 * (int64_t)T)), dim3(256), 0, st, cp);
 }
 
 }  // namespace

@@ -541,3 +541,27 @@ def test_cuda_graph_capture(moe):
             torch.cuda.synchronize()
             assert torch.equal(out.view(torch.int16), ref.view(torch.int16))
         blk.close()
+
+
+def test_large_token_counts(moe):
+    """T > 65535 (1-D grids everywhere; no gridDim.y limit), tiny hidden size."""
+    shape = synth.MoEShape(T=70000, d=64, f=128, E=4, k=2)
+    inp = _inputs(shape, 1234)
+    blk = _block(moe, inp, 2, shape.T)
+    run = GpuRun(blk, inp["x"])
+    rng = np.random.default_rng(1)
+    toks = np.unique(np.concatenate([[0, 65535, 65536, shape.T - 1], rng.choice(shape.T, 60, replace=False)]))
+    check_forward(run, to_host_inputs(inp), 2, tokens=toks)
+    blk.close()
+
+
+def test_ep_exact_many_slots(moe):
+    """EP exact-count exchange with more than 65535 receive slots (G * max_tokens * k)."""
+    shape = synth.MoEShape(T=40000, d=64, f=128, E=4, k=2)
+    inp = _inputs(shape, 4321)
+    host = to_host_inputs(inp)
+    shards = [inp["x"][:20000], inp["x"][20000:]]
+    res = _run_group(moe, inp, moe.MOE_PAR_EP, 2, shards, flags=moe.MOE_FLAG_EP_EXACT, max_tokens=20000)
+    outs = [r[0] for r in res]
+    auxs = [r[1] for r in res]
+    _check_group_outputs(host, 2, host["x"], outs, auxs)
