@@ -951,10 +951,11 @@ __global__ void __launch_bounds__(kFp8Threads, 1)
 template <int KIND, int NB, int KB>
 struct Fp8TmemCfg {
     static_assert(NB <= 64, "TMEM-A fp8 variant: NB <= 64");
-    static_assert(KB == 64 || KB == 128, "K per stage");
+    static_assert(KB == 64 || KB == 128 || KB == 256, "K per stage");
     static constexpr int kHalves = KIND == kG1Swap ? 2 : 1;
     static constexpr int kARows = 128 * kHalves;
-    static constexpr int kA8Bytes = kARows * KB;              // fp8 rows x KB bytes
+    static constexpr int kA8Sub = kARows * (KB < 128 ? KB : 128);  // one TMA box: rows x min(KB,128) B
+    static constexpr int kA8Bytes = kARows * KB;              // fp8 rows x KB bytes (KB/128 boxes)
     static constexpr int kBSub = NB * 128;                    // one 64-element fp16 token atom
     static constexpr int kBBytes = kBSub * (KB / 64);
     static constexpr int kAcc = kHalves * NB;                 // TMEM columns per accumulator stage
@@ -965,7 +966,7 @@ struct Fp8TmemCfg {
     static constexpr int kS1Raw = (kSmemBudget - 2048) / kLoadBytes;
     static constexpr int kS1 = kS1Raw > 10 ? 10 : kS1Raw;
     static constexpr int kSmemBytes = kS1 * kLoadBytes + 2048;
-    static_assert(kS2 >= 2 && kS1 >= 4, "bad fp8 pipeline");
+    static_assert(kS2 >= 2 && kS1 >= 3, "bad fp8 pipeline");
 };
 
 #ifndef MOE_FP8_CVT_INSN
@@ -1049,8 +1050,10 @@ __global__ void __launch_bounds__(kFp8tThreads, 1)
                     ptx::mbar_wait(&empty1[st], ph ^ 1);
                     ptx::mbar_arrive_expect_tx(&full1[st], C::kLoadBytes);
                     const int kc = (ti.kb0 + kb) * KB;
-                    ptx::tma_load_3d(&tmA8, &full1[st], ring8 + st * C::kA8Bytes, kc, ti.a_row, ti.e,
-                                     ptx::kEvictFirst);
+#pragma unroll
+                    for (int sub = 0; sub < (KB > 128 ? KB / 128 : 1); ++sub)
+                        ptx::tma_load_3d(&tmA8, &full1[st], ring8 + st * C::kA8Bytes + sub * C::kA8Sub, kc + 128 * sub,
+                                         ti.a_row, ti.e, ptx::kEvictFirst);
 #pragma unroll
                     for (int sub = 0; sub < KB / 64; ++sub)
                         ptx::tma_load_2d(&tmB, &full1[st], ring_b + st * C::kBBytes + sub * C::kBSub, kc + 64 * sub,
@@ -1120,15 +1123,16 @@ __global__ void __launch_bounds__(kFp8tThreads, 1)
 #pragma unroll
                 for (int h = 0; h < C::kHalves; ++h) {
                     const int rr = r + 128 * h;
-                    const uint32_t srow = ptx::smem_u32(src + rr * KB);
+                    const uint32_t srow = ptx::smem_u32(src + rr * (KB < 128 ? KB : 128));
 #pragma unroll
                     for (int half = 0; half < KB / 64; ++half) {   // 64 K elements -> 32 TMEM columns
                         uint4 vv[4];
 #pragma unroll
                         for (int c = 0; c < 4; ++c) {  // all shared loads issued first
                             const int lc = 4 * half + c;  // logical 16-byte chunk of the row
-                            const int pc = KB == 64 ? (lc ^ ((rr >> 1) & 3)) : (lc ^ (rr & 7));  // 64B / 128B swizzle
-                            vv[c] = ptx::lds128(srow + 16 * pc);
+                            // 64B / 128B swizzle inside a box; KB = 256 rows span two 128-byte boxes
+                            const int pc = KB == 64 ? (lc ^ ((rr >> 1) & 3)) : ((lc & 7) ^ (rr & 7));
+                            vv[c] = ptx::lds128(srow + (lc >> 3) * C::kA8Sub + 16 * pc);
                         }
                         uint32_t o[32];
 #pragma unroll

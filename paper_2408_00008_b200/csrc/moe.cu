@@ -164,6 +164,7 @@ struct moe_ctx {
     int64_t split_stride = 0; // elements between split-K partial buffers of this forward
     bool fp8 = false;             // MOE_FLAG_FP8_WEIGHTS
     bool fp8_smem_a = false;
+    bool fp8_g2_kb256 = false;    // fp8 w2 GEMM with 256-element K blocks (f_local % 256 == 0)
     bool fp8_kb128 = false;       // fp8 TMEM-A GEMMs with 128-element K blocks (d % 128 == 0); env
                                   // MOE_FP8_KB=64 selects 64 (r01: 0.3304 ms vs 0.2975 ms per step)      // env MOE_FP8_SMEM_A=1: widen fp8 weights in smem (not TMEM) at NB <= 64
     moe_expert_weights cur_w{};   // weights of the current forward
@@ -292,6 +293,10 @@ moe_status set_fp8t_attr(moe_ctx* c) {
                                      Fp8TmemCfg<KIND, NB, 64>::kSmemBytes));
     CUDA_TRY(c, cudaFuncSetAttribute(moe_gemm_fp8t_kernel<KIND, NB, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      Fp8TmemCfg<KIND, NB, 128>::kSmemBytes));
+    if (KIND == kG2Swap)
+        CUDA_TRY(c, cudaFuncSetAttribute(moe_gemm_fp8t_kernel<kG2Swap, NB, 256>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         Fp8TmemCfg<kG2Swap, NB, 256>::kSmemBytes));
     return MOE_OK;
 }
 
@@ -470,6 +475,9 @@ moe_status launch_gemm_fp8(moe_ctx* c, int slot, const GemmParams& p, const floa
 template <int KIND, int NB>
 moe_status launch_gemm_fp8t(moe_ctx* c, int slot, const GemmParams& p, const float* scales, const CUtensorMap& a8,
                             const CUtensorMap& b, int grid, cudaStream_t st) {
+    if (c->fp8_kb128 && KIND == kG2Swap && c->fp8_g2_kb256)  // 256-element K blocks (two 128-byte boxes)
+        return launch(c, slot, moe_gemm_fp8t_kernel<kG2Swap, NB, 256>, dim3(grid), dim3(kFp8tThreads),
+                      (size_t)Fp8TmemCfg<kG2Swap, NB, 256>::kSmemBytes, st, p, scales, a8, b);
     if (c->fp8_kb128)  // 128-element K blocks (maps encoded with a 128-byte fp8 box)
         return launch(c, slot, moe_gemm_fp8t_kernel<KIND, NB, 128>, dim3(grid), dim3(kFp8tThreads),
                       (size_t)Fp8TmemCfg<KIND, NB, 128>::kSmemBytes, st, p, scales, a8, b);
@@ -585,7 +593,7 @@ moe_status run_gemms(moe_ctx* c, bool swap, int64_t rows_bound, int64_t rows_tot
         const int64_t rows_needed = round_up(rows_total + (int64_t)c->E_local * (kSegAlign - 1), kSegAlign);
         splits = c->cfg.split_k ? c->cfg.split_k : c->max_splits;
         splits = (int)std::max<int64_t>(1, std::min<int64_t>(splits, c->y_elems / (rows_needed * c->d)));
-        splits = std::min(splits, c->f_local / (c->fp8_kb128 ? 128 : kBK));  // every split owns >= 1 K block
+        splits = std::min(splits, c->f_local / (c->fp8_g2_kb256 ? 256 : c->fp8_kb128 ? 128 : kBK));  // >= 1 K block per split
         c->split_stride = rows_needed * c->d;
         // Token tile NB: one tile covers an expert's rows when possible (the weight tile
         // then streams once). GEMM1 stops at 128 (NB = 256 leaves its w1|w3 accumulators
@@ -962,7 +970,9 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
     c->fp8 = (cfg->flags & MOE_FLAG_FP8_WEIGHTS) != 0;
     if (const char* v = getenv("MOE_FP8_SMEM_A")) c->fp8_smem_a = atoi(v) != 0;
     c->fp8_kb128 = c->fp8 && c->d % 128 == 0 && c->f_local % 128 == 0;
-    if (const char* v = getenv("MOE_FP8_KB")) c->fp8_kb128 = c->fp8_kb128 && atoi(v) == 128;
+    if (const char* v = getenv("MOE_FP8_KB")) c->fp8_kb128 = c->fp8_kb128 && atoi(v) >= 128;
+    c->fp8_g2_kb256 = c->fp8_kb128 && c->f_local % 256 == 0;
+    if (const char* v = getenv("MOE_FP8_G2_KB")) c->fp8_g2_kb256 = c->fp8_g2_kb256 && atoi(v) == 256;
     if (const char* pt = getenv("MOE_PAIR_TUNE")) c->pair_tune = atoi(pt);
     // router blocks of >= 2 rows; EP also routes the G*max_T*k receive slots
     c->nblk_max = (int)(((int64_t)c->max_T * (c->ep_world > 1 ? c->ep_world * c->k : 1) + 1) / 2 + 1);
