@@ -95,6 +95,10 @@ typedef enum {
 #define MOE_FLAG_EP_EXACT    0x20u /* EP: always exchange exact row counts (one host sync per forward);
                                       default: exact only when a fixed-capacity exchange would move
                                       more than 32 MB, i.e. prefill-sized batches                  */
+#define MOE_FLAG_GATHER      0x80u /* bf16, non-EP: the w1/w3 GEMM fetches token rows itself with TMA
+                                      tile::gather4 instead of step 7 copying them into a permuted
+                                      buffer. Bit-identical results; measured
+                                      SLOWER on B200, so off by default            */
 
 typedef struct {
     int32_t hidden;      /* d: 4096 for Mixtral (C1: 64). Must be a multiple of 64.   */

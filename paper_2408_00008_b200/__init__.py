@@ -32,6 +32,7 @@ MOE_PAR_NONE, MOE_PAR_EP, MOE_PAR_TP, MOE_PAR_HYBRID = 0, 1, 2, 3
 MOE_FLAG_RESIDUAL, MOE_FLAG_FORCE_SWAP, MOE_FLAG_FORCE_TILED, MOE_FLAG_NO_PDL, MOE_FLAG_NO_PAIR = 0x1, 0x2, 0x4, 0x8, 0x10
 MOE_FLAG_EP_EXACT = 0x20
 MOE_FLAG_FP8_WEIGHTS = 0x40
+MOE_FLAG_GATHER = 0x80
 NUM_KERNEL_SLOTS = 8
 KERNEL_SLOTS = ("router", "permute", "gemm1_w13_swiglu", "gemm2_w2", "combine", "dispatch", "exchange", "pack")
 

@@ -43,6 +43,10 @@ struct GemmParams {
     int32_t raster;          // pair kernels: tile order, see pair_decode
     int32_t band;            // pair kernels: band width (tiles) of the banded orders
     uint64_t hint_a, hint_b; // pair kernels: L2 cache-policy operands of the A / B TMA loads
+    // kG1* gather mode (nullable): token row of each permuted row. The token operand is
+    // then fetched with TMA tile::gather4 straight from the caller's rows (its map has a
+    // {64, 1} box) instead of from a materialised permuted copy.
+    const int32_t* src_row;
 };
 
 constexpr int kGemmThreads = 192;
@@ -214,52 +218,68 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
     if (warp == 0) {
         // ---------------------------------------------------------------- TMA producer
-        if (lane == 0) {
-            int stage = 0;
-            uint32_t phase = 0;
-            int pre = 0;  // k-blocks of the first tile whose weight loads precede the wait
-            if (C::kSwap && MOE_PDL_PREFETCH > 0) {
-                if ((int)blockIdx.x < total) {
-                    TileInfo t0;
-                    decode_tile<KIND, NB>(blockIdx.x, p, s_counts, s_offsets, t0);
-                    pre = min(S, t0.nkb);
+        // Lane 0 waits for free stages and issues the loads; in gather mode every lane
+        // then issues one tile::gather4 (4 token rows) of the token operand.
+        constexpr int kTokRows = C::kSwap ? NB : 128;
+        constexpr bool kCanGather = C::kG1 && kTokRows <= 128;
+        const bool gather = kCanGather && p.src_row != nullptr;
+        const CUtensorMap* tm_tok = C::kSwap ? &tmB : &tmA;
+        int stage = 0;
+        uint32_t phase = 0;
+        int pre = 0;  // k-blocks of the first tile whose weight loads precede the wait
+        if (C::kSwap && MOE_PDL_PREFETCH > 0) {
+            if ((int)blockIdx.x < total) {
+                TileInfo t0;
+                decode_tile<KIND, NB>(blockIdx.x, p, s_counts, s_offsets, t0);
+                pre = min(S, t0.nkb);
+                if (lane == 0)
                     for (int kb = 0; kb < pre; ++kb) {  // fresh stages: no empty-wait needed
                         ptx::mbar_arrive_expect_tx(&full[kb], C::kStageBytes);
                         ptx::tma_load_3d(&tmA, &full[kb], smem_a + kb * C::kABytes, (t0.kb0 + kb) * kBK, t0.a_row,
                                          t0.e, ptx::kEvictFirst);
                     }
-                }
-                ptx::pdl_wait();
             }
-            bool first = true;
-            for (int t = blockIdx.x; t < total; t += gridDim.x) {
-                TileInfo ti;
-                decode_tile<KIND, NB>(t, p, s_counts, s_offsets, ti);
-                for (int kb = 0; kb < ti.nkb; ++kb) {
-                    const int kc = (ti.kb0 + kb) * kBK;
-                    uint8_t* sa = smem_a + stage * C::kABytes;
-                    uint8_t* sb = smem_b + stage * C::kBBytes;
-                    if (first && kb < pre) {
-                        // weights already in flight on this armed stage: add the token operand
-                        ptx::tma_load_2d(&tmB, &full[stage], sb, kc, ti.b_row, ptx::kEvictLast);
-                        if (++stage == S) { stage = 0; phase ^= 1; }
-                        continue;
+            ptx::pdl_wait();
+        }
+        bool first = true;
+        for (int t = blockIdx.x; t < total; t += gridDim.x) {
+            TileInfo ti;
+            decode_tile<KIND, NB>(t, p, s_counts, s_offsets, ti);
+            const int tok_row = C::kSwap ? ti.b_row : ti.a_row;
+            int4 rows = make_int4(0, 0, 0, 0);
+            if (gather && lane < kTokRows / 4) {
+                const int32_t* sr = p.src_row + tok_row + 4 * lane;
+                rows = make_int4(sr[0], sr[1], sr[2], sr[3]);
+            }
+            for (int kb = 0; kb < ti.nkb; ++kb) {
+                const int kc = (ti.kb0 + kb) * kBK;
+                uint8_t* sa = smem_a + stage * C::kABytes;
+                uint8_t* sb = smem_b + stage * C::kBBytes;
+                uint8_t* s_tok = C::kSwap ? sb : sa;
+                const bool armed = first && kb < pre;  // weights already in flight on this stage
+                if (lane == 0) {
+                    if (!armed) {
+                        ptx::mbar_wait(&empty[stage], phase ^ 1);
+                        ptx::mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
                     }
-                    ptx::mbar_wait(&empty[stage], phase ^ 1);
-                    ptx::mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
                     if (C::kSwap) {
                         // A = weights (3D map [K, rows, E]) streamed once: evict-first.
-                        ptx::tma_load_3d(&tmA, &full[stage], sa, kc, ti.a_row, ti.e, ptx::kEvictFirst);
+                        if (!armed) ptx::tma_load_3d(&tmA, &full[stage], sa, kc, ti.a_row, ti.e, ptx::kEvictFirst);
                         // B = permuted tokens / activations (2D map [K, Cap]): keep in L2.
-                        ptx::tma_load_2d(&tmB, &full[stage], sb, kc, ti.b_row, ptx::kEvictLast);
+                        if (!gather) ptx::tma_load_2d(&tmB, &full[stage], sb, kc, ti.b_row, ptx::kEvictLast);
                     } else {
-                        ptx::tma_load_2d(&tmA, &full[stage], sa, kc, ti.a_row, ptx::kEvictLast);
+                        if (!gather) ptx::tma_load_2d(&tmA, &full[stage], sa, kc, ti.a_row, ptx::kEvictLast);
                         ptx::tma_load_3d(&tmB, &full[stage], sb, kc, ti.b_row, ti.e, ptx::kEvictNormal);
                     }
-                    if (++stage == S) { stage = 0; phase ^= 1; }
                 }
-                first = false;
+                if (gather) {
+                    __syncwarp();  // the stage is armed before any gather completes on it
+                    if (lane < kTokRows / 4)
+                        ptx::tma_gather4(tm_tok, &full[stage], s_tok + lane * 512, kc, rows, ptx::kEvictLast);
+                }
+                if (++stage == S) { stage = 0; phase ^= 1; }
             }
+            first = false;
         }
     } else if (warp == 1) {
         // ---------------------------------------------------------------- MMA issuer
@@ -541,24 +561,36 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
     if (warp == 0) {
         // ---------------------------------------------------------------- TMA producer (both CTAs)
-        if (lane == 0) {
-            int stage = 0;
-            uint32_t phase = 0;
-            for (int t = cid; t < total; t += ncl) {
-                TileInfo ti;
-                pair_decode<KIND>(t, p, s_counts, s_offsets, ti);
-                const int n_mma = KIND == kG1Pair ? 256 : min(256, p.d - ti.n_idx * 256);
-                const int a_row = ti.seg + ti.m_idx * 256 + (int)crank * 128;
-                const int b_row = ti.n_idx * 256 + (int)crank * (n_mma / 2);
-                for (int kb = 0; kb < ti.nkb; ++kb) {
+        // Lane 0 waits for free stages and issues the loads; in gather mode (kG1Pair with
+        // src_row) every lane issues one tile::gather4 of this CTA's 128 token rows.
+        const bool gather = KIND == kG1Pair && p.src_row != nullptr;
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int t = cid; t < total; t += ncl) {
+            TileInfo ti;
+            pair_decode<KIND>(t, p, s_counts, s_offsets, ti);
+            const int n_mma = KIND == kG1Pair ? 256 : min(256, p.d - ti.n_idx * 256);
+            const int a_row = ti.seg + ti.m_idx * 256 + (int)crank * 128;
+            const int b_row = ti.n_idx * 256 + (int)crank * (n_mma / 2);
+            int4 rows = make_int4(0, 0, 0, 0);
+            if (gather) {
+                const int32_t* sr = p.src_row + a_row + 4 * lane;
+                rows = make_int4(sr[0], sr[1], sr[2], sr[3]);
+            }
+            for (int kb = 0; kb < ti.nkb; ++kb) {
+                const uint32_t fb = ptx::map_cluster(&full[stage], 0);
+                const int kc = kb * kBK;
+                if (lane == 0) {
                     ptx::mbar_wait(&empty[stage], phase ^ 1);
-                    const uint32_t fb = ptx::map_cluster(&full[stage], 0);
                     if (leader) ptx::mbar_arrive_expect_tx(&full[stage], 2 * kPairStageBytes);
-                    const int kc = kb * kBK;
-                    ptx::tma_load_2d_pair(&tmA, fb, smem_a + stage * 16384, kc, a_row, p.hint_a);
+                    if (!gather) ptx::tma_load_2d_pair(&tmA, fb, smem_a + stage * 16384, kc, a_row, p.hint_a);
                     ptx::tma_load_3d_pair(&tmB, fb, smem_b + stage * 16384, kc, b_row, ti.e, p.hint_b);
-                    if (++stage == S) { stage = 0; phase ^= 1; }
                 }
+                if (gather) {
+                    __syncwarp();
+                    ptx::tma_gather4_pair(&tmA, fb, smem_a + stage * 16384 + lane * 512, kc, rows, p.hint_a);
+                }
+                if (++stage == S) { stage = 0; phase ^= 1; }
             }
         }
     } else if (warp == 1) {

@@ -422,6 +422,7 @@ struct PermuteParams {
     int32_t* pos_aux;         // optional copy for the caller
     __nv_bfloat16* x_perm;    // [Cap, d]
     int32_t to_f16;           // store rows as fp16 (fp8-weight GEMMs) instead of copying bf16
+    int32_t* src_row;         // gather mode (x_perm == nullptr): [Cap] token of each permuted row
 };
 
 __device__ __forceinline__ uint4 bf16x8_to_f16x8(const uint4& v) {
@@ -474,8 +475,13 @@ __global__ void __launch_bounds__(kPermuteThreads) moe_permute_kernel(const Perm
             }
             p.pos[(int64_t)t * p.k + j] = ps;
             if (p.pos_aux) p.pos_aux[(int64_t)t * p.k + j] = ps;
+            if (p.src_row && ps >= 0) p.src_row[ps] = t;
             s_pos[tl][j] = ps;
         }
+    }
+    if (p.x_perm == nullptr) {  // gather mode: the w1/w3 GEMM fetches the rows itself
+        ptx::pdl_launch_dependents();
+        return;
     }
     __syncthreads();
     const int wpt = 8 / p.PT;            // warps per token row

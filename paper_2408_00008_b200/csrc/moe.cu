@@ -176,6 +176,10 @@ struct moe_ctx {
     float* topk_w = nullptr;
     unsigned int* done = nullptr;
     __nv_bfloat16 *x_perm = nullptr, *h = nullptr;
+    int32_t* src_row = nullptr;  // gather mode: [cap + 512] token of each permuted row
+    bool gather = false;         // MOE_FLAG_GATHER (or env MOE_GATHER=1): tile::gather4 token fetch
+    bool gather_now = false;     // the current forward gathers (set per call)
+    CUtensorMap tm_src{};        // gather map over the current call's tokens [T, d], box {64, 1}
     float* y = nullptr;
     int64_t y_elems = 0;
     __nv_bfloat16 *stage_in = nullptr, *stage_out = nullptr;  // moe_forward_host staging (2 input slots)
@@ -490,6 +494,10 @@ moe_status launch_gemm_fp8t(moe_ctx* c, int slot, const GemmParams& p, const flo
 template <int NB>
 moe_status run_swap_g1(moe_ctx* c, int nbi, const moe_expert_weights* w, cudaStream_t st) {
     GemmParams p1{c->counts, c->offsets, c->E_local, c->d, c->f_local, 1, c->h, 0};
+    if (c->gather_now) {
+        p1.src_row = c->src_row;
+        return launch_gemm<kG1Swap, NB>(c, kSlotGemm1, p1, c->tm_w13, c->tm_src, c->num_sms, st);
+    }
     if constexpr (NB <= 64)
         if (c->fp8 && !c->fp8_smem_a)
             return launch_gemm_fp8t<kG1Swap, NB>(c, kSlotGemm1, p1, w->w13_scale, c->tm_w13, c->tm_x_swap[nbi],
@@ -531,7 +539,8 @@ struct RouteSpec {
     float* topk_w = nullptr;
     int32_t* pos = nullptr;
     int32_t* pos_aux = nullptr;
-    void* dst_rows = nullptr;    // x_perm (normal) or EP send buffer (dispatch)
+    void* dst_rows = nullptr;    // x_perm (normal) or EP send buffer (dispatch); nullptr: gather mode
+    int32_t* src_row = nullptr;  // gather mode: token of each permuted row
     int cap = 0;                 // > 0: EP dispatch buckets of `cap` rows per key
     int32_t* meta = nullptr;
 };
@@ -575,6 +584,7 @@ moe_status route_and_permute(moe_ctx* c, const RouteSpec& r, cudaStream_t st) {
     pp.TB = TB;
     pp.PT = r.T <= 1024 ? 2 : 8;
     pp.pos = r.pos; pp.pos_aux = r.pos_aux; pp.x_perm = static_cast<__nv_bfloat16*>(r.dst_rows);
+    pp.src_row = r.src_row;
     pp.to_f16 = c->fp8 && r.cap == 0;  // fp8-weight GEMMs take fp16 tokens
     return launch(c, kSlotPermute, moe_permute_kernel, dim3((r.T + pp.PT - 1) / pp.PT), dim3(kPermuteThreads), 0,
                   st, pp);
@@ -625,8 +635,10 @@ moe_status run_gemms(moe_ctx* c, bool swap, int64_t rows_bound, int64_t rows_tot
             b1 = std::max(1, (c->pair_tune >> 4) & 63); b2 = std::max(1, (c->pair_tune >> 10) & 63);
         }
         GemmParams p1{c->counts, c->offsets, c->E_local, c->d, c->f_local, 1, c->h, 0, r1, b1,
-                      ptx::kEvictNormal, ptx::kEvictNormal};
-        if ((s = launch_gemm_pair<kG1Pair>(c, kSlotGemm1, p1, c->tm_x_tiled, c->tm_w13_pair, g1, st))) return s;
+                      ptx::kEvictNormal, ptx::kEvictNormal, c->gather_now ? c->src_row : nullptr};
+        if ((s = launch_gemm_pair<kG1Pair>(c, kSlotGemm1, p1, c->gather_now ? c->tm_src : c->tm_x_tiled,
+                                           c->tm_w13_pair, g1, st)))
+            return s;
         GemmParams p2{c->counts, c->offsets, c->E_local, c->d, c->f_local, 1, c->y, 0, r2, b2,
                       ptx::kEvictNormal, ptx::kEvictNormal};
         if ((s = launch_gemm_pair<kG2Pair>(c, kSlotGemm2, p2, c->tm_h_tiled, c->tm_w2_swap, g2, st))) return s;
@@ -635,7 +647,10 @@ moe_status run_gemms(moe_ctx* c, bool swap, int64_t rows_bound, int64_t rows_tot
         const int g1 = (int)std::min<int64_t>(c->num_sms, mt_max * (c->f_local / 128));
         const int g2 = (int)std::min<int64_t>(c->num_sms, mt_max * ((c->d + 255) / 256));
         GemmParams p1{c->counts, c->offsets, c->E_local, c->d, c->f_local, 1, c->h, 0};
-        if ((s = launch_gemm<kG1Tiled, 256>(c, kSlotGemm1, p1, c->tm_x_tiled, c->tm_w13, g1, st))) return s;
+        p1.src_row = c->gather_now ? c->src_row : nullptr;
+        if ((s = launch_gemm<kG1Tiled, 256>(c, kSlotGemm1, p1, c->gather_now ? c->tm_src : c->tm_x_tiled, c->tm_w13,
+                                            g1, st)))
+            return s;
         GemmParams p2{c->counts, c->offsets, c->E_local, c->d, c->f_local, 1, c->y, 0};
         if ((s = launch_gemm<kG2Tiled, 256>(c, kSlotGemm2, p2, c->tm_h_tiled, c->tm_w2_tiled, g2, st))) return s;
     }
@@ -974,6 +989,8 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
     c->fp8_g2_kb256 = c->fp8_kb128 && c->f_local % 256 == 0;
     if (const char* v = getenv("MOE_FP8_G2_KB")) c->fp8_g2_kb256 = c->fp8_g2_kb256 && atoi(v) == 256;
     if (const char* pt = getenv("MOE_PAIR_TUNE")) c->pair_tune = atoi(pt);
+    if (const char* v = getenv("MOE_GATHER")) c->gather = atoi(v) != 0;
+    if (cfg->flags & MOE_FLAG_GATHER) c->gather = true;
     // router blocks of >= 2 rows; EP also routes the G*max_T*k receive slots
     c->nblk_max = (int)(((int64_t)c->max_T * (c->ep_world > 1 ? c->ep_world * c->k : 1) + 1) / 2 + 1);
 
@@ -1024,6 +1041,7 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
     ALLOC(c->offsets, sizeof(int32_t) * 64);
     ALLOC(c->done, sizeof(unsigned int) * 4);
     ALLOC(c->x_perm, sizeof(__nv_bfloat16) * c->cap * c->d);
+    ALLOC(c->src_row, sizeof(int32_t) * (c->cap + 512));
     ALLOC(c->h, sizeof(__nv_bfloat16) * c->cap * c->f_local);
     ALLOC(c->y, sizeof(float) * c->y_elems);
     ALLOC(c->stage_in, 2 * sizeof(__nv_bfloat16) * c->max_T * c->d);
@@ -1057,6 +1075,7 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
 #undef ALLOC
     if ((e = cudaMemset(c->done, 0, sizeof(unsigned int) * 4)) != cudaSuccess) return fail_init("memset", e);
     if ((e = cudaMemset(c->x_perm, 0, sizeof(__nv_bfloat16) * c->cap * c->d)) != cudaSuccess) return fail_init("memset", e);
+    if ((e = cudaMemset(c->src_row, 0, sizeof(int32_t) * (c->cap + 512))) != cudaSuccess) return fail_init("memset", e);
     if ((e = cudaMemset(c->h, 0, sizeof(__nv_bfloat16) * c->cap * c->f_local)) != cudaSuccess) return fail_init("memset", e);
 
     // workspace TMA descriptors
@@ -1344,7 +1363,16 @@ moe_status forward_impl(moe_ctx* c, const void* tokens, int32_t T, const void* r
     r.logits = aux ? aux->logits : nullptr;
     r.topk_idx = c->topk_idx; r.topk_w = c->topk_w;
     r.pos = c->pos; r.pos_aux = aux ? aux->pos : nullptr;
-    r.dst_rows = c->x_perm;
+    // Gather mode (MOE_FLAG_GATHER, bf16 weights): the w1/w3 GEMM fetches token rows
+    // from `tokens` through a {64, 1}-box map with tile::gather4; the permute step only
+    // records which token each permuted row is. Off by default: one gather4 moves 512 B
+    // and measured ~70 SM cycles each, so the GEMM's producer becomes the bottleneck
+    // (r01: decode 0.533 vs 0.451 ms, prefill 37.5 vs 19.1 ms with the copy).
+    c->gather_now = c->gather && !c->fp8;
+    if (c->gather_now && !encode_map(&c->tm_src, tokens, 2, c->d, (uint64_t)T, 1, 1))
+        return fail(c, MOE_ERR_CUDA, "cuTensorMapEncodeTiled(tokens) failed");
+    r.dst_rows = c->gather_now ? nullptr : c->x_perm;
+    r.src_row = c->gather_now ? c->src_row : nullptr;
     if ((s = route_and_permute(c, r, st))) return s;
     const bool swap = use_swap_path(c, T);
     int splits = 1;
@@ -1404,6 +1432,7 @@ moe_status forward_impl(moe_ctx* c, const void* tokens, int32_t T, const void* r
 moe_status forward_ep(moe_ctx* c, const void* tokens, int32_t T, const void* router_w, void* out,
                       const moe_aux* aux, cudaStream_t st) {
     moe_status s;
+    c->gather_now = false;  // received rows are compacted into x_perm by the receive-side permute
     const int G = c->ep_world;
     const CommRef epc = ep_comm(c);
     const int64_t cap = (int64_t)c->max_T * c->k;

@@ -38,7 +38,9 @@ def _inputs(shape, seed, device="cuda"):
     return synth.make_inputs(shape, seed, device=device)
 
 
-MODES = {"auto": 0, "swap": 0x2, "tiled": 0x4, "tiled1cta": 0x4 | 0x10}
+# 0x80 = MOE_FLAG_GATHER: token rows gathered by the w1/w3 GEMM (tile::gather4), no permuted copy
+MODES = {"auto": 0, "swap": 0x2, "tiled": 0x4, "tiled1cta": 0x4 | 0x10,
+         "swap_gather": 0x2 | 0x80, "tiled_gather": 0x4 | 0x80, "tiled1cta_gather": 0x4 | 0x10 | 0x80}
 
 
 # ---------------------------------------------------------------- worked example
@@ -225,6 +227,21 @@ def test_c3_prefill_full(moe, mixtral_weights):
     torch.cuda.synchronize()
     assert torch.equal(out2.view(torch.int16), run.out.view(torch.int16))
     blk.close()
+
+
+@pytest.mark.parametrize("T,flags", [(64, 0), (300, 0x2), (4096, 0), (4096, 0x10), (1000, 0x4 | 0x10)])
+def test_gather_equals_copy(moe, mixtral_weights, T, flags):
+    """The tile::gather4 token fetch and the materialised permuted copy feed the same
+    bytes to the same MMAs: outputs must agree bit for bit (Mixtral size)."""
+    w, _ = mixtral_weights
+    x = synth.make_tokens(T, 4096, seed=300 + T, device="cuda")
+    outs = []
+    for extra in (0, moe.MOE_FLAG_GATHER):
+        blk = moe.MoEBlock(w["wg"], w["w1"], w["w3"], w["w2"], top_k=2, max_tokens=T, flags=flags | extra)
+        outs.append(blk.forward(x).clone())
+        torch.cuda.synchronize()
+        blk.close()
+    assert torch.equal(outs[0].view(torch.int16), outs[1].view(torch.int16))
 
 
 # ---------------------------------------------------------------- EP / TP device path (loopback transport)
