@@ -62,6 +62,8 @@ def workload_config(args, world):
         "global_tokens": Tg, "tokens_per_gpu": T,
         "parallelism": {"none": "single" if world == 1 else f"replicas{world}", "ep": f"ep{world}",
                         "tp": f"tp{world}", "hybrid": f"ep{world // args.tp}xtp{args.tp}"}[par],
+        "transport": ("peer memory (MOE_FLAG_P2P)" if getattr(args, "p2p", False) else "nccl")
+                     if par in ("ep", "tp", "hybrid") else None,
         "layers": STACK_LAYERS if stack else 1,
         "l2": "weights (2.8 GB per layer) > L2 (126 MB): streamed from HBM every step, no flush"}
 
@@ -85,6 +87,9 @@ def parse():
     ap.add_argument("--par", default=None, choices=["ep", "tp", "hybrid", "none"],
                     help="multi-GPU variant (default: ep when N > 1)")
     ap.add_argument("--tp", type=int, default=2, help="TP degree of --par hybrid (EP degree = N / tp)")
+    ap.add_argument("--p2p", action="store_true",
+                    help="--par ep / tp: exchange through peer memory (MOE_FLAG_P2P: the producing kernels store "
+                         "into the other GPUs' buffers) instead of NCCL collectives")
     return ap.parse_args()
 
 
@@ -396,7 +401,7 @@ def main():
     if par == "hybrid":
         tp_size = args.tp
         comm, tp_comm = moe.nccl_hybrid_comms(world, rank, tp_size, local)
-    elif par != "none":
+    elif par != "none" and not args.p2p:
         comm = moe.nccl_comm_from_process_group(world, rank, local) if world > 1 else \
             moe.moe_nccl_comm_init(moe.moe_nccl_unique_id(), 1, 0, local)
     # EP / hybrid: the global batch is sharded across the EP groups (strong scaling of
@@ -406,6 +411,10 @@ def main():
     nbuf = 4  # distinct token batches cycled through the steps
     xs = [synth.make_tokens(Tg, d, seed=args.seed + 1 + i, device=dev)[shard * T:(shard + 1) * T] for i in range(nbuf)]
     flags = args.flags
+    if args.p2p:
+        if par not in ("ep", "tp"):
+            raise SystemExit("--p2p needs --par ep or tp")
+        flags |= moe.MOE_FLAG_P2P
     if args.fp8:
         flags |= moe.MOE_FLAG_FP8_WEIGHTS
         for n in ("w1", "w3", "w2"):
@@ -413,6 +422,11 @@ def main():
     blk = moe.MoEBlock(w["wg"], w["w1"], w["w3"], w["w2"], top_k=k, max_tokens=T, par=pmap[par],
                        world_size=world if par != "none" else 1, rank=rank if par != "none" else 0, nccl_comm=comm,
                        flags=flags, tp_size=tp_size, tp_comm=tp_comm)
+    if args.p2p:
+        if world > 1:
+            moe.p2p_connect_process_group(blk.ctx)
+        else:
+            blk.p2p_connect([blk.p2p_handle()])
     del w["w1"], w["w3"], w["w2"]
     torch.cuda.empty_cache()
     out = torch.empty(T, d, dtype=torch.bfloat16, device=dev)

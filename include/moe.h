@@ -247,6 +247,27 @@ MOE_API moe_status moe_loopback_comm_create(int32_t world, void** group);
 MOE_API moe_status moe_loopback_comm_rank(void* group, int32_t rank, void** comm);
 MOE_API moe_status moe_loopback_comm_destroy(void* group_or_rank);
 
+/* ---- Peer-memory transport (MOE_FLAG_P2P, "NVLink").
+ * The EP / TP exchange steps become stores and loads into the other ranks' device
+ * memory issued by the kernels that produce / consume the rows (dispatch permute,
+ * expert-output gather, TP combine / finish), completed by a device-side release
+ * counter per exchange and a stream wait -- no NCCL call and no staging copy on
+ * the data path. Each context owns one symmetric device region; the ranks of the
+ * EP group (MOE_PAR_EP) or TP group (MOE_PAR_TP) exchange its handle once:
+ *   1. every rank: moe_p2p_handle(ctx, buf)  -> MOE_P2P_HANDLE_BYTES opaque bytes
+ *   2. all-gather the buffers over any host channel (a process-group all-gather, files ...)
+ *   3. every rank: moe_p2p_connect(ctx, all, world)  (rank-ordered concatenation)
+ * Handles of ranks in the same process are used directly (loopback tests: G ranks
+ * on one GPU); others are opened with CUDA IPC (one process per GPU, or several
+ * processes on one GPU). nccl_comm may be NULL with this flag. MOE_PAR_HYBRID is
+ * not supported (MOE_ERR_UNSUPPORTED). moe_forward before moe_p2p_connect fails
+ * with MOE_ERR_STATE. Every rank must call moe_forward the same number of times
+ * (TP: with the same T), as with the NCCL transport.                           */
+#define MOE_FLAG_P2P 0x100u
+#define MOE_P2P_HANDLE_BYTES 128
+MOE_API moe_status moe_p2p_handle(moe_ctx* ctx, void* handle_out);
+MOE_API moe_status moe_p2p_connect(moe_ctx* ctx, const void* handles, int32_t world);
+
 #ifdef __cplusplus
 }
 #endif

@@ -33,6 +33,8 @@ MOE_FLAG_RESIDUAL, MOE_FLAG_FORCE_SWAP, MOE_FLAG_FORCE_TILED, MOE_FLAG_NO_PDL, M
 MOE_FLAG_EP_EXACT = 0x20
 MOE_FLAG_FP8_WEIGHTS = 0x40
 MOE_FLAG_GATHER = 0x80
+MOE_FLAG_P2P = 0x100
+P2P_HANDLE_BYTES = 128
 NUM_KERNEL_SLOTS = 8
 KERNEL_SLOTS = ("router", "permute", "gemm1_w13_swiglu", "gemm2_w2", "combine", "dispatch", "exchange", "pack")
 
@@ -41,7 +43,8 @@ EXPORTED = ("moe_init", "moe_packed_sizes", "moe_pack_weights", "moe_forward", "
             "moe_forward_host", "moe_destroy", "moe_last_error", "moe_status_string", "moe_set_profiling",
             "moe_reset_profile", "moe_kernel_times", "moe_launch_count", "moe_nccl_unique_id",
             "moe_nccl_comm_init", "moe_nccl_comm_destroy", "moe_loopback_comm_create", "moe_loopback_comm_rank",
-            "moe_loopback_comm_destroy", "moe_packed_sizes_fp8", "moe_pack_weights_fp8")
+            "moe_loopback_comm_destroy", "moe_packed_sizes_fp8", "moe_pack_weights_fp8", "moe_p2p_handle",
+            "moe_p2p_connect")
 
 
 class moe_config(ctypes.Structure):
@@ -88,6 +91,8 @@ _sig = {
     "moe_pack_weights_fp8": ([_P] * 12, _I32),
     "moe_loopback_comm_rank": ([_P, _I32, ctypes.POINTER(_P)], _I32),
     "moe_loopback_comm_destroy": ([_P], _I32),
+    "moe_p2p_handle": ([_P, _P], _I32),
+    "moe_p2p_connect": ([_P, _P, _I32], _I32),
 }
 for _name, (_args, _res) in _sig.items():
     _fn = getattr(_lib, _name)
@@ -249,6 +254,32 @@ def moe_loopback_comm_destroy(handle):
     _check(_lib.moe_loopback_comm_destroy(handle))
 
 
+def moe_p2p_handle(ctx) -> bytes:
+    """This rank's symmetric-region handle (MOE_P2P_HANDLE_BYTES opaque bytes)."""
+    buf = ctypes.create_string_buffer(P2P_HANDLE_BYTES)
+    _check(_lib.moe_p2p_handle(ctx, buf), ctx)
+    return buf.raw
+
+
+def moe_p2p_connect(ctx, handles):
+    """handles: the group's handles in rank order (list of bytes, or their concatenation)."""
+    blob = b"".join(handles) if isinstance(handles, (list, tuple)) else bytes(handles)
+    if len(blob) % P2P_HANDLE_BYTES:
+        raise ValueError("handle blob size is not a multiple of P2P_HANDLE_BYTES")
+    buf = ctypes.create_string_buffer(blob, len(blob))
+    _check(_lib.moe_p2p_connect(ctx, buf, len(blob) // P2P_HANDLE_BYTES), ctx)
+
+
+def p2p_connect_process_group(ctx, group=None):
+    """MOE_FLAG_P2P over torch.distributed: all-gather the handles on the host
+    process group (any backend), then connect. Call on every rank of the group."""
+    import torch.distributed as dist
+    mine = moe_p2p_handle(ctx)
+    allh = [None] * dist.get_world_size(group)
+    dist.all_gather_object(allh, mine, group=group)
+    moe_p2p_connect(ctx, allh)
+
+
 def nccl_comm_from_process_group(world: int, rank: int, device: int):
     """Create libmoe's NCCL communicator for the current torch.distributed group:
     rank 0 draws the ncclUniqueId, the host process group broadcasts it."""
@@ -316,6 +347,12 @@ class MoEBlock:
             out = torch.empty_like(x)
         moe_forward(self.ctx, x, T, self.router_w, self.w13, self.w2, out, aux, stream, self.s13, self.s2)
         return out
+
+    def p2p_handle(self) -> bytes:
+        return moe_p2p_handle(self.ctx)
+
+    def p2p_connect(self, handles):
+        moe_p2p_connect(self.ctx, handles)
 
     def forward_routed(self, x, topk_idx, topk_w, out=None, aux=None, stream=None):
         if out is None:

@@ -16,6 +16,7 @@
 #include <cuda_fp16.h>
 #include <stdint.h>
 #include "sm100.cuh"
+#include "p2p.cuh"
 
 namespace moe {
 
@@ -423,6 +424,11 @@ struct PermuteParams {
     __nv_bfloat16* x_perm;    // [Cap, d]
     int32_t to_f16;           // store rows as fp16 (fp8-weight GEMMs) instead of copying bf16
     int32_t* src_row;         // gather mode (x_perm == nullptr): [Cap] token of each permuted row
+    // EP dispatch over peer memory (MOE_FLAG_P2P): rows / meta go straight into slot
+    // (my_rank * cap + r) of the destination rank's receive buffer.
+    uint8_t* const* peers;
+    int64_t peer_rows_off, peer_meta_off;
+    int32_t my_rank;
 };
 
 __device__ __forceinline__ uint4 bf16x8_to_f16x8(const uint4& v) {
@@ -468,7 +474,10 @@ __global__ void __launch_bounds__(kPermuteThreads) moe_permute_kernel(const Perm
                 const int32_t r = p.blockoff[(int64_t)b * p.nkeys + e] + p.pos[(int64_t)t * p.k + j];
                 if (p.cap > 0) {  // EP dispatch: bucket of destination rank e
                     ps = e * p.cap + r;
-                    p.meta[ps] = ex - e * p.key_div;  // expert index local to the destination
+                    int32_t* meta = p.peers ? reinterpret_cast<int32_t*>(p.peers[e] + p.peer_meta_off) +
+                                                  (int64_t)p.my_rank * p.cap + r
+                                            : p.meta + ps;
+                    *meta = ex - e * p.key_div;  // expert index local to the destination
                 } else {
                     ps = p.offsets[e] + r;
                 }
@@ -479,7 +488,7 @@ __global__ void __launch_bounds__(kPermuteThreads) moe_permute_kernel(const Perm
             s_pos[tl][j] = ps;
         }
     }
-    if (p.x_perm == nullptr) {  // gather mode: the w1/w3 GEMM fetches the rows itself
+    if (p.x_perm == nullptr && p.peers == nullptr) {  // gather mode: the w1/w3 GEMM fetches the rows itself
         ptx::pdl_launch_dependents();
         return;
     }
@@ -491,8 +500,17 @@ __global__ void __launch_bounds__(kPermuteThreads) moe_permute_kernel(const Perm
         const int nvec = p.d / 8;
         const uint4* src = reinterpret_cast<const uint4*>(p.x + (int64_t)t * p.d);
         const int32_t d0 = s_pos[tl][0], d1 = p.k > 1 ? s_pos[tl][1] : -1;
-        uint4* dst0 = d0 >= 0 ? reinterpret_cast<uint4*>(p.x_perm + (int64_t)d0 * p.d) : nullptr;
-        uint4* dst1 = d1 >= 0 ? reinterpret_cast<uint4*>(p.x_perm + (int64_t)d1 * p.d) : nullptr;
+        auto row_ptr = [&](int32_t ps) -> uint4* {
+            if (ps < 0) return nullptr;
+            if (p.peers) {  // P2P dispatch: the destination rank's receive slot
+                const int e = ps / p.cap, r = ps - e * p.cap;
+                return reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.peers[e] + p.peer_rows_off) +
+                                                ((int64_t)p.my_rank * p.cap + r) * p.d);
+            }
+            return reinterpret_cast<uint4*>(p.x_perm + (int64_t)ps * p.d);
+        };
+        uint4* dst0 = row_ptr(d0);
+        uint4* dst1 = row_ptr(d1);
         const int stride = 32 * wpt;
         for (int v0 = sw * 32 + lane; v0 < nvec; v0 += 4 * stride) {
             uint4 buf[4];
@@ -524,6 +542,11 @@ struct CombineParams {
     int32_t T, d, k;
     __nv_bfloat16* out;       // [T, d]
     float* out_f32;           // [T, d] optional (fp32 before rounding)
+    // TP reduce-scatter over peer memory (MOE_FLAG_P2P): the fp32 row of token t goes
+    // to slot [my_rank][t - row0(owner)] of its owner's region (out/out_f32 unused).
+    uint8_t* const* peers;
+    int64_t peer_off;
+    int32_t G, my_rank, shard_max;
 };
 
 // K5 (a9): out[t] = bf16_rne( sum_j w_j * (sum_s y_s[pos_j]) (+ x[t]) ), fixed order:
@@ -580,6 +603,12 @@ __global__ void __launch_bounds__(256) moe_combine_kernel(const CombineParams p)
             const float2 a = __bfloat1622float2(xs[0]), b = __bfloat1622float2(xs[1]);
             r.x += a.x; r.y += a.y; r.z += b.x; r.w += b.y;
         }
+        if (p.peers) {
+            const int o = tp_owner(t, p.T, p.G);
+            float* dst = reinterpret_cast<float*>(p.peers[o] + p.peer_off) +
+                         ((int64_t)p.my_rank * p.shard_max + (t - tp_row0(o, p.T, p.G))) * p.d + c;
+            *reinterpret_cast<float4*>(dst) = r;
+        }
         if (p.out_f32) __stcs(reinterpret_cast<float4*>(p.out_f32 + (int64_t)t * p.d + c), r);
         if (p.out) {
             __nv_bfloat162 o0 = __floats2bfloat162_rn(r.x, r.y), o1 = __floats2bfloat162_rn(r.z, r.w);
@@ -594,8 +623,12 @@ __global__ void __launch_bounds__(256) moe_combine_kernel(const CombineParams p)
 
 // EP return path: ysend[slot] = sum_s y_s[pos[slot]] for every occupied receive
 // slot (fp32 rows; splits summed in ascending order, as in the combine).
+// P2P (peers != nullptr): the row goes straight to slot (my_rank * cap + r) of the
+// return buffer of source rank slot / cap, r = slot % cap.
 __global__ void __launch_bounds__(256) moe_ep_gather_kernel(const float* y, int64_t split_stride, int splits,
-                                                            const int32_t* pos, int nslots, int d, float* ysend) {
+                                                            const int32_t* pos, int nslots, int d, float* ysend,
+                                                            uint8_t* const* peers, int64_t peer_off, int cap,
+                                                            int my_rank) {
     const int nxb = (d + 1023) / 1024;  // 1-D grid: block b -> slot b / nxb
     const int slot = blockIdx.x / nxb;
     const int c = (blockIdx.x % nxb) * 1024 + threadIdx.x * 4;
@@ -610,7 +643,12 @@ __global__ void __launch_bounds__(256) moe_ep_gather_kernel(const float* y, int6
                 const float4 u = __ldcs(reinterpret_cast<const float4*>(yr + sp * split_stride));
                 s.x += u.x; s.y += u.y; s.z += u.z; s.w += u.w;
             }
-            *reinterpret_cast<float4*>(ysend + (int64_t)slot * d + c) = s;
+            float* dst = ysend + (int64_t)slot * d + c;
+            if (peers) {
+                const int src = slot / cap, r = slot - src * cap;
+                dst = reinterpret_cast<float*>(peers[src] + peer_off) + ((int64_t)my_rank * cap + r) * d + c;
+            }
+            *reinterpret_cast<float4*>(dst) = s;
         }
     }
     ptx::pdl_launch_dependents();

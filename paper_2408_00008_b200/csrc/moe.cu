@@ -12,6 +12,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <cstdarg>
@@ -109,6 +110,20 @@ PFN_encodeTiled_t get_encode_fn() {
     return fn;
 }
 
+typedef CUresult (*PFN_waitValue64_t)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+PFN_waitValue64_t get_wait64_fn() {
+    static PFN_waitValue64_t fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuStreamWaitValue64", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_waitValue64_t>(p);
+    });
+    return fn;
+}
+
 // rank-2 [rows, K] or rank-3 [batch, rows, K] bf16, K innermost; box {64, box_rows(, 1)}; 128B swizzle.
 bool encode_map(CUtensorMap* m, const void* base, int rank, uint64_t K, uint64_t rows, uint64_t batch,
                 uint32_t box_rows) {
@@ -197,6 +212,21 @@ struct moe_ctx {
     int32_t* ep_rcounts = nullptr;    // device: rows each peer sends me (exact mode)
     int32_t* h_counts = nullptr;      // pinned host: [0,64) my send counts, [64,128) receive counts
     int64_t ep_exact_bytes = 32ll << 20;  // exact mode when a capacity exchange would move more bf16 bytes
+    // peer-memory transport (MOE_FLAG_P2P, p2p.cuh)
+    bool p2p = false;             // flag given at init: symmetric region allocated
+    bool p2p_ready = false;       // moe_p2p_connect done
+    int p2p_world = 1, p2p_rank = 0;
+    uint8_t* sym = nullptr;       // this rank's symmetric region
+    size_t sym_bytes = 0;
+    struct SymLayout {
+        int64_t ep_rows = 0, ep_meta = 0, ep_yret = 0;      // EP: [G*cap, d] bf16, [G*cap] i32, [G*cap, d] f32
+        int64_t tp_slots = 0, tp_keep16 = 0, tp_keep32 = 0; // TP: [G][shard_max, d] f32, [max_T, d] bf16 / f32
+        int64_t sig = 0;                                    // 4 u64 arrival counters
+    } so;
+    int tp_shard_max = 0;
+    uint8_t** d_peers = nullptr;  // device [p2p_world] region bases (own included)
+    std::vector<void*> p2p_opened;  // IPC mappings to close at destroy
+    uint64_t p2p_epoch[4]{};      // exchanges done per counter
     // TMA descriptors: workspace operands
     CUtensorMap tm_x_tiled{}, tm_h_tiled{};
     CUtensorMap tm_x_swap[4]{}, tm_h_swap[4]{};  // NB = 32, 64, 128, 256
@@ -413,9 +443,13 @@ moe_status validate_cfg(const moe_config* cfg, moe_ctx* c) {
     if (cfg->num_experts % ps.ep_world) return fail(c, MOE_ERR_INVALID, "num_experts % ep_world != 0");
     if (cfg->par == MOE_PAR_TP && cfg->hidden % (4 * G))
         return fail(c, MOE_ERR_INVALID, "TP needs hidden % (4*world) == 0 (reduce-scatter shards)");
-    if ((cfg->par == MOE_PAR_EP || cfg->par == MOE_PAR_HYBRID) && !cfg->nccl_comm)
+    const bool p2p = (cfg->flags & MOE_FLAG_P2P) != 0;
+    if (p2p && cfg->par == MOE_PAR_HYBRID)
+        return fail(c, MOE_ERR_UNSUPPORTED, "MOE_FLAG_P2P supports MOE_PAR_EP and MOE_PAR_TP");
+    if (p2p && cfg->par == MOE_PAR_NONE) return fail(c, MOE_ERR_INVALID, "MOE_FLAG_P2P needs MOE_PAR_EP or MOE_PAR_TP");
+    if (!p2p && (cfg->par == MOE_PAR_EP || cfg->par == MOE_PAR_HYBRID) && !cfg->nccl_comm)
         return fail(c, MOE_ERR_INVALID, "nccl_comm (EP group) required");
-    if (cfg->par == MOE_PAR_TP && G > 1 && !cfg->nccl_comm) return fail(c, MOE_ERR_INVALID, "nccl_comm required");
+    if (!p2p && cfg->par == MOE_PAR_TP && G > 1 && !cfg->nccl_comm) return fail(c, MOE_ERR_INVALID, "nccl_comm required");
     if (cfg->par == MOE_PAR_HYBRID && ps.tp_world > 1 && !cfg->tp_comm)
         return fail(c, MOE_ERR_INVALID, "tp_comm (TP group) required");
     if (cfg->split_k < 0 || cfg->split_k > 8) return fail(c, MOE_ERR_INVALID, "split_k must be in [0,8]");
@@ -543,6 +577,9 @@ struct RouteSpec {
     int32_t* src_row = nullptr;  // gather mode: token of each permuted row
     int cap = 0;                 // > 0: EP dispatch buckets of `cap` rows per key
     int32_t* meta = nullptr;
+    uint8_t* const* peers = nullptr;  // P2P dispatch: rows / meta into the destinations' regions
+    int64_t peer_rows_off = 0, peer_meta_off = 0;
+    int my_rank = 0;
 };
 
 moe_status route_and_permute(moe_ctx* c, const RouteSpec& r, cudaStream_t st) {
@@ -585,6 +622,7 @@ moe_status route_and_permute(moe_ctx* c, const RouteSpec& r, cudaStream_t st) {
     pp.PT = r.T <= 1024 ? 2 : 8;
     pp.pos = r.pos; pp.pos_aux = r.pos_aux; pp.x_perm = static_cast<__nv_bfloat16*>(r.dst_rows);
     pp.src_row = r.src_row;
+    pp.peers = r.peers; pp.peer_rows_off = r.peer_rows_off; pp.peer_meta_off = r.peer_meta_off; pp.my_rank = r.my_rank;
     pp.to_f16 = c->fp8 && r.cap == 0;  // fp8-weight GEMMs take fp16 tokens
     return launch(c, kSlotPermute, moe_permute_kernel, dim3((r.T + pp.PT - 1) / pp.PT), dim3(kPermuteThreads), 0,
                   st, pp);
@@ -691,6 +729,11 @@ struct StepTimer {
         }
     }
 };
+
+// P2P exchange completion: counter `idx` of every rank's region += 1 after the
+// producing kernel (device-side release), then this rank's stream waits until all
+// G ranks have arrived for this epoch (no SM is held while waiting).
+moe_status p2p_arrive_and_wait(moe_ctx* c, int idx, cudaStream_t st);
 
 #define NCCL_TRY(ctx, expr)                                                                          \
     do {                                                                                             \
@@ -901,6 +944,18 @@ moe_status check_ready(moe_ctx* c) {
     return MOE_OK;
 }
 
+moe_status p2p_arrive_and_wait(moe_ctx* c, int idx, cudaStream_t st) {
+    const int64_t sig_off = c->so.sig + 8 * idx;
+    moe_status s = launch(c, kSlotExchange, moe_p2p_signal_kernel, dim3(1), dim3(32), 0, st,
+                          static_cast<uint8_t* const*>(c->d_peers), c->p2p_world, sig_off);
+    if (s) return s;
+    const uint64_t target = ++c->p2p_epoch[idx] * (uint64_t)c->p2p_world;
+    CUresult r = get_wait64_fn()(reinterpret_cast<CUstream>(st), reinterpret_cast<CUdeviceptr>(c->sym + sig_off), target,
+                                 CU_STREAM_WAIT_VALUE_GEQ);
+    if (r != CUDA_SUCCESS) return fail(c, MOE_ERR_CUDA, "cuStreamWaitValue64 failed (%d)", (int)r);
+    return MOE_OK;
+}
+
 moe_status forward_impl(moe_ctx* c, const void* tokens, int32_t T, const void* router_w, const int32_t* in_idx,
                         const float* in_w, const moe_expert_weights* w, void* out, const moe_aux* aux,
                         cudaStream_t st);
@@ -1021,7 +1076,7 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
                     return fail(nullptr, MOE_ERR_INVALID, "loopback comm rank/world does not match cfg");
                 }
     }
-    if (!as_loopback(cfg->nccl_comm) && cfg->par != MOE_PAR_NONE && c->G > 1) {
+    if (!(cfg->flags & MOE_FLAG_P2P) && !as_loopback(cfg->nccl_comm) && cfg->par != MOE_PAR_NONE && c->G > 1) {
         std::string lerr;
         if (!load_nccl(lerr)) {
             moe_destroy(c);
@@ -1072,6 +1127,30 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
         if ((e = cudaMallocHost(reinterpret_cast<void**>(&c->h_counts), sizeof(int32_t) * 128)) != cudaSuccess)
             return fail_init("h_counts", e);
     }
+    if (cfg->flags & MOE_FLAG_P2P) {
+        // symmetric region: identical layout on every rank of the group
+        c->p2p = true;
+        c->p2p_world = cfg->par == MOE_PAR_TP ? c->tp_world : c->ep_world;
+        c->p2p_rank = cfg->par == MOE_PAR_TP ? c->tp_rank : c->ep_rank;
+        int64_t off = 0;
+        auto take = [&](int64_t bytes) { const int64_t o = off; off = round_up(off + bytes, 4096); return o; };
+        if (cfg->par == MOE_PAR_EP) {
+            const int64_t slots = (int64_t)c->ep_world * c->max_T * c->k;
+            c->so.ep_rows = take(slots * c->d * 2);
+            c->so.ep_meta = take(slots * 4);
+            c->so.ep_yret = take(slots * c->d * 4);
+        } else {
+            c->tp_shard_max = (c->max_T + c->tp_world - 1) / c->tp_world;
+            c->so.tp_slots = take((int64_t)c->tp_world * c->tp_shard_max * c->d * 4);
+            c->so.tp_keep16 = take((int64_t)c->max_T * c->d * 2);
+            c->so.tp_keep32 = take((int64_t)c->max_T * c->d * 4);
+        }
+        c->so.sig = take(64);
+        c->sym_bytes = (size_t)off;
+        ALLOC(c->sym, c->sym_bytes);
+        if ((e = cudaMemset(c->sym, 0, c->sym_bytes)) != cudaSuccess) return fail_init("memset", e);
+        ALLOC(c->d_peers, sizeof(uint8_t*) * c->p2p_world);
+    }
 #undef ALLOC
     if ((e = cudaMemset(c->done, 0, sizeof(unsigned int) * 4)) != cudaSuccess) return fail_init("memset", e);
     if ((e = cudaMemset(c->x_perm, 0, sizeof(__nv_bfloat16) * c->cap * c->d)) != cudaSuccess) return fail_init("memset", e);
@@ -1106,6 +1185,29 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
         g_init_error = m;
         return as;
     }
+    // Load every kernel now. Under CUDA lazy loading a kernel's first launch loads its
+    // code, which can wait on work already queued on the device -- including a P2P
+    // rank's stream blocked until a peer signals (and the peer's signal may sit behind
+    // that load): load up front so no launch inside a forward ever loads code.
+    {
+        cudaFuncAttributes fa;
+        const void* fns[] = {
+            reinterpret_cast<const void*>(moe_router_mma_kernel<1>), reinterpret_cast<const void*>(moe_router_mma_kernel<8>),
+            reinterpret_cast<const void*>(moe_router_kernel<8, 2>), reinterpret_cast<const void*>(moe_router_kernel<16, 2>),
+            reinterpret_cast<const void*>(moe_router_kernel<32, 2>), reinterpret_cast<const void*>(moe_permute_kernel),
+            reinterpret_cast<const void*>(moe_combine_kernel), reinterpret_cast<const void*>(moe_ep_gather_kernel),
+            reinterpret_cast<const void*>(moe_tp_finish_kernel), reinterpret_cast<const void*>(moe_loopback_add_kernel),
+            reinterpret_cast<const void*>(moe_p2p_signal_kernel), reinterpret_cast<const void*>(moe_ep_p2p_fill_kernel),
+            reinterpret_cast<const void*>(moe_tp_p2p_finish_kernel), reinterpret_cast<const void*>(moe_tp_p2p_pull_kernel),
+            reinterpret_cast<const void*>(moe_gemm_kernel<kG1Tiled, 256>), reinterpret_cast<const void*>(moe_gemm_kernel<kG2Tiled, 256>),
+            reinterpret_cast<const void*>(moe_gemm_kernel<kG1Swap, 32>), reinterpret_cast<const void*>(moe_gemm_kernel<kG2Swap, 32>),
+            reinterpret_cast<const void*>(moe_gemm_kernel<kG1Swap, 64>), reinterpret_cast<const void*>(moe_gemm_kernel<kG2Swap, 64>),
+            reinterpret_cast<const void*>(moe_gemm_kernel<kG1Swap, 128>), reinterpret_cast<const void*>(moe_gemm_kernel<kG2Swap, 128>),
+            reinterpret_cast<const void*>(moe_gemm_kernel<kG2Swap, 256>), reinterpret_cast<const void*>(moe_gemm_pair_kernel<kG1Pair>),
+            reinterpret_cast<const void*>(moe_gemm_pair_kernel<kG2Pair>)};
+        for (const void* fn : fns)
+            if ((e = cudaFuncGetAttributes(&fa, fn)) != cudaSuccess) return fail_init("cudaFuncGetAttributes", e);
+    }
     if ((e = cudaDeviceSynchronize()) != cudaSuccess) return fail_init("sync", e);
     *out = c;
     return MOE_OK;
@@ -1117,7 +1219,12 @@ moe_status moe_destroy(moe_ctx* c) {
     void* bufs[] = {c->topk_idx, c->topk_w, c->pos, c->blockcount, c->blockoff, c->counts, c->offsets, c->done,
                     c->x_perm, c->h, c->y, c->stage_in, c->stage_out, c->tp_partial, c->tp_scatter, c->ep_send,
                     c->ep_recv, c->ep_ysend, c->ep_yrecv, c->ep_meta_send, c->ep_meta_recv,
-                    c->ep_ridx, c->ep_rpos, c->ep_rw, c->ep_rcounts, c->lb_scratch};
+                    c->ep_ridx, c->ep_rpos, c->ep_rw, c->ep_rcounts, c->lb_scratch, c->d_peers};
+    for (void* p : c->p2p_opened) cudaIpcCloseMemHandle(p);
+    if (c->sym) {
+        cudaDeviceSynchronize();  // peers' stores into this region have drained (same-process group)
+        cudaFree(c->sym);
+    }
     for (void* b : bufs)
         if (b) cudaFree(b);
     if (c->h_counts) cudaFreeHost(c->h_counts);
@@ -1314,6 +1421,75 @@ moe_status moe_loopback_comm_rank(void* group, int32_t rank, void** comm) {
     return MOE_OK;
 }
 
+namespace {
+struct P2PHandle {
+    uint32_t magic;     // "MP2P"
+    int32_t pid, device, rank;
+    uint64_t ptr, bytes;
+    cudaIpcMemHandle_t ipc;
+};
+static_assert(sizeof(P2PHandle) <= MOE_P2P_HANDLE_BYTES, "handle too large");
+constexpr uint32_t kP2PMagic = 0x5032504Du;
+}  // namespace
+
+moe_status moe_p2p_handle(moe_ctx* c, void* handle_out) {
+    moe_status s = check_ready(c);
+    if (s) return s;
+    if (!handle_out) return fail(c, MOE_ERR_INVALID, "handle_out is NULL");
+    if (!c->p2p) return fail(c, MOE_ERR_STATE, "context was not created with MOE_FLAG_P2P");
+    P2PHandle h{};
+    h.magic = kP2PMagic;
+    h.pid = (int32_t)getpid();
+    h.device = c->device;
+    h.rank = c->p2p_rank;
+    h.ptr = reinterpret_cast<uint64_t>(c->sym);
+    h.bytes = c->sym_bytes;
+    CUDA_TRY(c, cudaIpcGetMemHandle(&h.ipc, c->sym));
+    memset(handle_out, 0, MOE_P2P_HANDLE_BYTES);
+    memcpy(handle_out, &h, sizeof(h));
+    return MOE_OK;
+}
+
+moe_status moe_p2p_connect(moe_ctx* c, const void* handles, int32_t world) {
+    moe_status s = check_ready(c);
+    if (s) return s;
+    if (!handles) return fail(c, MOE_ERR_INVALID, "handles is NULL");
+    if (!c->p2p) return fail(c, MOE_ERR_STATE, "context was not created with MOE_FLAG_P2P");
+    if (c->p2p_ready) return fail(c, MOE_ERR_STATE, "already connected");
+    if (world != c->p2p_world) return fail(c, MOE_ERR_INVALID, "world %d != group size %d", world, c->p2p_world);
+    if (!get_wait64_fn()) return fail(c, MOE_ERR_UNSUPPORTED, "cuStreamWaitValue64 unavailable");
+    std::vector<uint8_t*> bases(world, nullptr);
+    const int me = (int)getpid();
+    for (int r = 0; r < world; ++r) {
+        P2PHandle h;
+        memcpy(&h, static_cast<const uint8_t*>(handles) + (size_t)r * MOE_P2P_HANDLE_BYTES, sizeof(h));
+        if (h.magic != kP2PMagic || h.rank != r) return fail(c, MOE_ERR_INVALID, "handle %d is not rank %d's", r, r);
+        if (h.bytes != c->sym_bytes)
+            return fail(c, MOE_ERR_INVALID, "rank %d region is %llu bytes, mine %zu (configs differ)", r,
+                        (unsigned long long)h.bytes, c->sym_bytes);
+        if (r == c->p2p_rank) {
+            if (h.pid != me || h.ptr != reinterpret_cast<uint64_t>(c->sym))
+                return fail(c, MOE_ERR_INVALID, "handle %d is not this context's", r);
+            bases[r] = c->sym;
+        } else if (h.pid == me) {
+            if (h.device != c->device) {  // same process, another GPU: direct peer access
+                cudaError_t e = cudaDeviceEnablePeerAccess(h.device, 0);
+                if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+                else CUDA_TRY(c, e);
+            }
+            bases[r] = reinterpret_cast<uint8_t*>(h.ptr);
+        } else {
+            void* p = nullptr;
+            CUDA_TRY(c, cudaIpcOpenMemHandle(&p, h.ipc, cudaIpcMemLazyEnablePeerAccess));
+            c->p2p_opened.push_back(p);
+            bases[r] = static_cast<uint8_t*>(p);
+        }
+    }
+    CUDA_TRY(c, cudaMemcpy(c->d_peers, bases.data(), sizeof(uint8_t*) * world, cudaMemcpyHostToDevice));
+    c->p2p_ready = true;
+    return MOE_OK;
+}
+
 moe_status moe_loopback_comm_destroy(void* group_or_rank) {
     if (!group_or_rank) return MOE_OK;
     if (LoopbackRank* r = as_loopback(group_or_rank)) {
@@ -1349,6 +1525,7 @@ moe_status forward_impl(moe_ctx* c, const void* tokens, int32_t T, const void* r
     if (aux && aux->out_f32 && !aligned16(aux->out_f32)) return fail(c, MOE_ERR_INVALID, "aux.out_f32 misaligned");
     if (c->fp8 && (!w->w13_scale || !w->w2_scale))
         return fail(c, MOE_ERR_INVALID, "MOE_FLAG_FP8_WEIGHTS needs w13_scale and w2_scale");
+    if (c->p2p && !c->p2p_ready) return fail(c, MOE_ERR_STATE, "MOE_FLAG_P2P context: call moe_p2p_connect first");
     c->cur_w = *w;
     moe_status s = ensure_weight_maps(c, w);
     if (s) return s;
@@ -1398,8 +1575,38 @@ moe_status forward_impl(moe_ctx* c, const void* tokens, int32_t T, const void* r
     cp.x = nullptr;
     cp.out = nullptr;
     cp.out_f32 = c->tp_partial;
+    if (c->p2p) {
+        // reduce-scatter by stores: each token's fp32 partial goes to its owner's slot
+        cp.out_f32 = nullptr;
+        cp.peers = c->d_peers; cp.peer_off = c->so.tp_slots;
+        cp.G = c->tp_world; cp.my_rank = c->tp_rank; cp.shard_max = c->tp_shard_max;
+    }
     if ((s = launch(c, kSlotCombine, moe_combine_kernel, dim3((unsigned)((c->d + 4095) / 4096 * (int64_t)T)), dim3(256), 0, st, cp)))
         return s;
+    if (c->p2p) {
+        const int G = c->tp_world, r = c->tp_rank;
+        const int t0 = (int)((int64_t)r * T / G), n = (int)((int64_t)(r + 1) * T / G) - t0;
+        float* of32 = aux ? aux->out_f32 : nullptr;
+        StepTimer t1(c, kSlotExchange, st);
+        if ((s = p2p_arrive_and_wait(c, 2, st))) return s;
+        t1.done();
+        const int fb = (int)std::max<int64_t>(1, std::min<int64_t>(4 * c->num_sms, ((int64_t)n * c->d / 4 + 255) / 256));
+        if ((s = launch(c, kSlotCombine, moe_tp_p2p_finish_kernel, dim3(fb), dim3(256), 0, st,
+                        reinterpret_cast<const float*>(c->sym + c->so.tp_slots), G, c->tp_shard_max, t0, n, c->d,
+                        residual ? static_cast<const __nv_bfloat16*>(tokens) : nullptr,
+                        static_cast<__nv_bfloat16*>(out), of32, reinterpret_cast<__nv_bfloat16*>(c->sym + c->so.tp_keep16),
+                        reinterpret_cast<float*>(c->sym + c->so.tp_keep32))))
+            return s;
+        StepTimer t2(c, kSlotExchange, st);
+        if ((s = p2p_arrive_and_wait(c, 3, st))) return s;
+        const int pb = (int)std::max<int64_t>(1, std::min<int64_t>(4 * c->num_sms, ((int64_t)T * c->d / 8 + 255) / 256));
+        if ((s = launch(c, kSlotExchange, moe_tp_p2p_pull_kernel, dim3(pb), dim3(256), 0, st,
+                        static_cast<uint8_t* const*>(c->d_peers), c->so.tp_keep16, c->so.tp_keep32, G, r, T, c->d,
+                        static_cast<__nv_bfloat16*>(out), of32)))
+            return s;
+        t2.done();
+        return MOE_OK;
+    }
     const int64_t n = (int64_t)T * c->d, cnt = n / c->G, base = cnt * c->rank;
     const CommRef tpc = tp_comm(c);
     ncclComm_t comm = c->cfg.nccl_comm;
@@ -1429,6 +1636,74 @@ moe_status forward_impl(moe_ctx* c, const void* tokens, int32_t T, const void* r
 // all-to-all (bf16 rows + local-expert ids, -1 = empty slot) -> group the received
 // rows by local expert (same K1/K2 machinery, k = 1) -> K3/K4 -> fp32 rows back to
 // their slots -> NCCL all-to-all -> K5 combine at the source rank.
+// EP over peer memory (MOE_FLAG_P2P): the dispatch permute stores each routed row
+// into its slot of the destination's receive buffer, the gather kernel stores each
+// expert-output row into the source's return buffer; one arrival counter per
+// exchange. Same slots, same arithmetic as the NCCL capacity path.
+moe_status forward_ep_p2p(moe_ctx* c, const void* tokens, int32_t T, const void* router_w, void* out,
+                          const moe_aux* aux, cudaStream_t st) {
+    moe_status s;
+    const int G = c->ep_world, me = c->ep_rank;
+    const int cap = c->max_T * c->k;
+    const int64_t R = (int64_t)cap * G;
+    uint8_t* const* peers = c->d_peers;
+    StepTimer t1(c, kSlotDispatch, st);
+    if (T > 0) {
+        RouteSpec r;
+        r.x = tokens; r.T = T; r.k = c->k; r.router_w = router_w;
+        r.key_lo = 0; r.key_div = c->E_local; r.nkeys = G; r.seg_align = 1;
+        r.logits = aux ? aux->logits : nullptr;
+        r.topk_idx = c->topk_idx; r.topk_w = c->topk_w;
+        r.pos = c->pos; r.pos_aux = aux ? aux->pos : nullptr;
+        r.dst_rows = nullptr; r.cap = cap; r.meta = nullptr;
+        r.peers = peers; r.peer_rows_off = c->so.ep_rows; r.peer_meta_off = c->so.ep_meta; r.my_rank = me;
+        if ((s = route_and_permute(c, r, st))) return s;
+        if ((s = copy_aux(c, aux, T, st))) return s;
+    }
+    // this rank's unused slots in every destination's receive buffer -> -1
+    const int fbx = std::max(1, std::min(64, (cap + 255) / 256));
+    if ((s = launch(c, kSlotDispatch, moe_ep_p2p_fill_kernel, dim3(fbx, G), dim3(256), 0, st, peers, c->so.ep_meta,
+                    T > 0 ? static_cast<const int32_t*>(c->counts) : nullptr, G, cap, me)))
+        return s;
+    if ((s = p2p_arrive_and_wait(c, 0, st))) return s;
+    t1.done();
+    // receive side: as the NCCL path, over this rank's region
+    RouteSpec r2;
+    r2.x = c->sym + c->so.ep_rows; r2.T = (int)R; r2.k = 1;
+    r2.in_idx = reinterpret_cast<const int32_t*>(c->sym + c->so.ep_meta); r2.in_w = nullptr; r2.allow_neg = 1;
+    r2.key_lo = 0; r2.key_div = 1; r2.nkeys = c->E_local; r2.seg_align = kSegAlign;
+    r2.topk_idx = c->ep_ridx; r2.topk_w = c->ep_rw; r2.pos = c->ep_rpos;
+    r2.dst_rows = c->x_perm;
+    if ((s = route_and_permute(c, r2, st))) return s;
+    if ((s = copy_aux_segments(c, aux, st))) return s;
+    const int64_t rows_expected = (int64_t)T * c->k;
+    const bool swap = (c->cfg.flags & MOE_FLAG_FORCE_SWAP) || c->fp8 ? true
+                    : (c->cfg.flags & MOE_FLAG_FORCE_TILED) ? false
+                    : rows_expected <= (int64_t)c->swap_rows_per_expert * c->E_local;
+    int splits = 1;
+    if ((s = run_gemms(c, swap, std::min<int64_t>(R, (int64_t)G * c->max_T), R, &splits, st))) return s;
+    StepTimer t2(c, kSlotExchange, st);
+    if ((s = launch(c, kSlotExchange, moe_ep_gather_kernel, dim3((unsigned)((c->d + 1023) / 1024 * R)), dim3(256), 0,
+                    st, static_cast<const float*>(c->y), c->split_stride, splits,
+                    static_cast<const int32_t*>(c->ep_rpos), (int)R, c->d, static_cast<float*>(nullptr), peers,
+                    c->so.ep_yret, cap, me)))
+        return s;
+    if ((s = p2p_arrive_and_wait(c, 1, st))) return s;
+    t2.done();
+    if (T == 0) return MOE_OK;
+    CombineParams cp{};
+    cp.y = reinterpret_cast<const float*>(c->sym + c->so.ep_yret);
+    cp.split_stride = 0;
+    cp.splits = 1;
+    cp.pos = c->pos;
+    cp.topk_w = c->topk_w;
+    cp.x = (c->cfg.flags & MOE_FLAG_RESIDUAL) ? static_cast<const __nv_bfloat16*>(tokens) : nullptr;
+    cp.T = T; cp.d = c->d; cp.k = c->k;
+    cp.out = static_cast<__nv_bfloat16*>(out);
+    cp.out_f32 = aux ? aux->out_f32 : nullptr;
+    return launch(c, kSlotCombine, moe_combine_kernel, dim3((unsigned)((c->d + 4095) / 4096 * (int64_t)T)), dim3(256), 0, st, cp);
+}
+
 moe_status forward_ep(moe_ctx* c, const void* tokens, int32_t T, const void* router_w, void* out,
                       const moe_aux* aux, cudaStream_t st) {
     moe_status s;
@@ -1438,6 +1713,7 @@ moe_status forward_ep(moe_ctx* c, const void* tokens, int32_t T, const void* rou
     const int64_t cap = (int64_t)c->max_T * c->k;
     const int64_t R = cap * G;
     ncclComm_t comm = c->cfg.nccl_comm;
+    if (c->p2p) return forward_ep_p2p(c, tokens, T, router_w, out, aux, st);
     CUDA_TRY(c, cudaMemsetAsync(c->ep_meta_send, 0xFF, sizeof(int32_t) * R, st));  // all slots empty (-1)
     if (T > 0) {
         RouteSpec r;
@@ -1499,7 +1775,8 @@ moe_status forward_ep(moe_ctx* c, const void* tokens, int32_t T, const void* rou
     if ((s = run_gemms(c, swap, std::min<int64_t>(R, (int64_t)G * c->max_T), R, &splits, st))) return s;
     if ((s = launch(c, kSlotExchange, moe_ep_gather_kernel, dim3((unsigned)((c->d + 1023) / 1024 * R)), dim3(256), 0,
                     st, static_cast<const float*>(c->y), c->split_stride, splits,
-                    static_cast<const int32_t*>(c->ep_rpos), (int)R, c->d, c->ep_ysend)))
+                    static_cast<const int32_t*>(c->ep_rpos), (int)R, c->d, c->ep_ysend,
+                    static_cast<uint8_t* const*>(nullptr), (int64_t)0, 0, 0)))
         return s;
     StepTimer t2(c, kSlotExchange, st);
     if (c->tp_world > 1) {

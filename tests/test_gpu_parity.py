@@ -245,33 +245,49 @@ def test_gather_equals_copy(moe, mixtral_weights, T, flags):
 
 
 # ---------------------------------------------------------------- EP / TP device path (loopback transport)
-def _run_group(moe, inp, par, G, shards, k=2, flags=0, max_tokens=None):
-    """G contexts on one GPU, each driven by its own thread, exchanging through the
-    loopback transport. shards[r] = token tensor of rank r. Returns per-rank (out, aux)."""
+def _run_group(moe, inp, par, G, shards, k=2, flags=0, max_tokens=None, p2p=False, iters=1):
+    """G contexts on one GPU, each driven by its own thread (and stream), exchanging
+    through the loopback transport, or through peer memory (p2p: MOE_FLAG_P2P, the
+    handles of the G regions connected in-process). shards[r] = token tensor of rank
+    r. Returns per-rank (out, aux) of the last of `iters` forwards (all must agree)."""
     import threading
-    grp = moe.moe_loopback_comm_create(G)
-    comms = [moe.moe_loopback_comm_rank(grp, r) for r in range(G)]
+    if p2p:
+        grp, comms, flags = None, [None] * G, flags | moe.MOE_FLAG_P2P
+    else:
+        grp = moe.moe_loopback_comm_create(G)
+        comms = [moe.moe_loopback_comm_rank(grp, r) for r in range(G)]
     mt = max_tokens or max(1, max(s.shape[0] for s in shards))
     blocks = [moe.MoEBlock(inp["wg"], inp["w1"], inp["w3"], inp["w2"], top_k=k, max_tokens=mt, par=par,
                            world_size=G, rank=r, nccl_comm=comms[r], flags=flags) for r in range(G)]
+    if p2p:
+        handles = [b.p2p_handle() for b in blocks]
+        for b in blocks:
+            b.p2p_connect(handles)
     torch.cuda.synchronize()
     E, d = inp["wg"].shape
     res = [None] * G
     errs = []
+    streams = [torch.cuda.Stream() for _ in range(G)]  # consecutive pool streams: distinct hardware queues
 
     def work(r):
         try:
-            st = torch.cuda.Stream()
+            st = streams[r]
             x = shards[r]
             T = x.shape[0]
             aux = {"topk_idx": torch.empty(max(T, 1), k, dtype=torch.int32, device="cuda"),
                    "out_f32": torch.empty(max(T, 1), d, dtype=torch.float32, device="cuda")}
             out = torch.empty(max(T, 1), d, dtype=torch.bfloat16, device="cuda")
-            with torch.cuda.stream(st):
-                moe.moe_forward(blocks[r].ctx, x if T else out, T, blocks[r].router_w, blocks[r].w13, blocks[r].w2,
-                                out, aux, st)
-            st.synchronize()
-            res[r] = (out[:T].clone(), {n: v[:T].clone() for n, v in aux.items()})
+            first = None
+            for it in range(iters):
+                with torch.cuda.stream(st):
+                    moe.moe_forward(blocks[r].ctx, x if T else out, T, blocks[r].router_w, blocks[r].w13,
+                                    blocks[r].w2, out, aux, st)
+                st.synchronize()
+                res[r] = (out[:T].clone(), {n: v[:T].clone() for n, v in aux.items()})
+                if first is None:
+                    first = res[r][0]
+                elif not torch.equal(first.view(torch.int16), res[r][0].view(torch.int16)):
+                    raise AssertionError(f"rank {r}: iteration {it} differs from iteration 0")
         except Exception as ex:  # pragma: no cover - surfaced below
             errs.append((r, ex))
 
@@ -282,9 +298,10 @@ def _run_group(moe, inp, par, G, shards, k=2, flags=0, max_tokens=None):
         t.join(timeout=600)
     for b in blocks:
         b.close()
-    for cm in comms:
-        moe.moe_loopback_comm_destroy(cm)
-    moe.moe_loopback_comm_destroy(grp)
+    if grp is not None:
+        for cm in comms:
+            moe.moe_loopback_comm_destroy(cm)
+        moe.moe_loopback_comm_destroy(grp)
     assert not errs, errs
     return res
 
@@ -327,6 +344,99 @@ def test_ep_loopback(moe, G, mode):
     _check_group_outputs(host, 2, host["x"], outs, auxs)
 
 
+@pytest.mark.parametrize("G", [1, 2, 4, 8])
+@pytest.mark.parametrize("par", ["ep", "tp"])
+@pytest.mark.parametrize("mode", ["swap", "tiled"])
+def test_p2p_equals_collectives(moe, G, par, mode):
+    """Peer-memory transport (MOE_FLAG_P2P): the same slots and the same summation
+    order as the collective path, so outputs must match it bit for bit (and the
+    oracle within tolerance), over 3 back-to-back forwards (counter epochs, buffer
+    reuse), with a rank that has no tokens (EP)."""
+    if par == "tp" and G == 8:
+        pytest.skip("f=512 / 8 < 128")
+    shape = synth.MoEShape(T=96, d=256, f=512, E=8, k=2)
+    inp = _inputs(shape, 70 + G)
+    host = to_host_inputs(inp)
+    if par == "ep":
+        cuts = np.linspace(0, shape.T, G + 1).astype(int)
+        if G >= 2:
+            cuts[1] = 0
+        shards = [inp["x"][cuts[r]:cuts[r + 1]] for r in range(G)]
+        pm = moe.MOE_PAR_EP
+    else:
+        shards = [inp["x"]] * G
+        pm = moe.MOE_PAR_TP
+    ref = _run_group(moe, inp, pm, G, shards, flags=MODES[mode], max_tokens=shape.T)
+    got = _run_group(moe, inp, pm, G, shards, flags=MODES[mode], max_tokens=shape.T, p2p=True, iters=3)
+    for r in range(G):
+        assert torch.equal(ref[r][0].view(torch.int16), got[r][0].view(torch.int16)), r
+        assert torch.equal(ref[r][1]["out_f32"], got[r][1]["out_f32"]), r
+    if par == "ep":
+        _check_group_outputs(host, 2, host["x"], [g[0] for g in got], [g[1] for g in got])
+    else:
+        for r in range(1, G):
+            assert torch.equal(got[0][0], got[r][0])
+        _check_group_outputs(host, 2, host["x"], [got[0][0]], [got[0][1]])
+
+
+@pytest.mark.parametrize("par", ["ep", "tp"])
+def test_p2p_multiprocess_ipc(moe, par, tmp_path):
+    """MOE_FLAG_P2P across two PROCESSES (CUDA IPC mappings of each other's region,
+    handles all-gathered over gloo), both on this GPU: bitwise equal to the
+    in-process collective path and to itself over 3 forwards."""
+    import socket
+    import subprocess
+    import sys
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.join(root, "tests", "p2p_worker.py"), par, str(tmp_path)]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=root)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    got = [torch.load(tmp_path / f"rank{i}.pt") for i in range(2)]
+    shape = synth.MoEShape(T=96, d=256, f=512, E=8, k=2)
+    inp = _inputs(shape, 81)
+    if par == "ep":
+        cuts = np.linspace(0, shape.T, 3).astype(int)
+        shards = [inp["x"][cuts[i]:cuts[i + 1]] for i in range(2)]
+        ref = _run_group(moe, inp, moe.MOE_PAR_EP, 2, shards, max_tokens=shape.T)
+    else:
+        ref = _run_group(moe, inp, moe.MOE_PAR_TP, 2, [inp["x"]] * 2, max_tokens=shape.T)
+    for i in range(2):
+        for o in got[i]["outs"]:
+            assert torch.equal(o.view(torch.int16), ref[i][0].cpu().view(torch.int16)), i
+        assert torch.equal(got[i]["out_f32"], ref[i][1]["out_f32"].cpu())
+
+
+def test_p2p_errors(moe):
+    """MOE_FLAG_P2P: forward before connect, wrong world, hybrid, foreign handle."""
+    shape = synth.MoEShape(T=8, d=64, f=256, E=4, k=2)
+    inp = _inputs(shape, 3)
+    mk = lambda r, G=2: moe.MoEBlock(inp["wg"], inp["w1"], inp["w3"], inp["w2"], max_tokens=8, par=moe.MOE_PAR_EP,
+                                     world_size=G, rank=r, flags=moe.MOE_FLAG_P2P)
+    a, b = mk(0), mk(1)
+    with pytest.raises(moe.MoEError, match="connect"):
+        a.forward(inp["x"])
+    with pytest.raises(moe.MoEError):
+        a.p2p_connect([a.p2p_handle()])                      # world 1 != 2
+    with pytest.raises(moe.MoEError):
+        a.p2p_connect([b.p2p_handle(), a.p2p_handle()])      # rank order swapped
+    c4 = mk(0, 4)
+    with pytest.raises(moe.MoEError):
+        a.p2p_connect([c4.p2p_handle(), b.p2p_handle()])     # region of another config
+    with pytest.raises(moe.MoEError):
+        moe.MoEBlock(inp["wg"], inp["w1"], inp["w3"], inp["w2"], max_tokens=8, par=moe.MOE_PAR_HYBRID,
+                     world_size=2, rank=0, tp_size=2, flags=moe.MOE_FLAG_P2P)
+    plain = moe.MoEBlock(inp["wg"], inp["w1"], inp["w3"], inp["w2"], max_tokens=8)
+    with pytest.raises(moe.MoEError):
+        plain.p2p_handle()
+    for blk in (a, b, c4, plain):
+        blk.close()
+
+
 @pytest.mark.parametrize("G", [1, 2, 4])
 @pytest.mark.parametrize("mode", ["swap", "tiled"])
 def test_tp_loopback(moe, G, mode):
@@ -341,19 +451,21 @@ def test_tp_loopback(moe, G, mode):
     _check_group_outputs(host, 2, host["x"], [res[0][0]], [res[0][1]])
 
 
-@pytest.mark.parametrize("par", ["ep", "ep_exact", "tp"])
+@pytest.mark.parametrize("par", ["ep", "ep_exact", "tp", "ep_p2p", "tp_p2p"])
 def test_mixtral_decode_8_ranks(moe, mixtral_weights, par):
-    """BASELINE configs[3]/[4] shapes at G=8 (loopback): 64-token decode, Mixtral layer."""
+    """BASELINE configs[3]/[4] shapes at G=8 (loopback / in-process peer memory):
+    64-token decode, Mixtral layer."""
     w, host = mixtral_weights
     x = synth.make_tokens(64, 4096, seed=300, device="cuda")
     G = 8
+    p2p = par.endswith("p2p")
     if par.startswith("ep"):
         shards = [x[8 * r:8 * (r + 1)] for r in range(G)]
         res = _run_group(moe, w, moe.MOE_PAR_EP, G, shards, max_tokens=8,
-                         flags=moe.MOE_FLAG_EP_EXACT if par == "ep_exact" else 0)
+                         flags=moe.MOE_FLAG_EP_EXACT if par == "ep_exact" else 0, p2p=p2p, iters=2 if p2p else 1)
         outs, auxs = [r[0] for r in res], [r[1] for r in res]
     else:
-        res = _run_group(moe, w, moe.MOE_PAR_TP, G, [x] * G, max_tokens=64)
+        res = _run_group(moe, w, moe.MOE_PAR_TP, G, [x] * G, max_tokens=64, p2p=p2p, iters=2 if p2p else 1)
         for r in range(1, G):
             assert torch.equal(res[r][0].view(torch.int16), res[0][0].view(torch.int16))
         outs, auxs = [res[0][0]], [res[0][1]]
