@@ -945,6 +945,10 @@ moe_status check_ready(moe_ctx* c) {
 }
 
 moe_status p2p_arrive_and_wait(moe_ctx* c, int idx, cudaStream_t st) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    CUDA_TRY(c, cudaStreamIsCapturing(st, &cs));
+    if (cs != cudaStreamCaptureStatusNone)  // the wait target advances every forward
+        return fail(c, MOE_ERR_UNSUPPORTED, "MOE_FLAG_P2P forwards cannot be captured into a CUDA graph");
     const int64_t sig_off = c->so.sig + 8 * idx;
     moe_status s = launch(c, kSlotExchange, moe_p2p_signal_kernel, dim3(1), dim3(32), 0, st,
                           static_cast<uint8_t* const*>(c->d_peers), c->p2p_world, sig_off);

@@ -433,7 +433,18 @@ def test_p2p_errors(moe):
     plain = moe.MoEBlock(inp["wg"], inp["w1"], inp["w3"], inp["w2"], max_tokens=8)
     with pytest.raises(moe.MoEError):
         plain.p2p_handle()
-    for blk in (a, b, c4, plain):
+    one = mk(0, 1)
+    one.p2p_connect([one.p2p_handle()])
+    with pytest.raises(moe.MoEError):
+        one.p2p_connect([one.p2p_handle()])                  # connected twice
+    one.forward(inp["x"])
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with pytest.raises(Exception):
+        with torch.cuda.graph(g):
+            one.forward(inp["x"])                            # not graph-capturable
+    torch.cuda.synchronize()
+    for blk in (a, b, c4, plain, one):
         blk.close()
 
 
