@@ -174,7 +174,12 @@ struct moe_ctx {
     // decode (swap-AB) GEMMs while the mean rows per local expert T*k/E_l <= this:
     // the weight stream dominates up to ~2 token tiles of 128 per expert (bench r01:
     // 32-layer T=575 stack 18.5 ms swap vs 20.8 ms CTA-pair tiles)
-    int swap_rows_per_expert = 256;
+    int swap_rows_per_expert = 256;   // w1/w3 GEMM (env MOE_G1_SWAP_ROWS)
+    // w2 GEMM (env MOE_G2_SWAP_ROWS). r01: an isolated layer favours CTA pairs for the
+    // w2 GEMM from ~40 rows per expert (scripts/exp/sweep_g2.sh), but inside the
+    // 32-layer stack (T=575) the swap kernel's weight prefetch under PDL wins:
+    // 17.85 ms vs 18.5-18.7 ms per step (scripts/ab_env.sh, interleaved) -> 256.
+    int swap2_rows_per_expert = 256;
     int max_splits = 4;
     int64_t split_stride = 0; // elements between split-K partial buffers of this forward
     bool fp8 = false;             // MOE_FLAG_FP8_WEIGHTS
@@ -632,63 +637,89 @@ moe_status route_and_permute(moe_ctx* c, const RouteSpec& r, cudaStream_t st) {
 // rows_bound: upper bound of the rows of any one local expert (picks the swap-path
 // token tile NB so one tile covers the whole expert at decode); rows_total: bound
 // of all permuted rows (sizes the split-K partial buffers).
-moe_status run_gemms(moe_ctx* c, bool swap, int64_t rows_bound, int64_t rows_total, int* splits_out,
+// Which GEMM family runs each GEMM: the swap-AB (decode) kernels while the rows of a
+// local expert stay small, the tokens-as-M tiles (CTA pairs) beyond. The two GEMMs
+// switch at different sizes: the w2 swap tile reads its token operand (h, NB rows)
+// from L2 for every 128 weight rows, which costs more than the w1/w3 tile (256
+// weight rows per token tile) -- r01 sweep, scripts/exp/stack_breakdown.py.
+struct GemmPaths {
+    bool swap1, swap2;
+};
+GemmPaths gemm_paths(const moe_ctx* c, int64_t rows_expected) {
+    if ((c->cfg.flags & MOE_FLAG_FORCE_SWAP) || c->fp8) return {true, true};  // fp8 weights: decode GEMMs only
+    if (c->cfg.flags & MOE_FLAG_FORCE_TILED) return {false, false};
+    return {rows_expected <= (int64_t)c->swap_rows_per_expert * c->E_local,
+            rows_expected <= (int64_t)c->swap2_rows_per_expert * c->E_local};
+}
+
+// K3 + K4 over the expert segments described by the device-side counts/offsets.
+// rows_bound: upper bound of the rows of any one local expert (picks the swap-path
+// token tile NB so one tile covers the whole expert at decode); rows_total: bound
+// of all permuted rows (sizes the split-K partial buffers).
+moe_status run_gemms(moe_ctx* c, GemmPaths gp, int64_t rows_bound, int64_t rows_total, int* splits_out,
                      cudaStream_t st) {
     moe_status s;
     int splits = 1;
     c->split_stride = 0;
-    if (swap) {
-        const int64_t rows_needed = round_up(rows_total + (int64_t)c->E_local * (kSegAlign - 1), kSegAlign);
-        splits = c->cfg.split_k ? c->cfg.split_k : c->max_splits;
-        splits = (int)std::max<int64_t>(1, std::min<int64_t>(splits, c->y_elems / (rows_needed * c->d)));
-        splits = std::min(splits, c->f_local / (c->fp8_g2_kb256 ? 256 : c->fp8_kb128 ? 128 : kBK));  // >= 1 K block per split
-        c->split_stride = rows_needed * c->d;
-        // Token tile NB: one tile covers an expert's rows when possible (the weight tile
-        // then streams once). GEMM1 stops at 128 (NB = 256 leaves its w1|w3 accumulators
-        // single-buffered: measured slower, 32-layer stack r01), GEMM2 goes to 256;
-        // FP8 kernels stop at 128.
-        const int nbw = (int)std::max<int64_t>(32, std::min<int64_t>(256, next_pow2((int)std::min<int64_t>(rows_bound, 1 << 20))));
-        const int nb1 = std::min(nbw, 128), nb2 = c->fp8 ? nb1 : nbw;
+    // Token tile NB of the swap kernels: one tile covers an expert's rows when possible
+    // (the weight tile then streams once). GEMM1 stops at 128 (NB = 256 leaves its
+    // w1|w3 accumulators single-buffered: measured slower, 32-layer stack r01), GEMM2
+    // goes to 256; FP8 kernels stop at 128.
+    const int nbw = (int)std::max<int64_t>(32, std::min<int64_t>(256, next_pow2((int)std::min<int64_t>(rows_bound, 1 << 20))));
+    const int nb1 = std::min(nbw, 128), nb2 = c->fp8 ? nb1 : nbw;
+    const bool pair = !(c->cfg.flags & MOE_FLAG_NO_PAIR);
+    // CTA-pair (cta_group::2) 256x256 tiles, one cluster of 2 CTAs per TPC; tile order
+    // per GEMM (see pair_decode); env MOE_PAIR_TUNE overrides for experiments:
+    // bits 0-1 G1 order, 2-3 G2 order, 4-9 G1 band, 10-15 G2 band
+    int r1 = c->g1_raster, r2 = c->g2_raster, b1 = c->g1_band, b2 = c->g2_band;
+    if (c->pair_tune) {
+        r1 = c->pair_tune & 3; r2 = (c->pair_tune >> 2) & 3;
+        b1 = std::max(1, (c->pair_tune >> 4) & 63); b2 = std::max(1, (c->pair_tune >> 10) & 63);
+    }
+    const int ncl = c->num_sms / 2;
+    if (gp.swap1) {
         const int i1 = nb1 == 32 ? 0 : nb1 == 64 ? 1 : 2;
         if (nb1 == 32) s = run_swap_g1<32>(c, i1, &c->cur_w, st);
         else if (nb1 == 64) s = run_swap_g1<64>(c, i1, &c->cur_w, st);
         else s = run_swap_g1<128>(c, i1, &c->cur_w, st);
         if (s) return s;
-        if (nb2 == 32) s = run_swap_g2<32>(c, 0, &c->cur_w, splits, st);
-        else if (nb2 == 64) s = run_swap_g2<64>(c, 1, &c->cur_w, splits, st);
-        else if (nb2 == 128) s = run_swap_g2<128>(c, 2, &c->cur_w, splits, st);
-        else s = run_swap_g2<256>(c, 3, &c->cur_w, splits, st);
-        if (s) return s;
-    } else if (!(c->cfg.flags & MOE_FLAG_NO_PAIR)) {
-        // CTA-pair (cta_group::2) 256x256 tiles, one cluster of 2 CTAs per TPC
+    } else if (pair) {
         const int64_t mt_max = rows_total / 256 + c->E_local;
-        const int ncl = c->num_sms / 2;
         const int g1 = (int)std::min<int64_t>(ncl, mt_max * (c->f_local / 128));
-        const int g2 = (int)std::min<int64_t>(ncl, mt_max * ((c->d + 255) / 256));
-        // tile order per GEMM (see pair_decode); env MOE_PAIR_TUNE overrides for experiments:
-        // bits 0-1 G1 order, 2-3 G2 order, 4-9 G1 band, 10-15 G2 band
-        int r1 = c->g1_raster, r2 = c->g2_raster, b1 = c->g1_band, b2 = c->g2_band;
-        if (c->pair_tune) {
-            r1 = c->pair_tune & 3; r2 = (c->pair_tune >> 2) & 3;
-            b1 = std::max(1, (c->pair_tune >> 4) & 63); b2 = std::max(1, (c->pair_tune >> 10) & 63);
-        }
         GemmParams p1{c->counts, c->offsets, c->E_local, c->d, c->f_local, 1, c->h, 0, r1, b1,
                       ptx::kEvictNormal, ptx::kEvictNormal, c->gather_now ? c->src_row : nullptr};
         if ((s = launch_gemm_pair<kG1Pair>(c, kSlotGemm1, p1, c->gather_now ? c->tm_src : c->tm_x_tiled,
                                            c->tm_w13_pair, g1, st)))
             return s;
-        GemmParams p2{c->counts, c->offsets, c->E_local, c->d, c->f_local, 1, c->y, 0, r2, b2,
-                      ptx::kEvictNormal, ptx::kEvictNormal};
-        if ((s = launch_gemm_pair<kG2Pair>(c, kSlotGemm2, p2, c->tm_h_tiled, c->tm_w2_swap, g2, st))) return s;
     } else {
         const int64_t mt_max = rows_total / 128 + c->E_local;
         const int g1 = (int)std::min<int64_t>(c->num_sms, mt_max * (c->f_local / 128));
-        const int g2 = (int)std::min<int64_t>(c->num_sms, mt_max * ((c->d + 255) / 256));
         GemmParams p1{c->counts, c->offsets, c->E_local, c->d, c->f_local, 1, c->h, 0};
         p1.src_row = c->gather_now ? c->src_row : nullptr;
         if ((s = launch_gemm<kG1Tiled, 256>(c, kSlotGemm1, p1, c->gather_now ? c->tm_src : c->tm_x_tiled, c->tm_w13,
                                             g1, st)))
             return s;
+    }
+    if (gp.swap2) {
+        const int64_t rows_needed = round_up(rows_total + (int64_t)c->E_local * (kSegAlign - 1), kSegAlign);
+        splits = c->cfg.split_k ? c->cfg.split_k : c->max_splits;
+        splits = (int)std::max<int64_t>(1, std::min<int64_t>(splits, c->y_elems / (rows_needed * c->d)));
+        splits = std::min(splits, c->f_local / (c->fp8_g2_kb256 ? 256 : c->fp8_kb128 ? 128 : kBK));  // >= 1 K block per split
+        c->split_stride = rows_needed * c->d;
+        if (nb2 == 32) s = run_swap_g2<32>(c, 0, &c->cur_w, splits, st);
+        else if (nb2 == 64) s = run_swap_g2<64>(c, 1, &c->cur_w, splits, st);
+        else if (nb2 == 128) s = run_swap_g2<128>(c, 2, &c->cur_w, splits, st);
+        else s = run_swap_g2<256>(c, 3, &c->cur_w, splits, st);
+        if (s) return s;
+    } else if (pair) {
+        const int64_t mt_max = rows_total / 256 + c->E_local;
+        const int g2 = (int)std::min<int64_t>(ncl, mt_max * ((c->d + 255) / 256));
+        GemmParams p2{c->counts, c->offsets, c->E_local, c->d, c->f_local, 1, c->y, 0, r2, b2,
+                      ptx::kEvictNormal, ptx::kEvictNormal};
+        if ((s = launch_gemm_pair<kG2Pair>(c, kSlotGemm2, p2, c->tm_h_tiled, c->tm_w2_swap, g2, st))) return s;
+    } else {
+        const int64_t mt_max = rows_total / 128 + c->E_local;
+        const int g2 = (int)std::min<int64_t>(c->num_sms, mt_max * ((c->d + 255) / 256));
         GemmParams p2{c->counts, c->offsets, c->E_local, c->d, c->f_local, 1, c->y, 0};
         if ((s = launch_gemm<kG2Tiled, 256>(c, kSlotGemm2, p2, c->tm_h_tiled, c->tm_w2_tiled, g2, st))) return s;
     }
@@ -931,12 +962,6 @@ CommRef tp_comm(const moe_ctx* c) {
     return {c->cfg.par == MOE_PAR_HYBRID ? c->cfg.tp_comm : c->cfg.nccl_comm, c->tp_world, c->tp_rank};
 }
 
-bool use_swap_path(const moe_ctx* c, int T) {
-    if ((c->cfg.flags & MOE_FLAG_FORCE_SWAP) || c->fp8) return true;  // fp8 weights: decode GEMMs only
-    if (c->cfg.flags & MOE_FLAG_FORCE_TILED) return false;
-    return (int64_t)T * c->k <= (int64_t)c->swap_rows_per_expert * c->E_local;
-}
-
 moe_status check_ready(moe_ctx* c) {
     if (!c) return MOE_ERR_INVALID;
     if (c->poisoned) return fail(c, MOE_ERR_STATE, "context poisoned by an earlier CUDA error: %s", c->err.c_str());
@@ -1049,6 +1074,8 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
     if (const char* v = getenv("MOE_FP8_G2_KB")) c->fp8_g2_kb256 = c->fp8_g2_kb256 && atoi(v) == 256;
     if (const char* pt = getenv("MOE_PAIR_TUNE")) c->pair_tune = atoi(pt);
     if (const char* v = getenv("MOE_GATHER")) c->gather = atoi(v) != 0;
+    if (const char* v = getenv("MOE_G1_SWAP_ROWS")) c->swap_rows_per_expert = atoi(v);
+    if (const char* v = getenv("MOE_G2_SWAP_ROWS")) c->swap2_rows_per_expert = atoi(v);
     if (cfg->flags & MOE_FLAG_GATHER) c->gather = true;
     // router blocks of >= 2 rows; EP also routes the G*max_T*k receive slots
     c->nblk_max = (int)(((int64_t)c->max_T * (c->ep_world > 1 ? c->ep_world * c->k : 1) + 1) / 2 + 1);
@@ -1057,7 +1084,7 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
     const bool ep_like = cfg->par == MOE_PAR_EP || cfg->par == MOE_PAR_HYBRID;
     const int64_t rows_in = ep_like ? (int64_t)c->max_T * c->ep_world : c->max_T;
     c->cap = round_up(rows_in * c->k + (int64_t)c->E_local * (kSegAlign - 1), kSegAlign);
-    const int64_t swap_T = std::min<int64_t>(rows_in, (int64_t)c->swap_rows_per_expert * c->E_local / c->k);
+    const int64_t swap_T = std::min<int64_t>(rows_in, (int64_t)c->swap2_rows_per_expert * c->E_local / c->k);
     c->cap_swap = round_up(swap_T * c->k + (int64_t)c->E_local * (kSegAlign - 1), kSegAlign);
     c->y_elems = std::max<int64_t>(c->cap, c->cap_swap * c->max_splits) * c->d;
 
@@ -1555,9 +1582,8 @@ moe_status forward_impl(moe_ctx* c, const void* tokens, int32_t T, const void* r
     r.dst_rows = c->gather_now ? nullptr : c->x_perm;
     r.src_row = c->gather_now ? c->src_row : nullptr;
     if ((s = route_and_permute(c, r, st))) return s;
-    const bool swap = use_swap_path(c, T);
     int splits = 1;
-    if ((s = run_gemms(c, swap, T, (int64_t)T * c->k, &splits, st))) return s;
+    if ((s = run_gemms(c, gemm_paths(c, (int64_t)T * c->k), T, (int64_t)T * c->k, &splits, st))) return s;
     if ((s = copy_aux(c, aux, T, st)) || (s = copy_aux_segments(c, aux, st))) return s;
 
     CombineParams cp{};
@@ -1681,11 +1707,9 @@ moe_status forward_ep_p2p(moe_ctx* c, const void* tokens, int32_t T, const void*
     if ((s = route_and_permute(c, r2, st))) return s;
     if ((s = copy_aux_segments(c, aux, st))) return s;
     const int64_t rows_expected = (int64_t)T * c->k;
-    const bool swap = (c->cfg.flags & MOE_FLAG_FORCE_SWAP) || c->fp8 ? true
-                    : (c->cfg.flags & MOE_FLAG_FORCE_TILED) ? false
-                    : rows_expected <= (int64_t)c->swap_rows_per_expert * c->E_local;
     int splits = 1;
-    if ((s = run_gemms(c, swap, std::min<int64_t>(R, (int64_t)G * c->max_T), R, &splits, st))) return s;
+    if ((s = run_gemms(c, gemm_paths(c, rows_expected), std::min<int64_t>(R, (int64_t)G * c->max_T), R, &splits, st)))
+        return s;
     StepTimer t2(c, kSlotExchange, st);
     if ((s = launch(c, kSlotExchange, moe_ep_gather_kernel, dim3((unsigned)((c->d + 1023) / 1024 * R)), dim3(256), 0,
                     st, static_cast<const float*>(c->y), c->split_stride, splits,
@@ -1772,11 +1796,9 @@ moe_status forward_ep(moe_ctx* c, const void* tokens, int32_t T, const void* rou
         rows_expected = 0;
         for (int p = 0; p < G; ++p) rows_expected += c->h_counts[64 + p];
     }
-    const bool swap = (c->cfg.flags & MOE_FLAG_FORCE_SWAP) || c->fp8 ? true
-                    : (c->cfg.flags & MOE_FLAG_FORCE_TILED) ? false
-                    : rows_expected <= (int64_t)c->swap_rows_per_expert * c->E_local;
     int splits = 1;
-    if ((s = run_gemms(c, swap, std::min<int64_t>(R, (int64_t)G * c->max_T), R, &splits, st))) return s;
+    if ((s = run_gemms(c, gemm_paths(c, rows_expected), std::min<int64_t>(R, (int64_t)G * c->max_T), R, &splits, st)))
+        return s;
     if ((s = launch(c, kSlotExchange, moe_ep_gather_kernel, dim3((unsigned)((c->d + 1023) / 1024 * R)), dim3(256), 0,
                     st, static_cast<const float*>(c->y), c->split_stride, splits,
                     static_cast<const int32_t*>(c->ep_rpos), (int)R, c->d, c->ep_ysend,

@@ -110,6 +110,23 @@ def test_multi_tile_mid_size(moe, mode):
     blk.close()
 
 
+@pytest.mark.parametrize("flags", [0, 0x10])
+def test_mixed_gemm_paths(moe, flags):
+    """Per-GEMM path choice: ~150 rows per expert with the w2 threshold at 40 runs the
+    w1/w3 GEMM swap-AB and the w2 GEMM on tokens-as-M tiles (CTA pairs, or single
+    CTAs with MOE_FLAG_NO_PAIR) -- the h buffer hand-off between the two families."""
+    shape = synth.MoEShape(T=600, d=512, f=1024, E=8, k=2)
+    inp = _inputs(shape, 17)
+    os.environ["MOE_G2_SWAP_ROWS"] = "40"  # read at moe_init: w2 GEMM on tiles from 40 rows/expert
+    try:
+        blk = _block(moe, inp, 2, 600, flags)
+    finally:
+        del os.environ["MOE_G2_SWAP_ROWS"]
+    run = GpuRun(blk, inp["x"])
+    check_forward(run, to_host_inputs(inp), 2)
+    blk.close()
+
+
 def _forced_gates(host, idx):
     l = oracle.router(host["x"], host["wg"], 1)["logits"]
     li = np.take_along_axis(l, idx.astype(np.int64), 1)
