@@ -118,11 +118,19 @@ typedef struct {
     int32_t reserved[3]; /* must be zero                                               */
 } moe_config;
 
-/* Packed expert weights of THIS rank (device, bf16, produced by moe_pack_weights).
- *   w13: [E_local, 2*f_local, d] -- w1 and w3 rows interleaved in blocks of 128:
+/* Packed expert weights of THIS rank (device, produced by moe_pack_weights).
+ *   w13 rows: 2*f_local per expert, w1 and w3 rows interleaved in blocks of 128:
  *        packed row 256*b + i     = w1 row 128*b + i  (i < 128)
  *        packed row 256*b + 128+i = w3 row 128*b + i
- *   w2:  [E_local, d, f_local]   -- HF layout, ffn slice of this rank.
+ *   w2 rows: d per expert (HF layout rows, ffn slice of this rank), zero rows
+ *        appended up to a multiple of 256.
+ *   bf16 (moe_pack_weights) -- TILED: the rows of each expert are cut into tiles
+ *        (w13: 256 rows, w2: 128 rows) and each tile is stored as K/64 consecutive
+ *        [tile_rows][64] blocks (K = d for w13, f_local for w2), so one 64-wide K
+ *        step of one tile is one contiguous 32 / 16 KB range:
+ *        element (e, row, k) of w13 at ((((e*T13 + row/256)*(d/64) + k/64)*256
+ *        + row%256)*64 + k%64, T13 = 2*f_local/256 (w2 alike with 128, f_local, T2).
+ *   FP8 (moe_pack_weights_fp8) -- plain row-major [E_local][rows][K] bytes.
  * (E_local = E/ep, f_local = f/tp: EP ep = G, TP tp = G, hybrid ep * tp = G.)   */
 typedef struct {
     const void* w13;

@@ -47,7 +47,27 @@ struct GemmParams {
     // then fetched with TMA tile::gather4 straight from the caller's rows (its map has a
     // {64, 1} box) instead of from a materialised permuted copy.
     const int32_t* src_row;
+    // kG1Swap tail split (nullable): workspace for the fp32 partial accumulators of the
+    // K-sliced tail tiles ([<= grid][2][128][NB]) and their arrival counters (zeroed;
+    // each is reset by the CTA that completes its tile); tail_parts: max slices per tile.
+    float* tail_ws;
+    int32_t* tail_cnt;
+    int32_t tail_parts;
+    // bf16 weights in the tiled packed layout (moe.cu, pack kernels): each expert's rows
+    // in tiles of w_tr rows, each tile stored as d/64 (or f/64) consecutive [w_tr][64]
+    // blocks, so one K block of one tile is one contiguous chunk of HBM. w_nt: tiles
+    // per expert. The weight maps are 4D {64, w_tr, K/64, w_nt * E}.
+    int32_t w_tr, w_nt;
 };
+
+// 4D coordinates of rows [row, row + box) of expert e at K offset kc in a tiled weight map
+// (row % w_tr + box <= w_tr, or a box spanning whole consecutive tiles).
+struct WCoord {
+    int32_t c1, c2, c3;
+};
+__device__ __forceinline__ WCoord wcoord(const GemmParams& p, int kc, int row, int e) {
+    return {row % p.w_tr, kc / 64, row / p.w_tr + e * p.w_nt};
+}
 
 constexpr int kGemmThreads = 192;
 constexpr int kBK = 64;                 // K per stage = one 128-byte swizzle atom of bf16
@@ -85,6 +105,8 @@ struct TileInfo {
     int32_t kb0, nkb; // K-block range
     int32_t m_idx, n_idx, split;
     int32_t n_valid;  // swap: valid token columns in this tile
+    int32_t part;     // tail split: K slice of this unit (-1: whole tile)
+    int32_t lidx;     // tail split: index of the tail tile
 };
 
 // Number of tiles of expert e and the tile decode. Both must be identical in
@@ -140,6 +162,48 @@ __device__ __forceinline__ bool decode_tile(int t, const GemmParams& p, const in
     return true;
 }
 
+// Tail split of the decode w1/w3 GEMM. Its tiles all stream the same bytes (256
+// weight rows x d), so with `total` tiles on G persistent CTAs the last
+// left = total % G tiles keep `left` SMs busy for a whole tile while the others idle
+// (Mixtral decode: 896 tiles on 148 SMs -> 8 SMs run a 7th tile; a streaming-read
+// model of that split reaches 6.59 TB/s vs 7.2 TB/s balanced, scripts/exp/read_bw.cu).
+// When left <= G/2, each tail tile instead runs as P K-slices on P CTAs; the slices'
+// fp32 accumulators meet in a workspace and the CTA that completes a tile sums them in
+// slice order (deterministic) and applies SwiGLU.
+struct TailPlan {
+    int full, P, units;
+};
+__device__ __forceinline__ TailPlan tail_plan(int total, int G, int nkb, const GemmParams& p) {
+    TailPlan tp{total, 1, total};
+    if (p.tail_ws == nullptr || total <= G) return tp;
+    const int left = total % G;
+    if (left == 0 || 2 * left > G) return tp;
+    const int P = min(G / left, min(p.tail_parts, nkb / 2));
+    if (P < 2) return tp;
+    tp.full = total - left;
+    tp.P = P;
+    tp.units = tp.full + left * P;
+    return tp;
+}
+
+template <int KIND, int NB>
+__device__ __forceinline__ void decode_unit(int u, const TailPlan& tp, const GemmParams& p, const int32_t* s_counts,
+                                            const int32_t* s_offsets, TileInfo& ti) {
+    if (u < tp.full) {
+        decode_tile<KIND, NB>(u, p, s_counts, s_offsets, ti);
+        ti.part = -1;
+        ti.lidx = 0;
+        return;
+    }
+    const int v = u - tp.full, l = v / tp.P, part = v % tp.P;
+    decode_tile<KIND, NB>(tp.full + l, p, s_counts, s_offsets, ti);
+    const int nk = ti.nkb, k0 = ti.kb0;
+    ti.kb0 = k0 + nk * part / tp.P;
+    ti.nkb = nk * (part + 1) / tp.P - nk * part / tp.P;
+    ti.part = part;
+    ti.lidx = l;
+}
+
 __device__ __forceinline__ float silu_f32(float a) { return a / (1.0f + __expf(-a)); }
 
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
@@ -167,6 +231,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 4);
     int32_t* s_counts = reinterpret_cast<int32_t*>(bars + 2 * S + 5);      // [32]
     int32_t* s_offsets = s_counts + 32;                                    // [33]
+    volatile int32_t* tail_flag = s_offsets + 33;                          // [1]
 
     const int warp = threadIdx.x / 32;
     const int lane = threadIdx.x % 32;
@@ -215,6 +280,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
     int total = 0;
     for (int e = 0; e < p.E; ++e) total += tiles_of<KIND, NB>(s_counts[e], p);
+    const TailPlan tp = KIND == kG1Swap ? tail_plan(total, gridDim.x, p.d / kBK, p) : TailPlan{total, 1, total};
 
     if (warp == 0) {
         // ---------------------------------------------------------------- TMA producer
@@ -228,23 +294,26 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         uint32_t phase = 0;
         int pre = 0;  // k-blocks of the first tile whose weight loads precede the wait
         if (C::kSwap && MOE_PDL_PREFETCH > 0) {
-            if ((int)blockIdx.x < total) {
+            if ((int)blockIdx.x < tp.units) {
                 TileInfo t0;
-                decode_tile<KIND, NB>(blockIdx.x, p, s_counts, s_offsets, t0);
+                decode_unit<KIND, NB>(blockIdx.x, tp, p, s_counts, s_offsets, t0);
                 pre = min(S, t0.nkb);
                 if (lane == 0)
                     for (int kb = 0; kb < pre; ++kb) {  // fresh stages: no empty-wait needed
                         ptx::mbar_arrive_expect_tx(&full[kb], C::kStageBytes);
-                        ptx::tma_load_3d(&tmA, &full[kb], smem_a + kb * C::kABytes, (t0.kb0 + kb) * kBK, t0.a_row,
-                                         t0.e, ptx::kEvictFirst);
+                    {
+                        const WCoord w = wcoord(p, (t0.kb0 + kb) * kBK, t0.a_row, t0.e);
+                        ptx::tma_load_4d(&tmA, &full[kb], smem_a + kb * C::kABytes, 0, w.c1, w.c2, w.c3,
+                                         ptx::kEvictFirst);
+                    }
                     }
             }
             ptx::pdl_wait();
         }
         bool first = true;
-        for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        for (int t = blockIdx.x; t < tp.units; t += gridDim.x) {
             TileInfo ti;
-            decode_tile<KIND, NB>(t, p, s_counts, s_offsets, ti);
+            decode_unit<KIND, NB>(t, tp, p, s_counts, s_offsets, ti);
             const int tok_row = C::kSwap ? ti.b_row : ti.a_row;
             int4 rows = make_int4(0, 0, 0, 0);
             if (gather && lane < kTokRows / 4) {
@@ -264,12 +333,16 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                     }
                     if (C::kSwap) {
                         // A = weights (3D map [K, rows, E]) streamed once: evict-first.
-                        if (!armed) ptx::tma_load_3d(&tmA, &full[stage], sa, kc, ti.a_row, ti.e, ptx::kEvictFirst);
+                        if (!armed) {
+                            const WCoord w = wcoord(p, kc, ti.a_row, ti.e);
+                            ptx::tma_load_4d(&tmA, &full[stage], sa, 0, w.c1, w.c2, w.c3, ptx::kEvictFirst);
+                        }
                         // B = permuted tokens / activations (2D map [K, Cap]): keep in L2.
                         if (!gather) ptx::tma_load_2d(&tmB, &full[stage], sb, kc, ti.b_row, ptx::kEvictLast);
                     } else {
                         if (!gather) ptx::tma_load_2d(&tmA, &full[stage], sa, kc, ti.a_row, ptx::kEvictLast);
-                        ptx::tma_load_3d(&tmB, &full[stage], sb, kc, ti.b_row, ti.e, ptx::kEvictNormal);
+                        const WCoord w = wcoord(p, kc, ti.b_row, ti.e);
+                        ptx::tma_load_4d(&tmB, &full[stage], sb, 0, w.c1, w.c2, w.c3, ptx::kEvictNormal);
                     }
                 }
                 if (gather) {
@@ -288,9 +361,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             uint32_t phase = 0;
             int acc = 0;
             uint32_t acc_phase = 0;
-            for (int t = blockIdx.x; t < total; t += gridDim.x) {
+            for (int t = blockIdx.x; t < tp.units; t += gridDim.x) {
                 TileInfo ti;
-                decode_tile<KIND, NB>(t, p, s_counts, s_offsets, ti);
+                decode_unit<KIND, NB>(t, tp, p, s_counts, s_offsets, ti);
                 uint32_t n_mma;
                 if (KIND == kG1Tiled) n_mma = 256;
                 else if (KIND == kG2Tiled) n_mma = min(256, p.d - ti.n_idx * 256);
@@ -332,9 +405,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         const int r = q * 32 + lane;             // accumulator row (= TMEM lane) of this thread
         int acc = 0;
         uint32_t acc_phase = 0;
-        for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        for (int t = blockIdx.x; t < tp.units; t += gridDim.x) {
             TileInfo ti;
-            decode_tile<KIND, NB>(t, p, s_counts, s_offsets, ti);
+            decode_unit<KIND, NB>(t, tp, p, s_counts, s_offsets, ti);
             ptx::mbar_wait(&tmem_full[acc], acc_phase);
             ptx::tc_fence_after();
             const uint32_t tbase = tmem_base + acc * C::kAccCols + (static_cast<uint32_t>(q * 32) << 16);
@@ -379,6 +452,55 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                                                  __uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3]));
                     }
                 }
+            } else if (KIND == kG1Swap && ti.part >= 0) {
+                // tail slice: fp32 partials of a (w1) and b (w3) -> workspace, column-major
+                // by token so the 128 rows of a column are one coalesced 512-byte store
+                float* ws = p.tail_ws + static_cast<int64_t>(ti.lidx * tp.P + ti.part) * (2 * 128 * NB);
+                const int nchunks = (ti.n_valid + 15) / 16;
+#pragma unroll 1
+                for (int c = 0; c < nchunks; ++c) {
+                    uint32_t a[16], b[16];
+                    ptx::tmem_ld16(tbase + c * 16, a);
+                    ptx::tmem_ld16(tbase + C::kBOff + c * 16, b);
+                    ptx::tmem_wait_ld();
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        const int n = c * 16 + i;
+                        if (n < ti.n_valid) {
+                            ws[n * 128 + r] = __uint_as_float(a[i]);
+                            ws[(NB + n) * 128 + r] = __uint_as_float(b[i]);
+                        }
+                    }
+                }
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(&tmem_empty[acc]);  // TMEM free before the fix-up
+                if (++acc == C::kAccStages) { acc = 0; acc_phase ^= 1; }
+                __threadfence();
+                asm volatile("bar.sync 1, 128;" ::: "memory");  // the 4 epilogue warps
+                if (threadIdx.x == 64) {
+                    const int old = atomicAdd(&p.tail_cnt[ti.lidx], 1);
+                    *tail_flag = old == tp.P - 1;
+                    if (old == tp.P - 1) p.tail_cnt[ti.lidx] = 0;  // all slices arrived: reset for the next launch
+                }
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+                if (*tail_flag) {  // last slice of this tile: sum the slices in order, SwiGLU, h
+                    __threadfence();
+                    const float* ws0 = p.tail_ws + static_cast<int64_t>(ti.lidx * tp.P) * (2 * 128 * NB);
+                    __nv_bfloat16* h = static_cast<__nv_bfloat16*>(p.out) + static_cast<int64_t>(ti.b_row) * p.f +
+                                       ti.m_idx * 128 + r;
+                    for (int n = 0; n < ti.n_valid; ++n) {
+                        float av = 0.f, bv = 0.f;
+                        for (int q2 = 0; q2 < tp.P; ++q2) {
+                            const float* w = ws0 + static_cast<int64_t>(q2) * (2 * 128 * NB);
+                            av += __ldcg(w + n * 128 + r);
+                            bv += __ldcg(w + (NB + n) * 128 + r);
+                        }
+                        h[static_cast<int64_t>(n) * p.f] = __float2bfloat16_rn(silu_f32(av) * bv);
+                    }
+                }
+                asm volatile("bar.sync 1, 128;" ::: "memory");  // tail_flag is reused by the next slice
+                continue;
             } else if (KIND == kG1Swap) {
                 // row r = ffn index m*128 + r (w1 at cols [0,NB), w3 at cols [128,128+NB)); col n = token
                 __nv_bfloat16* h = static_cast<__nv_bfloat16*>(p.out) + static_cast<int64_t>(ti.b_row) * p.f +
@@ -569,9 +691,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         for (int t = cid; t < total; t += ncl) {
             TileInfo ti;
             pair_decode<KIND>(t, p, s_counts, s_offsets, ti);
-            const int n_mma = KIND == kG1Pair ? 256 : min(256, p.d - ti.n_idx * 256);
+            // weights are packed with rows padded to a multiple of 256: every N tile is a full
+            // 256-row MMA (the padding rows are zeros; the epilogue stores only d columns)
             const int a_row = ti.seg + ti.m_idx * 256 + (int)crank * 128;
-            const int b_row = ti.n_idx * 256 + (int)crank * (n_mma / 2);
+            const int b_row = ti.n_idx * 256 + (int)crank * 128;
             int4 rows = make_int4(0, 0, 0, 0);
             if (gather) {
                 const int32_t* sr = p.src_row + a_row + 4 * lane;
@@ -584,7 +707,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                     ptx::mbar_wait(&empty[stage], phase ^ 1);
                     if (leader) ptx::mbar_arrive_expect_tx(&full[stage], 2 * kPairStageBytes);
                     if (!gather) ptx::tma_load_2d_pair(&tmA, fb, smem_a + stage * 16384, kc, a_row, p.hint_a);
-                    ptx::tma_load_3d_pair(&tmB, fb, smem_b + stage * 16384, kc, b_row, ti.e, p.hint_b);
+                    const WCoord w = wcoord(p, kc, b_row, ti.e);
+                    ptx::tma_load_4d_pair(&tmB, fb, smem_b + stage * 16384, 0, w.c1, w.c2, w.c3, p.hint_b);
                 }
                 if (gather) {
                     __syncwarp();
@@ -603,8 +727,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             for (int t = cid; t < total; t += ncl) {
                 TileInfo ti;
                 pair_decode<KIND>(t, p, s_counts, s_offsets, ti);
-                const uint32_t n_mma = KIND == kG1Pair ? 256u : (uint32_t)min(256, p.d - ti.n_idx * 256);
-                const uint32_t idesc = ptx::make_idesc_bf16(256, n_mma);
+                const uint32_t idesc = ptx::make_idesc_bf16(256, 256);
                 const uint32_t d_tmem = tmem_base + acc * 256;
                 ptx::mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
                 ptx::tc_fence_after();
@@ -980,6 +1103,9 @@ __global__ void __launch_bounds__(kFp8Threads, 1)
 // TMEM ([a_tmem] operand), leaving shared memory with the fp8 tile and the tokens.
 // TMEM columns: accumulators [0, 2*ACC) (ACC = 2*NB for w1|w3, NB for w2), A ring
 // after them (32 columns per 128 fp16 rows x 64 K per stage).
+#ifndef MOE_FP8_ACC_STAGES
+#define MOE_FP8_ACC_STAGES 2  // r01: 1 (3 TMEM A stages instead of 2 at NB=64) measured 0.3018 vs 0.2901 ms
+#endif
 template <int KIND, int NB, int KB>
 struct Fp8TmemCfg {
     static_assert(NB <= 64, "TMEM-A fp8 variant: NB <= 64");
@@ -992,7 +1118,8 @@ struct Fp8TmemCfg {
     static constexpr int kBBytes = kBSub * (KB / 64);
     static constexpr int kAcc = kHalves * NB;                 // TMEM columns per accumulator stage
     static constexpr int kACols = (KB / 2) * kHalves;         // TMEM columns per A stage (2 fp16 / column)
-    static constexpr int kS2Raw = (512 - 2 * kAcc) / kACols;
+    static constexpr int kAccSt = MOE_FP8_ACC_STAGES;         // accumulator stages
+    static constexpr int kS2Raw = (512 - kAccSt * kAcc) / kACols;
     static constexpr int kS2 = kS2Raw > 6 ? 6 : kS2Raw;
     static constexpr int kLoadBytes = kA8Bytes + kBBytes;
     static constexpr int kS1Raw = (kSmemBudget - 2048) / kLoadBytes;
@@ -1067,7 +1194,7 @@ __global__ void __launch_bounds__(kFp8tThreads, 1)
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_base_slot;
-    const uint32_t a_base = tmem_base + 2 * C::kAcc;
+    const uint32_t a_base = tmem_base + C::kAccSt * C::kAcc;
     int total = 0;
     for (int e = 0; e < p.E; ++e) total += tiles_of<KIND, NB>(s_counts[e], p);
 
@@ -1128,7 +1255,7 @@ __global__ void __launch_bounds__(kFp8tThreads, 1)
                     if (++s1 == S1) { s1 = 0; ph1 ^= 1; }
                 }
                 ptx::mma_commit(&tmem_full[acc]);
-                if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+                if (++acc == C::kAccSt) { acc = 0; acc_phase ^= 1; }
             }
         }
     } else if (warp >= 6) {
@@ -1256,7 +1383,7 @@ __global__ void __launch_bounds__(kFp8tThreads, 1)
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(&tmem_empty[acc]);
-            if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+            if (++acc == C::kAccSt) { acc = 0; acc_phase ^= 1; }
         }
     }
     ptx::pdl_launch_dependents();

@@ -683,8 +683,16 @@ __global__ void __launch_bounds__(256) moe_tp_finish_kernel(const float* shard, 
 // w13p[e][256*b + i][c] = w1[eg][f_off + 128*b + i][c]        (i < 128)
 //                       = w3[eg][f_off + 128*b + i - 128][c]  (i >= 128)
 // w2p[e][r][i] = w2[eg][r][f_off + i], eg = e_off + e.
+// Packing (moe_pack_weights). Row order of W13: blocks of 256 rows = 128 w1 rows then
+// the 128 w3 rows of the same ffn columns (this rank's f slice). `tiled` (bf16): every
+// 256-row block of W13 / 128-row block of W2 is stored as K/64 consecutive [rows][64]
+// chunks (32 / 16 KB): one K block of one tile is one contiguous HBM range -- a
+// streaming read of such chunks runs at 7.26 TB/s vs 6.19 TB/s for 128-byte pieces of
+// 128 rows 28 KB apart (the row-major W2), scripts/exp/read_bw.cu. W2 rows are padded
+// with zeros to a multiple of 256. tiled = 0 (FP8 packing, 1-byte weights moved as
+// 2-byte units): plain row-major [E_l][rows][K].
 __global__ void moe_pack_w13_kernel(const __nv_bfloat16* w1, const __nv_bfloat16* w3, __nv_bfloat16* w13p,
-                                    int E_local, int e_off, int d, int f, int f_local, int f_off) {
+                                    int E_local, int e_off, int d, int f, int f_local, int f_off, int tiled) {
     const int64_t nvec_row = d / 8;
     const int64_t total = (int64_t)E_local * 2 * f_local * nvec_row;
     for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < total; v += (int64_t)gridDim.x * blockDim.x) {
@@ -693,18 +701,30 @@ __global__ void moe_pack_w13_kernel(const __nv_bfloat16* w1, const __nv_bfloat16
         const int64_t blk = pr / 256, i = pr % 256;
         const __nv_bfloat16* src = (i < 128 ? w1 : w3) +
                                    ((e_off + e) * (int64_t)f + f_off + blk * 128 + (i % 128)) * d;
-        reinterpret_cast<uint4*>(w13p)[v] = reinterpret_cast<const uint4*>(src)[cv];
+        int64_t dst = v;
+        if (tiled) {
+            const int64_t nkb = d / 64, tile = e * (2 * f_local / 256) + blk;
+            dst = ((tile * nkb + cv / 8) * 256 + i) * 8 + cv % 8;
+        }
+        reinterpret_cast<uint4*>(w13p)[dst] = reinterpret_cast<const uint4*>(src)[cv];
     }
 }
 __global__ void moe_pack_w2_kernel(const __nv_bfloat16* w2, __nv_bfloat16* w2p, int E_local, int e_off, int d,
-                                   int f, int f_local, int f_off) {
+                                   int f, int f_local, int f_off, int tiled, int pad_rows) {
     const int64_t nvec_row = f_local / 8;
-    const int64_t total = (int64_t)E_local * d * nvec_row;
+    const int rows = pad_rows ? (d + 255) / 256 * 256 : d;  // bf16: zero rows up to a multiple of 256
+    const int64_t total = (int64_t)E_local * rows * nvec_row;
     for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < total; v += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t row = v / nvec_row, cv = v % nvec_row;  // row = e*d + r
-        const int64_t e = row / d, r = row % d;
-        const __nv_bfloat16* src = w2 + ((e_off + e) * (int64_t)d + r) * f + f_off;
-        reinterpret_cast<uint4*>(w2p)[v] = reinterpret_cast<const uint4*>(src)[cv];
+        const int64_t row = v / nvec_row, cv = v % nvec_row;  // row = e*rows + r
+        const int64_t e = row / rows, r = row % rows;
+        uint4 val = make_uint4(0, 0, 0, 0);
+        if (r < d) val = reinterpret_cast<const uint4*>(w2 + ((e_off + e) * (int64_t)d + r) * f + f_off)[cv];
+        int64_t dst = v;
+        if (tiled) {
+            const int64_t nkb = f_local / 64, tile = e * (rows / 128) + r / 128;
+            dst = ((tile * nkb + cv / 8) * 128 + r % 128) * 8 + cv % 8;
+        }
+        reinterpret_cast<uint4*>(w2p)[dst] = val;
     }
 }
 

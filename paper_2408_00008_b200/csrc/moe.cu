@@ -139,6 +139,32 @@ bool encode_map(CUtensorMap* m, const void* base, int rank, uint64_t K, uint64_t
     return r == CUDA_SUCCESS;
 }
 
+// Tiled bf16 weights (moe_pack_weights): 4D {64, tile_rows, K/64, tiles_per_expert * E}, each
+// [tile_rows][64] chunk contiguous; box {64, box_rows, 1, box_tiles}; 128B swizzle.
+// MOE_WTILE=0 (A/B experiments): the same 4D view over plain row-major packing
+// (strides: row K*2, K block 128 B, tile tile_rows*K*2), same kernels.
+#ifndef MOE_WTILE
+#define MOE_WTILE 1
+#endif
+bool encode_wmap(CUtensorMap* m, const void* base, uint64_t K, uint64_t tile_rows, uint64_t ntiles_total,
+                 uint32_t box_rows, uint32_t box_tiles) {
+    PFN_encodeTiled_t fn = get_encode_fn();
+    if (!fn) return false;
+    cuuint64_t dims[4] = {64, tile_rows, K / 64, ntiles_total};
+    cuuint64_t strides[3] = {128, tile_rows * 128, (K / 64) * tile_rows * 128};
+    if (!MOE_WTILE) {
+        strides[0] = K * 2;
+        strides[1] = 128;
+        strides[2] = tile_rows * K * 2;
+    }
+    cuuint32_t box[4] = {64, box_rows, 1, box_tiles};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
 // rank-3 [batch, rows, K] fp8 (1 byte), box {64, box_rows, 1}, 64-byte swizzle (FP8 weights)
 bool encode_map_fp8(CUtensorMap* m, const void* base, uint64_t K, uint64_t rows, uint64_t batch, uint32_t box_rows,
                     uint32_t box_k = 64) {
@@ -197,6 +223,13 @@ struct moe_ctx {
     unsigned int* done = nullptr;
     __nv_bfloat16 *x_perm = nullptr, *h = nullptr;
     int32_t* src_row = nullptr;  // gather mode: [cap + 512] token of each permuted row
+    float* tail_ws = nullptr;    // decode w1/w3 GEMM tail split: [num_sms][2][128][128] fp32
+    int32_t* tail_cnt = nullptr; // [num_sms] arrival counters (zero between launches)
+    // max K slices per tail tile of the decode w1/w3 GEMM (env MOE_TAIL_PARTS; 0/1 = off).
+    // Off: r01 interleaved A/B with the tiled weight layout, decode step 0.4412 ms at 0
+    // vs 0.4475 ms at 4 or 8 (on the row-major layout 8 had won, 0.4534 vs 0.4587 ms).
+    int tail_parts = 0;
+    int w13_nt = 0, w2_nt = 0;   // tiles per expert of the tiled bf16 weight layout (256 / 128 rows)
     bool gather = false;         // MOE_FLAG_GATHER (or env MOE_GATHER=1): tile::gather4 token fetch
     bool gather_now = false;     // the current forward gathers (set per call)
     CUtensorMap tm_src{};        // gather map over the current call's tokens [T, d], box {64, 1}
@@ -487,11 +520,13 @@ moe_status ensure_weight_maps(moe_ctx* c, const moe_expert_weights* w) {
             !encode_map_fp8(&m.tm8_w2_64, w->w2, c->f_local, c->d, c->E_local, 128, 64))
             return fail(c, MOE_ERR_CUDA, "cuTensorMapEncodeTiled(fp8 weights) failed");
     } else {
-        if (!encode_map(&m.tm_w13, w->w13, 3, c->d, 2 * (uint64_t)c->f_local, c->E_local, 256) ||
-            !encode_map(&m.tm_w13_pair, w->w13, 3, c->d, 2 * (uint64_t)c->f_local, c->E_local, 128))
+        // tiled layout: W13 in 256-row tiles, W2 in 128-row tiles (rows padded to 256)
+        const uint64_t nt13 = (uint64_t)c->E_local * c->w13_nt, nt2 = (uint64_t)c->E_local * c->w2_nt;
+        if (!encode_wmap(&m.tm_w13, w->w13, c->d, 256, nt13, 256, 1) ||
+            !encode_wmap(&m.tm_w13_pair, w->w13, c->d, 256, nt13, 128, 1))
             return fail(c, MOE_ERR_CUDA, "cuTensorMapEncodeTiled(w13) failed");
-        if (!encode_map(&m.tm_w2_tiled, w->w2, 3, c->f_local, c->d, c->E_local, 256) ||
-            !encode_map(&m.tm_w2_swap, w->w2, 3, c->f_local, c->d, c->E_local, 128))
+        if (!encode_wmap(&m.tm_w2_tiled, w->w2, c->f_local, 128, nt2, 128, 2) ||
+            !encode_wmap(&m.tm_w2_swap, w->w2, c->f_local, 128, nt2, 128, 1))
             return fail(c, MOE_ERR_CUDA, "cuTensorMapEncodeTiled(w2) failed");
     }
     if (c->wmaps.size() >= moe_ctx::kWeightMapCache) {
@@ -533,6 +568,13 @@ moe_status launch_gemm_fp8t(moe_ctx* c, int slot, const GemmParams& p, const flo
 template <int NB>
 moe_status run_swap_g1(moe_ctx* c, int nbi, const moe_expert_weights* w, cudaStream_t st) {
     GemmParams p1{c->counts, c->offsets, c->E_local, c->d, c->f_local, 1, c->h, 0};
+    p1.w_tr = 256;
+    p1.w_nt = c->w13_nt;
+    if (c->tail_parts > 1) {  // K-sliced tail tiles (bf16 kernel; gemm_sm100.cuh tail_plan)
+        p1.tail_ws = c->tail_ws;
+        p1.tail_cnt = c->tail_cnt;
+        p1.tail_parts = c->tail_parts;
+    }
     if (c->gather_now) {
         p1.src_row = c->src_row;
         return launch_gemm<kG1Swap, NB>(c, kSlotGemm1, p1, c->tm_w13, c->tm_src, c->num_sms, st);
@@ -551,6 +593,8 @@ moe_status run_swap_g1(moe_ctx* c, int nbi, const moe_expert_weights* w, cudaStr
 template <int NB>
 moe_status run_swap_g2(moe_ctx* c, int nbi, const moe_expert_weights* w, int splits, cudaStream_t st) {
     GemmParams p2{c->counts, c->offsets, c->E_local, c->d, c->f_local, splits, c->y, c->split_stride};
+    p2.w_tr = 128;
+    p2.w_nt = c->w2_nt;
     if constexpr (NB <= 64)
         if (c->fp8 && !c->fp8_smem_a)
             return launch_gemm_fp8t<kG2Swap, NB>(c, kSlotGemm2, p2, w->w2_scale, c->tm_w2_swap, c->tm_h_swap[nbi],
@@ -688,6 +732,8 @@ moe_status run_gemms(moe_ctx* c, GemmPaths gp, int64_t rows_bound, int64_t rows_
         const int g1 = (int)std::min<int64_t>(ncl, mt_max * (c->f_local / 128));
         GemmParams p1{c->counts, c->offsets, c->E_local, c->d, c->f_local, 1, c->h, 0, r1, b1,
                       ptx::kEvictNormal, ptx::kEvictNormal, c->gather_now ? c->src_row : nullptr};
+        p1.w_tr = 256;
+        p1.w_nt = c->w13_nt;
         if ((s = launch_gemm_pair<kG1Pair>(c, kSlotGemm1, p1, c->gather_now ? c->tm_src : c->tm_x_tiled,
                                            c->tm_w13_pair, g1, st)))
             return s;
@@ -695,6 +741,8 @@ moe_status run_gemms(moe_ctx* c, GemmPaths gp, int64_t rows_bound, int64_t rows_
         const int64_t mt_max = rows_total / 128 + c->E_local;
         const int g1 = (int)std::min<int64_t>(c->num_sms, mt_max * (c->f_local / 128));
         GemmParams p1{c->counts, c->offsets, c->E_local, c->d, c->f_local, 1, c->h, 0};
+        p1.w_tr = 256;
+        p1.w_nt = c->w13_nt;
         p1.src_row = c->gather_now ? c->src_row : nullptr;
         if ((s = launch_gemm<kG1Tiled, 256>(c, kSlotGemm1, p1, c->gather_now ? c->tm_src : c->tm_x_tiled, c->tm_w13,
                                             g1, st)))
@@ -716,11 +764,15 @@ moe_status run_gemms(moe_ctx* c, GemmPaths gp, int64_t rows_bound, int64_t rows_
         const int g2 = (int)std::min<int64_t>(ncl, mt_max * ((c->d + 255) / 256));
         GemmParams p2{c->counts, c->offsets, c->E_local, c->d, c->f_local, 1, c->y, 0, r2, b2,
                       ptx::kEvictNormal, ptx::kEvictNormal};
+        p2.w_tr = 128;
+        p2.w_nt = c->w2_nt;
         if ((s = launch_gemm_pair<kG2Pair>(c, kSlotGemm2, p2, c->tm_h_tiled, c->tm_w2_swap, g2, st))) return s;
     } else {
         const int64_t mt_max = rows_total / 128 + c->E_local;
         const int g2 = (int)std::min<int64_t>(c->num_sms, mt_max * ((c->d + 255) / 256));
         GemmParams p2{c->counts, c->offsets, c->E_local, c->d, c->f_local, 1, c->y, 0};
+        p2.w_tr = 128;
+        p2.w_nt = c->w2_nt;
         if ((s = launch_gemm<kG2Tiled, 256>(c, kSlotGemm2, p2, c->tm_h_tiled, c->tm_w2_tiled, g2, st))) return s;
     }
     *splits_out = splits;
@@ -1017,7 +1069,7 @@ moe_status moe_packed_sizes(const moe_config* cfg, size_t* w13_bytes, size_t* w2
     if (!w13_bytes || !w2_bytes) return fail(nullptr, MOE_ERR_INVALID, "NULL output pointer");
     const ParShape ps = par_shape(cfg);
     *w13_bytes = (size_t)ps.E_local * 2 * ps.f_local * cfg->hidden * 2;
-    *w2_bytes = (size_t)ps.E_local * cfg->hidden * ps.f_local * 2;
+    *w2_bytes = (size_t)ps.E_local * ((cfg->hidden + 255) / 256 * 256) * ps.f_local * 2;  // rows padded (tiled layout)
     return MOE_OK;
 }
 
@@ -1066,6 +1118,8 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
     }
     c->rank = cfg->rank;
     c->max_T = cfg->max_tokens;
+    c->w13_nt = 2 * c->f_local / 256;
+    c->w2_nt = (c->d + 255) / 256 * 2;
     c->fp8 = (cfg->flags & MOE_FLAG_FP8_WEIGHTS) != 0;
     if (const char* v = getenv("MOE_FP8_SMEM_A")) c->fp8_smem_a = atoi(v) != 0;
     c->fp8_kb128 = c->fp8 && c->d % 128 == 0 && c->f_local % 128 == 0;
@@ -1075,6 +1129,7 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
     if (const char* pt = getenv("MOE_PAIR_TUNE")) c->pair_tune = atoi(pt);
     if (const char* v = getenv("MOE_GATHER")) c->gather = atoi(v) != 0;
     if (const char* v = getenv("MOE_G1_SWAP_ROWS")) c->swap_rows_per_expert = atoi(v);
+    if (const char* v = getenv("MOE_TAIL_PARTS")) c->tail_parts = atoi(v);
     if (const char* v = getenv("MOE_G2_SWAP_ROWS")) c->swap2_rows_per_expert = atoi(v);
     if (cfg->flags & MOE_FLAG_GATHER) c->gather = true;
     // router blocks of >= 2 rows; EP also routes the G*max_T*k receive slots
@@ -1128,6 +1183,8 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
     ALLOC(c->done, sizeof(unsigned int) * 4);
     ALLOC(c->x_perm, sizeof(__nv_bfloat16) * c->cap * c->d);
     ALLOC(c->src_row, sizeof(int32_t) * (c->cap + 512));
+    ALLOC(c->tail_ws, sizeof(float) * c->num_sms * 2 * 128 * 128);
+    ALLOC(c->tail_cnt, sizeof(int32_t) * c->num_sms);
     ALLOC(c->h, sizeof(__nv_bfloat16) * c->cap * c->f_local);
     ALLOC(c->y, sizeof(float) * c->y_elems);
     ALLOC(c->stage_in, 2 * sizeof(__nv_bfloat16) * c->max_T * c->d);
@@ -1186,6 +1243,7 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
     if ((e = cudaMemset(c->done, 0, sizeof(unsigned int) * 4)) != cudaSuccess) return fail_init("memset", e);
     if ((e = cudaMemset(c->x_perm, 0, sizeof(__nv_bfloat16) * c->cap * c->d)) != cudaSuccess) return fail_init("memset", e);
     if ((e = cudaMemset(c->src_row, 0, sizeof(int32_t) * (c->cap + 512))) != cudaSuccess) return fail_init("memset", e);
+    if ((e = cudaMemset(c->tail_cnt, 0, sizeof(int32_t) * c->num_sms)) != cudaSuccess) return fail_init("memset", e);
     if ((e = cudaMemset(c->h, 0, sizeof(__nv_bfloat16) * c->cap * c->f_local)) != cudaSuccess) return fail_init("memset", e);
 
     // workspace TMA descriptors
@@ -1250,7 +1308,8 @@ moe_status moe_destroy(moe_ctx* c) {
     void* bufs[] = {c->topk_idx, c->topk_w, c->pos, c->blockcount, c->blockoff, c->counts, c->offsets, c->done,
                     c->x_perm, c->h, c->y, c->stage_in, c->stage_out, c->tp_partial, c->tp_scatter, c->ep_send,
                     c->ep_recv, c->ep_ysend, c->ep_yrecv, c->ep_meta_send, c->ep_meta_recv,
-                    c->ep_ridx, c->ep_rpos, c->ep_rw, c->ep_rcounts, c->lb_scratch, c->d_peers};
+                    c->ep_ridx, c->ep_rpos, c->ep_rw, c->ep_rcounts, c->lb_scratch, c->d_peers, c->src_row,
+                    c->tail_ws, c->tail_cnt};
     for (void* p : c->p2p_opened) cudaIpcCloseMemHandle(p);
     if (c->sym) {
         cudaDeviceSynchronize();  // peers' stores into this region have drained (same-process group)
@@ -1281,11 +1340,11 @@ moe_status moe_pack_weights(moe_ctx* c, const void* w1, const void* w3, const vo
     const int e_off = c->e_lo;  // 0 unless experts are sharded (EP, hybrid)
     if ((s = launch(c, kSlotPack, moe_pack_w13_kernel, dim3(4 * c->num_sms), dim3(256), 0, st,
                     static_cast<const __nv_bfloat16*>(w1), static_cast<const __nv_bfloat16*>(w3),
-                    static_cast<__nv_bfloat16*>(w13_out), c->E_local, e_off, c->d, c->f, c->f_local, c->f_off)))
+                    static_cast<__nv_bfloat16*>(w13_out), c->E_local, e_off, c->d, c->f, c->f_local, c->f_off, MOE_WTILE)))
         return s;
     if ((s = launch(c, kSlotPack, moe_pack_w2_kernel, dim3(4 * c->num_sms), dim3(256), 0, st,
                     static_cast<const __nv_bfloat16*>(w2), static_cast<__nv_bfloat16*>(w2_out), c->E_local, e_off,
-                    c->d, c->f, c->f_local, c->f_off)))
+                    c->d, c->f, c->f_local, c->f_off, MOE_WTILE, 1)))
         return s;
     // descriptors keyed by these pointers must be re-encoded if memory was reused
     (void)w13_out;  // descriptors hold addresses only; repacking in place keeps them valid
@@ -1308,11 +1367,11 @@ moe_status moe_pack_weights_fp8(moe_ctx* c, const void* q1, const void* q3, cons
     // one byte per weight: pack pairs of fp8 as 2-byte units with the bf16 packers
     if ((s = launch(c, kSlotPack, moe_pack_w13_kernel, dim3(4 * c->num_sms), dim3(256), 0, st,
                     static_cast<const __nv_bfloat16*>(q1), static_cast<const __nv_bfloat16*>(q3),
-                    static_cast<__nv_bfloat16*>(w13_out), c->E_local, e_off, c->d / 2, c->f, c->f_local, c->f_off)))
+                    static_cast<__nv_bfloat16*>(w13_out), c->E_local, e_off, c->d / 2, c->f, c->f_local, c->f_off, 0)))
         return s;
     if ((s = launch(c, kSlotPack, moe_pack_w2_kernel, dim3(4 * c->num_sms), dim3(256), 0, st,
                     static_cast<const __nv_bfloat16*>(q2), static_cast<__nv_bfloat16*>(w2_out), c->E_local, e_off,
-                    c->d, c->f / 2, c->f_local / 2, c->f_off / 2)))
+                    c->d, c->f / 2, c->f_local / 2, c->f_off / 2, 0, 0)))
         return s;
     if ((s = launch(c, kSlotPack, moe_pack_scales_kernel, dim3(c->num_sms), dim3(256), 0, st, s1, s3, s2,
                     w13_scale_out, w2_scale_out, c->E_local, e_off, c->d, c->f, c->f_local, c->f_off)))

@@ -43,6 +43,8 @@ def test_packed_sizes_and_validation():
     cfg = moe.make_config(4096, 14336, 8, 2, 64)
     a, b = moe.moe_packed_sizes(cfg)
     assert a == 8 * 2 * 14336 * 4096 * 2 and b == 8 * 4096 * 14336 * 2
+    odd = moe.make_config(320, 1024, 4, 2, 64)  # W2 rows padded to a multiple of 256 (tiled layout)
+    assert moe.moe_packed_sizes(odd) == (4 * 2 * 1024 * 320 * 2, 4 * 512 * 1024 * 2)
     tp = moe.make_config(4096, 14336, 8, 2, 64, par=moe.MOE_PAR_TP, world_size=8, rank=3, nccl_comm=1)
     a, b = moe.moe_packed_sizes(tp)
     assert a == 8 * 2 * 1792 * 4096 * 2 and b == 8 * 4096 * 1792 * 2

@@ -127,6 +127,30 @@ def test_mixed_gemm_paths(moe, flags):
     blk.close()
 
 
+@pytest.mark.parametrize("parts", ["8", "3", "0"])
+@pytest.mark.parametrize("T,d,f,E", [(64, 1024, 2560, 8), (40, 512, 5120, 4), (300, 256, 2560, 8)])
+def test_tail_split(moe, T, d, f, E, parts):
+    """Decode w1/w3 GEMM with K-sliced tail tiles (gemm_sm100.cuh tail_plan; off by
+    default, env MOE_TAIL_PARTS): 160 tiles on 148 SMs leave 12 tail tiles, each run as
+    up to MOE_TAIL_PARTS slices whose fp32 partials are summed in slice order by the
+    completing CTA (0 = whole tiles).
+    Oracle parity, and bitwise determinism across calls (graph-free, counters reset)."""
+    shape = synth.MoEShape(T=T, d=d, f=f, E=E, k=2)
+    inp = _inputs(shape, 23)
+    os.environ["MOE_TAIL_PARTS"] = parts
+    try:
+        blk = _block(moe, inp, 2, T, 0x2)
+    finally:
+        del os.environ["MOE_TAIL_PARTS"]
+    run = GpuRun(blk, inp["x"])
+    check_forward(run, to_host_inputs(inp), 2)
+    for _ in range(3):
+        again = blk.forward(inp["x"])
+        torch.cuda.synchronize()
+        assert torch.equal(again.view(torch.int16), run.out.view(torch.int16))
+    blk.close()
+
+
 def _forced_gates(host, idx):
     l = oracle.router(host["x"], host["wg"], 1)["logits"]
     li = np.take_along_axis(l, idx.astype(np.int64), 1)
