@@ -73,6 +73,16 @@ constexpr int kGemmThreads = 192;
 constexpr int kBK = 64;                 // K per stage = one 128-byte swizzle atom of bf16
 constexpr int kSmemBudget = 232448;     // 227 KB opt-in dynamic shared memory per CTA
 
+// Stage caps of the decode kernels (A/B knobs). A streaming-read model peaks at 3-4
+// stages of 32 KB (scripts/exp/read_bw.cu: 7.27 TB/s at 3, 6.78 at 7), but the GEMMs
+// want the full ring: r01 decode step 0.4364 ms at (G1 5 = smem limit, G2 8) vs
+// 0.4393 (5,5), 0.4399 (4,6), 0.547 (4,4), 0.613 ms (3,3).
+#ifndef MOE_SWAP_STAGES_G1
+#define MOE_SWAP_STAGES_G1 8
+#endif
+#ifndef MOE_SWAP_STAGES_G2
+#define MOE_SWAP_STAGES_G2 8
+#endif
 template <int KIND, int NB>
 struct GemmCfg {
     static constexpr bool kSwap = (KIND == kG1Swap || KIND == kG2Swap);
@@ -84,7 +94,8 @@ struct GemmCfg {
     static constexpr int kBBytes = kBRows * 128;
     static constexpr int kStageBytes = kABytes + kBBytes;
     static constexpr int kStagesRaw = (kSmemBudget - 2048) / kStageBytes;
-    static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
+    static constexpr int kStagesCap = KIND == kG1Swap ? MOE_SWAP_STAGES_G1 : KIND == kG2Swap ? MOE_SWAP_STAGES_G2 : 8;
+    static constexpr int kStages = kStagesRaw > kStagesCap ? kStagesCap : kStagesRaw;
     static constexpr int kSmemBytes = kStages * kStageBytes + 2048;  // + barriers + 1 KB align slack
     // TMEM: 512 columns = kAccStages x kAccCols. The w1|w3 swap tile with NB = 256 token
     // columns needs a 256-column accumulator for each of a and b -> one stage only.

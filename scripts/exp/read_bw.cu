@@ -18,13 +18,13 @@ __device__ __forceinline__ void expect_tx(uint64_t* b, uint32_t n) { asm volatil
 __device__ __forceinline__ void wait(uint64_t* b, uint32_t ph) {
     asm volatile("{ .reg .pred p; W: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1; @!p bra W; }" ::"r"(su(b)), "r"(ph));
 }
-constexpr int S = 6, STAGE = 32768;
+constexpr int SMAX = 7, STAGE = 32768;
 __global__ void __launch_bounds__(128, 1) k_tma(const __grid_constant__ CUtensorMap m, int mode, const uint8_t* base,
                                                 int64_t nchunks, int nkb, float* sink, int stage_bytes = STAGE,
-                                                int box_rows = 256, int nkb_row = 64) {
+                                                int box_rows = 256, int nkb_row = 64, int S = 6, int delay = 0) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-    __shared__ uint64_t full[S];
+    __shared__ uint64_t full[SMAX];
     if (threadIdx.x == 0) {
         for (int i = 0; i < S; ++i) mbar_init(&full[i], 1);
         asm volatile("fence.mbarrier_init.release.cluster;");
@@ -66,6 +66,10 @@ __global__ void __launch_bounds__(128, 1) k_tma(const __grid_constant__ CUtensor
         const int st = done % S;
         wait(&full[st], (done / S) & 1);
         acc += smem[st * STAGE + 7];
+        if (delay) {  // emulate the MMA hold time of a stage before it is released
+            const long long t0 = clock64();
+            while (clock64() - t0 < delay) {}
+        }
         ++done;
         if (j < my_n) { issue(chunk_of(j)); ++j; }
     }
@@ -98,7 +102,7 @@ int main() {
     cuuint32_t box[2] = {64, 256}, es[2] = {1, 1};
     ((enc_t)fn)(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, d, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                 CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    cudaFuncSetAttribute(k_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, S * STAGE + 1024);
+    cudaFuncSetAttribute(k_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, SMAX * STAGE + 1024);
     const int nkb = (int)(K / 64);
     const int64_t nchunks = bytes / STAGE;
     cudaEvent_t a, b;
@@ -118,10 +122,10 @@ int main() {
             float best = 1e9;
             for (int rep = 0; rep < 8; ++rep) {
                 cudaEventRecord(a);
-                if (mode < 2) k_tma<<<148, 128, S * STAGE + 1024>>>(m, mode, d, nchunks, nkb, sink);
-                else if (mode == 3) k_tma<<<148, 128, S * STAGE + 1024>>>(m, mode, d, 896LL * nkb, nkb, sink);
-                else if (mode == 4) k_tma<<<148, 128, S * STAGE + 1024>>>(m2, 4, d, rows2 / 128 * 224, 56, sink, 16384, 128, 224);
-                else if (mode == 5) k_tma<<<148, 128, S * STAGE + 1024>>>(m, 5, d, bytes / 16384, nkb, sink, 16384);
+                if (mode < 2) k_tma<<<148, 128, SMAX * STAGE + 1024>>>(m, mode, d, nchunks, nkb, sink);
+                else if (mode == 3) k_tma<<<148, 128, SMAX * STAGE + 1024>>>(m, mode, d, 896LL * nkb, nkb, sink);
+                else if (mode == 4) k_tma<<<148, 128, SMAX * STAGE + 1024>>>(m2, 4, d, rows2 / 128 * 224, 56, sink, 16384, 128, 224);
+                else if (mode == 5) k_tma<<<148, 128, SMAX * STAGE + 1024>>>(m, 5, d, bytes / 16384, nkb, sink, 16384);
                 else k_ldg<<<148 * 8 * grid_mul, 256>>>((const uint4*)d, bytes / 16, sink);
                 cudaEventRecord(b);
                 cudaEventSynchronize(b);
@@ -132,6 +136,21 @@ int main() {
             const double by = mode == 3 ? 896.0 * nkb * STAGE : mode == 4 ? (double)rows2 * K2 * 2 : (double)bytes;
             printf("%-36s grid x%d: %.3f ms  %.1f GB/s  (%s)\n", names[mode], grid_mul, best, by / best / 1e6,
                    cudaGetErrorString(cudaGetLastError()));
+        }
+    // stage-depth / hold-time sweep on the contiguous 32 KB chunk stream (mode 1)
+    for (int S = 2; S <= SMAX; ++S)
+        for (int delay : {0, 500, 1000}) {
+            float best = 1e9;
+            for (int rep = 0; rep < 6; ++rep) {
+                cudaEventRecord(a);
+                k_tma<<<148, 128, SMAX * STAGE + 1024>>>(m, 1, d, nchunks, nkb, sink, STAGE, 256, 64, S, delay);
+                cudaEventRecord(b);
+                cudaEventSynchronize(b);
+                float ms;
+                cudaEventElapsedTime(&ms, a, b);
+                if (rep > 0 && ms < best) best = ms;
+            }
+            printf("mode1 S=%d hold=%4d cycles: %.1f GB/s\n", S, delay, bytes / best / 1e6);
         }
     return 0;
 }
