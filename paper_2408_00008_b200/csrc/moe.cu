@@ -215,7 +215,11 @@ struct moe_ctx {
                                   // MOE_FP8_KB=64 selects 64 (r01: 0.3304 ms vs 0.2975 ms per step)      // env MOE_FP8_SMEM_A=1: widen fp8 weights in smem (not TMEM) at NB <= 64
     moe_expert_weights cur_w{};   // weights of the current forward
     int pair_tune = 0;        // experiment override of the prefill tile orders (env MOE_PAIR_TUNE)
-    int g1_raster = 2, g1_band = 16, g2_raster = 1, g2_band = 1;  // prefill tile orders (pair_decode; ncu DRAM sweep r01)
+    // prefill tile orders (pair_decode). G1: bands of 16 token tiles (ncu DRAM sweep r01).
+    // G2: bands of 8 weight tiles, weight tiles fastest (tiled weights, interleaved A/B on
+    // two boxes: 18.57/18.52 and 18.30/18.11 ms per step vs 19.14/19.04 and 18.36/18.48 ms
+    // for weight-tiles-fastest; DRAM 17.2 vs 17.6 GB per launch, scripts/sweep_order.sh)
+    int g1_raster = 2, g1_band = 16, g2_raster = 3, g2_band = 8;
     // workspace (device)
     int32_t *topk_idx = nullptr, *pos = nullptr, *blockcount = nullptr, *blockoff = nullptr;
     int32_t *counts = nullptr, *offsets = nullptr;
