@@ -243,6 +243,7 @@ struct moe_ctx {
     cudaStream_t copy_stream = nullptr;                        // moe_forward_host uploads
     cudaEvent_t slot_free[2]{}, slot_loaded[2]{};
     int host_slot = 0;
+    bool host_zero_copy = true;  // moe_forward_host: combine writes pinned output directly (env MOE_HOST_ZERO_COPY=0: copy)
     float* tp_partial = nullptr;                               // TP: fp32 partial [max_T, d]
     float* tp_scatter = nullptr;                               // TP: reduce-scatter result
     // EP staging
@@ -1134,6 +1135,7 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
     if (const char* v = getenv("MOE_GATHER")) c->gather = atoi(v) != 0;
     if (const char* v = getenv("MOE_G1_SWAP_ROWS")) c->swap_rows_per_expert = atoi(v);
     if (const char* v = getenv("MOE_TAIL_PARTS")) c->tail_parts = atoi(v);
+    if (const char* v = getenv("MOE_HOST_ZERO_COPY")) c->host_zero_copy = atoi(v) != 0;
     if (const char* v = getenv("MOE_G2_SWAP_ROWS")) c->swap2_rows_per_expert = atoi(v);
     if (cfg->flags & MOE_FLAG_GATHER) c->gather = true;
     // router blocks of >= 2 rows; EP also routes the G*max_T*k receive slots
@@ -1424,10 +1426,21 @@ moe_status moe_forward_host(moe_ctx* c, const void* tokens_host, int32_t T, cons
         CUDA_TRY(c, cudaEventRecord(c->slot_loaded[slot], c->copy_stream));
         CUDA_TRY(c, cudaStreamWaitEvent(st, c->slot_loaded[slot], 0));
     }
-    if ((s = moe_forward(c, in, T, router_w, w, c->stage_out, nullptr, stream))) return s;
+    // Pinned (page-locked, device-mapped) output: the combine kernel stores the bf16 rows
+    // straight into host memory over the host link -- no staging buffer, no separate
+    // device->host copy on the stream. Pageable output: staging buffer + copy.
+    void* out_dev = nullptr;
+    if (T > 0 && c->host_zero_copy) {
+        cudaPointerAttributes pa{};
+        if (cudaPointerGetAttributes(&pa, out_host) == cudaSuccess && pa.type == cudaMemoryTypeHost &&
+            pa.devicePointer && aligned16(pa.devicePointer))
+            out_dev = pa.devicePointer;
+        cudaGetLastError();  // pageable memory: not an error
+    }
+    if ((s = moe_forward(c, in, T, router_w, w, out_dev ? out_dev : c->stage_out, nullptr, stream))) return s;
     if (T > 0) {
         CUDA_TRY(c, cudaEventRecord(c->slot_free[slot], st));
-        CUDA_TRY(c, cudaMemcpyAsync(out_host, c->stage_out, bytes, cudaMemcpyDeviceToHost, st));
+        if (!out_dev) CUDA_TRY(c, cudaMemcpyAsync(out_host, c->stage_out, bytes, cudaMemcpyDeviceToHost, st));
     }
     return MOE_OK;
 }

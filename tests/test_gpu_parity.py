@@ -221,9 +221,17 @@ def test_host_entry_point(moe):
     blk = _block(moe, inp, 2, 16)
     ref = blk.forward(inp["x"]).cpu()
     xh = inp["x"].cpu().pin_memory()
-    oh = torch.empty_like(xh).pin_memory()
+    oh = torch.empty_like(xh).pin_memory()      # pinned: the combine kernel writes it directly
     moe.moe_forward_host(blk.ctx, xh, 16, blk.router_w, blk.w13, blk.w2, oh)
     torch.cuda.synchronize()
+    assert torch.equal(oh.view(torch.int16), ref.view(torch.int16))
+    op = torch.zeros_like(inp["x"].cpu())       # pageable: staging buffer + copy
+    xp = inp["x"].cpu()
+    for _ in range(3):                          # back-to-back calls rotate the two input slots
+        moe.moe_forward_host(blk.ctx, xp, 16, blk.router_w, blk.w13, blk.w2, op)
+        moe.moe_forward_host(blk.ctx, xh, 16, blk.router_w, blk.w13, blk.w2, oh)
+    torch.cuda.synchronize()
+    assert torch.equal(op.view(torch.int16), ref.view(torch.int16))
     assert torch.equal(oh.view(torch.int16), ref.view(torch.int16))
     blk.close()
 
