@@ -292,6 +292,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     int total = 0;
     for (int e = 0; e < p.E; ++e) total += tiles_of<KIND, NB>(s_counts[e], p);
     const TailPlan tp = KIND == kG1Swap ? tail_plan(total, gridDim.x, p.d / kBK, p) : TailPlan{total, 1, total};
+    // swap kinds: L2 policy of the streamed weight tiles (hint_a; 0 = evict-first, the
+    // decode default where each weight tile meets all of its expert's tokens at once)
+    const uint64_t w_hint = p.hint_a ? p.hint_a : ptx::kEvictFirst;
 
     if (warp == 0) {
         // ---------------------------------------------------------------- TMA producer
@@ -315,7 +318,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                     {
                         const WCoord w = wcoord(p, (t0.kb0 + kb) * kBK, t0.a_row, t0.e);
                         ptx::tma_load_4d(&tmA, &full[kb], smem_a + kb * C::kABytes, 0, w.c1, w.c2, w.c3,
-                                         ptx::kEvictFirst);
+                                         w_hint);
                     }
                     }
             }
@@ -346,7 +349,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                         // A = weights (3D map [K, rows, E]) streamed once: evict-first.
                         if (!armed) {
                             const WCoord w = wcoord(p, kc, ti.a_row, ti.e);
-                            ptx::tma_load_4d(&tmA, &full[stage], sa, 0, w.c1, w.c2, w.c3, ptx::kEvictFirst);
+                            ptx::tma_load_4d(&tmA, &full[stage], sa, 0, w.c1, w.c2, w.c3, w_hint);
                         }
                         // B = permuted tokens / activations (2D map [K, Cap]): keep in L2.
                         if (!gather) ptx::tma_load_2d(&tmB, &full[stage], sb, kc, ti.b_row, ptx::kEvictLast);

@@ -243,6 +243,8 @@ struct moe_ctx {
     cudaStream_t copy_stream = nullptr;                        // moe_forward_host uploads
     cudaEvent_t slot_free[2]{}, slot_loaded[2]{};
     int host_slot = 0;
+    uint64_t swap_w_hint = 0;    // L2 policy of the decode GEMMs' weight stream (set per forward)
+    int swap_hint_mode = 0;      // env MOE_SWAP_HINT: 0 auto, 1 evict-first, 2 normal, 3 evict-last
     bool host_zero_copy = true;  // moe_forward_host: combine writes pinned output directly (env MOE_HOST_ZERO_COPY=0: copy)
     float* tp_partial = nullptr;                               // TP: fp32 partial [max_T, d]
     float* tp_scatter = nullptr;                               // TP: reduce-scatter result
@@ -573,6 +575,7 @@ moe_status launch_gemm_fp8t(moe_ctx* c, int slot, const GemmParams& p, const flo
 template <int NB>
 moe_status run_swap_g1(moe_ctx* c, int nbi, const moe_expert_weights* w, cudaStream_t st) {
     GemmParams p1{c->counts, c->offsets, c->E_local, c->d, c->f_local, 1, c->h, 0};
+    p1.hint_a = c->swap_w_hint;
     p1.w_tr = 256;
     p1.w_nt = c->w13_nt;
     if (c->tail_parts > 1) {  // K-sliced tail tiles (bf16 kernel; gemm_sm100.cuh tail_plan)
@@ -598,6 +601,7 @@ moe_status run_swap_g1(moe_ctx* c, int nbi, const moe_expert_weights* w, cudaStr
 template <int NB>
 moe_status run_swap_g2(moe_ctx* c, int nbi, const moe_expert_weights* w, int splits, cudaStream_t st) {
     GemmParams p2{c->counts, c->offsets, c->E_local, c->d, c->f_local, splits, c->y, c->split_stride};
+    p2.hint_a = c->swap_w_hint;
     p2.w_tr = 128;
     p2.w_nt = c->w2_nt;
     if constexpr (NB <= 64)
@@ -716,6 +720,13 @@ moe_status run_gemms(moe_ctx* c, GemmPaths gp, int64_t rows_bound, int64_t rows_
     // goes to 256; FP8 kernels stop at 128.
     const int nbw = (int)std::max<int64_t>(32, std::min<int64_t>(256, next_pow2((int)std::min<int64_t>(rows_bound, 1 << 20))));
     const int nb1 = std::min(nbw, 128), nb2 = c->fp8 ? nb1 : nbw;
+    // weight tiles re-read by a second token tile of the same expert (rows > NB) should
+    // survive in L2 between the passes: evict-normal then, evict-first otherwise (r01
+    // stack T=575, interleaved: 17.97 / 17.84 ms vs 18.38 / 18.61 ms all-evict-first)
+    c->swap_w_hint = c->swap_hint_mode == 1 ? ptx::kEvictFirst
+                   : c->swap_hint_mode == 2 ? ptx::kEvictNormal
+                   : c->swap_hint_mode == 3 ? ptx::kEvictLast
+                   : (rows_bound > nb1 ? ptx::kEvictNormal : ptx::kEvictFirst);
     const bool pair = !(c->cfg.flags & MOE_FLAG_NO_PAIR);
     // CTA-pair (cta_group::2) 256x256 tiles, one cluster of 2 CTAs per TPC; tile order
     // per GEMM (see pair_decode); env MOE_PAIR_TUNE overrides for experiments:
@@ -1136,6 +1147,7 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
     if (const char* v = getenv("MOE_G1_SWAP_ROWS")) c->swap_rows_per_expert = atoi(v);
     if (const char* v = getenv("MOE_TAIL_PARTS")) c->tail_parts = atoi(v);
     if (const char* v = getenv("MOE_HOST_ZERO_COPY")) c->host_zero_copy = atoi(v) != 0;
+    if (const char* v = getenv("MOE_SWAP_HINT")) c->swap_hint_mode = atoi(v);
     if (const char* v = getenv("MOE_G2_SWAP_ROWS")) c->swap2_rows_per_expert = atoi(v);
     if (cfg->flags & MOE_FLAG_GATHER) c->gather = true;
     // router blocks of >= 2 rows; EP also routes the G*max_T*k receive slots
