@@ -639,6 +639,12 @@ __device__ __forceinline__ void pair_decode(int t, const GemmParams& p, const in
     ti.n_valid = 0;
 }
 
+// Weight prefetch before the PDL wait in the CTA-pair kernels: measured WORSE (r01
+// prefill, interleaved: 19.6 / 20.1 / 19.9 ms with vs 18.8 / 19.0 / 18.9 ms without;
+// the 32-layer stack with the w2 GEMM on pairs stayed slower than swap-AB), so off.
+#ifndef MOE_PAIR_PDL_PREFETCH
+#define MOE_PAIR_PDL_PREFETCH 0
+#endif
 template <int KIND>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     moe_gemm_pair_kernel(const GemmParams p, const __grid_constant__ CUtensorMap tmA,
@@ -679,7 +685,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         ptx::tmem_alloc_pair(tmem_base_slot, 512);
         ptx::tmem_relinquish_pair();
     }
-    ptx::pdl_wait();
+    // With MOE_PAIR_PDL_PREFETCH the producer issues the first weight (B) stages of its
+    // first tile before waiting for the previous kernel (weights do not depend on it);
+    // only its token / activation (A) loads wait. The other warps consume smem / TMEM
+    // gated by the pipeline barriers and write h / y, which no still-running kernel
+    // reads (the PDL chain orders the previous layer's combine before this grid).
+    if (!MOE_PAIR_PDL_PREFETCH) ptx::pdl_wait();
     if (threadIdx.x < 32) {
         for (int e = threadIdx.x; e < p.E; e += 32) {
             s_counts[e] = p.counts[e];
@@ -702,6 +713,23 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         const bool gather = KIND == kG1Pair && p.src_row != nullptr;
         int stage = 0;
         uint32_t phase = 0;
+        int pre = 0;  // k-blocks of the first tile whose weight loads precede the wait
+        if (MOE_PAIR_PDL_PREFETCH) {
+            if (cid < total) {
+                TileInfo t0;
+                pair_decode<KIND>(cid, p, s_counts, s_offsets, t0);
+                pre = min(S, t0.nkb);
+                if (lane == 0)
+                    for (int kb = 0; kb < pre; ++kb) {  // fresh stages: no empty-wait needed
+                        const uint32_t fb = ptx::map_cluster(&full[kb], 0);
+                        if (leader) ptx::mbar_arrive_expect_tx(&full[kb], 2 * kPairStageBytes);
+                        const WCoord w = wcoord(p, kb * kBK, t0.n_idx * 256 + (int)crank * 128, t0.e);
+                        ptx::tma_load_4d_pair(&tmB, fb, smem_b + kb * 16384, 0, w.c1, w.c2, w.c3, p.hint_b);
+                    }
+            }
+            ptx::pdl_wait();
+        }
+        bool first = true;
         for (int t = cid; t < total; t += ncl) {
             TileInfo ti;
             pair_decode<KIND>(t, p, s_counts, s_offsets, ti);
@@ -717,12 +745,17 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             for (int kb = 0; kb < ti.nkb; ++kb) {
                 const uint32_t fb = ptx::map_cluster(&full[stage], 0);
                 const int kc = kb * kBK;
+                const bool armed = first && kb < pre;  // weights already in flight on this stage
                 if (lane == 0) {
-                    ptx::mbar_wait(&empty[stage], phase ^ 1);
-                    if (leader) ptx::mbar_arrive_expect_tx(&full[stage], 2 * kPairStageBytes);
+                    if (!armed) {
+                        ptx::mbar_wait(&empty[stage], phase ^ 1);
+                        if (leader) ptx::mbar_arrive_expect_tx(&full[stage], 2 * kPairStageBytes);
+                    }
                     if (!gather) ptx::tma_load_2d_pair(&tmA, fb, smem_a + stage * 16384, kc, a_row, p.hint_a);
-                    const WCoord w = wcoord(p, kc, b_row, ti.e);
-                    ptx::tma_load_4d_pair(&tmB, fb, smem_b + stage * 16384, 0, w.c1, w.c2, w.c3, p.hint_b);
+                    if (!armed) {
+                        const WCoord w = wcoord(p, kc, b_row, ti.e);
+                        ptx::tma_load_4d_pair(&tmB, fb, smem_b + stage * 16384, 0, w.c1, w.c2, w.c3, p.hint_b);
+                    }
                 }
                 if (gather) {
                     __syncwarp();
@@ -730,6 +763,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 }
                 if (++stage == S) { stage = 0; phase ^= 1; }
             }
+            first = false;
         }
     } else if (warp == 1) {
         // ---------------------------------------------------------------- MMA issuer (leader CTA)
