@@ -276,6 +276,42 @@ def test_partition_sums_to_full(mode, G):
         assert np.all(nz <= 2)
 
 
+@pytest.mark.parametrize("G,dead", [(2, [2, 3]), (2, [0, 1]), (4, [1, 3])])
+def test_partition_ep_ownership(G, dead):
+    """EP rank r owns experts [r*E/G, (r+1)*E/G): with x > 0 and the router rows of the
+    `dead` experts negated (their logits < 0 < the others', so top-2 never picks them),
+    the ranks owning only dead experts hold exactly zero and the rest sum to y."""
+    inp = _tiny(11, "f32")
+    x = np.abs(inp["x"])
+    wg = np.abs(inp["wg"])
+    wg[dead] *= -1
+    args = (x, wg, inp["w1"], inp["w3"], inp["w2"])
+    P = oracle.partition(*args, k=2, G=G, mode="ep")
+    E = wg.shape[0]
+    for r in range(G):
+        owned = set(range(r * E // G, (r + 1) * E // G))
+        if owned <= set(dead):
+            assert np.all(P[r] == 0), r
+        else:
+            assert np.abs(P[r]).max() > 0, r
+    np.testing.assert_allclose(P.sum(0), oracle.moe_forward(*args, k=2), rtol=1e-12, atol=1e-14)
+
+
+@pytest.mark.parametrize("G,dead_rank", [(2, 1), (2, 0), (4, 2)])
+def test_partition_tp_ownership(G, dead_rank):
+    """TP rank r owns ffn columns [r*f/G, (r+1)*f/G): with those W2 columns zeroed for
+    dead_rank, its partial is exactly zero and the others still sum to y."""
+    inp = _tiny(12, "f32")
+    f = inp["w1"].shape[1]
+    w2 = inp["w2"].copy()
+    w2[:, :, dead_rank * f // G:(dead_rank + 1) * f // G] = 0
+    args = (inp["x"], inp["wg"], inp["w1"], inp["w3"], w2)
+    P = oracle.partition(*args, k=2, G=G, mode="tp")
+    for r in range(G):
+        assert (np.all(P[r] == 0)) == (r == dead_rank), r
+    np.testing.assert_allclose(P.sum(0), oracle.moe_forward(*args, k=2), rtol=1e-12, atol=1e-14)
+
+
 # ---------------------------------------------------------------- permutation (step 7)
 def _brute_perm(idx, E, align):
     T, k = idx.shape

@@ -30,6 +30,12 @@ MUTANTS = [
     ("residual dropped", "acc[r] += dec(x, (size_t)t * d + r);", "acc[r] += 0.0;"),
     ("segment not padded", "offsets[e + 1] = offsets[e] + ((int64_t)(counts[e] + align - 1) / align) * align;",
      "offsets[e + 1] = offsets[e] + counts[e];"),
+    ("logits sorted ascending", "if (l[a] != l[b]) return l[a] > l[b];", "if (l[a] != l[b]) return l[a] < l[b];"),
+    ("gates paired with the wrong expert", "acc[r] += wt[j] * o[r];", "acc[r] += wt[k - 1 - j] * o[r];"),
+    ("w3 read as w1", "b += dec(w3, ((size_t)e * f + i) * d + c) * xc;",
+     "b += dec(w1, ((size_t)e * f + i) * d + c) * xc;"),
+    ("EP experts owned round-robin", "if (e / (E / G) != r) continue;", "if (e % G != r) continue;"),
+    ("TP ffn slices reversed", "r * (f / G), (r + 1) * (f / G)", "(G - 1 - r) * (f / G), (G - r) * (f / G)"),
 ]
 
 
