@@ -583,6 +583,9 @@ def main():
         line["cpu_baseline"] = cb
     if rank == 0:
         print(json.dumps(line), flush=True)
+    if args.p2p and world > 1:  # peers may still read / write my region until everyone is done
+        torch.cuda.synchronize()
+        barrier()
     blk.close()
     for cm in (comm, tp_comm):
         if cm is not None:

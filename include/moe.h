@@ -271,7 +271,10 @@ MOE_API moe_status moe_loopback_comm_destroy(void* group_or_rank);
  * not supported (MOE_ERR_UNSUPPORTED). moe_forward before moe_p2p_connect fails
  * with MOE_ERR_STATE. Every rank must call moe_forward the same number of times
  * (TP: with the same T), as with the NCCL transport. Forwards cannot be
- * captured into a CUDA graph (MOE_ERR_UNSUPPORTED): the counter targets advance. */
+ * captured into a CUDA graph (MOE_ERR_UNSUPPORTED): the counter targets advance.
+ * Teardown: every rank's last forward must have completed on every rank (e.g.
+ * stream sync + process-group barrier) before any rank calls moe_destroy, since
+ * peers load from / store into this rank's region until then.                */
 #define MOE_FLAG_P2P 0x100u
 #define MOE_P2P_HANDLE_BYTES 128
 MOE_API moe_status moe_p2p_handle(moe_ctx* ctx, void* handle_out);
