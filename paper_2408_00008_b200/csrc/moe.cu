@@ -206,7 +206,8 @@ struct moe_ctx {
     // 32-layer stack (T=575) the swap kernel's weight prefetch under PDL wins:
     // 17.85 ms vs 18.5-18.7 ms per step (scripts/ab_env.sh, interleaved) -> 256.
     int swap2_rows_per_expert = 256;
-    int max_splits = 4;
+    int max_splits = 4;       // split-K partial buffers are sized for this many splits
+    int max_splits_env = 0;   // env MOE_MAX_SPLITS: force the split count (A/B; <= 8, clamped by the buffers)
     int64_t split_stride = 0; // elements between split-K partial buffers of this forward
     bool fp8 = false;             // MOE_FLAG_FP8_WEIGHTS
     bool fp8_smem_a = false;
@@ -766,7 +767,13 @@ moe_status run_gemms(moe_ctx* c, GemmPaths gp, int64_t rows_bound, int64_t rows_
     }
     if (gp.swap2) {
         const int64_t rows_needed = round_up(rows_total + (int64_t)c->E_local * (kSegAlign - 1), kSegAlign);
-        splits = c->cfg.split_k ? c->cfg.split_k : c->max_splits;
+        // split-K of the decode w2 GEMM (fixed-order fp32 partials summed by the combine).
+        // r01 interleaved A/B (tiled weights): 64-token decode 0.4298 ms at 1 split vs
+        // 0.434 at 2 and 0.442 at 4 (each tile's K range is one contiguous region and
+        // >= 108 SMs stay busy in the last wave); the T=575 stack 17.4 ms at 2 vs 18.2 at
+        // 1 and 17.4 at 4; FP8 0.2917 ms at 4 vs 0.2970 at 2.
+        const int auto_splits = c->fp8 ? 4 : nb2 <= 64 ? 1 : 2;
+        splits = c->cfg.split_k ? c->cfg.split_k : c->max_splits_env ? c->max_splits_env : auto_splits;
         splits = (int)std::max<int64_t>(1, std::min<int64_t>(splits, c->y_elems / (rows_needed * c->d)));
         splits = std::min(splits, c->f_local / (c->fp8_g2_kb256 ? 256 : c->fp8_kb128 ? 128 : kBK));  // >= 1 K block per split
         c->split_stride = rows_needed * c->d;
@@ -1148,6 +1155,7 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
     if (const char* v = getenv("MOE_TAIL_PARTS")) c->tail_parts = atoi(v);
     if (const char* v = getenv("MOE_HOST_ZERO_COPY")) c->host_zero_copy = atoi(v) != 0;
     if (const char* v = getenv("MOE_SWAP_HINT")) c->swap_hint_mode = atoi(v);
+    if (const char* v = getenv("MOE_MAX_SPLITS")) c->max_splits_env = std::max(1, std::min(8, atoi(v)));
     if (const char* v = getenv("MOE_G2_SWAP_ROWS")) c->swap2_rows_per_expert = atoi(v);
     if (cfg->flags & MOE_FLAG_GATHER) c->gather = true;
     // router blocks of >= 2 rows; EP also routes the G*max_T*k receive slots

@@ -151,6 +151,19 @@ def test_tail_split(moe, T, d, f, E, parts):
     blk.close()
 
 
+@pytest.mark.parametrize("split_k", [1, 2, 3, 4, 8])
+@pytest.mark.parametrize("T", [40, 200])
+def test_split_k(moe, T, split_k):
+    """Decode w2 GEMM with an explicit K split (moe_config.split_k; fixed-order fp32
+    partials summed by the combine), incl. uneven splits of 1024/64 = 16 K blocks."""
+    shape = synth.MoEShape(T=T, d=256, f=1024, E=8, k=2)
+    inp = _inputs(shape, 29)
+    blk = _block(moe, inp, 2, T, 0x2, split_k=split_k)
+    run = GpuRun(blk, inp["x"])
+    check_forward(run, to_host_inputs(inp), 2)
+    blk.close()
+
+
 def _forced_gates(host, idx):
     l = oracle.router(host["x"], host["wg"], 1)["logits"]
     li = np.take_along_axis(l, idx.astype(np.int64), 1)
