@@ -215,7 +215,34 @@ __device__ __forceinline__ void decode_unit(int u, const TailPlan& tp, const Gem
     ti.lidx = l;
 }
 
-__device__ __forceinline__ float silu_f32(float a) { return a / (1.0f + __expf(-a)); }
+// silu(z) = z * sigmoid(z) (R11). The prefill w1/w3 epilogue evaluates it on 1.9 G
+// elements per forward, and with 256 x 512 pair tiles (single-buffered TMEM) the drain
+// of a tile's first TMEM half is on the MMA critical path; the SFU (16 results / clk /
+// SM) is its bound. MOE_SILU:
+//   2 (default): sigmoid(z) = 0.5 + 0.5 tanh(z/2), one tanh.approx.f32 (max rel. error
+//      2^-10.99 of tanh -> abs. error <= 2.5e-4 of sigmoid; h is then rounded to bf16,
+//      half-ulp 2^-9 relative), 1 SFU op per element
+//   1: z / (1 + e^-z) with ex2.approx + rcp.approx (2 SFU ops)
+//   0: z / (1 + e^-z) with an IEEE division (2 SFU ops + a ~10-instruction sequence)
+// r01 prefill A/B (interleaved): see DESIGN.md section 12.
+#ifndef MOE_SILU
+#define MOE_SILU 2
+#endif
+__device__ __forceinline__ float tanh_approx(float x) {
+    float y;
+    asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float silu_f32(float a) {
+#if MOE_SILU == 2
+    const float ha = 0.5f * a;
+    return fmaf(ha, tanh_approx(ha), ha);
+#elif MOE_SILU == 1
+    return __fdividef(a, 1.0f + __expf(-a));  // 1 + e^-a = inf for a < -88: rcp -> 0, silu -> -0
+#else
+    return a / (1.0f + __expf(-a));
+#endif
+}
 
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
     __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
@@ -583,23 +610,53 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 // full barrier), warp 1 of the leader = MMA issuer (commits multicast to both
 // CTAs' empty / tmem_full barriers), warps 2..5 of both CTAs = epilogue (arrive
 // on the leader's tmem_empty barrier; 8 arrivals per accumulator).
-constexpr int kPairStageBytes = 2 * 128 * 128;  // A half 16 KB + B half 16 KB
-constexpr int kPairStages = (kSmemBudget - 2048) / kPairStageBytes > 8 ? 8 : (kSmemBudget - 2048) / kPairStageBytes;
-constexpr int kPairSmemBytes = kPairStages * kPairStageBytes + 2048;
+//
+// NBLK = 2 ("wide" tiles): the pair computes 256 tokens x 2 weight blocks (512 columns:
+// two N = 256 MMAs per K step into the two halves of the 512 TMEM columns), so each
+// staged token tile feeds twice the MMAs -- 24 instead of 32 KB of L2->SM traffic per
+// CTA per 4.2 MFLOP. The accumulator is then single-buffered; the MMA issuer starts
+// the next tile's first S K-blocks on block 0 (TMEM half 0) while the epilogue still
+// drains half 1 (per-half tmem_empty barriers), then catches up block 1.
+// Why: under the 1 kW cap the prefill GEMMs are clock-bound; ncu (r01) showed
+// 1.76x the L2 read traffic of cuBLAS's 256x512-per-pair tiles at the same FLOPs and a
+// ~25 % lower SM clock at the same board power (scripts/exp/power_ab.py).
+//
+// Epilogue stores go through shared memory and TMA (cp.async.bulk.tensor store): each
+// epilogue warp owns two 4 KB buffers (32 rows x 128 B, 128-byte swizzle) and stores
+// 32-row boxes of h (64 bf16 columns) or y (32 fp32 columns). With per-thread row
+// stores (16 B per row per instruction, 32 rows per warp instruction) the epilogue cost
+// 11-12 % of the prefill step (r01 A/B with the stores compiled out: 18.2 -> 16.0 ms).
+constexpr int kPairOutBytes = 4 * 2 * 4096;
+template <int NBLK>
+struct PairCfg {
+    static constexpr int kStageBytes = 128 * 128 * (1 + NBLK);  // A half 16 KB + NBLK B halves of 16 KB
+    static constexpr int kRing = kSmemBudget - 2048 - kPairOutBytes;
+    static constexpr int kStages = kRing / kStageBytes > 8 ? 8 : kRing / kStageBytes;
+    static constexpr int kSmemBytes = kStages * kStageBytes + kPairOutBytes + 2048;
+};
+constexpr int kPairStageBytes = PairCfg<1>::kStageBytes;
+constexpr int kPairStages = PairCfg<1>::kStages;
+constexpr int kPairSmemBytes = PairCfg<1>::kSmemBytes;
 
+// 256-column weight blocks of one expert (w1|w3 block pairs of 128 ffn columns / 256 W2 rows)
 template <int KIND>
+__device__ __forceinline__ int pair_blocks(const GemmParams& p) {
+    return KIND == kG1Pair ? p.f / 128 : (p.d + 255) / 256;
+}
+
+template <int KIND, int NBLK = 1>
 __device__ __forceinline__ int pair_tiles_of(int n_e, const GemmParams& p) {
     if (n_e <= 0) return 0;
     const int mt = (n_e + 255) / 256;
-    return KIND == kG1Pair ? mt * (p.f / 128) : mt * ((p.d + 255) / 256);
+    return mt * ((pair_blocks<KIND>(p) + NBLK - 1) / NBLK);
 }
 
-template <int KIND>
+template <int KIND, int NBLK = 1>
 __device__ __forceinline__ void pair_decode(int t, const GemmParams& p, const int32_t* s_counts,
                                             const int32_t* s_offsets, TileInfo& ti) {
     int e = 0;
     for (; e < p.E; ++e) {
-        const int n = pair_tiles_of<KIND>(s_counts[e], p);
+        const int n = pair_tiles_of<KIND, NBLK>(s_counts[e], p);
         if (t < n) break;
         t -= n;
     }
@@ -607,7 +664,7 @@ __device__ __forceinline__ void pair_decode(int t, const GemmParams& p, const in
     ti.seg = s_offsets[e];
     ti.rows = s_counts[e];
     const int mt = (ti.rows + 255) / 256;
-    const int nt = KIND == kG1Pair ? p.f / 128 : (p.d + 255) / 256;
+    const int nt = (pair_blocks<KIND>(p) + NBLK - 1) / NBLK;
     // Tile orders (the ~74 clusters of one wave work on consecutive tiles):
     //   0: token tiles fastest        1: weight tiles fastest
     //   2: bands of `band` token tiles; inside a band token tiles fastest -- the
@@ -636,7 +693,7 @@ __device__ __forceinline__ void pair_decode(int t, const GemmParams& p, const in
     ti.kb0 = 0;
     ti.nkb = (KIND == kG1Pair ? p.d : p.f) / kBK;
     ti.split = 0;
-    ti.n_valid = 0;
+    ti.n_valid = min(NBLK, pair_blocks<KIND>(p) - ti.n_idx * NBLK);  // weight blocks in this tile
 }
 
 // Weight prefetch before the PDL wait in the CTA-pair kernels: measured WORSE (r01
@@ -645,18 +702,23 @@ __device__ __forceinline__ void pair_decode(int t, const GemmParams& p, const in
 #ifndef MOE_PAIR_PDL_PREFETCH
 #define MOE_PAIR_PDL_PREFETCH 0
 #endif
-template <int KIND>
+template <int KIND, int NBLK>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     moe_gemm_pair_kernel(const GemmParams p, const __grid_constant__ CUtensorMap tmA,
-                         const __grid_constant__ CUtensorMap tmB) {
-    constexpr int S = kPairStages;
+                         const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmOut) {
+    static_assert(NBLK == 1 || NBLK == 2, "one or two 256-column weight blocks per tile");
+    constexpr int S = PairCfg<NBLK>::kStages;
+    constexpr bool kPrefetch = MOE_PAIR_PDL_PREFETCH && NBLK == 1;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* smem_a = smem;
-    uint8_t* smem_b = smem + S * 16384;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * kPairStageBytes);
+    uint8_t* smem_b = smem + S * 16384;  // stage s, block j at (s * NBLK + j) * 16 KB
+    uint8_t* smem_out = smem + S * PairCfg<NBLK>::kStageBytes;  // [4 warps][2 buffers][32 rows][128 B]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_out + kPairOutBytes);
     uint64_t* full = bars;
     uint64_t* empty = bars + S;
+    // NBLK = 1: two accumulators (tmem_full/empty[acc]); NBLK = 2: one accumulator,
+    // tmem_full[0] + one tmem_empty barrier per 256-column half
     uint64_t* tmem_full = bars + 2 * S;
     uint64_t* tmem_empty = bars + 2 * S + 2;
     uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 4);
@@ -671,6 +733,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     if (warp == 0 && lane == 0) {
         ptx::prefetch_tmap(&tmA);
         ptx::prefetch_tmap(&tmB);
+        ptx::prefetch_tmap(&tmOut);
         for (int i = 0; i < S; ++i) {
             ptx::mbar_init(&full[i], 1);
             ptx::mbar_init(&empty[i], 1);
@@ -690,7 +753,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     // only its token / activation (A) loads wait. The other warps consume smem / TMEM
     // gated by the pipeline barriers and write h / y, which no still-running kernel
     // reads (the PDL chain orders the previous layer's combine before this grid).
-    if (!MOE_PAIR_PDL_PREFETCH) ptx::pdl_wait();
+    if (!kPrefetch) ptx::pdl_wait();
     if (threadIdx.x < 32) {
         for (int e = threadIdx.x; e < p.E; e += 32) {
             s_counts[e] = p.counts[e];
@@ -703,21 +766,21 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const uint32_t tmem_base = *tmem_base_slot;
 
     int total = 0;
-    for (int e = 0; e < p.E; ++e) total += pair_tiles_of<KIND>(s_counts[e], p);
+    for (int e = 0; e < p.E; ++e) total += pair_tiles_of<KIND, NBLK>(s_counts[e], p);
     const int cid = blockIdx.x / 2, ncl = gridDim.x / 2;
 
     if (warp == 0) {
         // ---------------------------------------------------------------- TMA producer (both CTAs)
         // Lane 0 waits for free stages and issues the loads; in gather mode (kG1Pair with
-        // src_row) every lane issues one tile::gather4 of this CTA's 128 token rows.
-        const bool gather = KIND == kG1Pair && p.src_row != nullptr;
+        // src_row, NBLK = 1) every lane issues one tile::gather4 of this CTA's 128 token rows.
+        const bool gather = KIND == kG1Pair && NBLK == 1 && p.src_row != nullptr;
         int stage = 0;
         uint32_t phase = 0;
         int pre = 0;  // k-blocks of the first tile whose weight loads precede the wait
-        if (MOE_PAIR_PDL_PREFETCH) {
+        if (kPrefetch) {
             if (cid < total) {
                 TileInfo t0;
-                pair_decode<KIND>(cid, p, s_counts, s_offsets, t0);
+                pair_decode<KIND, NBLK>(cid, p, s_counts, s_offsets, t0);
                 pre = min(S, t0.nkb);
                 if (lane == 0)
                     for (int kb = 0; kb < pre; ++kb) {  // fresh stages: no empty-wait needed
@@ -732,11 +795,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         bool first = true;
         for (int t = cid; t < total; t += ncl) {
             TileInfo ti;
-            pair_decode<KIND>(t, p, s_counts, s_offsets, ti);
-            // weights are packed with rows padded to a multiple of 256: every N tile is a full
+            pair_decode<KIND, NBLK>(t, p, s_counts, s_offsets, ti);
+            // weights are packed with rows padded to a multiple of 256: every N block is a full
             // 256-row MMA (the padding rows are zeros; the epilogue stores only d columns)
             const int a_row = ti.seg + ti.m_idx * 256 + (int)crank * 128;
-            const int b_row = ti.n_idx * 256 + (int)crank * 128;
+            const int b_row = ti.n_idx * NBLK * 256 + (int)crank * 128;
+            const uint32_t tx = 2u * 16384u * (1u + (uint32_t)ti.n_valid);  // both CTAs' A + B halves
             int4 rows = make_int4(0, 0, 0, 0);
             if (gather) {
                 const int32_t* sr = p.src_row + a_row + 4 * lane;
@@ -749,13 +813,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 if (lane == 0) {
                     if (!armed) {
                         ptx::mbar_wait(&empty[stage], phase ^ 1);
-                        if (leader) ptx::mbar_arrive_expect_tx(&full[stage], 2 * kPairStageBytes);
+                        if (leader) ptx::mbar_arrive_expect_tx(&full[stage], tx);
                     }
                     if (!gather) ptx::tma_load_2d_pair(&tmA, fb, smem_a + stage * 16384, kc, a_row, p.hint_a);
-                    if (!armed) {
-                        const WCoord w = wcoord(p, kc, b_row, ti.e);
-                        ptx::tma_load_4d_pair(&tmB, fb, smem_b + stage * 16384, 0, w.c1, w.c2, w.c3, p.hint_b);
-                    }
+                    if (!armed)
+                        for (int j = 0; j < ti.n_valid; ++j) {
+                            const WCoord w = wcoord(p, kc, b_row + j * 256, ti.e);
+                            ptx::tma_load_4d_pair(&tmB, fb, smem_b + (stage * NBLK + j) * 16384, 0, w.c1, w.c2, w.c3,
+                                                  p.hint_b);
+                        }
                 }
                 if (gather) {
                     __syncwarp();
@@ -768,92 +834,168 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     } else if (warp == 1) {
         // ---------------------------------------------------------------- MMA issuer (leader CTA)
         if (leader && lane == 0) {
+            const uint32_t idesc = ptx::make_idesc_bf16(256, 256);
             int stage = 0;
             uint32_t phase = 0;
             int acc = 0;
             uint32_t acc_phase = 0;
+            // MMAs of weight block j over the 4 K=16 slices of one staged K block
+            auto mma_block = [&](int st, int j, uint32_t d_tmem, bool first_k) {
+                const uint64_t adesc = ptx::make_smem_desc_sw128(ptx::smem_u32(smem_a + st * 16384));
+                const uint64_t bdesc = ptx::make_smem_desc_sw128(ptx::smem_u32(smem_b + (st * NBLK + j) * 16384));
+#pragma unroll
+                for (int kk = 0; kk < kBK / 16; ++kk)
+                    ptx::mma_bf16_pair(d_tmem, adesc + 2 * kk, bdesc + 2 * kk, idesc, (!first_k || kk) ? 1u : 0u);
+            };
             for (int t = cid; t < total; t += ncl) {
                 TileInfo ti;
-                pair_decode<KIND>(t, p, s_counts, s_offsets, ti);
-                const uint32_t idesc = ptx::make_idesc_bf16(256, 256);
-                const uint32_t d_tmem = tmem_base + acc * 256;
-                ptx::mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
-                ptx::tc_fence_after();
-                for (int kb = 0; kb < ti.nkb; ++kb) {
-                    ptx::mbar_wait(&full[stage], phase);
+                pair_decode<KIND, NBLK>(t, p, s_counts, s_offsets, ti);
+                if (NBLK == 1) {
+                    const uint32_t d_tmem = tmem_base + acc * 256;
+                    ptx::mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
                     ptx::tc_fence_after();
-                    const uint64_t adesc = ptx::make_smem_desc_sw128(ptx::smem_u32(smem_a + stage * 16384));
-                    const uint64_t bdesc = ptx::make_smem_desc_sw128(ptx::smem_u32(smem_b + stage * 16384));
-#pragma unroll
-                    for (int kk = 0; kk < kBK / 16; ++kk)
-                        ptx::mma_bf16_pair(d_tmem, adesc + 2 * kk, bdesc + 2 * kk, idesc, (kb | kk) ? 1u : 0u);
-                    ptx::mma_commit_pair(&empty[stage], 0x3);
-                    if (++stage == S) { stage = 0; phase ^= 1; }
+                    for (int kb = 0; kb < ti.nkb; ++kb) {
+                        ptx::mbar_wait(&full[stage], phase);
+                        ptx::tc_fence_after();
+                        mma_block(stage, 0, d_tmem, kb == 0);
+                        ptx::mma_commit_pair(&empty[stage], 0x3);
+                        if (++stage == S) { stage = 0; phase ^= 1; }
+                    }
+                    ptx::mma_commit_pair(&tmem_full[acc], 0x3);
+                    if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+                } else {
+                    // block 0 of the first P K-blocks while the epilogue drains TMEM half 1,
+                    // then block 1 of those K-blocks, then both blocks per K-block
+                    const int P = ti.n_valid == 2 ? min(S, ti.nkb) : 0;
+                    ptx::mbar_wait(&tmem_empty[0], acc_phase ^ 1);
+                    ptx::tc_fence_after();
+                    int st = stage;
+                    uint32_t ph = phase;
+                    for (int kb = 0; kb < P; ++kb) {
+                        ptx::mbar_wait(&full[st], ph);
+                        ptx::tc_fence_after();
+                        mma_block(st, 0, tmem_base, kb == 0);
+                        if (++st == S) { st = 0; ph ^= 1; }
+                    }
+                    ptx::mbar_wait(&tmem_empty[1], acc_phase ^ 1);
+                    ptx::tc_fence_after();
+                    for (int kb = 0; kb < P; ++kb) {  // stages already full (not released yet)
+                        mma_block(stage, 1, tmem_base + 256, kb == 0);
+                        ptx::mma_commit_pair(&empty[stage], 0x3);
+                        if (++stage == S) { stage = 0; phase ^= 1; }
+                    }
+                    for (int kb = P; kb < ti.nkb; ++kb) {
+                        ptx::mbar_wait(&full[stage], phase);
+                        ptx::tc_fence_after();
+                        mma_block(stage, 0, tmem_base, kb == 0);
+                        if (ti.n_valid == 2) mma_block(stage, 1, tmem_base + 256, kb == 0);
+                        ptx::mma_commit_pair(&empty[stage], 0x3);
+                        if (++stage == S) { stage = 0; phase ^= 1; }
+                    }
+                    ptx::mma_commit_pair(&tmem_full[0], 0x3);
+                    acc_phase ^= 1;
                 }
-                ptx::mma_commit_pair(&tmem_full[acc], 0x3);
-                if (++acc == 2) { acc = 0; acc_phase ^= 1; }
             }
         }
     } else {
         // ---------------------------------------------------------------- epilogue (warps 2..5, both CTAs)
+        // Warp q drains TMEM lanes [32q, 32q+32) (one token row per lane) and stores them as
+        // 32-row boxes through its two swizzled smem buffers. Segments are padded to 128
+        // rows, so this CTA's 128-row half is either inside the expert's padded segment
+        // (stored whole; padding rows hold finite values nothing reads) or past it (skipped).
         const int q = warp & 3;
-        const int r = q * 32 + lane;
         const uint32_t leader_empty0 = ptx::map_cluster(&tmem_empty[0], 0);
         const uint32_t leader_empty1 = ptx::map_cluster(&tmem_empty[1], 0);
+        const uint32_t obase = ptx::smem_u32(smem_out) + q * 8192;
+        const uint32_t row_off = (uint32_t)lane * 128;
+        const uint32_t sw = (uint32_t)(lane & 7);
+        uint32_t obuf = 0;
         int acc = 0;
         uint32_t acc_phase = 0;
         for (int t = cid; t < total; t += ncl) {
             TileInfo ti;
-            pair_decode<KIND>(t, p, s_counts, s_offsets, ti);
+            pair_decode<KIND, NBLK>(t, p, s_counts, s_offsets, ti);
             ptx::mbar_wait(&tmem_full[acc], acc_phase);
             ptx::tc_fence_after();
-            const uint32_t tbase = tmem_base + acc * 256 + (static_cast<uint32_t>(q * 32) << 16);
-            const int mrow = ti.m_idx * 256 + (int)crank * 128 + r;  // row within the expert segment
-            const bool valid = mrow < ti.rows;
-            if (KIND == kG1Pair) {
-                __nv_bfloat16* h = static_cast<__nv_bfloat16*>(p.out) + static_cast<int64_t>(ti.seg + mrow) * p.f +
-                                   ti.n_idx * 128;
+            const int half0 = ti.m_idx * 256 + (int)crank * 128;  // first row of this CTA's half
+            const bool store = half0 < ti.rows;
+            const int grow = ti.seg + half0 + q * 32;             // global row of this warp's box
+            for (int j = 0; j < NBLK; ++j) {
+                const int blk = ti.n_idx * NBLK + j;  // 256-column weight block
+                const uint32_t tbase = tmem_base + (NBLK == 1 ? acc : j) * 256 + (static_cast<uint32_t>(q * 32) << 16);
+                if (j < ti.n_valid) {
+                    if (KIND == kG1Pair) {
 #pragma unroll 1
-                for (int c = 0; c < 8; ++c) {
-                    uint32_t a[16], b[16];
-                    ptx::tmem_ld16(tbase + c * 16, a);
-                    ptx::tmem_ld16(tbase + 128 + c * 16, b);
-                    ptx::tmem_wait_ld();
-                    uint32_t o[8];
+                        for (int c2 = 0; c2 < 2; ++c2) {  // 64 h columns per box
+                            const uint32_t ob = obase + obuf * 4096 + row_off;
+                            if (lane == 0) ptx::bulk_wait_read<1>();  // this buffer's previous box was read
+                            __syncwarp();
+#pragma unroll 1
+                            for (int cc = 0; cc < 4; ++cc) {
+                                uint32_t a[16], b[16];
+                                ptx::tmem_ld16(tbase + c2 * 64 + cc * 16, a);
+                                ptx::tmem_ld16(tbase + 128 + c2 * 64 + cc * 16, b);
+                                ptx::tmem_wait_ld();
+                                uint32_t o[8];
 #pragma unroll
-                    for (int i = 0; i < 8; ++i) {
-                        float h0 = silu_f32(__uint_as_float(a[2 * i])) * __uint_as_float(b[2 * i]);
-                        float h1 = silu_f32(__uint_as_float(a[2 * i + 1])) * __uint_as_float(b[2 * i + 1]);
-                        o[i] = pack_bf16x2(h0, h1);
-                    }
-                    if (valid) {
-                        uint4* dst = reinterpret_cast<uint4*>(h + c * 16);
-                        dst[0] = make_uint4(o[0], o[1], o[2], o[3]);
-                        dst[1] = make_uint4(o[4], o[5], o[6], o[7]);
+                                for (int i = 0; i < 8; ++i) {
+                                    float h0 = silu_f32(__uint_as_float(a[2 * i])) * __uint_as_float(b[2 * i]);
+                                    float h1 = silu_f32(__uint_as_float(a[2 * i + 1])) * __uint_as_float(b[2 * i + 1]);
+                                    o[i] = pack_bf16x2(h0, h1);
+                                }
+                                ptx::sts128(ob + (((2 * cc) ^ sw) << 4), o[0], o[1], o[2], o[3]);
+                                ptx::sts128(ob + (((2 * cc + 1) ^ sw) << 4), o[4], o[5], o[6], o[7]);
+                            }
+                            ptx::fence_proxy_async();
+                            __syncwarp();
+                            if (lane == 0 && store) {
+                                ptx::tma_store_2d(&tmOut, smem_out + q * 8192 + obuf * 4096, blk * 128 + c2 * 64, grow);
+                                ptx::bulk_commit();
+                            }
+                            obuf ^= 1;
+                        }
+                    } else {
+                        const int nbox = min(256, p.d - blk * 256) / 32;  // 32 fp32 columns per box
+#pragma unroll 1
+                        for (int c = 0; c < nbox; ++c) {
+                            const uint32_t ob = obase + obuf * 4096 + row_off;
+                            if (lane == 0) ptx::bulk_wait_read<1>();
+                            __syncwarp();
+                            uint32_t v[16], w[16];
+                            ptx::tmem_ld16(tbase + c * 32, v);
+                            ptx::tmem_ld16(tbase + c * 32 + 16, w);
+                            ptx::tmem_wait_ld();
+#pragma unroll
+                            for (int i = 0; i < 4; ++i) {
+                                ptx::sts128(ob + ((i ^ sw) << 4), v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+                                ptx::sts128(ob + (((4 + i) ^ sw) << 4), w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
+                            }
+                            ptx::fence_proxy_async();
+                            __syncwarp();
+                            if (lane == 0 && store) {
+                                ptx::tma_store_2d(&tmOut, smem_out + q * 8192 + obuf * 4096, blk * 256 + c * 32, grow);
+                                ptx::bulk_commit();
+                            }
+                            obuf ^= 1;
+                        }
                     }
                 }
-            } else {
-                const int ncols = min(256, p.d - ti.n_idx * 256);
-                float* y = static_cast<float*>(p.out) + static_cast<int64_t>(ti.seg + mrow) * p.d + ti.n_idx * 256;
-#pragma unroll 1
-                for (int c = 0; c < ncols / 16; ++c) {
-                    uint32_t v[16];
-                    ptx::tmem_ld16(tbase + c * 16, v);
-                    ptx::tmem_wait_ld();
-                    if (valid) {
-                        float4* dst = reinterpret_cast<float4*>(y + c * 16);
-#pragma unroll
-                        for (int i = 0; i < 4; ++i)
-                            dst[i] = make_float4(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]),
-                                                 __uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3]));
-                    }
+                if (NBLK == 2) {  // this TMEM half is free for the next tile's MMAs
+                    ptx::tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive_cluster(j == 0 ? leader_empty0 : leader_empty1);
                 }
             }
-            ptx::tc_fence_before();
-            __syncwarp();
-            if (lane == 0) ptx::mbar_arrive_cluster(acc == 0 ? leader_empty0 : leader_empty1);
-            if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+            if (NBLK == 1) {
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive_cluster(acc == 0 ? leader_empty0 : leader_empty1);
+                if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+            } else {
+                acc_phase ^= 1;
+            }
         }
+        if (lane == 0) ptx::bulk_wait<0>();  // h / y stores performed before the grid completes
     }
     ptx::pdl_launch_dependents();
     ptx::tc_fence_before();

@@ -139,6 +139,22 @@ bool encode_map(CUtensorMap* m, const void* base, int rank, uint64_t K, uint64_t
     return r == CUDA_SUCCESS;
 }
 
+// Store map of a row-major [rows, cols] output (h: bf16, y: fp32) for the CTA-pair epilogue:
+// box {128 B of columns, 32 rows}, 128-byte swizzle (gemm_sm100.cuh kPairOutBytes).
+bool encode_store_map(CUtensorMap* m, const void* base, bool fp32, uint64_t cols, uint64_t rows) {
+    PFN_encodeTiled_t fn = get_encode_fn();
+    if (!fn) return false;
+    const uint64_t eb = fp32 ? 4 : 2;
+    cuuint64_t dims[2] = {cols, rows};
+    cuuint64_t strides[1] = {cols * eb};
+    cuuint32_t box[2] = {(cuuint32_t)(128 / eb), 32};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = fn(m, fp32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                    const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
 // Tiled bf16 weights (moe_pack_weights): 4D {64, tile_rows, K/64, tiles_per_expert * E}, each
 // [tile_rows][64] chunk contiguous; box {64, box_rows, 1, box_tiles}; 128B swizzle.
 // MOE_WTILE=0 (A/B experiments): the same 4D view over plain row-major packing
@@ -221,6 +237,10 @@ struct moe_ctx {
     // two boxes: 18.57/18.52 and 18.30/18.11 ms per step vs 19.14/19.04 and 18.36/18.48 ms
     // for weight-tiles-fastest; DRAM 17.2 vs 17.6 GB per launch, scripts/sweep_order.sh)
     int g1_raster = 2, g1_band = 16, g2_raster = 3, g2_band = 8;
+    // weight blocks (256 columns) per CTA-pair tile: 2 = 256 x 512 tiles with a
+    // single-buffered TMEM accumulator (gemm_sm100.cuh PairCfg), 1 = 256 x 256 tiles
+    // with two accumulators; env MOE_PAIR_NBLK. G2 band counts wide tiles when 2.
+    int pair_nblk = 2;
     // workspace (device)
     int32_t *topk_idx = nullptr, *pos = nullptr, *blockcount = nullptr, *blockoff = nullptr;
     int32_t *counts = nullptr, *offsets = nullptr;
@@ -275,6 +295,7 @@ struct moe_ctx {
     uint64_t p2p_epoch[4]{};      // exchanges done per counter
     // TMA descriptors: workspace operands
     CUtensorMap tm_x_tiled{}, tm_h_tiled{};
+    CUtensorMap tm_h_store{}, tm_y_store{};       // CTA-pair epilogue TMA stores
     CUtensorMap tm_x_swap[4]{}, tm_h_swap[4]{};  // NB = 32, 64, 128, 256
     // weight descriptor cache (keyed by pointer)
     struct WeightMaps {
@@ -387,10 +408,10 @@ moe_status set_fp8_attr(moe_ctx* c) {
     return MOE_OK;
 }
 
-template <int KIND>
+template <int KIND, int NBLK>
 moe_status set_pair_attr(moe_ctx* c) {
-    CUDA_TRY(c, cudaFuncSetAttribute(moe_gemm_pair_kernel<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     kPairSmemBytes));
+    CUDA_TRY(c, cudaFuncSetAttribute(moe_gemm_pair_kernel<KIND, NBLK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     PairCfg<NBLK>::kSmemBytes));
     return MOE_OK;
 }
 
@@ -401,9 +422,9 @@ moe_status set_gemm_attr(moe_ctx* c) {
     return MOE_OK;
 }
 
-template <int KIND>
+template <int KIND, int NBLK>
 moe_status launch_gemm_pair(moe_ctx* c, int slot, const GemmParams& p, const CUtensorMap& a, const CUtensorMap& b,
-                            int nclusters, cudaStream_t st) {
+                            const CUtensorMap& out, int nclusters, cudaStream_t st) {
     cudaEvent_t ea = nullptr, eb = nullptr;
     if (c->profiling) {
         ea = take_event(c);
@@ -413,7 +434,7 @@ moe_status launch_gemm_pair(moe_ctx* c, int slot, const GemmParams& p, const CUt
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(2 * nclusters);
     cfg.blockDim = dim3(kGemmThreads);
-    cfg.dynamicSmemBytes = kPairSmemBytes;
+    cfg.dynamicSmemBytes = PairCfg<NBLK>::kSmemBytes;
     cfg.stream = st;
     cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -424,7 +445,7 @@ moe_status launch_gemm_pair(moe_ctx* c, int slot, const GemmParams& p, const CUt
     attr[1].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 2;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, moe_gemm_pair_kernel<KIND>, p, a, b);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, moe_gemm_pair_kernel<KIND, NBLK>, p, a, b, out);
     if (e != cudaSuccess) return fail(c, MOE_ERR_CUDA, "pair kernel launch (slot %d) failed: %s", slot, cudaGetErrorString(e));
     c->launch_count++;
     if (c->profiling) {
@@ -745,15 +766,17 @@ moe_status run_gemms(moe_ctx* c, GemmPaths gp, int64_t rows_bound, int64_t rows_
         else s = run_swap_g1<128>(c, i1, &c->cur_w, st);
         if (s) return s;
     } else if (pair) {
+        const int nblk = c->gather_now ? 1 : c->pair_nblk;  // gather4 token fetch: 256 x 256 tiles only
         const int64_t mt_max = rows_total / 256 + c->E_local;
-        const int g1 = (int)std::min<int64_t>(ncl, mt_max * (c->f_local / 128));
+        const int g1 = (int)std::min<int64_t>(ncl, mt_max * ((c->f_local / 128 + nblk - 1) / nblk));
         GemmParams p1{c->counts, c->offsets, c->E_local, c->d, c->f_local, 1, c->h, 0, r1, b1,
                       ptx::kEvictNormal, ptx::kEvictNormal, c->gather_now ? c->src_row : nullptr};
         p1.w_tr = 256;
         p1.w_nt = c->w13_nt;
-        if ((s = launch_gemm_pair<kG1Pair>(c, kSlotGemm1, p1, c->gather_now ? c->tm_src : c->tm_x_tiled,
-                                           c->tm_w13_pair, g1, st)))
-            return s;
+        const CUtensorMap& ta = c->gather_now ? c->tm_src : c->tm_x_tiled;
+        s = nblk == 2 ? launch_gemm_pair<kG1Pair, 2>(c, kSlotGemm1, p1, ta, c->tm_w13_pair, c->tm_h_store, g1, st)
+                      : launch_gemm_pair<kG1Pair, 1>(c, kSlotGemm1, p1, ta, c->tm_w13_pair, c->tm_h_store, g1, st);
+        if (s) return s;
     } else {
         const int64_t mt_max = rows_total / 128 + c->E_local;
         const int g1 = (int)std::min<int64_t>(c->num_sms, mt_max * (c->f_local / 128));
@@ -783,13 +806,16 @@ moe_status run_gemms(moe_ctx* c, GemmPaths gp, int64_t rows_bound, int64_t rows_
         else s = run_swap_g2<256>(c, 3, &c->cur_w, splits, st);
         if (s) return s;
     } else if (pair) {
+        const int nblk = c->pair_nblk;
         const int64_t mt_max = rows_total / 256 + c->E_local;
-        const int g2 = (int)std::min<int64_t>(ncl, mt_max * ((c->d + 255) / 256));
-        GemmParams p2{c->counts, c->offsets, c->E_local, c->d, c->f_local, 1, c->y, 0, r2, b2,
-                      ptx::kEvictNormal, ptx::kEvictNormal};
+        const int g2 = (int)std::min<int64_t>(ncl, mt_max * (((c->d + 255) / 256 + nblk - 1) / nblk));
+        GemmParams p2{c->counts, c->offsets, c->E_local, c->d, c->f_local, 1, c->y, 0, r2,
+                      nblk == 2 && !c->pair_tune ? std::max(1, b2 / 2) : b2, ptx::kEvictNormal, ptx::kEvictNormal};
         p2.w_tr = 128;
         p2.w_nt = c->w2_nt;
-        if ((s = launch_gemm_pair<kG2Pair>(c, kSlotGemm2, p2, c->tm_h_tiled, c->tm_w2_swap, g2, st))) return s;
+        s = nblk == 2 ? launch_gemm_pair<kG2Pair, 2>(c, kSlotGemm2, p2, c->tm_h_tiled, c->tm_w2_swap, c->tm_y_store, g2, st)
+                      : launch_gemm_pair<kG2Pair, 1>(c, kSlotGemm2, p2, c->tm_h_tiled, c->tm_w2_swap, c->tm_y_store, g2, st);
+        if (s) return s;
     } else {
         const int64_t mt_max = rows_total / 128 + c->E_local;
         const int g2 = (int)std::min<int64_t>(c->num_sms, mt_max * ((c->d + 255) / 256));
@@ -1150,6 +1176,7 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
     c->fp8_g2_kb256 = c->fp8_kb128 && c->f_local % 256 == 0;
     if (const char* v = getenv("MOE_FP8_G2_KB")) c->fp8_g2_kb256 = c->fp8_g2_kb256 && atoi(v) == 256;
     if (const char* pt = getenv("MOE_PAIR_TUNE")) c->pair_tune = atoi(pt);
+    if (const char* v = getenv("MOE_PAIR_NBLK")) c->pair_nblk = atoi(v) == 1 ? 1 : 2;
     if (const char* v = getenv("MOE_GATHER")) c->gather = atoi(v) != 0;
     if (const char* v = getenv("MOE_G1_SWAP_ROWS")) c->swap_rows_per_expert = atoi(v);
     if (const char* v = getenv("MOE_TAIL_PARTS")) c->tail_parts = atoi(v);
@@ -1274,7 +1301,9 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
 
     // workspace TMA descriptors
     bool ok = encode_map(&c->tm_x_tiled, c->x_perm, 2, c->d, c->cap, 1, 128) &&
-              encode_map(&c->tm_h_tiled, c->h, 2, c->f_local, c->cap, 1, 128);
+              encode_map(&c->tm_h_tiled, c->h, 2, c->f_local, c->cap, 1, 128) &&
+              encode_store_map(&c->tm_h_store, c->h, false, c->f_local, c->cap) &&
+              encode_store_map(&c->tm_y_store, c->y, true, c->d, c->y_elems / c->d);
     const uint32_t nbs[4] = {32, 64, 128, 256};
     for (int i = 0; i < 4 && ok; ++i)
         ok = encode_map(&c->tm_x_swap[i], c->x_perm, 2, c->d, c->cap, 1, nbs[i]) &&
@@ -1289,7 +1318,8 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
         (as = set_gemm_attr<kG1Swap, 64>(c)) || (as = set_gemm_attr<kG2Swap, 64>(c)) ||
         (as = set_gemm_attr<kG1Swap, 128>(c)) || (as = set_gemm_attr<kG2Swap, 128>(c)) ||
         (as = set_gemm_attr<kG2Swap, 256>(c)) ||
-        (as = set_pair_attr<kG1Pair>(c)) || (as = set_pair_attr<kG2Pair>(c)) ||
+        (as = set_pair_attr<kG1Pair, 1>(c)) || (as = set_pair_attr<kG2Pair, 1>(c)) ||
+        (as = set_pair_attr<kG1Pair, 2>(c)) || (as = set_pair_attr<kG2Pair, 2>(c)) ||
         (as = set_fp8_attr<kG1Swap, 32>(c)) || (as = set_fp8_attr<kG2Swap, 32>(c)) ||
         (as = set_fp8_attr<kG1Swap, 64>(c)) || (as = set_fp8_attr<kG2Swap, 64>(c)) ||
         (as = set_fp8_attr<kG1Swap, 128>(c)) || (as = set_fp8_attr<kG2Swap, 128>(c)) ||
@@ -1318,8 +1348,9 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
             reinterpret_cast<const void*>(moe_gemm_kernel<kG1Swap, 32>), reinterpret_cast<const void*>(moe_gemm_kernel<kG2Swap, 32>),
             reinterpret_cast<const void*>(moe_gemm_kernel<kG1Swap, 64>), reinterpret_cast<const void*>(moe_gemm_kernel<kG2Swap, 64>),
             reinterpret_cast<const void*>(moe_gemm_kernel<kG1Swap, 128>), reinterpret_cast<const void*>(moe_gemm_kernel<kG2Swap, 128>),
-            reinterpret_cast<const void*>(moe_gemm_kernel<kG2Swap, 256>), reinterpret_cast<const void*>(moe_gemm_pair_kernel<kG1Pair>),
-            reinterpret_cast<const void*>(moe_gemm_pair_kernel<kG2Pair>)};
+            reinterpret_cast<const void*>(moe_gemm_kernel<kG2Swap, 256>), reinterpret_cast<const void*>(moe_gemm_pair_kernel<kG1Pair, 1>),
+            reinterpret_cast<const void*>(moe_gemm_pair_kernel<kG2Pair, 1>), reinterpret_cast<const void*>(moe_gemm_pair_kernel<kG1Pair, 2>),
+            reinterpret_cast<const void*>(moe_gemm_pair_kernel<kG2Pair, 2>)};
         for (const void* fn : fns)
             if ((e = cudaFuncGetAttributes(&fa, fn)) != cudaSuccess) return fail_init("cudaFuncGetAttributes", e);
     }

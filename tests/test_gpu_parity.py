@@ -127,6 +127,33 @@ def test_mixed_gemm_paths(moe, flags):
     blk.close()
 
 
+@pytest.mark.parametrize("T,d,f,E,k", [(16, 64, 128, 4, 2), (333, 320, 256, 6, 2), (1000, 512, 1024, 8, 2),
+                                       (700, 768, 384, 4, 2), (129, 64, 128, 4, 2)])
+def test_pair_wide_tiles(moe, T, d, f, E, k):
+    """CTA-pair GEMMs with 256 x 512 tiles (MOE_PAIR_NBLK=2, single-buffered TMEM,
+    block-0-first catch-up) vs 256 x 256 tiles (NBLK=1, two accumulators): both against
+    the oracle, and bit-identical to each other (the same MMAs accumulate each 256-column
+    block in the same K order). Odd block counts (f/128 = 3, ceil(d/256) = 3) leave a
+    half-empty last tile."""
+    shape = synth.MoEShape(T=T, d=d, f=f, E=E, k=k)
+    inp = _inputs(shape, 4000 + T)
+    outs = []
+    for nblk in ("1", "2"):
+        os.environ["MOE_PAIR_NBLK"] = nblk  # read at moe_init
+        try:
+            blk = _block(moe, inp, k, T, moe.MOE_FLAG_FORCE_TILED)
+        finally:
+            del os.environ["MOE_PAIR_NBLK"]
+        run = GpuRun(blk, inp["x"])
+        check_forward(run, to_host_inputs(inp), k)
+        outs.append(run.np("out_f32").copy())
+        out2 = blk.forward(inp["x"])  # second forward: barrier phases carried across calls
+        torch.cuda.synchronize()
+        assert torch.equal(out2.view(torch.int16), run.out.view(torch.int16))
+        blk.close()
+    assert np.array_equal(outs[0].view(np.int32), outs[1].view(np.int32))
+
+
 @pytest.mark.parametrize("parts", ["8", "3", "0"])
 @pytest.mark.parametrize("T,d,f,E", [(64, 1024, 2560, 8), (40, 512, 5120, 4), (300, 256, 2560, 8)])
 def test_tail_split(moe, T, d, f, E, parts):
