@@ -251,8 +251,22 @@ __device__ __forceinline__ uint32_t map_cluster(const void* p, uint32_t rank) {
     return r;
 }
 // remote (or local) arrive on an mbarrier given by its shared::cluster address
+// Arrive on an mbarrier of another CTA of the cluster (the pair leader's tmem_empty). Default
+// semantics (release at CTA scope): the epilogue's TMEM reads are ordered before the
+// leader's next MMAs by tcgen05.fence::before/after_thread_sync around this arrive/wait,
+// and nothing the MMA issuer does depends on this thread's global or shared stores. A
+// .release.cluster arrive compiles to MEMBAR.ALL.GPU + ERRBAR, i.e. waits for every
+// outstanding store of the thread: with the 256 x 512 pair tiles that put the epilogue's
+// stores on the MMA critical path (ncu r01: ERRBAR the top epilogue stall).
+#ifndef MOE_ARRIVE_RELEASE_CLUSTER
+#define MOE_ARRIVE_RELEASE_CLUSTER 0
+#endif
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+#if MOE_ARRIVE_RELEASE_CLUSTER
     asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+#else
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+#endif
 }
 // TMA load whose complete_tx goes to the mbarrier at `bar_cluster` (the pair leader's)
 __device__ __forceinline__ void tma_load_2d_pair(const CUtensorMap* m, uint32_t bar_cluster, void* dst, int32_t c0,
