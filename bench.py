@@ -543,14 +543,17 @@ def main():
     if decode:
         achieved = alg["g1_bytes"] / (dom_ms * 1e-3) / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                "frac": achieved / peaks["hbm_gbs"], "traffic": None, "kernel": "moe_gemm_kernel<kG1Swap> (w1/w3 + SwiGLU)",
+                "frac": achieved / peaks["hbm_gbs"], "traffic": None,
+                "kernel": ("moe_gemm_fp8t_kernel<kG1Swap> (FP8 w1/w3 + SwiGLU)" if args.fp8
+                           else "moe_gemm_kernel<kG1Swap> (w1/w3 + SwiGLU)"),
                 "peak_src": peaks["src"] + " (MEASURED_PEAKS.json hbm_gbs)"}
         step_frac = alg["bytes"] / (ms * 1e-3) / 1e9 / peaks["hbm_gbs"]
     else:
         achieved = alg["g1_flops"] / (dom_ms * 1e-3) / 1e12
         pk = peaks["bf16_tflops_sustained"]
         roof = {"bound": "tensor", "achieved": achieved, "peak": pk, "unit": "TFLOP/s", "frac": achieved / pk,
-                "traffic": None, "kernel": "moe_gemm_kernel<kG1Tiled> (w1/w3 + SwiGLU)",
+                "traffic": None,
+                "kernel": "moe_gemm_pair_kernel<kG1Pair,2> (w1/w3 + SwiGLU, 256x512 CTA-pair tiles)",
                 "peak_src": peaks["src"] + " (MEASURED_PEAKS.json bf16_tflops_sustained)"}
         step_frac = alg["flops"] / (ms * 1e-3) / 1e12 / pk
     tr, tr_src = load_traffic(args.config + ("_fp8" if args.fp8 else "")) if world == 1 and par == "none" \

@@ -56,15 +56,15 @@ def launches(path):
     agg = {}
     for _, n, v in mine:
         short = n.split("(")[0].replace("void ", "")
-        a = agg.setdefault(short, [0, 0.0])
-        a[0] += 1
-        a[1] += v
-    fwd = {k: v for k, v in agg.items() if "pack" not in k}
-    tot = sum(v[1] for v in fwd.values())
-    print("| kernel | launches | mean us | share of forward |")
+        agg.setdefault(short, []).append(v)
+    # medians: the list also holds bench.py's e2e pass, whose combine stores into pinned
+    # HOST memory (over PCIe) -- an outlier for the device-resident forward
+    med = {k: sorted(v)[len(v) // 2] for k, v in agg.items() if "pack" not in k}
+    tot = sum(med.values())
+    print("| kernel | launches | median us | share of forward (medians) |")
     print("|---|---|---|---|")
-    for k, (n, t) in sorted(fwd.items(), key=lambda kv: -kv[1][1]):
-        print(f"| `{k}` | {n} | {t / n / 1000:.2f} | {t / tot:.3f} |")
+    for k, m in sorted(med.items(), key=lambda kv: -kv[1]):
+        print(f"| `{k}` | {len(agg[k])} | {m / 1000:.2f} | {m / tot:.3f} |")
     print()
     print("| ID | kernel | ns |")
     print("|---|---|---|")
