@@ -58,6 +58,11 @@ struct GemmParams {
     // blocks, so one K block of one tile is one contiguous chunk of HBM. w_nt: tiles
     // per expert. The weight maps are 4D {64, w_tr, K/64, w_nt * E}.
     int32_t w_tr, w_nt;
+    // FP8 w2 GEMM after the two-term (fp8x) w1/w3 GEMM (nullable): 2^-s of each permuted
+    // row. The fp8x epilogue stores h * 2^(2s - 6) in fp16 (keeps fp16 h in its normal
+    // range for any token scale: h grows ~quadratically with the token), so y is scaled
+    // back by 2^(6 - 2s) -- powers of two, exact.
+    const float* tok_scale;
 };
 
 // 4D coordinates of rows [row, row + box) of expert e at K offset kc in a tiled weight map
@@ -1264,8 +1269,221 @@ __global__ void __launch_bounds__(kFp8Threads, 1)
 #pragma unroll
                         for (int i = 0; i < 16; ++i) {
                             const int n = cc * 16 + i;
-                            if (n < ti.n_valid) y[static_cast<int64_t>(n) * p.d] = __uint_as_float(v[i]) * s2v;
+                            if (n < ti.n_valid) {
+                                float u = s2v;
+                                if (p.tok_scale) {
+                                    const float tsn = p.tok_scale[ti.b_row + n];
+                                    u *= tsn * tsn * 64.f;
+                                }
+                                y[static_cast<int64_t>(n) * p.d] = __uint_as_float(v[i]) * u;
+                            }
                         }
+                    }
+                }
+            }
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&tmem_empty[acc]);
+            if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        }
+    }
+    ptx::pdl_launch_dependents();
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc(tmem_base, 512);
+    }
+}
+
+// ----------------------------------------------------------------------------
+// FP8-weight decode w1/w3 GEMM on the 8-bit tensor core path (tcgen05 kind::f8f6f4),
+// no weight conversion. The tokens are split into two E4M3 terms by the permute kernel
+// (hi + lo = x * 2^s, exact for bf16 x above ~1e-3 of the row max: permute_row_fp8x),
+// so each K step runs two MMAs, D += W * hi^T and D += W * lo^T, with both operands
+// straight from TMA-staged shared memory. The epilogue applies the weight row scale
+// (power of two) and the token scale 2^-s, then SwiGLU, and stores fp16 h for the
+// FP8 w2 GEMM. Why: the converter pipeline of moe_gemm_fp8t_kernel (e4m3 -> fp16 in
+// TMEM, ~16 cvt results / clk / SM) capped K3 at ~5 TB/s (ncu r01: converter warps
+// waiting on TMEM A stages; 79 % of the HBM roofline at 1 B/weight).
+// Warps: 0 = TMA producer, 1 = TMEM + MMA issuer, 2..5 = epilogue.
+template <int NB>
+struct Fp8xCfg {
+    static_assert(NB >= 16 && NB <= 128 && NB % 16 == 0, "token tile");
+    static constexpr int kABytes = 256 * 128;   // w1|w3 rows x 128 E4M3 (one 128-byte swizzle row)
+    static constexpr int kBBytes = NB * 128;    // token rows x 128 E4M3, per term (hi, lo)
+    static constexpr int kStageBytes = kABytes + 2 * kBBytes;
+    static constexpr int kStagesRaw = (kSmemBudget - 2048) / kStageBytes;
+    static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
+    static constexpr int kSmemBytes = kStages * kStageBytes + 2048;
+    static_assert(kStages >= 3, "pipeline too shallow");
+};
+
+template <int NB>
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    moe_gemm_fp8x_kernel(const GemmParams p, const float* __restrict__ scales, const float* __restrict__ tok_scale,
+                         const __grid_constant__ CUtensorMap tmA8, const __grid_constant__ CUtensorMap tmB8) {
+    using C = Fp8xCfg<NB>;
+    constexpr int S = C::kStages;
+    constexpr int KB = 128;  // K elements (bytes) per stage
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* smem_a = smem;                  // stage s at s * kABytes
+    uint8_t* smem_b = smem + S * C::kABytes; // stage s: hi at s * 2 * kBBytes, lo at + kBBytes
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * C::kStageBytes);
+    uint64_t* full = bars;
+    uint64_t* empty = bars + S;
+    uint64_t* tmem_full = bars + 2 * S;
+    uint64_t* tmem_empty = bars + 2 * S + 2;
+    uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 4);
+    int32_t* s_counts = reinterpret_cast<int32_t*>(bars + 2 * S + 5);
+    int32_t* s_offsets = s_counts + 32;
+
+    const int warp = threadIdx.x / 32;
+    const int lane = threadIdx.x % 32;
+    if (warp == 0 && lane == 0) {
+        ptx::prefetch_tmap(&tmA8);
+        ptx::prefetch_tmap(&tmB8);
+        for (int i = 0; i < S; ++i) {
+            ptx::mbar_init(&full[i], 1);
+            ptx::mbar_init(&empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            ptx::mbar_init(&tmem_full[i], 1);
+            ptx::mbar_init(&tmem_empty[i], 4);
+        }
+        ptx::fence_mbar_init();
+    }
+    if (warp == 1) {
+        ptx::tmem_alloc(tmem_base_slot, 512);
+        ptx::tmem_relinquish();
+    }
+    // counts / offsets come from the router, complete before this grid launches (the
+    // permute kernel triggers its dependents after its own griddepcontrol.wait). The
+    // producer issues the first tile's weight stages before anything waits on the
+    // permute (PDL); its token loads and every other warp wait for it.
+    if (threadIdx.x < 32)
+        for (int e = threadIdx.x; e < p.E; e += 32) {
+            s_counts[e] = p.counts[e];
+            s_offsets[e] = p.offsets[e];
+        }
+    __syncwarp();
+    int pre = 0;  // producer: weight stages of its first tile already issued
+    if (warp == 0 && lane == 0) {
+        int total0 = 0;  // warp 0 wrote s_counts itself
+        for (int e = 0; e < p.E; ++e) total0 += tiles_of<kG1Swap, NB>(s_counts[e], p);
+        if ((int)blockIdx.x < total0) {
+        TileInfo t0;
+        decode_tile<kG1Swap, NB, KB>(blockIdx.x, p, s_counts, s_offsets, t0);
+        pre = min(S, t0.nkb);
+        for (int kb = 0; kb < pre; ++kb) {  // fresh stages: no empty-wait
+            ptx::mbar_arrive_expect_tx(&full[kb], C::kStageBytes);
+            ptx::tma_load_3d(&tmA8, &full[kb], smem_a + kb * C::kABytes, (t0.kb0 + kb) * KB, t0.a_row, t0.e,
+                             ptx::kEvictFirst);
+        }
+        }
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    ptx::pdl_wait();
+    const uint32_t tmem_base = *tmem_base_slot;
+    int total = 0;
+    for (int e = 0; e < p.E; ++e) total += tiles_of<kG1Swap, NB>(s_counts[e], p);
+
+    if (warp == 0) {
+        if (lane == 0) {  // ------------------------------------------------ TMA producer
+            int st = 0;
+            uint32_t ph = 0;
+            bool first = true;
+            for (int t = blockIdx.x; t < total; t += gridDim.x) {
+                TileInfo ti;
+                decode_tile<kG1Swap, NB, KB>(t, p, s_counts, s_offsets, ti);
+                for (int kb = 0; kb < ti.nkb; ++kb) {
+                    const int kc = (ti.kb0 + kb) * KB;
+                    if (!(first && kb < pre)) {
+                        ptx::mbar_wait(&empty[st], ph ^ 1);
+                        ptx::mbar_arrive_expect_tx(&full[st], C::kStageBytes);
+                        ptx::tma_load_3d(&tmA8, &full[st], smem_a + st * C::kABytes, kc, ti.a_row, ti.e,
+                                         ptx::kEvictFirst);
+                    }
+                    uint8_t* b = smem_b + st * 2 * C::kBBytes;
+                    ptx::tma_load_3d(&tmB8, &full[st], b, kc, ti.b_row, 0, ptx::kEvictLast);
+                    ptx::tma_load_3d(&tmB8, &full[st], b + C::kBBytes, kc, ti.b_row, 1, ptx::kEvictLast);
+                    if (++st == S) { st = 0; ph ^= 1; }
+                }
+                first = false;
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // ------------------------------------------------ MMA issuer
+            int st = 0;
+            uint32_t ph = 0;
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            for (int t = blockIdx.x; t < total; t += gridDim.x) {
+                TileInfo ti;
+                decode_tile<kG1Swap, NB, KB>(t, p, s_counts, s_offsets, ti);
+                const uint32_t n_mma = (uint32_t)((ti.n_valid + 15) / 16 * 16);
+                // D f32 (bit 4), A = B = E4M3 (format 0), K-major, N >> 3 at 17, M >> 4 at 24
+                const uint32_t idesc = (1u << 4) | ((n_mma >> 3) << 17) | ((128u >> 4) << 24);
+                const uint32_t d_a = tmem_base + acc * 256, d_b = d_a + 128;
+                ptx::mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
+                ptx::tc_fence_after();
+                for (int kb = 0; kb < ti.nkb; ++kb) {
+                    ptx::mbar_wait(&full[st], ph);
+                    ptx::tc_fence_after();
+                    const uint64_t a1 = ptx::make_smem_desc_sw128(ptx::smem_u32(smem_a + st * C::kABytes));
+                    const uint64_t a3 = ptx::make_smem_desc_sw128(ptx::smem_u32(smem_a + st * C::kABytes + 16384));
+                    const uint64_t bh = ptx::make_smem_desc_sw128(ptx::smem_u32(smem_b + st * 2 * C::kBBytes));
+                    const uint64_t bl = ptx::make_smem_desc_sw128(ptx::smem_u32(smem_b + st * 2 * C::kBBytes + C::kBBytes));
+#pragma unroll
+                    for (int kk = 0; kk < KB / 32; ++kk) {  // 32 bytes of K per MMA: +2 in the descriptor
+                        const uint32_t init = (kb | kk) ? 1u : 0u;
+                        ptx::mma_e4m3(d_a, a1 + 2 * kk, bh + 2 * kk, idesc, init);
+                        ptx::mma_e4m3(d_a, a1 + 2 * kk, bl + 2 * kk, idesc, 1u);
+                        ptx::mma_e4m3(d_b, a3 + 2 * kk, bh + 2 * kk, idesc, init);
+                        ptx::mma_e4m3(d_b, a3 + 2 * kk, bl + 2 * kk, idesc, 1u);
+                    }
+                    ptx::mma_commit(&empty[st]);
+                    if (++st == S) { st = 0; ph ^= 1; }
+                }
+                ptx::mma_commit(&tmem_full[acc]);
+                if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+            }
+        }
+    } else {
+        // ---------------------------------------------------------------- epilogue (warps 2..5)
+        const int q = warp & 3;
+        const int r = q * 32 + lane;  // weight row in the w1 (and w3) half = ffn column of the tile
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int t = blockIdx.x; t < total; t += gridDim.x) {
+            TileInfo ti;
+            decode_tile<kG1Swap, NB, KB>(t, p, s_counts, s_offsets, ti);
+            ptx::mbar_wait(&tmem_full[acc], acc_phase);
+            ptx::tc_fence_after();
+            const uint32_t tbase = tmem_base + acc * 256 + (static_cast<uint32_t>(q * 32) << 16);
+            const float* sc = scales + (int64_t)ti.e * 2 * p.f + ti.m_idx * 256;
+            const float s1v = sc[r], s3v = sc[128 + r];
+            __half* hp = static_cast<__half*>(p.out) + static_cast<int64_t>(ti.b_row) * p.f + ti.m_idx * 128 + r;
+            const float* ts = tok_scale + ti.b_row;
+            const int nchunks = (ti.n_valid + 15) / 16;
+#pragma unroll 1
+            for (int cc = 0; cc < nchunks; ++cc) {
+                uint32_t a[16], b[16];
+                ptx::tmem_ld16(tbase + cc * 16, a);
+                ptx::tmem_ld16(tbase + 128 + cc * 16, b);
+                ptx::tmem_wait_ld();
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    const int n = cc * 16 + i;
+                    if (n < ti.n_valid) {
+                        const float tsn = ts[n];
+                        const float hv = silu_f32(__uint_as_float(a[i]) * (s1v * tsn)) *
+                                         (__uint_as_float(b[i]) * (s3v * tsn));
+                        // fp16 h normalised by the token scale: h * 2^(2s - 6) (see GemmParams)
+                        hp[static_cast<int64_t>(n) * p.f] = __float2half_rn(hv * (0.015625f / (tsn * tsn)));
                     }
                 }
             }
@@ -1565,7 +1783,14 @@ __global__ void __launch_bounds__(kFp8tThreads, 1)
 #pragma unroll
                         for (int i = 0; i < 16; ++i) {
                             const int n = cc * 16 + i;
-                            if (n < ti.n_valid) y[static_cast<int64_t>(n) * p.d] = __uint_as_float(v[i]) * s2v;
+                            if (n < ti.n_valid) {
+                                float u = s2v;
+                                if (p.tok_scale) {
+                                    const float tsn = p.tok_scale[ti.b_row + n];
+                                    u *= tsn * tsn * 64.f;
+                                }
+                                y[static_cast<int64_t>(n) * p.d] = __uint_as_float(v[i]) * u;
+                            }
                         }
                     }
                 }

@@ -423,6 +423,12 @@ struct PermuteParams {
     int32_t* pos_aux;         // optional copy for the caller
     __nv_bfloat16* x_perm;    // [Cap, d]
     int32_t to_f16;           // store rows as fp16 (fp8-weight GEMMs) instead of copying bf16
+    // FP8 two-term token split (fp8-weight w1/w3 GEMM on kind::f8f6f4): x8 != nullptr ->
+    // row ps is stored as bytes hi = e4m3(x * 2^s) in plane 0 and lo = e4m3(x * 2^s - hi)
+    // in plane 1 ([2][plane_rows][d] bytes, reusing x_perm's memory), tok_scale[ps] = 2^-s
+    uint8_t* x8;
+    float* tok_scale;
+    int64_t plane_rows;
     int32_t* src_row;         // gather mode (x_perm == nullptr): [Cap] token of each permuted row
     // EP dispatch over peer memory (MOE_FLAG_P2P): rows / meta go straight into slot
     // (my_rank * cap + r) of the destination rank's receive buffer.
@@ -442,6 +448,83 @@ __device__ __forceinline__ uint4 bf16x8_to_f16x8(const uint4& v) {
     r.z = *reinterpret_cast<uint32_t*>(&h2);
     r.w = *reinterpret_cast<uint32_t*>(&h3);
     return r;
+}
+
+// Two E4M3 codes (lower byte = first element) <-> floats
+__device__ __forceinline__ uint16_t f32x2_to_e4m3x2(float first, float second) {
+    uint16_t r;
+    asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(r) : "f"(second), "f"(first));
+    return r;
+}
+__device__ __forceinline__ float2 e4m3x2_to_f32x2(uint16_t v) {
+    uint32_t h;
+    asm("cvt.rn.f16x2.e4m3x2 %0, %1;" : "=r"(h) : "h"(v));
+    return __half22float2(*reinterpret_cast<__half2*>(&h));
+}
+
+// FP8 two-term split of one token row for the kind::f8f6f4 w1/w3 GEMM (R15):
+// s = the power of two putting the row max |x| in (224, 448]; hi = RNE_e4m3(x 2^s),
+// lo = RNE_e4m3(x 2^s - hi). For bf16 x the residual x 2^s - hi has at most 4
+// significant bits, so hi + lo == x 2^s exactly wherever |x 2^s| >= 2^-2 (lo stays above
+// the E4M3 subnormal step 2^-9); smaller elements (below ~1e-3 of the row max) keep an
+// error <= 2^-10 / 2^s. The GEMM multiplies its fp32 accumulator by tok_scale = 2^-s.
+__device__ __forceinline__ void permute_row_fp8x(const PermuteParams& p, int t, int tl, int sw, int wpt, int lane,
+                                              const int32_t (*s_pos)[2]) {
+    __shared__ uint32_t s_max[8];
+    const int nvec = p.d / 8;
+    const int stride = 32 * wpt;
+    const bool valid = t < p.T;
+    const uint4* src = reinterpret_cast<const uint4*>(p.x + (int64_t)(valid ? t : 0) * p.d);
+    // pass 1: row max of |x| on the bf16 bit patterns (magnitude order == integer order)
+    uint32_t m = 0;
+    if (valid)
+        for (int v = sw * 32 + lane; v < nvec; v += stride) {
+            const uint4 q = __ldg(src + v);
+            const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+            for (int i = 0; i < 4; ++i) m = max(m, max(w[i] & 0x7FFFu, (w[i] >> 16) & 0x7FFFu));
+        }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane == 0) s_max[threadIdx.x / 32] = m;
+    __syncthreads();
+    if (!valid) return;
+    uint32_t rm = 0;
+    for (int w = 0; w < wpt; ++w) rm = max(rm, s_max[tl * wpt + w]);
+    const float rmax = __uint_as_float(rm << 16);
+    int sh = 0;
+    if (rmax > 0.f) {  // 448 / rmax = 2^e * 1.xx  ->  s = e, rmax * 2^s in (224, 448]
+        const int e = ((__float_as_int(448.f / rmax) >> 23) & 0xFF) - 127;
+        sh = max(-60, min(60, e));  // keeps 2^(+-2s) of the fp16 h normalisation in fp32 range
+    }
+    const float scale = __int_as_float((sh + 127) << 23);
+    const int32_t d0 = s_pos[tl][0], d1 = p.k > 1 ? s_pos[tl][1] : -1;
+    if (sw == 0 && lane == 0) {
+        const float inv = __int_as_float((127 - sh) << 23);
+        if (d0 >= 0) p.tok_scale[d0] = inv;
+        if (d1 >= 0) p.tok_scale[d1] = inv;
+    }
+    const int64_t plane = p.plane_rows * p.d;
+    uint2* hi0 = d0 >= 0 ? reinterpret_cast<uint2*>(p.x8 + (int64_t)d0 * p.d) : nullptr;
+    uint2* hi1 = d1 >= 0 ? reinterpret_cast<uint2*>(p.x8 + (int64_t)d1 * p.d) : nullptr;
+    for (int v = sw * 32 + lane; v < nvec; v += stride) {
+        float f[8];
+        bf16x8_to_f32(__ldg(src + v), f);
+        uint32_t hw[4], lw[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const float a = f[2 * i] * scale, b = f[2 * i + 1] * scale;
+            const uint16_t h = f32x2_to_e4m3x2(a, b);
+            const float2 hf = e4m3x2_to_f32x2(h);
+            const uint16_t l = f32x2_to_e4m3x2(a - hf.x, b - hf.y);
+            hw[i] = h;
+            lw[i] = l;
+        }
+        const uint2 hv = make_uint2(hw[0] | (hw[1] << 16), hw[2] | (hw[3] << 16));
+        const uint2 lv = make_uint2(lw[0] | (lw[1] << 16), lw[2] | (lw[3] << 16));
+        if (hi0) { hi0[v] = hv; reinterpret_cast<uint2*>(reinterpret_cast<uint8_t*>(hi0) + plane)[v] = lv; }
+        if (hi1) { hi1[v] = hv; reinterpret_cast<uint2*>(reinterpret_cast<uint8_t*>(hi1) + plane)[v] = lv; }
+    }
 }
 
 // K2 (a6): position of each assignment = segment start + rank of its router block
@@ -496,6 +579,11 @@ __global__ void __launch_bounds__(kPermuteThreads) moe_permute_kernel(const Perm
     const int wpt = 8 / p.PT;            // warps per token row
     const int tl = warp / wpt, sw = warp % wpt;
     const int t = tok0 + tl;
+    if (p.x8) {
+        permute_row_fp8x(p, t, tl, sw, wpt, lane, s_pos);
+        ptx::pdl_launch_dependents();
+        return;
+    }
     if (t < p.T) {
         const int nvec = p.d / 8;
         const uint4* src = reinterpret_cast<const uint4*>(p.x + (int64_t)t * p.d);

@@ -241,6 +241,12 @@ struct moe_ctx {
     // single-buffered TMEM accumulator (gemm_sm100.cuh PairCfg), 1 = 256 x 256 tiles
     // with two accumulators; env MOE_PAIR_NBLK. G2 band counts wide tiles when 2.
     int pair_nblk = 2;
+    int swap_nb_cap = 0;      // env MOE_SWAP_NB_CAP (see run_gemms)
+    // FP8 w1/w3 GEMM on kind::f8f6f4 with two-term E4M3 tokens (moe_gemm_fp8x_kernel);
+    // needs d % 128 == 0; env MOE_FP8_X=0 selects the fp16-converter kernels
+    bool fp8x = false;
+    float* tok_scale = nullptr;   // [cap] 2^-s of each permuted row (fp8x)
+    CUtensorMap tm_x8[3]{};       // x_perm as [2][cap][d] E4M3 planes, box {128, NB}, NB = 32, 64, 128
     // workspace (device)
     int32_t *topk_idx = nullptr, *pos = nullptr, *blockcount = nullptr, *blockoff = nullptr;
     int32_t *counts = nullptr, *offsets = nullptr;
@@ -405,6 +411,13 @@ template <int KIND, int NB>
 moe_status set_fp8_attr(moe_ctx* c) {
     CUDA_TRY(c, cudaFuncSetAttribute(moe_gemm_fp8_kernel<KIND, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      Fp8Cfg<KIND, NB>::kSmemBytes));
+    return MOE_OK;
+}
+
+template <int NB>
+moe_status set_fp8x_attr(moe_ctx* c) {
+    CUDA_TRY(c, cudaFuncSetAttribute(moe_gemm_fp8x_kernel<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     Fp8xCfg<NB>::kSmemBytes));
     return MOE_OK;
 }
 
@@ -609,6 +622,11 @@ moe_status run_swap_g1(moe_ctx* c, int nbi, const moe_expert_weights* w, cudaStr
         p1.src_row = c->src_row;
         return launch_gemm<kG1Swap, NB>(c, kSlotGemm1, p1, c->tm_w13, c->tm_src, c->num_sms, st);
     }
+    if constexpr (NB <= 128)
+        if (c->fp8 && c->fp8x)
+            return launch(c, kSlotGemm1, moe_gemm_fp8x_kernel<NB>, dim3(c->num_sms), dim3(kGemmThreads),
+                          (size_t)Fp8xCfg<NB>::kSmemBytes, st, p1, static_cast<const float*>(w->w13_scale),
+                          static_cast<const float*>(c->tok_scale), c->tm_w13, c->tm_x8[nbi]);
     if constexpr (NB <= 64)
         if (c->fp8 && !c->fp8_smem_a)
             return launch_gemm_fp8t<kG1Swap, NB>(c, kSlotGemm1, p1, w->w13_scale, c->tm_w13, c->tm_x_swap[nbi],
@@ -626,6 +644,7 @@ moe_status run_swap_g2(moe_ctx* c, int nbi, const moe_expert_weights* w, int spl
     p2.hint_a = c->swap_w_hint;
     p2.w_tr = 128;
     p2.w_nt = c->w2_nt;
+    if (c->fp8 && c->fp8x) p2.tok_scale = c->tok_scale;  // undo the fp8x epilogue's h normalisation
     if constexpr (NB <= 64)
         if (c->fp8 && !c->fp8_smem_a)
             return launch_gemm_fp8t<kG2Swap, NB>(c, kSlotGemm2, p2, w->w2_scale, c->tm_w2_swap, c->tm_h_swap[nbi],
@@ -704,6 +723,12 @@ moe_status route_and_permute(moe_ctx* c, const RouteSpec& r, cudaStream_t st) {
     pp.src_row = r.src_row;
     pp.peers = r.peers; pp.peer_rows_off = r.peer_rows_off; pp.peer_meta_off = r.peer_meta_off; pp.my_rank = r.my_rank;
     pp.to_f16 = c->fp8 && r.cap == 0;  // fp8-weight GEMMs take fp16 tokens
+    if (c->fp8x && r.cap == 0 && r.dst_rows == c->x_perm) {  // ... or two E4M3 terms (fp8x)
+        pp.to_f16 = 0;
+        pp.x8 = reinterpret_cast<uint8_t*>(c->x_perm);
+        pp.tok_scale = c->tok_scale;
+        pp.plane_rows = c->cap;
+    }
     return launch(c, kSlotPermute, moe_permute_kernel, dim3((r.T + pp.PT - 1) / pp.PT), dim3(kPermuteThreads), 0,
                   st, pp);
 }
@@ -741,7 +766,22 @@ moe_status run_gemms(moe_ctx* c, GemmPaths gp, int64_t rows_bound, int64_t rows_
     // w1|w3 accumulators single-buffered: measured slower, 32-layer stack r01), GEMM2
     // goes to 256; FP8 kernels stop at 128.
     const int nbw = (int)std::max<int64_t>(32, std::min<int64_t>(256, next_pow2((int)std::min<int64_t>(rows_bound, 1 << 20))));
-    const int nb1 = std::min(nbw, 128), nb2 = c->fp8 ? nb1 : nbw;
+    int nb1 = std::min(nbw, 128), nb2 = c->fp8 ? nb1 : nbw;
+    // experiment knob (env MOE_SWAP_NB_CAP): cap the swap-path token tile below the
+    // worst-case bound; an expert with more rows then takes several token tiles
+    // (device-side tile count: still correct), re-streaming its weights per tile
+    // FP8 (fp8x) decode: a 32-token tile while the mean rows per expert is <= 16 (64-token
+    // decode: per-expert counts ~ Bin(64, 1/4), P(> 32) ~ 1e-6; a larger expert just runs
+    // two token tiles). The smaller B stages leave room for a 5th pipeline stage
+    // (r01 A/B: 0.2744 -> 0.2686 ms per step).
+    if (c->fp8 && c->fp8x && rows_total <= 16LL * c->E_local) {
+        nb1 = std::min(nb1, 32);
+        nb2 = std::min(nb2, 32);
+    }
+    if (c->swap_nb_cap >= 32) {
+        nb1 = std::min(nb1, c->swap_nb_cap);
+        nb2 = std::min(nb2, c->swap_nb_cap);
+    }
     // weight tiles re-read by a second token tile of the same expert (rows > NB) should
     // survive in L2 between the passes: evict-normal then, evict-first otherwise (r01
     // stack T=575, interleaved: 17.97 / 17.84 ms vs 18.38 / 18.61 ms all-evict-first)
@@ -1175,8 +1215,11 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
     if (const char* v = getenv("MOE_FP8_KB")) c->fp8_kb128 = c->fp8_kb128 && atoi(v) >= 128;
     c->fp8_g2_kb256 = c->fp8_kb128 && c->f_local % 256 == 0;
     if (const char* v = getenv("MOE_FP8_G2_KB")) c->fp8_g2_kb256 = c->fp8_g2_kb256 && atoi(v) == 256;
+    c->fp8x = c->fp8_kb128;
+    if (const char* v = getenv("MOE_FP8_X")) c->fp8x = c->fp8x && atoi(v) != 0;
     if (const char* pt = getenv("MOE_PAIR_TUNE")) c->pair_tune = atoi(pt);
     if (const char* v = getenv("MOE_PAIR_NBLK")) c->pair_nblk = atoi(v) == 1 ? 1 : 2;
+    if (const char* v = getenv("MOE_SWAP_NB_CAP")) c->swap_nb_cap = atoi(v);
     if (const char* v = getenv("MOE_GATHER")) c->gather = atoi(v) != 0;
     if (const char* v = getenv("MOE_G1_SWAP_ROWS")) c->swap_rows_per_expert = atoi(v);
     if (const char* v = getenv("MOE_TAIL_PARTS")) c->tail_parts = atoi(v);
@@ -1235,6 +1278,7 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
     ALLOC(c->offsets, sizeof(int32_t) * 64);
     ALLOC(c->done, sizeof(unsigned int) * 4);
     ALLOC(c->x_perm, sizeof(__nv_bfloat16) * c->cap * c->d);
+    ALLOC(c->tok_scale, sizeof(float) * c->cap);
     ALLOC(c->src_row, sizeof(int32_t) * (c->cap + 512));
     ALLOC(c->tail_ws, sizeof(float) * c->num_sms * 2 * 128 * 128);
     ALLOC(c->tail_cnt, sizeof(int32_t) * c->num_sms);
@@ -1308,6 +1352,8 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
     for (int i = 0; i < 4 && ok; ++i)
         ok = encode_map(&c->tm_x_swap[i], c->x_perm, 2, c->d, c->cap, 1, nbs[i]) &&
              encode_map(&c->tm_h_swap[i], c->h, 2, c->f_local, c->cap, 1, nbs[i]);
+    for (int i = 0; i < 3 && ok && c->fp8x; ++i)
+        ok = encode_map_fp8(&c->tm_x8[i], c->x_perm, c->d, c->cap, 2, nbs[i], 128);
     if (!ok) {
         moe_destroy(c);
         return fail(nullptr, MOE_ERR_CUDA, "cuTensorMapEncodeTiled(workspace) failed");
@@ -1320,6 +1366,7 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
         (as = set_gemm_attr<kG2Swap, 256>(c)) ||
         (as = set_pair_attr<kG1Pair, 1>(c)) || (as = set_pair_attr<kG2Pair, 1>(c)) ||
         (as = set_pair_attr<kG1Pair, 2>(c)) || (as = set_pair_attr<kG2Pair, 2>(c)) ||
+        (as = set_fp8x_attr<32>(c)) || (as = set_fp8x_attr<64>(c)) || (as = set_fp8x_attr<128>(c)) ||
         (as = set_fp8_attr<kG1Swap, 32>(c)) || (as = set_fp8_attr<kG2Swap, 32>(c)) ||
         (as = set_fp8_attr<kG1Swap, 64>(c)) || (as = set_fp8_attr<kG2Swap, 64>(c)) ||
         (as = set_fp8_attr<kG1Swap, 128>(c)) || (as = set_fp8_attr<kG2Swap, 128>(c)) ||
@@ -1350,7 +1397,9 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
             reinterpret_cast<const void*>(moe_gemm_kernel<kG1Swap, 128>), reinterpret_cast<const void*>(moe_gemm_kernel<kG2Swap, 128>),
             reinterpret_cast<const void*>(moe_gemm_kernel<kG2Swap, 256>), reinterpret_cast<const void*>(moe_gemm_pair_kernel<kG1Pair, 1>),
             reinterpret_cast<const void*>(moe_gemm_pair_kernel<kG2Pair, 1>), reinterpret_cast<const void*>(moe_gemm_pair_kernel<kG1Pair, 2>),
-            reinterpret_cast<const void*>(moe_gemm_pair_kernel<kG2Pair, 2>)};
+            reinterpret_cast<const void*>(moe_gemm_pair_kernel<kG2Pair, 2>),
+            reinterpret_cast<const void*>(moe_gemm_fp8x_kernel<32>), reinterpret_cast<const void*>(moe_gemm_fp8x_kernel<64>),
+            reinterpret_cast<const void*>(moe_gemm_fp8x_kernel<128>)};
         for (const void* fn : fns)
             if ((e = cudaFuncGetAttributes(&fa, fn)) != cudaSuccess) return fail_init("cudaFuncGetAttributes", e);
     }
@@ -1366,7 +1415,7 @@ moe_status moe_destroy(moe_ctx* c) {
                     c->x_perm, c->h, c->y, c->stage_in, c->stage_out, c->tp_partial, c->tp_scatter, c->ep_send,
                     c->ep_recv, c->ep_ysend, c->ep_yrecv, c->ep_meta_send, c->ep_meta_recv,
                     c->ep_ridx, c->ep_rpos, c->ep_rw, c->ep_rcounts, c->lb_scratch, c->d_peers, c->src_row,
-                    c->tail_ws, c->tail_cnt};
+                    c->tail_ws, c->tail_cnt, c->tok_scale};
     for (void* p : c->p2p_opened) cudaIpcCloseMemHandle(p);
     if (c->sym) {
         cudaDeviceSynchronize();  // peers' stores into this region have drained (same-process group)

@@ -154,6 +154,29 @@ def test_pair_wide_tiles(moe, T, d, f, E, k):
     assert np.array_equal(outs[0].view(np.int32), outs[1].view(np.int32))
 
 
+@pytest.mark.parametrize("fp8", [False, True])
+@pytest.mark.parametrize("T,d,f,E", [(64, 512, 1024, 8), (300, 256, 512, 8), (100, 256, 512, 2)])
+def test_swap_nb_cap(moe, T, d, f, E, fp8):
+    """Swap-AB token tile capped at 32 (env MOE_SWAP_NB_CAP): experts with more rows run
+    several token tiles (device-side tile count), bf16 and FP8 weights."""
+    shape = synth.MoEShape(T=T, d=d, f=f, E=E, k=2)
+    os.environ["MOE_SWAP_NB_CAP"] = "32"
+    try:
+        if fp8:
+            inp, qs, host = _fp8_inputs(shape, 5000 + T)
+            blk = moe.MoEBlock(inp["wg"], qs["w1"], qs["w3"], qs["w2"], top_k=2, max_tokens=T,
+                               flags=moe.MOE_FLAG_FP8_WEIGHTS)
+        else:
+            inp = _inputs(shape, 5000 + T)
+            host = to_host_inputs(inp)
+            blk = _block(moe, inp, 2, T, moe.MOE_FLAG_FORCE_SWAP)
+    finally:
+        del os.environ["MOE_SWAP_NB_CAP"]
+    run = GpuRun(blk, inp["x"])
+    check_forward(run, host, 2)
+    blk.close()
+
+
 @pytest.mark.parametrize("parts", ["8", "3", "0"])
 @pytest.mark.parametrize("T,d,f,E", [(64, 1024, 2560, 8), (40, 512, 5120, 4), (300, 256, 2560, 8)])
 def test_tail_split(moe, T, d, f, E, parts):
@@ -732,6 +755,43 @@ def test_fp8_weights(moe, T, d, f, E):
     st = check_forward(run, host, 2)
     print("fp8", T, d, f, E, st)
     blk.close()
+
+
+@pytest.mark.parametrize("T", [64, 300])
+def test_fp8_two_term_tokens(moe, T):
+    """FP8 w1/w3 GEMM on kind::f8f6f4 with tokens split into two E4M3 terms (MOE_FP8_X=1,
+    default) vs the fp16-token converter kernels (MOE_FP8_X=0). Rows scaled by 2^3 and
+    2^-10 (exact in bf16) and a zero row exercise the per-row power-of-two token scale
+    and the fp16 h normalisation h * 2^(2s-6): the two-term path must pass the oracle on
+    every row; the converter path (unnormalised fp16 h, which underflows for the 2^-10
+    row) must agree with it far inside the tolerance on the unscaled rows (both multiply
+    exact token values; they differ only in accumulation order and fp16 h roundings)."""
+    shape = synth.MoEShape(T=T, d=512, f=1024, E=8, k=2)
+    inp, qs, host = _fp8_inputs(shape, 900 + T)
+    x = inp["x"].float()
+    x[1] *= 8.0
+    x[2] *= 2.0 ** -10
+    x[3] = 0
+    inp["x"] = x.to(torch.bfloat16)
+    host["x"] = inp["x"].float().cpu().numpy()
+    outs = []
+    for v in ("0", "1"):
+        os.environ["MOE_FP8_X"] = v
+        try:
+            blk = moe.MoEBlock(inp["wg"], qs["w1"], qs["w3"], qs["w2"], top_k=2, max_tokens=T,
+                               flags=moe.MOE_FLAG_FP8_WEIGHTS)
+        finally:
+            del os.environ["MOE_FP8_X"]
+        run = GpuRun(blk, inp["x"])
+        if v == "1":
+            print("fp8x", T, check_forward(run, host, 2))
+        outs.append(run.np("out_f32").astype(np.float64))
+        blk.close()
+    assert np.all(outs[1][3] == 0)
+    a, b = outs[0][4:], outs[1][4:]
+    rms = np.sqrt(np.mean(a ** 2, axis=1, keepdims=True))
+    rel = np.abs(a - b) / rms
+    assert rel.max() < 3e-3, rel.max()
 
 
 def test_fp8_mixtral_decode(moe):
