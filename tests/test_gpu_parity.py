@@ -393,7 +393,7 @@ def _run_group(moe, inp, par, G, shards, k=2, flags=0, max_tokens=None, p2p=Fals
             for it in range(iters):
                 with torch.cuda.stream(st):
                     moe.moe_forward(blocks[r].ctx, x if T else out, T, blocks[r].router_w, blocks[r].w13,
-                                    blocks[r].w2, out, aux, st)
+                                    blocks[r].w2, out, aux, st, blocks[r].s13, blocks[r].s2)
                 st.synchronize()
                 res[r] = (out[:T].clone(), {n: v[:T].clone() for n, v in aux.items()})
                 if first is None:
@@ -435,6 +435,26 @@ def _check_group_outputs(host, k, x_rows, outs, auxs):
     rne = torch.from_numpy(of32).to(torch.bfloat16).float().numpy().astype(np.float64)
     np.testing.assert_array_equal(ob16, rne)
     return e32, e16
+
+
+@pytest.mark.parametrize("par,G", [("ep", 2), ("ep", 4), ("tp", 2), ("ep_exact", 2)])
+def test_fp8_group(moe, par, G):
+    """FP8 weights under expert / tensor parallelism (loopback transport): each rank packs
+    its expert range / ffn slice of the E4M3 weights and scales; the receive-side permute
+    splits tokens into the two E4M3 terms of the kind::f8f6f4 w1/w3 GEMM."""
+    shape = synth.MoEShape(T=96, d=256, f=512, E=8, k=2)
+    inp, qs, host = _fp8_inputs(shape, 70 + G)
+    inp8 = dict(inp, w1=qs["w1"], w3=qs["w3"], w2=qs["w2"])
+    flags = moe.MOE_FLAG_FP8_WEIGHTS | (moe.MOE_FLAG_EP_EXACT if par == "ep_exact" else 0)
+    if par == "tp":
+        res = _run_group(moe, inp8, moe.MOE_PAR_TP, G, [inp["x"]] * G, flags=flags)
+        outs, auxs = [res[0][0]], [res[0][1]]
+    else:
+        cuts = np.linspace(0, shape.T, G + 1).astype(int)
+        shards = [inp["x"][cuts[r]:cuts[r + 1]] for r in range(G)]
+        res = _run_group(moe, inp8, moe.MOE_PAR_EP, G, shards, flags=flags, max_tokens=shape.T)
+        outs, auxs = [r[0] for r in res], [r[1] for r in res]
+    _check_group_outputs(host, 2, host["x"], outs, auxs)
 
 
 @pytest.mark.parametrize("G", [1, 2, 4, 8])
