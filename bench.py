@@ -93,6 +93,9 @@ def parse():
     return ap.parse_args()
 
 
+READ_STREAM_GBS = 7260.0  # measured read-only streaming rate (scripts/exp/read_bw.cu)
+
+
 def load_traffic(config):
     """DRAM bytes per launch of the dominant kernel from the newest committed ncu
     capture (profiles/<round>/traffic.json), or None."""
@@ -548,6 +551,11 @@ def main():
                            else "moe_gemm_kernel<kG1Swap> (w1/w3 + SwiGLU)"),
                 "peak_src": peaks["src"] + " (MEASURED_PEAKS.json hbm_gbs)"}
         step_frac = alg["bytes"] / (ms * 1e-3) / 1e9 / peaks["hbm_gbs"]
+        # context: a read-only stream reaches more than the copy (read+write) peak on this HBM
+        roof["read_stream_peak"] = READ_STREAM_GBS
+        roof["frac_read_stream"] = achieved / READ_STREAM_GBS
+        roof["read_stream_src"] = ("scripts/exp/read_bw.cu, r01: 148 SMs streaming contiguous 16 KB chunks "
+                                   "(the tiled weight layout's TMA boxes)")
     else:
         achieved = alg["g1_flops"] / (dom_ms * 1e-3) / 1e12
         pk = peaks["bf16_tflops_sustained"]
