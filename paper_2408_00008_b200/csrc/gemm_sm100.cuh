@@ -1307,29 +1307,36 @@ __global__ void __launch_bounds__(kFp8Threads, 1)
 // TMEM, ~16 cvt results / clk / SM) capped K3 at ~5 TB/s (ncu r01: converter warps
 // waiting on TMEM A stages; 79 % of the HBM roofline at 1 B/weight).
 // Warps: 0 = TMA producer, 1 = TMEM + MMA issuer, 2..5 = epilogue.
-template <int NB>
+template <int KIND, int NB>
 struct Fp8xCfg {
     static_assert(NB >= 16 && NB <= 128 && NB % 16 == 0, "token tile");
-    static constexpr int kABytes = 256 * 128;   // w1|w3 rows x 128 E4M3 (one 128-byte swizzle row)
-    static constexpr int kBBytes = NB * 128;    // token rows x 128 E4M3, per term (hi, lo)
-    static constexpr int kStageBytes = kABytes + 2 * kBBytes;
+    static_assert(KIND == kG1Swap || KIND == kG2Swap, "decode kinds");
+    // w1|w3 rows (G1) or W2 rows (G2) x 128 E4M3 (one 128-byte swizzle row)
+    static constexpr int kABytes = (KIND == kG1Swap ? 256 : 128) * 128;
+    static constexpr int kTerms = KIND == kG1Swap ? 2 : 3;  // E4M3 terms of the B operand rows
+    static constexpr int kBBytes = NB * 128;    // B rows x 128 E4M3, per term
+    static constexpr int kStageBytes = kABytes + kTerms * kBBytes;
     static constexpr int kStagesRaw = (kSmemBudget - 2048) / kStageBytes;
     static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
     static constexpr int kSmemBytes = kStages * kStageBytes + 2048;
     static_assert(kStages >= 3, "pipeline too shallow");
 };
 
-template <int NB>
+// KIND = kG1Swap: w1/w3 + SwiGLU, B = two-term tokens, row_scale = token scales 2^-t.
+// KIND = kG2Swap: w2 (split-K), B = two-term h (moe_h_split_kernel), row_scale = the
+// per-row factor that undoes both the h split scale and the h normalisation.
+template <int KIND, int NB>
 __global__ void __launch_bounds__(kGemmThreads, 1)
-    moe_gemm_fp8x_kernel(const GemmParams p, const float* __restrict__ scales, const float* __restrict__ tok_scale,
+    moe_gemm_fp8x_kernel(const GemmParams p, const float* __restrict__ scales, const float* __restrict__ row_scale,
                          const __grid_constant__ CUtensorMap tmA8, const __grid_constant__ CUtensorMap tmB8) {
-    using C = Fp8xCfg<NB>;
+    using C = Fp8xCfg<KIND, NB>;
+    constexpr bool kG1 = KIND == kG1Swap;
     constexpr int S = C::kStages;
     constexpr int KB = 128;  // K elements (bytes) per stage
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* smem_a = smem;                  // stage s at s * kABytes
-    uint8_t* smem_b = smem + S * C::kABytes; // stage s: hi at s * 2 * kBBytes, lo at + kBBytes
+    uint8_t* smem_b = smem + S * C::kABytes; // stage s: term j at (s * kTerms + j) * kBBytes
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * C::kStageBytes);
     uint64_t* full = bars;
     uint64_t* empty = bars + S;
@@ -1371,10 +1378,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     int pre = 0;  // producer: weight stages of its first tile already issued
     if (warp == 0 && lane == 0) {
         int total0 = 0;  // warp 0 wrote s_counts itself
-        for (int e = 0; e < p.E; ++e) total0 += tiles_of<kG1Swap, NB>(s_counts[e], p);
+        for (int e = 0; e < p.E; ++e) total0 += tiles_of<KIND, NB>(s_counts[e], p);
         if ((int)blockIdx.x < total0) {
         TileInfo t0;
-        decode_tile<kG1Swap, NB, KB>(blockIdx.x, p, s_counts, s_offsets, t0);
+        decode_tile<KIND, NB, KB>(blockIdx.x, p, s_counts, s_offsets, t0);
         pre = min(S, t0.nkb);
         for (int kb = 0; kb < pre; ++kb) {  // fresh stages: no empty-wait
             ptx::mbar_arrive_expect_tx(&full[kb], C::kStageBytes);
@@ -1389,7 +1396,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     ptx::pdl_wait();
     const uint32_t tmem_base = *tmem_base_slot;
     int total = 0;
-    for (int e = 0; e < p.E; ++e) total += tiles_of<kG1Swap, NB>(s_counts[e], p);
+    for (int e = 0; e < p.E; ++e) total += tiles_of<KIND, NB>(s_counts[e], p);
 
     if (warp == 0) {
         if (lane == 0) {  // ------------------------------------------------ TMA producer
@@ -1398,7 +1405,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             bool first = true;
             for (int t = blockIdx.x; t < total; t += gridDim.x) {
                 TileInfo ti;
-                decode_tile<kG1Swap, NB, KB>(t, p, s_counts, s_offsets, ti);
+                decode_tile<KIND, NB, KB>(t, p, s_counts, s_offsets, ti);
                 for (int kb = 0; kb < ti.nkb; ++kb) {
                     const int kc = (ti.kb0 + kb) * KB;
                     if (!(first && kb < pre)) {
@@ -1407,9 +1414,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                         ptx::tma_load_3d(&tmA8, &full[st], smem_a + st * C::kABytes, kc, ti.a_row, ti.e,
                                          ptx::kEvictFirst);
                     }
-                    uint8_t* b = smem_b + st * 2 * C::kBBytes;
-                    ptx::tma_load_3d(&tmB8, &full[st], b, kc, ti.b_row, 0, ptx::kEvictLast);
-                    ptx::tma_load_3d(&tmB8, &full[st], b + C::kBBytes, kc, ti.b_row, 1, ptx::kEvictLast);
+                    uint8_t* b = smem_b + st * C::kTerms * C::kBBytes;
+#pragma unroll
+                    for (int j = 0; j < C::kTerms; ++j)
+                        ptx::tma_load_3d(&tmB8, &full[st], b + j * C::kBBytes, kc, ti.b_row, j, ptx::kEvictLast);
                     if (++st == S) { st = 0; ph ^= 1; }
                 }
                 first = false;
@@ -1423,7 +1431,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             uint32_t acc_phase = 0;
             for (int t = blockIdx.x; t < total; t += gridDim.x) {
                 TileInfo ti;
-                decode_tile<kG1Swap, NB, KB>(t, p, s_counts, s_offsets, ti);
+                decode_tile<KIND, NB, KB>(t, p, s_counts, s_offsets, ti);
                 const uint32_t n_mma = (uint32_t)((ti.n_valid + 15) / 16 * 16);
                 // D f32 (bit 4), A = B = E4M3 (format 0), K-major, N >> 3 at 17, M >> 4 at 24
                 const uint32_t idesc = (1u << 4) | ((n_mma >> 3) << 17) | ((128u >> 4) << 24);
@@ -1434,16 +1442,16 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                     ptx::mbar_wait(&full[st], ph);
                     ptx::tc_fence_after();
                     const uint64_t a1 = ptx::make_smem_desc_sw128(ptx::smem_u32(smem_a + st * C::kABytes));
-                    const uint64_t a3 = ptx::make_smem_desc_sw128(ptx::smem_u32(smem_a + st * C::kABytes + 16384));
-                    const uint64_t bh = ptx::make_smem_desc_sw128(ptx::smem_u32(smem_b + st * 2 * C::kBBytes));
-                    const uint64_t bl = ptx::make_smem_desc_sw128(ptx::smem_u32(smem_b + st * 2 * C::kBBytes + C::kBBytes));
+                    const uint64_t b0 = ptx::make_smem_desc_sw128(ptx::smem_u32(smem_b + st * C::kTerms * C::kBBytes));
 #pragma unroll
                     for (int kk = 0; kk < KB / 32; ++kk) {  // 32 bytes of K per MMA: +2 in the descriptor
                         const uint32_t init = (kb | kk) ? 1u : 0u;
-                        ptx::mma_e4m3(d_a, a1 + 2 * kk, bh + 2 * kk, idesc, init);
-                        ptx::mma_e4m3(d_a, a1 + 2 * kk, bl + 2 * kk, idesc, 1u);
-                        ptx::mma_e4m3(d_b, a3 + 2 * kk, bh + 2 * kk, idesc, init);
-                        ptx::mma_e4m3(d_b, a3 + 2 * kk, bl + 2 * kk, idesc, 1u);
+#pragma unroll
+                        for (int j = 0; j < C::kTerms; ++j) {  // term j: kBBytes further (>> 4 in the descriptor)
+                            const uint64_t bj = b0 + j * (C::kBBytes >> 4) + 2 * kk;
+                            ptx::mma_e4m3(d_a, a1 + 2 * kk, bj, idesc, j ? 1u : init);
+                            if (kG1) ptx::mma_e4m3(d_b, a1 + (16384 >> 4) + 2 * kk, bj, idesc, j ? 1u : init);
+                        }
                     }
                     ptx::mma_commit(&empty[st]);
                     if (++st == S) { st = 0; ph ^= 1; }
@@ -1460,30 +1468,50 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         uint32_t acc_phase = 0;
         for (int t = blockIdx.x; t < total; t += gridDim.x) {
             TileInfo ti;
-            decode_tile<kG1Swap, NB, KB>(t, p, s_counts, s_offsets, ti);
+            decode_tile<KIND, NB, KB>(t, p, s_counts, s_offsets, ti);
             ptx::mbar_wait(&tmem_full[acc], acc_phase);
             ptx::tc_fence_after();
             const uint32_t tbase = tmem_base + acc * 256 + (static_cast<uint32_t>(q * 32) << 16);
-            const float* sc = scales + (int64_t)ti.e * 2 * p.f + ti.m_idx * 256;
-            const float s1v = sc[r], s3v = sc[128 + r];
-            __half* hp = static_cast<__half*>(p.out) + static_cast<int64_t>(ti.b_row) * p.f + ti.m_idx * 128 + r;
-            const float* ts = tok_scale + ti.b_row;
+            const float* rs = row_scale + ti.b_row;
             const int nchunks = (ti.n_valid + 15) / 16;
+            if (kG1) {
+                const float* sc = scales + (int64_t)ti.e * 2 * p.f + ti.m_idx * 256;
+                const float s1v = sc[r], s3v = sc[128 + r];
+                __half* hp = static_cast<__half*>(p.out) + static_cast<int64_t>(ti.b_row) * p.f + ti.m_idx * 128 + r;
 #pragma unroll 1
-            for (int cc = 0; cc < nchunks; ++cc) {
-                uint32_t a[16], b[16];
-                ptx::tmem_ld16(tbase + cc * 16, a);
-                ptx::tmem_ld16(tbase + 128 + cc * 16, b);
-                ptx::tmem_wait_ld();
+                for (int cc = 0; cc < nchunks; ++cc) {
+                    uint32_t a[16], b[16];
+                    ptx::tmem_ld16(tbase + cc * 16, a);
+                    ptx::tmem_ld16(tbase + 128 + cc * 16, b);
+                    ptx::tmem_wait_ld();
 #pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                    const int n = cc * 16 + i;
-                    if (n < ti.n_valid) {
-                        const float tsn = ts[n];
-                        const float hv = silu_f32(__uint_as_float(a[i]) * (s1v * tsn)) *
-                                         (__uint_as_float(b[i]) * (s3v * tsn));
-                        // fp16 h normalised by the token scale: h * 2^(2s - 6) (see GemmParams)
-                        hp[static_cast<int64_t>(n) * p.f] = __float2half_rn(hv * (0.015625f / (tsn * tsn)));
+                    for (int i = 0; i < 16; ++i) {
+                        const int n = cc * 16 + i;
+                        if (n < ti.n_valid) {
+                            const float tsn = rs[n];
+                            const float hv = silu_f32(__uint_as_float(a[i]) * (s1v * tsn)) *
+                                             (__uint_as_float(b[i]) * (s3v * tsn));
+                            // fp16 h normalised by the token scale: h * 2^(2s - 6) (see GemmParams)
+                            hp[static_cast<int64_t>(n) * p.f] = __float2half_rn(hv * (0.015625f / (tsn * tsn)));
+                        }
+                    }
+                }
+            } else {
+                const int drow = ti.m_idx * 128 + r;
+                const float s2v = drow < p.d ? scales[(int64_t)ti.e * p.d + drow] : 0.f;
+                float* y = static_cast<float*>(p.out) + p.out_split_stride * ti.split +
+                           static_cast<int64_t>(ti.b_row) * p.d + drow;
+#pragma unroll 1
+                for (int cc = 0; cc < nchunks; ++cc) {
+                    uint32_t v[16];
+                    ptx::tmem_ld16(tbase + cc * 16, v);
+                    ptx::tmem_wait_ld();
+                    if (drow < p.d) {
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) {
+                            const int n = cc * 16 + i;
+                            if (n < ti.n_valid) y[static_cast<int64_t>(n) * p.d] = __uint_as_float(v[i]) * (s2v * rs[n]);
+                        }
                     }
                 }
             }

@@ -246,6 +246,11 @@ struct moe_ctx {
     // needs d % 128 == 0; env MOE_FP8_X=0 selects the fp16-converter kernels
     bool fp8x = false;
     float* tok_scale = nullptr;   // [cap] 2^-s of each permuted row (fp8x)
+    uint8_t* h8 = nullptr;        // [3][cap][f_local] E4M3 terms of h for the fp8x w2 GEMM
+    float* h_factor = nullptr;    // [cap] per-row output factor of the fp8x w2 GEMM
+    CUtensorMap tm_h8[3]{};       // h8 planes, box {128, NB}, NB = 32, 64, 128
+    int64_t rows_needed_cur = 0;  // permuted rows (incl. segment padding) of the current forward
+    bool fp8_w2_x = false;        // fp8x w2 GEMM (env MOE_FP8_W2_X=0: fp16-converter w2 kernel)
     CUtensorMap tm_x8[3]{};       // x_perm as [2][cap][d] E4M3 planes, box {128, NB}, NB = 32, 64, 128
     // workspace (device)
     int32_t *topk_idx = nullptr, *pos = nullptr, *blockcount = nullptr, *blockoff = nullptr;
@@ -416,8 +421,10 @@ moe_status set_fp8_attr(moe_ctx* c) {
 
 template <int NB>
 moe_status set_fp8x_attr(moe_ctx* c) {
-    CUDA_TRY(c, cudaFuncSetAttribute(moe_gemm_fp8x_kernel<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     Fp8xCfg<NB>::kSmemBytes));
+    CUDA_TRY(c, cudaFuncSetAttribute(moe_gemm_fp8x_kernel<kG1Swap, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     Fp8xCfg<kG1Swap, NB>::kSmemBytes));
+    CUDA_TRY(c, cudaFuncSetAttribute(moe_gemm_fp8x_kernel<kG2Swap, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     Fp8xCfg<kG2Swap, NB>::kSmemBytes));
     return MOE_OK;
 }
 
@@ -624,8 +631,8 @@ moe_status run_swap_g1(moe_ctx* c, int nbi, const moe_expert_weights* w, cudaStr
     }
     if constexpr (NB <= 128)
         if (c->fp8 && c->fp8x)
-            return launch(c, kSlotGemm1, moe_gemm_fp8x_kernel<NB>, dim3(c->num_sms), dim3(kGemmThreads),
-                          (size_t)Fp8xCfg<NB>::kSmemBytes, st, p1, static_cast<const float*>(w->w13_scale),
+            return launch(c, kSlotGemm1, moe_gemm_fp8x_kernel<kG1Swap, NB>, dim3(c->num_sms), dim3(kGemmThreads),
+                          (size_t)Fp8xCfg<kG1Swap, NB>::kSmemBytes, st, p1, static_cast<const float*>(w->w13_scale),
                           static_cast<const float*>(c->tok_scale), c->tm_w13, c->tm_x8[nbi]);
     if constexpr (NB <= 64)
         if (c->fp8 && !c->fp8_smem_a)
@@ -645,6 +652,33 @@ moe_status run_swap_g2(moe_ctx* c, int nbi, const moe_expert_weights* w, int spl
     p2.w_tr = 128;
     p2.w_nt = c->w2_nt;
     if (c->fp8 && c->fp8x) p2.tok_scale = c->tok_scale;  // undo the fp8x epilogue's h normalisation
+    if constexpr (NB <= 128)
+        if (c->fp8 && c->fp8x && c->fp8_w2_x) {
+            // h -> three E4M3 terms + per-row factor, then the w2 GEMM on kind::f8f6f4; both
+            // launches are timed as the w2 GEMM slot
+            cudaEvent_t ea = nullptr, eb = nullptr;
+            const bool prof = c->profiling;
+            if (prof) {
+                ea = take_event(c);
+                eb = take_event(c);
+                cudaEventRecord(ea, st);
+                c->profiling = false;
+            }
+            HSplitParams hp{static_cast<const __half*>(static_cast<const void*>(c->h)), c->counts, c->offsets,
+                            c->tok_scale, c->h8, c->h_factor, c->cap, c->E_local, c->f_local};
+            moe_status s = launch(c, kSlotGemm2, moe_h_split_kernel, dim3((unsigned)std::max<int64_t>(1, c->rows_needed_cur)),
+                                  dim3(256), 0, st, hp);
+            if (!s)
+                s = launch(c, kSlotGemm2, moe_gemm_fp8x_kernel<kG2Swap, NB>, dim3(c->num_sms), dim3(kGemmThreads),
+                           (size_t)Fp8xCfg<kG2Swap, NB>::kSmemBytes, st, p2, static_cast<const float*>(w->w2_scale),
+                           static_cast<const float*>(c->h_factor), c->tm_w2_swap, c->tm_h8[nbi]);
+            if (prof) {
+                c->profiling = true;
+                cudaEventRecord(eb, st);
+                c->pending.push_back({kSlotGemm2, ea, eb});
+            }
+            return s;
+        }
     if constexpr (NB <= 64)
         if (c->fp8 && !c->fp8_smem_a)
             return launch_gemm_fp8t<kG2Swap, NB>(c, kSlotGemm2, p2, w->w2_scale, c->tm_w2_swap, c->tm_h_swap[nbi],
@@ -840,6 +874,7 @@ moe_status run_gemms(moe_ctx* c, GemmPaths gp, int64_t rows_bound, int64_t rows_
         splits = (int)std::max<int64_t>(1, std::min<int64_t>(splits, c->y_elems / (rows_needed * c->d)));
         splits = std::min(splits, c->f_local / (c->fp8_g2_kb256 ? 256 : c->fp8_kb128 ? 128 : kBK));  // >= 1 K block per split
         c->split_stride = rows_needed * c->d;
+        c->rows_needed_cur = std::min<int64_t>(rows_needed, c->cap);
         if (nb2 == 32) s = run_swap_g2<32>(c, 0, &c->cur_w, splits, st);
         else if (nb2 == 64) s = run_swap_g2<64>(c, 1, &c->cur_w, splits, st);
         else if (nb2 == 128) s = run_swap_g2<128>(c, 2, &c->cur_w, splits, st);
@@ -1217,6 +1252,12 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
     if (const char* v = getenv("MOE_FP8_G2_KB")) c->fp8_g2_kb256 = c->fp8_g2_kb256 && atoi(v) == 256;
     c->fp8x = c->fp8_kb128;
     if (const char* v = getenv("MOE_FP8_X")) c->fp8x = c->fp8x && atoi(v) != 0;
+    // fp8x w2 GEMM: off by default. r01 (64-token decode, interleaved A/B): 0.3062 vs
+    // 0.2708 ms per step -- the h split kernel costs 9.5 us and the w2 GEMM on row-major
+    // E4M3 W2 with 128-byte K blocks streams at ~4 TB/s (122 us) against the converter
+    // kernel's 95 us with 256-byte K blocks. Env MOE_FP8_W2_X=1 enables it (tested).
+    c->fp8_w2_x = false;
+    if (const char* v = getenv("MOE_FP8_W2_X")) c->fp8_w2_x = c->fp8x && atoi(v) != 0;
     if (const char* pt = getenv("MOE_PAIR_TUNE")) c->pair_tune = atoi(pt);
     if (const char* v = getenv("MOE_PAIR_NBLK")) c->pair_nblk = atoi(v) == 1 ? 1 : 2;
     if (const char* v = getenv("MOE_SWAP_NB_CAP")) c->swap_nb_cap = atoi(v);
@@ -1279,6 +1320,10 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
     ALLOC(c->done, sizeof(unsigned int) * 4);
     ALLOC(c->x_perm, sizeof(__nv_bfloat16) * c->cap * c->d);
     ALLOC(c->tok_scale, sizeof(float) * c->cap);
+    if (c->fp8_w2_x) {
+        ALLOC(c->h8, (size_t)3 * c->cap * c->f_local);
+        ALLOC(c->h_factor, sizeof(float) * c->cap);
+    }
     ALLOC(c->src_row, sizeof(int32_t) * (c->cap + 512));
     ALLOC(c->tail_ws, sizeof(float) * c->num_sms * 2 * 128 * 128);
     ALLOC(c->tail_cnt, sizeof(int32_t) * c->num_sms);
@@ -1353,7 +1398,8 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
         ok = encode_map(&c->tm_x_swap[i], c->x_perm, 2, c->d, c->cap, 1, nbs[i]) &&
              encode_map(&c->tm_h_swap[i], c->h, 2, c->f_local, c->cap, 1, nbs[i]);
     for (int i = 0; i < 3 && ok && c->fp8x; ++i)
-        ok = encode_map_fp8(&c->tm_x8[i], c->x_perm, c->d, c->cap, 2, nbs[i], 128);
+        ok = encode_map_fp8(&c->tm_x8[i], c->x_perm, c->d, c->cap, 2, nbs[i], 128) &&
+             (!c->fp8_w2_x || encode_map_fp8(&c->tm_h8[i], c->h8, c->f_local, c->cap, 3, nbs[i], 128));
     if (!ok) {
         moe_destroy(c);
         return fail(nullptr, MOE_ERR_CUDA, "cuTensorMapEncodeTiled(workspace) failed");
@@ -1398,8 +1444,13 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
             reinterpret_cast<const void*>(moe_gemm_kernel<kG2Swap, 256>), reinterpret_cast<const void*>(moe_gemm_pair_kernel<kG1Pair, 1>),
             reinterpret_cast<const void*>(moe_gemm_pair_kernel<kG2Pair, 1>), reinterpret_cast<const void*>(moe_gemm_pair_kernel<kG1Pair, 2>),
             reinterpret_cast<const void*>(moe_gemm_pair_kernel<kG2Pair, 2>),
-            reinterpret_cast<const void*>(moe_gemm_fp8x_kernel<32>), reinterpret_cast<const void*>(moe_gemm_fp8x_kernel<64>),
-            reinterpret_cast<const void*>(moe_gemm_fp8x_kernel<128>)};
+            reinterpret_cast<const void*>(moe_gemm_fp8x_kernel<kG1Swap, 32>),
+            reinterpret_cast<const void*>(moe_gemm_fp8x_kernel<kG1Swap, 64>),
+            reinterpret_cast<const void*>(moe_gemm_fp8x_kernel<kG1Swap, 128>),
+            reinterpret_cast<const void*>(moe_gemm_fp8x_kernel<kG2Swap, 32>),
+            reinterpret_cast<const void*>(moe_gemm_fp8x_kernel<kG2Swap, 64>),
+            reinterpret_cast<const void*>(moe_gemm_fp8x_kernel<kG2Swap, 128>),
+            reinterpret_cast<const void*>(moe_h_split_kernel)};
         for (const void* fn : fns)
             if ((e = cudaFuncGetAttributes(&fa, fn)) != cudaSuccess) return fail_init("cudaFuncGetAttributes", e);
     }
@@ -1415,7 +1466,7 @@ moe_status moe_destroy(moe_ctx* c) {
                     c->x_perm, c->h, c->y, c->stage_in, c->stage_out, c->tp_partial, c->tp_scatter, c->ep_send,
                     c->ep_recv, c->ep_ysend, c->ep_yrecv, c->ep_meta_send, c->ep_meta_recv,
                     c->ep_ridx, c->ep_rpos, c->ep_rw, c->ep_rcounts, c->lb_scratch, c->d_peers, c->src_row,
-                    c->tail_ws, c->tail_cnt, c->tok_scale};
+                    c->tail_ws, c->tail_cnt, c->tok_scale, c->h8, c->h_factor};
     for (void* p : c->p2p_opened) cudaIpcCloseMemHandle(p);
     if (c->sym) {
         cudaDeviceSynchronize();  // peers' stores into this region have drained (same-process group)

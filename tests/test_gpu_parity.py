@@ -814,6 +814,22 @@ def test_fp8_two_term_tokens(moe, T):
     assert rel.max() < 3e-3, rel.max()
 
 
+@pytest.mark.parametrize("T,d,f,E", [(64, 512, 1024, 8), (300, 256, 512, 8), (7, 128, 256, 2)])
+def test_fp8_w2_three_term(moe, T, d, f, E):
+    """Optional FP8 w2 GEMM on kind::f8f6f4 (env MOE_FP8_W2_X=1): h split into three E4M3
+    terms per row (exact for fp16 h above ~1 % of the row max) by moe_h_split_kernel."""
+    inp, qs, host = _fp8_inputs(synth.MoEShape(T=T, d=d, f=f, E=E, k=2), 1100 + T)
+    os.environ["MOE_FP8_W2_X"] = "1"
+    try:
+        blk = moe.MoEBlock(inp["wg"], qs["w1"], qs["w3"], qs["w2"], top_k=2, max_tokens=T,
+                           flags=moe.MOE_FLAG_FP8_WEIGHTS)
+    finally:
+        del os.environ["MOE_FP8_W2_X"]
+    run = GpuRun(blk, inp["x"])
+    check_forward(run, host, 2)
+    blk.close()
+
+
 def test_fp8_mixtral_decode(moe):
     """64-token decode at Mixtral size with FP8 weights, all tokens vs the oracle."""
     w = synth.make_weights(4096, 14336, 8, seed=43, device="cuda")
