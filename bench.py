@@ -547,7 +547,7 @@ def main():
         achieved = alg["g1_bytes"] / (dom_ms * 1e-3) / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": achieved / peaks["hbm_gbs"], "traffic": None,
-                "kernel": ("moe_gemm_fp8t_kernel<kG1Swap> (FP8 w1/w3 + SwiGLU)" if args.fp8
+                "kernel": ("moe_gemm_fp8x_kernel<kG1Swap> (FP8 w1/w3 + SwiGLU, kind::f8f6f4)" if args.fp8
                            else "moe_gemm_kernel<kG1Swap> (w1/w3 + SwiGLU)"),
                 "peak_src": peaks["src"] + " (MEASURED_PEAKS.json hbm_gbs)"}
         step_frac = alg["bytes"] / (ms * 1e-3) / 1e9 / peaks["hbm_gbs"]
