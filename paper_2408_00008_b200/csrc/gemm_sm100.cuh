@@ -704,6 +704,11 @@ __device__ __forceinline__ void pair_decode(int t, const GemmParams& p, const in
 // Weight prefetch before the PDL wait in the CTA-pair kernels: measured WORSE (r01
 // prefill, interleaved: 19.6 / 20.1 / 19.9 ms with vs 18.8 / 19.0 / 18.9 ms without;
 // the 32-layer stack with the w2 GEMM on pairs stayed slower than swap-AB), so off.
+// Pair epilogue drain: 1 = software-pipelined TMEM loads + early release of each TMEM
+// half (MOE_PAIR_EPI_PIPE=0: one load-wait-math round trip per 16 columns)
+#ifndef MOE_PAIR_EPI_PIPE
+#define MOE_PAIR_EPI_PIPE 1
+#endif
 #ifndef MOE_PAIR_PDL_PREFETCH
 #define MOE_PAIR_PDL_PREFETCH 0
 #endif
@@ -929,6 +934,91 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 const int blk = ti.n_idx * NBLK + j;  // 256-column weight block
                 const uint32_t tbase = tmem_base + (NBLK == 1 ? acc : j) * 256 + (static_cast<uint32_t>(q * 32) << 16);
                 if (j < ti.n_valid) {
+#if MOE_PAIR_EPI_PIPE
+                    // software-pipelined drain: the TMEM loads of chunk ch+1 are issued before the
+                    // math of chunk ch (one tcgen05.wait::ld per chunk covers them), and the half is
+                    // released right after its last load lands, before the last chunk's math/stores
+                    if (KIND == kG1Pair) {
+                        uint32_t a[2][32], b[2][32];  // 32 h columns per chunk, double-buffered
+                        ptx::tmem_ld32(tbase, a[0]);
+                        ptx::tmem_ld32(tbase + 128, b[0]);
+#pragma unroll
+                        for (int ch = 0; ch < 4; ++ch) {
+                            const int cb = ch & 1;
+                            ptx::tmem_wait_ld();
+                            if (ch + 1 < 4) {
+                                const uint32_t tc = tbase + (ch + 1) * 32;
+                                ptx::tmem_ld32(tc, a[cb ^ 1]);
+                                ptx::tmem_ld32(tc + 128, b[cb ^ 1]);
+                            } else if (NBLK == 2) {  // all of this half is in registers: release it
+                                ptx::tc_fence_before();
+                                __syncwarp();
+                                if (lane == 0) ptx::mbar_arrive_cluster(j == 0 ? leader_empty0 : leader_empty1);
+                            }
+                            const uint32_t ob = obase + obuf * 4096 + row_off;
+                            if ((ch & 1) == 0) {
+                                if (lane == 0) ptx::bulk_wait_read<1>();  // this buffer's previous box was read
+                                __syncwarp();
+                            }
+                            uint32_t o[16];
+#pragma unroll
+                            for (int i = 0; i < 16; ++i) {
+                                const float h0 = silu_f32(__uint_as_float(a[cb][2 * i])) * __uint_as_float(b[cb][2 * i]);
+                                const float h1 =
+                                    silu_f32(__uint_as_float(a[cb][2 * i + 1])) * __uint_as_float(b[cb][2 * i + 1]);
+                                o[i] = pack_bf16x2(h0, h1);
+                            }
+                            const int c0 = (ch & 1) * 4;  // 16-byte chunk of the 128-byte box row
+#pragma unroll
+                            for (int i = 0; i < 4; ++i)
+                                ptx::sts128(ob + (((c0 + i) ^ sw) << 4), o[4 * i], o[4 * i + 1], o[4 * i + 2], o[4 * i + 3]);
+                            if (ch & 1) {
+                                ptx::fence_proxy_async();
+                                __syncwarp();
+                                if (lane == 0 && store) {
+                                    ptx::tma_store_2d(&tmOut, smem_out + q * 8192 + obuf * 4096, blk * 128 + (ch >> 1) * 64,
+                                                      grow);
+                                    ptx::bulk_commit();
+                                }
+                                obuf ^= 1;
+                            }
+                        }
+                    } else {
+                        const int nbox = min(256, p.d - blk * 256) / 32;  // 32 fp32 columns per box (>= 2)
+                        uint32_t v0[32], v1[32];
+                        ptx::tmem_ld32(tbase, v0);
+                        // one box: wait for its loads, issue the next box's into the other buffer
+                        // (or release the half after the last), stage it in smem, TMA-store it
+                        auto box = [&](int c, uint32_t(&cur)[32], uint32_t(&nxt)[32]) {
+                            ptx::tmem_wait_ld();
+                            if (c + 1 < nbox) {
+                                ptx::tmem_ld32(tbase + (c + 1) * 32, nxt);
+                            } else if (NBLK == 2) {
+                                ptx::tc_fence_before();
+                                __syncwarp();
+                                if (lane == 0) ptx::mbar_arrive_cluster(j == 0 ? leader_empty0 : leader_empty1);
+                            }
+                            const uint32_t ob = obase + obuf * 4096 + row_off;
+                            if (lane == 0) ptx::bulk_wait_read<1>();
+                            __syncwarp();
+#pragma unroll
+                            for (int i = 0; i < 8; ++i)
+                                ptx::sts128(ob + ((i ^ sw) << 4), cur[4 * i], cur[4 * i + 1], cur[4 * i + 2], cur[4 * i + 3]);
+                            ptx::fence_proxy_async();
+                            __syncwarp();
+                            if (lane == 0 && store) {
+                                ptx::tma_store_2d(&tmOut, smem_out + q * 8192 + obuf * 4096, blk * 256 + c * 32, grow);
+                                ptx::bulk_commit();
+                            }
+                            obuf ^= 1;
+                        };
+#pragma unroll 1
+                        for (int c = 0; c < nbox; c += 2) {
+                            box(c, v0, v1);
+                            if (c + 1 < nbox) box(c + 1, v1, v0);
+                        }
+                    }
+#else
                     if (KIND == kG1Pair) {
 #pragma unroll 1
                         for (int c2 = 0; c2 < 2; ++c2) {  // 64 h columns per box
@@ -984,8 +1074,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                             obuf ^= 1;
                         }
                     }
+#endif
                 }
-                if (NBLK == 2) {  // this TMEM half is free for the next tile's MMAs
+                // this TMEM half is free for the next tile's MMAs (the pipelined drain arrived
+                // already after its last TMEM load, unless the half held no block)
+                if (NBLK == 2 && (!MOE_PAIR_EPI_PIPE || j >= ti.n_valid)) {
                     ptx::tc_fence_before();
                     __syncwarp();
                     if (lane == 0) ptx::mbar_arrive_cluster(j == 0 ? leader_empty0 : leader_empty1);
