@@ -90,8 +90,13 @@ typedef enum {
 #define MOE_FLAG_NO_PDL      0x8u /* disable programmatic dependent launch               */
 #define MOE_FLAG_NO_PAIR     0x10u /* prefill GEMMs on single CTAs (M=128) instead of CTA pairs (M=256) */
 #define MOE_FLAG_FP8_WEIGHTS 0x40u /* expert weights are FP8 E4M3 with per-row power-of-two scales
-                                      (moe_pack_weights_fp8); tokens / activations on the GEMMs are
-                                      fp16; decode (swap-AB) GEMMs at any T */
+                                      (moe_pack_weights_fp8); decode (swap-AB) GEMMs at any T
+                                      (SURVEY 8(f) NEXT #2). hidden % 128 == 0 and ffn slice
+                                      % 128 == 0: the w1/w3 GEMM runs 8-bit MMAs on tokens split
+                                      into two E4M3 terms (hi + lo == the bf16 token exactly above
+                                      ~1e-3 of its row max) and stores h in fp16 scaled by the
+                                      token scale; otherwise tokens enter as fp16. The w2 GEMM
+                                      widens the weights to fp16 (R15)                  */
 #define MOE_FLAG_EP_EXACT    0x20u /* EP: always exchange exact row counts (one host sync per forward);
                                       default: exact only when a fixed-capacity exchange would move
                                       more than 32 MB, i.e. prefill-sized batches                  */
