@@ -242,6 +242,9 @@ struct moe_ctx {
     // with two accumulators; env MOE_PAIR_NBLK. G2 band counts wide tiles when 2.
     int pair_nblk = 2;
     int swap_nb_cap = 0;      // env MOE_SWAP_NB_CAP (see run_gemms)
+    // env MOE_ROUTER_CC: CUDA-core router (2 tokens / block, 32 blocks at T = 64) for T <= this.
+    // r01 64-token decode, interleaved: 0.4335 vs 0.4312 ms with the mma.sync router (4 blocks)
+    int router_cc_max_T = 0;
     // FP8 w1/w3 GEMM on kind::f8f6f4 with two-term E4M3 tokens (moe_gemm_fp8x_kernel);
     // needs d % 128 == 0; env MOE_FP8_X=0 selects the fp16-converter kernels
     bool fp8x = false;
@@ -720,7 +723,7 @@ moe_status route_and_permute(moe_ctx* c, const RouteSpec& r, cudaStream_t st) {
     // per block with K split over 8 warps for small batches (latency), 128 tokens
     // per block for large ones (throughput). Routed mode / E > 8 -> CUDA-core
     // router, 2 tokens per block.
-    const bool mma = r.in_idx == nullptr && c->E <= 8;
+    const bool mma = r.in_idx == nullptr && c->E <= 8 && r.T > c->router_cc_max_T;
     const int KS = r.T >= 2048 ? 1 : 8;
     const int TB = mma ? 16 * (8 / KS) : 2;
     const int nblk = (r.T + TB - 1) / TB;
@@ -1261,6 +1264,7 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
     if (const char* pt = getenv("MOE_PAIR_TUNE")) c->pair_tune = atoi(pt);
     if (const char* v = getenv("MOE_PAIR_NBLK")) c->pair_nblk = atoi(v) == 1 ? 1 : 2;
     if (const char* v = getenv("MOE_SWAP_NB_CAP")) c->swap_nb_cap = atoi(v);
+    if (const char* v = getenv("MOE_ROUTER_CC")) c->router_cc_max_T = atoi(v);
     if (const char* v = getenv("MOE_GATHER")) c->gather = atoi(v) != 0;
     if (const char* v = getenv("MOE_G1_SWAP_ROWS")) c->swap_rows_per_expert = atoi(v);
     if (const char* v = getenv("MOE_TAIL_PARTS")) c->tail_parts = atoi(v);
