@@ -69,6 +69,12 @@ __device__ __forceinline__ void bf16x8_to_f32(const uint4& v, float (&f)[8]) {
 // then the last block to finish runs the exclusive scan over blocks (one block,
 // fixed order: deterministic; classic threadfence-reduction handshake):
 //   blockoff[b][key], counts[key], offsets[key] (segments padded to seg_align).
+// Kept small on purpose: every loop over keys / warps / blocks runs with a runtime
+// trip count and is not unrolled. The earlier form held 32-entry per-key register
+// arrays with fully unrolled key loops (~6.7k SASS instructions per router kernel)
+// and cost ~15 us per launch at decode even for T = 1 -- fixed cost of cold
+// instruction fetch, since the 2.8 GB weight stream evicts the kernel's code from
+// L2 every step (scripts/exp/router_lat.py).
 template <int NTHREADS>
 __device__ __forceinline__ void route_block_finish(const RouteParams& p, const int32_t (*s_idx)[2], int ntok,
                                                    int tok0) {
@@ -76,7 +82,6 @@ __device__ __forceinline__ void route_block_finish(const RouteParams& p, const i
     __shared__ int s_last;
     __shared__ int32_t s_wk[NW][32];    // per-warp assignment count of every key
     __shared__ int32_t s_tot[32];
-    __shared__ int32_t s_base[NW][32];  // scan: per-warp partial sums of every key
     const int NK = p.nkeys;
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     // thread i <-> assignment i = (token i / k, slot i % k); NTHREADS >= TB * k
@@ -88,16 +93,16 @@ __device__ __forceinline__ void route_block_finish(const RouteParams& p, const i
         if (p.k > 1 && (i % p.k) == 1 && e >= 0 && e == s_idx[i / p.k][0]) __trap();  // duplicate expert
         key = e >= 0 ? hist_key(e, p.key_lo, p.key_div, NK) : -1;
     }
-    const uint32_t lt = (1u << lane) - 1u;
-    int32_t lrank = 0;
-    for (int e = 0; e < NK; ++e) {
-        const uint32_t m = __ballot_sync(0xffffffffu, key == e);
-        if (key == e) lrank = __popc(m & lt);
-        if (lane == 0) s_wk[warp][e] = __popc(m);
-    }
+    for (int j = threadIdx.x; j < NW * 32; j += NTHREADS) (&s_wk[0][0])[j] = 0;
+    __syncthreads();
+    // lanes with the same key: stable in-warp rank and the warp's count of that key
+    const uint32_t same = __match_any_sync(0xffffffffu, key);
+    const int32_t lrank = __popc(same & ((1u << lane) - 1u));
+    if (key >= 0 && lrank == 0) s_wk[warp][key] = __popc(same);
     __syncthreads();
     if (key >= 0) {
         int32_t r = lrank;
+#pragma unroll 1
         for (int w = 0; w < warp; ++w) r += s_wk[w][key];
         p.rank[(int64_t)tok0 * p.k + i] = r;
     } else if (valid) {
@@ -105,6 +110,7 @@ __device__ __forceinline__ void route_block_finish(const RouteParams& p, const i
     }
     if (threadIdx.x < NK) {
         int32_t cnt = 0;
+#pragma unroll 1
         for (int w = 0; w < NW; ++w) cnt += s_wk[w][threadIdx.x];
         p.blockcount[(int64_t)blockIdx.x * NK + threadIdx.x] = cnt;
     }
@@ -114,53 +120,44 @@ __device__ __forceinline__ void route_block_finish(const RouteParams& p, const i
     __syncthreads();
     if (!s_last) return;
     __threadfence();
-    // Exclusive scan over blocks for every key. Thread t owns the contiguous run of
-    // blocks [t*per, (t+1)*per): pass 1 sums the run for all keys (independent
-    // loads, in flight together), a block-wide scan in shared memory gives each
-    // run's base, pass 2 writes the per-block offsets. Fixed order: deterministic.
+    // Exclusive scan over blocks, all keys at once: a group of R lanes (R = 32 / KP,
+    // KP = keys per warp, a power of two) owns one key; lane g of the group owns the
+    // contiguous run of blocks [g*per, (g+1)*per). Pass 1 sums the run (independent
+    // loads), a shuffle scan inside the group gives each run's base, pass 2 writes the
+    // per-block offsets. Fixed order: deterministic.
+    int KP = 1;  // keys per warp: the smallest power of two with KP * NW >= NK
+    while (KP * NW < NK && KP < 32) KP <<= 1;
+    const int R = 32 / KP;                                   // lanes per key
+    const int my_key = warp * KP + lane / R, g = lane % R;
     const int nblk = gridDim.x;
-    const int per = (nblk + NTHREADS - 1) / NTHREADS;
-    const int b0 = min(nblk, threadIdx.x * per), b1 = min(nblk, b0 + per);
-    int32_t sum[32];
-#pragma unroll
-    for (int e = 0; e < 32; ++e) sum[e] = 0;
-    for (int bb = b0; bb < b1; ++bb)
-#pragma unroll
-        for (int e = 0; e < 32; ++e)
-            if (e < NK) sum[e] += __ldcg(&p.blockcount[(int64_t)bb * NK + e]);
-    int32_t excl[32];
-#pragma unroll
-    for (int e = 0; e < 32; ++e) {
-        if (e >= NK) break;
-        int32_t inc = sum[e];
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int32_t u = __shfl_up_sync(0xffffffffu, inc, o);
-            if (lane >= o) inc += u;
+    const int per = (nblk + R - 1) / R;
+    const int b0 = min(nblk, g * per), b1 = min(nblk, b0 + per);
+    const bool own = my_key < NK;
+    int32_t sum = 0;
+    if (own) {
+#pragma unroll 4
+        for (int bb = b0; bb < b1; ++bb) sum += __ldcg(&p.blockcount[(int64_t)bb * NK + my_key]);
+    }
+    int32_t inc = sum;
+#pragma unroll 1
+    for (int o = 1; o < R; o <<= 1) {
+        const int32_t u = __shfl_up_sync(0xffffffffu, inc, o, R);
+        if (g >= o) inc += u;
+    }
+    if (own) {
+        int32_t ex = inc - sum;
+#pragma unroll 1
+        for (int bb = b0; bb < b1; ++bb) {
+            p.blockoff[(int64_t)bb * NK + my_key] = ex;
+            ex += __ldcg(&p.blockcount[(int64_t)bb * NK + my_key]);
         }
-        excl[e] = inc - sum[e];
-        if (lane == 31) s_base[warp][e] = inc;
+        if (g == R - 1) s_tot[my_key] = inc;
     }
-    __syncthreads();
-#pragma unroll
-    for (int e = 0; e < 32; ++e) {
-        if (e >= NK) break;
-        int32_t base = 0;
-        for (int w = 0; w < warp; ++w) base += s_base[w][e];
-        excl[e] += base;
-        if (threadIdx.x == NTHREADS - 1) s_tot[e] = excl[e] + sum[e];
-    }
-    for (int bb = b0; bb < b1; ++bb)
-#pragma unroll
-        for (int e = 0; e < 32; ++e)
-            if (e < NK) {
-                p.blockoff[(int64_t)bb * NK + e] = excl[e];
-                excl[e] += __ldcg(&p.blockcount[(int64_t)bb * NK + e]);
-            }
     __syncthreads();
     if (threadIdx.x == 0) {
         int32_t off = 0;
         p.offsets[0] = 0;
+#pragma unroll 1
         for (int e = 0; e < NK; ++e) {
             p.counts[e] = s_tot[e];
             off += (s_tot[e] + p.seg_align - 1) / p.seg_align * p.seg_align;
