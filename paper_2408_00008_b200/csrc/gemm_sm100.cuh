@@ -63,6 +63,13 @@ struct GemmParams {
     // range for any token scale: h grows ~quadratically with the token), so y is scaled
     // back by 2^(6 - 2s) -- powers of two, exact.
     const float* tok_scale;
+    // kG1Swap speculative L2 prefetch (moe.cu spec_l2): K blocks of this CTA's first
+    // weight tile to prefetch into L2 BEFORE the routing is known, assuming every
+    // expert holds 1..NB rows (one token tile each: unit u = expert u / (f/128), weight
+    // tile u % (f/128)). A wrong guess only wastes the prefetch. 0 = off; when set, the
+    // kernel reads counts / offsets after griddepcontrol.wait (it may launch before the
+    // router has finished).
+    int32_t spec_l2;
 };
 
 // 4D coordinates of rows [row, row + box) of expert e at K offset kc in a tiled weight map
@@ -309,7 +316,19 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     // dependents after its own griddepcontrol.wait, and the w1/w3 GEMM after its
     // wait) -- and their producer issues the first weight stages before waiting for
     // the permuted tokens / activations of the previous kernel.
-    if (!C::kSwap || MOE_PDL_PREFETCH == 0) ptx::pdl_wait();
+    const bool spec = KIND == kG1Swap && p.spec_l2 > 0 && p.tail_ws == nullptr && p.src_row == nullptr;
+    if (spec && threadIdx.x == 0) {
+        const int wt = p.f / 128;
+        if ((int)blockIdx.x < p.E * wt) {
+            const int e = blockIdx.x / wt, m = blockIdx.x % wt;
+            const int nk = min(p.spec_l2, p.d / kBK);
+            for (int kb = 0; kb < nk; ++kb) {
+                const WCoord w = wcoord(p, kb * kBK, m * 256, e);
+                ptx::tma_prefetch_l2_4d(&tmA, 0, w.c1, w.c2, w.c3);
+            }
+        }
+    }
+    if (!C::kSwap || MOE_PDL_PREFETCH == 0 || spec) ptx::pdl_wait();
     if (threadIdx.x < 32) {
         for (int e = threadIdx.x; e < p.E; e += 32) {
             s_counts[e] = p.counts[e];
@@ -339,7 +358,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         int stage = 0;
         uint32_t phase = 0;
         int pre = 0;  // k-blocks of the first tile whose weight loads precede the wait
-        if (C::kSwap && MOE_PDL_PREFETCH > 0) {
+        if (C::kSwap && MOE_PDL_PREFETCH > 0 && !spec) {
             if ((int)blockIdx.x < tp.units) {
                 TileInfo t0;
                 decode_unit<KIND, NB>(blockIdx.x, tp, p, s_counts, s_offsets, t0);

@@ -45,6 +45,9 @@ struct RouteParams {
     int32_t* counts;          // [nkeys]
     int32_t* offsets;         // [nkeys + 1]
     unsigned int* done;       // block-completion counter (zero between launches)
+    // decode speculative weight prefetch (moe.cu spec_l2): let the permute kernel (and
+    // through it the w1/w3 GEMM) launch while this grid still runs
+    int32_t early_trigger;
 };
 
 __device__ __forceinline__ int hist_key(int e, int key_lo, int key_div, int nkeys) {
@@ -182,6 +185,7 @@ __global__ void __launch_bounds__(kRouteThreads) moe_router_kernel(const RoutePa
     const int ntok = min(TB, p.T - tok0);
 
     ptx::pdl_wait();
+    if (p.early_trigger) ptx::pdl_launch_dependents();
 
     if (p.in_idx == nullptr) {
         float acc[TB][E_MAX];
@@ -317,6 +321,7 @@ __global__ void __launch_bounds__(256) moe_router_mma_kernel(const RouteParams p
     const int gid = lane >> 2, q = lane & 3;
 
     ptx::pdl_wait();
+    if (p.early_trigger) ptx::pdl_launch_dependents();
 
     const int r0 = min(tok0 + g * 16 + gid, p.T - 1), r1 = min(tok0 + g * 16 + gid + 8, p.T - 1);
     const uint4* xa = reinterpret_cast<const uint4*>(p.x + (int64_t)r0 * p.d);
@@ -420,6 +425,10 @@ struct PermuteParams {
     int32_t* pos_aux;         // optional copy for the caller
     __nv_bfloat16* x_perm;    // [Cap, d]
     int32_t to_f16;           // store rows as fp16 (fp8-weight GEMMs) instead of copying bf16
+    // decode speculative weight prefetch (moe.cu spec_l2): trigger the w1/w3 GEMM before
+    // waiting for the router, so its L2 weight prefetch overlaps routing. That GEMM then
+    // reads counts / offsets only after its own griddepcontrol.wait.
+    int32_t early_trigger;
     // FP8 two-term token split (fp8-weight w1/w3 GEMM on kind::f8f6f4): x8 != nullptr ->
     // row ps is stored as bytes hi = e4m3(x * 2^s) in plane 0 and lo = e4m3(x * 2^s - hi)
     // in plane 1 ([2][plane_rows][d] bytes, reusing x_perm's memory), tok_scale[ps] = 2^-s
@@ -532,6 +541,7 @@ __global__ void __launch_bounds__(kPermuteThreads) moe_permute_kernel(const Perm
     __shared__ int32_t s_pos[8][2];
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int tok0 = blockIdx.x * p.PT;
+    if (p.early_trigger) ptx::pdl_launch_dependents();
     ptx::pdl_wait();
 #ifndef MOE_PERMUTE_EARLY_TRIGGER
 #define MOE_PERMUTE_EARLY_TRIGGER 1  // r01 A/B: 0.4522 -> 0.4510 ms per decode step

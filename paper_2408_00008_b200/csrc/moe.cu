@@ -271,6 +271,13 @@ struct moe_ctx {
     int w13_nt = 0, w2_nt = 0;   // tiles per expert of the tiled bf16 weight layout (256 / 128 rows)
     bool gather = false;         // MOE_FLAG_GATHER (or env MOE_GATHER=1): tile::gather4 token fetch
     bool gather_now = false;     // the current forward gathers (set per call)
+    // Decode speculative L2 weight prefetch (env MOE_SPEC_L2 = K blocks per CTA, 0 = off):
+    // the router and permute kernels trigger their PDL dependents early, so the w1/w3
+    // GEMM launches while routing runs and prefetches the first K blocks of the weight
+    // tile it will most likely own (every expert holding one token tile) into L2.
+    // Only for 16 <= T <= 128 (one token tile per expert, all experts likely used).
+    int spec_l2 = 16;
+    bool spec_now = false;       // the current forward prefetches speculatively (set per call)
     CUtensorMap tm_src{};        // gather map over the current call's tokens [T, d], box {64, 1}
     float* y = nullptr;
     int64_t y_elems = 0;
@@ -645,6 +652,7 @@ moe_status run_swap_g1(moe_ctx* c, int nbi, const moe_expert_weights* w, cudaStr
         if (c->fp8)
             return launch_gemm_fp8<kG1Swap, NB>(c, kSlotGemm1, p1, w->w13_scale, c->tm8_w13_64, c->tm_x_swap[nbi],
                                                 c->num_sms, st);
+    if (c->spec_now) p1.spec_l2 = c->spec_l2;
     return launch_gemm<kG1Swap, NB>(c, kSlotGemm1, p1, c->tm_w13, c->tm_x_swap[nbi], c->num_sms, st);
 }
 
@@ -716,6 +724,7 @@ struct RouteSpec {
     uint8_t* const* peers = nullptr;  // P2P dispatch: rows / meta into the destinations' regions
     int64_t peer_rows_off = 0, peer_meta_off = 0;
     int my_rank = 0;
+    bool early = false;          // spec_l2: router and permute trigger their dependents early
 };
 
 moe_status route_and_permute(moe_ctx* c, const RouteSpec& r, cudaStream_t st) {
@@ -740,6 +749,7 @@ moe_status route_and_permute(moe_ctx* c, const RouteSpec& r, cudaStream_t st) {
     rp.rank = r.pos;
     rp.blockcount = c->blockcount; rp.blockoff = c->blockoff;
     rp.counts = c->counts; rp.offsets = c->offsets; rp.done = c->done;
+    rp.early_trigger = r.early;
     moe_status s;
     const dim3 rg(nblk);
     if (mma && KS == 1) s = launch(c, kSlotRouter, moe_router_mma_kernel<1>, rg, dim3(256), 0, st, rp);
@@ -758,6 +768,7 @@ moe_status route_and_permute(moe_ctx* c, const RouteSpec& r, cudaStream_t st) {
     pp.PT = r.T <= 1024 ? 2 : 8;
     pp.pos = r.pos; pp.pos_aux = r.pos_aux; pp.x_perm = static_cast<__nv_bfloat16*>(r.dst_rows);
     pp.src_row = r.src_row;
+    pp.early_trigger = r.early;
     pp.peers = r.peers; pp.peer_rows_off = r.peer_rows_off; pp.peer_meta_off = r.peer_meta_off; pp.my_rank = r.my_rank;
     pp.to_f16 = c->fp8 && r.cap == 0;  // fp8-weight GEMMs take fp16 tokens
     if (c->fp8x && r.cap == 0 && r.dst_rows == c->x_perm) {  // ... or two E4M3 terms (fp8x)
@@ -1268,6 +1279,7 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
     if (const char* v = getenv("MOE_GATHER")) c->gather = atoi(v) != 0;
     if (const char* v = getenv("MOE_G1_SWAP_ROWS")) c->swap_rows_per_expert = atoi(v);
     if (const char* v = getenv("MOE_TAIL_PARTS")) c->tail_parts = atoi(v);
+    if (const char* v = getenv("MOE_SPEC_L2")) c->spec_l2 = std::max(0, atoi(v));
     if (const char* v = getenv("MOE_HOST_ZERO_COPY")) c->host_zero_copy = atoi(v) != 0;
     if (const char* v = getenv("MOE_SWAP_HINT")) c->swap_hint_mode = atoi(v);
     if (const char* v = getenv("MOE_MAX_SPLITS")) c->max_splits_env = std::max(1, std::min(8, atoi(v)));
@@ -1812,9 +1824,17 @@ moe_status forward_impl(moe_ctx* c, const void* tokens, int32_t T, const void* r
         return fail(c, MOE_ERR_CUDA, "cuTensorMapEncodeTiled(tokens) failed");
     r.dst_rows = c->gather_now ? nullptr : c->x_perm;
     r.src_row = c->gather_now ? c->src_row : nullptr;
-    if ((s = route_and_permute(c, r, st))) return s;
+    const GemmPaths gpaths = gemm_paths(c, (int64_t)T * c->k);
+    c->spec_now = c->spec_l2 > 0 && gpaths.swap1 && !c->fp8 && !c->gather_now && c->tail_parts <= 1 &&
+                  c->swap_nb_cap == 0 && T >= 16 && T <= 128 && !c->profiling;
+    r.early = c->spec_now;
+    moe_status s2 = route_and_permute(c, r, st);
+    c->spec_now = c->spec_now && s2 == MOE_OK;
+    if ((s = s2)) return s;
     int splits = 1;
-    if ((s = run_gemms(c, gemm_paths(c, (int64_t)T * c->k), T, (int64_t)T * c->k, &splits, st))) return s;
+    s = run_gemms(c, gpaths, T, (int64_t)T * c->k, &splits, st);
+    c->spec_now = false;
+    if (s) return s;
     if ((s = copy_aux(c, aux, T, st)) || (s = copy_aux_segments(c, aux, st))) return s;
 
     CombineParams cp{};
