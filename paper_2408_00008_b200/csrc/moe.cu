@@ -1826,7 +1826,7 @@ moe_status forward_impl(moe_ctx* c, const void* tokens, int32_t T, const void* r
     r.src_row = c->gather_now ? c->src_row : nullptr;
     const GemmPaths gpaths = gemm_paths(c, (int64_t)T * c->k);
     c->spec_now = c->spec_l2 > 0 && gpaths.swap1 && !c->fp8 && !c->gather_now && c->tail_parts <= 1 &&
-                  c->swap_nb_cap == 0 && T >= 16 && T <= 128 && !c->profiling;
+                  T >= 16 && T <= 128 && !c->profiling;
     r.early = c->spec_now;
     moe_status s2 = route_and_permute(c, r, st);
     c->spec_now = c->spec_now && s2 == MOE_OK;
