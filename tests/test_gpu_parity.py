@@ -238,6 +238,26 @@ def test_pathological_routing(moe, n, mode):
     blk.close()
 
 
+@pytest.mark.parametrize("T", [16, 48, 128])
+def test_speculative_prefetch_wrong_guess(moe, T):
+    """Decode speculative L2 prefetch (16 <= T <= 128, bf16 swap path): the w1/w3 GEMM
+    launches before routing completes and guesses one token tile per expert. Forced
+    routing to experts (3, 6) of 8 leaves six experts empty, so every guess is wrong;
+    the GEMM must still read counts only after its wait (oracle parity)."""
+    shape = synth.MoEShape(T=T, d=256, f=512, E=8, k=2)
+    inp = _inputs(shape, 200 + T)
+    host = to_host_inputs(inp)
+    idx = np.tile(np.array([[6, 3]], np.int32), (T, 1))
+    gw = _forced_gates(host, idx)
+    blk = _block(moe, inp, 2, T, MODES["swap"])
+    run = GpuRun(blk, inp["x"], routed=(torch.from_numpy(idx).cuda(), torch.from_numpy(gw).cuda()))
+    check_forward(run, host, 2, routed=True)
+    assert run.np("expert_counts").tolist() == [0, 0, 0, T, 0, 0, T, 0]
+    blk.close()
+    run = GpuRun(_block(moe, inp, 2, T, MODES["swap"]), inp["x"])  # router path, same shapes
+    check_forward(run, host, 2)
+
+
 def test_t_zero_and_determinism(moe):
     inp = _inputs(synth.TINY, 3)
     blk = _block(moe, inp, 2, 16)
@@ -320,6 +340,24 @@ def test_c2_decode_full(moe, mixtral_weights, seed):
     st = check_forward(run, h, 2)
     print("C2", seed, st)
     blk.close()
+
+
+def test_c2_speculative_prefetch_bit_identical(moe, mixtral_weights, monkeypatch):
+    """The speculative L2 prefetch (MOE_SPEC_L2, read at moe_init) changes only timing:
+    64-token decode outputs are bit-identical with it off and at two depths."""
+    w, _ = mixtral_weights
+    x = synth.make_tokens(64, 4096, seed=321, device="cuda")
+    outs = []
+    for v in ("0", "16", "64"):
+        monkeypatch.setenv("MOE_SPEC_L2", v)
+        blk = moe.MoEBlock(w["wg"], w["w1"], w["w3"], w["w2"], top_k=2, max_tokens=64)
+        for _ in range(2):
+            o = blk.forward(x)
+        torch.cuda.synchronize()
+        outs.append(o.clone())
+        blk.close()
+    assert torch.equal(outs[0].view(torch.int16), outs[1].view(torch.int16))
+    assert torch.equal(outs[0].view(torch.int16), outs[2].view(torch.int16))
 
 
 def test_c3_prefill_full(moe, mixtral_weights):
