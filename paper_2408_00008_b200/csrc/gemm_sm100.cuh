@@ -70,6 +70,10 @@ struct GemmParams {
     // kernel reads counts / offsets after griddepcontrol.wait (it may launch before the
     // router has finished).
     int32_t spec_l2;
+    // swap kinds: tmB has a 32-row box and the producer loads only ceil(n_valid / 32)
+    // boxes of the token operand per stage (stacked 4 KB apart: the 128-byte swizzle is
+    // address-based, so the smem image equals one NB-row box) instead of all NB rows.
+    int32_t b_rows32;
 };
 
 // 4D coordinates of rows [row, row + box) of expert e at K offset kc in a tiled weight map
@@ -363,9 +367,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 TileInfo t0;
                 decode_unit<KIND, NB>(blockIdx.x, tp, p, s_counts, s_offsets, t0);
                 pre = min(S, t0.nkb);
+                const uint32_t bytes0 = C::kABytes + (p.b_rows32 ? ((t0.n_valid + 31) / 32) * 4096 : C::kBBytes);
                 if (lane == 0)
                     for (int kb = 0; kb < pre; ++kb) {  // fresh stages: no empty-wait needed
-                        ptx::mbar_arrive_expect_tx(&full[kb], C::kStageBytes);
+                        ptx::mbar_arrive_expect_tx(&full[kb], bytes0);
                     {
                         const WCoord w = wcoord(p, (t0.kb0 + kb) * kBK, t0.a_row, t0.e);
                         ptx::tma_load_4d(&tmA, &full[kb], smem_a + kb * C::kABytes, 0, w.c1, w.c2, w.c3,
@@ -391,10 +396,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 uint8_t* sb = smem_b + stage * C::kBBytes;
                 uint8_t* s_tok = C::kSwap ? sb : sa;
                 const bool armed = first && kb < pre;  // weights already in flight on this stage
+                const int nb32 = C::kSwap && p.b_rows32 ? (ti.n_valid + 31) / 32 : 0;  // 32-row token boxes
                 if (lane == 0) {
                     if (!armed) {
                         ptx::mbar_wait(&empty[stage], phase ^ 1);
-                        ptx::mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
+                        ptx::mbar_arrive_expect_tx(&full[stage], nb32 ? C::kABytes + nb32 * 4096 : C::kStageBytes);
                     }
                     if (C::kSwap) {
                         // A = weights (3D map [K, rows, E]) streamed once: evict-first.
@@ -403,7 +409,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                             ptx::tma_load_4d(&tmA, &full[stage], sa, 0, w.c1, w.c2, w.c3, w_hint);
                         }
                         // B = permuted tokens / activations (2D map [K, Cap]): keep in L2.
-                        if (!gather) ptx::tma_load_2d(&tmB, &full[stage], sb, kc, ti.b_row, ptx::kEvictLast);
+                        if (nb32) {
+                            for (int i = 0; i < nb32; ++i)
+                                ptx::tma_load_2d(&tmB, &full[stage], sb + i * 4096, kc, ti.b_row + 32 * i,
+                                                 ptx::kEvictLast);
+                        } else if (!gather) {
+                            ptx::tma_load_2d(&tmB, &full[stage], sb, kc, ti.b_row, ptx::kEvictLast);
+                        }
                     } else {
                         if (!gather) ptx::tma_load_2d(&tmA, &full[stage], sa, kc, ti.a_row, ptx::kEvictLast);
                         const WCoord w = wcoord(p, kc, ti.b_row, ti.e);

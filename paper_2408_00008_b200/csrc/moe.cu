@@ -278,6 +278,11 @@ struct moe_ctx {
     // Only for 16 <= T <= 128 (one token tile per expert, all experts likely used).
     int spec_l2 = 16;
     bool spec_now = false;       // the current forward prefetches speculatively (set per call)
+    // bf16 swap GEMMs: load the token operand in 32-row boxes, only ceil(n_valid / 32) of
+    // them per stage, instead of one NB-row box (env MOE_TRIM_B=1; GemmParams::b_rows32).
+    // Off: measured slower although it moves fewer bytes (r01 interleaved A/B, one box:
+    // decode 0.4350 -> 0.4569 ms, stack 16.1 -> 21.6 ms; profiles/r01/experiments/ab_trim_*.log)
+    int trim_b = 0;
     CUtensorMap tm_src{};        // gather map over the current call's tokens [T, d], box {64, 1}
     float* y = nullptr;
     int64_t y_elems = 0;
@@ -653,7 +658,8 @@ moe_status run_swap_g1(moe_ctx* c, int nbi, const moe_expert_weights* w, cudaStr
             return launch_gemm_fp8<kG1Swap, NB>(c, kSlotGemm1, p1, w->w13_scale, c->tm8_w13_64, c->tm_x_swap[nbi],
                                                 c->num_sms, st);
     if (c->spec_now) p1.spec_l2 = c->spec_l2;
-    return launch_gemm<kG1Swap, NB>(c, kSlotGemm1, p1, c->tm_w13, c->tm_x_swap[nbi], c->num_sms, st);
+    p1.b_rows32 = c->trim_b;
+    return launch_gemm<kG1Swap, NB>(c, kSlotGemm1, p1, c->tm_w13, c->tm_x_swap[c->trim_b ? 0 : nbi], c->num_sms, st);
 }
 
 template <int NB>
@@ -700,7 +706,8 @@ moe_status run_swap_g2(moe_ctx* c, int nbi, const moe_expert_weights* w, int spl
             return launch_gemm_fp8<kG2Swap, NB>(c, kSlotGemm2, p2, w->w2_scale, c->tm8_w2_64, c->tm_h_swap[nbi],
                                                 c->num_sms, st);
         }
-    return launch_gemm<kG2Swap, NB>(c, kSlotGemm2, p2, c->tm_w2_swap, c->tm_h_swap[nbi], c->num_sms, st);
+    p2.b_rows32 = c->trim_b;
+    return launch_gemm<kG2Swap, NB>(c, kSlotGemm2, p2, c->tm_w2_swap, c->tm_h_swap[c->trim_b ? 0 : nbi], c->num_sms, st);
 }
 
 // One routing + permutation pass (K1 + K2) over `T` rows of `x`.
@@ -1280,6 +1287,7 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
     if (const char* v = getenv("MOE_G1_SWAP_ROWS")) c->swap_rows_per_expert = atoi(v);
     if (const char* v = getenv("MOE_TAIL_PARTS")) c->tail_parts = atoi(v);
     if (const char* v = getenv("MOE_SPEC_L2")) c->spec_l2 = std::max(0, atoi(v));
+    if (const char* v = getenv("MOE_TRIM_B")) c->trim_b = atoi(v) != 0;
     if (const char* v = getenv("MOE_HOST_ZERO_COPY")) c->host_zero_copy = atoi(v) != 0;
     if (const char* v = getenv("MOE_SWAP_HINT")) c->swap_hint_mode = atoi(v);
     if (const char* v = getenv("MOE_MAX_SPLITS")) c->max_splits_env = std::max(1, std::min(8, atoi(v)));
