@@ -82,8 +82,10 @@ def parse():
     ap.add_argument("--fp8", action="store_true",
                     help="FP8 E4M3 expert weights with per-row power-of-two scales (SURVEY 8(f) NEXT #2); "
                          "not the BASELINE bf16 headline")
-    ap.add_argument("--graph", action="store_true",
-                    help="headline pass as CUDA-graph replays of the forward (single GPU; default: eager launches)")
+    ap.add_argument("--graph", dest="graph", action="store_true", default=True,
+                    help="headline pass as CUDA-graph replays of the forward (single GPU, no EP/TP; the default: "
+                         "r01 interleaved A/B at the 64-token decode, 3 of 3 rounds 0.4364 vs 0.4397 ms eager)")
+    ap.add_argument("--no-graph", dest="graph", action="store_false", help="headline pass as eager launches")
     ap.add_argument("--par", default=None, choices=["ep", "tp", "hybrid", "none"],
                     help="multi-GPU variant (default: ep when N > 1)")
     ap.add_argument("--tp", type=int, default=2, help="TP degree of --par hybrid (EP degree = N / tp)")
@@ -512,6 +514,30 @@ def main():
         dist.all_reduce(tms, op=dist.ReduceOp.MAX)
         ms, ms_prof = float(tms[0]), float(tms[1])
 
+    # ---------------- per-step distribution (median and p10/p90): a separate
+    # pass with an event between consecutive steps (the events cut the PDL overlap of one
+    # step's combine with the next step's router, so the headline above stays the clean
+    # K-step region); max over ranks per step.
+    sev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    barrier()
+    torch.cuda.synchronize()
+    sev[0].record(stream)
+    for i in range(args.steps):
+        if use_graph:
+            graphs[i % nbuf].replay()
+        else:
+            step(i)
+        sev[i + 1].record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    per_step = torch.tensor([sev[i].elapsed_time(sev[i + 1]) for i in range(args.steps)], device=dev)
+    if world > 1:
+        import torch.distributed as dist
+        dist.all_reduce(per_step, op=dist.ReduceOp.MAX)
+    q = np.percentile(per_step.cpu().numpy(), [10, 50, 90])
+    step_dist = {"p10": float(q[0]), "p50": float(q[1]), "p90": float(q[2]), "n": args.steps,
+                 "how": "separate pass, CUDA event between consecutive steps, max over ranks"}
+
     # ---------------- e2e: host buffers through moe_forward_host (H2D + forward + D2H per step)
     xh = [x.cpu().pin_memory() for x in xs]
     oh = torch.empty(T, d, dtype=torch.bfloat16).pin_memory()
@@ -586,6 +612,7 @@ def main():
         "kernel_ms": {n: round(per[n], 5) for n in per if ktimes[n][1]},
         "kernel_share": kernel_share,
         "ms_per_step_profiled": ms_prof,
+        "step_ms_dist": step_dist,
         "gpu_launches": launches,
         "graph_replay": use_graph,
         "clocks": clk,

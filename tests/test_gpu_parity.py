@@ -906,6 +906,28 @@ def test_cuda_graph_capture(moe):
         blk.close()
 
 
+def test_cuda_graph_capture_fp8(moe):
+    """FP8-weight forward (bench.py --fp8 replays it as a CUDA graph): capturable, and
+    replays bit-identical to the eager call."""
+    T = 64
+    inp, qs, _ = _fp8_inputs(synth.MoEShape(T=T, d=256, f=512, E=8, k=2), 950)
+    blk = moe.MoEBlock(inp["wg"], qs["w1"], qs["w3"], qs["w2"], top_k=2, max_tokens=T,
+                       flags=moe.MOE_FLAG_FP8_WEIGHTS)
+    ref = blk.forward(inp["x"]).clone()
+    out = torch.empty_like(ref)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        moe.moe_forward(blk.ctx, inp["x"], T, blk.router_w, blk.w13, blk.w2, out, None,
+                        torch.cuda.current_stream(), blk.s13, blk.s2)
+    for _ in range(3):
+        out.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(out.view(torch.int16), ref.view(torch.int16))
+    blk.close()
+
+
 def test_large_token_counts(moe):
     """T > 65535 (1-D grids everywhere; no gridDim.y limit), tiny hidden size."""
     shape = synth.MoEShape(T=70000, d=64, f=128, E=4, k=2)
