@@ -283,6 +283,16 @@ struct moe_ctx {
     // Off: measured slower although it moves fewer bytes (r01 interleaved A/B, one box:
     // decode 0.4350 -> 0.4569 ms, stack 16.1 -> 21.6 ms; profiles/r01/experiments/ab_trim_*.log)
     int trim_b = 0;
+    // Persistent grid of the bf16 swap GEMMs (run_gemms; env MOE_G1_GRID / MOE_G2_GRID
+    // override, 0 = auto). Auto, when every expert fits one token tile (decode): the w1/w3
+    // GEMM runs (f_l/128) * floor(SMs / (f_l/128)) CTAs -- Mixtral: 112, so CTA m streams
+    // weight tile m of every expert -- and the w2 GEMM ceil(U / ceil(U / SMs)) CTAs for U
+    // units (256 -> 128: two equal waves). r01 interleaved sweep at the 64-token decode
+    // (profiles/r01/experiments/ab_grid*.log): w1/w3 grid 148 -> 282.4 us, 136 -> 296,
+    // 128 -> ~283, 120 -> 278.7, 112 -> 266.8 (7.06 TB/s), 104 -> 274, 96 -> 286; w2 grid
+    // 148 -> 154.8 us, 136 -> 146, 128 -> 142.7, 112 -> 207; step 0.4340 -> 0.4124 ms.
+    int g1_grid = 0, g2_grid = 0;
+    int g1_grid_now = 0, g2_grid_now = 0;  // the current forward's choice
     CUtensorMap tm_src{};        // gather map over the current call's tokens [T, d], box {64, 1}
     float* y = nullptr;
     int64_t y_elems = 0;
@@ -659,7 +669,8 @@ moe_status run_swap_g1(moe_ctx* c, int nbi, const moe_expert_weights* w, cudaStr
                                                 c->num_sms, st);
     if (c->spec_now) p1.spec_l2 = c->spec_l2;
     p1.b_rows32 = c->trim_b;
-    return launch_gemm<kG1Swap, NB>(c, kSlotGemm1, p1, c->tm_w13, c->tm_x_swap[c->trim_b ? 0 : nbi], c->num_sms, st);
+    return launch_gemm<kG1Swap, NB>(c, kSlotGemm1, p1, c->tm_w13, c->tm_x_swap[c->trim_b ? 0 : nbi],
+                                    c->g1_grid_now, st);
 }
 
 template <int NB>
@@ -707,7 +718,8 @@ moe_status run_swap_g2(moe_ctx* c, int nbi, const moe_expert_weights* w, int spl
                                                 c->num_sms, st);
         }
     p2.b_rows32 = c->trim_b;
-    return launch_gemm<kG2Swap, NB>(c, kSlotGemm2, p2, c->tm_w2_swap, c->tm_h_swap[c->trim_b ? 0 : nbi], c->num_sms, st);
+    return launch_gemm<kG2Swap, NB>(c, kSlotGemm2, p2, c->tm_w2_swap, c->tm_h_swap[c->trim_b ? 0 : nbi],
+                                    c->g2_grid_now, st);
 }
 
 // One routing + permutation pass (K1 + K2) over `T` rows of `x`.
@@ -854,6 +866,11 @@ moe_status run_gemms(moe_ctx* c, GemmPaths gp, int64_t rows_bound, int64_t rows_
         b1 = std::max(1, (c->pair_tune >> 4) & 63); b2 = std::max(1, (c->pair_tune >> 10) & 63);
     }
     const int ncl = c->num_sms / 2;
+    {
+        const int wt = c->f_local / 128, ns = c->num_sms;
+        c->g1_grid_now = c->g1_grid > 0 ? std::min(c->g1_grid, ns)
+                       : (rows_bound <= nb1 && wt <= ns) ? wt * (ns / wt) : ns;
+    }
     if (gp.swap1) {
         const int i1 = nb1 == 32 ? 0 : nb1 == 64 ? 1 : 2;
         if (nb1 == 32) s = run_swap_g1<32>(c, i1, &c->cur_w, st);
@@ -896,6 +913,13 @@ moe_status run_gemms(moe_ctx* c, GemmPaths gp, int64_t rows_bound, int64_t rows_
         splits = std::min(splits, c->f_local / (c->fp8_g2_kb256 ? 256 : c->fp8_kb128 ? 128 : kBK));  // >= 1 K block per split
         c->split_stride = rows_needed * c->d;
         c->rows_needed_cur = std::min<int64_t>(rows_needed, c->cap);
+        {
+            const int64_t U = (int64_t)c->E_local * ((c->d + 127) / 128) * splits;
+            const int ns = c->num_sms;
+            const int64_t waves = (U + ns - 1) / ns;
+            c->g2_grid_now = c->g2_grid > 0 ? std::min(c->g2_grid, ns)
+                           : rows_bound <= nb2 ? (int)std::min<int64_t>(ns, (U + waves - 1) / waves) : ns;
+        }
         if (nb2 == 32) s = run_swap_g2<32>(c, 0, &c->cur_w, splits, st);
         else if (nb2 == 64) s = run_swap_g2<64>(c, 1, &c->cur_w, splits, st);
         else if (nb2 == 128) s = run_swap_g2<128>(c, 2, &c->cur_w, splits, st);
@@ -1288,6 +1312,8 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
     if (const char* v = getenv("MOE_TAIL_PARTS")) c->tail_parts = atoi(v);
     if (const char* v = getenv("MOE_SPEC_L2")) c->spec_l2 = std::max(0, atoi(v));
     if (const char* v = getenv("MOE_TRIM_B")) c->trim_b = atoi(v) != 0;
+    if (const char* v = getenv("MOE_G1_GRID")) c->g1_grid = std::max(0, atoi(v));
+    if (const char* v = getenv("MOE_G2_GRID")) c->g2_grid = std::max(0, atoi(v));
     if (const char* v = getenv("MOE_HOST_ZERO_COPY")) c->host_zero_copy = atoi(v) != 0;
     if (const char* v = getenv("MOE_SWAP_HINT")) c->swap_hint_mode = atoi(v);
     if (const char* v = getenv("MOE_MAX_SPLITS")) c->max_splits_env = std::max(1, std::min(8, atoi(v)));
