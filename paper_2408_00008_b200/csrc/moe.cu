@@ -291,6 +291,8 @@ struct moe_ctx {
     // (profiles/r01/experiments/ab_grid*.log): w1/w3 grid 148 -> 282.4 us, 136 -> 296,
     // 128 -> ~283, 120 -> 278.7, 112 -> 266.8 (7.06 TB/s), 104 -> 274, 96 -> 286; w2 grid
     // 148 -> 154.8 us, 136 -> 146, 128 -> 142.7, 112 -> 207; step 0.4340 -> 0.4124 ms.
+    // bf16 only: the FP8 kernels are slower on the smaller grids (ab_grid_fp8.log: w1/w3
+    // 165 -> 184 us at 112, w2 94 -> 105 us at 128), so they keep one CTA per SM.
     int g1_grid = 0, g2_grid = 0;
     int g1_grid_now = 0, g2_grid_now = 0;  // the current forward's choice
     CUtensorMap tm_src{};        // gather map over the current call's tokens [T, d], box {64, 1}
@@ -656,7 +658,7 @@ moe_status run_swap_g1(moe_ctx* c, int nbi, const moe_expert_weights* w, cudaStr
     }
     if constexpr (NB <= 128)
         if (c->fp8 && c->fp8x)
-            return launch(c, kSlotGemm1, moe_gemm_fp8x_kernel<kG1Swap, NB>, dim3(c->num_sms), dim3(kGemmThreads),
+            return launch(c, kSlotGemm1, moe_gemm_fp8x_kernel<kG1Swap, NB>, dim3(c->g1_grid_now), dim3(kGemmThreads),
                           (size_t)Fp8xCfg<kG1Swap, NB>::kSmemBytes, st, p1, static_cast<const float*>(w->w13_scale),
                           static_cast<const float*>(c->tok_scale), c->tm_w13, c->tm_x8[nbi]);
     if constexpr (NB <= 64)
@@ -710,7 +712,7 @@ moe_status run_swap_g2(moe_ctx* c, int nbi, const moe_expert_weights* w, int spl
     if constexpr (NB <= 64)
         if (c->fp8 && !c->fp8_smem_a)
             return launch_gemm_fp8t<kG2Swap, NB>(c, kSlotGemm2, p2, w->w2_scale, c->tm_w2_swap, c->tm_h_swap[nbi],
-                                                 c->num_sms, st);
+                                                 c->g2_grid_now, st);
     if constexpr (NB <= 128)
         if (c->fp8) {
             p2.splits = std::min(splits, c->f_local / kBK);
@@ -869,7 +871,7 @@ moe_status run_gemms(moe_ctx* c, GemmPaths gp, int64_t rows_bound, int64_t rows_
     {
         const int wt = c->f_local / 128, ns = c->num_sms;
         c->g1_grid_now = c->g1_grid > 0 ? std::min(c->g1_grid, ns)
-                       : (rows_bound <= nb1 && wt <= ns) ? wt * (ns / wt) : ns;
+                       : (!c->fp8 && rows_bound <= nb1 && wt <= ns) ? wt * (ns / wt) : ns;
     }
     if (gp.swap1) {
         const int i1 = nb1 == 32 ? 0 : nb1 == 64 ? 1 : 2;
@@ -918,7 +920,7 @@ moe_status run_gemms(moe_ctx* c, GemmPaths gp, int64_t rows_bound, int64_t rows_
             const int ns = c->num_sms;
             const int64_t waves = (U + ns - 1) / ns;
             c->g2_grid_now = c->g2_grid > 0 ? std::min(c->g2_grid, ns)
-                           : rows_bound <= nb2 ? (int)std::min<int64_t>(ns, (U + waves - 1) / waves) : ns;
+                           : (!c->fp8 && rows_bound <= nb2) ? (int)std::min<int64_t>(ns, (U + waves - 1) / waves) : ns;
         }
         if (nb2 == 32) s = run_swap_g2<32>(c, 0, &c->cur_w, splits, st);
         else if (nb2 == 64) s = run_swap_g2<64>(c, 1, &c->cur_w, splits, st);
