@@ -76,6 +76,8 @@ if __name__ == "__main__":
     single(small, 0x2 | moe.MOE_FLAG_GATHER)  # gather4, swap
     single(small, 0x4 | moe.MOE_FLAG_GATHER)  # gather4, pair
     single(synth.MoEShape(T=64, d=1024, f=2560, E=8, k=2), 0x2, {"MOE_TAIL_PARTS": "8"})  # tail slices
+    single(synth.MoEShape(T=64, d=1024, f=2560, E=8, k=2), 0x2)  # speculative L2 prefetch, auto grids
+    single(synth.MoEShape(T=64, d=1024, f=2560, E=8, k=2), 0x2, {"MOE_TRIM_B": "1"})  # 32-row token boxes
     single(synth.MoEShape(T=32, d=256, f=512, E=4, k=2), moe.MOE_FLAG_FP8_WEIGHTS)
     for par in ("ep", "tp"):
         for p2p in (False, True):
