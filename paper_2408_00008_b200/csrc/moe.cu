@@ -276,7 +276,9 @@ struct moe_ctx {
     // GEMM launches while routing runs and prefetches the first K blocks of the weight
     // tile it will most likely own (every expert holding one token tile) into L2.
     // Only for 16 <= T <= 128 (one token tile per expert, all experts likely used).
-    int spec_l2 = 16;
+    // Default 48 K blocks after the grid change (ab_spec2.log, 3/3 rounds: 0.4121 ms at 48,
+    // 0.4127 at 32, 0.4132 at 16 and off; first sweep on 148-CTA grids: ab_spec_l2.log).
+    int spec_l2 = 48;
     bool spec_now = false;       // the current forward prefetches speculatively (set per call)
     // bf16 swap GEMMs: load the token operand in 32-row boxes, only ceil(n_valid / 32) of
     // them per stage, instead of one NB-row box (env MOE_TRIM_B=1; GemmParams::b_rows32).
