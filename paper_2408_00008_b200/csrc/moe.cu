@@ -871,9 +871,11 @@ moe_status run_gemms(moe_ctx* c, GemmPaths gp, int64_t rows_bound, int64_t rows_
     }
     const int ncl = c->num_sms / 2;
     {
+        // expert-stride grid only where it also balances the waves (all experts used)
         const int wt = c->f_local / 128, ns = c->num_sms;
+        const int gs = wt <= ns ? wt * (ns / wt) : ns;
         c->g1_grid_now = c->g1_grid > 0 ? std::min(c->g1_grid, ns)
-                       : (!c->fp8 && rows_bound <= nb1 && wt <= ns) ? wt * (ns / wt) : ns;
+                       : (!c->fp8 && rows_bound <= nb1 && wt <= ns && (c->E_local * wt) % gs == 0) ? gs : ns;
     }
     if (gp.swap1) {
         const int i1 = nb1 == 32 ? 0 : nb1 == 64 ? 1 : 2;
