@@ -74,6 +74,10 @@ struct GemmParams {
     // boxes of the token operand per stage (stacked 4 KB apart: the 128-byte swizzle is
     // address-based, so the smem image equals one NB-row box) instead of all NB rows.
     int32_t b_rows32;
+    // swap kinds: trigger the dependent grid (PDL) right after the prologue instead of at
+    // the end, so its CTAs can take SMs this grid leaves idle (smaller decode grids) and
+    // run their prologue / pre-wait weight stages early (moe.cu early_dep)
+    int32_t early_dep;
 };
 
 // 4D coordinates of rows [row, row + box) of expert e at K offset kc in a tiled weight map
@@ -343,6 +347,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_base_slot;
+    if (C::kSwap && p.early_dep) ptx::pdl_launch_dependents();
 
     int total = 0;
     for (int e = 0; e < p.E; ++e) total += tiles_of<KIND, NB>(s_counts[e], p);

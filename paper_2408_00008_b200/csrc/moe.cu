@@ -296,6 +296,10 @@ struct moe_ctx {
     // bf16 only: the FP8 kernels are slower on the smaller grids (ab_grid_fp8.log: w1/w3
     // 165 -> 184 us at 112, w2 94 -> 105 us at 128), so they keep one CTA per SM.
     int g1_grid = 0, g2_grid = 0;
+    // env MOE_EARLY_DEP=1: GemmParams::early_dep for the bf16 swap GEMMs. Off: no measurable
+    // effect (decode 0.4119 vs 0.4119 ms over 4 interleaved rounds, stack within noise;
+    // profiles/r01/experiments/ab_early_dep.log); parity suite green with it on.
+    int early_dep = 0;
     int g1_grid_now = 0, g2_grid_now = 0;  // the current forward's choice
     CUtensorMap tm_src{};        // gather map over the current call's tokens [T, d], box {64, 1}
     float* y = nullptr;
@@ -673,6 +677,7 @@ moe_status run_swap_g1(moe_ctx* c, int nbi, const moe_expert_weights* w, cudaStr
                                                 c->num_sms, st);
     if (c->spec_now) p1.spec_l2 = c->spec_l2;
     p1.b_rows32 = c->trim_b;
+    p1.early_dep = c->early_dep;
     return launch_gemm<kG1Swap, NB>(c, kSlotGemm1, p1, c->tm_w13, c->tm_x_swap[c->trim_b ? 0 : nbi],
                                     c->g1_grid_now, st);
 }
@@ -722,6 +727,7 @@ moe_status run_swap_g2(moe_ctx* c, int nbi, const moe_expert_weights* w, int spl
                                                 c->num_sms, st);
         }
     p2.b_rows32 = c->trim_b;
+    p2.early_dep = c->early_dep;
     return launch_gemm<kG2Swap, NB>(c, kSlotGemm2, p2, c->tm_w2_swap, c->tm_h_swap[c->trim_b ? 0 : nbi],
                                     c->g2_grid_now, st);
 }
@@ -1319,6 +1325,7 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
     if (const char* v = getenv("MOE_SPEC_L2")) c->spec_l2 = std::max(0, atoi(v));
     if (const char* v = getenv("MOE_TRIM_B")) c->trim_b = atoi(v) != 0;
     if (const char* v = getenv("MOE_G1_GRID")) c->g1_grid = std::max(0, atoi(v));
+    if (const char* v = getenv("MOE_EARLY_DEP")) c->early_dep = atoi(v) != 0;
     if (const char* v = getenv("MOE_G2_GRID")) c->g2_grid = std::max(0, atoi(v));
     if (const char* v = getenv("MOE_HOST_ZERO_COPY")) c->host_zero_copy = atoi(v) != 0;
     if (const char* v = getenv("MOE_SWAP_HINT")) c->swap_hint_mode = atoi(v);
