@@ -29,7 +29,9 @@
 
 namespace moe {
 
-enum GemmKind : int { kG1Tiled = 0, kG2Tiled = 1, kG1Swap = 2, kG2Swap = 3, kG1Pair = 4, kG2Pair = 5 };
+// kG2Dual: kG2Swap whose unit is TWO 128-row W2 tiles (256 hidden rows, two 16 KB boxes
+// per stage, two M=128 MMAs into two TMEM accumulators, as kG1Swap does with w1/w3).
+enum GemmKind : int { kG1Tiled = 0, kG2Tiled = 1, kG1Swap = 2, kG2Swap = 3, kG1Pair = 4, kG2Pair = 5, kG2Dual = 6 };
 
 struct GemmParams {
     const int32_t* counts;   // [E] rows per local expert (device, from the permute step)
@@ -105,16 +107,17 @@ constexpr int kSmemBudget = 232448;     // 227 KB opt-in dynamic shared memory p
 #endif
 template <int KIND, int NB>
 struct GemmCfg {
-    static constexpr bool kSwap = (KIND == kG1Swap || KIND == kG2Swap);
+    static constexpr bool kSwap = (KIND == kG1Swap || KIND == kG2Swap || KIND == kG2Dual);
     static constexpr bool kG1 = (KIND == kG1Tiled || KIND == kG1Swap);
     // bytes per stage of each operand (rows x 128 B)
-    static constexpr int kARows = (KIND == kG1Swap) ? 256 : 128;
+    static constexpr int kARows = (KIND == kG1Swap || KIND == kG2Dual) ? 256 : 128;
     static constexpr int kBRows = kSwap ? NB : 256;
     static constexpr int kABytes = kARows * 128;
     static constexpr int kBBytes = kBRows * 128;
     static constexpr int kStageBytes = kABytes + kBBytes;
     static constexpr int kStagesRaw = (kSmemBudget - 2048) / kStageBytes;
-    static constexpr int kStagesCap = KIND == kG1Swap ? MOE_SWAP_STAGES_G1 : KIND == kG2Swap ? MOE_SWAP_STAGES_G2 : 8;
+    static constexpr int kStagesCap = KIND == kG1Swap ? MOE_SWAP_STAGES_G1
+                                    : (KIND == kG2Swap || KIND == kG2Dual) ? MOE_SWAP_STAGES_G2 : 8;
     static constexpr int kStages = kStagesRaw > kStagesCap ? kStagesCap : kStagesRaw;
     static constexpr int kSmemBytes = kStages * kStageBytes + 2048;  // + barriers + 1 KB align slack
     // TMEM: 512 columns = kAccStages x kAccCols. The w1|w3 swap tile with NB = 256 token
@@ -148,6 +151,7 @@ __device__ __forceinline__ int tiles_of(int n_e, const GemmParams& p) {
     if (KIND == kG1Tiled) return ((n_e + 127) / 128) * (p.f / 128);
     if (KIND == kG2Tiled) return ((n_e + 127) / 128) * ((p.d + 255) / 256);
     if (KIND == kG1Swap) return ((n_e + NB - 1) / NB) * (p.f / 128);
+    if (KIND == kG2Dual) return ((n_e + NB - 1) / NB) * ((p.d + 255) / 256) * p.splits;
     return ((n_e + NB - 1) / NB) * ((p.d + 127) / 128) * p.splits;  // kG2Swap
 }
 
@@ -178,13 +182,13 @@ __device__ __forceinline__ bool decode_tile(int t, const GemmParams& p, const in
         int nt = (ti.rows + NB - 1) / NB;
         ti.n_idx = t % nt;             // token tiles fastest: same weight tile back-to-back
         int rest = t / nt;
-        int wt = (KIND == kG1Swap) ? (p.f / 128) : ((p.d + 127) / 128);
+        int wt = (KIND == kG1Swap) ? (p.f / 128) : (KIND == kG2Dual) ? ((p.d + 255) / 256) : ((p.d + 127) / 128);
         ti.m_idx = rest % wt;
         ti.split = rest / wt;
-        ti.a_row = ti.m_idx * (KIND == kG1Swap ? 256 : 128);
+        ti.a_row = ti.m_idx * ((KIND == kG1Swap || KIND == kG2Dual) ? 256 : 128);
         ti.b_row = ti.seg + ti.n_idx * NB;
         int nkb_all = (KIND == kG1Swap ? p.d : p.f) / KBLK;
-        int S = (KIND == kG2Swap) ? p.splits : 1;
+        int S = (KIND == kG2Swap || KIND == kG2Dual) ? p.splits : 1;
         ti.kb0 = (nkb_all * ti.split) / S;
         ti.nkb = (nkb_all * (ti.split + 1)) / S - ti.kb0;
         int rem = ti.rows - ti.n_idx * NB;
@@ -380,6 +384,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                         const WCoord w = wcoord(p, (t0.kb0 + kb) * kBK, t0.a_row, t0.e);
                         ptx::tma_load_4d(&tmA, &full[kb], smem_a + kb * C::kABytes, 0, w.c1, w.c2, w.c3,
                                          w_hint);
+                        if (KIND == kG2Dual) {  // second 128-row W2 tile of the unit
+                            const WCoord w2 = wcoord(p, (t0.kb0 + kb) * kBK, t0.a_row + 128, t0.e);
+                            ptx::tma_load_4d(&tmA, &full[kb], smem_a + kb * C::kABytes + 128 * 128, 0, w2.c1,
+                                             w2.c2, w2.c3, w_hint);
+                        }
                     }
                     }
             }
@@ -412,6 +421,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                         if (!armed) {
                             const WCoord w = wcoord(p, kc, ti.a_row, ti.e);
                             ptx::tma_load_4d(&tmA, &full[stage], sa, 0, w.c1, w.c2, w.c3, w_hint);
+                            if (KIND == kG2Dual) {
+                                const WCoord w2 = wcoord(p, kc, ti.a_row + 128, ti.e);
+                                ptx::tma_load_4d(&tmA, &full[stage], sa + 128 * 128, 0, w2.c1, w2.c2, w2.c3, w_hint);
+                            }
                         }
                         // B = permuted tokens / activations (2D map [K, Cap]): keep in L2.
                         if (nb32) {
@@ -468,8 +481,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                     for (int kk = 0; kk < kBK / 16; ++kk) {
                         const uint32_t accum = (kb | kk) ? 1u : 0u;
                         ptx::mma_bf16(d_tmem, adesc + 2 * kk, bdesc + 2 * kk, idesc, accum);
-                        if (KIND == kG1Swap) {
-                            // w3 half of the 256-row A tile (rows 128..255, +16 KB) -> columns +128
+                        if (KIND == kG1Swap || KIND == kG2Dual) {
+                            // w3 half (kG2Dual: second W2 tile) of the 256-row A tile (rows 128..255, +16 KB)
                             const uint64_t adesc3 = ptx::make_smem_desc_sw128(sa + 128 * 128);
                             ptx::mma_bf16(d_tmem + C::kBOff, adesc3 + 2 * kk, bdesc + 2 * kk, idesc, accum);
                         }
@@ -600,6 +613,28 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                         if (n < ti.n_valid) {
                             float hv = silu_f32(__uint_as_float(a[i])) * __uint_as_float(b[i]);
                             h[static_cast<int64_t>(n) * p.f] = __float2bfloat16_rn(hv);
+                        }
+                    }
+                }
+            } else if (KIND == kG2Dual) {
+                // rows r and 128 + r of the 256-row unit = hidden m*256 + r (+128); col n = token
+#pragma unroll 1
+                for (int half = 0; half < 2; ++half) {
+                    const int drow = ti.m_idx * 256 + half * 128 + r;
+                    float* y = static_cast<float*>(p.out) + p.out_split_stride * ti.split +
+                               static_cast<int64_t>(ti.b_row) * p.d + drow;
+                    const int nchunks = (ti.n_valid + 15) / 16;
+#pragma unroll 1
+                    for (int c = 0; c < nchunks; ++c) {
+                        uint32_t v[16];
+                        ptx::tmem_ld16(tbase + half * C::kBOff + c * 16, v);
+                        ptx::tmem_wait_ld();
+                        if (drow < p.d) {
+#pragma unroll
+                            for (int i = 0; i < 16; ++i) {
+                                const int n = c * 16 + i;
+                                if (n < ti.n_valid) y[static_cast<int64_t>(n) * p.d] = __uint_as_float(v[i]);
+                            }
                         }
                     }
                 }

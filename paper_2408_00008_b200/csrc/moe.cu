@@ -300,6 +300,13 @@ struct moe_ctx {
     // effect (decode 0.4119 vs 0.4119 ms over 4 interleaved rounds, stack within noise;
     // profiles/r01/experiments/ab_early_dep.log); parity suite green with it on.
     int early_dep = 0;
+    // env MOE_G2_DUAL=1: the decode w2 GEMM on 256-row units (kG2Dual, two W2 tiles per
+    // unit, 32 KB of weights per stage like the w1/w3 GEMM), NB <= 128, bf16. Off: parity
+    // green but no gain (w2 GEMM 142.6 vs 143.2 us, step within noise over 4 interleaved
+    // rounds, profiles/r01/experiments/ab_g2dual.log) -- the box size is not what holds
+    // the w2 GEMM below the w1/w3 GEMM's streaming rate.
+    int g2_dual = 0;
+    bool g2_dual_now = false;
     int g1_grid_now = 0, g2_grid_now = 0;  // the current forward's choice
     CUtensorMap tm_src{};        // gather map over the current call's tokens [T, d], box {64, 1}
     float* y = nullptr;
@@ -728,6 +735,10 @@ moe_status run_swap_g2(moe_ctx* c, int nbi, const moe_expert_weights* w, int spl
         }
     p2.b_rows32 = c->trim_b;
     p2.early_dep = c->early_dep;
+    if constexpr (NB <= 128)
+        if (c->g2_dual_now)
+            return launch_gemm<kG2Dual, NB>(c, kSlotGemm2, p2, c->tm_w2_swap, c->tm_h_swap[c->trim_b ? 0 : nbi],
+                                            c->g2_grid_now, st);
     return launch_gemm<kG2Swap, NB>(c, kSlotGemm2, p2, c->tm_w2_swap, c->tm_h_swap[c->trim_b ? 0 : nbi],
                                     c->g2_grid_now, st);
 }
@@ -925,8 +936,9 @@ moe_status run_gemms(moe_ctx* c, GemmPaths gp, int64_t rows_bound, int64_t rows_
         splits = std::min(splits, c->f_local / (c->fp8_g2_kb256 ? 256 : c->fp8_kb128 ? 128 : kBK));  // >= 1 K block per split
         c->split_stride = rows_needed * c->d;
         c->rows_needed_cur = std::min<int64_t>(rows_needed, c->cap);
+        c->g2_dual_now = c->g2_dual && !c->fp8 && nb2 <= 128 && !c->trim_b;
         {
-            const int64_t U = (int64_t)c->E_local * ((c->d + 127) / 128) * splits;
+            const int64_t U = (int64_t)c->E_local * ((c->d + (c->g2_dual_now ? 255 : 127)) / (c->g2_dual_now ? 256 : 128)) * splits;
             const int ns = c->num_sms;
             const int64_t waves = (U + ns - 1) / ns;
             c->g2_grid_now = c->g2_grid > 0 ? std::min(c->g2_grid, ns)
@@ -1326,6 +1338,7 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
     if (const char* v = getenv("MOE_TRIM_B")) c->trim_b = atoi(v) != 0;
     if (const char* v = getenv("MOE_G1_GRID")) c->g1_grid = std::max(0, atoi(v));
     if (const char* v = getenv("MOE_EARLY_DEP")) c->early_dep = atoi(v) != 0;
+    if (const char* v = getenv("MOE_G2_DUAL")) c->g2_dual = atoi(v) != 0;
     if (const char* v = getenv("MOE_G2_GRID")) c->g2_grid = std::max(0, atoi(v));
     if (const char* v = getenv("MOE_HOST_ZERO_COPY")) c->host_zero_copy = atoi(v) != 0;
     if (const char* v = getenv("MOE_SWAP_HINT")) c->swap_hint_mode = atoi(v);
@@ -1470,6 +1483,8 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
     moe_status as;
     if ((as = set_gemm_attr<kG1Tiled, 256>(c)) || (as = set_gemm_attr<kG2Tiled, 256>(c)) ||
         (as = set_gemm_attr<kG1Swap, 32>(c)) || (as = set_gemm_attr<kG2Swap, 32>(c)) ||
+        (as = set_gemm_attr<kG2Dual, 32>(c)) || (as = set_gemm_attr<kG2Dual, 64>(c)) ||
+        (as = set_gemm_attr<kG2Dual, 128>(c)) ||
         (as = set_gemm_attr<kG1Swap, 64>(c)) || (as = set_gemm_attr<kG2Swap, 64>(c)) ||
         (as = set_gemm_attr<kG1Swap, 128>(c)) || (as = set_gemm_attr<kG2Swap, 128>(c)) ||
         (as = set_gemm_attr<kG2Swap, 256>(c)) ||
@@ -1504,6 +1519,8 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
             reinterpret_cast<const void*>(moe_gemm_kernel<kG1Swap, 32>), reinterpret_cast<const void*>(moe_gemm_kernel<kG2Swap, 32>),
             reinterpret_cast<const void*>(moe_gemm_kernel<kG1Swap, 64>), reinterpret_cast<const void*>(moe_gemm_kernel<kG2Swap, 64>),
             reinterpret_cast<const void*>(moe_gemm_kernel<kG1Swap, 128>), reinterpret_cast<const void*>(moe_gemm_kernel<kG2Swap, 128>),
+            reinterpret_cast<const void*>(moe_gemm_kernel<kG2Dual, 32>), reinterpret_cast<const void*>(moe_gemm_kernel<kG2Dual, 64>),
+            reinterpret_cast<const void*>(moe_gemm_kernel<kG2Dual, 128>),
             reinterpret_cast<const void*>(moe_gemm_kernel<kG2Swap, 256>), reinterpret_cast<const void*>(moe_gemm_pair_kernel<kG1Pair, 1>),
             reinterpret_cast<const void*>(moe_gemm_pair_kernel<kG2Pair, 1>), reinterpret_cast<const void*>(moe_gemm_pair_kernel<kG1Pair, 2>),
             reinterpret_cast<const void*>(moe_gemm_pair_kernel<kG2Pair, 2>),
