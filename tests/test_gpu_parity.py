@@ -258,6 +258,19 @@ def test_speculative_prefetch_wrong_guess(moe, T):
     check_forward(run, host, 2)
 
 
+@pytest.mark.parametrize("d", [384, 512])
+def test_g2_dual_units(moe, d, monkeypatch):
+    """Optional 256-row-unit w2 GEMM (MOE_G2_DUAL=1, read at moe_init): oracle parity,
+    including a hidden size whose last unit is half padding (d = 384)."""
+    monkeypatch.setenv("MOE_G2_DUAL", "1")
+    shape = synth.MoEShape(T=40, d=d, f=512, E=8, k=2)
+    inp = _inputs(shape, 300 + d)
+    host = to_host_inputs(inp)
+    blk = _block(moe, inp, 2, 40, MODES["swap"])
+    check_forward(GpuRun(blk, inp["x"]), host, 2)
+    blk.close()
+
+
 def test_t_zero_and_determinism(moe):
     inp = _inputs(synth.TINY, 3)
     blk = _block(moe, inp, 2, 16)
