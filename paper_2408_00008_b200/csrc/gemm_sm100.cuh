@@ -99,6 +99,9 @@ constexpr int kSmemBudget = 232448;     // 227 KB opt-in dynamic shared memory p
 // stages of 32 KB (scripts/exp/read_bw.cu: 7.27 TB/s at 3, 6.78 at 7), but the GEMMs
 // want the full ring: r01 decode step 0.4364 ms at (G1 5 = smem limit, G2 8) vs
 // 0.4393 (5,5), 0.4399 (4,6), 0.547 (4,4), 0.613 ms (3,3).
+// Re-measured on the 112/128-CTA decode grids (profiles/r01/experiments/ab_build_vars*.log):
+// G2 stages 5 -> 0.4210 ms, 6 -> 0.4154, 8 -> 0.4124, 9 -> 0.4119 (noise); MOE_PDL_PREFETCH=0
+// 0.4122 (the pre-wait weight stages no longer matter at this grid).
 #ifndef MOE_SWAP_STAGES_G1
 #define MOE_SWAP_STAGES_G1 8
 #endif
