@@ -342,7 +342,7 @@ def mixtral_weights():
     return w, host
 
 
-@pytest.mark.parametrize("seed", [0, 1])
+@pytest.mark.parametrize("seed", [0, 1, 2, 3, 4])  # C2 x 5 parity seeds
 def test_c2_decode_full(moe, mixtral_weights, seed):
     """64-token decode at Mixtral size, all tokens checked against the oracle."""
     w, host = mixtral_weights
@@ -373,15 +373,16 @@ def test_c2_speculative_prefetch_bit_identical(moe, mixtral_weights, monkeypatch
     assert torch.equal(outs[0].view(torch.int16), outs[2].view(torch.int16))
 
 
-def test_c3_prefill_full(moe, mixtral_weights):
+@pytest.mark.parametrize("seed", [0, 1])  # C3 x 2 parity seeds
+def test_c3_prefill_full(moe, mixtral_weights, seed):
     """32k-token prefill: full routing + permutation exact, outputs on sampled tokens."""
     w, host = mixtral_weights
     T = 32768
-    x = synth.make_tokens(T, 4096, seed=200, device="cuda")
+    x = synth.make_tokens(T, 4096, seed=200 + seed, device="cuda")
     blk = moe.MoEBlock(w["wg"], w["w1"], w["w3"], w["w2"], top_k=2, max_tokens=T)
     run = GpuRun(blk, x)
     h = dict(host, x=synth.bf16_bits(x))
-    rng = np.random.default_rng(0)
+    rng = np.random.default_rng(seed)
     toks = np.unique(np.concatenate([[0, 1, 63, 64, T - 1], rng.choice(T, 27, replace=False)]))
     st = check_forward(run, h, 2, tokens=toks, literal_bf16=False)
     print("C3", st)
