@@ -293,8 +293,9 @@ struct moe_ctx {
     // (profiles/r01/experiments/ab_grid*.log): w1/w3 grid 148 -> 282.4 us, 136 -> 296,
     // 128 -> ~283, 120 -> 278.7, 112 -> 266.8 (7.06 TB/s), 104 -> 274, 96 -> 286; w2 grid
     // 148 -> 154.8 us, 136 -> 146, 128 -> 142.7, 112 -> 207; step 0.4340 -> 0.4124 ms.
-    // bf16 only: the FP8 kernels are slower on the smaller grids (ab_grid_fp8.log: w1/w3
-    // 165 -> 184 us at 112, w2 94 -> 105 us at 128), so they keep one CTA per SM.
+    // These two rules are bf16 only: the FP8 kernels are slower on them (ab_grid_fp8.log:
+    // w1/w3 165 -> 184 us at 112, w2 94 -> 105 us at 128); the FP8 w1/w3 GEMM takes equal
+    // waves instead (run_gemms), the FP8 w2 GEMM one CTA per SM.
     int g1_grid = 0, g2_grid = 0;
     // env MOE_EARLY_DEP=1: GemmParams::early_dep for the bf16 swap GEMMs. Off: no measurable
     // effect (decode 0.4119 vs 0.4119 ms over 4 interleaved rounds, stack within noise;

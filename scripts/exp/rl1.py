@@ -1,3 +1,5 @@
+"""Six small-ffn decode forwards (T from argv) for an ncu capture of the router / permute /
+combine kernels: ncu ... -k regex:"router|permute|combine" python scripts/exp/rl1.py 64"""
 import os, sys
 sys.path.insert(0, os.getcwd())
 import torch, synth
