@@ -45,7 +45,7 @@
 extern "C" {
 #endif
 
-#define MOE_ABI_VERSION 1
+#define MOE_ABI_VERSION 2
 
 #if defined(__GNUC__)
 #define MOE_API __attribute__((visibility("default")))
@@ -105,6 +105,36 @@ typedef enum {
                                       buffer. Bit-identical results; measured
                                       SLOWER on B200, so off by default            */
 
+/* Tuning overrides (moe_config.tuning; NULL = the measured defaults). These change
+ * only which kernel variant / grid / tile order runs, never the arithmetic of the
+ * block: every setting is covered by the parity tests (tests/test_gpu_parity.py).
+ * A zero field keeps the default; the library reads nothing from the environment
+ * (except MOE_NCCL_LIB, the path of libnccl.so.2 to dlopen).                     */
+typedef struct moe_tuning {
+    int32_t g1_swap_rows;   /* w1/w3 GEMM on the decode (swap-AB) kernels while the mean rows
+                               per local expert is <= this (0: 256); tiles beyond           */
+    int32_t g2_swap_rows;   /* w2 GEMM, same rule (0: 256)                                   */
+    int32_t g1_grid;        /* decode w1/w3 GEMM CTAs (0: auto)                */
+    int32_t g2_grid;        /* decode w2 GEMM CTAs (0: auto)                                 */
+    int32_t spec_l2;        /* decode speculative L2 weight prefetch, K blocks per CTA
+                               (0: 48; < 0: off)                                              */
+    int32_t swap_nb_cap;    /* cap the swap-AB token tile at 32/64/128 rows (0: no cap): an
+                               expert with more rows runs several token tiles               */
+    int32_t pair_nblk;      /* prefill CTA-pair tile width in 256-column blocks, 1 or 2 (0: 2) */
+    int32_t pair_order;     /* prefill tile-order override (0: default): bits 0-1 w1/w3 order,
+                               2-3 w2 order, 4-9 w1/w3 band, 10-15 w2 band (tiles)          */
+    int32_t router_cc_max_T;/* CUDA-core router for T <= this (0: tensor-core router, E <= 8) */
+    int32_t weight_hint;    /* L2 policy of the decode weight stream: 0 auto, 1 evict-first,
+                               2 evict-normal, 3 evict-last                                  */
+    int32_t host_stage;     /* moe_forward_host: 1 = always stage the output on the device and
+                               copy it back (0: pinned output written directly)             */
+    int32_t fp8_fp16_tokens;/* FP8 weights: 1 = w1/w3 GEMM on fp16 tokens with converter warps
+                               instead of two E4M3 token terms on kind::f8f6f4 (0)          */
+    int32_t fp8_w2_split;   /* FP8 weights: 1 = w2 GEMM on three E4M3 terms of h
+                               (kind::f8f6f4) instead of fp16 h with converter warps (0)    */
+    int32_t reserved[11];   /* must be zero                                                  */
+} moe_tuning;
+
 typedef struct {
     int32_t hidden;      /* d: 4096 for Mixtral (C1: 64). Must be a multiple of 64.   */
     int32_t ffn;         /* f: 14336 for Mixtral (C1: 128). f/G must be a multiple of 128. */
@@ -120,7 +150,8 @@ typedef struct {
     int32_t device;      /* CUDA device ordinal the context binds to; -1 = current    */
     int32_t tp_size;     /* MOE_PAR_HYBRID: TP degree (world_size = ep * tp_size); else 0 */
     void* tp_comm;       /* MOE_PAR_HYBRID: communicator of my TP group; else NULL      */
-    int32_t reserved[3]; /* must be zero                                               */
+    const moe_tuning* tuning; /* optional overrides (copied at moe_init); NULL = defaults */
+    int32_t reserved[2]; /* must be zero                                               */
 } moe_config;
 
 /* Packed expert weights of THIS rank (device, produced by moe_pack_weights).

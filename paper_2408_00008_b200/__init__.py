@@ -47,12 +47,22 @@ EXPORTED = ("moe_init", "moe_packed_sizes", "moe_pack_weights", "moe_forward", "
             "moe_p2p_connect")
 
 
+TUNING_FIELDS = ("g1_swap_rows", "g2_swap_rows", "g1_grid", "g2_grid", "spec_l2", "swap_nb_cap", "pair_nblk",
+                 "pair_order", "router_cc_max_T", "weight_hint", "host_stage", "fp8_fp16_tokens", "fp8_w2_split")
+
+
+class moe_tuning(ctypes.Structure):
+    """include/moe.h moe_tuning: kernel-variant / grid overrides (0 = default)."""
+    _fields_ = [(n, ctypes.c_int32) for n in TUNING_FIELDS] + [("reserved", ctypes.c_int32 * 11)]
+
+
 class moe_config(ctypes.Structure):
     _fields_ = [("hidden", ctypes.c_int32), ("ffn", ctypes.c_int32), ("num_experts", ctypes.c_int32),
                 ("top_k", ctypes.c_int32), ("max_tokens", ctypes.c_int32), ("par", ctypes.c_int32),
                 ("world_size", ctypes.c_int32), ("rank", ctypes.c_int32), ("nccl_comm", ctypes.c_void_p),
                 ("flags", ctypes.c_uint32), ("split_k", ctypes.c_int32), ("device", ctypes.c_int32),
-                ("tp_size", ctypes.c_int32), ("tp_comm", ctypes.c_void_p), ("reserved", ctypes.c_int32 * 3)]
+                ("tp_size", ctypes.c_int32), ("tp_comm", ctypes.c_void_p),
+                ("tuning", ctypes.POINTER(moe_tuning)), ("reserved", ctypes.c_int32 * 2)]
 
 
 class moe_expert_weights(ctypes.Structure):
@@ -127,13 +137,29 @@ def _stream(stream):
     return stream.cuda_stream
 
 
+def make_tuning(tuning=None):
+    """dict of moe_tuning fields (unknown names raise) -> moe_tuning, or None."""
+    if not tuning:
+        return None
+    t = moe_tuning()
+    for k, v in tuning.items():
+        if k not in TUNING_FIELDS:
+            raise KeyError(f"unknown tuning field {k!r} (fields: {TUNING_FIELDS})")
+        setattr(t, k, int(v))
+    return t
+
+
 def make_config(hidden, ffn, num_experts, top_k, max_tokens, par=MOE_PAR_NONE, world_size=1, rank=0,
-                nccl_comm=None, flags=0, split_k=0, device=-1, tp_size=0, tp_comm=None) -> moe_config:
+                nccl_comm=None, flags=0, split_k=0, device=-1, tp_size=0, tp_comm=None, tuning=None) -> moe_config:
     c = moe_config()
     c.hidden, c.ffn, c.num_experts, c.top_k, c.max_tokens = hidden, ffn, num_experts, top_k, max_tokens
     c.par, c.world_size, c.rank, c.nccl_comm = par, world_size, rank, nccl_comm
     c.flags, c.split_k, c.device = flags, split_k, device
     c.tp_size, c.tp_comm = tp_size, tp_comm
+    t = make_tuning(tuning) if not isinstance(tuning, moe_tuning) else tuning
+    if t is not None:
+        c._tuning_ref = t  # keep the struct alive as long as the config (moe_init copies it)
+        c.tuning = ctypes.pointer(t)
     return c
 
 
@@ -313,14 +339,15 @@ class MoEBlock:
     """
 
     def __init__(self, router_w, w1, w3, w2, top_k=2, max_tokens=64, par=MOE_PAR_NONE, world_size=1, rank=0,
-                 nccl_comm=None, flags=0, split_k=0, device=None, tp_size=0, tp_comm=None):
+                 nccl_comm=None, flags=0, split_k=0, device=None, tp_size=0, tp_comm=None, tuning=None):
         """FP8 weights: pass flags |= MOE_FLAG_FP8_WEIGHTS and w1/w3/w2 as (q, scale) pairs
-        (synth.quantize_fp8_rows)."""
+        (synth.quantize_fp8_rows). tuning: dict of moe_tuning overrides (include/moe.h)."""
         dev = router_w.device if device is None else torch.device(device)
         w1_fp8 = (w1, w3, w2) if flags & MOE_FLAG_FP8_WEIGHTS else None
         E, f, d = (w1[0] if w1_fp8 else w1).shape
         self.cfg = make_config(d, f, E, top_k, max_tokens, par, world_size, rank, nccl_comm, flags, split_k,
-                               dev.index if dev.index is not None else torch.cuda.current_device(), tp_size, tp_comm)
+                               dev.index if dev.index is not None else torch.cuda.current_device(), tp_size, tp_comm,
+                               tuning)
         self.ctx = moe_init(self.cfg)
         self.d, self.f, self.E, self.k = d, f, E, top_k
         self.router_w = router_w.contiguous()
@@ -384,13 +411,13 @@ class MoEStack:
     """
 
     def __init__(self, layers, top_k=2, max_tokens=64, par=MOE_PAR_NONE, world_size=1, rank=0, nccl_comm=None,
-                 flags=0, split_k=0, device=None):
+                 flags=0, split_k=0, device=None, tuning=None):
         first = layers[0]
         dev = first["wg"].device if device is None else torch.device(device)
         E, f, d = first["w1"].shape
         self.cfg = make_config(d, f, E, top_k, max_tokens, par, world_size, rank, nccl_comm,
                                flags | MOE_FLAG_RESIDUAL, split_k,
-                               dev.index if dev.index is not None else torch.cuda.current_device())
+                               dev.index if dev.index is not None else torch.cuda.current_device(), tuning=tuning)
         self.ctx = moe_init(self.cfg)
         self.d, self.T_max = d, max_tokens
         b13, b2 = moe_packed_sizes(self.cfg)
@@ -414,15 +441,18 @@ class MoEStack:
     def num_layers(self):
         return len(self.w13)
 
-    def forward(self, x, out=None, stream=None, layer_outputs=None):
+    def forward(self, x, out=None, stream=None, layer_outputs=None, layer_aux=None):
         """x [T, d] bf16 -> out [T, d] bf16 after all layers. layer_outputs: optional
         list that receives each layer's output tensor (views of internal buffers are
-        cloned) -- used by the per-layer parity tests."""
+        cloned); layer_aux: optional list of per-layer moe_aux dicts (or None) filled by
+        the layer's forward (routing, out_f32 before the rounding) -- both used by the
+        per-layer parity tests."""
         T = x.shape[0]
         cur = x
         for l in range(self.num_layers):
             dst = out if (l == self.num_layers - 1 and out is not None) else self._buf[l % 2][:T]
-            moe_forward(self.ctx, cur, T, self.router_w[l], self.w13[l], self.w2[l], dst, None, stream)
+            aux = layer_aux[l] if layer_aux is not None else None
+            moe_forward(self.ctx, cur, T, self.router_w[l], self.w13[l], self.w2[l], dst, aux, stream)
             if layer_outputs is not None:
                 layer_outputs.append(dst.clone())
             cur = dst

@@ -29,9 +29,7 @@
 
 namespace moe {
 
-// kG2Dual: kG2Swap whose unit is TWO 128-row W2 tiles (256 hidden rows, two 16 KB boxes
-// per stage, two M=128 MMAs into two TMEM accumulators, as kG1Swap does with w1/w3).
-enum GemmKind : int { kG1Tiled = 0, kG2Tiled = 1, kG1Swap = 2, kG2Swap = 3, kG1Pair = 4, kG2Pair = 5, kG2Dual = 6 };
+enum GemmKind : int { kG1Tiled = 0, kG2Tiled = 1, kG1Swap = 2, kG2Swap = 3, kG1Pair = 4, kG2Pair = 5 };
 
 struct GemmParams {
     const int32_t* counts;   // [E] rows per local expert (device, from the permute step)
@@ -49,12 +47,6 @@ struct GemmParams {
     // then fetched with TMA tile::gather4 straight from the caller's rows (its map has a
     // {64, 1} box) instead of from a materialised permuted copy.
     const int32_t* src_row;
-    // kG1Swap tail split (nullable): workspace for the fp32 partial accumulators of the
-    // K-sliced tail tiles ([<= grid][2][128][NB]) and their arrival counters (zeroed;
-    // each is reset by the CTA that completes its tile); tail_parts: max slices per tile.
-    float* tail_ws;
-    int32_t* tail_cnt;
-    int32_t tail_parts;
     // bf16 weights in the tiled packed layout (moe.cu, pack kernels): each expert's rows
     // in tiles of w_tr rows, each tile stored as d/64 (or f/64) consecutive [w_tr][64]
     // blocks, so one K block of one tile is one contiguous chunk of HBM. w_nt: tiles
@@ -72,14 +64,6 @@ struct GemmParams {
     // kernel reads counts / offsets after griddepcontrol.wait (it may launch before the
     // router has finished).
     int32_t spec_l2;
-    // swap kinds: tmB has a 32-row box and the producer loads only ceil(n_valid / 32)
-    // boxes of the token operand per stage (stacked 4 KB apart: the 128-byte swizzle is
-    // address-based, so the smem image equals one NB-row box) instead of all NB rows.
-    int32_t b_rows32;
-    // swap kinds: trigger the dependent grid (PDL) right after the prologue instead of at
-    // the end, so its CTAs can take SMs this grid leaves idle (smaller decode grids) and
-    // run their prologue / pre-wait weight stages early (moe.cu early_dep)
-    int32_t early_dep;
 };
 
 // 4D coordinates of rows [row, row + box) of expert e at K offset kc in a tiled weight map
@@ -110,17 +94,17 @@ constexpr int kSmemBudget = 232448;     // 227 KB opt-in dynamic shared memory p
 #endif
 template <int KIND, int NB>
 struct GemmCfg {
-    static constexpr bool kSwap = (KIND == kG1Swap || KIND == kG2Swap || KIND == kG2Dual);
+    static constexpr bool kSwap = (KIND == kG1Swap || KIND == kG2Swap);
     static constexpr bool kG1 = (KIND == kG1Tiled || KIND == kG1Swap);
     // bytes per stage of each operand (rows x 128 B)
-    static constexpr int kARows = (KIND == kG1Swap || KIND == kG2Dual) ? 256 : 128;
+    static constexpr int kARows = KIND == kG1Swap ? 256 : 128;
     static constexpr int kBRows = kSwap ? NB : 256;
     static constexpr int kABytes = kARows * 128;
     static constexpr int kBBytes = kBRows * 128;
     static constexpr int kStageBytes = kABytes + kBBytes;
     static constexpr int kStagesRaw = (kSmemBudget - 2048) / kStageBytes;
     static constexpr int kStagesCap = KIND == kG1Swap ? MOE_SWAP_STAGES_G1
-                                    : (KIND == kG2Swap || KIND == kG2Dual) ? MOE_SWAP_STAGES_G2 : 8;
+                                    : KIND == kG2Swap ? MOE_SWAP_STAGES_G2 : 8;
     static constexpr int kStages = kStagesRaw > kStagesCap ? kStagesCap : kStagesRaw;
     static constexpr int kSmemBytes = kStages * kStageBytes + 2048;  // + barriers + 1 KB align slack
     // TMEM: 512 columns = kAccStages x kAccCols. The w1|w3 swap tile with NB = 256 token
@@ -142,8 +126,6 @@ struct TileInfo {
     int32_t kb0, nkb; // K-block range
     int32_t m_idx, n_idx, split;
     int32_t n_valid;  // swap: valid token columns in this tile
-    int32_t part;     // tail split: K slice of this unit (-1: whole tile)
-    int32_t lidx;     // tail split: index of the tail tile
 };
 
 // Number of tiles of expert e and the tile decode. Both must be identical in
@@ -154,7 +136,6 @@ __device__ __forceinline__ int tiles_of(int n_e, const GemmParams& p) {
     if (KIND == kG1Tiled) return ((n_e + 127) / 128) * (p.f / 128);
     if (KIND == kG2Tiled) return ((n_e + 127) / 128) * ((p.d + 255) / 256);
     if (KIND == kG1Swap) return ((n_e + NB - 1) / NB) * (p.f / 128);
-    if (KIND == kG2Dual) return ((n_e + NB - 1) / NB) * ((p.d + 255) / 256) * p.splits;
     return ((n_e + NB - 1) / NB) * ((p.d + 127) / 128) * p.splits;  // kG2Swap
 }
 
@@ -185,61 +166,19 @@ __device__ __forceinline__ bool decode_tile(int t, const GemmParams& p, const in
         int nt = (ti.rows + NB - 1) / NB;
         ti.n_idx = t % nt;             // token tiles fastest: same weight tile back-to-back
         int rest = t / nt;
-        int wt = (KIND == kG1Swap) ? (p.f / 128) : (KIND == kG2Dual) ? ((p.d + 255) / 256) : ((p.d + 127) / 128);
+        int wt = (KIND == kG1Swap) ? (p.f / 128) : ((p.d + 127) / 128);
         ti.m_idx = rest % wt;
         ti.split = rest / wt;
-        ti.a_row = ti.m_idx * ((KIND == kG1Swap || KIND == kG2Dual) ? 256 : 128);
+        ti.a_row = ti.m_idx * (KIND == kG1Swap ? 256 : 128);
         ti.b_row = ti.seg + ti.n_idx * NB;
         int nkb_all = (KIND == kG1Swap ? p.d : p.f) / KBLK;
-        int S = (KIND == kG2Swap || KIND == kG2Dual) ? p.splits : 1;
+        int S = KIND == kG2Swap ? p.splits : 1;
         ti.kb0 = (nkb_all * ti.split) / S;
         ti.nkb = (nkb_all * (ti.split + 1)) / S - ti.kb0;
         int rem = ti.rows - ti.n_idx * NB;
         ti.n_valid = rem < NB ? rem : NB;
     }
     return true;
-}
-
-// Tail split of the decode w1/w3 GEMM. Its tiles all stream the same bytes (256
-// weight rows x d), so with `total` tiles on G persistent CTAs the last
-// left = total % G tiles keep `left` SMs busy for a whole tile while the others idle
-// (Mixtral decode: 896 tiles on 148 SMs -> 8 SMs run a 7th tile; a streaming-read
-// model of that split reaches 6.59 TB/s vs 7.2 TB/s balanced, scripts/exp/read_bw.cu).
-// When left <= G/2, each tail tile instead runs as P K-slices on P CTAs; the slices'
-// fp32 accumulators meet in a workspace and the CTA that completes a tile sums them in
-// slice order (deterministic) and applies SwiGLU.
-struct TailPlan {
-    int full, P, units;
-};
-__device__ __forceinline__ TailPlan tail_plan(int total, int G, int nkb, const GemmParams& p) {
-    TailPlan tp{total, 1, total};
-    if (p.tail_ws == nullptr || total <= G) return tp;
-    const int left = total % G;
-    if (left == 0 || 2 * left > G) return tp;
-    const int P = min(G / left, min(p.tail_parts, nkb / 2));
-    if (P < 2) return tp;
-    tp.full = total - left;
-    tp.P = P;
-    tp.units = tp.full + left * P;
-    return tp;
-}
-
-template <int KIND, int NB>
-__device__ __forceinline__ void decode_unit(int u, const TailPlan& tp, const GemmParams& p, const int32_t* s_counts,
-                                            const int32_t* s_offsets, TileInfo& ti) {
-    if (u < tp.full) {
-        decode_tile<KIND, NB>(u, p, s_counts, s_offsets, ti);
-        ti.part = -1;
-        ti.lidx = 0;
-        return;
-    }
-    const int v = u - tp.full, l = v / tp.P, part = v % tp.P;
-    decode_tile<KIND, NB>(tp.full + l, p, s_counts, s_offsets, ti);
-    const int nk = ti.nkb, k0 = ti.kb0;
-    ti.kb0 = k0 + nk * part / tp.P;
-    ti.nkb = nk * (part + 1) / tp.P - nk * part / tp.P;
-    ti.part = part;
-    ti.lidx = l;
 }
 
 // silu(z) = z * sigmoid(z) (R11). The prefill w1/w3 epilogue evaluates it on 1.9 G
@@ -296,7 +235,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 4);
     int32_t* s_counts = reinterpret_cast<int32_t*>(bars + 2 * S + 5);      // [32]
     int32_t* s_offsets = s_counts + 32;                                    // [33]
-    volatile int32_t* tail_flag = s_offsets + 33;                          // [1]
 
     const int warp = threadIdx.x / 32;
     const int lane = threadIdx.x % 32;
@@ -331,7 +269,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     // dependents after its own griddepcontrol.wait, and the w1/w3 GEMM after its
     // wait) -- and their producer issues the first weight stages before waiting for
     // the permuted tokens / activations of the previous kernel.
-    const bool spec = KIND == kG1Swap && p.spec_l2 > 0 && p.tail_ws == nullptr && p.src_row == nullptr;
+    const bool spec = KIND == kG1Swap && p.spec_l2 > 0 && p.src_row == nullptr;
     if (spec && threadIdx.x == 0) {
         const int wt = p.f / 128;
         if ((int)blockIdx.x < p.E * wt) {
@@ -354,11 +292,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_base_slot;
-    if (C::kSwap && p.early_dep) ptx::pdl_launch_dependents();
 
     int total = 0;
     for (int e = 0; e < p.E; ++e) total += tiles_of<KIND, NB>(s_counts[e], p);
-    const TailPlan tp = KIND == kG1Swap ? tail_plan(total, gridDim.x, p.d / kBK, p) : TailPlan{total, 1, total};
     // swap kinds: L2 policy of the streamed weight tiles (hint_a; 0 = evict-first, the
     // decode default where each weight tile meets all of its expert's tokens at once)
     const uint64_t w_hint = p.hint_a ? p.hint_a : ptx::kEvictFirst;
@@ -375,32 +311,24 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         uint32_t phase = 0;
         int pre = 0;  // k-blocks of the first tile whose weight loads precede the wait
         if (C::kSwap && MOE_PDL_PREFETCH > 0 && !spec) {
-            if ((int)blockIdx.x < tp.units) {
+            if ((int)blockIdx.x < total) {
                 TileInfo t0;
-                decode_unit<KIND, NB>(blockIdx.x, tp, p, s_counts, s_offsets, t0);
+                decode_tile<KIND, NB>(blockIdx.x, p, s_counts, s_offsets, t0);
                 pre = min(S, t0.nkb);
-                const uint32_t bytes0 = C::kABytes + (p.b_rows32 ? ((t0.n_valid + 31) / 32) * 4096 : C::kBBytes);
                 if (lane == 0)
                     for (int kb = 0; kb < pre; ++kb) {  // fresh stages: no empty-wait needed
-                        ptx::mbar_arrive_expect_tx(&full[kb], bytes0);
-                    {
+                        ptx::mbar_arrive_expect_tx(&full[kb], C::kStageBytes);
                         const WCoord w = wcoord(p, (t0.kb0 + kb) * kBK, t0.a_row, t0.e);
                         ptx::tma_load_4d(&tmA, &full[kb], smem_a + kb * C::kABytes, 0, w.c1, w.c2, w.c3,
                                          w_hint);
-                        if (KIND == kG2Dual) {  // second 128-row W2 tile of the unit
-                            const WCoord w2 = wcoord(p, (t0.kb0 + kb) * kBK, t0.a_row + 128, t0.e);
-                            ptx::tma_load_4d(&tmA, &full[kb], smem_a + kb * C::kABytes + 128 * 128, 0, w2.c1,
-                                             w2.c2, w2.c3, w_hint);
-                        }
-                    }
                     }
             }
             ptx::pdl_wait();
         }
         bool first = true;
-        for (int t = blockIdx.x; t < tp.units; t += gridDim.x) {
+        for (int t = blockIdx.x; t < total; t += gridDim.x) {
             TileInfo ti;
-            decode_unit<KIND, NB>(t, tp, p, s_counts, s_offsets, ti);
+            decode_tile<KIND, NB>(t, p, s_counts, s_offsets, ti);
             const int tok_row = C::kSwap ? ti.b_row : ti.a_row;
             int4 rows = make_int4(0, 0, 0, 0);
             if (gather && lane < kTokRows / 4) {
@@ -413,28 +341,19 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 uint8_t* sb = smem_b + stage * C::kBBytes;
                 uint8_t* s_tok = C::kSwap ? sb : sa;
                 const bool armed = first && kb < pre;  // weights already in flight on this stage
-                const int nb32 = C::kSwap && p.b_rows32 ? (ti.n_valid + 31) / 32 : 0;  // 32-row token boxes
                 if (lane == 0) {
                     if (!armed) {
                         ptx::mbar_wait(&empty[stage], phase ^ 1);
-                        ptx::mbar_arrive_expect_tx(&full[stage], nb32 ? C::kABytes + nb32 * 4096 : C::kStageBytes);
+                        ptx::mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
                     }
                     if (C::kSwap) {
                         // A = weights (3D map [K, rows, E]) streamed once: evict-first.
                         if (!armed) {
                             const WCoord w = wcoord(p, kc, ti.a_row, ti.e);
                             ptx::tma_load_4d(&tmA, &full[stage], sa, 0, w.c1, w.c2, w.c3, w_hint);
-                            if (KIND == kG2Dual) {
-                                const WCoord w2 = wcoord(p, kc, ti.a_row + 128, ti.e);
-                                ptx::tma_load_4d(&tmA, &full[stage], sa + 128 * 128, 0, w2.c1, w2.c2, w2.c3, w_hint);
-                            }
                         }
                         // B = permuted tokens / activations (2D map [K, Cap]): keep in L2.
-                        if (nb32) {
-                            for (int i = 0; i < nb32; ++i)
-                                ptx::tma_load_2d(&tmB, &full[stage], sb + i * 4096, kc, ti.b_row + 32 * i,
-                                                 ptx::kEvictLast);
-                        } else if (!gather) {
+                        if (!gather) {
                             ptx::tma_load_2d(&tmB, &full[stage], sb, kc, ti.b_row, ptx::kEvictLast);
                         }
                     } else {
@@ -459,17 +378,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             uint32_t phase = 0;
             int acc = 0;
             uint32_t acc_phase = 0;
-            for (int t = blockIdx.x; t < tp.units; t += gridDim.x) {
+            for (int t = blockIdx.x; t < total; t += gridDim.x) {
                 TileInfo ti;
-                decode_unit<KIND, NB>(t, tp, p, s_counts, s_offsets, ti);
+                decode_tile<KIND, NB>(t, p, s_counts, s_offsets, ti);
                 uint32_t n_mma;
                 if (KIND == kG1Tiled) n_mma = 256;
                 else if (KIND == kG2Tiled) n_mma = min(256, p.d - ti.n_idx * 256);
                 else n_mma = (uint32_t)((ti.n_valid + 15) / 16 * 16);
                 uint32_t idesc = ptx::make_idesc_bf16(128, n_mma);
-#if defined(MOE_EXP_A_F16)
-                if (C::kSwap) idesc &= ~(7u << 7);  // experiment: A operand read as fp16 (B stays bf16)
-#endif
                 const uint32_t d_tmem = tmem_base + acc * C::kAccCols;
                 ptx::mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
                 ptx::tc_fence_after();
@@ -484,8 +400,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                     for (int kk = 0; kk < kBK / 16; ++kk) {
                         const uint32_t accum = (kb | kk) ? 1u : 0u;
                         ptx::mma_bf16(d_tmem, adesc + 2 * kk, bdesc + 2 * kk, idesc, accum);
-                        if (KIND == kG1Swap || KIND == kG2Dual) {
-                            // w3 half (kG2Dual: second W2 tile) of the 256-row A tile (rows 128..255, +16 KB)
+                        if (KIND == kG1Swap) {
+                            // w3 half of the 256-row A tile (rows 128..255, +16 KB)
                             const uint64_t adesc3 = ptx::make_smem_desc_sw128(sa + 128 * 128);
                             ptx::mma_bf16(d_tmem + C::kBOff, adesc3 + 2 * kk, bdesc + 2 * kk, idesc, accum);
                         }
@@ -503,9 +419,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         const int r = q * 32 + lane;             // accumulator row (= TMEM lane) of this thread
         int acc = 0;
         uint32_t acc_phase = 0;
-        for (int t = blockIdx.x; t < tp.units; t += gridDim.x) {
+        for (int t = blockIdx.x; t < total; t += gridDim.x) {
             TileInfo ti;
-            decode_unit<KIND, NB>(t, tp, p, s_counts, s_offsets, ti);
+            decode_tile<KIND, NB>(t, p, s_counts, s_offsets, ti);
             ptx::mbar_wait(&tmem_full[acc], acc_phase);
             ptx::tc_fence_after();
             const uint32_t tbase = tmem_base + acc * C::kAccCols + (static_cast<uint32_t>(q * 32) << 16);
@@ -550,55 +466,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                                                  __uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3]));
                     }
                 }
-            } else if (KIND == kG1Swap && ti.part >= 0) {
-                // tail slice: fp32 partials of a (w1) and b (w3) -> workspace, column-major
-                // by token so the 128 rows of a column are one coalesced 512-byte store
-                float* ws = p.tail_ws + static_cast<int64_t>(ti.lidx * tp.P + ti.part) * (2 * 128 * NB);
-                const int nchunks = (ti.n_valid + 15) / 16;
-#pragma unroll 1
-                for (int c = 0; c < nchunks; ++c) {
-                    uint32_t a[16], b[16];
-                    ptx::tmem_ld16(tbase + c * 16, a);
-                    ptx::tmem_ld16(tbase + C::kBOff + c * 16, b);
-                    ptx::tmem_wait_ld();
-#pragma unroll
-                    for (int i = 0; i < 16; ++i) {
-                        const int n = c * 16 + i;
-                        if (n < ti.n_valid) {
-                            ws[n * 128 + r] = __uint_as_float(a[i]);
-                            ws[(NB + n) * 128 + r] = __uint_as_float(b[i]);
-                        }
-                    }
-                }
-                ptx::tc_fence_before();
-                __syncwarp();
-                if (lane == 0) ptx::mbar_arrive(&tmem_empty[acc]);  // TMEM free before the fix-up
-                if (++acc == C::kAccStages) { acc = 0; acc_phase ^= 1; }
-                __threadfence();
-                asm volatile("bar.sync 1, 128;" ::: "memory");  // the 4 epilogue warps
-                if (threadIdx.x == 64) {
-                    const int old = atomicAdd(&p.tail_cnt[ti.lidx], 1);
-                    *tail_flag = old == tp.P - 1;
-                    if (old == tp.P - 1) p.tail_cnt[ti.lidx] = 0;  // all slices arrived: reset for the next launch
-                }
-                asm volatile("bar.sync 1, 128;" ::: "memory");
-                if (*tail_flag) {  // last slice of this tile: sum the slices in order, SwiGLU, h
-                    __threadfence();
-                    const float* ws0 = p.tail_ws + static_cast<int64_t>(ti.lidx * tp.P) * (2 * 128 * NB);
-                    __nv_bfloat16* h = static_cast<__nv_bfloat16*>(p.out) + static_cast<int64_t>(ti.b_row) * p.f +
-                                       ti.m_idx * 128 + r;
-                    for (int n = 0; n < ti.n_valid; ++n) {
-                        float av = 0.f, bv = 0.f;
-                        for (int q2 = 0; q2 < tp.P; ++q2) {
-                            const float* w = ws0 + static_cast<int64_t>(q2) * (2 * 128 * NB);
-                            av += __ldcg(w + n * 128 + r);
-                            bv += __ldcg(w + (NB + n) * 128 + r);
-                        }
-                        h[static_cast<int64_t>(n) * p.f] = __float2bfloat16_rn(silu_f32(av) * bv);
-                    }
-                }
-                asm volatile("bar.sync 1, 128;" ::: "memory");  // tail_flag is reused by the next slice
-                continue;
             } else if (KIND == kG1Swap) {
                 // row r = ffn index m*128 + r (w1 at cols [0,NB), w3 at cols [128,128+NB)); col n = token
                 __nv_bfloat16* h = static_cast<__nv_bfloat16*>(p.out) + static_cast<int64_t>(ti.b_row) * p.f +
@@ -616,28 +483,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                         if (n < ti.n_valid) {
                             float hv = silu_f32(__uint_as_float(a[i])) * __uint_as_float(b[i]);
                             h[static_cast<int64_t>(n) * p.f] = __float2bfloat16_rn(hv);
-                        }
-                    }
-                }
-            } else if (KIND == kG2Dual) {
-                // rows r and 128 + r of the 256-row unit = hidden m*256 + r (+128); col n = token
-#pragma unroll 1
-                for (int half = 0; half < 2; ++half) {
-                    const int drow = ti.m_idx * 256 + half * 128 + r;
-                    float* y = static_cast<float*>(p.out) + p.out_split_stride * ti.split +
-                               static_cast<int64_t>(ti.b_row) * p.d + drow;
-                    const int nchunks = (ti.n_valid + 15) / 16;
-#pragma unroll 1
-                    for (int c = 0; c < nchunks; ++c) {
-                        uint32_t v[16];
-                        ptx::tmem_ld16(tbase + half * C::kBOff + c * 16, v);
-                        ptx::tmem_wait_ld();
-                        if (drow < p.d) {
-#pragma unroll
-                            for (int i = 0; i < 16; ++i) {
-                                const int n = c * 16 + i;
-                                if (n < ti.n_valid) y[static_cast<int64_t>(n) * p.d] = __uint_as_float(v[i]);
-                            }
                         }
                     }
                 }

@@ -870,6 +870,7 @@ __global__ void __launch_bounds__(256) moe_tp_finish_kernel(const float* shard, 
 // 2-byte units): plain row-major [E_l][rows][K].
 __global__ void moe_pack_w13_kernel(const __nv_bfloat16* w1, const __nv_bfloat16* w3, __nv_bfloat16* w13p,
                                     int E_local, int e_off, int d, int f, int f_local, int f_off, int tiled) {
+    ptx::pdl_wait();  // launched with PDL: the caller's producer of w1/w3 (a cast, a copy) has finished
     const int64_t nvec_row = d / 8;
     const int64_t total = (int64_t)E_local * 2 * f_local * nvec_row;
     for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < total; v += (int64_t)gridDim.x * blockDim.x) {
@@ -888,6 +889,7 @@ __global__ void moe_pack_w13_kernel(const __nv_bfloat16* w1, const __nv_bfloat16
 }
 __global__ void moe_pack_w2_kernel(const __nv_bfloat16* w2, __nv_bfloat16* w2p, int E_local, int e_off, int d,
                                    int f, int f_local, int f_off, int tiled, int pad_rows) {
+    ptx::pdl_wait();
     const int64_t nvec_row = f_local / 8;
     const int rows = pad_rows ? (d + 255) / 256 * 256 : d;  // bf16: zero rows up to a multiple of 256
     const int64_t total = (int64_t)E_local * rows * nvec_row;
@@ -909,6 +911,7 @@ __global__ void moe_pack_w2_kernel(const __nv_bfloat16* w2, __nv_bfloat16* w2p, 
 // s13[e][256*b + i] = s1[eg][f_off + 128*b + i] (i < 128), s3[...][... + i - 128] (i >= 128)
 __global__ void moe_pack_scales_kernel(const float* s1, const float* s3, const float* s2, float* s13p, float* s2p,
                                        int E_local, int e_off, int d, int f, int f_local, int f_off) {
+    ptx::pdl_wait();
     const int64_t n13 = (int64_t)E_local * 2 * f_local, n2 = (int64_t)E_local * d;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n13 + n2; i += (int64_t)gridDim.x * blockDim.x) {
         if (i < n13) {

@@ -51,7 +51,7 @@ struct NcclApi {
     ncclResult_t (*AllReduce)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t);
     ncclResult_t (*ReduceScatter)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t);
     ncclResult_t (*AllGather)(const void*, void*, size_t, int, ncclComm_t, cudaStream_t);
-    ncclResult_t (*AlltoAll)(const void*, void*, size_t, int, ncclComm_t, cudaStream_t);
+    ncclResult_t (*AlltoAll)(const void*, void*, size_t, int, ncclComm_t, cudaStream_t);  // optional (>= 2.28)
     ncclResult_t (*Send)(const void*, size_t, int, int, ncclComm_t, cudaStream_t);
     ncclResult_t (*Recv)(void*, size_t, int, int, ncclComm_t, cudaStream_t);
     ncclResult_t (*GroupStart)();
@@ -76,13 +76,15 @@ bool load_nccl(std::string& err) {
 #define LOADSYM(field, name)                                                     \
     g_nccl.field = reinterpret_cast<decltype(g_nccl.field)>(dlsym(h, name));    \
     if (!g_nccl.field) { err = "missing NCCL symbol " name; return false; }
+    // ncclAlltoAll exists only from NCCL 2.28 (the system libnccl here is 2.27): optional,
+    // comm_alltoall falls back to grouped ncclSend / ncclRecv with the same counts
+    g_nccl.AlltoAll = reinterpret_cast<decltype(g_nccl.AlltoAll)>(dlsym(h, "ncclAlltoAll"));
     LOADSYM(GetUniqueId, "ncclGetUniqueId");
     LOADSYM(CommInitRank, "ncclCommInitRank");
     LOADSYM(CommDestroy, "ncclCommDestroy");
     LOADSYM(AllReduce, "ncclAllReduce");
     LOADSYM(ReduceScatter, "ncclReduceScatter");
     LOADSYM(AllGather, "ncclAllGather");
-    LOADSYM(AlltoAll, "ncclAlltoAll");
     LOADSYM(Send, "ncclSend");
     LOADSYM(Recv, "ncclRecv");
     LOADSYM(GroupStart, "ncclGroupStart");
@@ -157,22 +159,12 @@ bool encode_store_map(CUtensorMap* m, const void* base, bool fp32, uint64_t cols
 
 // Tiled bf16 weights (moe_pack_weights): 4D {64, tile_rows, K/64, tiles_per_expert * E}, each
 // [tile_rows][64] chunk contiguous; box {64, box_rows, 1, box_tiles}; 128B swizzle.
-// MOE_WTILE=0 (A/B experiments): the same 4D view over plain row-major packing
-// (strides: row K*2, K block 128 B, tile tile_rows*K*2), same kernels.
-#ifndef MOE_WTILE
-#define MOE_WTILE 1
-#endif
 bool encode_wmap(CUtensorMap* m, const void* base, uint64_t K, uint64_t tile_rows, uint64_t ntiles_total,
                  uint32_t box_rows, uint32_t box_tiles) {
     PFN_encodeTiled_t fn = get_encode_fn();
     if (!fn) return false;
     cuuint64_t dims[4] = {64, tile_rows, K / 64, ntiles_total};
     cuuint64_t strides[3] = {128, tile_rows * 128, (K / 64) * tile_rows * 128};
-    if (!MOE_WTILE) {
-        strides[0] = K * 2;
-        strides[1] = 128;
-        strides[2] = tile_rows * K * 2;
-    }
     cuuint32_t box[4] = {64, box_rows, 1, box_tiles};
     cuuint32_t estr[4] = {1, 1, 1, 1};
     CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, estr,
@@ -213,25 +205,23 @@ struct moe_ctx {
     int max_T = 0, nblk_max = 0;
     int64_t cap = 0;          // rows of the permuted buffers (tiled path)
     int64_t cap_swap = 0;     // rows used by the swap (decode) path
-    // decode (swap-AB) GEMMs while the mean rows per local expert T*k/E_l <= this:
-    // the weight stream dominates up to ~2 token tiles of 128 per expert (bench r01:
-    // 32-layer T=575 stack 18.5 ms swap vs 20.8 ms CTA-pair tiles)
-    int swap_rows_per_expert = 256;   // w1/w3 GEMM (env MOE_G1_SWAP_ROWS)
-    // w2 GEMM (env MOE_G2_SWAP_ROWS). r01: an isolated layer favours CTA pairs for the
-    // w2 GEMM from ~40 rows per expert (scripts/exp/sweep_g2.sh), but inside the
-    // 32-layer stack (T=575) the swap kernel's weight prefetch under PDL wins:
-    // 17.85 ms vs 18.5-18.7 ms per step (scripts/ab_env.sh, interleaved) -> 256.
-    int swap2_rows_per_expert = 256;
+    // Tuning (moe_config.tuning, include/moe.h moe_tuning; defaults below). Measurements
+    // behind each default: DESIGN.md section 12 and profiles/r01/experiments/.
+    // Decode (swap-AB) GEMMs while the mean rows per local expert T*k/E_l <= this: the
+    // weight stream dominates up to ~2 token tiles of 128 per expert (r01: 32-layer
+    // T=575 stack 18.5 ms swap vs 20.8 ms CTA-pair tiles). For the w2 GEMM an isolated
+    // layer favours CTA pairs from ~40 rows per expert, but inside the 32-layer stack the
+    // swap kernel's weight prefetch under PDL wins (17.85 vs 18.5-18.7 ms).
+    int swap_rows_per_expert = 256;   // w1/w3 GEMM
+    int swap2_rows_per_expert = 256;  // w2 GEMM
     int max_splits = 4;       // split-K partial buffers are sized for this many splits
-    int max_splits_env = 0;   // env MOE_MAX_SPLITS: force the split count (A/B; <= 8, clamped by the buffers)
     int64_t split_stride = 0; // elements between split-K partial buffers of this forward
     bool fp8 = false;             // MOE_FLAG_FP8_WEIGHTS
-    bool fp8_smem_a = false;
     bool fp8_g2_kb256 = false;    // fp8 w2 GEMM with 256-element K blocks (f_local % 256 == 0)
-    bool fp8_kb128 = false;       // fp8 TMEM-A GEMMs with 128-element K blocks (d % 128 == 0); env
-                                  // MOE_FP8_KB=64 selects 64 (r01: 0.3304 ms vs 0.2975 ms per step)      // env MOE_FP8_SMEM_A=1: widen fp8 weights in smem (not TMEM) at NB <= 64
+    bool fp8_kb128 = false;       // fp8 TMEM-A GEMMs with 128-element K blocks (d % 128 == 0;
+                                  // r01: 0.2975 vs 0.3304 ms per step with 64-element blocks)
     moe_expert_weights cur_w{};   // weights of the current forward
-    int pair_tune = 0;        // experiment override of the prefill tile orders (env MOE_PAIR_TUNE)
+    int pair_tune = 0;        // prefill tile-order override (tuning.pair_order)
     // prefill tile orders (pair_decode). G1: bands of 16 token tiles (ncu DRAM sweep r01).
     // G2: bands of 8 weight tiles, weight tiles fastest (tiled weights, interleaved A/B on
     // two boxes: 18.57/18.52 and 18.30/18.11 ms per step vs 19.14/19.04 and 18.36/18.48 ms
@@ -239,21 +229,21 @@ struct moe_ctx {
     int g1_raster = 2, g1_band = 16, g2_raster = 3, g2_band = 8;
     // weight blocks (256 columns) per CTA-pair tile: 2 = 256 x 512 tiles with a
     // single-buffered TMEM accumulator (gemm_sm100.cuh PairCfg), 1 = 256 x 256 tiles
-    // with two accumulators; env MOE_PAIR_NBLK. G2 band counts wide tiles when 2.
+    // with two accumulators. G2 band counts wide tiles when 2.
     int pair_nblk = 2;
-    int swap_nb_cap = 0;      // env MOE_SWAP_NB_CAP (see run_gemms)
-    // env MOE_ROUTER_CC: CUDA-core router (2 tokens / block, 32 blocks at T = 64) for T <= this.
+    int swap_nb_cap = 0;      // cap of the swap-path token tile (tuning; see run_gemms)
+    // CUDA-core router (2 tokens / block, 32 blocks at T = 64) for T <= this.
     // r01 64-token decode, interleaved: 0.4335 vs 0.4312 ms with the mma.sync router (4 blocks)
     int router_cc_max_T = 0;
     // FP8 w1/w3 GEMM on kind::f8f6f4 with two-term E4M3 tokens (moe_gemm_fp8x_kernel);
-    // needs d % 128 == 0; env MOE_FP8_X=0 selects the fp16-converter kernels
+    // needs d % 128 == 0 (else, or tuning.fp8_fp16_tokens: the fp16-converter kernels)
     bool fp8x = false;
     float* tok_scale = nullptr;   // [cap] 2^-s of each permuted row (fp8x)
     uint8_t* h8 = nullptr;        // [3][cap][f_local] E4M3 terms of h for the fp8x w2 GEMM
     float* h_factor = nullptr;    // [cap] per-row output factor of the fp8x w2 GEMM
     CUtensorMap tm_h8[3]{};       // h8 planes, box {128, NB}, NB = 32, 64, 128
     int64_t rows_needed_cur = 0;  // permuted rows (incl. segment padding) of the current forward
-    bool fp8_w2_x = false;        // fp8x w2 GEMM (env MOE_FP8_W2_X=0: fp16-converter w2 kernel)
+    bool fp8_w2_x = false;        // fp8x w2 GEMM (tuning.fp8_w2_split; off: fp16-converter w2 kernel)
     CUtensorMap tm_x8[3]{};       // x_perm as [2][cap][d] E4M3 planes, box {128, NB}, NB = 32, 64, 128
     // workspace (device)
     int32_t *topk_idx = nullptr, *pos = nullptr, *blockcount = nullptr, *blockoff = nullptr;
@@ -262,34 +252,23 @@ struct moe_ctx {
     unsigned int* done = nullptr;
     __nv_bfloat16 *x_perm = nullptr, *h = nullptr;
     int32_t* src_row = nullptr;  // gather mode: [cap + 512] token of each permuted row
-    float* tail_ws = nullptr;    // decode w1/w3 GEMM tail split: [num_sms][2][128][128] fp32
-    int32_t* tail_cnt = nullptr; // [num_sms] arrival counters (zero between launches)
-    // max K slices per tail tile of the decode w1/w3 GEMM (env MOE_TAIL_PARTS; 0/1 = off).
-    // Off: r01 interleaved A/B with the tiled weight layout, decode step 0.4412 ms at 0
-    // vs 0.4475 ms at 4 or 8 (on the row-major layout 8 had won, 0.4534 vs 0.4587 ms).
-    int tail_parts = 0;
     int w13_nt = 0, w2_nt = 0;   // tiles per expert of the tiled bf16 weight layout (256 / 128 rows)
-    bool gather = false;         // MOE_FLAG_GATHER (or env MOE_GATHER=1): tile::gather4 token fetch
+    bool gather = false;         // MOE_FLAG_GATHER: tile::gather4 token fetch
     bool gather_now = false;     // the current forward gathers (set per call)
-    // Decode speculative L2 weight prefetch (env MOE_SPEC_L2 = K blocks per CTA, 0 = off):
-    // the router and permute kernels trigger their PDL dependents early, so the w1/w3
-    // GEMM launches while routing runs and prefetches the first K blocks of the weight
-    // tile it will most likely own (every expert holding one token tile) into L2.
+    // Decode speculative L2 weight prefetch (K blocks per CTA, 0 = off): the router and
+    // permute kernels trigger their PDL dependents early, so the w1/w3 GEMM launches
+    // while routing runs and prefetches the first K blocks of the weight tile it will
+    // most likely own (every expert holding one token tile) into L2.
     // Only for 16 <= T <= 128 (one token tile per expert, all experts likely used).
-    // Default 48 K blocks after the grid change (ab_spec2.log, 3/3 rounds: 0.4121 ms at 48,
-    // 0.4127 at 32, 0.4132 at 16 and off; first sweep on 148-CTA grids: ab_spec_l2.log).
+    // 48 after the grid change (ab_spec2.log, 3/3 rounds: 0.4121 ms at 48, 0.4127 at 32,
+    // 0.4132 at 16 and off; first sweep on 148-CTA grids: ab_spec_l2.log).
     int spec_l2 = 48;
     bool spec_now = false;       // the current forward prefetches speculatively (set per call)
-    // bf16 swap GEMMs: load the token operand in 32-row boxes, only ceil(n_valid / 32) of
-    // them per stage, instead of one NB-row box (env MOE_TRIM_B=1; GemmParams::b_rows32).
-    // Off: measured slower although it moves fewer bytes (r01 interleaved A/B, one box:
-    // decode 0.4350 -> 0.4569 ms, stack 16.1 -> 21.6 ms; profiles/r01/experiments/ab_trim_*.log)
-    int trim_b = 0;
-    // Persistent grid of the bf16 swap GEMMs (run_gemms; env MOE_G1_GRID / MOE_G2_GRID
-    // override, 0 = auto). Auto, when every expert fits one token tile (decode): the w1/w3
-    // GEMM runs (f_l/128) * floor(SMs / (f_l/128)) CTAs -- Mixtral: 112, so CTA m streams
-    // weight tile m of every expert -- and the w2 GEMM ceil(U / ceil(U / SMs)) CTAs for U
-    // units (256 -> 128: two equal waves). r01 interleaved sweep at the 64-token decode
+    // Persistent grid of the bf16 swap GEMMs (run_gemms; tuning g1_grid / g2_grid override,
+    // 0 = auto). Auto, when every expert fits one token tile (decode): the w1/w3 GEMM runs
+    // (f_l/128) * floor(SMs / (f_l/128)) CTAs -- Mixtral: 112, so CTA m streams weight tile
+    // m of every expert -- and the w2 GEMM ceil(U / ceil(U / SMs)) CTAs for U units (256 ->
+    // 128: two equal waves). r01 interleaved sweep at the 64-token decode
     // (profiles/r01/experiments/ab_grid*.log): w1/w3 grid 148 -> 282.4 us, 136 -> 296,
     // 128 -> ~283, 120 -> 278.7, 112 -> 266.8 (7.06 TB/s), 104 -> 274, 96 -> 286; w2 grid
     // 148 -> 154.8 us, 136 -> 146, 128 -> 142.7, 112 -> 207; step 0.4340 -> 0.4124 ms.
@@ -297,17 +276,6 @@ struct moe_ctx {
     // w1/w3 165 -> 184 us at 112, w2 94 -> 105 us at 128); the FP8 w1/w3 GEMM takes equal
     // waves instead (run_gemms), the FP8 w2 GEMM one CTA per SM.
     int g1_grid = 0, g2_grid = 0;
-    // env MOE_EARLY_DEP=1: GemmParams::early_dep for the bf16 swap GEMMs. Off: no measurable
-    // effect (decode 0.4119 vs 0.4119 ms over 4 interleaved rounds, stack within noise;
-    // profiles/r01/experiments/ab_early_dep.log); parity suite green with it on.
-    int early_dep = 0;
-    // env MOE_G2_DUAL=1: the decode w2 GEMM on 256-row units (kG2Dual, two W2 tiles per
-    // unit, 32 KB of weights per stage like the w1/w3 GEMM), NB <= 128, bf16. Off: parity
-    // green but no gain (w2 GEMM 142.6 vs 143.2 us, step within noise over 4 interleaved
-    // rounds, profiles/r01/experiments/ab_g2dual.log) -- the box size is not what holds
-    // the w2 GEMM below the w1/w3 GEMM's streaming rate.
-    int g2_dual = 0;
-    bool g2_dual_now = false;
     int g1_grid_now = 0, g2_grid_now = 0;  // the current forward's choice
     CUtensorMap tm_src{};        // gather map over the current call's tokens [T, d], box {64, 1}
     float* y = nullptr;
@@ -317,8 +285,8 @@ struct moe_ctx {
     cudaEvent_t slot_free[2]{}, slot_loaded[2]{};
     int host_slot = 0;
     uint64_t swap_w_hint = 0;    // L2 policy of the decode GEMMs' weight stream (set per forward)
-    int swap_hint_mode = 0;      // env MOE_SWAP_HINT: 0 auto, 1 evict-first, 2 normal, 3 evict-last
-    bool host_zero_copy = true;  // moe_forward_host: combine writes pinned output directly (env MOE_HOST_ZERO_COPY=0: copy)
+    int swap_hint_mode = 0;      // tuning.weight_hint: 0 auto, 1 evict-first, 2 normal, 3 evict-last
+    bool host_zero_copy = true;  // moe_forward_host: combine writes pinned output directly (tuning.host_stage: copy)
     float* tp_partial = nullptr;                               // TP: fp32 partial [max_T, d]
     float* tp_scatter = nullptr;                               // TP: reduce-scatter result
     // EP staging
@@ -384,7 +352,9 @@ moe_status fail(moe_ctx* c, moe_status s, const char* fmt, ...) {
     va_end(ap);
     if (c) {
         c->err = buf;
-        if (s == MOE_ERR_CUDA) c->poisoned = true;
+        // CUDA faults are sticky; a failed NCCL call may leave a group open or peers
+        // blocked in a collective, so no later forward on this context may start one
+        if (s == MOE_ERR_CUDA || s == MOE_ERR_NCCL) c->poisoned = true;
     } else {
         g_init_error = buf;
     }
@@ -575,14 +545,26 @@ moe_status validate_cfg(const moe_config* cfg, moe_ctx* c) {
     if (p2p && cfg->par == MOE_PAR_HYBRID)
         return fail(c, MOE_ERR_UNSUPPORTED, "MOE_FLAG_P2P supports MOE_PAR_EP and MOE_PAR_TP");
     if (p2p && cfg->par == MOE_PAR_NONE) return fail(c, MOE_ERR_INVALID, "MOE_FLAG_P2P needs MOE_PAR_EP or MOE_PAR_TP");
+    if (p2p && G > 32) return fail(c, MOE_ERR_UNSUPPORTED, "MOE_FLAG_P2P supports groups of at most 32 ranks");
     if (!p2p && (cfg->par == MOE_PAR_EP || cfg->par == MOE_PAR_HYBRID) && !cfg->nccl_comm)
         return fail(c, MOE_ERR_INVALID, "nccl_comm (EP group) required");
     if (!p2p && cfg->par == MOE_PAR_TP && G > 1 && !cfg->nccl_comm) return fail(c, MOE_ERR_INVALID, "nccl_comm required");
     if (cfg->par == MOE_PAR_HYBRID && ps.tp_world > 1 && !cfg->tp_comm)
         return fail(c, MOE_ERR_INVALID, "tp_comm (TP group) required");
     if (cfg->split_k < 0 || cfg->split_k > 8) return fail(c, MOE_ERR_INVALID, "split_k must be in [0,8]");
-    for (int i = 0; i < 3; ++i)
+    for (int i = 0; i < 2; ++i)
         if (cfg->reserved[i]) return fail(c, MOE_ERR_INVALID, "reserved fields must be zero");
+    if (const moe_tuning* tu = cfg->tuning) {
+        for (int i = 0; i < 11; ++i)
+            if (tu->reserved[i]) return fail(c, MOE_ERR_INVALID, "tuning.reserved fields must be zero");
+        if (tu->g1_swap_rows < 0 || tu->g2_swap_rows < 0 || tu->g1_grid < 0 || tu->g2_grid < 0 ||
+            tu->swap_nb_cap < 0 || tu->router_cc_max_T < 0 || tu->pair_order < 0)
+            return fail(c, MOE_ERR_INVALID, "tuning fields must be >= 0 (spec_l2 may be < 0: off)");
+        if (tu->pair_nblk < 0 || tu->pair_nblk > 2) return fail(c, MOE_ERR_INVALID, "tuning.pair_nblk must be 0, 1 or 2");
+        if (tu->weight_hint < 0 || tu->weight_hint > 3) return fail(c, MOE_ERR_INVALID, "tuning.weight_hint must be 0..3");
+        if (tu->swap_nb_cap && tu->swap_nb_cap != 32 && tu->swap_nb_cap != 64 && tu->swap_nb_cap != 128)
+            return fail(c, MOE_ERR_INVALID, "tuning.swap_nb_cap must be 0, 32, 64 or 128");
+    }
     if ((cfg->flags & MOE_FLAG_FORCE_SWAP) && (cfg->flags & MOE_FLAG_FORCE_TILED))
         return fail(c, MOE_ERR_INVALID, "FORCE_SWAP and FORCE_TILED are exclusive");
     return MOE_OK;
@@ -661,11 +643,6 @@ moe_status run_swap_g1(moe_ctx* c, int nbi, const moe_expert_weights* w, cudaStr
     p1.hint_a = c->swap_w_hint;
     p1.w_tr = 256;
     p1.w_nt = c->w13_nt;
-    if (c->tail_parts > 1) {  // K-sliced tail tiles (bf16 kernel; gemm_sm100.cuh tail_plan)
-        p1.tail_ws = c->tail_ws;
-        p1.tail_cnt = c->tail_cnt;
-        p1.tail_parts = c->tail_parts;
-    }
     if (c->gather_now) {
         p1.src_row = c->src_row;
         return launch_gemm<kG1Swap, NB>(c, kSlotGemm1, p1, c->tm_w13, c->tm_src, c->num_sms, st);
@@ -676,7 +653,7 @@ moe_status run_swap_g1(moe_ctx* c, int nbi, const moe_expert_weights* w, cudaStr
                           (size_t)Fp8xCfg<kG1Swap, NB>::kSmemBytes, st, p1, static_cast<const float*>(w->w13_scale),
                           static_cast<const float*>(c->tok_scale), c->tm_w13, c->tm_x8[nbi]);
     if constexpr (NB <= 64)
-        if (c->fp8 && !c->fp8_smem_a)
+        if (c->fp8)
             return launch_gemm_fp8t<kG1Swap, NB>(c, kSlotGemm1, p1, w->w13_scale, c->tm_w13, c->tm_x_swap[nbi],
                                                  c->num_sms, st);
     if constexpr (NB <= 128)
@@ -684,9 +661,7 @@ moe_status run_swap_g1(moe_ctx* c, int nbi, const moe_expert_weights* w, cudaStr
             return launch_gemm_fp8<kG1Swap, NB>(c, kSlotGemm1, p1, w->w13_scale, c->tm8_w13_64, c->tm_x_swap[nbi],
                                                 c->num_sms, st);
     if (c->spec_now) p1.spec_l2 = c->spec_l2;
-    p1.b_rows32 = c->trim_b;
-    p1.early_dep = c->early_dep;
-    return launch_gemm<kG1Swap, NB>(c, kSlotGemm1, p1, c->tm_w13, c->tm_x_swap[c->trim_b ? 0 : nbi],
+    return launch_gemm<kG1Swap, NB>(c, kSlotGemm1, p1, c->tm_w13, c->tm_x_swap[nbi],
                                     c->g1_grid_now, st);
 }
 
@@ -725,7 +700,7 @@ moe_status run_swap_g2(moe_ctx* c, int nbi, const moe_expert_weights* w, int spl
             return s;
         }
     if constexpr (NB <= 64)
-        if (c->fp8 && !c->fp8_smem_a)
+        if (c->fp8)
             return launch_gemm_fp8t<kG2Swap, NB>(c, kSlotGemm2, p2, w->w2_scale, c->tm_w2_swap, c->tm_h_swap[nbi],
                                                  c->g2_grid_now, st);
     if constexpr (NB <= 128)
@@ -734,13 +709,7 @@ moe_status run_swap_g2(moe_ctx* c, int nbi, const moe_expert_weights* w, int spl
             return launch_gemm_fp8<kG2Swap, NB>(c, kSlotGemm2, p2, w->w2_scale, c->tm8_w2_64, c->tm_h_swap[nbi],
                                                 c->num_sms, st);
         }
-    p2.b_rows32 = c->trim_b;
-    p2.early_dep = c->early_dep;
-    if constexpr (NB <= 128)
-        if (c->g2_dual_now)
-            return launch_gemm<kG2Dual, NB>(c, kSlotGemm2, p2, c->tm_w2_swap, c->tm_h_swap[c->trim_b ? 0 : nbi],
-                                            c->g2_grid_now, st);
-    return launch_gemm<kG2Swap, NB>(c, kSlotGemm2, p2, c->tm_w2_swap, c->tm_h_swap[c->trim_b ? 0 : nbi],
+    return launch_gemm<kG2Swap, NB>(c, kSlotGemm2, p2, c->tm_w2_swap, c->tm_h_swap[nbi],
                                     c->g2_grid_now, st);
 }
 
@@ -939,14 +908,13 @@ moe_status run_gemms(moe_ctx* c, GemmPaths gp, int64_t rows_bound, int64_t rows_
         // >= 108 SMs stay busy in the last wave); the T=575 stack 17.4 ms at 2 vs 18.2 at
         // 1 and 17.4 at 4; FP8 0.2917 ms at 4 vs 0.2970 at 2.
         const int auto_splits = c->fp8 ? 4 : nb2 <= 64 ? 1 : 2;
-        splits = c->cfg.split_k ? c->cfg.split_k : c->max_splits_env ? c->max_splits_env : auto_splits;
+        splits = c->cfg.split_k ? c->cfg.split_k : auto_splits;
         splits = (int)std::max<int64_t>(1, std::min<int64_t>(splits, c->y_elems / (rows_needed * c->d)));
         splits = std::min(splits, c->f_local / (c->fp8_g2_kb256 ? 256 : c->fp8_kb128 ? 128 : kBK));  // >= 1 K block per split
         c->split_stride = rows_needed * c->d;
         c->rows_needed_cur = std::min<int64_t>(rows_needed, c->cap);
-        c->g2_dual_now = c->g2_dual && !c->fp8 && nb2 <= 128 && !c->trim_b;
         {
-            const int64_t U = (int64_t)c->E_local * ((c->d + (c->g2_dual_now ? 255 : 127)) / (c->g2_dual_now ? 256 : 128)) * splits;
+            const int64_t U = (int64_t)c->E_local * ((c->d + 127) / 128) * splits;
             const int ns = c->num_sms;
             const int64_t waves = (U + ns - 1) / ns;
             c->g2_grid_now = c->g2_grid > 0 ? std::min(c->g2_grid, ns)
@@ -1025,6 +993,25 @@ moe_status p2p_arrive_and_wait(moe_ctx* c, int idx, cudaStream_t st);
         if (_r != 0) return fail(ctx, MOE_ERR_NCCL, "%s failed: %s", #expr, g_nccl.GetErrorString(_r)); \
     } while (0)
 
+// ncclGroupStart / ncclGroupEnd bracket that is closed on every path: an early error
+// return inside the group still ends it (the NCCL group depth is per host thread and
+// would otherwise swallow the caller's next NCCL calls).
+struct NcclGroup {
+    bool active = false;
+    ncclResult_t start(bool use) {
+        if (!use) return 0;
+        ncclResult_t r = g_nccl.GroupStart();
+        active = r == 0;
+        return r;
+    }
+    ncclResult_t end() {
+        if (!active) return 0;
+        active = false;
+        return g_nccl.GroupEnd();
+    }
+    ~NcclGroup() { end(); }
+};
+
 // ------------------------------------------------------------------ collectives
 // Two transports behind the same three collectives: NCCL (production; one process
 // per GPU) and a loopback group (TEST ONLY: G contexts in one process on one
@@ -1095,7 +1082,19 @@ moe_status comm_alltoall(moe_ctx* c, CommRef cm, const void* send, void* recv, s
         g->barrier();
         return MOE_OK;
     }
-    NCCL_TRY(c, g_nccl.AlltoAll(send, recv, count, nccl_type, cm.comm, st));
+    if (g_nccl.AlltoAll) {
+        NCCL_TRY(c, g_nccl.AlltoAll(send, recv, count, nccl_type, cm.comm, st));
+        return MOE_OK;
+    }
+    // NCCL < 2.28: the same exchange as grouped point-to-point calls
+    const size_t b = count * esize;
+    NcclGroup grp;
+    NCCL_TRY(c, grp.start(true));
+    for (int p = 0; p < cm.world; ++p) {
+        NCCL_TRY(c, g_nccl.Send(static_cast<const char*>(send) + p * b, count, nccl_type, p, cm.comm, st));
+        NCCL_TRY(c, g_nccl.Recv(static_cast<char*>(recv) + p * b, count, nccl_type, p, cm.comm, st));
+    }
+    NCCL_TRY(c, grp.end());
     return MOE_OK;
 }
 
@@ -1174,7 +1173,8 @@ moe_status comm_alltoallv(moe_ctx* c, CommRef cm, const void* send, void* recv, 
         g->barrier();
         return MOE_OK;
     }
-    NCCL_TRY(c, g_nccl.GroupStart());
+    NcclGroup grp;
+    NCCL_TRY(c, grp.start(true));
     for (int p = 0; p < cm.world; ++p) {
         if (scount[p] > 0)
             NCCL_TRY(c, g_nccl.Send(static_cast<const char*>(send) + p * cap * row_b, scount[p] * row_elems, nccl_type,
@@ -1183,7 +1183,7 @@ moe_status comm_alltoallv(moe_ctx* c, CommRef cm, const void* send, void* recv, 
             NCCL_TRY(c, g_nccl.Recv(static_cast<char*>(recv) + p * cap * row_b, rcount[p] * row_elems, nccl_type, p,
                                     cm.comm, st));
     }
-    NCCL_TRY(c, g_nccl.GroupEnd());
+    NCCL_TRY(c, grp.end());
     return MOE_OK;
 }
 
@@ -1322,42 +1322,35 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
     c->w13_nt = 2 * c->f_local / 256;
     c->w2_nt = (c->d + 255) / 256 * 2;
     c->fp8 = (cfg->flags & MOE_FLAG_FP8_WEIGHTS) != 0;
-    if (const char* v = getenv("MOE_FP8_SMEM_A")) c->fp8_smem_a = atoi(v) != 0;
     c->fp8_kb128 = c->fp8 && c->d % 128 == 0 && c->f_local % 128 == 0;
-    if (const char* v = getenv("MOE_FP8_KB")) c->fp8_kb128 = c->fp8_kb128 && atoi(v) >= 128;
     c->fp8_g2_kb256 = c->fp8_kb128 && c->f_local % 256 == 0;
-    if (const char* v = getenv("MOE_FP8_G2_KB")) c->fp8_g2_kb256 = c->fp8_g2_kb256 && atoi(v) == 256;
     c->fp8x = c->fp8_kb128;
-    if (const char* v = getenv("MOE_FP8_X")) c->fp8x = c->fp8x && atoi(v) != 0;
     // fp8x w2 GEMM: off by default. r01 (64-token decode, interleaved A/B): 0.3062 vs
     // 0.2708 ms per step -- the h split kernel costs 9.5 us and the w2 GEMM on row-major
     // E4M3 W2 with 128-byte K blocks streams at ~4 TB/s (122 us) against the converter
-    // kernel's 95 us with 256-byte K blocks. Env MOE_FP8_W2_X=1 enables it (tested).
+    // kernel's 95 us with 256-byte K blocks.
     c->fp8_w2_x = false;
-    if (const char* v = getenv("MOE_FP8_W2_X")) c->fp8_w2_x = c->fp8x && atoi(v) != 0;
-    if (const char* pt = getenv("MOE_PAIR_TUNE")) c->pair_tune = atoi(pt);
-    if (const char* v = getenv("MOE_PAIR_NBLK")) c->pair_nblk = atoi(v) == 1 ? 1 : 2;
-    if (const char* v = getenv("MOE_SWAP_NB_CAP")) c->swap_nb_cap = atoi(v);
-    if (const char* v = getenv("MOE_ROUTER_CC")) c->router_cc_max_T = atoi(v);
-    if (const char* v = getenv("MOE_GATHER")) c->gather = atoi(v) != 0;
-    if (const char* v = getenv("MOE_G1_SWAP_ROWS")) c->swap_rows_per_expert = atoi(v);
-    if (const char* v = getenv("MOE_TAIL_PARTS")) c->tail_parts = atoi(v);
-    if (const char* v = getenv("MOE_SPEC_L2")) c->spec_l2 = std::max(0, atoi(v));
-    if (const char* v = getenv("MOE_TRIM_B")) c->trim_b = atoi(v) != 0;
-    if (const char* v = getenv("MOE_G1_GRID")) c->g1_grid = std::max(0, atoi(v));
-    if (const char* v = getenv("MOE_EARLY_DEP")) c->early_dep = atoi(v) != 0;
-    if (const char* v = getenv("MOE_G2_DUAL")) c->g2_dual = atoi(v) != 0;
-    if (const char* v = getenv("MOE_G2_GRID")) c->g2_grid = std::max(0, atoi(v));
-    if (const char* v = getenv("MOE_HOST_ZERO_COPY")) c->host_zero_copy = atoi(v) != 0;
-    if (const char* v = getenv("MOE_SWAP_HINT")) c->swap_hint_mode = atoi(v);
-    if (const char* v = getenv("MOE_MAX_SPLITS")) c->max_splits_env = std::max(1, std::min(8, atoi(v)));
-    if (const char* v = getenv("MOE_G2_SWAP_ROWS")) c->swap2_rows_per_expert = atoi(v);
+    if (const moe_tuning* tu = cfg->tuning) {
+        if (tu->fp8_fp16_tokens) c->fp8x = false;
+        c->fp8_w2_x = c->fp8x && tu->fp8_w2_split != 0;
+        c->pair_tune = tu->pair_order;
+        if (tu->pair_nblk) c->pair_nblk = tu->pair_nblk == 1 ? 1 : 2;
+        c->swap_nb_cap = tu->swap_nb_cap;
+        c->router_cc_max_T = tu->router_cc_max_T;
+        if (tu->g1_swap_rows) c->swap_rows_per_expert = tu->g1_swap_rows;
+        if (tu->g2_swap_rows) c->swap2_rows_per_expert = tu->g2_swap_rows;
+        if (tu->spec_l2) c->spec_l2 = std::max(0, tu->spec_l2);
+        c->g1_grid = tu->g1_grid;
+        c->g2_grid = tu->g2_grid;
+        c->host_zero_copy = tu->host_stage == 0;
+        c->swap_hint_mode = tu->weight_hint;
+    }
     if (cfg->flags & MOE_FLAG_GATHER) c->gather = true;
-    // router blocks of >= 2 rows; EP also routes the G*max_T*k receive slots
-    c->nblk_max = (int)(((int64_t)c->max_T * (c->ep_world > 1 ? c->ep_world * c->k : 1) + 1) / 2 + 1);
-
     // EP: a rank may receive up to every token of every peer (dropless, reading R6).
     const bool ep_like = cfg->par == MOE_PAR_EP || cfg->par == MOE_PAR_HYBRID;
+    // router blocks of >= 2 rows; EP-like contexts (also at ep_world 1) route the
+    // ep_world*max_T*k receive slots too
+    c->nblk_max = (int)(((int64_t)c->max_T * (ep_like ? c->ep_world * c->k : 1) + 1) / 2 + 1);
     const int64_t rows_in = ep_like ? (int64_t)c->max_T * c->ep_world : c->max_T;
     c->cap = round_up(rows_in * c->k + (int64_t)c->E_local * (kSegAlign - 1), kSegAlign);
     const int64_t swap_T = std::min<int64_t>(rows_in, (int64_t)c->swap2_rows_per_expert * c->E_local / c->k);
@@ -1409,8 +1402,6 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
         ALLOC(c->h_factor, sizeof(float) * c->cap);
     }
     ALLOC(c->src_row, sizeof(int32_t) * (c->cap + 512));
-    ALLOC(c->tail_ws, sizeof(float) * c->num_sms * 2 * 128 * 128);
-    ALLOC(c->tail_cnt, sizeof(int32_t) * c->num_sms);
     ALLOC(c->h, sizeof(__nv_bfloat16) * c->cap * c->f_local);
     ALLOC(c->y, sizeof(float) * c->y_elems);
     ALLOC(c->stage_in, 2 * sizeof(__nv_bfloat16) * c->max_T * c->d);
@@ -1469,7 +1460,6 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
     if ((e = cudaMemset(c->done, 0, sizeof(unsigned int) * 4)) != cudaSuccess) return fail_init("memset", e);
     if ((e = cudaMemset(c->x_perm, 0, sizeof(__nv_bfloat16) * c->cap * c->d)) != cudaSuccess) return fail_init("memset", e);
     if ((e = cudaMemset(c->src_row, 0, sizeof(int32_t) * (c->cap + 512))) != cudaSuccess) return fail_init("memset", e);
-    if ((e = cudaMemset(c->tail_cnt, 0, sizeof(int32_t) * c->num_sms)) != cudaSuccess) return fail_init("memset", e);
     if ((e = cudaMemset(c->h, 0, sizeof(__nv_bfloat16) * c->cap * c->f_local)) != cudaSuccess) return fail_init("memset", e);
 
     // workspace TMA descriptors
@@ -1491,8 +1481,6 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
     moe_status as;
     if ((as = set_gemm_attr<kG1Tiled, 256>(c)) || (as = set_gemm_attr<kG2Tiled, 256>(c)) ||
         (as = set_gemm_attr<kG1Swap, 32>(c)) || (as = set_gemm_attr<kG2Swap, 32>(c)) ||
-        (as = set_gemm_attr<kG2Dual, 32>(c)) || (as = set_gemm_attr<kG2Dual, 64>(c)) ||
-        (as = set_gemm_attr<kG2Dual, 128>(c)) ||
         (as = set_gemm_attr<kG1Swap, 64>(c)) || (as = set_gemm_attr<kG2Swap, 64>(c)) ||
         (as = set_gemm_attr<kG1Swap, 128>(c)) || (as = set_gemm_attr<kG2Swap, 128>(c)) ||
         (as = set_gemm_attr<kG2Swap, 256>(c)) ||
@@ -1527,8 +1515,6 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
             reinterpret_cast<const void*>(moe_gemm_kernel<kG1Swap, 32>), reinterpret_cast<const void*>(moe_gemm_kernel<kG2Swap, 32>),
             reinterpret_cast<const void*>(moe_gemm_kernel<kG1Swap, 64>), reinterpret_cast<const void*>(moe_gemm_kernel<kG2Swap, 64>),
             reinterpret_cast<const void*>(moe_gemm_kernel<kG1Swap, 128>), reinterpret_cast<const void*>(moe_gemm_kernel<kG2Swap, 128>),
-            reinterpret_cast<const void*>(moe_gemm_kernel<kG2Dual, 32>), reinterpret_cast<const void*>(moe_gemm_kernel<kG2Dual, 64>),
-            reinterpret_cast<const void*>(moe_gemm_kernel<kG2Dual, 128>),
             reinterpret_cast<const void*>(moe_gemm_kernel<kG2Swap, 256>), reinterpret_cast<const void*>(moe_gemm_pair_kernel<kG1Pair, 1>),
             reinterpret_cast<const void*>(moe_gemm_pair_kernel<kG2Pair, 1>), reinterpret_cast<const void*>(moe_gemm_pair_kernel<kG1Pair, 2>),
             reinterpret_cast<const void*>(moe_gemm_pair_kernel<kG2Pair, 2>),
@@ -1554,7 +1540,7 @@ moe_status moe_destroy(moe_ctx* c) {
                     c->x_perm, c->h, c->y, c->stage_in, c->stage_out, c->tp_partial, c->tp_scatter, c->ep_send,
                     c->ep_recv, c->ep_ysend, c->ep_yrecv, c->ep_meta_send, c->ep_meta_recv,
                     c->ep_ridx, c->ep_rpos, c->ep_rw, c->ep_rcounts, c->lb_scratch, c->d_peers, c->src_row,
-                    c->tail_ws, c->tail_cnt, c->tok_scale, c->h8, c->h_factor};
+                    c->tok_scale, c->h8, c->h_factor};
     for (void* p : c->p2p_opened) cudaIpcCloseMemHandle(p);
     if (c->sym) {
         cudaDeviceSynchronize();  // peers' stores into this region have drained (same-process group)
@@ -1585,11 +1571,11 @@ moe_status moe_pack_weights(moe_ctx* c, const void* w1, const void* w3, const vo
     const int e_off = c->e_lo;  // 0 unless experts are sharded (EP, hybrid)
     if ((s = launch(c, kSlotPack, moe_pack_w13_kernel, dim3(4 * c->num_sms), dim3(256), 0, st,
                     static_cast<const __nv_bfloat16*>(w1), static_cast<const __nv_bfloat16*>(w3),
-                    static_cast<__nv_bfloat16*>(w13_out), c->E_local, e_off, c->d, c->f, c->f_local, c->f_off, MOE_WTILE)))
+                    static_cast<__nv_bfloat16*>(w13_out), c->E_local, e_off, c->d, c->f, c->f_local, c->f_off, 1)))
         return s;
     if ((s = launch(c, kSlotPack, moe_pack_w2_kernel, dim3(4 * c->num_sms), dim3(256), 0, st,
                     static_cast<const __nv_bfloat16*>(w2), static_cast<__nv_bfloat16*>(w2_out), c->E_local, e_off,
-                    c->d, c->f, c->f_local, c->f_off, MOE_WTILE, 1)))
+                    c->d, c->f, c->f_local, c->f_off, 1, 1)))
         return s;
     // descriptors keyed by these pointers must be re-encoded if memory was reused
     (void)w13_out;  // descriptors hold addresses only; repacking in place keeps them valid
@@ -1897,7 +1883,7 @@ moe_status forward_impl(moe_ctx* c, const void* tokens, int32_t T, const void* r
     r.dst_rows = c->gather_now ? nullptr : c->x_perm;
     r.src_row = c->gather_now ? c->src_row : nullptr;
     const GemmPaths gpaths = gemm_paths(c, (int64_t)T * c->k);
-    c->spec_now = c->spec_l2 > 0 && gpaths.swap1 && !c->fp8 && !c->gather_now && c->tail_parts <= 1 &&
+    c->spec_now = c->spec_l2 > 0 && gpaths.swap1 && !c->fp8 && !c->gather_now &&
                   T >= 16 && T <= 128 && !c->profiling;
     r.early = c->spec_now;
     moe_status s2 = route_and_permute(c, r, st);
@@ -1974,11 +1960,11 @@ moe_status forward_impl(moe_ctx* c, const void* tokens, int32_t T, const void* r
                     of32)))
         return s;
     StepTimer t2(c, kSlotExchange, st);
-    const bool nccl = as_loopback(comm) == nullptr;
-    if (nccl) NCCL_TRY(c, g_nccl.GroupStart());
+    NcclGroup grp;
+    NCCL_TRY(c, grp.start(as_loopback(comm) == nullptr));
     if ((s = comm_allgather_inplace(c, tpc, out, (size_t)cnt, ncclBfloat16, 2, st))) return s;
     if (of32 && (s = comm_allgather_inplace(c, tpc, of32, (size_t)cnt, ncclFloat32, 4, st))) return s;
-    if (nccl) NCCL_TRY(c, g_nccl.GroupEnd());
+    NCCL_TRY(c, grp.end());
     t2.done();
     return MOE_OK;
 }
@@ -2098,10 +2084,11 @@ moe_status forward_ep(moe_ctx* c, const void* tokens, int32_t T, const void* rou
                                 st)))
             return s;
     } else {
-        if (nccl) NCCL_TRY(c, g_nccl.GroupStart());
+        NcclGroup grp;
+        NCCL_TRY(c, grp.start(nccl));
         if ((s = comm_alltoall(c, epc, c->ep_meta_send, c->ep_meta_recv, (size_t)cap, ncclInt32, 4, st))) return s;
         if ((s = comm_alltoall(c, epc, c->ep_send, c->ep_recv, (size_t)(cap * c->d), ncclBfloat16, 2, st))) return s;
-        if (nccl) NCCL_TRY(c, g_nccl.GroupEnd());
+        NCCL_TRY(c, grp.end());
     }
     t1.done();
     // receive side: R slots (peer-major), k = 1, expert = meta (local index, -1 empty)

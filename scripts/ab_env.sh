@@ -1,8 +1,8 @@
-# A/B timing of environment settings on one bench config, interleaved.
-# usage: bash scripts/ab_env.sh "<VAR=a> <VAR=b> ..." [rounds] [extra bench args]
+# A/B timing of moe_tuning settings (bench.py --tuning) on one bench config, interleaved.
+# usage: bash scripts/ab_env.sh "<field=a> <field=b,field2=c> ..." [rounds] [extra bench args]
 SETS=$1; R=${2:-3}; shift 2
 for r in $(seq 1 $R); do for v in $SETS; do
-  env $v timeout -s KILL 300 python bench.py --steps 50 --warmup 5 --no-cpu-baseline "$@" > gpurun_out/abenv.log 2>&1
+  timeout -s KILL 300 python bench.py --steps 50 --warmup 5 --no-cpu-baseline --tuning "$v" "$@" > gpurun_out/abenv.log 2>&1
   grep -h "^{" gpurun_out/abenv.log | python -c "
 import json,sys
 for l in sys.stdin:

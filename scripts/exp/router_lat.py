@@ -2,7 +2,7 @@
 Per-kernel event times (profiling breaks PDL overlap) and the whole-step time of a
 small-ffn block (d=4096, f=1024, E=8: GEMMs tiny, so the step is the fixed latency of
 the five-kernel chain), for the tensor-core router and the CUDA-core router
-(MOE_ROUTER_CC=T_max, read at moe_init)."""
+(moe_tuning.router_cc_max_T = T_max)."""
 import os
 import sys
 
@@ -16,12 +16,9 @@ w = synth.make_weights(4096, f, 8, seed=0, device="cuda")
 
 
 def run(T, cc):
-    if cc:
-        os.environ["MOE_ROUTER_CC"] = str(T)
-    else:
-        os.environ.pop("MOE_ROUTER_CC", None)
     x = synth.make_tokens(T, 4096, seed=1, device="cuda")
-    blk = moe.MoEBlock(w["wg"], w["w1"], w["w3"], w["w2"], max_tokens=max(T, 64))
+    blk = moe.MoEBlock(w["wg"], w["w1"], w["w3"], w["w2"], max_tokens=max(T, 64),
+                       tuning={"router_cc_max_T": T} if cc else None)
     for _ in range(10):
         blk.forward(x)
     torch.cuda.synchronize()

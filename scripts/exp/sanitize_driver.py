@@ -1,6 +1,6 @@
 """Small forwards over every kernel family, for compute-sanitizer (scripts/sanitize.sh):
 swap-AB decode GEMMs, CTA-pair and 1-CTA prefill tiles, tile::gather4 token fetch,
-K-sliced tail tiles, FP8 weights, and the EP / TP paths over the loopback and the
+FP8 weights, and the EP / TP paths over the loopback and the
 peer-memory (MOE_FLAG_P2P) transports at G = 2."""
 import os
 import sys
@@ -14,21 +14,17 @@ import synth  # noqa: E402
 import paper_2408_00008_b200 as moe  # noqa: E402
 
 
-def single(shape, flags, env=None):
-    for k, v in (env or {}).items():
-        os.environ[k] = v
+def single(shape, flags, tuning=None):
     inp = synth.make_inputs(shape, 5, device="cuda")
     w = dict(inp)
     if flags & moe.MOE_FLAG_FP8_WEIGHTS:
         for n in ("w1", "w3", "w2"):
             w[n] = synth.quantize_fp8_rows(w[n])
-    blk = moe.MoEBlock(w["wg"], w["w1"], w["w3"], w["w2"], max_tokens=shape.T, flags=flags)
-    for k in (env or {}):
-        del os.environ[k]
+    blk = moe.MoEBlock(w["wg"], w["w1"], w["w3"], w["w2"], max_tokens=shape.T, flags=flags, tuning=tuning)
     blk.forward(inp["x"])
     torch.cuda.synchronize()
     blk.close()
-    print("ok", shape, hex(flags), env, flush=True)
+    print("ok", shape, hex(flags), tuning, flush=True)
 
 
 def group(par, G, p2p):
@@ -75,9 +71,7 @@ if __name__ == "__main__":
     single(small, 0x4 | 0x10)                # 1-CTA tiles
     single(small, 0x2 | moe.MOE_FLAG_GATHER)  # gather4, swap
     single(small, 0x4 | moe.MOE_FLAG_GATHER)  # gather4, pair
-    single(synth.MoEShape(T=64, d=1024, f=2560, E=8, k=2), 0x2, {"MOE_TAIL_PARTS": "8"})  # tail slices
     single(synth.MoEShape(T=64, d=1024, f=2560, E=8, k=2), 0x2)  # speculative L2 prefetch, auto grids
-    single(synth.MoEShape(T=64, d=1024, f=2560, E=8, k=2), 0x2, {"MOE_TRIM_B": "1"})  # 32-row token boxes
     single(synth.MoEShape(T=32, d=256, f=512, E=4, k=2), moe.MOE_FLAG_FP8_WEIGHTS)
     for par in ("ep", "tp"):
         for p2p in (False, True):

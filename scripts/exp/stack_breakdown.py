@@ -1,5 +1,5 @@
 """Per-kernel times of the mid-size (stack, T=575) forward on one Mixtral layer:
-python scripts/exp/stack_breakdown.py [T] [flags]  (profiling events break PDL overlap)."""
+python scripts/exp/stack_breakdown.py [T] [flags] [field=v,... (moe_tuning)]  (profiling events break PDL overlap)."""
 import os
 import sys
 
@@ -10,9 +10,10 @@ import paper_2408_00008_b200 as moe  # noqa: E402
 
 T = int(sys.argv[1]) if len(sys.argv) > 1 else 575
 flags = int(sys.argv[2], 0) if len(sys.argv) > 2 else 0
+tuning = dict((kv.split("=")[0], int(kv.split("=")[1])) for kv in sys.argv[3].split(",")) if len(sys.argv) > 3 else None
 w = synth.make_weights(4096, 14336, 8, seed=0, device="cuda")
 x = synth.make_tokens(T, 4096, seed=1, device="cuda")
-blk = moe.MoEBlock(w["wg"], w["w1"], w["w3"], w["w2"], max_tokens=T, flags=flags)
+blk = moe.MoEBlock(w["wg"], w["w1"], w["w3"], w["w2"], max_tokens=T, flags=flags, tuning=tuning)
 counts = torch.empty(8, dtype=torch.int32, device="cuda")
 for _ in range(5):
     blk.forward(x)

@@ -1,6 +1,6 @@
-# sweep raster / L2-hint settings of the CTA-pair prefill GEMMs (MOE_PAIR_TUNE bits, see moe.cu)
+# sweep raster / L2-hint settings of the CTA-pair prefill GEMMs (moe_tuning.pair_order bits, include/moe.h)
 for t in "$@"; do
-  MOE_PAIR_TUNE=$t timeout -s KILL 300 python bench.py --config prefill --steps 4 --warmup 3 --no-cpu-baseline > gpurun_out/sweep_$t.log 2>&1
+  timeout -s KILL 300 python bench.py --tuning pair_order=$t --config prefill --steps 4 --warmup 3 --no-cpu-baseline > gpurun_out/sweep_$t.log 2>&1
   python - "$t" <<'PY'
 import json,sys
 t=sys.argv[1]

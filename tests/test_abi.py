@@ -74,3 +74,55 @@ def test_init_fails_loudly_without_gpu():
     with pytest.raises(moe.MoEError) as ei:
         moe.moe_init(moe.make_config(64, 128, 4, 2, 16))
     assert ei.value.status == moe.MOE_ERR_UNSUPPORTED
+
+
+def test_tuning_validation():
+    """moe_config.tuning (include/moe.h moe_tuning): out-of-range overrides and nonzero
+    reserved fields are rejected before anything runs; valid ones pass validation."""
+    import paper_2408_00008_b200 as moe
+    ok = moe.make_config(4096, 14336, 8, 2, 64, tuning={"g1_grid": 112, "spec_l2": -1, "pair_nblk": 1,
+                                                        "swap_nb_cap": 32, "weight_hint": 3})
+    moe.moe_packed_sizes(ok)
+    for bad in ({"pair_nblk": 3}, {"weight_hint": 4}, {"swap_nb_cap": 48}, {"g1_grid": -1}, {"g2_swap_rows": -5}):
+        with pytest.raises(moe.MoEError) as ei:
+            moe.moe_packed_sizes(moe.make_config(4096, 14336, 8, 2, 64, tuning=bad))
+        assert ei.value.status == moe.MOE_ERR_INVALID, bad
+    t = moe.make_tuning({"g1_grid": 1})
+    t.reserved[3] = 1
+    with pytest.raises(moe.MoEError):
+        moe.moe_packed_sizes(moe.make_config(4096, 14336, 8, 2, 64, tuning=t))
+    with pytest.raises(KeyError):
+        moe.make_tuning({"no_such_knob": 1})
+    # P2P groups are bounded by the one-warp signal kernel
+    with pytest.raises(moe.MoEError) as ei:
+        moe.moe_packed_sizes(moe.make_config(4096, 16384, 8, 2, 64, par=moe.MOE_PAR_TP, world_size=64,
+                                             flags=moe.MOE_FLAG_P2P))
+    assert ei.value.status == moe.MOE_ERR_UNSUPPORTED
+
+
+def test_struct_layout_matches_header(tmp_path):
+    """The ctypes mirrors of moe_config / moe_tuning / moe_aux / moe_expert_weights have
+    the size and field offsets a C compiler gives the header's structs."""
+    import subprocess
+    import paper_2408_00008_b200 as moe
+    structs = {"moe_config": moe.moe_config, "moe_tuning": moe.moe_tuning, "moe_aux": moe.moe_aux,
+               "moe_expert_weights": moe.moe_expert_weights}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "moe.h"', "int main(void) {"]
+    for name, py in structs.items():
+        lines.append(f'printf("{name} size %zu\\n", sizeof({name}));')
+        for fname, _ in py._fields_:
+            lines.append(f'printf("{name} {fname} %zu\\n", offsetof({name}, {fname}));')
+    lines.append("return 0; }")
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-std=c99", "-pedantic", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"),
+                    str(src), "-o", str(exe)], check=True)
+    got = {}
+    for ln in subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.splitlines():
+        n, f, v = ln.split()
+        got[(n, f)] = int(v)
+    for name, py in structs.items():
+        assert got[(name, "size")] == ctypes.sizeof(py), name
+        for fname, _ in py._fields_:
+            assert got[(name, fname)] == getattr(py, fname).offset, (name, fname)

@@ -29,9 +29,9 @@ def moe():
     return m
 
 
-def _block(moe, inp, k, max_tokens, flags=0, split_k=0):
+def _block(moe, inp, k, max_tokens, flags=0, split_k=0, tuning=None):
     return moe.MoEBlock(inp["wg"], inp["w1"], inp["w3"], inp["w2"], top_k=k, max_tokens=max_tokens,
-                        flags=flags, split_k=split_k)
+                        flags=flags, split_k=split_k, tuning=tuning)
 
 
 def _inputs(shape, seed, device="cuda"):
@@ -117,11 +117,7 @@ def test_mixed_gemm_paths(moe, flags):
     CTAs with MOE_FLAG_NO_PAIR) -- the h buffer hand-off between the two families."""
     shape = synth.MoEShape(T=600, d=512, f=1024, E=8, k=2)
     inp = _inputs(shape, 17)
-    os.environ["MOE_G2_SWAP_ROWS"] = "40"  # read at moe_init: w2 GEMM on tiles from 40 rows/expert
-    try:
-        blk = _block(moe, inp, 2, 600, flags)
-    finally:
-        del os.environ["MOE_G2_SWAP_ROWS"]
+    blk = _block(moe, inp, 2, 600, flags, tuning={"g2_swap_rows": 40})  # w2 GEMM on tiles from 40 rows/expert
     run = GpuRun(blk, inp["x"])
     check_forward(run, to_host_inputs(inp), 2)
     blk.close()
@@ -130,7 +126,7 @@ def test_mixed_gemm_paths(moe, flags):
 @pytest.mark.parametrize("T,d,f,E,k", [(16, 64, 128, 4, 2), (333, 320, 256, 6, 2), (1000, 512, 1024, 8, 2),
                                        (700, 768, 384, 4, 2), (129, 64, 128, 4, 2)])
 def test_pair_wide_tiles(moe, T, d, f, E, k):
-    """CTA-pair GEMMs with 256 x 512 tiles (MOE_PAIR_NBLK=2, single-buffered TMEM,
+    """CTA-pair GEMMs with 256 x 512 tiles (tuning pair_nblk=2, single-buffered TMEM,
     block-0-first catch-up) vs 256 x 256 tiles (NBLK=1, two accumulators): both against
     the oracle, and bit-identical to each other (the same MMAs accumulate each 256-column
     block in the same K order). Odd block counts (f/128 = 3, ceil(d/256) = 3) leave a
@@ -138,12 +134,8 @@ def test_pair_wide_tiles(moe, T, d, f, E, k):
     shape = synth.MoEShape(T=T, d=d, f=f, E=E, k=k)
     inp = _inputs(shape, 4000 + T)
     outs = []
-    for nblk in ("1", "2"):
-        os.environ["MOE_PAIR_NBLK"] = nblk  # read at moe_init
-        try:
-            blk = _block(moe, inp, k, T, moe.MOE_FLAG_FORCE_TILED)
-        finally:
-            del os.environ["MOE_PAIR_NBLK"]
+    for nblk in (1, 2):
+        blk = _block(moe, inp, k, T, moe.MOE_FLAG_FORCE_TILED, tuning={"pair_nblk": nblk})
         run = GpuRun(blk, inp["x"])
         check_forward(run, to_host_inputs(inp), k)
         outs.append(run.np("out_f32").copy())
@@ -157,47 +149,20 @@ def test_pair_wide_tiles(moe, T, d, f, E, k):
 @pytest.mark.parametrize("fp8", [False, True])
 @pytest.mark.parametrize("T,d,f,E", [(64, 512, 1024, 8), (300, 256, 512, 8), (100, 256, 512, 2)])
 def test_swap_nb_cap(moe, T, d, f, E, fp8):
-    """Swap-AB token tile capped at 32 (env MOE_SWAP_NB_CAP): experts with more rows run
+    """Swap-AB token tile capped at 32 (tuning swap_nb_cap): experts with more rows run
     several token tiles (device-side tile count), bf16 and FP8 weights."""
     shape = synth.MoEShape(T=T, d=d, f=f, E=E, k=2)
-    os.environ["MOE_SWAP_NB_CAP"] = "32"
-    try:
-        if fp8:
-            inp, qs, host = _fp8_inputs(shape, 5000 + T)
-            blk = moe.MoEBlock(inp["wg"], qs["w1"], qs["w3"], qs["w2"], top_k=2, max_tokens=T,
-                               flags=moe.MOE_FLAG_FP8_WEIGHTS)
-        else:
-            inp = _inputs(shape, 5000 + T)
-            host = to_host_inputs(inp)
-            blk = _block(moe, inp, 2, T, moe.MOE_FLAG_FORCE_SWAP)
-    finally:
-        del os.environ["MOE_SWAP_NB_CAP"]
+    tu = {"swap_nb_cap": 32}
+    if fp8:
+        inp, qs, host = _fp8_inputs(shape, 5000 + T)
+        blk = moe.MoEBlock(inp["wg"], qs["w1"], qs["w3"], qs["w2"], top_k=2, max_tokens=T,
+                           flags=moe.MOE_FLAG_FP8_WEIGHTS, tuning=tu)
+    else:
+        inp = _inputs(shape, 5000 + T)
+        host = to_host_inputs(inp)
+        blk = _block(moe, inp, 2, T, moe.MOE_FLAG_FORCE_SWAP, tuning=tu)
     run = GpuRun(blk, inp["x"])
     check_forward(run, host, 2)
-    blk.close()
-
-
-@pytest.mark.parametrize("parts", ["8", "3", "0"])
-@pytest.mark.parametrize("T,d,f,E", [(64, 1024, 2560, 8), (40, 512, 5120, 4), (300, 256, 2560, 8)])
-def test_tail_split(moe, T, d, f, E, parts):
-    """Decode w1/w3 GEMM with K-sliced tail tiles (gemm_sm100.cuh tail_plan; off by
-    default, env MOE_TAIL_PARTS): 160 tiles on 148 SMs leave 12 tail tiles, each run as
-    up to MOE_TAIL_PARTS slices whose fp32 partials are summed in slice order by the
-    completing CTA (0 = whole tiles).
-    Oracle parity, and bitwise determinism across calls (graph-free, counters reset)."""
-    shape = synth.MoEShape(T=T, d=d, f=f, E=E, k=2)
-    inp = _inputs(shape, 23)
-    os.environ["MOE_TAIL_PARTS"] = parts
-    try:
-        blk = _block(moe, inp, 2, T, 0x2)
-    finally:
-        del os.environ["MOE_TAIL_PARTS"]
-    run = GpuRun(blk, inp["x"])
-    check_forward(run, to_host_inputs(inp), 2)
-    for _ in range(3):
-        again = blk.forward(inp["x"])
-        torch.cuda.synchronize()
-        assert torch.equal(again.view(torch.int16), run.out.view(torch.int16))
     blk.close()
 
 
@@ -256,19 +221,6 @@ def test_speculative_prefetch_wrong_guess(moe, T):
     blk.close()
     run = GpuRun(_block(moe, inp, 2, T, MODES["swap"]), inp["x"])  # router path, same shapes
     check_forward(run, host, 2)
-
-
-@pytest.mark.parametrize("d", [384, 512])
-def test_g2_dual_units(moe, d, monkeypatch):
-    """Optional 256-row-unit w2 GEMM (MOE_G2_DUAL=1, read at moe_init): oracle parity,
-    including a hidden size whose last unit is half padding (d = 384)."""
-    monkeypatch.setenv("MOE_G2_DUAL", "1")
-    shape = synth.MoEShape(T=40, d=d, f=512, E=8, k=2)
-    inp = _inputs(shape, 300 + d)
-    host = to_host_inputs(inp)
-    blk = _block(moe, inp, 2, 40, MODES["swap"])
-    check_forward(GpuRun(blk, inp["x"]), host, 2)
-    blk.close()
 
 
 def test_t_zero_and_determinism(moe):
@@ -355,15 +307,14 @@ def test_c2_decode_full(moe, mixtral_weights, seed):
     blk.close()
 
 
-def test_c2_speculative_prefetch_bit_identical(moe, mixtral_weights, monkeypatch):
-    """The speculative L2 prefetch (MOE_SPEC_L2, read at moe_init) changes only timing:
-    64-token decode outputs are bit-identical with it off and at two depths."""
+def test_c2_speculative_prefetch_bit_identical(moe, mixtral_weights):
+    """The speculative L2 prefetch (tuning spec_l2) changes only timing: 64-token decode
+    outputs are bit-identical with it off and at two depths."""
     w, _ = mixtral_weights
     x = synth.make_tokens(64, 4096, seed=321, device="cuda")
     outs = []
-    for v in ("0", "16", "64"):
-        monkeypatch.setenv("MOE_SPEC_L2", v)
-        blk = moe.MoEBlock(w["wg"], w["w1"], w["w3"], w["w2"], top_k=2, max_tokens=64)
+    for v in (-1, 16, 64):
+        blk = moe.MoEBlock(w["wg"], w["w1"], w["w3"], w["w2"], top_k=2, max_tokens=64, tuning={"spec_l2": v})
         for _ in range(2):
             o = blk.forward(x)
         torch.cuda.synchronize()
@@ -831,8 +782,8 @@ def test_fp8_weights(moe, T, d, f, E):
 
 @pytest.mark.parametrize("T", [64, 300])
 def test_fp8_two_term_tokens(moe, T):
-    """FP8 w1/w3 GEMM on kind::f8f6f4 with tokens split into two E4M3 terms (MOE_FP8_X=1,
-    default) vs the fp16-token converter kernels (MOE_FP8_X=0). Rows scaled by 2^3 and
+    """FP8 w1/w3 GEMM on kind::f8f6f4 with tokens split into two E4M3 terms (default) vs the fp16-token
+    converter kernels (tuning fp8_fp16_tokens=1). Rows scaled by 2^3 and
     2^-10 (exact in bf16) and a zero row exercise the per-row power-of-two token scale
     and the fp16 h normalisation h * 2^(2s-6): the two-term path must pass the oracle on
     every row; the converter path (unnormalised fp16 h, which underflows for the 2^-10
@@ -848,12 +799,8 @@ def test_fp8_two_term_tokens(moe, T):
     host["x"] = inp["x"].float().cpu().numpy()
     outs = []
     for v in ("0", "1"):
-        os.environ["MOE_FP8_X"] = v
-        try:
-            blk = moe.MoEBlock(inp["wg"], qs["w1"], qs["w3"], qs["w2"], top_k=2, max_tokens=T,
-                               flags=moe.MOE_FLAG_FP8_WEIGHTS)
-        finally:
-            del os.environ["MOE_FP8_X"]
+        blk = moe.MoEBlock(inp["wg"], qs["w1"], qs["w3"], qs["w2"], top_k=2, max_tokens=T,
+                           flags=moe.MOE_FLAG_FP8_WEIGHTS, tuning={"fp8_fp16_tokens": int(v == "0")})
         run = GpuRun(blk, inp["x"])
         if v == "1":
             print("fp8x", T, check_forward(run, host, 2))
@@ -868,15 +815,11 @@ def test_fp8_two_term_tokens(moe, T):
 
 @pytest.mark.parametrize("T,d,f,E", [(64, 512, 1024, 8), (300, 256, 512, 8), (7, 128, 256, 2)])
 def test_fp8_w2_three_term(moe, T, d, f, E):
-    """Optional FP8 w2 GEMM on kind::f8f6f4 (env MOE_FP8_W2_X=1): h split into three E4M3
+    """Optional FP8 w2 GEMM on kind::f8f6f4 (tuning fp8_w2_split=1): h split into three E4M3
     terms per row (exact for fp16 h above ~1 % of the row max) by moe_h_split_kernel."""
     inp, qs, host = _fp8_inputs(synth.MoEShape(T=T, d=d, f=f, E=E, k=2), 1100 + T)
-    os.environ["MOE_FP8_W2_X"] = "1"
-    try:
-        blk = moe.MoEBlock(inp["wg"], qs["w1"], qs["w3"], qs["w2"], top_k=2, max_tokens=T,
-                           flags=moe.MOE_FLAG_FP8_WEIGHTS)
-    finally:
-        del os.environ["MOE_FP8_W2_X"]
+    blk = moe.MoEBlock(inp["wg"], qs["w1"], qs["w3"], qs["w2"], top_k=2, max_tokens=T,
+                       flags=moe.MOE_FLAG_FP8_WEIGHTS, tuning={"fp8_w2_split": 1})
     run = GpuRun(blk, inp["x"])
     check_forward(run, host, 2)
     blk.close()
