@@ -89,6 +89,13 @@ def parse():
     ap.add_argument("--par", default=None, choices=["ep", "tp", "hybrid", "none"],
                     help="multi-GPU variant (default: ep when N > 1)")
     ap.add_argument("--tp", type=int, default=2, help="TP degree of --par hybrid (EP degree = N / tp)")
+    ap.add_argument("--tuning", default="",
+                    help="moe_tuning overrides, 'field=v,field=v' (include/moe.h; A/B experiments)")
+    ap.add_argument("--shard", default=None, choices=["ep2", "ep4", "ep8", "tp2", "tp4", "tp8"],
+                    help="ONE GPU running one rank's share of the EP / TP variant (its E/G experts with the rows "
+                         "the global batch routes to them, or its f/G ffn slice): per-kernel roofline of the "
+                         "per-rank shapes of the 2/4/8-GPU runs (--config decode|prefill)")
+    ap.add_argument("--no-parity", action="store_true", help="skip the sampled per-rank oracle check")
     ap.add_argument("--p2p", action="store_true",
                     help="--par ep / tp: exchange through peer memory (MOE_FLAG_P2P: the producing kernels store "
                          "into the other GPUs' buffers) instead of NCCL collectives")
@@ -119,12 +126,25 @@ def load_peaks():
     return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "src": "fallback"}
 
 
+def parse_tuning(spec):
+    """'field=v,field=v' -> dict for moe_tuning (None if empty)."""
+    if not spec:
+        return None
+    out = {}
+    for kv in spec.split(","):
+        k, v = kv.split("=")
+        out[k.strip()] = int(v, 0)
+    return out
+
+
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+    """nvidia-smi clocks, power and throttle reasons sampled every 50 ms while the GPU
+    runs the step (bench.py keeps it loaded for >= 1 s: the timed passes plus a
+    sustained pass of the same step)."""
 
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,enforced.power.limit")
 
     def __init__(self, gpu_index):
         self.idx = gpu_index
@@ -134,7 +154,7 @@ class ClockSampler:
     def start(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thr = threading.Thread(target=self._read, daemon=True)
             self.thr.start()
@@ -154,8 +174,15 @@ class ClockSampler:
             self.proc.wait(timeout=2)
         except Exception:
             self.proc.kill()
-        sm = [float(r[1]) for r in self.rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if len(r) >= 9 and r[2].replace(".", "").isdigit()]
+        def num(v):
+            try:
+                return float(v)
+            except ValueError:
+                return None
+        sm = [num(r[1]) for r in self.rows if len(r) >= 9 and num(r[1]) is not None]
+        mx = [num(r[2]) for r in self.rows if len(r) >= 9 and num(r[2]) is not None]
+        pw = [num(r[3]) for r in self.rows if len(r) >= 9 and num(r[3]) is not None]
+        lim = [num(r[9]) for r in self.rows if len(r) >= 10 and num(r[9]) is not None]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = set()
         for r in self.rows:
@@ -165,7 +192,9 @@ class ClockSampler:
                         reasons.add(n)
         sm_sorted = sorted(sm)
         return {"sm_mhz": sm_sorted[len(sm_sorted) // 2] if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons), "samples": len(sm)}
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons), "samples": len(sm),
+                "sm_mhz_min": min(sm) if sm else None, "power_w_max": max(pw) if pw else None,
+                "power_limit_w": max(lim) if lim else None, "interval_ms": 50}
 
 
 def dist_setup(args):
@@ -204,13 +233,25 @@ def algorithmic(T, d, f, E, k, counts, wbytes=2):
                 g2_flops=g2_flops, touched=touched)
 
 
-def cpu_baseline_run(x_host, w_host, k, sample_tokens, min_s=0.0, max_s=30.0):
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def cpu_baseline_run(x_host, w_host, k, sample_tokens, min_s=0.0, max_s=30.0, threads=0):
     """Time the fp64 oracle (as it stands) on a bounded sample of the workload: passes
     over the first `sample_tokens` tokens of the batch, repeated until at least min_s
-    seconds of CPU work (capped at max_s)."""
+    seconds of CPU work (capped at max_s). threads > 0: OpenMP threads of the oracle
+    (restored afterwards); 0: all host cores."""
     import numpy as np
     import oracle
     ncores = os.cpu_count() or 1
+    prev = oracle.set_threads(threads) if threads > 0 else None
     T = x_host.shape[0]
     n = min(T, max(1, sample_tokens))
     toks = np.arange(n)
@@ -222,10 +263,205 @@ def cpu_baseline_run(x_host, w_host, k, sample_tokens, min_s=0.0, max_s=30.0):
         dt = time.perf_counter() - t0
         if dt >= min_s or dt * (passes + 1) / passes > max_s:
             break
-    threads = int(os.environ.get("OMP_NUM_THREADS", ncores))
-    return {"value": passes * n / dt, "unit": "tokens/s", "cores": min(threads, ncores, n), "kind": "oracle",
+    if prev is not None:
+        oracle.set_threads(prev)
+    used = threads if threads > 0 else int(os.environ.get("OMP_NUM_THREADS", ncores))
+    return {"value": passes * n / dt, "unit": "tokens/s", "cores": min(used, ncores, n), "kind": "oracle",
             "sample": f"{passes} pass(es) over {n} of the batch's {T} tokens (full Mixtral layer weights), fp64 C++ "
                       f"OpenMP over tokens, {dt:.1f} s"}, dt
+
+
+def cpu_baseline_full(x_host, w_host, k, sample_tokens):
+    """BASELINE.md CPU-baseline plan: the oracle with all host cores and single-threaded,
+    plus nproc and the CPU model name."""
+    cb, _ = cpu_baseline_run(x_host, w_host, k, sample_tokens, min_s=10.0)
+    one, _ = cpu_baseline_run(x_host, w_host, k, 2, min_s=4.0, max_s=15.0, threads=1)
+    cb["single_thread"] = {"value": one["value"], "unit": one["unit"], "cores": 1, "sample": one["sample"]}
+    cb["nproc"] = os.cpu_count()
+    cb["cpu_model"] = cpu_model()
+    return cb
+
+
+def sustained_steps(step, world, dev, seconds=1.0):
+    """Number of steps that keep the GPU busy for `seconds` (from 10 timed eager steps;
+    max over ranks so every rank issues the same collectives)."""
+    import torch
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for i in range(10):
+        step(i)
+    torch.cuda.synchronize()
+    per = max((time.perf_counter() - t0) / 10, 1e-5)
+    n = torch.tensor([int(seconds / per) + 1], device=dev)
+    if world > 1:
+        import torch.distributed as dist
+        dist.all_reduce(n, op=dist.ReduceOp.MAX)
+    return int(n.item())
+
+
+def bench_parity(moe, blk, x, T, w_host, k, world, dev, seed, n_sample=8):
+    """Sampled per-rank oracle check of the benchmarked configuration (north_star:
+    "matching the CPU oracle within the stated tolerance at 1/2/4/8 GPUs"): one forward
+    of this rank's first batch with aux outputs; routing of every local token checked
+    against the fp64 oracle outside the 1e-3 margin band (R4); n_sample tokens (first,
+    last, random) compared element by element, out_f32 and the bf16 output, normalised
+    by the oracle row RMS (R8), under the GPU's routing. Result reduced over ranks."""
+    import numpy as np
+    import torch
+    import oracle
+    import synth
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from parity import rel_err, routing_check
+    d = x.shape[1]
+    aux = {"topk_idx": torch.empty(max(T, 1), k, dtype=torch.int32, device=dev),
+           "out_f32": torch.empty(max(T, 1), d, dtype=torch.float32, device=dev)}
+    out = torch.empty(max(T, 1), d, dtype=torch.bfloat16, device=dev)
+    moe.moe_forward(blk.ctx, x, T, blk.router_w, blk.w13, blk.w2, out, aux, None, blk.s13, blk.s2)
+    torch.cuda.synchronize()
+    xb = synth.bf16_bits(x)
+    gidx = aux["topk_idx"][:T].cpu().numpy()
+    excl, bad = routing_check(gidx, oracle.router(xb, w_host["wg"], k))
+    rng = np.random.default_rng(seed + 17)
+    toks = np.unique(np.concatenate([[0, T - 1], rng.choice(T, min(T, n_sample), replace=False)])) if T else []
+    e32 = e16 = 0.0
+    if len(toks):
+        y = oracle.moe_forward(xb, w_host["wg"], w_host["w1"], w_host["w3"], w_host["w2"], k, forced_idx=gidx,
+                               tokens=toks)
+        e32 = float(rel_err(aux["out_f32"][:T].cpu().numpy()[toks], y).max())
+        e16 = float(rel_err(out[:T].float().cpu().numpy().astype(np.float64)[toks], y).max())
+    v = torch.tensor([e32, e16, float(len(bad)), float(len(toks)), float(excl.sum())], device=dev,
+                     dtype=torch.float64)
+    if world > 1:
+        import torch.distributed as dist
+        mx = v[:2].clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sm = v[2:].clone()
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        v = torch.cat([mx, sm])
+    e32, e16, nbad, ntok, nex = (float(t) for t in v.cpu())
+    return {"ok": bool(nbad == 0 and e32 <= 2e-2), "max_rel_err_f32": e32, "max_rel_err_bf16": e16,
+            "routing_mismatches": int(nbad), "margin_band_tokens": int(nex), "tokens_checked": int(ntok),
+            "ranks": world, "tol": 2e-2,
+            "how": "per rank: routing of every local token vs the fp64 oracle (margin rule), first/last/random "
+                   "tokens element by element under the GPU's routing; max / sums over ranks"}
+
+
+def run_shard(args):
+    """--shard ep<G>|tp<G>: the per-rank share of the G-GPU EP / TP variant, on ONE GPU
+    (SURVEY.md 8(d) wave table). EP: rank r's E/G experts and exactly the rows the
+    global batch routes to them (the GPU router's routing of the global batch; the
+    busiest rank, which sets the step time), run as the receive side does -- routed
+    (k = 1, gate applied at the source), permute, w1/w3, w2, combine. TP: the f/G ffn
+    slice of every expert over the whole batch. Prints one JSON line per shard with each
+    GEMM's achieved bytes (decode) or FLOPs (prefill) against the measured peaks. No
+    exchange is timed (that needs G GPUs); this isolates the per-rank kernels."""
+    import numpy as np
+    import torch
+    import synth
+    import paper_2408_00008_b200 as moe
+    torch.cuda.set_device(0)
+    dev = torch.device("cuda", 0)
+    kind, G = args.shard[:2], int(args.shard[2:])
+    Tg, d, f, E, k, ci = CONFIGS[args.config]
+    if args.config == "stack":
+        raise SystemExit("--shard: --config decode or prefill")
+    tuning = parse_tuning(args.tuning)
+    w = synth.make_weights(d, f, E, seed=args.seed, device=dev)
+    x = synth.make_tokens(Tg, d, seed=args.seed + 1, device=dev)
+    if kind == "tp":
+        f_l = f // G
+        blk = moe.MoEBlock(w["wg"], w["w1"][:, :f_l].contiguous(), w["w3"][:, :f_l].contiguous(),
+                           w["w2"][:, :, :f_l].contiguous(), top_k=k, max_tokens=Tg, tuning=tuning)
+        E_l, xin, T_run = E, x, Tg
+        routed = None
+        rows_note = {"tokens": Tg, "f_local": f_l}
+    else:
+        f_l, E_l = f, E // G
+        full = moe.MoEBlock(w["wg"], w["w1"], w["w3"], w["w2"], top_k=k, max_tokens=Tg)
+        aux = {"topk_idx": torch.empty(Tg, k, dtype=torch.int32, device=dev)}
+        full.forward(x, aux=aux)
+        torch.cuda.synchronize()
+        full.close()
+        idx = aux["topk_idx"].long()
+        rank_rows = [int(((idx >= r * E_l) & (idx < (r + 1) * E_l)).sum()) for r in range(G)]
+        r = int(np.argmax(rank_rows))                    # the busiest rank sets the step time
+        sel = (idx >= r * E_l) & (idx < (r + 1) * E_l)
+        tok = sel.nonzero()[:, 0]
+        xin = x[tok].contiguous()                        # the rows rank r receives
+        T_run = xin.shape[0]
+        loc = (idx[sel] - r * E_l).to(torch.int32).view(-1, 1).contiguous()
+        gate = torch.ones(T_run, 1, dtype=torch.float32, device=dev)
+        routed = (loc, gate)
+        e0, e1 = r * E_l, (r + 1) * E_l
+        blk = moe.MoEBlock(w["wg"][e0:e1].contiguous(), w["w1"][e0:e1].contiguous(), w["w3"][e0:e1].contiguous(),
+                           w["w2"][e0:e1].contiguous(), top_k=1, max_tokens=T_run, tuning=tuning)
+        rows_note = {"rank": r, "rows_per_rank": rank_rows, "E_local": E_l}
+    del w
+    torch.cuda.empty_cache()
+    out = torch.empty(T_run, d, dtype=torch.bfloat16, device=dev)
+    counts = torch.empty(E_l, dtype=torch.int32, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step(aux=None):
+        if routed is None:
+            moe.moe_forward(blk.ctx, xin, T_run, blk.router_w, blk.w13, blk.w2, out, aux, stream)
+        else:
+            blk.forward_routed(xin, routed[0], routed[1], out, aux, stream)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    step({"expert_counts": counts})
+    torch.cuda.synchronize()
+    cts = counts.cpu().tolist()
+    moe.moe_reset_profile(blk.ctx)
+    moe.moe_set_profiling(blk.ctx, True)
+    for _ in range(args.steps):
+        step()
+    torch.cuda.synchronize()
+    kt = moe.moe_kernel_times(blk.ctx)
+    moe.moe_set_profiling(blk.ctx, False)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        step()
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        g.replay()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    peaks = load_peaks()
+    A = int(sum(cts))
+    touched = sum(1 for c in cts if c > 0)
+    per = {n: (v[0] / v[1] if v[1] else 0.0) for n, v in kt.items()}
+    g1_b = touched * 2 * f_l * d * 2 + A * d * 2 + A * f_l * 2
+    g2_b = touched * d * f_l * 2 + A * f_l * 2 + A * d * 4
+    g1_f, g2_f = 2 * A * 2 * d * f_l, 2 * A * d * f_l
+    decode = args.config == "decode"
+    kern = {}
+    for name, b, fl in (("gemm1_w13_swiglu", g1_b, g1_f), ("gemm2_w2", g2_b, g2_f)):
+        t = per[name] * 1e-3
+        if decode:
+            kern[name] = {"ms": round(per[name], 5), "GB/s": b / t / 1e9, "frac_hbm": b / t / 1e9 / peaks["hbm_gbs"],
+                          "frac_read_stream": b / t / 1e9 / READ_STREAM_GBS, "bytes": b}
+        else:
+            kern[name] = {"ms": round(per[name], 5), "TFLOP/s": fl / t / 1e12,
+                          "frac_sustained": fl / t / 1e12 / peaks["bf16_tflops_sustained"], "flops": fl}
+    step_bytes = touched * 3 * f_l * d * 2 + 2 * T_run * d * 2
+    line = {"metric": "per-rank shard kernels (one GPU)", "shard": args.shard, "config": args.config,
+            "workload": f"BASELINE.json configs[3]/[4] per-rank share of the {args.config} batch T={Tg}",
+            "ms_per_step": ms, "graph_replay": True, "steps": args.steps,
+            "kernel_ms": {n: round(v, 5) for n, v in per.items() if kt[n][1]},
+            "kernels": kern, "expert_rows": cts, **rows_note,
+            "step_frac_hbm" if decode else "step_frac_sustained":
+                (step_bytes / (ms * 1e-3) / 1e9 / peaks["hbm_gbs"]) if decode
+                else ((g1_f + g2_f) / (ms * 1e-3) / 1e12 / peaks["bf16_tflops_sustained"]),
+            "peaks": peaks, "tuning": tuning}
+    print(json.dumps(line), flush=True)
+    blk.close()
 
 
 def run_reference(args):
@@ -263,7 +499,8 @@ def run_reference(args):
             "config": cfg,
             "cpu_baseline": {"value": val, "unit": "tokens/s", "cores": min(ncores, sample), "kind": "oracle",
                              "sample": f"{sample} of {T} tokens of the batch per step, full Mixtral layer weights, "
-                                       f"fp64 C++ (OpenMP over tokens), median of {len(times)} steps"},
+                                       f"fp64 C++ (OpenMP over tokens), median of {len(times)} steps",
+                             "nproc": ncores, "cpu_model": cpu_model()},
             "e2e": {"value": val, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -391,6 +628,9 @@ def main():
     if args.impl == "reference":
         run_reference(args)
         return
+    if args.shard:
+        run_shard(args)
+        return
     if args.config == "stack":
         import torch
         world, rank, local = dist_setup(args)
@@ -433,12 +673,15 @@ def main():
             w[n] = synth.quantize_fp8_rows(w[n])
     blk = moe.MoEBlock(w["wg"], w["w1"], w["w3"], w["w2"], top_k=k, max_tokens=T, par=pmap[par],
                        world_size=world if par != "none" else 1, rank=rank if par != "none" else 0, nccl_comm=comm,
-                       flags=flags, tp_size=tp_size, tp_comm=tp_comm)
+                       flags=flags, tp_size=tp_size, tp_comm=tp_comm, tuning=parse_tuning(args.tuning))
     if args.p2p:
         if world > 1:
             moe.p2p_connect_process_group(blk.ctx)
         else:
             blk.p2p_connect([blk.p2p_handle()])
+    # host copy of the bf16 weights for the sampled oracle check (FP8 weights: the FP8
+    # parity is covered by the tests; the oracle would need 11 GB of fp32 weights here)
+    w_host = None if (args.no_parity or args.fp8) else {n: synth.bf16_bits(v) for n, v in w.items()}
     del w["w1"], w["w3"], w["w2"]
     torch.cuda.empty_cache()
     out = torch.empty(T, d, dtype=torch.bfloat16, device=dev)
@@ -459,9 +702,18 @@ def main():
             import torch.distributed as dist
             dist.barrier()
 
-    # ---------------- timed region (device): K steps, kernel-level events live
+    # ---------------- clock record: the sampler runs from here through the timed passes;
+    # first >= 1 s of the same step back to back (a fixed step count, equal on all ranks)
+    # so the clocks are seen under sustained load, not only over the ms-long timed region
     clocks = ClockSampler(local)
     clocks.start()
+    t_load0 = time.perf_counter()
+    n_sustain = sustained_steps(lambda i: step(i), world, dev)
+    for i in range(n_sustain):
+        step(i)
+    torch.cuda.synchronize()
+
+    # ---------------- timed region (device): K steps, kernel-level events live
     moe.moe_reset_profile(blk.ctx)
     moe.moe_set_profiling(blk.ctx, True)
     launches0 = moe.moe_launch_count(blk.ctx)
@@ -506,7 +758,6 @@ def main():
     ev1.record(stream)
     torch.cuda.synchronize()
     barrier()
-    clk = clocks.stop()
     ms = ev0.elapsed_time(ev1) / args.steps
     if world > 1:
         import torch.distributed as dist
@@ -534,6 +785,9 @@ def main():
     if world > 1:
         import torch.distributed as dist
         dist.all_reduce(per_step, op=dist.ReduceOp.MAX)
+    clk = clocks.stop()
+    clk["load_s"] = round(time.perf_counter() - t_load0, 2)
+    clk["sustain_steps"] = n_sustain
     q = np.percentile(per_step.cpu().numpy(), [10, 50, 90])
     step_dist = {"p10": float(q[0]), "p50": float(q[1]), "p90": float(q[2]), "n": args.steps,
                  "how": "separate pass, CUDA event between consecutive steps, max over ranks"}
@@ -621,13 +875,14 @@ def main():
                 "h2d_bytes_per_step": T * d * 2, "d2h_bytes_per_step": T * d * 2,
                 "api": "moe_forward_host (pinned host tokens -> device -> host output)"},
     }
+    if w_host is not None:
+        line["parity"] = bench_parity(moe, blk, xs[0], T, w_host, k, world, dev, args.seed)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         wh = {n: synth.bf16_bits(v) for n, v in synth.make_weights(d, f, E, seed=args.seed, device=dev).items()}
         ncores = os.cpu_count() or 1
         # bounded sample: passes over (up to) the first 64 tokens of the batch -- the whole
         # batch at decode -- repeated for >= 10 s of CPU work
-        cb, _ = cpu_baseline_run(synth.bf16_bits(xs[0]), wh, k, min(T, 64), min_s=10.0)
-        line["cpu_baseline"] = cb
+        line["cpu_baseline"] = cpu_baseline_full(synth.bf16_bits(xs[0]), wh, k, min(T, 64))
     if rank == 0:
         print(json.dumps(line), flush=True)
     if args.p2p and world > 1:  # peers may still read / write my region until everyone is done

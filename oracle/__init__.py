@@ -48,8 +48,9 @@ def _load():
         lib.oracle_moe_forward.argtypes = [I, P, P, P, P, P, L, I, I, I, I, P, P, L, I, P]
         lib.oracle_partition.argtypes = [I, P, P, P, P, P, L, I, I, I, I, I, I, P, L, P]
         lib.oracle_permutation.argtypes = [P, L, I, I, I, P, P, P]
+        lib.oracle_set_threads.argtypes = [I]
         for fn in (lib.oracle_router, lib.oracle_moe_forward, lib.oracle_partition,
-                   lib.oracle_permutation):
+                   lib.oracle_permutation, lib.oracle_set_threads):
             fn.restype = ctypes.c_int
         _lib = lib
     return _lib
@@ -143,16 +144,28 @@ def permutation(idx, E, align):
     return {"counts": counts, "offsets": offsets, "pos": pos}
 
 
+def set_threads(n):
+    """OpenMP threads of the oracle's parallel loops (n <= 0: unchanged); returns the
+    previous maximum. Timing only (bench.py cpu_baseline): results do not depend on it."""
+    return int(_load().oracle_set_threads(int(n)))
+
+
 def bf16_round(a):
-    """Round fp32/fp64 values to bf16 (RNE) and return fp64 -- used to form the
-    bf16 rounding floor of the expected output (reading R8). Own bit
-    arithmetic: float32 bits + 0x7FFF + lsb, truncated."""
-    f = np.asarray(a, np.float32)
-    u = f.view(np.uint32).astype(np.uint64)
-    lsb = (u >> 16) & 1
-    r = ((u + 0x7FFF + lsb) >> 16).astype(np.uint32) << 16
-    # NaN stays NaN; Inf/overflow follows IEEE RNE naturally with this formula
-    return r.astype(np.uint32).view(np.float32).astype(np.float64)
+    """Round fp32/fp64 values to bf16 (RNE, one rounding straight from the input's own
+    precision -- no intermediate fp32 step) and return fp64 -- used to form the bf16
+    rounding floor of the expected output (reading R8). bf16 keeps 8
+    significant bits and the fp32 exponent range: a = q * 2^(e-8) with q in [128, 256)
+    for normals (e from frexp, clamped at the subnormal exponent -125), q rounded to an
+    integer half-to-even (np.rint), magnitudes >= 2^128 -> inf."""
+    a = np.asarray(a, np.float64)
+    with np.errstate(over="ignore", invalid="ignore"):
+        _, e = np.frexp(a)
+        e = np.maximum(e, -125)
+        q = np.ldexp(a, 8 - e)                  # exact: a power-of-two scaling
+        r = np.ldexp(np.rint(q), e - 8)
+        r = np.where(np.abs(r) >= 2.0 ** 128, np.copysign(np.inf, a), r)
+        r = np.where(np.isfinite(a), r, a)      # inf / nan pass through
+    return r
 
 
 def bf16_to_f64(bits):

@@ -34,6 +34,7 @@
 #include <cstdint>
 #include <cstring>
 #include <cmath>
+#include <omp.h>
 #include <vector>
 #include <algorithm>
 
@@ -288,6 +289,15 @@ int oracle_permutation(const int32_t* idx, int64_t T, int k, int E, int align,
             seen[e] += 1;
         }
     return 0;
+}
+
+// Host-thread count of the OpenMP loops (bench.py times the oracle both with all
+// cores and single-threaded, BASELINE.md "CPU baseline plan"); returns the previous
+// setting. Does not touch the arithmetic: every token is computed the same way.
+int oracle_set_threads(int n) {
+    const int prev = omp_get_max_threads();
+    if (n > 0) omp_set_num_threads(n);
+    return prev;
 }
 
 }  // extern "C"

@@ -858,11 +858,16 @@ moe_status run_gemms(moe_ctx* c, GemmPaths gp, int64_t rows_bound, int64_t rows_
     }
     const int ncl = c->num_sms / 2;
     {
-        // expert-stride grid only where it also balances the waves (all experts used)
+        // bf16, one token tile per expert: the expert-stride grid where it also balances the
+        // waves (all experts used; Mixtral single GPU: 896 units on 112 CTAs), else equal
+        // waves over the units (TP4: 224 units -> 112 CTAs of 2 instead of 76 CTAs doing a
+        // second unit while 72 idle; TP8 / EP8: 112 units -> 112 CTAs)
         const int wt = c->f_local / 128, ns = c->num_sms;
         const int gs = wt <= ns ? wt * (ns / wt) : ns;
+        const int64_t U1 = (int64_t)c->E_local * wt, wv1 = (U1 + ns - 1) / ns;
         c->g1_grid_now = c->g1_grid > 0 ? std::min(c->g1_grid, ns)
-                       : (!c->fp8 && rows_bound <= nb1 && wt <= ns && (c->E_local * wt) % gs == 0) ? gs : ns;
+                       : (c->fp8 || rows_bound > nb1) ? ns
+                       : (wt <= ns && U1 % gs == 0) ? gs : (int)std::min<int64_t>(ns, (U1 + wv1 - 1) / wv1);
         // FP8 w1/w3 (fp8x) at the 32-token tile (mean <= 16 rows per expert): equal waves
         // over the E_l * wt one-tile-per-expert units (896 -> 128 CTAs; ab_grid_fp8_2.log:
         // 165.6 -> 164.2 us, step 0.2685 -> 0.2668 ms)
@@ -907,7 +912,13 @@ moe_status run_gemms(moe_ctx* c, GemmPaths gp, int64_t rows_bound, int64_t rows_
         // 0.434 at 2 and 0.442 at 4 (each tile's K range is one contiguous region and
         // >= 108 SMs stay busy in the last wave); the T=575 stack 17.4 ms at 2 vs 18.2 at
         // 1 and 17.4 at 4; FP8 0.2917 ms at 4 vs 0.2970 at 2.
-        const int auto_splits = c->fp8 ? 4 : nb2 <= 64 ? 1 : 2;
+        // Few weight units (EP / hybrid ranks holding E/G experts): split K until the units
+        // cover the SMs -- EP8 at decode has 32 units of 128 W2 rows (21.6 % of 148 SMs),
+        // 4 splits -> 128 units (SURVEY 8(d) wave table); EP4 64 -> 2 splits.
+        const int64_t U0 = (int64_t)c->E_local * ((c->d + 127) / 128);
+        int auto_splits = c->fp8 ? 4 : nb2 <= 64 ? 1 : 2;
+        if (rows_bound <= nb2 && 4 * U0 < 3 * (int64_t)c->num_sms)
+            auto_splits = std::max<int>(auto_splits, (int)std::min<int64_t>(c->max_splits, c->num_sms / U0));
         splits = c->cfg.split_k ? c->cfg.split_k : auto_splits;
         splits = (int)std::max<int64_t>(1, std::min<int64_t>(splits, c->y_elems / (rows_needed * c->d)));
         splits = std::min(splits, c->f_local / (c->fp8_g2_kb256 ? 256 : c->fp8_kb128 ? 128 : kBK));  // >= 1 K block per split

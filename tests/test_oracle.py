@@ -378,3 +378,42 @@ def test_bf16_helpers():
     bits = synth.bf16_bits(v.to(torch.bfloat16))
     np.testing.assert_array_equal(oracle.bf16_to_f64(bits), v.to(torch.bfloat16).double().numpy())
     np.testing.assert_array_equal(oracle.bf16_round(v.numpy()), v.to(torch.bfloat16).double().numpy())
+
+
+def test_bf16_round_fp64_single_rounding():
+    """bf16_round on fp64 inputs rounds ONCE (no fp64 -> fp32 -> bf16 double rounding).
+    Pins: hand-derived cases where double rounding is wrong, and brute-force RNE in
+    exact rational arithmetic (fractions.Fraction) over random fp64 values incl.
+    subnormal-range and overflow edges."""
+    from fractions import Fraction
+    # 1 + 2^-8 is the midpoint of the bf16 neighbours 1 and 1 + 2^-7; a hair above it must
+    # round UP, although fp32(1 + 2^-8 + 2^-30) is the midpoint itself (which rounds to even = 1)
+    cases = {1 + 2.0 ** -8 + 2.0 ** -30: 1 + 2.0 ** -7, 1 + 2.0 ** -8 - 2.0 ** -30: 1.0,
+             1 + 2.0 ** -8: 1.0, 1 + 3 * 2.0 ** -8: 1 + 2.0 ** -6, -(1 + 2.0 ** -8 + 2.0 ** -40): -(1 + 2.0 ** -7),
+             2.0 ** 128: np.inf, 3.3895313892515355e38: 3.3895313892515355e38, 0.0: 0.0}
+    got = oracle.bf16_round(np.array(list(cases)))
+    np.testing.assert_array_equal(got, np.array(list(cases.values())))
+
+    def rne_exact(x):
+        if x == 0:
+            return 0.0
+        fx = Fraction(x)
+        s = -1 if fx < 0 else 1
+        fx = abs(fx)
+        e = 0
+        while fx >= 2 ** (e + 1):
+            e += 1
+        while fx < 2 ** e:
+            e -= 1
+        e = max(e, -126)                      # bf16 subnormals share the spacing 2^-133
+        ulp = Fraction(2) ** (e - 7)
+        q, rem = divmod(fx, ulp)
+        if rem * 2 > ulp or (rem * 2 == ulp and q % 2 == 1):
+            q += 1
+        v = q * ulp
+        return s * (np.inf if v >= 2 ** 128 else float(v))
+
+    rng = np.random.default_rng(5)
+    xs = np.concatenate([rng.standard_normal(300) * 10.0 ** rng.integers(-5, 5, 300),
+                         rng.standard_normal(50) * 2.0 ** -130, rng.standard_normal(20) * 3e38])
+    np.testing.assert_array_equal(oracle.bf16_round(xs), np.array([rne_exact(float(x)) for x in xs]))
