@@ -91,10 +91,11 @@ def parse():
     ap.add_argument("--tp", type=int, default=2, help="TP degree of --par hybrid (EP degree = N / tp)")
     ap.add_argument("--tuning", default="",
                     help="moe_tuning overrides, 'field=v,field=v' (include/moe.h; A/B experiments)")
-    ap.add_argument("--shard", default=None, choices=["ep2", "ep4", "ep8", "tp2", "tp4", "tp8"],
+    ap.add_argument("--shard", default=None, choices=["ep1", "ep2", "ep4", "ep8", "tp1", "tp2", "tp4", "tp8"],
                     help="ONE GPU running one rank's share of the EP / TP variant (its E/G experts with the rows "
                          "the global batch routes to them, or its f/G ffn slice): per-kernel roofline of the "
                          "per-rank shapes of the 2/4/8-GPU runs (--config decode|prefill)")
+    ap.add_argument("--split-k", type=int, default=0, help="moe_config.split_k of the decode w2 GEMM (0 = auto)")
     ap.add_argument("--no-parity", action="store_true", help="skip the sampled per-rank oracle check")
     ap.add_argument("--p2p", action="store_true",
                     help="--par ep / tp: exchange through peer memory (MOE_FLAG_P2P: the producing kernels store "
@@ -362,16 +363,15 @@ def run_shard(args):
     torch.cuda.set_device(0)
     dev = torch.device("cuda", 0)
     kind, G = args.shard[:2], int(args.shard[2:])
-    Tg, d, f, E, k, ci = CONFIGS[args.config]
-    if args.config == "stack":
-        raise SystemExit("--shard: --config decode or prefill")
+    Tg, d, f, E, k, ci = CONFIGS[args.config]  # stack: ONE layer of the T = 575 mixed batch
     tuning = parse_tuning(args.tuning)
     w = synth.make_weights(d, f, E, seed=args.seed, device=dev)
     x = synth.make_tokens(Tg, d, seed=args.seed + 1, device=dev)
     if kind == "tp":
         f_l = f // G
         blk = moe.MoEBlock(w["wg"], w["w1"][:, :f_l].contiguous(), w["w3"][:, :f_l].contiguous(),
-                           w["w2"][:, :, :f_l].contiguous(), top_k=k, max_tokens=Tg, tuning=tuning)
+                           w["w2"][:, :, :f_l].contiguous(), top_k=k, max_tokens=Tg, tuning=tuning,
+                           split_k=args.split_k)
         E_l, xin, T_run = E, x, Tg
         routed = None
         rows_note = {"tokens": Tg, "f_local": f_l}
@@ -394,7 +394,8 @@ def run_shard(args):
         routed = (loc, gate)
         e0, e1 = r * E_l, (r + 1) * E_l
         blk = moe.MoEBlock(w["wg"][e0:e1].contiguous(), w["w1"][e0:e1].contiguous(), w["w3"][e0:e1].contiguous(),
-                           w["w2"][e0:e1].contiguous(), top_k=1, max_tokens=T_run, tuning=tuning)
+                           w["w2"][e0:e1].contiguous(), top_k=1, max_tokens=T_run, tuning=tuning,
+                           split_k=args.split_k)
         rows_note = {"rank": r, "rows_per_rank": rank_rows, "E_local": E_l}
     del w
     torch.cuda.empty_cache()
@@ -403,10 +404,11 @@ def run_shard(args):
     stream = torch.cuda.current_stream()
 
     def step(aux=None):
+        st = torch.cuda.current_stream()  # the capture stream inside torch.cuda.graph
         if routed is None:
-            moe.moe_forward(blk.ctx, xin, T_run, blk.router_w, blk.w13, blk.w2, out, aux, stream)
+            moe.moe_forward(blk.ctx, xin, T_run, blk.router_w, blk.w13, blk.w2, out, aux, st)
         else:
-            blk.forward_routed(xin, routed[0], routed[1], out, aux, stream)
+            blk.forward_routed(xin, routed[0], routed[1], out, aux, st)
 
     for _ in range(max(3, args.warmup)):
         step()
@@ -440,7 +442,7 @@ def run_shard(args):
     g1_b = touched * 2 * f_l * d * 2 + A * d * 2 + A * f_l * 2
     g2_b = touched * d * f_l * 2 + A * f_l * 2 + A * d * 4
     g1_f, g2_f = 2 * A * 2 * d * f_l, 2 * A * d * f_l
-    decode = args.config == "decode"
+    decode = args.config != "prefill"  # decode and the T = 575 stack layer are HBM-bound
     kern = {}
     for name, b, fl in (("gemm1_w13_swiglu", g1_b, g1_f), ("gemm2_w2", g2_b, g2_f)):
         t = per[name] * 1e-3
@@ -452,7 +454,8 @@ def run_shard(args):
                           "frac_sustained": fl / t / 1e12 / peaks["bf16_tflops_sustained"], "flops": fl}
     step_bytes = touched * 3 * f_l * d * 2 + 2 * T_run * d * 2
     line = {"metric": "per-rank shard kernels (one GPU)", "shard": args.shard, "config": args.config,
-            "workload": f"BASELINE.json configs[3]/[4] per-rank share of the {args.config} batch T={Tg}",
+            "workload": f"BASELINE.json configs[3]/[4] per-rank share of the {args.config} batch T={Tg}"
+                        + (" (one layer of the 32-layer stack)" if args.config == "stack" else ""),
             "ms_per_step": ms, "graph_replay": True, "steps": args.steps,
             "kernel_ms": {n: round(v, 5) for n, v in per.items() if kt[n][1]},
             "kernels": kern, "expert_rows": cts, **rows_note,
@@ -673,7 +676,8 @@ def main():
             w[n] = synth.quantize_fp8_rows(w[n])
     blk = moe.MoEBlock(w["wg"], w["w1"], w["w3"], w["w2"], top_k=k, max_tokens=T, par=pmap[par],
                        world_size=world if par != "none" else 1, rank=rank if par != "none" else 0, nccl_comm=comm,
-                       flags=flags, tp_size=tp_size, tp_comm=tp_comm, tuning=parse_tuning(args.tuning))
+                       flags=flags, tp_size=tp_size, tp_comm=tp_comm, tuning=parse_tuning(args.tuning),
+                       split_k=args.split_k)
     if args.p2p:
         if world > 1:
             moe.p2p_connect_process_group(blk.ctx)

@@ -1,7 +1,7 @@
 # Per-rank shard shapes on one GPU (bench.py --shard), decode and prefill.
 # usage: bash scripts/shard_sweep.sh <tag> [configs] [extra bench args]
 TAG=${1:-run}; CONFS=${2:-"decode prefill"}; shift 2
-for c in $CONFS; do for s in ep2 ep4 ep8 tp2 tp4 tp8; do
+for c in $CONFS; do for s in ${SHARDS:-ep2 ep4 ep8 tp2 tp4 tp8}; do
   st=20; [ $c = prefill ] && st=5
   timeout -s KILL 300 python bench.py --shard $s --config $c --steps $st --warmup 3 "$@" 2>&1 | grep "^{" >> gpurun_out/shard_${c}_$TAG.jsonl
 done; done
