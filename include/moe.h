@@ -132,7 +132,9 @@ typedef struct moe_tuning {
                                instead of two E4M3 token terms on kind::f8f6f4 (0)          */
     int32_t fp8_w2_split;   /* FP8 weights: 1 = w2 GEMM on three E4M3 terms of h
                                (kind::f8f6f4) instead of fp16 h with converter warps (0)    */
-    int32_t reserved[11];   /* must be zero                                                  */
+    int32_t g1_nb;          /* force the swap-AB token tile of the w1/w3 GEMM: 32/64/128/192 (0: auto) */
+    int32_t g2_nb;          /* same for the w2 GEMM, also 256 (0: auto)                        */
+    int32_t reserved[9];    /* must be zero                                                  */
 } moe_tuning;
 
 typedef struct {

@@ -15,6 +15,7 @@
 #include <unistd.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -232,6 +233,7 @@ struct moe_ctx {
     // with two accumulators. G2 band counts wide tiles when 2.
     int pair_nblk = 2;
     int swap_nb_cap = 0;      // cap of the swap-path token tile (tuning; see run_gemms)
+    int tune_g1_nb = 0, tune_g2_nb = 0;  // forced swap-path token tiles (tuning g1_nb / g2_nb; 0 = auto)
     // CUDA-core router (2 tokens / block, 32 blocks at T = 64) for T <= this.
     // r01 64-token decode, interleaved: 0.4335 vs 0.4312 ms with the mma.sync router (4 blocks)
     int router_cc_max_T = 0;
@@ -316,7 +318,7 @@ struct moe_ctx {
     // TMA descriptors: workspace operands
     CUtensorMap tm_x_tiled{}, tm_h_tiled{};
     CUtensorMap tm_h_store{}, tm_y_store{};       // CTA-pair epilogue TMA stores
-    CUtensorMap tm_x_swap[4]{}, tm_h_swap[4]{};  // NB = 32, 64, 128, 256
+    CUtensorMap tm_x_swap[5]{}, tm_h_swap[5]{};  // NB = 32, 64, 128, 256, 192
     // weight descriptor cache (keyed by pointer)
     struct WeightMaps {
         const void* w13 = nullptr;
@@ -555,7 +557,7 @@ moe_status validate_cfg(const moe_config* cfg, moe_ctx* c) {
     for (int i = 0; i < 2; ++i)
         if (cfg->reserved[i]) return fail(c, MOE_ERR_INVALID, "reserved fields must be zero");
     if (const moe_tuning* tu = cfg->tuning) {
-        for (int i = 0; i < 11; ++i)
+        for (int i = 0; i < 9; ++i)
             if (tu->reserved[i]) return fail(c, MOE_ERR_INVALID, "tuning.reserved fields must be zero");
         if (tu->g1_swap_rows < 0 || tu->g2_swap_rows < 0 || tu->g1_grid < 0 || tu->g2_grid < 0 ||
             tu->swap_nb_cap < 0 || tu->router_cc_max_T < 0 || tu->pair_order < 0)
@@ -564,6 +566,9 @@ moe_status validate_cfg(const moe_config* cfg, moe_ctx* c) {
         if (tu->weight_hint < 0 || tu->weight_hint > 3) return fail(c, MOE_ERR_INVALID, "tuning.weight_hint must be 0..3");
         if (tu->swap_nb_cap && tu->swap_nb_cap != 32 && tu->swap_nb_cap != 64 && tu->swap_nb_cap != 128)
             return fail(c, MOE_ERR_INVALID, "tuning.swap_nb_cap must be 0, 32, 64 or 128");
+        auto nb_ok = [](int v, bool g2) { return v == 0 || v == 32 || v == 64 || v == 128 || v == 192 || (g2 && v == 256); };
+        if (!nb_ok(tu->g1_nb, false) || !nb_ok(tu->g2_nb, true))
+            return fail(c, MOE_ERR_INVALID, "tuning.g1_nb must be 0/32/64/128/192, g2_nb also 256");
     }
     if ((cfg->flags & MOE_FLAG_FORCE_SWAP) && (cfg->flags & MOE_FLAG_FORCE_TILED))
         return fail(c, MOE_ERR_INVALID, "FORCE_SWAP and FORCE_TILED are exclusive");
@@ -814,17 +819,40 @@ GemmPaths gemm_paths(const moe_ctx* c, int64_t rows_expected) {
 // rows_bound: upper bound of the rows of any one local expert (picks the swap-path
 // token tile NB so one tile covers the whole expert at decode); rows_total: bound
 // of all permuted rows (sizes the split-K partial buffers).
-moe_status run_gemms(moe_ctx* c, GemmPaths gp, int64_t rows_bound, int64_t rows_total, int* splits_out,
-                     cudaStream_t st) {
+// Smallest supported swap-AB token tile >= n (GEMM1: 32, 64, 128, 192; GEMM2 adds 256).
+int swap_nb_ceil(int n, bool g2) {
+    if (n <= 32) return 32;
+    if (n <= 64) return 64;
+    if (n <= 128) return 128;
+    if (n <= 192 || !g2) return 192;
+    return 256;
+}
+
+moe_status run_gemms(moe_ctx* c, GemmPaths gp, int64_t rows_bound, int64_t rows_total, int64_t rows_expected,
+                     int* splits_out, cudaStream_t st) {
     moe_status s;
     int splits = 1;
     c->split_stride = 0;
     // Token tile NB of the swap kernels: one tile covers an expert's rows when possible
-    // (the weight tile then streams once). GEMM1 stops at 128 (NB = 256 leaves its
-    // w1|w3 accumulators single-buffered: measured slower, 32-layer stack r01), GEMM2
-    // goes to 256; FP8 kernels stop at 128.
-    const int nbw = (int)std::max<int64_t>(32, std::min<int64_t>(256, next_pow2((int)std::min<int64_t>(rows_bound, 1 << 20))));
-    int nb1 = std::min(nbw, 128), nb2 = c->fp8 ? nb1 : nbw;
+    // (the weight tile then streams once from HBM and once from L2). rows_bound (an exact
+    // bound: no expert gets more rows than tokens) <= 128: the power of two above it
+    // (decode). Beyond, a statistical bound on the busiest expert, mean + 4 sqrt(mean)
+    // of the expected rows per local expert (T = 575 stack: 144 + 48 -> 192; an expert
+    // with more rows just runs a second token tile), capped at 192 for the w1/w3 GEMM
+    // (a and b accumulators of 192 columns: single-buffered TMEM) and 256 for w2.
+    int nb1, nb2;
+    int64_t need = rows_bound;  // rows the busiest local expert is expected to hold (at most)
+    if (rows_bound <= 128) {
+        nb1 = nb2 = std::max(32, next_pow2((int)rows_bound));
+    } else {
+        const double mean = (double)std::max<int64_t>(1, rows_expected) / c->E_local;
+        need = std::min<int64_t>(rows_bound, (int64_t)(mean + 4.0 * std::sqrt(mean)) + 1);
+        nb1 = swap_nb_ceil((int)std::min<int64_t>(need, 192), false);
+        nb2 = swap_nb_ceil((int)std::min<int64_t>(need, 256), true);
+    }
+    if (c->tune_g1_nb) nb1 = c->tune_g1_nb;
+    if (c->tune_g2_nb) nb2 = c->tune_g2_nb;
+    if (c->fp8) nb1 = nb2 = std::min(nb1, 128);  // FP8 kernels: token tiles up to 128
     // experiment knob (env MOE_SWAP_NB_CAP): cap the swap-path token tile below the
     // worst-case bound; an expert with more rows then takes several token tiles
     // (device-side tile count: still correct), re-streaming its weights per tile
@@ -846,7 +874,7 @@ moe_status run_gemms(moe_ctx* c, GemmPaths gp, int64_t rows_bound, int64_t rows_
     c->swap_w_hint = c->swap_hint_mode == 1 ? ptx::kEvictFirst
                    : c->swap_hint_mode == 2 ? ptx::kEvictNormal
                    : c->swap_hint_mode == 3 ? ptx::kEvictLast
-                   : (rows_bound > nb1 ? ptx::kEvictNormal : ptx::kEvictFirst);
+                   : (need > nb1 ? ptx::kEvictNormal : ptx::kEvictFirst);
     const bool pair = !(c->cfg.flags & MOE_FLAG_NO_PAIR);
     // CTA-pair (cta_group::2) 256x256 tiles, one cluster of 2 CTAs per TPC; tile order
     // per GEMM (see pair_decode); env MOE_PAIR_TUNE overrides for experiments:
@@ -866,7 +894,7 @@ moe_status run_gemms(moe_ctx* c, GemmPaths gp, int64_t rows_bound, int64_t rows_
         const int gs = wt <= ns ? wt * (ns / wt) : ns;
         const int64_t U1 = (int64_t)c->E_local * wt, wv1 = (U1 + ns - 1) / ns;
         c->g1_grid_now = c->g1_grid > 0 ? std::min(c->g1_grid, ns)
-                       : (c->fp8 || rows_bound > nb1) ? ns
+                       : (c->fp8 || need > nb1) ? ns
                        : (wt <= ns && U1 % gs == 0) ? gs : (int)std::min<int64_t>(ns, (U1 + wv1 - 1) / wv1);
         // FP8 w1/w3 (fp8x) at the 32-token tile (mean <= 16 rows per expert): equal waves
         // over the E_l * wt one-tile-per-expert units (896 -> 128 CTAs; ab_grid_fp8_2.log:
@@ -877,10 +905,11 @@ moe_status run_gemms(moe_ctx* c, GemmPaths gp, int64_t rows_bound, int64_t rows_
         }
     }
     if (gp.swap1) {
-        const int i1 = nb1 == 32 ? 0 : nb1 == 64 ? 1 : 2;
+        const int i1 = nb1 == 32 ? 0 : nb1 == 64 ? 1 : nb1 == 128 ? 2 : 4;
         if (nb1 == 32) s = run_swap_g1<32>(c, i1, &c->cur_w, st);
         else if (nb1 == 64) s = run_swap_g1<64>(c, i1, &c->cur_w, st);
-        else s = run_swap_g1<128>(c, i1, &c->cur_w, st);
+        else if (nb1 == 128) s = run_swap_g1<128>(c, i1, &c->cur_w, st);
+        else s = run_swap_g1<192>(c, i1, &c->cur_w, st);
         if (s) return s;
     } else if (pair) {
         const int nblk = c->gather_now ? 1 : c->pair_nblk;  // gather4 token fetch: 256 x 256 tiles only
@@ -917,7 +946,7 @@ moe_status run_gemms(moe_ctx* c, GemmPaths gp, int64_t rows_bound, int64_t rows_
         // 4 splits -> 128 units (SURVEY 8(d) wave table); EP4 64 -> 2 splits.
         const int64_t U0 = (int64_t)c->E_local * ((c->d + 127) / 128);
         int auto_splits = c->fp8 ? 4 : nb2 <= 64 ? 1 : 2;
-        if (rows_bound <= nb2 && 4 * U0 < 3 * (int64_t)c->num_sms)
+        if (need <= nb2 && 4 * U0 < 3 * (int64_t)c->num_sms)
             auto_splits = std::max<int>(auto_splits, (int)std::min<int64_t>(c->max_splits, c->num_sms / U0));
         splits = c->cfg.split_k ? c->cfg.split_k : auto_splits;
         splits = (int)std::max<int64_t>(1, std::min<int64_t>(splits, c->y_elems / (rows_needed * c->d)));
@@ -929,11 +958,12 @@ moe_status run_gemms(moe_ctx* c, GemmPaths gp, int64_t rows_bound, int64_t rows_
             const int ns = c->num_sms;
             const int64_t waves = (U + ns - 1) / ns;
             c->g2_grid_now = c->g2_grid > 0 ? std::min(c->g2_grid, ns)
-                           : (!c->fp8 && rows_bound <= nb2) ? (int)std::min<int64_t>(ns, (U + waves - 1) / waves) : ns;
+                           : (!c->fp8 && need <= nb2) ? (int)std::min<int64_t>(ns, (U + waves - 1) / waves) : ns;
         }
         if (nb2 == 32) s = run_swap_g2<32>(c, 0, &c->cur_w, splits, st);
         else if (nb2 == 64) s = run_swap_g2<64>(c, 1, &c->cur_w, splits, st);
         else if (nb2 == 128) s = run_swap_g2<128>(c, 2, &c->cur_w, splits, st);
+        else if (nb2 == 192) s = run_swap_g2<192>(c, 4, &c->cur_w, splits, st);
         else s = run_swap_g2<256>(c, 3, &c->cur_w, splits, st);
         if (s) return s;
     } else if (pair) {
@@ -1347,6 +1377,8 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
         c->pair_tune = tu->pair_order;
         if (tu->pair_nblk) c->pair_nblk = tu->pair_nblk == 1 ? 1 : 2;
         c->swap_nb_cap = tu->swap_nb_cap;
+        c->tune_g1_nb = tu->g1_nb;
+        c->tune_g2_nb = tu->g2_nb;
         c->router_cc_max_T = tu->router_cc_max_T;
         if (tu->g1_swap_rows) c->swap_rows_per_expert = tu->g1_swap_rows;
         if (tu->g2_swap_rows) c->swap2_rows_per_expert = tu->g2_swap_rows;
@@ -1478,8 +1510,8 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
               encode_map(&c->tm_h_tiled, c->h, 2, c->f_local, c->cap, 1, 128) &&
               encode_store_map(&c->tm_h_store, c->h, false, c->f_local, c->cap) &&
               encode_store_map(&c->tm_y_store, c->y, true, c->d, c->y_elems / c->d);
-    const uint32_t nbs[4] = {32, 64, 128, 256};
-    for (int i = 0; i < 4 && ok; ++i)
+    const uint32_t nbs[5] = {32, 64, 128, 256, 192};
+    for (int i = 0; i < 5 && ok; ++i)
         ok = encode_map(&c->tm_x_swap[i], c->x_perm, 2, c->d, c->cap, 1, nbs[i]) &&
              encode_map(&c->tm_h_swap[i], c->h, 2, c->f_local, c->cap, 1, nbs[i]);
     for (int i = 0; i < 3 && ok && c->fp8x; ++i)
@@ -1494,7 +1526,8 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
         (as = set_gemm_attr<kG1Swap, 32>(c)) || (as = set_gemm_attr<kG2Swap, 32>(c)) ||
         (as = set_gemm_attr<kG1Swap, 64>(c)) || (as = set_gemm_attr<kG2Swap, 64>(c)) ||
         (as = set_gemm_attr<kG1Swap, 128>(c)) || (as = set_gemm_attr<kG2Swap, 128>(c)) ||
-        (as = set_gemm_attr<kG2Swap, 256>(c)) ||
+        (as = set_gemm_attr<kG2Swap, 256>(c)) || (as = set_gemm_attr<kG1Swap, 192>(c)) ||
+        (as = set_gemm_attr<kG2Swap, 192>(c)) ||
         (as = set_pair_attr<kG1Pair, 1>(c)) || (as = set_pair_attr<kG2Pair, 1>(c)) ||
         (as = set_pair_attr<kG1Pair, 2>(c)) || (as = set_pair_attr<kG2Pair, 2>(c)) ||
         (as = set_fp8x_attr<32>(c)) || (as = set_fp8x_attr<64>(c)) || (as = set_fp8x_attr<128>(c)) ||
@@ -1527,6 +1560,7 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
             reinterpret_cast<const void*>(moe_gemm_kernel<kG1Swap, 64>), reinterpret_cast<const void*>(moe_gemm_kernel<kG2Swap, 64>),
             reinterpret_cast<const void*>(moe_gemm_kernel<kG1Swap, 128>), reinterpret_cast<const void*>(moe_gemm_kernel<kG2Swap, 128>),
             reinterpret_cast<const void*>(moe_gemm_kernel<kG2Swap, 256>), reinterpret_cast<const void*>(moe_gemm_pair_kernel<kG1Pair, 1>),
+            reinterpret_cast<const void*>(moe_gemm_kernel<kG1Swap, 192>), reinterpret_cast<const void*>(moe_gemm_kernel<kG2Swap, 192>),
             reinterpret_cast<const void*>(moe_gemm_pair_kernel<kG2Pair, 1>), reinterpret_cast<const void*>(moe_gemm_pair_kernel<kG1Pair, 2>),
             reinterpret_cast<const void*>(moe_gemm_pair_kernel<kG2Pair, 2>),
             reinterpret_cast<const void*>(moe_gemm_fp8x_kernel<kG1Swap, 32>),
@@ -1901,7 +1935,7 @@ moe_status forward_impl(moe_ctx* c, const void* tokens, int32_t T, const void* r
     c->spec_now = c->spec_now && s2 == MOE_OK;
     if ((s = s2)) return s;
     int splits = 1;
-    s = run_gemms(c, gpaths, T, (int64_t)T * c->k, &splits, st);
+    s = run_gemms(c, gpaths, T, (int64_t)T * c->k, (int64_t)T * c->k, &splits, st);
     c->spec_now = false;
     if (s) return s;
     if ((s = copy_aux(c, aux, T, st)) || (s = copy_aux_segments(c, aux, st))) return s;
@@ -2028,7 +2062,8 @@ moe_status forward_ep_p2p(moe_ctx* c, const void* tokens, int32_t T, const void*
     if ((s = copy_aux_segments(c, aux, st))) return s;
     const int64_t rows_expected = (int64_t)T * c->k;
     int splits = 1;
-    if ((s = run_gemms(c, gemm_paths(c, rows_expected), std::min<int64_t>(R, (int64_t)G * c->max_T), R, &splits, st)))
+    if ((s = run_gemms(c, gemm_paths(c, rows_expected), std::min<int64_t>(R, (int64_t)G * c->max_T), R, rows_expected,
+                       &splits, st)))
         return s;
     StepTimer t2(c, kSlotExchange, st);
     if ((s = launch(c, kSlotExchange, moe_ep_gather_kernel, dim3((unsigned)((c->d + 1023) / 1024 * R)), dim3(256), 0,
@@ -2118,7 +2153,8 @@ moe_status forward_ep(moe_ctx* c, const void* tokens, int32_t T, const void* rou
         for (int p = 0; p < G; ++p) rows_expected += c->h_counts[64 + p];
     }
     int splits = 1;
-    if ((s = run_gemms(c, gemm_paths(c, rows_expected), std::min<int64_t>(R, (int64_t)G * c->max_T), R, &splits, st)))
+    if ((s = run_gemms(c, gemm_paths(c, rows_expected), std::min<int64_t>(R, (int64_t)G * c->max_T), R, rows_expected,
+                       &splits, st)))
         return s;
     if ((s = launch(c, kSlotExchange, moe_ep_gather_kernel, dim3((unsigned)((c->d + 1023) / 1024 * R)), dim3(256), 0,
                     st, static_cast<const float*>(c->y), c->split_stride, splits,
