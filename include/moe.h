@@ -91,12 +91,12 @@ typedef enum {
 #define MOE_FLAG_NO_PAIR     0x10u /* prefill GEMMs on single CTAs (M=128) instead of CTA pairs (M=256) */
 #define MOE_FLAG_FP8_WEIGHTS 0x40u /* expert weights are FP8 E4M3 with per-row power-of-two scales
                                       (moe_pack_weights_fp8); decode (swap-AB) GEMMs at any T
-                                      (SURVEY 8(f) NEXT #2). hidden % 128 == 0 and ffn slice
-                                      % 128 == 0: the w1/w3 GEMM runs 8-bit MMAs on tokens split
-                                      into two E4M3 terms (hi + lo == the bf16 token exactly above
-                                      ~1e-3 of its row max) and stores h in fp16 scaled by the
-                                      token scale; otherwise tokens enter as fp16. The w2 GEMM
-                                      widens the weights to fp16 (R15)                  */
+                                      (SURVEY 8(f) NEXT #2); hidden % 128 == 0. Both GEMMs run
+                                      8-bit tensor-core MMAs: the w1/w3 GEMM on tokens split into
+                                      two E4M3 terms (hi + lo == the bf16 token exactly above
+                                      ~1e-3 of its row max), the w2 GEMM block-scaled
+                                      (kind::mxf8f6f4) on h stored as two E4M3 terms with one
+                                      UE8M0 scale per 32 ffn columns (R15)             */
 #define MOE_FLAG_EP_EXACT    0x20u /* EP: always exchange exact row counts (one host sync per forward);
                                       default: exact only when a fixed-capacity exchange would move
                                       more than 32 MB, i.e. prefill-sized batches                  */
@@ -128,13 +128,9 @@ typedef struct moe_tuning {
                                2 evict-normal, 3 evict-last                                  */
     int32_t host_stage;     /* moe_forward_host: 1 = always stage the output on the device and
                                copy it back (0: pinned output written directly)             */
-    int32_t fp8_fp16_tokens;/* FP8 weights: 1 = w1/w3 GEMM on fp16 tokens with converter warps
-                               instead of two E4M3 token terms on kind::f8f6f4 (0)          */
-    int32_t fp8_w2_split;   /* FP8 weights: 1 = w2 GEMM on three E4M3 terms of h
-                               (kind::f8f6f4) instead of fp16 h with converter warps (0)    */
     int32_t g1_nb;          /* force the swap-AB token tile of the w1/w3 GEMM: 32/64/128/192 (0: auto) */
     int32_t g2_nb;          /* same for the w2 GEMM, also 256 (0: auto)                        */
-    int32_t reserved[9];    /* must be zero                                                  */
+    int32_t reserved[11];   /* must be zero                                                  */
 } moe_tuning;
 
 typedef struct {
@@ -168,7 +164,9 @@ typedef struct {
  *        step of one tile is one contiguous 32 / 16 KB range:
  *        element (e, row, k) of w13 at ((((e*T13 + row/256)*(d/64) + k/64)*256
  *        + row%256)*64 + k%64, T13 = 2*f_local/256 (w2 alike with 128, f_local, T2).
- *   FP8 (moe_pack_weights_fp8) -- plain row-major [E_local][rows][K] bytes.
+ *   FP8 (moe_pack_weights_fp8) -- TILED the same way with 128-byte K chunks: w13 tiles of
+ *        256 rows, w2 tiles of 128 rows, each stored as K/128 consecutive [rows][128 B]
+ *        blocks (one E4M3 byte per weight).
  * (E_local = E/ep, f_local = f/tp: EP ep = G, TP tp = G, hybrid ep * tp = G.)   */
 typedef struct {
     const void* w13;

@@ -52,11 +52,12 @@ struct GemmParams {
     // blocks, so one K block of one tile is one contiguous chunk of HBM. w_nt: tiles
     // per expert. The weight maps are 4D {64, w_tr, K/64, w_nt * E}.
     int32_t w_tr, w_nt;
-    // FP8 w2 GEMM after the two-term (fp8x) w1/w3 GEMM (nullable): 2^-s of each permuted
-    // row. The fp8x epilogue stores h * 2^(2s - 6) in fp16 (keeps fp16 h in its normal
-    // range for any token scale: h grows ~quadratically with the token), so y is scaled
-    // back by 2^(6 - 2s) -- powers of two, exact.
-    const float* tok_scale;
+    // FP8 weights (block-scaled path): h leaves the w1/w3 GEMM as two E4M3 planes
+    // [2][plane_rows][f] (p.out) and their UE8M0 scales h_sf [2][plane_rows/128][f/128][512],
+    // one scale per (row, 32 consecutive ffn columns), each 512-byte group holding 128 rows
+    // x 4 K blocks in the block-scaled MMA's scale layout: byte 16*(r%32) + 4*((r%128)/32) + kb.
+    uint8_t* h_sf;
+    int64_t plane_rows;
     // kG1Swap speculative L2 prefetch (moe.cu spec_l2): K blocks of this CTA's first
     // weight tile to prefetch into L2 BEFORE the routing is known, assuming every
     // expert holds 1..NB rows (one token tile each: unit u = expert u / (f/128), weight
@@ -1024,319 +1025,60 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
 }
 
+
 // ============================================================================
-// FP8-weight decode GEMMs ("8-bit (fp8) floating point").
-// Expert weights are E4M3 with one power-of-two scale per output row; tokens and
-// activations are fp16. tcgen05 kind::f16 needs A and B of the same 16-bit type
-// (a bf16 x fp16 descriptor traps), so the weight tile is widened in shared memory:
-//   TMA (fp8 box, 64-byte swizzle) -> converter warps (cvt.rn.f16x2.e4m3x2, exact)
-//   -> fp16 tile in the 128-byte-swizzled K-major layout -> tcgen05.mma (fp32 acc)
-// and the epilogue multiplies by the row scale (a power of two: exact). HBM sees one
-// byte per weight, so the weight stream -- the decode roofline -- halves.
-// Two rings: the load ring (fp8 A + fp16 B, deep, keeps HBM busy) and the fp16 ring
-// (shallow). Warps: 0 TMA, 1 MMA + TMEM, 2..5 epilogue, 6..9 converters.
-constexpr int kFp8Threads = 320;
-
-template <int KIND, int NB>
-struct Fp8Cfg {
-    static_assert(KIND == kG1Swap || KIND == kG2Swap, "fp8 weights: decode (swap-AB) GEMMs only");
-    static constexpr int kARows = KIND == kG1Swap ? 256 : 128;
-    static constexpr int kA8Bytes = kARows * 64;    // fp8 rows x 64 B (one 64-element K block)
-    static constexpr int kA16Bytes = kARows * 128;  // fp16 rows x 128 B
-    static constexpr int kBBytes = NB * 128;        // fp16 tokens
-    static constexpr int kS2 = KIND == kG1Swap ? 2 : 3;
-    static constexpr int kLoadBytes = kA8Bytes + kBBytes;
-    static constexpr int kS1Raw = (kSmemBudget - 2048 - kS2 * kA16Bytes) / kLoadBytes;
-    static constexpr int kS1 = kS1Raw > 8 ? 8 : kS1Raw;
-    static constexpr int kSmemBytes = kS1 * kLoadBytes + kS2 * kA16Bytes + 2048;
-    static_assert(kS1 >= 3, "fp8 load ring too shallow");
-};
-
-__device__ __forceinline__ uint32_t cvt_e4m3x2_f16x2(uint32_t two_fp8) {
-    uint32_t r;
-    const uint16_t v = static_cast<uint16_t>(two_fp8);
-    asm("cvt.rn.f16x2.e4m3x2 %0, %1;" : "=r"(r) : "h"(v));
-    return r;
-}
-
-// 4 E4M3 bytes -> 4 fp16 equal to (e4m3 value) * 2^-8, EXACTLY, with integer ops only:
-// fp16 = sign << 15 | (e4m3 & 0x7F) << 7. E4M3 (bias 7) and fp16 (bias 15) differ by
-// 8 in the exponent bias, and E4M3 subnormals land on fp16 subnormals, so the bit
-// move is an exact scaling by 2^-8 for every finite code (the row scale absorbs 2^8).
-// Integer-ALU alternative to cvt.rn.f16x2.e4m3x2 (MOE_FP8_CVT_INSN=0); measured slower.
-__device__ __forceinline__ void e4m3x4_to_f16x4_scaled(uint32_t w, uint32_t& lo, uint32_t& hi) {
-    const uint32_t t0 = __byte_perm(w, 0u, 0x1404);  // b1 << 24 | b0 << 8
-    const uint32_t t1 = __byte_perm(w, 0u, 0x3424);  // b3 << 24 | b2 << 8
-    lo = (t0 & 0x80008000u) | ((t0 >> 1) & 0x3F803F80u);
-    hi = (t1 & 0x80008000u) | ((t1 >> 1) & 0x3F803F80u);
-}
-
-__device__ __forceinline__ uint32_t pack_f16x2(float lo, float hi) {
-    __half2 v = __floats2half2_rn(lo, hi);
-    return *reinterpret_cast<uint32_t*>(&v);
-}
-
-// scales: kG1Swap -> per packed w13 row [E][2f]; kG2Swap -> per w2 row [E][d]
-template <int KIND, int NB>
-__global__ void __launch_bounds__(kFp8Threads, 1)
-    moe_gemm_fp8_kernel(const GemmParams p, const float* __restrict__ scales,
-                        const __grid_constant__ CUtensorMap tmA8, const __grid_constant__ CUtensorMap tmB) {
-    using C = Fp8Cfg<KIND, NB>;
-    constexpr int S1 = C::kS1, S2 = C::kS2;
-    extern __shared__ __align__(1024) uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint8_t* ring16 = smem;                              // S2 x fp16 A tiles (1024-aligned)
-    uint8_t* ring_b = ring16 + S2 * C::kA16Bytes;        // S1 x fp16 B tiles (1024-aligned: NB*128)
-    uint8_t* ring8 = ring_b + S1 * C::kBBytes;           // S1 x fp8 A tiles (512-aligned)
-    uint64_t* bars = reinterpret_cast<uint64_t*>(ring8 + S1 * C::kA8Bytes);
-    uint64_t* full1 = bars;                 // TMA -> converters (fp8 A + B bytes)
-    uint64_t* empty1 = bars + S1;           // converters (4) + MMA commit (1) -> TMA
-    uint64_t* full2 = bars + 2 * S1;        // converters (4 warps) -> MMA
-    uint64_t* empty2 = full2 + S2;          // MMA commit -> converters
-    uint64_t* tmem_full = empty2 + S2;
-    uint64_t* tmem_empty = tmem_full + 2;
-    uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
-    int32_t* s_counts = reinterpret_cast<int32_t*>(tmem_empty + 3);
-    int32_t* s_offsets = s_counts + 32;
-
-    const int warp = threadIdx.x / 32;
-    const int lane = threadIdx.x % 32;
-    if (warp == 0 && lane == 0) {
-        ptx::prefetch_tmap(&tmA8);
-        ptx::prefetch_tmap(&tmB);
-        for (int i = 0; i < S1; ++i) {
-            ptx::mbar_init(&full1[i], 1);
-            ptx::mbar_init(&empty1[i], 5);
-        }
-        for (int i = 0; i < S2; ++i) {
-            ptx::mbar_init(&full2[i], 4);
-            ptx::mbar_init(&empty2[i], 1);
-        }
-        for (int i = 0; i < 2; ++i) {
-            ptx::mbar_init(&tmem_full[i], 1);
-            ptx::mbar_init(&tmem_empty[i], 4);
-        }
-        ptx::fence_mbar_init();
-    }
-    if (warp == 1) {
-        ptx::tmem_alloc(tmem_base_slot, 512);
-        ptx::tmem_relinquish();
-    }
-    ptx::pdl_wait();
-    if (threadIdx.x < 32)
-        for (int e = threadIdx.x; e < p.E; e += 32) {
-            s_counts[e] = p.counts[e];
-            s_offsets[e] = p.offsets[e];
-        }
-    ptx::tc_fence_before();
-    __syncthreads();
-    ptx::tc_fence_after();
-    const uint32_t tmem_base = *tmem_base_slot;
-    int total = 0;
-    for (int e = 0; e < p.E; ++e) total += tiles_of<KIND, NB>(s_counts[e], p);
-
-    if (warp == 0) {
-        // ---------------------------------------------------------------- TMA producer
-        if (lane == 0) {
-            int st = 0;
-            uint32_t ph = 0;
-            for (int t = blockIdx.x; t < total; t += gridDim.x) {
-                TileInfo ti;
-                decode_tile<KIND, NB>(t, p, s_counts, s_offsets, ti);
-                for (int kb = 0; kb < ti.nkb; ++kb) {
-                    ptx::mbar_wait(&empty1[st], ph ^ 1);
-                    ptx::mbar_arrive_expect_tx(&full1[st], C::kLoadBytes);
-                    const int kc = (ti.kb0 + kb) * kBK;
-                    ptx::tma_load_3d(&tmA8, &full1[st], ring8 + st * C::kA8Bytes, kc, ti.a_row, ti.e,
-                                     ptx::kEvictFirst);
-                    ptx::tma_load_2d(&tmB, &full1[st], ring_b + st * C::kBBytes, kc, ti.b_row, ptx::kEvictLast);
-                    if (++st == S1) { st = 0; ph ^= 1; }
-                }
-            }
-        }
-    } else if (warp == 1) {
-        // ---------------------------------------------------------------- MMA issuer
-        if (lane == 0) {
-            int s1 = 0, s2 = 0;
-            uint32_t ph1 = 0, ph2 = 0;
-            int acc = 0;
-            uint32_t acc_phase = 0;
-            for (int t = blockIdx.x; t < total; t += gridDim.x) {
-                TileInfo ti;
-                decode_tile<KIND, NB>(t, p, s_counts, s_offsets, ti);
-                const uint32_t n_mma = (uint32_t)((ti.n_valid + 15) / 16 * 16);
-                const uint32_t idesc = (1u << 4) | ((n_mma >> 3) << 17) | ((128u >> 4) << 24);  // f16 x f16 -> f32
-                const uint32_t d_tmem = tmem_base + acc * 256;
-                ptx::mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
-                ptx::tc_fence_after();
-                for (int kb = 0; kb < ti.nkb; ++kb) {
-                    ptx::mbar_wait(&full2[s2], ph2);
-                    ptx::tc_fence_after();
-                    const uint32_t sa = ptx::smem_u32(ring16 + s2 * C::kA16Bytes);
-                    const uint64_t adesc = ptx::make_smem_desc_sw128(sa);
-                    const uint64_t bdesc = ptx::make_smem_desc_sw128(ptx::smem_u32(ring_b + s1 * C::kBBytes));
-#pragma unroll
-                    for (int kk = 0; kk < kBK / 16; ++kk) {
-                        const uint32_t accum = (kb | kk) ? 1u : 0u;
-                        ptx::mma_bf16(d_tmem, adesc + 2 * kk, bdesc + 2 * kk, idesc, accum);
-                        if (KIND == kG1Swap) {
-                            const uint64_t adesc3 = ptx::make_smem_desc_sw128(sa + 128 * 128);
-                            ptx::mma_bf16(d_tmem + 128, adesc3 + 2 * kk, bdesc + 2 * kk, idesc, accum);
-                        }
-                    }
-                    ptx::mma_commit(&empty2[s2]);
-                    ptx::mma_commit(&empty1[s1]);
-                    if (++s2 == S2) { s2 = 0; ph2 ^= 1; }
-                    if (++s1 == S1) { s1 = 0; ph1 ^= 1; }
-                }
-                ptx::mma_commit(&tmem_full[acc]);
-                if (++acc == 2) { acc = 0; acc_phase ^= 1; }
-            }
-        }
-    } else if (warp >= 6) {
-        // ---------------------------------------------------------------- converters (warps 6..9)
-        // thread c owns A rows c (and c + 128 for the 256-row w1|w3 tile)
-        const int c = threadIdx.x - 6 * 32;
-        int s1 = 0, s2 = 0;
-        uint32_t ph1 = 0, ph2 = 0;
-        for (int t = blockIdx.x; t < total; t += gridDim.x) {
-            TileInfo ti;
-            decode_tile<KIND, NB>(t, p, s_counts, s_offsets, ti);
-            for (int kb = 0; kb < ti.nkb; ++kb) {
-                ptx::mbar_wait(&full1[s1], ph1);
-                ptx::mbar_wait(&empty2[s2], ph2 ^ 1);
-                const uint8_t* src = ring8 + s1 * C::kA8Bytes;
-                uint8_t* dst = ring16 + s2 * C::kA16Bytes;
-#pragma unroll
-                for (int h = 0; h < C::kARows / 128; ++h) {
-                    const int r = c + h * 128;
-                    const uint4* srow = reinterpret_cast<const uint4*>(src + r * 64);
-                    uint4* drow = reinterpret_cast<uint4*>(dst + r * 128);
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) {            // 16 fp8 of logical chunk q
-                        const uint4 v = srow[q ^ ((r >> 1) & 3)];  // 64-byte swizzle
-                        uint4 lo, hi;
-                        lo.x = cvt_e4m3x2_f16x2(v.x);       lo.y = cvt_e4m3x2_f16x2(v.x >> 16);
-                        lo.z = cvt_e4m3x2_f16x2(v.y);       lo.w = cvt_e4m3x2_f16x2(v.y >> 16);
-                        hi.x = cvt_e4m3x2_f16x2(v.z);       hi.y = cvt_e4m3x2_f16x2(v.z >> 16);
-                        hi.z = cvt_e4m3x2_f16x2(v.w);       hi.w = cvt_e4m3x2_f16x2(v.w >> 16);
-                        drow[(2 * q) ^ (r & 7)] = lo;       // 128-byte swizzle (UMMA SW128 K-major)
-                        drow[(2 * q + 1) ^ (r & 7)] = hi;
-                    }
-                }
-                ptx::fence_proxy_async();  // generic-proxy smem writes -> visible to tcgen05.mma
-                __syncwarp();
-                if (lane == 0) {
-                    ptx::mbar_arrive(&full2[s2]);
-                    ptx::mbar_arrive(&empty1[s1]);  // fp8 bytes consumed (B still owned by the MMA)
-                }
-                if (++s2 == S2) { s2 = 0; ph2 ^= 1; }
-                if (++s1 == S1) { s1 = 0; ph1 ^= 1; }
-            }
-        }
-    } else {
-        // ---------------------------------------------------------------- epilogue (warps 2..5)
-        const int q = warp & 3;
-        const int r = q * 32 + lane;
-        int acc = 0;
-        uint32_t acc_phase = 0;
-        for (int t = blockIdx.x; t < total; t += gridDim.x) {
-            TileInfo ti;
-            decode_tile<KIND, NB>(t, p, s_counts, s_offsets, ti);
-            ptx::mbar_wait(&tmem_full[acc], acc_phase);
-            ptx::tc_fence_after();
-            const uint32_t tbase = tmem_base + acc * 256 + (static_cast<uint32_t>(q * 32) << 16);
-            const int nchunks = (ti.n_valid + 15) / 16;
-            if (KIND == kG1Swap) {
-                // row r: ffn index m*128 + r; w1 scale at packed row 256m + r, w3 at 256m + 128 + r
-                const float* sc = scales + (int64_t)ti.e * 2 * p.f + ti.m_idx * 256;
-                const float s1v = sc[r], s3v = sc[128 + r];
-                __half* hp = static_cast<__half*>(p.out) + static_cast<int64_t>(ti.b_row) * p.f + ti.m_idx * 128 + r;
-#pragma unroll 1
-                for (int cc = 0; cc < nchunks; ++cc) {
-                    uint32_t a[16], b[16];
-                    ptx::tmem_ld16(tbase + cc * 16, a);
-                    ptx::tmem_ld16(tbase + 128 + cc * 16, b);
-                    ptx::tmem_wait_ld();
-#pragma unroll
-                    for (int i = 0; i < 16; ++i) {
-                        const int n = cc * 16 + i;
-                        if (n < ti.n_valid) {
-                            const float hv = silu_f32(__uint_as_float(a[i]) * s1v) * (__uint_as_float(b[i]) * s3v);
-                            hp[static_cast<int64_t>(n) * p.f] = __float2half_rn(hv);
-                        }
-                    }
-                }
-            } else {
-                const int drow = ti.m_idx * 128 + r;
-                const float s2v = drow < p.d ? scales[(int64_t)ti.e * p.d + drow] : 0.f;
-                float* y = static_cast<float*>(p.out) + p.out_split_stride * ti.split +
-                           static_cast<int64_t>(ti.b_row) * p.d + drow;
-#pragma unroll 1
-                for (int cc = 0; cc < nchunks; ++cc) {
-                    uint32_t v[16];
-                    ptx::tmem_ld16(tbase + cc * 16, v);
-                    ptx::tmem_wait_ld();
-                    if (drow < p.d) {
-#pragma unroll
-                        for (int i = 0; i < 16; ++i) {
-                            const int n = cc * 16 + i;
-                            if (n < ti.n_valid) {
-                                float u = s2v;
-                                if (p.tok_scale) {
-                                    const float tsn = p.tok_scale[ti.b_row + n];
-                                    u *= tsn * tsn * 64.f;
-                                }
-                                y[static_cast<int64_t>(n) * p.d] = __uint_as_float(v[i]) * u;
-                            }
-                        }
-                    }
-                }
-            }
-            ptx::tc_fence_before();
-            __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(&tmem_empty[acc]);
-            if (++acc == 2) { acc = 0; acc_phase ^= 1; }
-        }
-    }
-    ptx::pdl_launch_dependents();
-    ptx::tc_fence_before();
-    __syncthreads();
-    if (warp == 1) {
-        ptx::tc_fence_after();
-        ptx::tmem_dealloc(tmem_base, 512);
-    }
-}
-
-// ----------------------------------------------------------------------------
-// FP8-weight decode w1/w3 GEMM on the 8-bit tensor core path (tcgen05 kind::f8f6f4),
-// no weight conversion. The tokens are split into two E4M3 terms by the permute kernel
-// (hi + lo = x * 2^s, exact for bf16 x above ~1e-3 of the row max: permute_row_fp8x),
-// so each K step runs two MMAs, D += W * hi^T and D += W * lo^T, with both operands
-// straight from TMA-staged shared memory. The epilogue applies the weight row scale
-// (power of two) and the token scale 2^-s, then SwiGLU, and stores fp16 h for the
-// FP8 w2 GEMM. Why: the converter pipeline of moe_gemm_fp8t_kernel (e4m3 -> fp16 in
-// TMEM, ~16 cvt results / clk / SM) capped K3 at ~5 TB/s (ncu r01: converter warps
-// waiting on TMEM A stages; 79 % of the HBM roofline at 1 B/weight).
+// FP8-weight decode GEMMs ("8-bit (fp8) floating point"),
+// both on the 8-bit tensor-core path with no weight conversion. Weights: E4M3 with one
+// power-of-two scale per output row (R15), TILED like the bf16 weights (each
+// 256-row w13 / 128-row w2 tile stored as K/128 contiguous [rows][128 B] chunks: one TMA
+// box = one contiguous 32 / 16 KB range of HBM).
+//   kG1Swap (w1/w3 + SwiGLU): B = the tokens as two E4M3 terms hi + lo = x 2^s (exact
+//     for bf16 x above ~1e-3 of its row max; permute_row_fp8x), two kind::f8f6f4 MMAs per
+//     32-byte K step into the a (w1) and b (w3) accumulators; the epilogue applies the
+//     weight row scales and 2^-s, SwiGLU, and writes h for the w2 GEMM as two E4M3 terms
+//     with a UE8M0 scale per 32 ffn columns of each row -- the 32 lanes of one epilogue
+//     warp hold exactly those 32 columns, so the block max is one warp reduction:
+//       u = the power of two putting the block max in (224, 448],
+//       hi = e4m3(h 2^u)  (scale 2^-u),  lo = e4m3((h 2^u - hi) 16)  (scale 2^-(u+4)),
+//     |h - hi 2^-u - lo 2^-(u+4)| <= 2^-8 |h| (plus 2^-10 2^-u below the E4M3 normal range).
+//   kG2Swap (w2): A = W2 tile, B = hi and lo planes, block-scaled MMAs
+//     (kind::mxf8f6f4.block_scale): the scales of B ride in TMEM (tcgen05.cp per stage),
+//     those of A are all 1 (the weight row scale is applied in the epilogue). No h split
+//     kernel, no per-row factor.
 // Warps: 0 = TMA producer, 1 = TMEM + MMA issuer, 2..5 = epilogue.
 template <int KIND, int NB>
 struct Fp8xCfg {
-    static_assert(NB >= 16 && NB <= 128 && NB % 16 == 0, "token tile");
+    static_assert(NB >= 32 && NB <= 128 && NB % 32 == 0, "token tile");
     static_assert(KIND == kG1Swap || KIND == kG2Swap, "decode kinds");
+    static constexpr bool kMX = KIND == kG2Swap;
     // w1|w3 rows (G1) or W2 rows (G2) x 128 E4M3 (one 128-byte swizzle row)
-    static constexpr int kABytes = (KIND == kG1Swap ? 256 : 128) * 128;
-    static constexpr int kTerms = KIND == kG1Swap ? 2 : 3;  // E4M3 terms of the B operand rows
+    static constexpr int kARows = KIND == kG1Swap ? 256 : 128;
+    static constexpr int kABytes = kARows * 128;
+    static constexpr int kTerms = 2;            // E4M3 terms of the B operand rows
     static constexpr int kBBytes = NB * 128;    // B rows x 128 E4M3, per term
-    static constexpr int kStageBytes = kABytes + kTerms * kBBytes;
-    static constexpr int kStagesRaw = (kSmemBudget - 2048) / kStageBytes;
+    static constexpr int kSFBytes = kMX ? 1024 : 0;  // two 512-byte scale groups (hi, lo)
+    static constexpr int kStageBytes = kABytes + kTerms * kBBytes + kSFBytes;
+    static constexpr int kStagesRaw = (kSmemBudget - 2048 - 1024) / kStageBytes;
     static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
-    static constexpr int kSmemBytes = kStages * kStageBytes + 2048;
+    static constexpr int kSmemBytes = kStages * kStageBytes + 2048 + 1024;  // + barriers + the A scale atom
     static_assert(kStages >= 3, "pipeline too shallow");
+    // TMEM columns: two accumulator stages of 256, then the scale columns (MX)
+    static constexpr uint32_t kSfaCol = 496, kSfbCol = 500;  // SFA 4 columns, SFB hi / lo 4 each
 };
 
-// KIND = kG1Swap: w1/w3 + SwiGLU, B = two-term tokens, row_scale = token scales 2^-t.
-// KIND = kG2Swap: w2 (split-K), B = two-term h (moe_h_split_kernel), row_scale = the
-// per-row factor that undoes both the h split scale and the h normalisation.
+__device__ __forceinline__ uint8_t f32_to_e4m3(float v) {
+    uint16_t r;
+    asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(r) : "f"(0.0f), "f"(v));
+    return static_cast<uint8_t>(r & 0xFF);
+}
+__device__ __forceinline__ float e4m3_to_f32(uint8_t v) {
+    uint32_t h;
+    asm("cvt.rn.f16x2.e4m3x2 %0, %1;" : "=r"(h) : "h"(static_cast<uint16_t>(v)));
+    return __half2float(__ushort_as_half(static_cast<unsigned short>(h & 0xFFFF)));
+}
+
+// KIND = kG1Swap: w1/w3 + SwiGLU, B = two-term tokens, row_scale = token scales 2^-s.
+// KIND = kG2Swap: w2 (split-K), B = two-term h with block scales (row_scale unused).
 template <int KIND, int NB>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     moe_gemm_fp8x_kernel(const GemmParams p, const float* __restrict__ scales, const float* __restrict__ row_scale,
@@ -1349,7 +1091,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* smem_a = smem;                  // stage s at s * kABytes
     uint8_t* smem_b = smem + S * C::kABytes; // stage s: term j at (s * kTerms + j) * kBBytes
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * C::kStageBytes);
+    uint8_t* smem_sf = smem_b + S * C::kTerms * C::kBBytes;  // stage s: hi / lo scale groups (MX)
+    uint8_t* smem_sfa = smem_sf + S * C::kSFBytes;           // 512-byte A scale atom (all 1.0), MX
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_sfa + (C::kMX ? 512 : 0));
     uint64_t* full = bars;
     uint64_t* empty = bars + S;
     uint64_t* tmem_full = bars + 2 * S;
@@ -1360,6 +1104,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
     const int warp = threadIdx.x / 32;
     const int lane = threadIdx.x % 32;
+    const int k_chunks = (kG1 ? p.d : p.f) / KB;  // 128-byte K chunks per weight tile row
+    const int w_tiles = kG1 ? (2 * p.f) / 256 : p.d / 128;  // weight tiles per expert
     if (warp == 0 && lane == 0) {
         ptx::prefetch_tmap(&tmA8);
         ptx::prefetch_tmap(&tmB8);
@@ -1376,11 +1122,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     if (warp == 1) {
         ptx::tmem_alloc(tmem_base_slot, 512);
         ptx::tmem_relinquish();
+        if (C::kMX) {  // A scales: UE8M0 127 = 2^0 for every row and K block
+            reinterpret_cast<uint4*>(smem_sfa)[lane] = make_uint4(0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu);
+            ptx::fence_proxy_async();  // generic-proxy stores visible to tcgen05.cp
+        }
     }
     // counts / offsets come from the router, complete before this grid launches (the
     // permute kernel triggers its dependents after its own griddepcontrol.wait). The
     // producer issues the first tile's weight stages before anything waits on the
-    // permute (PDL); its token loads and every other warp wait for it.
+    // previous kernel (PDL); its token loads and every other warp wait for it.
     if (threadIdx.x < 32)
         for (int e = threadIdx.x; e < p.E; e += 32) {
             s_counts[e] = p.counts[e];
@@ -1392,14 +1142,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         int total0 = 0;  // warp 0 wrote s_counts itself
         for (int e = 0; e < p.E; ++e) total0 += tiles_of<KIND, NB>(s_counts[e], p);
         if ((int)blockIdx.x < total0) {
-        TileInfo t0;
-        decode_tile<KIND, NB, KB>(blockIdx.x, p, s_counts, s_offsets, t0);
-        pre = min(S, t0.nkb);
-        for (int kb = 0; kb < pre; ++kb) {  // fresh stages: no empty-wait
-            ptx::mbar_arrive_expect_tx(&full[kb], C::kStageBytes);
-            ptx::tma_load_3d(&tmA8, &full[kb], smem_a + kb * C::kABytes, (t0.kb0 + kb) * KB, t0.a_row, t0.e,
-                             ptx::kEvictFirst);
-        }
+            TileInfo t0;
+            decode_tile<KIND, NB, KB>(blockIdx.x, p, s_counts, s_offsets, t0);
+            pre = min(S, t0.nkb);
+            const int wt = t0.a_row / C::kARows + t0.e * w_tiles;
+            for (int kb = 0; kb < pre; ++kb) {  // fresh stages: no empty-wait
+                ptx::mbar_arrive_expect_tx(&full[kb], C::kStageBytes);
+                ptx::tma_load_4d(&tmA8, &full[kb], smem_a + kb * C::kABytes, 0, 0, t0.kb0 + kb, wt, ptx::kEvictFirst);
+            }
         }
     }
     ptx::tc_fence_before();
@@ -1415,23 +1165,31 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             int st = 0;
             uint32_t ph = 0;
             bool first = true;
+            const int64_t sf_terms = (p.plane_rows / 128) * (p.f / 128) * 512;  // bytes per scale plane
             for (int t = blockIdx.x; t < total; t += gridDim.x) {
                 TileInfo ti;
                 decode_tile<KIND, NB, KB>(t, p, s_counts, s_offsets, ti);
+                const int wt = ti.a_row / C::kARows + ti.e * w_tiles;
                 for (int kb = 0; kb < ti.nkb; ++kb) {
                     const int kc = (ti.kb0 + kb) * KB;
                     if (!(first && kb < pre)) {
                         ptx::mbar_wait(&empty[st], ph ^ 1);
                         ptx::mbar_arrive_expect_tx(&full[st], C::kStageBytes);
-                        ptx::tma_load_3d(&tmA8, &full[st], smem_a + st * C::kABytes, kc, ti.a_row, ti.e,
+                        ptx::tma_load_4d(&tmA8, &full[st], smem_a + st * C::kABytes, 0, 0, ti.kb0 + kb, wt,
                                          ptx::kEvictFirst);
                     }
                     uint8_t* b = smem_b + st * C::kTerms * C::kBBytes;
 #pragma unroll
                     for (int j = 0; j < C::kTerms; ++j)
                         ptx::tma_load_3d(&tmB8, &full[st], b + j * C::kBBytes, kc, ti.b_row, j, ptx::kEvictLast);
+                    if (C::kMX) {  // the 128-row scale groups of both terms at this K chunk
+                        const uint8_t* g = p.h_sf + ((int64_t)(ti.b_row / 128) * (p.f / 128) + kc / 128) * 512;
+                        ptx::bulk_load(smem_sf + st * C::kSFBytes, g, 512, &full[st]);
+                        ptx::bulk_load(smem_sf + st * C::kSFBytes + 512, g + sf_terms, 512, &full[st]);
+                    }
                     if (++st == S) { st = 0; ph ^= 1; }
                 }
+                (void)k_chunks;
                 first = false;
             }
         }
@@ -1441,13 +1199,19 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             uint32_t ph = 0;
             int acc = 0;
             uint32_t acc_phase = 0;
+            const uint32_t sfa = tmem_base + C::kSfaCol;
+            if (C::kMX) ptx::tmem_cp_32x128b_x4(sfa, ptx::make_smem_desc_rows16(ptx::smem_u32(smem_sfa)));
             for (int t = blockIdx.x; t < total; t += gridDim.x) {
                 TileInfo ti;
                 decode_tile<KIND, NB, KB>(t, p, s_counts, s_offsets, ti);
-                const uint32_t n_mma = (uint32_t)((ti.n_valid + 15) / 16 * 16);
+                // MX: N a multiple of 32 (the block-scale layout covers B rows in groups of 32)
+                const uint32_t n_mma = C::kMX ? (uint32_t)((ti.n_valid + 31) / 32 * 32)
+                                              : (uint32_t)((ti.n_valid + 15) / 16 * 16);
                 // D f32 (bit 4), A = B = E4M3 (format 0), K-major, N >> 3 at 17, M >> 4 at 24
                 const uint32_t idesc = (1u << 4) | ((n_mma >> 3) << 17) | ((128u >> 4) << 24);
                 const uint32_t d_a = tmem_base + acc * 256, d_b = d_a + 128;
+                // B scale columns of this token tile: 32-row group (b_row % 128) / 32 of the atom
+                const uint32_t sfb_grp = (uint32_t)((ti.b_row % 128) / 32);
                 ptx::mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
                 ptx::tc_fence_after();
                 for (int kb = 0; kb < ti.nkb; ++kb) {
@@ -1455,14 +1219,27 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                     ptx::tc_fence_after();
                     const uint64_t a1 = ptx::make_smem_desc_sw128(ptx::smem_u32(smem_a + st * C::kABytes));
                     const uint64_t b0 = ptx::make_smem_desc_sw128(ptx::smem_u32(smem_b + st * C::kTerms * C::kBBytes));
+                    if (C::kMX) {  // this stage's scale groups -> TMEM (ordered before the MMAs below)
+                        const uint32_t sfs = ptx::smem_u32(smem_sf + st * C::kSFBytes);
+                        ptx::tmem_cp_32x128b_x4(tmem_base + C::kSfbCol, ptx::make_smem_desc_rows16(sfs));
+                        ptx::tmem_cp_32x128b_x4(tmem_base + C::kSfbCol + 4, ptx::make_smem_desc_rows16(sfs + 512));
+                    }
 #pragma unroll
                     for (int kk = 0; kk < KB / 32; ++kk) {  // 32 bytes of K per MMA: +2 in the descriptor
                         const uint32_t init = (kb | kk) ? 1u : 0u;
 #pragma unroll
                         for (int j = 0; j < C::kTerms; ++j) {  // term j: kBBytes further (>> 4 in the descriptor)
                             const uint64_t bj = b0 + j * (C::kBBytes >> 4) + 2 * kk;
-                            ptx::mma_e4m3(d_a, a1 + 2 * kk, bj, idesc, j ? 1u : init);
-                            if (kG1) ptx::mma_e4m3(d_b, a1 + (16384 >> 4) + 2 * kk, bj, idesc, j ? 1u : init);
+                            if (C::kMX) {
+                                // K block kk of the 128-K chunk = byte kk of the scale columns
+                                const uint32_t sel = static_cast<uint32_t>(kk) << 30;
+                                const uint32_t sfb = (tmem_base + C::kSfbCol + 4 * j + sfb_grp) | sel;
+                                ptx::mma_mx_e4m3(d_a, a1 + 2 * kk, bj, ptx::make_idesc_mx_e4m3(128, n_mma, kk, kk),
+                                                 j ? 1u : init, sfa | sel, sfb);
+                            } else {
+                                ptx::mma_e4m3(d_a, a1 + 2 * kk, bj, idesc, j ? 1u : init);
+                                if (kG1) ptx::mma_e4m3(d_b, a1 + (16384 >> 4) + 2 * kk, bj, idesc, j ? 1u : init);
+                            }
                         }
                     }
                     ptx::mma_commit(&empty[st]);
@@ -1484,27 +1261,48 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             ptx::mbar_wait(&tmem_full[acc], acc_phase);
             ptx::tc_fence_after();
             const uint32_t tbase = tmem_base + acc * 256 + (static_cast<uint32_t>(q * 32) << 16);
-            const float* rs = row_scale + ti.b_row;
             const int nchunks = (ti.n_valid + 15) / 16;
             if (kG1) {
+                const float* rs = row_scale + ti.b_row;
                 const float* sc = scales + (int64_t)ti.e * 2 * p.f + ti.m_idx * 256;
                 const float s1v = sc[r], s3v = sc[128 + r];
-                __half* hp = static_cast<__half*>(p.out) + static_cast<int64_t>(ti.b_row) * p.f + ti.m_idx * 128 + r;
+                const int64_t plane = p.plane_rows * p.f;
+                uint8_t* hp = static_cast<uint8_t*>(p.out) + static_cast<int64_t>(ti.b_row) * p.f + ti.m_idx * 128 + r;
+                const int64_t sf_plane = (p.plane_rows / 128) * (p.f / 128) * 512;
 #pragma unroll 1
                 for (int cc = 0; cc < nchunks; ++cc) {
                     uint32_t a[16], b[16];
                     ptx::tmem_ld16(tbase + cc * 16, a);
                     ptx::tmem_ld16(tbase + 128 + cc * 16, b);
                     ptx::tmem_wait_ld();
-#pragma unroll
+#pragma unroll 4
                     for (int i = 0; i < 16; ++i) {
                         const int n = cc * 16 + i;
-                        if (n < ti.n_valid) {
+                        if (n < ti.n_valid) {  // warp-uniform
                             const float tsn = rs[n];
                             const float hv = silu_f32(__uint_as_float(a[i]) * (s1v * tsn)) *
                                              (__uint_as_float(b[i]) * (s3v * tsn));
-                            // fp16 h normalised by the token scale: h * 2^(2s - 6) (see GemmParams)
-                            hp[static_cast<int64_t>(n) * p.f] = __float2half_rn(hv * (0.015625f / (tsn * tsn)));
+                            // block max of |h| over the warp's 32 ffn columns (bits order == magnitude order)
+                            const uint32_t mbits = __reduce_max_sync(0xffffffffu, __float_as_uint(hv) & 0x7FFFFFFFu);
+                            const float m = __uint_as_float(mbits);
+                            int u = 0;
+                            if (m > 0.f) {  // 448 / m = 2^e * 1.xx -> u = e: m 2^u in (224, 448]
+                                const float ratio = 448.f / m;
+                                u = isinf(ratio) ? 120 : ((__float_as_int(ratio) >> 23) & 0xFF) - 127;
+                                u = max(-120, min(120, u));
+                            }
+                            const float v = hv * __int_as_float((u + 127) << 23);  // exact: a power of two
+                            const uint8_t hi = f32_to_e4m3(v);
+                            const uint8_t lo = f32_to_e4m3((v - e4m3_to_f32(hi)) * 16.f);  // residual exact in fp32
+                            hp[static_cast<int64_t>(n) * p.f] = hi;
+                            hp[static_cast<int64_t>(n) * p.f + plane] = lo;
+                            if (lane == 0) {
+                                const int64_t row = ti.b_row + n;
+                                const int64_t o = ((row / 128) * (p.f / 128) + ti.m_idx) * 512 + 16 * (row % 32) +
+                                                  4 * ((row % 128) / 32) + q;
+                                p.h_sf[o] = static_cast<uint8_t>(127 - u);           // hi: 2^-u
+                                p.h_sf[o + sf_plane] = static_cast<uint8_t>(123 - u); // lo: 2^-(u+4)
+                            }
                         }
                     }
                 }
@@ -1522,7 +1320,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
                         for (int i = 0; i < 16; ++i) {
                             const int n = cc * 16 + i;
-                            if (n < ti.n_valid) y[static_cast<int64_t>(n) * p.d] = __uint_as_float(v[i]) * (s2v * rs[n]);
+                            if (n < ti.n_valid) y[static_cast<int64_t>(n) * p.d] = __uint_as_float(v[i]) * s2v;
                         }
                     }
                 }
@@ -1531,314 +1329,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(&tmem_empty[acc]);
             if (++acc == 2) { acc = 0; acc_phase ^= 1; }
-        }
-    }
-    ptx::pdl_launch_dependents();
-    ptx::tc_fence_before();
-    __syncthreads();
-    if (warp == 1) {
-        ptx::tc_fence_after();
-        ptx::tmem_dealloc(tmem_base, 512);
-    }
-}
-
-// ----------------------------------------------------------------------------
-// FP8-weight decode GEMM, A widened straight into TENSOR memory (NB <= 64). The
-// smem-staged variant above needs ~180 B/cycle/SM of shared-memory traffic at the
-// HBM rate (fp8 in, fp16 out, fp16 read by the MMA, plus the token tile) -- over
-// the ~128 B/cycle an SM has, so it runs at ~60 % of the fp8 roofline. Here the
-// converter warps tcgen05.st their fp16 rows into TMEM and tcgen05.mma reads A from
-// TMEM ([a_tmem] operand), leaving shared memory with the fp8 tile and the tokens.
-// TMEM columns: accumulators [0, 2*ACC) (ACC = 2*NB for w1|w3, NB for w2), A ring
-// after them (32 columns per 128 fp16 rows x 64 K per stage).
-#ifndef MOE_FP8_ACC_STAGES
-#define MOE_FP8_ACC_STAGES 2  // r01: 1 (3 TMEM A stages instead of 2 at NB=64) measured 0.3018 vs 0.2901 ms
-#endif
-template <int KIND, int NB, int KB>
-struct Fp8TmemCfg {
-    static_assert(NB <= 64, "TMEM-A fp8 variant: NB <= 64");
-    static_assert(KB == 64 || KB == 128 || KB == 256, "K per stage");
-    static constexpr int kHalves = KIND == kG1Swap ? 2 : 1;
-    static constexpr int kARows = 128 * kHalves;
-    static constexpr int kA8Sub = kARows * (KB < 128 ? KB : 128);  // one TMA box: rows x min(KB,128) B
-    static constexpr int kA8Bytes = kARows * KB;              // fp8 rows x KB bytes (KB/128 boxes)
-    static constexpr int kBSub = NB * 128;                    // one 64-element fp16 token atom
-    static constexpr int kBBytes = kBSub * (KB / 64);
-    static constexpr int kAcc = kHalves * NB;                 // TMEM columns per accumulator stage
-    static constexpr int kACols = (KB / 2) * kHalves;         // TMEM columns per A stage (2 fp16 / column)
-    static constexpr int kAccSt = MOE_FP8_ACC_STAGES;         // accumulator stages
-    static constexpr int kS2Raw = (512 - kAccSt * kAcc) / kACols;
-    static constexpr int kS2 = kS2Raw > 6 ? 6 : kS2Raw;
-    static constexpr int kLoadBytes = kA8Bytes + kBBytes;
-    static constexpr int kS1Raw = (kSmemBudget - 2048) / kLoadBytes;
-    static constexpr int kS1 = kS1Raw > 10 ? 10 : kS1Raw;
-    static constexpr int kSmemBytes = kS1 * kLoadBytes + 2048;
-    static_assert(kS2 >= 2 && kS1 >= 3, "bad fp8 pipeline");
-};
-
-#ifndef MOE_FP8_CVT_INSN
-// 1: cvt.rn.f16x2.e4m3x2 (exact values); 0: integer bit move (values * 2^-8, also exact).
-// r01 A/B on one box: cvt 0.2987 ms vs bit move 0.3586 ms per decode step.
-#define MOE_FP8_CVT_INSN 1
-#endif
-constexpr float kFp8Rescale = MOE_FP8_CVT_INSN ? 1.0f : 256.0f;  // undoes the bit move's 2^-8 (exact)
-
-// Two converter groups (warps 6..9 and 10..13) take alternate k-blocks so that one
-// group's shared-memory / TMEM-store latency overlaps the other's.
-constexpr int kFp8tGroups = 1;  // r01: 2 groups measured slower (0.3466 vs 0.3388 ms per decode step)
-constexpr int kFp8tThreads = (6 + 4 * kFp8tGroups) * 32;
-
-template <int KIND, int NB, int KB>
-__global__ void __launch_bounds__(kFp8tThreads, 1)
-    moe_gemm_fp8t_kernel(const GemmParams p, const float* __restrict__ scales,
-                         const __grid_constant__ CUtensorMap tmA8, const __grid_constant__ CUtensorMap tmB) {
-    using C = Fp8TmemCfg<KIND, NB, KB>;
-    constexpr int S1 = C::kS1, S2 = C::kS2;
-    extern __shared__ __align__(1024) uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint8_t* ring_b = smem;                      // S1 x fp16 token tiles (NB*128 B, 1024-aligned)
-    uint8_t* ring8 = ring_b + S1 * C::kBBytes;   // S1 x fp8 weight tiles (64-byte swizzle)
-    uint64_t* bars = reinterpret_cast<uint64_t*>(ring8 + S1 * C::kA8Bytes);
-    uint64_t* full1 = bars;
-    uint64_t* empty1 = bars + S1;
-    uint64_t* full2 = bars + 2 * S1;
-    uint64_t* empty2 = full2 + S2;
-    uint64_t* tmem_full = empty2 + S2;
-    uint64_t* tmem_empty = tmem_full + 2;
-    uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
-    int32_t* s_counts = reinterpret_cast<int32_t*>(tmem_empty + 3);
-    int32_t* s_offsets = s_counts + 32;
-
-    const int warp = threadIdx.x / 32;
-    const int lane = threadIdx.x % 32;
-    if (warp == 0 && lane == 0) {
-        ptx::prefetch_tmap(&tmA8);
-        ptx::prefetch_tmap(&tmB);
-        for (int i = 0; i < S1; ++i) {
-            ptx::mbar_init(&full1[i], 1);
-            ptx::mbar_init(&empty1[i], 5);
-        }
-        for (int i = 0; i < S2; ++i) {
-            ptx::mbar_init(&full2[i], 4);
-            ptx::mbar_init(&empty2[i], 1);
-        }
-        for (int i = 0; i < 2; ++i) {
-            ptx::mbar_init(&tmem_full[i], 1);
-            ptx::mbar_init(&tmem_empty[i], 4);
-        }
-        ptx::fence_mbar_init();
-    }
-    if (warp == 1) {
-        ptx::tmem_alloc(tmem_base_slot, 512);
-        ptx::tmem_relinquish();
-    }
-    ptx::pdl_wait();
-    if (threadIdx.x < 32)
-        for (int e = threadIdx.x; e < p.E; e += 32) {
-            s_counts[e] = p.counts[e];
-            s_offsets[e] = p.offsets[e];
-        }
-    ptx::tc_fence_before();
-    __syncthreads();
-    ptx::tc_fence_after();
-    const uint32_t tmem_base = *tmem_base_slot;
-    const uint32_t a_base = tmem_base + C::kAccSt * C::kAcc;
-    int total = 0;
-    for (int e = 0; e < p.E; ++e) total += tiles_of<KIND, NB>(s_counts[e], p);
-
-    if (warp == 0) {
-        if (lane == 0) {  // ------------------------------------------------ TMA producer
-            int st = 0;
-            uint32_t ph = 0;
-            for (int t = blockIdx.x; t < total; t += gridDim.x) {
-                TileInfo ti;
-                decode_tile<KIND, NB, KB>(t, p, s_counts, s_offsets, ti);
-                for (int kb = 0; kb < ti.nkb; ++kb) {
-                    ptx::mbar_wait(&empty1[st], ph ^ 1);
-                    ptx::mbar_arrive_expect_tx(&full1[st], C::kLoadBytes);
-                    const int kc = (ti.kb0 + kb) * KB;
-#pragma unroll
-                    for (int sub = 0; sub < (KB > 128 ? KB / 128 : 1); ++sub)
-                        ptx::tma_load_3d(&tmA8, &full1[st], ring8 + st * C::kA8Bytes + sub * C::kA8Sub, kc + 128 * sub,
-                                         ti.a_row, ti.e, ptx::kEvictFirst);
-#pragma unroll
-                    for (int sub = 0; sub < KB / 64; ++sub)
-                        ptx::tma_load_2d(&tmB, &full1[st], ring_b + st * C::kBBytes + sub * C::kBSub, kc + 64 * sub,
-                                         ti.b_row, ptx::kEvictLast);
-                    if (++st == S1) { st = 0; ph ^= 1; }
-                }
-            }
-        }
-    } else if (warp == 1) {
-        if (lane == 0) {  // ------------------------------------------------ MMA issuer
-            int s1 = 0, s2 = 0;
-            uint32_t ph1 = 0, ph2 = 0;
-            int acc = 0;
-            uint32_t acc_phase = 0;
-            for (int t = blockIdx.x; t < total; t += gridDim.x) {
-                TileInfo ti;
-                decode_tile<KIND, NB, KB>(t, p, s_counts, s_offsets, ti);
-                const uint32_t n_mma = (uint32_t)((ti.n_valid + 15) / 16 * 16);
-                const uint32_t idesc = (1u << 4) | ((n_mma >> 3) << 17) | ((128u >> 4) << 24);  // f16 x f16 -> f32
-                const uint32_t d_tmem = tmem_base + acc * C::kAcc;
-                ptx::mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
-                ptx::tc_fence_after();
-                for (int kb = 0; kb < ti.nkb; ++kb) {
-                    ptx::mbar_wait(&full2[s2], ph2);
-                    ptx::tc_fence_after();
-                    const uint32_t a_t = a_base + s2 * C::kACols;
-#pragma unroll
-                    for (int kk = 0; kk < KB / 16; ++kk) {
-                        const uint64_t bdesc = ptx::make_smem_desc_sw128(
-                            ptx::smem_u32(ring_b + s1 * C::kBBytes + (kk / 4) * C::kBSub));
-                        const uint32_t accum = (kb | kk) ? 1u : 0u;
-                        ptx::mma_f16_tmem_a(d_tmem, a_t + 8 * kk, bdesc + 2 * (kk % 4), idesc, accum);
-                        if (KIND == kG1Swap)
-                            ptx::mma_f16_tmem_a(d_tmem + NB, a_t + KB / 2 + 8 * kk, bdesc + 2 * (kk % 4), idesc,
-                                                accum);
-                    }
-                    ptx::mma_commit(&empty2[s2]);
-                    ptx::mma_commit(&empty1[s1]);
-                    if (++s2 == S2) { s2 = 0; ph2 ^= 1; }
-                    if (++s1 == S1) { s1 = 0; ph1 ^= 1; }
-                }
-                ptx::mma_commit(&tmem_full[acc]);
-                if (++acc == C::kAccSt) { acc = 0; acc_phase ^= 1; }
-            }
-        }
-    } else if (warp >= 6) {
-        // ---------------------------------------------------------------- converters (warps 6..)
-        const int q = warp & 3;                 // TMEM lane quadrant of this warp
-        const int r = q * 32 + lane;            // A row (= TMEM lane) of this thread
-        const int grp = (warp - 6) / 4;         // converter group: takes k-blocks seq % kFp8tGroups == grp
-        int s1 = 0, s2 = 0;
-        uint32_t ph1 = 0, ph2 = 0;
-        int seq = 0;
-        for (int t = blockIdx.x; t < total; t += gridDim.x) {
-            TileInfo ti;
-            decode_tile<KIND, NB, KB>(t, p, s_counts, s_offsets, ti);
-            for (int kb = 0; kb < ti.nkb; ++kb, ++seq) {
-                if (seq % kFp8tGroups != grp) {
-                    if (++s2 == S2) { s2 = 0; ph2 ^= 1; }
-                    if (++s1 == S1) { s1 = 0; ph1 ^= 1; }
-                    continue;
-                }
-                ptx::mbar_wait(&full1[s1], ph1);
-                ptx::mbar_wait(&empty2[s2], ph2 ^ 1);
-                ptx::tc_fence_after();
-                const uint8_t* src = ring8 + s1 * C::kA8Bytes;
-#pragma unroll
-                for (int h = 0; h < C::kHalves; ++h) {
-                    const int rr = r + 128 * h;
-                    const uint32_t srow = ptx::smem_u32(src + rr * (KB < 128 ? KB : 128));
-#pragma unroll
-                    for (int half = 0; half < KB / 64; ++half) {   // 64 K elements -> 32 TMEM columns
-                        uint4 vv[4];
-#pragma unroll
-                        for (int c = 0; c < 4; ++c) {  // all shared loads issued first
-                            const int lc = 4 * half + c;  // logical 16-byte chunk of the row
-                            // 64B / 128B swizzle inside a box; KB = 256 rows span two 128-byte boxes
-                            const int pc = KB == 64 ? (lc ^ ((rr >> 1) & 3)) : ((lc & 7) ^ (rr & 7));
-                            vv[c] = ptx::lds128(srow + (lc >> 3) * C::kA8Sub + 16 * pc);
-                        }
-                        uint32_t o[32];
-#pragma unroll
-                        for (int c = 0; c < 4; ++c) {
-                            const uint4 v = vv[c];
-#if MOE_FP8_CVT_INSN
-                            o[8 * c + 0] = cvt_e4m3x2_f16x2(v.x);
-                            o[8 * c + 1] = cvt_e4m3x2_f16x2(v.x >> 16);
-                            o[8 * c + 2] = cvt_e4m3x2_f16x2(v.y);
-                            o[8 * c + 3] = cvt_e4m3x2_f16x2(v.y >> 16);
-                            o[8 * c + 4] = cvt_e4m3x2_f16x2(v.z);
-                            o[8 * c + 5] = cvt_e4m3x2_f16x2(v.z >> 16);
-                            o[8 * c + 6] = cvt_e4m3x2_f16x2(v.w);
-                            o[8 * c + 7] = cvt_e4m3x2_f16x2(v.w >> 16);
-#else
-                            e4m3x4_to_f16x4_scaled(v.x, o[8 * c + 0], o[8 * c + 1]);
-                            e4m3x4_to_f16x4_scaled(v.y, o[8 * c + 2], o[8 * c + 3]);
-                            e4m3x4_to_f16x4_scaled(v.z, o[8 * c + 4], o[8 * c + 5]);
-                            e4m3x4_to_f16x4_scaled(v.w, o[8 * c + 6], o[8 * c + 7]);
-#endif
-                        }
-                        ptx::tmem_st32(a_base + s2 * C::kACols + (KB / 2) * h + 32 * half +
-                                           (static_cast<uint32_t>(q * 32) << 16),
-                                       o);
-                    }
-                }
-                ptx::tmem_wait_st();
-                ptx::tc_fence_before();
-                __syncwarp();
-                if (lane == 0) {
-                    ptx::mbar_arrive(&full2[s2]);
-                    ptx::mbar_arrive(&empty1[s1]);
-                }
-                if (++s2 == S2) { s2 = 0; ph2 ^= 1; }
-                if (++s1 == S1) { s1 = 0; ph1 ^= 1; }
-            }
-        }
-    } else {
-        // ---------------------------------------------------------------- epilogue (warps 2..5)
-        const int q = warp & 3;
-        const int r = q * 32 + lane;
-        int acc = 0;
-        uint32_t acc_phase = 0;
-        for (int t = blockIdx.x; t < total; t += gridDim.x) {
-            TileInfo ti;
-            decode_tile<KIND, NB, KB>(t, p, s_counts, s_offsets, ti);
-            ptx::mbar_wait(&tmem_full[acc], acc_phase);
-            ptx::tc_fence_after();
-            const uint32_t tbase = tmem_base + acc * C::kAcc + (static_cast<uint32_t>(q * 32) << 16);
-            const int nchunks = (ti.n_valid + 15) / 16;
-            if (KIND == kG1Swap) {
-                const float* sc = scales + (int64_t)ti.e * 2 * p.f + ti.m_idx * 256;
-                const float s1v = sc[r] * kFp8Rescale, s3v = sc[128 + r] * kFp8Rescale;
-                __half* hp = static_cast<__half*>(p.out) + static_cast<int64_t>(ti.b_row) * p.f + ti.m_idx * 128 + r;
-#pragma unroll 1
-                for (int cc = 0; cc < nchunks; ++cc) {
-                    uint32_t a[16], b[16];
-                    ptx::tmem_ld16(tbase + cc * 16, a);
-                    ptx::tmem_ld16(tbase + NB + cc * 16, b);
-                    ptx::tmem_wait_ld();
-#pragma unroll
-                    for (int i = 0; i < 16; ++i) {
-                        const int n = cc * 16 + i;
-                        if (n < ti.n_valid) {
-                            const float hv = silu_f32(__uint_as_float(a[i]) * s1v) * (__uint_as_float(b[i]) * s3v);
-                            hp[static_cast<int64_t>(n) * p.f] = __float2half_rn(hv);
-                        }
-                    }
-                }
-            } else {
-                const int drow = ti.m_idx * 128 + r;
-                const float s2v = drow < p.d ? scales[(int64_t)ti.e * p.d + drow] * kFp8Rescale : 0.f;
-                float* y = static_cast<float*>(p.out) + p.out_split_stride * ti.split +
-                           static_cast<int64_t>(ti.b_row) * p.d + drow;
-#pragma unroll 1
-                for (int cc = 0; cc < nchunks; ++cc) {
-                    uint32_t v[16];
-                    ptx::tmem_ld16(tbase + cc * 16, v);
-                    ptx::tmem_wait_ld();
-                    if (drow < p.d) {
-#pragma unroll
-                        for (int i = 0; i < 16; ++i) {
-                            const int n = cc * 16 + i;
-                            if (n < ti.n_valid) {
-                                float u = s2v;
-                                if (p.tok_scale) {
-                                    const float tsn = p.tok_scale[ti.b_row + n];
-                                    u *= tsn * tsn * 64.f;
-                                }
-                                y[static_cast<int64_t>(n) * p.d] = __uint_as_float(v[i]) * u;
-                            }
-                        }
-                    }
-                }
-            }
-            ptx::tc_fence_before();
-            __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(&tmem_empty[acc]);
-            if (++acc == C::kAccSt) { acc = 0; acc_phase ^= 1; }
         }
     }
     ptx::pdl_launch_dependents();

@@ -424,7 +424,6 @@ struct PermuteParams {
     int32_t* pos;             // [T, k] in: in-block rank (router); out: permuted row (-1: not local)
     int32_t* pos_aux;         // optional copy for the caller
     __nv_bfloat16* x_perm;    // [Cap, d]
-    int32_t to_f16;           // store rows as fp16 (fp8-weight GEMMs) instead of copying bf16
     // decode speculative weight prefetch (moe.cu spec_l2): trigger the w1/w3 GEMM before
     // waiting for the router, so its L2 weight prefetch overlaps routing. That GEMM then
     // reads counts / offsets only after its own griddepcontrol.wait.
@@ -442,19 +441,6 @@ struct PermuteParams {
     int64_t peer_rows_off, peer_meta_off;
     int32_t my_rank;
 };
-
-__device__ __forceinline__ uint4 bf16x8_to_f16x8(const uint4& v) {
-    float f[8];
-    bf16x8_to_f32(v, f);
-    uint4 r;
-    __half2 h0 = __floats2half2_rn(f[0], f[1]), h1 = __floats2half2_rn(f[2], f[3]);
-    __half2 h2 = __floats2half2_rn(f[4], f[5]), h3 = __floats2half2_rn(f[6], f[7]);
-    r.x = *reinterpret_cast<uint32_t*>(&h0);
-    r.y = *reinterpret_cast<uint32_t*>(&h1);
-    r.z = *reinterpret_cast<uint32_t*>(&h2);
-    r.w = *reinterpret_cast<uint32_t*>(&h3);
-    return r;
-}
 
 // Two E4M3 codes (lower byte = first element) <-> floats
 __device__ __forceinline__ uint16_t f32x2_to_e4m3x2(float first, float second) {
@@ -612,10 +598,6 @@ __global__ void __launch_bounds__(kPermuteThreads) moe_permute_kernel(const Perm
 #pragma unroll
             for (int u = 0; u < 4; ++u)
                 if (v0 + u * stride < nvec) buf[u] = __ldg(src + v0 + u * stride);
-            if (p.to_f16) {
-#pragma unroll
-                for (int u = 0; u < 4; ++u) buf[u] = bf16x8_to_f16x8(buf[u]);
-            }
 #pragma unroll
             for (int u = 0; u < 4; ++u)
                 if (v0 + u * stride < nvec) {
@@ -623,88 +605,6 @@ __global__ void __launch_bounds__(kPermuteThreads) moe_permute_kernel(const Perm
                     if (dst1) dst1[v0 + u * stride] = buf[u];
                 }
         }
-    }
-    ptx::pdl_launch_dependents();
-}
-
-// FP8 w2 GEMM input (fp8x path): each valid permuted row of the fp16 activation h
-// (written by the fp8x w1/w3 epilogue, normalised by its token scale: h' = h 2^(2t-6))
-// is split into THREE E4M3 terms, t0 + t1 + t2 = h' 2^u with the row max in (224, 448]:
-// fp16 has 11 significant bits, each RNE term takes 4, so the third residual is exact
-// wherever |h' 2^u| >= 2 (above ~1 % of the row max; below, the error is <= 2^-10, i.e.
-// <= 2^-17 of the row max): the w2 GEMM multiplies exactly the fp16 h of R15.
-// Writes h8 planes [3][plane_rows][f] and row_factor[row] = 2^-u 2^(6-2t), which the
-// w2 GEMM multiplies into its fp32 outputs. One block per row; padding rows skipped.
-struct HSplitParams {
-    const __half* h;            // [rows, f] fp16
-    const int32_t* counts;      // [E] rows per local expert
-    const int32_t* offsets;     // [E + 1] segment starts
-    const float* tok_scale;     // [rows] 2^-t of each permuted row
-    uint8_t* h8;                // [3][plane_rows][f]
-    float* row_factor;          // [rows]
-    int64_t plane_rows;
-    int32_t E, f;
-};
-
-__global__ void __launch_bounds__(256) moe_h_split_kernel(const HSplitParams p) {
-    __shared__ uint32_t s_max[8];
-    const int row = blockIdx.x;
-    ptx::pdl_wait();
-    bool valid = false;
-    for (int e = 0; e < p.E; ++e) valid |= row >= p.offsets[e] && row < p.offsets[e] + p.counts[e];
-    if (!valid) {
-        ptx::pdl_launch_dependents();
-        return;
-    }
-    const int nvec = p.f / 8;
-    const uint4* src = reinterpret_cast<const uint4*>(p.h + (int64_t)row * p.f);
-    uint32_t m = 0;  // max |h| on fp16 bit patterns (magnitude order == integer order)
-    for (int v = threadIdx.x; v < nvec; v += 256) {
-        const uint4 q = src[v];
-        const uint32_t w[4] = {q.x, q.y, q.z, q.w};
-#pragma unroll
-        for (int i = 0; i < 4; ++i) m = max(m, max(w[i] & 0x7FFFu, (w[i] >> 16) & 0x7FFFu));
-    }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if ((threadIdx.x & 31) == 0) s_max[threadIdx.x >> 5] = m;
-    __syncthreads();
-    uint32_t rm = 0;
-#pragma unroll
-    for (int w = 0; w < 8; ++w) rm = max(rm, s_max[w]);
-    const float rmax = __half2float(__ushort_as_half(static_cast<unsigned short>(rm)));
-    int u = 0;
-    if (rmax > 0.f) {
-        const int e = ((__float_as_int(448.f / rmax) >> 23) & 0xFF) - 127;
-        u = max(-60, min(60, e));
-    }
-    const float scale = __int_as_float((u + 127) << 23);
-    if (threadIdx.x == 0) {
-        const float ts = p.tok_scale[row];
-        p.row_factor[row] = __int_as_float((127 - u) << 23) * (ts * ts * 64.f);
-    }
-    uint2* t0 = reinterpret_cast<uint2*>(p.h8 + (int64_t)row * p.f);
-    uint2* t1 = reinterpret_cast<uint2*>(p.h8 + (p.plane_rows + row) * (int64_t)p.f);
-    uint2* t2 = reinterpret_cast<uint2*>(p.h8 + (2 * p.plane_rows + row) * (int64_t)p.f);
-    for (int v = threadIdx.x; v < nvec; v += 256) {
-        const uint4 q = src[v];
-        const uint32_t w[4] = {q.x, q.y, q.z, q.w};
-        uint32_t c0[4], c1[4], c2[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const float2 f2 = __half22float2(*reinterpret_cast<const __half2*>(&w[i]));
-            float a = f2.x * scale, b = f2.y * scale;  // exact (power of two)
-            c0[i] = f32x2_to_e4m3x2(a, b);
-            float2 r = e4m3x2_to_f32x2(static_cast<uint16_t>(c0[i]));
-            a -= r.x;  // exact: the residual of an RNE rounding is representable
-            b -= r.y;
-            c1[i] = f32x2_to_e4m3x2(a, b);
-            r = e4m3x2_to_f32x2(static_cast<uint16_t>(c1[i]));
-            c2[i] = f32x2_to_e4m3x2(a - r.x, b - r.y);
-        }
-        t0[v] = make_uint2(c0[0] | (c0[1] << 16), c0[2] | (c0[3] << 16));
-        t1[v] = make_uint2(c1[0] | (c1[1] << 16), c1[2] | (c1[3] << 16));
-        t2[v] = make_uint2(c2[0] | (c2[1] << 16), c2[2] | (c2[3] << 16));
     }
     ptx::pdl_launch_dependents();
 }

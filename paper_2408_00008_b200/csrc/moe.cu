@@ -189,6 +189,21 @@ bool encode_map_fp8(CUtensorMap* m, const void* base, uint64_t K, uint64_t rows,
     return r == CUDA_SUCCESS;
 }
 
+// Tiled FP8 weights (moe_pack_weights_fp8): 4D {128 B, tile_rows, K/128, tiles_total}, each
+// [tile_rows][128 B] chunk contiguous; box {128, tile_rows, 1, 1}; 128B swizzle.
+bool encode_wmap_u8(CUtensorMap* m, const void* base, uint64_t K, uint64_t tile_rows, uint64_t ntiles_total) {
+    PFN_encodeTiled_t fn = get_encode_fn();
+    if (!fn) return false;
+    cuuint64_t dims[4] = {128, tile_rows, K / 128, ntiles_total};
+    cuuint64_t strides[3] = {128, tile_rows * 128, (K / 128) * tile_rows * 128};
+    cuuint32_t box[4] = {128, (cuuint32_t)tile_rows, 1, 1};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<void*>(base), dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
 int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
 int next_pow2(int v) { int p = 1; while (p < v) p <<= 1; return p; }
 
@@ -218,9 +233,6 @@ struct moe_ctx {
     int max_splits = 4;       // split-K partial buffers are sized for this many splits
     int64_t split_stride = 0; // elements between split-K partial buffers of this forward
     bool fp8 = false;             // MOE_FLAG_FP8_WEIGHTS
-    bool fp8_g2_kb256 = false;    // fp8 w2 GEMM with 256-element K blocks (f_local % 256 == 0)
-    bool fp8_kb128 = false;       // fp8 TMEM-A GEMMs with 128-element K blocks (d % 128 == 0;
-                                  // r01: 0.2975 vs 0.3304 ms per step with 64-element blocks)
     moe_expert_weights cur_w{};   // weights of the current forward
     int pair_tune = 0;        // prefill tile-order override (tuning.pair_order)
     // prefill tile orders (pair_decode). G1: bands of 16 token tiles (ncu DRAM sweep r01).
@@ -237,15 +249,12 @@ struct moe_ctx {
     // CUDA-core router (2 tokens / block, 32 blocks at T = 64) for T <= this.
     // r01 64-token decode, interleaved: 0.4335 vs 0.4312 ms with the mma.sync router (4 blocks)
     int router_cc_max_T = 0;
-    // FP8 w1/w3 GEMM on kind::f8f6f4 with two-term E4M3 tokens (moe_gemm_fp8x_kernel);
-    // needs d % 128 == 0 (else, or tuning.fp8_fp16_tokens: the fp16-converter kernels)
-    bool fp8x = false;
-    float* tok_scale = nullptr;   // [cap] 2^-s of each permuted row (fp8x)
-    uint8_t* h8 = nullptr;        // [3][cap][f_local] E4M3 terms of h for the fp8x w2 GEMM
-    float* h_factor = nullptr;    // [cap] per-row output factor of the fp8x w2 GEMM
+    // FP8 weights (moe_gemm_fp8x_kernel, both GEMMs on 8-bit MMAs): tokens as two E4M3
+    // terms with a per-row scale, h as two E4M3 terms with UE8M0 block scales
+    float* tok_scale = nullptr;   // [cap] 2^-s of each permuted row
+    uint8_t* h8 = nullptr;        // [2][cap][f_local] E4M3 terms of h (w1/w3 epilogue -> w2 GEMM)
+    uint8_t* h_sf = nullptr;      // [2][cap/128][f_local/128][512] their UE8M0 scales (MMA scale layout)
     CUtensorMap tm_h8[3]{};       // h8 planes, box {128, NB}, NB = 32, 64, 128
-    int64_t rows_needed_cur = 0;  // permuted rows (incl. segment padding) of the current forward
-    bool fp8_w2_x = false;        // fp8x w2 GEMM (tuning.fp8_w2_split; off: fp16-converter w2 kernel)
     CUtensorMap tm_x8[3]{};       // x_perm as [2][cap][d] E4M3 planes, box {128, NB}, NB = 32, 64, 128
     // workspace (device)
     int32_t *topk_idx = nullptr, *pos = nullptr, *blockcount = nullptr, *blockoff = nullptr;
@@ -325,13 +334,11 @@ struct moe_ctx {
         const void* w2 = nullptr;
         uint64_t tick = 0;
         CUtensorMap tm_w13{}, tm_w13_pair{}, tm_w2_tiled{}, tm_w2_swap{};
-        CUtensorMap tm8_w13_64{}, tm8_w2_64{};  // fp8 weights, 64-byte boxes (smem-widening variant)
     };
     static constexpr size_t kWeightMapCache = 64;
     std::vector<WeightMaps> wmaps;
     uint64_t use_tick = 0;
     CUtensorMap tm_w13{}, tm_w13_pair{}, tm_w2_tiled{}, tm_w2_swap{};  // maps of the current call
-    CUtensorMap tm8_w13_64{}, tm8_w2_64{};
     // instrumentation
     bool profiling = false;
     struct Ev { int slot; cudaEvent_t a, b; };
@@ -409,26 +416,6 @@ moe_status launch(moe_ctx* c, int slot, void (*kern)(KArgs...), dim3 grid, dim3 
         cudaEventRecord(eb, st);
         c->pending.push_back({slot, ea, eb});
     }
-    return MOE_OK;
-}
-
-template <int KIND, int NB>
-moe_status set_fp8t_attr(moe_ctx* c) {
-    CUDA_TRY(c, cudaFuncSetAttribute(moe_gemm_fp8t_kernel<KIND, NB, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     Fp8TmemCfg<KIND, NB, 64>::kSmemBytes));
-    CUDA_TRY(c, cudaFuncSetAttribute(moe_gemm_fp8t_kernel<KIND, NB, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     Fp8TmemCfg<KIND, NB, 128>::kSmemBytes));
-    if (KIND == kG2Swap)
-        CUDA_TRY(c, cudaFuncSetAttribute(moe_gemm_fp8t_kernel<kG2Swap, NB, 256>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         Fp8TmemCfg<kG2Swap, NB, 256>::kSmemBytes));
-    return MOE_OK;
-}
-
-template <int KIND, int NB>
-moe_status set_fp8_attr(moe_ctx* c) {
-    CUDA_TRY(c, cudaFuncSetAttribute(moe_gemm_fp8_kernel<KIND, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     Fp8Cfg<KIND, NB>::kSmemBytes));
     return MOE_OK;
 }
 
@@ -554,10 +541,12 @@ moe_status validate_cfg(const moe_config* cfg, moe_ctx* c) {
     if (cfg->par == MOE_PAR_HYBRID && ps.tp_world > 1 && !cfg->tp_comm)
         return fail(c, MOE_ERR_INVALID, "tp_comm (TP group) required");
     if (cfg->split_k < 0 || cfg->split_k > 8) return fail(c, MOE_ERR_INVALID, "split_k must be in [0,8]");
+    if ((cfg->flags & MOE_FLAG_FP8_WEIGHTS) && cfg->hidden % 128)
+        return fail(c, MOE_ERR_UNSUPPORTED, "MOE_FLAG_FP8_WEIGHTS needs hidden % 128 == 0 (128-byte E4M3 K chunks)");
     for (int i = 0; i < 2; ++i)
         if (cfg->reserved[i]) return fail(c, MOE_ERR_INVALID, "reserved fields must be zero");
     if (const moe_tuning* tu = cfg->tuning) {
-        for (int i = 0; i < 9; ++i)
+        for (int i = 0; i < 11; ++i)
             if (tu->reserved[i]) return fail(c, MOE_ERR_INVALID, "tuning.reserved fields must be zero");
         if (tu->g1_swap_rows < 0 || tu->g2_swap_rows < 0 || tu->g1_grid < 0 || tu->g2_grid < 0 ||
             tu->swap_nb_cap < 0 || tu->router_cc_max_T < 0 || tu->pair_order < 0)
@@ -582,19 +571,15 @@ moe_status ensure_weight_maps(moe_ctx* c, const moe_expert_weights* w) {
             m.tick = c->use_tick;
             c->tm_w13 = m.tm_w13; c->tm_w13_pair = m.tm_w13_pair;
             c->tm_w2_tiled = m.tm_w2_tiled; c->tm_w2_swap = m.tm_w2_swap;
-            c->tm8_w13_64 = m.tm8_w13_64; c->tm8_w2_64 = m.tm8_w2_64;
             return MOE_OK;
         }
     moe_ctx::WeightMaps m;
     m.w13 = w->w13;
     m.w2 = w->w2;
     m.tick = c->use_tick;
-    if (c->fp8) {  // E4M3 weights: only the decode (swap-AB) maps exist
-        const uint32_t bk = c->fp8_kb128 ? 128 : 64;
-        if (!encode_map_fp8(&m.tm_w13, w->w13, c->d, 2 * (uint64_t)c->f_local, c->E_local, 256, bk) ||
-            !encode_map_fp8(&m.tm_w2_swap, w->w2, c->f_local, c->d, c->E_local, 128, bk) ||
-            !encode_map_fp8(&m.tm8_w13_64, w->w13, c->d, 2 * (uint64_t)c->f_local, c->E_local, 256, 64) ||
-            !encode_map_fp8(&m.tm8_w2_64, w->w2, c->f_local, c->d, c->E_local, 128, 64))
+    if (c->fp8) {  // tiled E4M3 weights: only the decode (swap-AB) maps exist
+        if (!encode_wmap_u8(&m.tm_w13, w->w13, c->d, 256, (uint64_t)c->E_local * c->w13_nt) ||
+            !encode_wmap_u8(&m.tm_w2_swap, w->w2, c->f_local, 128, (uint64_t)c->E_local * (c->d / 128)))
             return fail(c, MOE_ERR_CUDA, "cuTensorMapEncodeTiled(fp8 weights) failed");
     } else {
         // tiled layout: W13 in 256-row tiles, W2 in 128-row tiles (rows padded to 256)
@@ -616,28 +601,7 @@ moe_status ensure_weight_maps(moe_ctx* c, const moe_expert_weights* w) {
     }
     c->tm_w13 = m.tm_w13; c->tm_w13_pair = m.tm_w13_pair;
     c->tm_w2_tiled = m.tm_w2_tiled; c->tm_w2_swap = m.tm_w2_swap;
-    c->tm8_w13_64 = m.tm8_w13_64; c->tm8_w2_64 = m.tm8_w2_64;
     return MOE_OK;
-}
-
-template <int KIND, int NB>
-moe_status launch_gemm_fp8(moe_ctx* c, int slot, const GemmParams& p, const float* scales, const CUtensorMap& a8,
-                           const CUtensorMap& b, int grid, cudaStream_t st) {
-    return launch(c, slot, moe_gemm_fp8_kernel<KIND, NB>, dim3(grid), dim3(kFp8Threads),
-                  (size_t)Fp8Cfg<KIND, NB>::kSmemBytes, st, p, scales, a8, b);
-}
-
-template <int KIND, int NB>
-moe_status launch_gemm_fp8t(moe_ctx* c, int slot, const GemmParams& p, const float* scales, const CUtensorMap& a8,
-                            const CUtensorMap& b, int grid, cudaStream_t st) {
-    if (c->fp8_kb128 && KIND == kG2Swap && c->fp8_g2_kb256)  // 256-element K blocks (two 128-byte boxes)
-        return launch(c, slot, moe_gemm_fp8t_kernel<kG2Swap, NB, 256>, dim3(grid), dim3(kFp8tThreads),
-                      (size_t)Fp8TmemCfg<kG2Swap, NB, 256>::kSmemBytes, st, p, scales, a8, b);
-    if (c->fp8_kb128)  // 128-element K blocks (maps encoded with a 128-byte fp8 box)
-        return launch(c, slot, moe_gemm_fp8t_kernel<KIND, NB, 128>, dim3(grid), dim3(kFp8tThreads),
-                      (size_t)Fp8TmemCfg<KIND, NB, 128>::kSmemBytes, st, p, scales, a8, b);
-    return launch(c, slot, moe_gemm_fp8t_kernel<KIND, NB, 64>, dim3(grid), dim3(kFp8tThreads),
-                  (size_t)Fp8TmemCfg<KIND, NB, 64>::kSmemBytes, st, p, scales, a8, b);
 }
 
 // Decode (swap-AB) GEMM1 with token tile NB: bf16 weights, or FP8 weights widened in
@@ -652,19 +616,15 @@ moe_status run_swap_g1(moe_ctx* c, int nbi, const moe_expert_weights* w, cudaStr
         p1.src_row = c->src_row;
         return launch_gemm<kG1Swap, NB>(c, kSlotGemm1, p1, c->tm_w13, c->tm_src, c->num_sms, st);
     }
-    if constexpr (NB <= 128)
-        if (c->fp8 && c->fp8x)
+    if constexpr (NB >= 32 && NB <= 128)
+        if (c->fp8) {  // h -> two E4M3 planes + block scales for the block-scaled w2 GEMM
+            p1.out = c->h8;
+            p1.h_sf = c->h_sf;
+            p1.plane_rows = c->cap;
             return launch(c, kSlotGemm1, moe_gemm_fp8x_kernel<kG1Swap, NB>, dim3(c->g1_grid_now), dim3(kGemmThreads),
                           (size_t)Fp8xCfg<kG1Swap, NB>::kSmemBytes, st, p1, static_cast<const float*>(w->w13_scale),
                           static_cast<const float*>(c->tok_scale), c->tm_w13, c->tm_x8[nbi]);
-    if constexpr (NB <= 64)
-        if (c->fp8)
-            return launch_gemm_fp8t<kG1Swap, NB>(c, kSlotGemm1, p1, w->w13_scale, c->tm_w13, c->tm_x_swap[nbi],
-                                                 c->num_sms, st);
-    if constexpr (NB <= 128)
-        if (c->fp8)
-            return launch_gemm_fp8<kG1Swap, NB>(c, kSlotGemm1, p1, w->w13_scale, c->tm8_w13_64, c->tm_x_swap[nbi],
-                                                c->num_sms, st);
+        }
     if (c->spec_now) p1.spec_l2 = c->spec_l2;
     return launch_gemm<kG1Swap, NB>(c, kSlotGemm1, p1, c->tm_w13, c->tm_x_swap[nbi],
                                     c->g1_grid_now, st);
@@ -676,43 +636,13 @@ moe_status run_swap_g2(moe_ctx* c, int nbi, const moe_expert_weights* w, int spl
     p2.hint_a = c->swap_w_hint;
     p2.w_tr = 128;
     p2.w_nt = c->w2_nt;
-    if (c->fp8 && c->fp8x) p2.tok_scale = c->tok_scale;  // undo the fp8x epilogue's h normalisation
-    if constexpr (NB <= 128)
-        if (c->fp8 && c->fp8x && c->fp8_w2_x) {
-            // h -> three E4M3 terms + per-row factor, then the w2 GEMM on kind::f8f6f4; both
-            // launches are timed as the w2 GEMM slot
-            cudaEvent_t ea = nullptr, eb = nullptr;
-            const bool prof = c->profiling;
-            if (prof) {
-                ea = take_event(c);
-                eb = take_event(c);
-                cudaEventRecord(ea, st);
-                c->profiling = false;
-            }
-            HSplitParams hp{static_cast<const __half*>(static_cast<const void*>(c->h)), c->counts, c->offsets,
-                            c->tok_scale, c->h8, c->h_factor, c->cap, c->E_local, c->f_local};
-            moe_status s = launch(c, kSlotGemm2, moe_h_split_kernel, dim3((unsigned)std::max<int64_t>(1, c->rows_needed_cur)),
-                                  dim3(256), 0, st, hp);
-            if (!s)
-                s = launch(c, kSlotGemm2, moe_gemm_fp8x_kernel<kG2Swap, NB>, dim3(c->num_sms), dim3(kGemmThreads),
-                           (size_t)Fp8xCfg<kG2Swap, NB>::kSmemBytes, st, p2, static_cast<const float*>(w->w2_scale),
-                           static_cast<const float*>(c->h_factor), c->tm_w2_swap, c->tm_h8[nbi]);
-            if (prof) {
-                c->profiling = true;
-                cudaEventRecord(eb, st);
-                c->pending.push_back({kSlotGemm2, ea, eb});
-            }
-            return s;
-        }
-    if constexpr (NB <= 64)
-        if (c->fp8)
-            return launch_gemm_fp8t<kG2Swap, NB>(c, kSlotGemm2, p2, w->w2_scale, c->tm_w2_swap, c->tm_h_swap[nbi],
-                                                 c->g2_grid_now, st);
-    if constexpr (NB <= 128)
-        if (c->fp8) {
-            p2.splits = std::min(splits, c->f_local / kBK);
-            return launch_gemm_fp8<kG2Swap, NB>(c, kSlotGemm2, p2, w->w2_scale, c->tm8_w2_64, c->tm_h_swap[nbi],
-                                                c->num_sms, st);
+    if constexpr (NB >= 32 && NB <= 128)
+        if (c->fp8) {  // block-scaled 8-bit MMAs on the two E4M3 planes of h
+            p2.h_sf = c->h_sf;
+            p2.plane_rows = c->cap;
+            return launch(c, kSlotGemm2, moe_gemm_fp8x_kernel<kG2Swap, NB>, dim3(c->g2_grid_now), dim3(kGemmThreads),
+                          (size_t)Fp8xCfg<kG2Swap, NB>::kSmemBytes, st, p2, static_cast<const float*>(w->w2_scale),
+                          static_cast<const float*>(nullptr), c->tm_w2_swap, c->tm_h8[nbi]);
         }
     return launch_gemm<kG2Swap, NB>(c, kSlotGemm2, p2, c->tm_w2_swap, c->tm_h_swap[nbi],
                                     c->g2_grid_now, st);
@@ -785,9 +715,7 @@ moe_status route_and_permute(moe_ctx* c, const RouteSpec& r, cudaStream_t st) {
     pp.src_row = r.src_row;
     pp.early_trigger = r.early;
     pp.peers = r.peers; pp.peer_rows_off = r.peer_rows_off; pp.peer_meta_off = r.peer_meta_off; pp.my_rank = r.my_rank;
-    pp.to_f16 = c->fp8 && r.cap == 0;  // fp8-weight GEMMs take fp16 tokens
-    if (c->fp8x && r.cap == 0 && r.dst_rows == c->x_perm) {  // ... or two E4M3 terms (fp8x)
-        pp.to_f16 = 0;
+    if (c->fp8 && r.cap == 0 && r.dst_rows == c->x_perm) {  // FP8 weights: two E4M3 token terms
         pp.x8 = reinterpret_cast<uint8_t*>(c->x_perm);
         pp.tok_scale = c->tok_scale;
         pp.plane_rows = c->cap;
@@ -860,7 +788,7 @@ moe_status run_gemms(moe_ctx* c, GemmPaths gp, int64_t rows_bound, int64_t rows_
     // decode: per-expert counts ~ Bin(64, 1/4), P(> 32) ~ 1e-6; a larger expert just runs
     // two token tiles). The smaller B stages leave room for a 5th pipeline stage
     // (r01 A/B: 0.2744 -> 0.2686 ms per step).
-    if (c->fp8 && c->fp8x && rows_total <= 16LL * c->E_local) {
+    if (c->fp8 && rows_total <= 16LL * c->E_local) {
         nb1 = std::min(nb1, 32);
         nb2 = std::min(nb2, 32);
     }
@@ -899,7 +827,7 @@ moe_status run_gemms(moe_ctx* c, GemmPaths gp, int64_t rows_bound, int64_t rows_
         // FP8 w1/w3 (fp8x) at the 32-token tile (mean <= 16 rows per expert): equal waves
         // over the E_l * wt one-tile-per-expert units (896 -> 128 CTAs; ab_grid_fp8_2.log:
         // 165.6 -> 164.2 us, step 0.2685 -> 0.2668 ms)
-        if (c->g1_grid <= 0 && c->fp8 && c->fp8x && rows_total <= 16LL * c->E_local) {
+        if (c->g1_grid <= 0 && c->fp8 && rows_total <= 16LL * c->E_local) {
             const int64_t U1 = (int64_t)c->E_local * wt, w1 = (U1 + ns - 1) / ns;
             c->g1_grid_now = (int)std::min<int64_t>(ns, (U1 + w1 - 1) / w1);
         }
@@ -945,14 +873,16 @@ moe_status run_gemms(moe_ctx* c, GemmPaths gp, int64_t rows_bound, int64_t rows_
         // cover the SMs -- EP8 at decode has 32 units of 128 W2 rows (21.6 % of 148 SMs),
         // 4 splits -> 128 units (SURVEY 8(d) wave table); EP4 64 -> 2 splits.
         const int64_t U0 = (int64_t)c->E_local * ((c->d + 127) / 128);
-        int auto_splits = c->fp8 ? 4 : nb2 <= 64 ? 1 : 2;
+        // r02 (shard sweeps, profiles/r02): with one token tile per expert (NB 192 at the
+        // T = 575 stack) 1 split beats 2 -- stack layer 527 vs 535 us, TP8 stack rank 94.6 vs
+        // 104.8 us; the 32-layer stack is unchanged (14.97 vs 14.93 ms)
+        int auto_splits = c->fp8 ? 4 : 1;
         if (need <= nb2 && 4 * U0 < 3 * (int64_t)c->num_sms)
             auto_splits = std::max<int>(auto_splits, (int)std::min<int64_t>(c->max_splits, c->num_sms / U0));
         splits = c->cfg.split_k ? c->cfg.split_k : auto_splits;
         splits = (int)std::max<int64_t>(1, std::min<int64_t>(splits, c->y_elems / (rows_needed * c->d)));
-        splits = std::min(splits, c->f_local / (c->fp8_g2_kb256 ? 256 : c->fp8_kb128 ? 128 : kBK));  // >= 1 K block per split
+        splits = std::min(splits, c->f_local / (c->fp8 ? 128 : kBK));  // >= 1 K block per split
         c->split_stride = rows_needed * c->d;
-        c->rows_needed_cur = std::min<int64_t>(rows_needed, c->cap);
         {
             const int64_t U = (int64_t)c->E_local * ((c->d + 127) / 128) * splits;
             const int ns = c->num_sms;
@@ -1363,17 +1293,7 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
     c->w13_nt = 2 * c->f_local / 256;
     c->w2_nt = (c->d + 255) / 256 * 2;
     c->fp8 = (cfg->flags & MOE_FLAG_FP8_WEIGHTS) != 0;
-    c->fp8_kb128 = c->fp8 && c->d % 128 == 0 && c->f_local % 128 == 0;
-    c->fp8_g2_kb256 = c->fp8_kb128 && c->f_local % 256 == 0;
-    c->fp8x = c->fp8_kb128;
-    // fp8x w2 GEMM: off by default. r01 (64-token decode, interleaved A/B): 0.3062 vs
-    // 0.2708 ms per step -- the h split kernel costs 9.5 us and the w2 GEMM on row-major
-    // E4M3 W2 with 128-byte K blocks streams at ~4 TB/s (122 us) against the converter
-    // kernel's 95 us with 256-byte K blocks.
-    c->fp8_w2_x = false;
     if (const moe_tuning* tu = cfg->tuning) {
-        if (tu->fp8_fp16_tokens) c->fp8x = false;
-        c->fp8_w2_x = c->fp8x && tu->fp8_w2_split != 0;
         c->pair_tune = tu->pair_order;
         if (tu->pair_nblk) c->pair_nblk = tu->pair_nblk == 1 ? 1 : 2;
         c->swap_nb_cap = tu->swap_nb_cap;
@@ -1440,9 +1360,9 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
     ALLOC(c->done, sizeof(unsigned int) * 4);
     ALLOC(c->x_perm, sizeof(__nv_bfloat16) * c->cap * c->d);
     ALLOC(c->tok_scale, sizeof(float) * c->cap);
-    if (c->fp8_w2_x) {
-        ALLOC(c->h8, (size_t)3 * c->cap * c->f_local);
-        ALLOC(c->h_factor, sizeof(float) * c->cap);
+    if (c->fp8) {
+        ALLOC(c->h8, (size_t)2 * c->cap * c->f_local);
+        ALLOC(c->h_sf, (size_t)2 * (c->cap / 128) * (c->f_local / 128) * 512);
     }
     ALLOC(c->src_row, sizeof(int32_t) * (c->cap + 512));
     ALLOC(c->h, sizeof(__nv_bfloat16) * c->cap * c->f_local);
@@ -1504,6 +1424,9 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
     if ((e = cudaMemset(c->x_perm, 0, sizeof(__nv_bfloat16) * c->cap * c->d)) != cudaSuccess) return fail_init("memset", e);
     if ((e = cudaMemset(c->src_row, 0, sizeof(int32_t) * (c->cap + 512))) != cudaSuccess) return fail_init("memset", e);
     if ((e = cudaMemset(c->h, 0, sizeof(__nv_bfloat16) * c->cap * c->f_local)) != cudaSuccess) return fail_init("memset", e);
+    if (c->fp8 && ((e = cudaMemset(c->h8, 0, (size_t)2 * c->cap * c->f_local)) != cudaSuccess ||
+                   (e = cudaMemset(c->h_sf, 0x7F, (size_t)2 * (c->cap / 128) * (c->f_local / 128) * 512)) != cudaSuccess))
+        return fail_init("memset", e);
 
     // workspace TMA descriptors
     bool ok = encode_map(&c->tm_x_tiled, c->x_perm, 2, c->d, c->cap, 1, 128) &&
@@ -1514,9 +1437,9 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
     for (int i = 0; i < 5 && ok; ++i)
         ok = encode_map(&c->tm_x_swap[i], c->x_perm, 2, c->d, c->cap, 1, nbs[i]) &&
              encode_map(&c->tm_h_swap[i], c->h, 2, c->f_local, c->cap, 1, nbs[i]);
-    for (int i = 0; i < 3 && ok && c->fp8x; ++i)
+    for (int i = 0; i < 3 && ok && c->fp8; ++i)
         ok = encode_map_fp8(&c->tm_x8[i], c->x_perm, c->d, c->cap, 2, nbs[i], 128) &&
-             (!c->fp8_w2_x || encode_map_fp8(&c->tm_h8[i], c->h8, c->f_local, c->cap, 3, nbs[i], 128));
+             encode_map_fp8(&c->tm_h8[i], c->h8, c->f_local, c->cap, 2, nbs[i], 128);
     if (!ok) {
         moe_destroy(c);
         return fail(nullptr, MOE_ERR_CUDA, "cuTensorMapEncodeTiled(workspace) failed");
@@ -1530,12 +1453,7 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
         (as = set_gemm_attr<kG2Swap, 192>(c)) ||
         (as = set_pair_attr<kG1Pair, 1>(c)) || (as = set_pair_attr<kG2Pair, 1>(c)) ||
         (as = set_pair_attr<kG1Pair, 2>(c)) || (as = set_pair_attr<kG2Pair, 2>(c)) ||
-        (as = set_fp8x_attr<32>(c)) || (as = set_fp8x_attr<64>(c)) || (as = set_fp8x_attr<128>(c)) ||
-        (as = set_fp8_attr<kG1Swap, 32>(c)) || (as = set_fp8_attr<kG2Swap, 32>(c)) ||
-        (as = set_fp8_attr<kG1Swap, 64>(c)) || (as = set_fp8_attr<kG2Swap, 64>(c)) ||
-        (as = set_fp8_attr<kG1Swap, 128>(c)) || (as = set_fp8_attr<kG2Swap, 128>(c)) ||
-        (as = set_fp8t_attr<kG1Swap, 32>(c)) || (as = set_fp8t_attr<kG2Swap, 32>(c)) ||
-        (as = set_fp8t_attr<kG1Swap, 64>(c)) || (as = set_fp8t_attr<kG2Swap, 64>(c))) {
+        (as = set_fp8x_attr<32>(c)) || (as = set_fp8x_attr<64>(c)) || (as = set_fp8x_attr<128>(c))) {
         std::string m = c->err;
         moe_destroy(c);
         g_init_error = m;
@@ -1568,8 +1486,7 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
             reinterpret_cast<const void*>(moe_gemm_fp8x_kernel<kG1Swap, 128>),
             reinterpret_cast<const void*>(moe_gemm_fp8x_kernel<kG2Swap, 32>),
             reinterpret_cast<const void*>(moe_gemm_fp8x_kernel<kG2Swap, 64>),
-            reinterpret_cast<const void*>(moe_gemm_fp8x_kernel<kG2Swap, 128>),
-            reinterpret_cast<const void*>(moe_h_split_kernel)};
+            reinterpret_cast<const void*>(moe_gemm_fp8x_kernel<kG2Swap, 128>)};
         for (const void* fn : fns)
             if ((e = cudaFuncGetAttributes(&fa, fn)) != cudaSuccess) return fail_init("cudaFuncGetAttributes", e);
     }
@@ -1585,7 +1502,7 @@ moe_status moe_destroy(moe_ctx* c) {
                     c->x_perm, c->h, c->y, c->stage_in, c->stage_out, c->tp_partial, c->tp_scatter, c->ep_send,
                     c->ep_recv, c->ep_ysend, c->ep_yrecv, c->ep_meta_send, c->ep_meta_recv,
                     c->ep_ridx, c->ep_rpos, c->ep_rw, c->ep_rcounts, c->lb_scratch, c->d_peers, c->src_row,
-                    c->tok_scale, c->h8, c->h_factor};
+                    c->tok_scale, c->h8, c->h_sf};
     for (void* p : c->p2p_opened) cudaIpcCloseMemHandle(p);
     if (c->sym) {
         cudaDeviceSynchronize();  // peers' stores into this region have drained (same-process group)
@@ -1637,17 +1554,18 @@ moe_status moe_pack_weights_fp8(moe_ctx* c, const void* q1, const void* q3, cons
         return fail(c, MOE_ERR_INVALID, "NULL pointer");
     if (!aligned16(q1) || !aligned16(q3) || !aligned16(q2) || !aligned16(w13_out) || !aligned16(w2_out))
         return fail(c, MOE_ERR_INVALID, "fp8 weight pointers must be 16-byte aligned");
-    if (c->d % 16) return fail(c, MOE_ERR_UNSUPPORTED, "fp8 packing needs hidden % 16 == 0");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const int e_off = c->e_lo;
-    // one byte per weight: pack pairs of fp8 as 2-byte units with the bf16 packers
+    // one byte per weight, tiled like the bf16 weights: pairs of E4M3 move as 2-byte units
+    // through the bf16 packers, so a [rows][64 units] chunk is a [rows][128 B] chunk of
+    // 128 E4M3 weights (w13: 256-row tiles, w2: 128-row tiles, include/moe.h)
     if ((s = launch(c, kSlotPack, moe_pack_w13_kernel, dim3(4 * c->num_sms), dim3(256), 0, st,
                     static_cast<const __nv_bfloat16*>(q1), static_cast<const __nv_bfloat16*>(q3),
-                    static_cast<__nv_bfloat16*>(w13_out), c->E_local, e_off, c->d / 2, c->f, c->f_local, c->f_off, 0)))
+                    static_cast<__nv_bfloat16*>(w13_out), c->E_local, e_off, c->d / 2, c->f, c->f_local, c->f_off, 1)))
         return s;
     if ((s = launch(c, kSlotPack, moe_pack_w2_kernel, dim3(4 * c->num_sms), dim3(256), 0, st,
                     static_cast<const __nv_bfloat16*>(q2), static_cast<__nv_bfloat16*>(w2_out), c->E_local, e_off,
-                    c->d, c->f / 2, c->f_local / 2, c->f_off / 2, 0, 0)))
+                    c->d, c->f / 2, c->f_local / 2, c->f_off / 2, 1, 0)))
         return s;
     if ((s = launch(c, kSlotPack, moe_pack_scales_kernel, dim3(c->num_sms), dim3(256), 0, st, s1, s3, s2,
                     w13_scale_out, w2_scale_out, c->E_local, e_off, c->d, c->f, c->f_local, c->f_off)))

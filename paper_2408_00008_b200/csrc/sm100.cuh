@@ -180,6 +180,48 @@ __device__ __forceinline__ void mma_e4m3(uint32_t d_tmem, uint64_t adesc, uint64
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
         : "memory");
 }
+// Block-scaled 8-bit MMA (kind::mxf8f6f4.block_scale, scale_vec 1X): D (+)= (A . 2^sfa)(B . 2^sfb)^T
+// with E4M3 A/B from shared memory, one UE8M0 scale per row per 32 K elements (= per
+// instruction, K = 32). sfa_tmem / sfb_tmem: TMEM addresses of the scale columns, bits
+// [30,32) selecting the byte (the K block) inside the 32-bit column (== idesc sf ids).
+__device__ __forceinline__ void mma_mx_e4m3(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t accumulate, uint32_t sfa_tmem, uint32_t sfb_tmem) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::mxf8f6f4.block_scale [%0], %1, %2, %3, [%5], [%6], p;\n\t}" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(sfa_tmem), "r"(sfb_tmem)
+        : "memory");
+}
+// Instruction descriptor of the block-scaled E4M3 x E4M3 MMA with UE8M0 scales (PTX ISA,
+// tcgen05 "instruction descriptor for .kind::mxf8f6f4"): bits [4,6) B scale id,
+// [7,10) A format (0 = E4M3), [10,13) B format, 15/16 A/B major (0 = K), [17,23) N >> 3,
+// bit 23 scale format (1 = UE8M0), [24,29) M >> 4, [29,31) A scale id. D is fp32.
+__host__ __device__ __forceinline__ uint32_t make_idesc_mx_e4m3(uint32_t M, uint32_t N, uint32_t a_sf, uint32_t b_sf) {
+    return (b_sf << 4) | ((N >> 3) << 17) | (1u << 23) | ((M >> 4) << 24) | (a_sf << 29);
+}
+// Shared memory -> TMEM copy of 32 rows x 128 bit, broadcast into all four 32-lane
+// quadrants (tcgen05.cp .32x128b.warpx4): row i -> lanes i, 32+i, 64+i, 96+i, four columns.
+__device__ __forceinline__ void tmem_cp_32x128b_x4(uint32_t tmem_dst, uint64_t sdesc) {
+    asm volatile("tcgen05.cp.cta_group::1.32x128b.warpx4 [%0], %1;" ::"r"(tmem_dst), "l"(sdesc) : "memory");
+}
+// Descriptor of a non-swizzled K-major block of 16-byte rows (core matrices of 8 rows x
+// 16 B = 128 B, stacked 128 B apart): the tcgen05.cp source of a 32 x 16 B scale atom.
+__device__ __forceinline__ uint64_t make_smem_desc_rows16(uint32_t smem_addr) {
+    uint64_t d = 0;
+    d |= static_cast<uint64_t>((smem_addr >> 4) & 0x3FFF);
+    d |= static_cast<uint64_t>(128 >> 4) << 16;  // leading byte offset (single core matrix in K)
+    d |= static_cast<uint64_t>(128 >> 4) << 32;  // stride byte offset: 8-row groups 128 B apart
+    d |= static_cast<uint64_t>(1) << 46;         // sm_100 descriptor version; layout 0 = no swizzle
+    return d;
+}
+// Contiguous bytes global -> shared with an mbarrier transaction count (cp.async.bulk).
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
 // Arrive (once) on an mbarrier when all previously issued tcgen05.mma of this thread complete.
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(

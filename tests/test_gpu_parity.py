@@ -936,7 +936,8 @@ def _fp8_inputs(shape, seed):
     return inp, qs, host
 
 
-@pytest.mark.parametrize("T,d,f,E", [(16, 64, 128, 4), (64, 512, 1024, 8), (300, 256, 512, 8), (7, 128, 256, 2)])
+@pytest.mark.parametrize("T,d,f,E", [(16, 128, 128, 4), (64, 512, 1024, 8), (300, 256, 512, 8), (7, 128, 256, 2),
+                                     (200, 384, 640, 6)])
 def test_fp8_weights(moe, T, d, f, E):
     """FP8 E4M3 weights with per-row power-of-two scales: the GPU must match the oracle
     evaluated on the exact dequantised weights (same tolerance as bf16)."""
@@ -951,13 +952,10 @@ def test_fp8_weights(moe, T, d, f, E):
 
 @pytest.mark.parametrize("T", [64, 300])
 def test_fp8_two_term_tokens(moe, T):
-    """FP8 w1/w3 GEMM on kind::f8f6f4 with tokens split into two E4M3 terms (default) vs the fp16-token
-    converter kernels (tuning fp8_fp16_tokens=1). Rows scaled by 2^3 and
-    2^-10 (exact in bf16) and a zero row exercise the per-row power-of-two token scale
-    and the fp16 h normalisation h * 2^(2s-6): the two-term path must pass the oracle on
-    every row; the converter path (unnormalised fp16 h, which underflows for the 2^-10
-    row) must agree with it far inside the tolerance on the unscaled rows (both multiply
-    exact token values; they differ only in accumulation order and fp16 h roundings)."""
+    """FP8 weights, both GEMMs on 8-bit MMAs: tokens split into two E4M3 terms with a
+    per-row power-of-two scale. Rows scaled by 2^3 and 2^-10 (exact in bf16) and a zero row
+    exercise the token scale, the h block scales (an all-zero block) and their ranges;
+    every row against the oracle, the zero row exactly zero."""
     shape = synth.MoEShape(T=T, d=512, f=1024, E=8, k=2)
     inp, qs, host = _fp8_inputs(shape, 900 + T)
     x = inp["x"].float()
@@ -966,31 +964,37 @@ def test_fp8_two_term_tokens(moe, T):
     x[3] = 0
     inp["x"] = x.to(torch.bfloat16)
     host["x"] = inp["x"].float().cpu().numpy()
-    outs = []
-    for v in ("0", "1"):
-        blk = moe.MoEBlock(inp["wg"], qs["w1"], qs["w3"], qs["w2"], top_k=2, max_tokens=T,
-                           flags=moe.MOE_FLAG_FP8_WEIGHTS, tuning={"fp8_fp16_tokens": int(v == "0")})
-        run = GpuRun(blk, inp["x"])
-        if v == "1":
-            print("fp8x", T, check_forward(run, host, 2))
-        outs.append(run.np("out_f32").astype(np.float64))
-        blk.close()
-    assert np.all(outs[1][3] == 0)
-    a, b = outs[0][4:], outs[1][4:]
-    rms = np.sqrt(np.mean(a ** 2, axis=1, keepdims=True))
-    rel = np.abs(a - b) / rms
-    assert rel.max() < 3e-3, rel.max()
-
-
-@pytest.mark.parametrize("T,d,f,E", [(64, 512, 1024, 8), (300, 256, 512, 8), (7, 128, 256, 2)])
-def test_fp8_w2_three_term(moe, T, d, f, E):
-    """Optional FP8 w2 GEMM on kind::f8f6f4 (tuning fp8_w2_split=1): h split into three E4M3
-    terms per row (exact for fp16 h above ~1 % of the row max) by moe_h_split_kernel."""
-    inp, qs, host = _fp8_inputs(synth.MoEShape(T=T, d=d, f=f, E=E, k=2), 1100 + T)
     blk = moe.MoEBlock(inp["wg"], qs["w1"], qs["w3"], qs["w2"], top_k=2, max_tokens=T,
-                       flags=moe.MOE_FLAG_FP8_WEIGHTS, tuning={"fp8_w2_split": 1})
+                       flags=moe.MOE_FLAG_FP8_WEIGHTS)
     run = GpuRun(blk, inp["x"])
-    check_forward(run, host, 2)
+    print("fp8", T, check_forward(run, host, 2))
+    assert np.all(run.np("out_f32")[3] == 0)
+    blk.close()
+
+
+@pytest.mark.parametrize("nb_cap", [0, 32, 64])
+def test_fp8_block_scales(moe, nb_cap):
+    """The UE8M0 block scales of h (one per token row and 32 ffn columns) must reach the
+    block-scaled w2 MMA at the right (row, K block): w1 rows scaled per 32-column block by
+    2^(b mod 7 - 3) and token rows by 2^(t mod 5 - 2), so neighbouring blocks and rows get
+    different scales -- a scale applied to the wrong row or block is off by powers of two.
+    Token tiles capped at 32 / 64 rows put B tiles at every 32-row group of the 128-row
+    scale atom."""
+    shape = synth.MoEShape(T=200, d=256, f=512, E=8, k=2)
+    inp = _inputs(shape, 1300 + nb_cap)
+    w1 = inp["w1"].float()
+    blk_scale = torch.tensor([2.0 ** (b % 7 - 3) for b in range(shape.f // 32)], device=w1.device)
+    w1 = w1 * blk_scale.repeat_interleave(32).view(1, -1, 1)
+    inp["w1"] = w1.to(torch.bfloat16)
+    x = inp["x"].float() * torch.tensor([2.0 ** (t % 5 - 2) for t in range(shape.T)], device=w1.device).view(-1, 1)
+    inp["x"] = x.to(torch.bfloat16)
+    qs = {n: synth.quantize_fp8_rows(inp[n]) for n in ("w1", "w3", "w2")}
+    host = {n: synth.dequantize_fp8_rows(*qs[n]).cpu().numpy() for n in qs}
+    host["x"] = inp["x"].float().cpu().numpy()
+    host["wg"] = inp["wg"].float().cpu().numpy()
+    blk = moe.MoEBlock(inp["wg"], qs["w1"], qs["w3"], qs["w2"], top_k=2, max_tokens=shape.T,
+                       flags=moe.MOE_FLAG_FP8_WEIGHTS, tuning={"swap_nb_cap": nb_cap} if nb_cap else None)
+    print("fp8 block scales", nb_cap, check_forward(GpuRun(blk, inp["x"]), host, 2))
     blk.close()
 
 
