@@ -862,7 +862,8 @@ def main():
         "value": tok_s, "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": max(3, args.warmup),
         "ms_per_step": ms, "higher_is_better": True,
         "scaling": "strong" if par in ("ep", "tp", "hybrid") else "weak", "vs_baseline": None,
-        "dtype": "fp8-e4m3 weights (per-row pow2 scales), fp16 GEMM activations, bf16 in/out" if args.fp8 else "bf16",
+        "dtype": ("e4m3 weights (per-row pow2 scales), e4m3 two-term activations (per-row / per-32 UE8M0 "
+                  "scales), fp32 accumulate, bf16 in/out") if args.fp8 else "bf16",
         "data": "synthetic (seeded Gaussian tokens, random-init Mixtral-shaped weights; DESIGN.md input recipe)",
         "config": workload_config(args, world)[2],
         "roofline": roof,

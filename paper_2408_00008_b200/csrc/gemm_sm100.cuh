@@ -53,11 +53,15 @@ struct GemmParams {
     // per expert. The weight maps are 4D {64, w_tr, K/64, w_nt * E}.
     int32_t w_tr, w_nt;
     // FP8 weights (block-scaled path): h leaves the w1/w3 GEMM as two E4M3 planes
-    // [2][plane_rows][f] (p.out) and their UE8M0 scales h_sf [2][plane_rows/128][f/128][512],
-    // one scale per (row, 32 consecutive ffn columns), each 512-byte group holding 128 rows
-    // x 4 K blocks in the block-scaled MMA's scale layout: byte 16*(r%32) + 4*((r%128)/32) + kb.
+    // [2][plane_rows][f] (p.out) and their UE8M0 scales, one per (row, 32 consecutive ffn
+    // columns), in h_sf [plane_rows / sf_nb][f / 128][sf block] -- one block per sf_nb-row
+    // token tile of the w2 GEMM and 128-column K chunk, laid out as the block-scaled MMA
+    // reads its B scales when the tile's hi rows and lo rows are stacked into one N = 2 sf_nb
+    // operand: virtual row v (hi of row v < sf_nb, lo of row v - sf_nb after) at byte
+    // 512 (v / 128) + 16 (v % 32) + 4 ((v % 128) / 32) + kb (tcgen05.cp 32x128b atoms).
     uint8_t* h_sf;
     int64_t plane_rows;
+    int32_t sf_nb;
     // kG1Swap speculative L2 prefetch (moe.cu spec_l2): K blocks of this CTA's first
     // weight tile to prefetch into L2 BEFORE the routing is known, assuming every
     // expert holds 1..NB rows (one token tile each: unit u = expert u / (f/128), weight
@@ -1031,20 +1035,21 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 // both on the 8-bit tensor-core path with no weight conversion. Weights: E4M3 with one
 // power-of-two scale per output row (R15), TILED like the bf16 weights (each
 // 256-row w13 / 128-row w2 tile stored as K/128 contiguous [rows][128 B] chunks: one TMA
-// box = one contiguous 32 / 16 KB range of HBM).
-//   kG1Swap (w1/w3 + SwiGLU): B = the tokens as two E4M3 terms hi + lo = x 2^s (exact
-//     for bf16 x above ~1e-3 of its row max; permute_row_fp8x), two kind::f8f6f4 MMAs per
-//     32-byte K step into the a (w1) and b (w3) accumulators; the epilogue applies the
-//     weight row scales and 2^-s, SwiGLU, and writes h for the w2 GEMM as two E4M3 terms
-//     with a UE8M0 scale per 32 ffn columns of each row -- the 32 lanes of one epilogue
-//     warp hold exactly those 32 columns, so the block max is one warp reduction:
+// box = one contiguous 32 / 16 KB range of HBM). The B operand is always two E4M3 terms,
+// staged back to back, so ONE MMA with N = 2 NB covers both (the A tile is read from
+// shared memory once per K step, not once per term) and the epilogue adds the halves.
+//   kG1Swap (w1/w3 + SwiGLU): B = the tokens as hi + lo = x 2^s (exact for bf16 x above
+//     ~1e-3 of its row max; permute_row_fp8x), kind::f8f6f4 into the a (w1) and b (w3)
+//     accumulators; the epilogue applies the weight row scales and 2^-s, SwiGLU, and writes
+//     h for the w2 GEMM as two E4M3 terms with a UE8M0 scale per 32 ffn columns of each
+//     row -- the 32 lanes of one epilogue warp hold exactly those 32 columns, so the block
+//     max is one warp reduction:
 //       u = the power of two putting the block max in (224, 448],
 //       hi = e4m3(h 2^u)  (scale 2^-u),  lo = e4m3((h 2^u - hi) 16)  (scale 2^-(u+4)),
 //     |h - hi 2^-u - lo 2^-(u+4)| <= 2^-8 |h| (plus 2^-10 2^-u below the E4M3 normal range).
-//   kG2Swap (w2): A = W2 tile, B = hi and lo planes, block-scaled MMAs
-//     (kind::mxf8f6f4.block_scale): the scales of B ride in TMEM (tcgen05.cp per stage),
-//     those of A are all 1 (the weight row scale is applied in the epilogue). No h split
-//     kernel, no per-row factor.
+//   kG2Swap (w2): A = W2 tile, B = hi and lo rows of h, block-scaled MMAs
+//     (kind::mxf8f6f4.block_scale): the B scales ride in TMEM (tcgen05.cp per stage), those
+//     of A are all 1 (the weight row scale is applied in the epilogue).
 // Warps: 0 = TMA producer, 1 = TMEM + MMA issuer, 2..5 = epilogue.
 template <int KIND, int NB>
 struct Fp8xCfg {
@@ -1054,16 +1059,18 @@ struct Fp8xCfg {
     // w1|w3 rows (G1) or W2 rows (G2) x 128 E4M3 (one 128-byte swizzle row)
     static constexpr int kARows = KIND == kG1Swap ? 256 : 128;
     static constexpr int kABytes = kARows * 128;
-    static constexpr int kTerms = 2;            // E4M3 terms of the B operand rows
-    static constexpr int kBBytes = NB * 128;    // B rows x 128 E4M3, per term
-    static constexpr int kSFBytes = kMX ? 1024 : 0;  // two 512-byte scale groups (hi, lo)
-    static constexpr int kStageBytes = kABytes + kTerms * kBBytes + kSFBytes;
+    static constexpr int kBBytes = 2 * NB * 128;          // hi rows then lo rows, 128 E4M3 each
+    static constexpr int kSFBytes = kMX ? (NB == 128 ? 1024 : 512) : 0;  // B scale block per K chunk
+    static constexpr int kStageBytes = kABytes + kBBytes + kSFBytes;
     static constexpr int kStagesRaw = (kSmemBudget - 2048 - 1024) / kStageBytes;
     static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
     static constexpr int kSmemBytes = kStages * kStageBytes + 2048 + 1024;  // + barriers + the A scale atom
     static_assert(kStages >= 3, "pipeline too shallow");
-    // TMEM columns: two accumulator stages of 256, then the scale columns (MX)
-    static constexpr uint32_t kSfaCol = 496, kSfbCol = 500;  // SFA 4 columns, SFB hi / lo 4 each
+    // TMEM: accumulator stage = (a, b) x 2 NB columns (G1) or 2 NB (G2), two stages if they fit
+    static constexpr int kAccCols = (KIND == kG1Swap ? 4 : 2) * NB;
+    static constexpr int kAccStages = 2 * kAccCols <= 448 ? 2 : 1;
+    static constexpr uint32_t kSfaCol = 480, kSfbCol = 488;  // SFA 4 columns, SFB up to 8 (MX)
+    static_assert(!kMX || kAccStages * kAccCols <= 480, "TMEM columns");
 };
 
 __device__ __forceinline__ uint8_t f32_to_e4m3(float v) {
@@ -1087,12 +1094,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     constexpr bool kG1 = KIND == kG1Swap;
     constexpr int S = C::kStages;
     constexpr int KB = 128;  // K elements (bytes) per stage
+    constexpr int AS = C::kAccStages;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* smem_a = smem;                  // stage s at s * kABytes
-    uint8_t* smem_b = smem + S * C::kABytes; // stage s: term j at (s * kTerms + j) * kBBytes
-    uint8_t* smem_sf = smem_b + S * C::kTerms * C::kBBytes;  // stage s: hi / lo scale groups (MX)
-    uint8_t* smem_sfa = smem_sf + S * C::kSFBytes;           // 512-byte A scale atom (all 1.0), MX
+    uint8_t* smem_b = smem + S * C::kABytes; // stage s at s * kBBytes: hi rows [0, NB), lo rows [NB, 2 NB)
+    uint8_t* smem_sf = smem_b + S * C::kBBytes;    // stage s: the B scale block (MX)
+    uint8_t* smem_sfa = smem_sf + S * C::kSFBytes; // 512-byte A scale atom (all 1.0), MX
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem_sfa + (C::kMX ? 512 : 0));
     uint64_t* full = bars;
     uint64_t* empty = bars + S;
@@ -1104,7 +1112,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
     const int warp = threadIdx.x / 32;
     const int lane = threadIdx.x % 32;
-    const int k_chunks = (kG1 ? p.d : p.f) / KB;  // 128-byte K chunks per weight tile row
     const int w_tiles = kG1 ? (2 * p.f) / 256 : p.d / 128;  // weight tiles per expert
     if (warp == 0 && lane == 0) {
         ptx::prefetch_tmap(&tmA8);
@@ -1165,7 +1172,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             int st = 0;
             uint32_t ph = 0;
             bool first = true;
-            const int64_t sf_terms = (p.plane_rows / 128) * (p.f / 128) * 512;  // bytes per scale plane
             for (int t = blockIdx.x; t < total; t += gridDim.x) {
                 TileInfo ti;
                 decode_tile<KIND, NB, KB>(t, p, s_counts, s_offsets, ti);
@@ -1178,18 +1184,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                         ptx::tma_load_4d(&tmA8, &full[st], smem_a + st * C::kABytes, 0, 0, ti.kb0 + kb, wt,
                                          ptx::kEvictFirst);
                     }
-                    uint8_t* b = smem_b + st * C::kTerms * C::kBBytes;
-#pragma unroll
-                    for (int j = 0; j < C::kTerms; ++j)
-                        ptx::tma_load_3d(&tmB8, &full[st], b + j * C::kBBytes, kc, ti.b_row, j, ptx::kEvictLast);
-                    if (C::kMX) {  // the 128-row scale groups of both terms at this K chunk
-                        const uint8_t* g = p.h_sf + ((int64_t)(ti.b_row / 128) * (p.f / 128) + kc / 128) * 512;
-                        ptx::bulk_load(smem_sf + st * C::kSFBytes, g, 512, &full[st]);
-                        ptx::bulk_load(smem_sf + st * C::kSFBytes + 512, g + sf_terms, 512, &full[st]);
-                    }
+                    uint8_t* b = smem_b + st * C::kBBytes;
+                    ptx::tma_load_3d(&tmB8, &full[st], b, kc, ti.b_row, 0, ptx::kEvictLast);
+                    ptx::tma_load_3d(&tmB8, &full[st], b + NB * 128, kc, ti.b_row, 1, ptx::kEvictLast);
+                    if (C::kMX)  // the tile's B scale block at this K chunk
+                        ptx::bulk_load(smem_sf + st * C::kSFBytes,
+                                       p.h_sf + ((int64_t)(ti.b_row / NB) * (p.f / 128) + kc / 128) * C::kSFBytes,
+                                       C::kSFBytes, &full[st]);
                     if (++st == S) { st = 0; ph ^= 1; }
                 }
-                (void)k_chunks;
                 first = false;
             }
         }
@@ -1201,52 +1204,44 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             uint32_t acc_phase = 0;
             const uint32_t sfa = tmem_base + C::kSfaCol;
             if (C::kMX) ptx::tmem_cp_32x128b_x4(sfa, ptx::make_smem_desc_rows16(ptx::smem_u32(smem_sfa)));
+            // hi and lo rows stacked: N = 2 NB (a multiple of 32, as the B scale layout needs)
+            constexpr uint32_t N2 = 2 * NB;
+            const uint32_t idesc = (1u << 4) | ((N2 >> 3) << 17) | ((128u >> 4) << 24);  // D f32, E4M3, K-major
             for (int t = blockIdx.x; t < total; t += gridDim.x) {
                 TileInfo ti;
                 decode_tile<KIND, NB, KB>(t, p, s_counts, s_offsets, ti);
-                // MX: N a multiple of 32 (the block-scale layout covers B rows in groups of 32)
-                const uint32_t n_mma = C::kMX ? (uint32_t)((ti.n_valid + 31) / 32 * 32)
-                                              : (uint32_t)((ti.n_valid + 15) / 16 * 16);
-                // D f32 (bit 4), A = B = E4M3 (format 0), K-major, N >> 3 at 17, M >> 4 at 24
-                const uint32_t idesc = (1u << 4) | ((n_mma >> 3) << 17) | ((128u >> 4) << 24);
-                const uint32_t d_a = tmem_base + acc * 256, d_b = d_a + 128;
-                // B scale columns of this token tile: 32-row group (b_row % 128) / 32 of the atom
-                const uint32_t sfb_grp = (uint32_t)((ti.b_row % 128) / 32);
+                const uint32_t d_a = tmem_base + acc * C::kAccCols, d_b = d_a + N2;
                 ptx::mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
                 ptx::tc_fence_after();
                 for (int kb = 0; kb < ti.nkb; ++kb) {
                     ptx::mbar_wait(&full[st], ph);
                     ptx::tc_fence_after();
                     const uint64_t a1 = ptx::make_smem_desc_sw128(ptx::smem_u32(smem_a + st * C::kABytes));
-                    const uint64_t b0 = ptx::make_smem_desc_sw128(ptx::smem_u32(smem_b + st * C::kTerms * C::kBBytes));
-                    if (C::kMX) {  // this stage's scale groups -> TMEM (ordered before the MMAs below)
+                    const uint64_t b0 = ptx::make_smem_desc_sw128(ptx::smem_u32(smem_b + st * C::kBBytes));
+                    if (C::kMX) {  // this stage's B scales -> TMEM (ordered before the MMAs below)
                         const uint32_t sfs = ptx::smem_u32(smem_sf + st * C::kSFBytes);
                         ptx::tmem_cp_32x128b_x4(tmem_base + C::kSfbCol, ptx::make_smem_desc_rows16(sfs));
-                        ptx::tmem_cp_32x128b_x4(tmem_base + C::kSfbCol + 4, ptx::make_smem_desc_rows16(sfs + 512));
+                        if (NB == 128)
+                            ptx::tmem_cp_32x128b_x4(tmem_base + C::kSfbCol + 4, ptx::make_smem_desc_rows16(sfs + 512));
                     }
 #pragma unroll
                     for (int kk = 0; kk < KB / 32; ++kk) {  // 32 bytes of K per MMA: +2 in the descriptor
-                        const uint32_t init = (kb | kk) ? 1u : 0u;
-#pragma unroll
-                        for (int j = 0; j < C::kTerms; ++j) {  // term j: kBBytes further (>> 4 in the descriptor)
-                            const uint64_t bj = b0 + j * (C::kBBytes >> 4) + 2 * kk;
-                            if (C::kMX) {
-                                // K block kk of the 128-K chunk = byte kk of the scale columns
-                                const uint32_t sel = static_cast<uint32_t>(kk) << 30;
-                                const uint32_t sfb = (tmem_base + C::kSfbCol + 4 * j + sfb_grp) | sel;
-                                ptx::mma_mx_e4m3(d_a, a1 + 2 * kk, bj, ptx::make_idesc_mx_e4m3(128, n_mma, kk, kk),
-                                                 j ? 1u : init, sfa | sel, sfb);
-                            } else {
-                                ptx::mma_e4m3(d_a, a1 + 2 * kk, bj, idesc, j ? 1u : init);
-                                if (kG1) ptx::mma_e4m3(d_b, a1 + (16384 >> 4) + 2 * kk, bj, idesc, j ? 1u : init);
-                            }
+                        const uint32_t acc_in = (kb | kk) ? 1u : 0u;
+                        if (C::kMX) {
+                            // K block kk of the 128-K chunk = byte kk of every scale column
+                            const uint32_t sel = static_cast<uint32_t>(kk) << 30;
+                            ptx::mma_mx_e4m3(d_a, a1 + 2 * kk, b0 + 2 * kk, ptx::make_idesc_mx_e4m3(128, N2, kk, kk),
+                                             acc_in, sfa | sel, (tmem_base + C::kSfbCol) | sel);
+                        } else {
+                            ptx::mma_e4m3(d_a, a1 + 2 * kk, b0 + 2 * kk, idesc, acc_in);
+                            ptx::mma_e4m3(d_b, a1 + (16384 >> 4) + 2 * kk, b0 + 2 * kk, idesc, acc_in);
                         }
                     }
                     ptx::mma_commit(&empty[st]);
                     if (++st == S) { st = 0; ph ^= 1; }
                 }
                 ptx::mma_commit(&tmem_full[acc]);
-                if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+                if (++acc == AS) { acc = 0; acc_phase ^= 1; }
             }
         }
     } else {
@@ -1260,7 +1255,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             decode_tile<KIND, NB, KB>(t, p, s_counts, s_offsets, ti);
             ptx::mbar_wait(&tmem_full[acc], acc_phase);
             ptx::tc_fence_after();
-            const uint32_t tbase = tmem_base + acc * 256 + (static_cast<uint32_t>(q * 32) << 16);
+            // columns [0, NB): the hi term, [NB, 2 NB): the lo term (+ 2 NB: the w3 accumulator)
+            const uint32_t tbase = tmem_base + acc * C::kAccCols + (static_cast<uint32_t>(q * 32) << 16);
             const int nchunks = (ti.n_valid + 15) / 16;
             if (kG1) {
                 const float* rs = row_scale + ti.b_row;
@@ -1268,20 +1264,24 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 const float s1v = sc[r], s3v = sc[128 + r];
                 const int64_t plane = p.plane_rows * p.f;
                 uint8_t* hp = static_cast<uint8_t*>(p.out) + static_cast<int64_t>(ti.b_row) * p.f + ti.m_idx * 128 + r;
-                const int64_t sf_plane = (p.plane_rows / 128) * (p.f / 128) * 512;
+                const int snb = p.sf_nb;
+                const int sfbytes = snb == 128 ? 1024 : 512;
 #pragma unroll 1
                 for (int cc = 0; cc < nchunks; ++cc) {
-                    uint32_t a[16], b[16];
-                    ptx::tmem_ld16(tbase + cc * 16, a);
-                    ptx::tmem_ld16(tbase + 128 + cc * 16, b);
+                    uint32_t a0[16], a1[16], b0[16], b1[16];
+                    ptx::tmem_ld16(tbase + cc * 16, a0);
+                    ptx::tmem_ld16(tbase + NB + cc * 16, a1);
+                    ptx::tmem_ld16(tbase + 2 * NB + cc * 16, b0);
+                    ptx::tmem_ld16(tbase + 3 * NB + cc * 16, b1);
                     ptx::tmem_wait_ld();
-#pragma unroll 4
+#pragma unroll
                     for (int i = 0; i < 16; ++i) {
                         const int n = cc * 16 + i;
                         if (n < ti.n_valid) {  // warp-uniform
                             const float tsn = rs[n];
-                            const float hv = silu_f32(__uint_as_float(a[i]) * (s1v * tsn)) *
-                                             (__uint_as_float(b[i]) * (s3v * tsn));
+                            const float av = __uint_as_float(a0[i]) + __uint_as_float(a1[i]);
+                            const float bv = __uint_as_float(b0[i]) + __uint_as_float(b1[i]);
+                            const float hv = silu_f32(av * (s1v * tsn)) * (bv * (s3v * tsn));
                             // block max of |h| over the warp's 32 ffn columns (bits order == magnitude order)
                             const uint32_t mbits = __reduce_max_sync(0xffffffffu, __float_as_uint(hv) & 0x7FFFFFFFu);
                             const float m = __uint_as_float(mbits);
@@ -1296,12 +1296,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                             const uint8_t lo = f32_to_e4m3((v - e4m3_to_f32(hi)) * 16.f);  // residual exact in fp32
                             hp[static_cast<int64_t>(n) * p.f] = hi;
                             hp[static_cast<int64_t>(n) * p.f + plane] = lo;
-                            if (lane == 0) {
+                            if (lane < 2) {  // lane 0: the hi scale, lane 1: the lo scale (virtual row +snb)
                                 const int64_t row = ti.b_row + n;
-                                const int64_t o = ((row / 128) * (p.f / 128) + ti.m_idx) * 512 + 16 * (row % 32) +
-                                                  4 * ((row % 128) / 32) + q;
-                                p.h_sf[o] = static_cast<uint8_t>(127 - u);           // hi: 2^-u
-                                p.h_sf[o + sf_plane] = static_cast<uint8_t>(123 - u); // lo: 2^-(u+4)
+                                const int v_row = static_cast<int>(row % snb) + lane * snb;
+                                const int64_t o = ((row / snb) * (p.f / 128) + ti.m_idx) * sfbytes + 512 * (v_row / 128) +
+                                                  16 * (v_row % 32) + 4 * ((v_row % 128) / 32) + q;
+                                p.h_sf[o] = static_cast<uint8_t>((lane ? 123 : 127) - u);  // 2^-u, 2^-(u+4)
                             }
                         }
                     }
@@ -1313,14 +1313,16 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                            static_cast<int64_t>(ti.b_row) * p.d + drow;
 #pragma unroll 1
                 for (int cc = 0; cc < nchunks; ++cc) {
-                    uint32_t v[16];
-                    ptx::tmem_ld16(tbase + cc * 16, v);
+                    uint32_t v0[16], v1[16];
+                    ptx::tmem_ld16(tbase + cc * 16, v0);
+                    ptx::tmem_ld16(tbase + NB + cc * 16, v1);
                     ptx::tmem_wait_ld();
                     if (drow < p.d) {
 #pragma unroll
                         for (int i = 0; i < 16; ++i) {
                             const int n = cc * 16 + i;
-                            if (n < ti.n_valid) y[static_cast<int64_t>(n) * p.d] = __uint_as_float(v[i]) * s2v;
+                            if (n < ti.n_valid)
+                                y[static_cast<int64_t>(n) * p.d] = (__uint_as_float(v0[i]) + __uint_as_float(v1[i])) * s2v;
                         }
                     }
                 }
@@ -1328,7 +1330,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(&tmem_empty[acc]);
-            if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+            if (++acc == AS) { acc = 0; acc_phase ^= 1; }
         }
     }
     ptx::pdl_launch_dependents();

@@ -253,7 +253,8 @@ struct moe_ctx {
     // terms with a per-row scale, h as two E4M3 terms with UE8M0 block scales
     float* tok_scale = nullptr;   // [cap] 2^-s of each permuted row
     uint8_t* h8 = nullptr;        // [2][cap][f_local] E4M3 terms of h (w1/w3 epilogue -> w2 GEMM)
-    uint8_t* h_sf = nullptr;      // [2][cap/128][f_local/128][512] their UE8M0 scales (MMA scale layout)
+    uint8_t* h_sf = nullptr;      // [cap/NB][f_local/128][2 NB * 4 B] their UE8M0 scales (GemmParams::h_sf)
+    int fp8_nb2 = 0;              // token tile of this forward's FP8 w2 GEMM (sets the scale layout)
     CUtensorMap tm_h8[3]{};       // h8 planes, box {128, NB}, NB = 32, 64, 128
     CUtensorMap tm_x8[3]{};       // x_perm as [2][cap][d] E4M3 planes, box {128, NB}, NB = 32, 64, 128
     // workspace (device)
@@ -621,6 +622,7 @@ moe_status run_swap_g1(moe_ctx* c, int nbi, const moe_expert_weights* w, cudaStr
             p1.out = c->h8;
             p1.h_sf = c->h_sf;
             p1.plane_rows = c->cap;
+            p1.sf_nb = c->fp8_nb2;  // scale blocks laid out for the w2 GEMM's token tile
             return launch(c, kSlotGemm1, moe_gemm_fp8x_kernel<kG1Swap, NB>, dim3(c->g1_grid_now), dim3(kGemmThreads),
                           (size_t)Fp8xCfg<kG1Swap, NB>::kSmemBytes, st, p1, static_cast<const float*>(w->w13_scale),
                           static_cast<const float*>(c->tok_scale), c->tm_w13, c->tm_x8[nbi]);
@@ -640,6 +642,7 @@ moe_status run_swap_g2(moe_ctx* c, int nbi, const moe_expert_weights* w, int spl
         if (c->fp8) {  // block-scaled 8-bit MMAs on the two E4M3 planes of h
             p2.h_sf = c->h_sf;
             p2.plane_rows = c->cap;
+            p2.sf_nb = NB;
             return launch(c, kSlotGemm2, moe_gemm_fp8x_kernel<kG2Swap, NB>, dim3(c->g2_grid_now), dim3(kGemmThreads),
                           (size_t)Fp8xCfg<kG2Swap, NB>::kSmemBytes, st, p2, static_cast<const float*>(w->w2_scale),
                           static_cast<const float*>(nullptr), c->tm_w2_swap, c->tm_h8[nbi]);
@@ -781,7 +784,7 @@ moe_status run_gemms(moe_ctx* c, GemmPaths gp, int64_t rows_bound, int64_t rows_
     if (c->tune_g1_nb) nb1 = c->tune_g1_nb;
     if (c->tune_g2_nb) nb2 = c->tune_g2_nb;
     if (c->fp8) nb1 = nb2 = std::min(nb1, 128);  // FP8 kernels: token tiles up to 128
-    // experiment knob (env MOE_SWAP_NB_CAP): cap the swap-path token tile below the
+    // tuning.swap_nb_cap: cap the swap-path token tile below the
     // worst-case bound; an expert with more rows then takes several token tiles
     // (device-side tile count: still correct), re-streaming its weights per tile
     // FP8 (fp8x) decode: a 32-token tile while the mean rows per expert is <= 16 (64-token
@@ -795,6 +798,10 @@ moe_status run_gemms(moe_ctx* c, GemmPaths gp, int64_t rows_bound, int64_t rows_
     if (c->swap_nb_cap >= 32) {
         nb1 = std::min(nb1, c->swap_nb_cap);
         nb2 = std::min(nb2, c->swap_nb_cap);
+    }
+    if (c->fp8) {  // the w1/w3 epilogue lays the h scales out for the w2 GEMM's token tile
+        nb2 = nb1;
+        c->fp8_nb2 = nb2;
     }
     // weight tiles re-read by a second token tile of the same expert (rows > NB) should
     // survive in L2 between the passes: evict-normal then, evict-first otherwise (r01
@@ -1362,7 +1369,7 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
     ALLOC(c->tok_scale, sizeof(float) * c->cap);
     if (c->fp8) {
         ALLOC(c->h8, (size_t)2 * c->cap * c->f_local);
-        ALLOC(c->h_sf, (size_t)2 * (c->cap / 128) * (c->f_local / 128) * 512);
+        ALLOC(c->h_sf, (size_t)(c->cap / 32) * (c->f_local / 128) * 512);  // max over NB: 512 B per 32 rows
     }
     ALLOC(c->src_row, sizeof(int32_t) * (c->cap + 512));
     ALLOC(c->h, sizeof(__nv_bfloat16) * c->cap * c->f_local);
@@ -1425,7 +1432,7 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
     if ((e = cudaMemset(c->src_row, 0, sizeof(int32_t) * (c->cap + 512))) != cudaSuccess) return fail_init("memset", e);
     if ((e = cudaMemset(c->h, 0, sizeof(__nv_bfloat16) * c->cap * c->f_local)) != cudaSuccess) return fail_init("memset", e);
     if (c->fp8 && ((e = cudaMemset(c->h8, 0, (size_t)2 * c->cap * c->f_local)) != cudaSuccess ||
-                   (e = cudaMemset(c->h_sf, 0x7F, (size_t)2 * (c->cap / 128) * (c->f_local / 128) * 512)) != cudaSuccess))
+                   (e = cudaMemset(c->h_sf, 0x7F, (size_t)(c->cap / 32) * (c->f_local / 128) * 512)) != cudaSuccess))
         return fail_init("memset", e);
 
     // workspace TMA descriptors
