@@ -312,6 +312,20 @@ MOE_API moe_status moe_loopback_comm_destroy(void* group_or_rank);
  * stream sync + process-group barrier) before any rank calls moe_destroy, since
  * peers load from / store into this rank's region until then.                */
 #define MOE_FLAG_P2P 0x100u
+
+/* ---- NVLink SHARP all-reduce (MOE_FLAG_NVLS).
+ * MOE_PAR_TP with an NCCL communicator from NCCL >= 2.28: moe_init (collective: every
+ * rank of the TP group calls it) allocates a symmetric window with ncclMemAlloc,
+ * registers it (NCCL_WIN_COLL_SYMMETRIC) and creates an NCCL device communicator with
+ * multimem; every forward then ends in ONE kernel that forms this rank's fp32 partial
+ * output, has the NVSwitch sum the ranks' partials (multimem.ld_reduce) for this rank's
+ * column slice, rounds once to bf16 (+ residual) and multicasts the finished slice to
+ * every rank (multimem.st), with device-side LSA barriers in between -- no separate
+ * reduce-scatter / all-gather calls, and the forward stays graph-capturable. The switch
+ * sums in its own order (fp32): results equal the collective path's up to fp32 rounding.
+ * moe_init returns MOE_ERR_UNSUPPORTED when the process's NCCL has no device API or the
+ * group has no multicast object (NVLS needs >= 2 GPUs on one NVSwitch domain).    */
+#define MOE_FLAG_NVLS 0x200u
 #define MOE_P2P_HANDLE_BYTES 128
 MOE_API moe_status moe_p2p_handle(moe_ctx* ctx, void* handle_out);
 MOE_API moe_status moe_p2p_connect(moe_ctx* ctx, const void* handles, int32_t world);

@@ -34,6 +34,7 @@ MOE_FLAG_EP_EXACT = 0x20
 MOE_FLAG_FP8_WEIGHTS = 0x40
 MOE_FLAG_GATHER = 0x80
 MOE_FLAG_P2P = 0x100
+MOE_FLAG_NVLS = 0x200
 P2P_HANDLE_BYTES = 128
 NUM_KERNEL_SLOTS = 8
 KERNEL_SLOTS = ("router", "permute", "gemm1_w13_swiglu", "gemm2_w2", "combine", "dispatch", "exchange", "pack")

@@ -22,8 +22,23 @@ NVCC_FLAGS = [
 ]
 
 
+def nccl_include():
+    """NCCL 2.28's headers (device API: symmetric windows, LSA barriers, multimem) shipped
+    with the nvidia-nccl wheel torch uses; None if absent (nvls.cu then builds a stub)."""
+    try:
+        import nvidia
+        for base in nvidia.__path__:
+            inc = os.path.join(base, "nccl", "include")
+            if os.path.exists(os.path.join(inc, "nccl_device.h")):
+                return inc
+    except ImportError:
+        pass
+    return None
+
+
 def sources():
     return sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cuh")) +
+                  glob.glob(os.path.join(CSRC, "*.h")) +
                   [os.path.join(ROOT, "include", "moe.h")])
 
 
@@ -40,8 +55,10 @@ def build(force: bool = False, verbose: bool = False, out: str = None, defines=(
     if not force and out is None and not needs_build():
         return LIB
     tmp = lib + f".tmp{os.getpid()}"
-    cmd = [NVCC, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-I", os.path.join(ROOT, "include"), "-o", tmp,
-           os.path.join(CSRC, "moe.cu"), "-ldl"]
+    inc = nccl_include()
+    nccl_flags = ["-I", inc, "-DMOE_HAVE_NCCL_DEVICE"] if inc else []
+    cmd = [NVCC, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-I", os.path.join(ROOT, "include"), *nccl_flags,
+           "-o", tmp, os.path.join(CSRC, "moe.cu"), os.path.join(CSRC, "nvls.cu"), "-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     log = os.path.join(PKG, "build.log")
     with open(log, "w") as fh:

@@ -28,6 +28,7 @@
 #include "../../include/moe.h"
 #include "gemm_sm100.cuh"
 #include "kernels.cuh"
+#include "nvls.h"
 
 using namespace moe;
 
@@ -299,6 +300,8 @@ struct moe_ctx {
     uint64_t swap_w_hint = 0;    // L2 policy of the decode GEMMs' weight stream (set per forward)
     int swap_hint_mode = 0;      // tuning.weight_hint: 0 auto, 1 evict-first, 2 normal, 3 evict-last
     bool host_zero_copy = true;  // moe_forward_host: combine writes pinned output directly (tuning.host_stage: copy)
+    moe_nvls::State* nvls = nullptr;  // MOE_FLAG_NVLS: symmetric window + device communicator (nvls.cu)
+    int nvls_blocks = 0;              // grid bound of the fused TP combine (its LSA barrier count)
     float* tp_partial = nullptr;                               // TP: fp32 partial [max_T, d]
     float* tp_scatter = nullptr;                               // TP: reduce-scatter result
     // EP staging
@@ -536,6 +539,8 @@ moe_status validate_cfg(const moe_config* cfg, moe_ctx* c) {
         return fail(c, MOE_ERR_UNSUPPORTED, "MOE_FLAG_P2P supports MOE_PAR_EP and MOE_PAR_TP");
     if (p2p && cfg->par == MOE_PAR_NONE) return fail(c, MOE_ERR_INVALID, "MOE_FLAG_P2P needs MOE_PAR_EP or MOE_PAR_TP");
     if (p2p && G > 32) return fail(c, MOE_ERR_UNSUPPORTED, "MOE_FLAG_P2P supports groups of at most 32 ranks");
+    if ((cfg->flags & MOE_FLAG_NVLS) && (cfg->par != MOE_PAR_TP || p2p || !cfg->nccl_comm))
+        return fail(c, MOE_ERR_INVALID, "MOE_FLAG_NVLS needs MOE_PAR_TP with an NCCL communicator (no MOE_FLAG_P2P)");
     if (!p2p && (cfg->par == MOE_PAR_EP || cfg->par == MOE_PAR_HYBRID) && !cfg->nccl_comm)
         return fail(c, MOE_ERR_INVALID, "nccl_comm (EP group) required");
     if (!p2p && cfg->par == MOE_PAR_TP && G > 1 && !cfg->nccl_comm) return fail(c, MOE_ERR_INVALID, "nccl_comm required");
@@ -783,6 +788,7 @@ moe_status run_gemms(moe_ctx* c, GemmPaths gp, int64_t rows_bound, int64_t rows_
     }
     if (c->tune_g1_nb) nb1 = c->tune_g1_nb;
     if (c->tune_g2_nb) nb2 = c->tune_g2_nb;
+    if (c->gather_now) nb1 = std::min(nb1, 128);  // tile::gather4 token fetch: up to 128 rows (4 per lane)
     if (c->fp8) nb1 = nb2 = std::min(nb1, 128);  // FP8 kernels: token tiles up to 128
     // tuning.swap_nb_cap: cap the swap-path token tile below the
     // worst-case bound; an expert with more rows then takes several token tiles
@@ -1427,6 +1433,18 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
         ALLOC(c->d_peers, sizeof(uint8_t*) * c->p2p_world);
     }
 #undef ALLOC
+    if (cfg->flags & MOE_FLAG_NVLS) {
+        if (as_loopback(cfg->nccl_comm)) {
+            moe_destroy(c);
+            return fail(nullptr, MOE_ERR_INVALID, "MOE_FLAG_NVLS needs a real NCCL communicator");
+        }
+        char nerr[256] = {0};
+        c->nvls_blocks = 2 * c->num_sms;
+        if (moe_nvls::setup(cfg->nccl_comm, c->max_T, c->d, c->nvls_blocks, &c->nvls, nerr, sizeof(nerr))) {
+            moe_destroy(c);
+            return fail(nullptr, MOE_ERR_UNSUPPORTED, "%s", nerr);
+        }
+    }
     if ((e = cudaMemset(c->done, 0, sizeof(unsigned int) * 4)) != cudaSuccess) return fail_init("memset", e);
     if ((e = cudaMemset(c->x_perm, 0, sizeof(__nv_bfloat16) * c->cap * c->d)) != cudaSuccess) return fail_init("memset", e);
     if ((e = cudaMemset(c->src_row, 0, sizeof(int32_t) * (c->cap + 512))) != cudaSuccess) return fail_init("memset", e);
@@ -1511,6 +1529,10 @@ moe_status moe_destroy(moe_ctx* c) {
                     c->ep_ridx, c->ep_rpos, c->ep_rw, c->ep_rcounts, c->lb_scratch, c->d_peers, c->src_row,
                     c->tok_scale, c->h8, c->h_sf};
     for (void* p : c->p2p_opened) cudaIpcCloseMemHandle(p);
+    if (c->nvls) {
+        cudaDeviceSynchronize();  // no fused combine still reads / writes the window
+        moe_nvls::destroy(c->nvls);
+    }
     if (c->sym) {
         cudaDeviceSynchronize();  // peers' stores into this region have drained (same-process group)
         cudaFree(c->sym);
@@ -1834,7 +1856,7 @@ moe_status forward_impl(moe_ctx* c, const void* tokens, int32_t T, const void* r
     if (c->cfg.par == MOE_PAR_EP || c->cfg.par == MOE_PAR_HYBRID) return forward_ep(c, tokens, T, router_w, out, aux, st);
     if (T == 0) return MOE_OK;  // TP: every rank passes the same T, so all skip together
 
-    const bool tp = c->cfg.par == MOE_PAR_TP && c->G > 1;
+    const bool tp = (c->cfg.par == MOE_PAR_TP && c->G > 1) || c->nvls;  // NVLS: the fused path at any G
     RouteSpec r;
     r.x = tokens; r.T = T; r.k = c->k;
     r.router_w = router_w; r.in_idx = in_idx; r.in_w = in_w;
@@ -1878,6 +1900,20 @@ moe_status forward_impl(moe_ctx* c, const void* tokens, int32_t T, const void* r
         cp.out = static_cast<__nv_bfloat16*>(out);
         cp.out_f32 = aux ? aux->out_f32 : nullptr;
         return launch(c, kSlotCombine, moe_combine_kernel, dim3((unsigned)((c->d + 4095) / 4096 * (int64_t)T)), dim3(256), 0, st, cp);
+    }
+    if (c->nvls) {
+        // ---- TP over NVLink SHARP (MOE_FLAG_NVLS, nvls.cu): combine, switch-side fp32 sum,
+        // one rounding and the all-gather in ONE kernel (multimem on a symmetric window)
+        moe_nvls::CombineArgs na{c->y, c->split_stride, splits, c->pos, c->topk_w,
+                                 residual ? static_cast<const __nv_bfloat16*>(tokens) : nullptr, T, c->d, c->k,
+                                 static_cast<__nv_bfloat16*>(out), aux ? aux->out_f32 : nullptr};
+        StepTimer tn(c, kSlotCombine, st);
+        cudaError_t ce = moe_nvls::launch_tp_combine(c->nvls, na, std::min(T, c->nvls_blocks),
+                                                     !(c->cfg.flags & MOE_FLAG_NO_PDL), st);
+        if (ce != cudaSuccess) return fail(c, MOE_ERR_CUDA, "NVLS combine launch failed: %s", cudaGetErrorString(ce));
+        c->launch_count++;
+        tn.done();
+        return MOE_OK;
     }
     // ---- TP: fp32 partial of this rank's ffn slice -> fp32 reduce-scatter ->
     // one bf16 rounding (+ residual) -> bf16 all-gather (R7: single rounding)

@@ -2,8 +2,8 @@
 torch.distributed.run, one process per GPU, NCCL for the collectives): the EP, TP
 and hybrid EP x TP variants over REAL NCCL communicators (libmoe's own, built from
 the process group with nccl_comm_from_process_group / nccl_hybrid_comms), capacity
-and exact-count EP exchanges, and the peer-memory (MOE_FLAG_P2P) transport across
-GPUs. Writes this rank's outputs per case to <outdir>/rank<r>.pt."""
+and exact-count EP exchanges, the peer-memory (MOE_FLAG_P2P) transport across
+GPUs and the NVLink SHARP TP all-reduce fused into the combine (MOE_FLAG_NVLS). Writes this rank's outputs per case to <outdir>/rank<r>.pt."""
 import os
 import sys
 
@@ -25,6 +25,7 @@ def cases(G):
     yield "tp", dict(par=moe.MOE_PAR_TP, flags=0)
     yield "ep_p2p", dict(par=moe.MOE_PAR_EP, flags=moe.MOE_FLAG_P2P)
     yield "tp_p2p", dict(par=moe.MOE_PAR_TP, flags=moe.MOE_FLAG_P2P)
+    yield "tp_nvls", dict(par=moe.MOE_PAR_TP, flags=moe.MOE_FLAG_NVLS)
     if G % 2 == 0:
         yield "hybrid", dict(par=moe.MOE_PAR_HYBRID, flags=0, tp=2)
 

@@ -126,3 +126,19 @@ def test_struct_layout_matches_header(tmp_path):
         assert got[(name, "size")] == ctypes.sizeof(py), name
         for fname, _ in py._fields_:
             assert got[(name, fname)] == getattr(py, fname).offset, (name, fname)
+
+
+def test_nvls_flag_validation():
+    """MOE_FLAG_NVLS (TP all-reduce over NVLink SHARP) is a TP + NCCL-communicator option."""
+    import paper_2408_00008_b200 as moe
+    for bad in (moe.make_config(4096, 14336, 8, 2, 64, par=moe.MOE_PAR_EP, world_size=2, nccl_comm=1,
+                                flags=moe.MOE_FLAG_NVLS),
+                moe.make_config(4096, 14336, 8, 2, 64, par=moe.MOE_PAR_TP, world_size=2, flags=moe.MOE_FLAG_NVLS),
+                moe.make_config(4096, 14336, 8, 2, 64, par=moe.MOE_PAR_TP, world_size=2,
+                                flags=moe.MOE_FLAG_NVLS | moe.MOE_FLAG_P2P),
+                moe.make_config(4096, 14336, 8, 2, 64, flags=moe.MOE_FLAG_NVLS)):
+        with pytest.raises(moe.MoEError) as ei:
+            moe.moe_packed_sizes(bad)
+        assert ei.value.status == moe.MOE_ERR_INVALID
+    moe.moe_packed_sizes(moe.make_config(4096, 14336, 8, 2, 64, par=moe.MOE_PAR_TP, world_size=2, nccl_comm=1,
+                                         flags=moe.MOE_FLAG_NVLS))

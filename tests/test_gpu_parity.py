@@ -736,6 +736,33 @@ def test_nccl_world1(moe, par):
     moe.moe_nccl_comm_destroy(comm)
 
 
+def test_nvls_world1(moe):
+    """MOE_FLAG_NVLS on a 1-rank NCCL communicator: NVLink SHARP needs a multicast object
+    over >= 2 GPUs, so moe_init must refuse cleanly with MOE_ERR_UNSUPPORTED (nothing
+    leaks: a plain TP context on the same communicator still works afterwards); if the
+    platform does give a 1-GPU multicast object, the fused path must pass the oracle.
+    The >= 2-GPU run is test_real_nccl_multigpu's tp_nvls case."""
+    uid = moe.moe_nccl_unique_id()
+    comm = moe.moe_nccl_comm_init(uid, 1, 0, torch.cuda.current_device())
+    inp = _inputs(synth.MoEShape(T=40, d=128, f=256, E=4, k=2), 92)
+    host = to_host_inputs(inp)
+    try:
+        blk = moe.MoEBlock(inp["wg"], inp["w1"], inp["w3"], inp["w2"], top_k=2, max_tokens=40, par=moe.MOE_PAR_TP,
+                           world_size=1, rank=0, nccl_comm=comm, flags=moe.MOE_FLAG_NVLS)
+    except moe.MoEError as ex:
+        assert ex.status == moe.MOE_ERR_UNSUPPORTED and "NVLS" in str(ex), str(ex)
+        print("NVLS at world 1:", ex)
+        blk = None
+    if blk is not None:
+        check_forward(GpuRun(blk, inp["x"]), host, 2)
+        blk.close()
+    plain = moe.MoEBlock(inp["wg"], inp["w1"], inp["w3"], inp["w2"], top_k=2, max_tokens=40, par=moe.MOE_PAR_TP,
+                         world_size=1, rank=0, nccl_comm=comm)
+    check_forward(GpuRun(plain, inp["x"]), host, 2)
+    plain.close()
+    moe.moe_nccl_comm_destroy(comm)
+
+
 # ---------------------------------------------------------------- C5: layer stack with residual
 def _stack_aux(L, T, d, k):
     return [{"topk_idx": torch.empty(T, k, dtype=torch.int32, device="cuda"),
