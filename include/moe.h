@@ -130,9 +130,7 @@ typedef struct moe_tuning {
                                copy it back (0: pinned output written directly)             */
     int32_t g1_nb;          /* force the swap-AB token tile of the w1/w3 GEMM: 32/64/128/192 (0: auto) */
     int32_t g2_nb;          /* same for the w2 GEMM, also 256 (0: auto)                        */
-    int32_t xpf_mb;         /* decode cross-GEMM L2 prefetch of w2 weights while a single-wave
-                               w1/w3 GEMM runs (EP / TP ranks): MB budget (0: 64; < 0: off) */
-    int32_t reserved[10];   /* must be zero                                                  */
+    int32_t reserved[11];   /* must be zero                                                  */
 } moe_tuning;
 
 typedef struct {

@@ -69,20 +69,6 @@ struct GemmParams {
     // kernel reads counts / offsets after griddepcontrol.wait (it may launch before the
     // router has finished).
     int32_t spec_l2;
-    // Cross-GEMM L2 prefetch (decode, when the w1/w3 GEMM is one wave on fewer CTAs than
-    // SMs -- EP / TP ranks: moe.cu xpf): the w1/w3 GEMM (kG1Swap) triggers its dependents
-    // right after its prologue, so w2 GEMM CTAs start on the SMs it leaves idle, and
-    // counts its finished CTAs in xpf_done. A w2 GEMM CTA (kG2Swap) that finds the w1/w3
-    // GEMM still running takes tickets (xpf_ticket) for w2 units -- highest unit first, the
-    // ones the CTAs launched last will own -- and prefetches their weights into L2 until
-    // the w1/w3 GEMM is done or xpf_units are covered; HBM is under-used by a short
-    // single-wave stream (scripts/exp/small_stream.cu: 4.8 TB/s at 112 x 2 MB). The last
-    // w2 CTA to finish resets the three counters (xpf_fin) for the next forward.
-    unsigned int* xpf_done;   // kG1Swap: increment at exit; kG2Swap: read (nullable = off)
-    unsigned int* xpf_ticket;
-    unsigned int* xpf_fin;
-    int32_t xpf_grid1;        // kG2Swap: the w1/w3 GEMM's grid
-    int32_t xpf_units;        // kG2Swap: units eligible for the prefetch (L2 budget)
 };
 
 // 4D coordinates of rows [row, row + box) of expert e at K offset kc in a tiled weight map
@@ -311,7 +297,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_base_slot;
-    if (KIND == kG1Swap && p.xpf_done) ptx::pdl_launch_dependents();  // w2 CTAs may take idle SMs now
 
     int total = 0;
     for (int e = 0; e < p.E; ++e) total += tiles_of<KIND, NB>(s_counts[e], p);
@@ -330,20 +315,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         int stage = 0;
         uint32_t phase = 0;
         int pre = 0;  // k-blocks of the first tile whose weight loads precede the wait
-        if (KIND == kG2Swap && p.xpf_done && lane == 0) {
-            // cross-GEMM L2 prefetch while the w1/w3 GEMM still runs (see GemmParams)
-            const int lim = min(total, p.xpf_units);
-            while (*reinterpret_cast<volatile unsigned int*>(p.xpf_done) < (unsigned)p.xpf_grid1) {
-                const int u = (int)atomicAdd(p.xpf_ticket, 1u);
-                if (u >= lim) break;
-                TileInfo tu;
-                decode_tile<KIND, NB>(total - 1 - u, p, s_counts, s_offsets, tu);
-                for (int kb = 0; kb < tu.nkb; ++kb) {
-                    const WCoord w = wcoord(p, (tu.kb0 + kb) * kBK, tu.a_row, tu.e);
-                    ptx::tma_prefetch_l2_4d(&tmA, 0, w.c1, w.c2, w.c3);
-                }
-            }
-        }
         if (C::kSwap && MOE_PDL_PREFETCH > 0 && !spec) {
             if ((int)blockIdx.x < total) {
                 TileInfo t0;
@@ -553,15 +524,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     if (warp == 1) {
         ptx::tc_fence_after();
         ptx::tmem_dealloc(tmem_base, C::kAccStages * C::kAccCols);
-    }
-    if (p.xpf_done && threadIdx.x == 0) {
-        if (KIND == kG1Swap) {
-            atomicAdd(p.xpf_done, 1u);
-        } else if (KIND == kG2Swap && atomicAdd(p.xpf_fin, 1u) == gridDim.x - 1) {
-            *p.xpf_done = 0u;  // every CTA of this grid has read xpf_done: ready for the next forward
-            *p.xpf_ticket = 0u;
-            *p.xpf_fin = 0u;
-        }
     }
 }
 

@@ -247,11 +247,6 @@ struct moe_ctx {
     int pair_nblk = 2;
     int swap_nb_cap = 0;      // cap of the swap-path token tile (tuning; see run_gemms)
     int tune_g1_nb = 0, tune_g2_nb = 0;  // forced swap-path token tiles (tuning g1_nb / g2_nb; 0 = auto)
-    // cross-GEMM L2 prefetch (GemmParams::xpf_*): MB of w2 weights early w2 CTAs may prefetch
-    // while a single-wave w1/w3 GEMM still streams (0 = off; tuning.xpf_mb)
-    int xpf_mb = 64;
-    bool xpf_now = false;
-    unsigned int* xpf_ctr = nullptr;  // [3] done / ticket / finish counters (zero between forwards)
     // CUDA-core router (2 tokens / block, 32 blocks at T = 64) for T <= this.
     // r01 64-token decode, interleaved: 0.4335 vs 0.4312 ms with the mma.sync router (4 blocks)
     int router_cc_max_T = 0;
@@ -557,7 +552,7 @@ moe_status validate_cfg(const moe_config* cfg, moe_ctx* c) {
     for (int i = 0; i < 2; ++i)
         if (cfg->reserved[i]) return fail(c, MOE_ERR_INVALID, "reserved fields must be zero");
     if (const moe_tuning* tu = cfg->tuning) {
-        for (int i = 0; i < 10; ++i)
+        for (int i = 0; i < 11; ++i)
             if (tu->reserved[i]) return fail(c, MOE_ERR_INVALID, "tuning.reserved fields must be zero");
         if (tu->g1_swap_rows < 0 || tu->g2_swap_rows < 0 || tu->g1_grid < 0 || tu->g2_grid < 0 ||
             tu->swap_nb_cap < 0 || tu->router_cc_max_T < 0 || tu->pair_order < 0)
@@ -638,7 +633,6 @@ moe_status run_swap_g1(moe_ctx* c, int nbi, const moe_expert_weights* w, cudaStr
                           static_cast<const float*>(c->tok_scale), c->tm_w13, c->tm_x8[nbi]);
         }
     if (c->spec_now) p1.spec_l2 = c->spec_l2;
-    if (c->xpf_now) p1.xpf_done = c->xpf_ctr;
     return launch_gemm<kG1Swap, NB>(c, kSlotGemm1, p1, c->tm_w13, c->tm_x_swap[nbi],
                                     c->g1_grid_now, st);
 }
@@ -658,14 +652,6 @@ moe_status run_swap_g2(moe_ctx* c, int nbi, const moe_expert_weights* w, int spl
                           (size_t)Fp8xCfg<kG2Swap, NB>::kSmemBytes, st, p2, static_cast<const float*>(w->w2_scale),
                           static_cast<const float*>(nullptr), c->tm_w2_swap, c->tm_h8[nbi]);
         }
-    if (c->xpf_now) {
-        p2.xpf_done = c->xpf_ctr;
-        p2.xpf_ticket = c->xpf_ctr + 1;
-        p2.xpf_fin = c->xpf_ctr + 2;
-        p2.xpf_grid1 = c->g1_grid_now;
-        const int64_t unit_bytes = 128LL * (c->f_local / std::max(1, splits)) * 2;
-        p2.xpf_units = (int)std::min<int64_t>(1 << 30, ((int64_t)c->xpf_mb << 20) / std::max<int64_t>(1, unit_bytes));
-    }
     return launch_gemm<kG2Swap, NB>(c, kSlotGemm2, p2, c->tm_w2_swap, c->tm_h_swap[nbi],
                                     c->g2_grid_now, st);
 }
@@ -858,13 +844,6 @@ moe_status run_gemms(moe_ctx* c, GemmPaths gp, int64_t rows_bound, int64_t rows_
             const int64_t U1 = (int64_t)c->E_local * wt, w1 = (U1 + ns - 1) / ns;
             c->g1_grid_now = (int)std::min<int64_t>(ns, (U1 + w1 - 1) / w1);
         }
-    }
-    {
-        // cross-GEMM L2 prefetch (GemmParams::xpf_*): only where the w1/w3 GEMM is one short
-        // wave leaving SMs idle (one unit per CTA: EP / TP ranks, e.g. 112 units on 112 CTAs)
-        const int64_t U1 = (int64_t)c->E_local * (c->f_local / 128);
-        c->xpf_now = c->xpf_mb > 0 && gp.swap1 && gp.swap2 && !c->fp8 && !c->gather_now && need <= nb1 &&
-                     U1 <= c->g1_grid_now && c->g1_grid_now < c->num_sms;
     }
     if (gp.swap1) {
         const int i1 = nb1 == 32 ? 0 : nb1 == 64 ? 1 : nb1 == 128 ? 2 : 4;
@@ -1332,7 +1311,6 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
         if (tu->pair_nblk) c->pair_nblk = tu->pair_nblk == 1 ? 1 : 2;
         c->swap_nb_cap = tu->swap_nb_cap;
         c->tune_g1_nb = tu->g1_nb;
-        if (tu->xpf_mb) c->xpf_mb = std::max(0, tu->xpf_mb);
         c->tune_g2_nb = tu->g2_nb;
         c->router_cc_max_T = tu->router_cc_max_T;
         if (tu->g1_swap_rows) c->swap_rows_per_expert = tu->g1_swap_rows;
@@ -1393,7 +1371,6 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
     ALLOC(c->counts, sizeof(int32_t) * 64);
     ALLOC(c->offsets, sizeof(int32_t) * 64);
     ALLOC(c->done, sizeof(unsigned int) * 4);
-    ALLOC(c->xpf_ctr, sizeof(unsigned int) * 4);
     ALLOC(c->x_perm, sizeof(__nv_bfloat16) * c->cap * c->d);
     ALLOC(c->tok_scale, sizeof(float) * c->cap);
     if (c->fp8) {
@@ -1469,7 +1446,6 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
         }
     }
     if ((e = cudaMemset(c->done, 0, sizeof(unsigned int) * 4)) != cudaSuccess) return fail_init("memset", e);
-    if ((e = cudaMemset(c->xpf_ctr, 0, sizeof(unsigned int) * 4)) != cudaSuccess) return fail_init("memset", e);
     if ((e = cudaMemset(c->x_perm, 0, sizeof(__nv_bfloat16) * c->cap * c->d)) != cudaSuccess) return fail_init("memset", e);
     if ((e = cudaMemset(c->src_row, 0, sizeof(int32_t) * (c->cap + 512))) != cudaSuccess) return fail_init("memset", e);
     if ((e = cudaMemset(c->h, 0, sizeof(__nv_bfloat16) * c->cap * c->f_local)) != cudaSuccess) return fail_init("memset", e);
@@ -1547,7 +1523,7 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
 moe_status moe_destroy(moe_ctx* c) {
     if (!c) return MOE_OK;
     cudaSetDevice(c->device);
-    void* bufs[] = {c->topk_idx, c->topk_w, c->pos, c->blockcount, c->blockoff, c->counts, c->offsets, c->done, c->xpf_ctr,
+    void* bufs[] = {c->topk_idx, c->topk_w, c->pos, c->blockcount, c->blockoff, c->counts, c->offsets, c->done,
                     c->x_perm, c->h, c->y, c->stage_in, c->stage_out, c->tp_partial, c->tp_scatter, c->ep_send,
                     c->ep_recv, c->ep_ysend, c->ep_yrecv, c->ep_meta_send, c->ep_meta_recv,
                     c->ep_ridx, c->ep_rpos, c->ep_rw, c->ep_rcounts, c->lb_scratch, c->d_peers, c->src_row,
