@@ -130,7 +130,10 @@ typedef struct moe_tuning {
                                copy it back (0: pinned output written directly)             */
     int32_t g1_nb;          /* force the swap-AB token tile of the w1/w3 GEMM: 32/64/128/192 (0: auto) */
     int32_t g2_nb;          /* same for the w2 GEMM, also 256 (0: auto)                        */
-    int32_t reserved[11];   /* must be zero                                                  */
+    int32_t pair_hints;     /* prefill CTA-pair L2 policies, 2 bits each (0 evict-normal, 1 evict-first,
+                               2 evict-last): bits 0-1 w1/w3 tokens, 2-3 w1/w3 weights, 4-5 w2 h,
+                               6-7 w2 weights (0: all evict-normal)                          */
+    int32_t reserved[10];   /* must be zero                                                  */
 } moe_tuning;
 
 typedef struct {

@@ -247,6 +247,7 @@ struct moe_ctx {
     int pair_nblk = 2;
     int swap_nb_cap = 0;      // cap of the swap-path token tile (tuning; see run_gemms)
     int tune_g1_nb = 0, tune_g2_nb = 0;  // forced swap-path token tiles (tuning g1_nb / g2_nb; 0 = auto)
+    int pair_hints = 0;                  // prefill L2 policies (tuning.pair_hints; see pair_hint())
     // CUDA-core router (2 tokens / block, 32 blocks at T = 64) for T <= this.
     // r01 64-token decode, interleaved: 0.4335 vs 0.4312 ms with the mma.sync router (4 blocks)
     int router_cc_max_T = 0;
@@ -552,7 +553,7 @@ moe_status validate_cfg(const moe_config* cfg, moe_ctx* c) {
     for (int i = 0; i < 2; ++i)
         if (cfg->reserved[i]) return fail(c, MOE_ERR_INVALID, "reserved fields must be zero");
     if (const moe_tuning* tu = cfg->tuning) {
-        for (int i = 0; i < 11; ++i)
+        for (int i = 0; i < 10; ++i)
             if (tu->reserved[i]) return fail(c, MOE_ERR_INVALID, "tuning.reserved fields must be zero");
         if (tu->g1_swap_rows < 0 || tu->g2_swap_rows < 0 || tu->g1_grid < 0 || tu->g2_grid < 0 ||
             tu->swap_nb_cap < 0 || tu->router_cc_max_T < 0 || tu->pair_order < 0)
@@ -755,6 +756,12 @@ GemmPaths gemm_paths(const moe_ctx* c, int64_t rows_expected) {
 // rows_bound: upper bound of the rows of any one local expert (picks the swap-path
 // token tile NB so one tile covers the whole expert at decode); rows_total: bound
 // of all permuted rows (sizes the split-K partial buffers).
+// L2 policy of field i (2 bits) of tuning.pair_hints: 0 evict-normal, 1 evict-first, 2 evict-last.
+uint64_t pair_hint(int hints, int i) {
+    const int v = (hints >> (2 * i)) & 3;
+    return v == 1 ? ptx::kEvictFirst : v == 2 ? ptx::kEvictLast : ptx::kEvictNormal;
+}
+
 // Smallest supported swap-AB token tile >= n (GEMM1: 32, 64, 128, 192; GEMM2 adds 256).
 int swap_nb_ceil(int n, bool g2) {
     if (n <= 32) return 32;
@@ -857,7 +864,7 @@ moe_status run_gemms(moe_ctx* c, GemmPaths gp, int64_t rows_bound, int64_t rows_
         const int64_t mt_max = rows_total / 256 + c->E_local;
         const int g1 = (int)std::min<int64_t>(ncl, mt_max * ((c->f_local / 128 + nblk - 1) / nblk));
         GemmParams p1{c->counts, c->offsets, c->E_local, c->d, c->f_local, 1, c->h, 0, r1, b1,
-                      ptx::kEvictNormal, ptx::kEvictNormal, c->gather_now ? c->src_row : nullptr};
+                      pair_hint(c->pair_hints, 0), pair_hint(c->pair_hints, 1), c->gather_now ? c->src_row : nullptr};
         p1.w_tr = 256;
         p1.w_nt = c->w13_nt;
         const CUtensorMap& ta = c->gather_now ? c->tm_src : c->tm_x_tiled;
@@ -914,7 +921,8 @@ moe_status run_gemms(moe_ctx* c, GemmPaths gp, int64_t rows_bound, int64_t rows_
         const int64_t mt_max = rows_total / 256 + c->E_local;
         const int g2 = (int)std::min<int64_t>(ncl, mt_max * (((c->d + 255) / 256 + nblk - 1) / nblk));
         GemmParams p2{c->counts, c->offsets, c->E_local, c->d, c->f_local, 1, c->y, 0, r2,
-                      nblk == 2 && !c->pair_tune ? std::max(1, b2 / 2) : b2, ptx::kEvictNormal, ptx::kEvictNormal};
+                      nblk == 2 && !c->pair_tune ? std::max(1, b2 / 2) : b2, pair_hint(c->pair_hints, 2),
+                      pair_hint(c->pair_hints, 3)};
         p2.w_tr = 128;
         p2.w_nt = c->w2_nt;
         s = nblk == 2 ? launch_gemm_pair<kG2Pair, 2>(c, kSlotGemm2, p2, c->tm_h_tiled, c->tm_w2_swap, c->tm_y_store, g2, st)
@@ -1311,6 +1319,7 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
         if (tu->pair_nblk) c->pair_nblk = tu->pair_nblk == 1 ? 1 : 2;
         c->swap_nb_cap = tu->swap_nb_cap;
         c->tune_g1_nb = tu->g1_nb;
+        c->pair_hints = tu->pair_hints;
         c->tune_g2_nb = tu->g2_nb;
         c->router_cc_max_T = tu->router_cc_max_T;
         if (tu->g1_swap_rows) c->swap_rows_per_expert = tu->g1_swap_rows;

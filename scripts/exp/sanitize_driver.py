@@ -72,7 +72,9 @@ if __name__ == "__main__":
     single(small, 0x2 | moe.MOE_FLAG_GATHER)  # gather4, swap
     single(small, 0x4 | moe.MOE_FLAG_GATHER)  # gather4, pair
     single(synth.MoEShape(T=64, d=1024, f=2560, E=8, k=2), 0x2)  # speculative L2 prefetch, auto grids
-    single(synth.MoEShape(T=32, d=256, f=512, E=4, k=2), moe.MOE_FLAG_FP8_WEIGHTS)
+    single(synth.MoEShape(T=32, d=256, f=512, E=4, k=2), moe.MOE_FLAG_FP8_WEIGHTS)   # FP8, block-scaled w2
+    single(synth.MoEShape(T=200, d=256, f=512, E=4, k=2), moe.MOE_FLAG_FP8_WEIGHTS, {"swap_nb_cap": 32})
+    single(synth.MoEShape(T=600, d=256, f=512, E=8, k=2), 0x2)   # statistical token tile 192 (T=575-like)
     for par in ("ep", "tp"):
         for p2p in (False, True):
             group(par, 2, p2p)

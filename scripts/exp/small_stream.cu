@@ -9,7 +9,7 @@
 #include <cstdint>
 __device__ __forceinline__ uint32_t su(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 constexpr int S = 6, STAGE = 32768;
-__global__ void __launch_bounds__(64, 1) k_stream(const uint8_t* base, int64_t per_cta, float* sink) {
+__global__ void __launch_bounds__(64, 1) k_stream(const uint8_t* base, int64_t per_cta, float* sink, int interleave) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     __shared__ uint64_t full[S];
@@ -19,7 +19,10 @@ __global__ void __launch_bounds__(64, 1) k_stream(const uint8_t* base, int64_t p
     }
     __syncthreads();
     if (threadIdx.x != 0) return;
-    const uint8_t* src = base + blockIdx.x * per_cta;
+    // contiguous: CTA i owns bytes [i * per_cta, (i+1) * per_cta); interleaved: CTA i reads
+    // chunks i, i + G, i + 2G, ... (the CTAs sweep one region together)
+    const uint8_t* src = interleave ? base + blockIdx.x * (int64_t)STAGE : base + blockIdx.x * per_cta;
+    const int64_t step = interleave ? (int64_t)gridDim.x * STAGE : STAGE;
     const int64_t n = per_cta / STAGE;
     int64_t issued = 0, done = 0;
     uint32_t acc = 0;
@@ -27,7 +30,7 @@ __global__ void __launch_bounds__(64, 1) k_stream(const uint8_t* base, int64_t p
         const int st = issued % S;
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su(&full[st])), "r"(STAGE));
         asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                     ::"r"(su(smem + st * STAGE)), "l"(src + issued * STAGE), "r"(STAGE), "r"(su(&full[st])) : "memory");
+                     ::"r"(su(smem + st * STAGE)), "l"(src + issued * step), "r"(STAGE), "r"(su(&full[st])) : "memory");
         ++issued;
     };
     while (issued < n && issued < S) issue();
@@ -54,6 +57,7 @@ int main() {
     cudaEvent_t a, b;
     cudaEventCreate(&a);
     cudaEventCreate(&b);
+    for (int il = 0; il < 2; ++il)
     for (int G : {112, 128, 148})
         for (int64_t mb : {1, 2, 4, 8, 16}) {
             const int64_t per = mb << 20;
@@ -62,14 +66,14 @@ int main() {
                 cudaMemsetAsync(flush, rep, 256 << 20);  // evict the previous pass from L2
                 const int64_t off = ((rep % 3) * (int64_t)G * per) % (bytes - G * per);
                 cudaEventRecord(a);
-                k_stream<<<G, 64, S * STAGE + 1024>>>(d + off / 4096 * 4096, per, sink);
+                k_stream<<<G, 64, S * STAGE + 1024>>>(d + off / 4096 * 4096, per, sink, il);
                 cudaEventRecord(b);
                 cudaEventSynchronize(b);
                 float ms;
                 cudaEventElapsedTime(&ms, a, b);
                 if (rep > 0 && ms < best) best = ms;
             }
-            printf("G=%3d per_cta=%2lld MB total=%5lld MB: %8.2f us  %7.1f GB/s  (%s)\n", G, (long long)mb,
+            printf("%s G=%3d per_cta=%2lld MB total=%5lld MB: %8.2f us  %7.1f GB/s  (%s)\n", il ? "interleaved" : "contiguous ", G, (long long)mb,
                    (long long)(G * mb), best * 1e3, G * per / best / 1e6, cudaGetErrorString(cudaGetLastError()));
         }
     return 0;
