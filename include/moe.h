@@ -309,8 +309,9 @@ MOE_API moe_status moe_loopback_comm_destroy(void* group_or_rank);
  * processes on one GPU). nccl_comm may be NULL with this flag. MOE_PAR_HYBRID is
  * not supported (MOE_ERR_UNSUPPORTED). moe_forward before moe_p2p_connect fails
  * with MOE_ERR_STATE. Every rank must call moe_forward the same number of times
- * (TP: with the same T), as with the NCCL transport. Forwards cannot be
- * captured into a CUDA graph (MOE_ERR_UNSUPPORTED): the counter targets advance.
+ * (TP: with the same T), as with the NCCL transport. Forwards can be captured
+ * into a CUDA graph: each exchange waits for its counter to reach G and resets it
+ * (stream memory ops, the same values every forward; EP capacity mode).
  * Teardown: every rank's last forward must have completed on every rank (e.g.
  * stream sync + process-group barrier) before any rank calls moe_destroy, since
  * peers load from / store into this rank's region until then.                */

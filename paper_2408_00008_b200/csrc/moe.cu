@@ -128,6 +128,20 @@ PFN_waitValue64_t get_wait64_fn() {
     return fn;
 }
 
+typedef CUresult (*PFN_writeValue64_t)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+PFN_writeValue64_t get_write64_fn() {
+    static PFN_writeValue64_t fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuStreamWriteValue64", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_writeValue64_t>(p);
+    });
+    return fn;
+}
+
 // rank-2 [rows, K] or rank-3 [batch, rows, K] bf16, K innermost; box {64, box_rows(, 1)}; 128B swizzle.
 bool encode_map(CUtensorMap* m, const void* base, int rank, uint64_t K, uint64_t rows, uint64_t batch,
                 uint32_t box_rows) {
@@ -328,7 +342,6 @@ struct moe_ctx {
     int tp_shard_max = 0;
     uint8_t** d_peers = nullptr;  // device [p2p_world] region bases (own included)
     std::vector<void*> p2p_opened;  // IPC mappings to close at destroy
-    uint64_t p2p_epoch[4]{};      // exchanges done per counter
     // TMA descriptors: workspace operands
     CUtensorMap tm_x_tiled{}, tm_h_tiled{};
     CUtensorMap tm_h_store{}, tm_y_store{};       // CTA-pair epilogue TMA stores
@@ -1214,19 +1227,22 @@ moe_status check_ready(moe_ctx* c) {
     return MOE_OK;
 }
 
+// The counter of exchange idx collects exactly G arrivals per forward; after the wait
+// this rank resets it to 0 (a stream memory op), so every forward waits for the SAME
+// value and the P2P forward can be captured into a CUDA graph. The reset cannot race
+// with the next forward's arrivals: a peer signals exchange idx of forward n+1 only
+// after it has received data this rank produces after the reset (the EP return / the
+// TP finished rows of forward n, or this rank's next dispatch), i.e. causally later.
 moe_status p2p_arrive_and_wait(moe_ctx* c, int idx, cudaStream_t st) {
-    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-    CUDA_TRY(c, cudaStreamIsCapturing(st, &cs));
-    if (cs != cudaStreamCaptureStatusNone)  // the wait target advances every forward
-        return fail(c, MOE_ERR_UNSUPPORTED, "MOE_FLAG_P2P forwards cannot be captured into a CUDA graph");
     const int64_t sig_off = c->so.sig + 8 * idx;
     moe_status s = launch(c, kSlotExchange, moe_p2p_signal_kernel, dim3(1), dim3(32), 0, st,
                           static_cast<uint8_t* const*>(c->d_peers), c->p2p_world, sig_off);
     if (s) return s;
-    const uint64_t target = ++c->p2p_epoch[idx] * (uint64_t)c->p2p_world;
-    CUresult r = get_wait64_fn()(reinterpret_cast<CUstream>(st), reinterpret_cast<CUdeviceptr>(c->sym + sig_off), target,
-                                 CU_STREAM_WAIT_VALUE_GEQ);
+    const CUdeviceptr ctr = reinterpret_cast<CUdeviceptr>(c->sym + sig_off);
+    CUresult r = get_wait64_fn()(reinterpret_cast<CUstream>(st), ctr, (uint64_t)c->p2p_world, CU_STREAM_WAIT_VALUE_GEQ);
     if (r != CUDA_SUCCESS) return fail(c, MOE_ERR_CUDA, "cuStreamWaitValue64 failed (%d)", (int)r);
+    r = get_write64_fn()(reinterpret_cast<CUstream>(st), ctr, 0, CU_STREAM_WRITE_VALUE_DEFAULT);
+    if (r != CUDA_SUCCESS) return fail(c, MOE_ERR_CUDA, "cuStreamWriteValue64 failed (%d)", (int)r);
     return MOE_OK;
 }
 
@@ -1790,7 +1806,8 @@ moe_status moe_p2p_connect(moe_ctx* c, const void* handles, int32_t world) {
     if (!c->p2p) return fail(c, MOE_ERR_STATE, "context was not created with MOE_FLAG_P2P");
     if (c->p2p_ready) return fail(c, MOE_ERR_STATE, "already connected");
     if (world != c->p2p_world) return fail(c, MOE_ERR_INVALID, "world %d != group size %d", world, c->p2p_world);
-    if (!get_wait64_fn()) return fail(c, MOE_ERR_UNSUPPORTED, "cuStreamWaitValue64 unavailable");
+    if (!get_wait64_fn() || !get_write64_fn())
+        return fail(c, MOE_ERR_UNSUPPORTED, "cuStreamWaitValue64 / cuStreamWriteValue64 unavailable");
     std::vector<uint8_t*> bases(world, nullptr);
     const int me = (int)getpid();
     for (int r = 0; r < world; ++r) {
