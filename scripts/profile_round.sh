@@ -5,6 +5,7 @@
 TAG=${1:-r02}
 O=gpurun_out/$TAG; mkdir -p $O
 python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1
+timeout -s KILL 900 python -m pytest tests -m gpu -q -x -rs -k "p2p or nvls or graph" > $O/pytest_p2p.log 2>&1; echo rc=$? >> $O/pytest_p2p.log
 timeout -s KILL 400 python bench.py --steps 100 --warmup 5 > $O/bench_decode.log 2>&1
 timeout -s KILL 400 python bench.py --config prefill --steps 10 --warmup 3 --no-cpu-baseline > $O/bench_prefill.log 2>&1
 timeout -s KILL 900 python bench.py --config stack --steps 10 --warmup 3 > $O/bench_stack.log 2>&1
