@@ -739,18 +739,37 @@ def main():
     # has no host synchronisation, so on one GPU it is captured once per input
     # buffer into a CUDA graph and replayed (PDL edges are kept as programmatic
     # graph edges); multi-GPU runs replay eagerly (NCCL calls).
-    use_graph = args.graph and world == 1 and par == "none"
+    # Multi-GPU: EP in capacity mode (decode: no host synchronisation), TP over NCCL / P2P /
+    # NVLS and P2P EP are capturable too (NCCL collectives and stream memory ops become graph
+    # nodes); an exact-count EP exchange (prefill) syncs on the host, so it replays eagerly.
+    # Every rank captures the same sequence; a rank whose capture fails falls back to eager
+    # launches on ALL ranks (the decision is reduced over the process group).
+    ep_world = world if par == "ep" else (world // args.tp if par == "hybrid" else 1)
+    ep_exact = par in ("ep", "hybrid") and T * k * d * 2 * ep_world > (32 << 20)  # libmoe's exact-count rule
+    use_graph = args.graph and not ep_exact
     graphs = []
     if use_graph:
-        for i in range(nbuf):
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g):
-                moe.moe_forward(blk.ctx, xs[i], T, blk.router_w, blk.w13, blk.w2, out, None,
-                                torch.cuda.current_stream(), blk.s13, blk.s2)
-            graphs.append(g)
-        for i in range(2 * nbuf):
-            graphs[i % nbuf].replay()
-        torch.cuda.synchronize()
+        try:
+            for i in range(nbuf):
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    moe.moe_forward(blk.ctx, xs[i], T, blk.router_w, blk.w13, blk.w2, out, None,
+                                    torch.cuda.current_stream(), blk.s13, blk.s2)
+                graphs.append(g)
+            ok = 1
+        except Exception as ex:  # pragma: no cover - reported in the JSON line
+            print(f"graph capture failed, eager replay: {ex}", file=sys.stderr)
+            graphs, ok = [], 0
+        if world > 1:
+            import torch.distributed as dist
+            t_ok = torch.tensor([ok], device=dev)
+            dist.all_reduce(t_ok, op=dist.ReduceOp.MIN)
+            ok = int(t_ok.item())
+        use_graph = bool(ok)
+        if use_graph:
+            for i in range(2 * nbuf):
+                graphs[i % nbuf].replay()
+            torch.cuda.synchronize()
     barrier()
     torch.cuda.synchronize()
     ev0.record(stream)
