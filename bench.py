@@ -65,7 +65,9 @@ def workload_config(args, world):
         "transport": ("peer memory (MOE_FLAG_P2P)" if getattr(args, "p2p", False) else "nccl")
                      if par in ("ep", "tp", "hybrid") else None,
         "layers": STACK_LAYERS if stack else 1,
-        "l2": "weights (2.8 GB per layer) > L2 (126 MB): streamed from HBM every step, no flush"}
+        "l2": "weights (2.8 GB per layer) > L2 (126 MB): streamed from HBM every step, no flush",
+        "routing": "skewed 4:1 (expert 0 popular; synth.make_tokens_skewed)" if getattr(args, "skew", False)
+                   else "Gaussian tokens (balanced in expectation)"}
 
 
 def parse():
@@ -96,6 +98,8 @@ def parse():
                          "the global batch routes to them, or its f/G ffn slice): per-kernel roofline of the "
                          "per-rank shapes of the 2/4/8-GPU runs (--config decode|prefill)")
     ap.add_argument("--split-k", type=int, default=0, help="moe_config.split_k of the decode w2 GEMM (0 = auto)")
+    ap.add_argument("--skew", action="store_true",
+                    help="4:1 expert-popularity tokens (SURVEY 8(d) optional skew variant; synth.make_tokens_skewed)")
     ap.add_argument("--no-parity", action="store_true", help="skip the sampled per-rank oracle check")
     ap.add_argument("--p2p", action="store_true",
                     help="--par ep / tp: exchange through peer memory (MOE_FLAG_P2P: the producing kernels store "
@@ -664,7 +668,9 @@ def main():
     shard = rank if par == "ep" else (rank // args.tp if par == "hybrid" else 0)
     w = synth.make_weights(d, f, E, seed=args.seed, device=dev)
     nbuf = 4  # distinct token batches cycled through the steps
-    xs = [synth.make_tokens(Tg, d, seed=args.seed + 1 + i, device=dev)[shard * T:(shard + 1) * T] for i in range(nbuf)]
+    mk = (lambda s_: synth.make_tokens_skewed(Tg, d, w["wg"], seed=s_, device=dev)) if args.skew else \
+         (lambda s_: synth.make_tokens(Tg, d, seed=s_, device=dev))
+    xs = [mk(args.seed + 1 + i)[shard * T:(shard + 1) * T] for i in range(nbuf)]
     flags = args.flags
     if args.p2p:
         if par not in ("ep", "tp"):
@@ -889,6 +895,7 @@ def main():
         "step_roofline_frac": step_frac,
         "kernel_ms": {n: round(per[n], 5) for n in per if ktimes[n][1]},
         "kernel_share": kernel_share,
+        "expert_rows": counts.cpu().tolist(),
         "ms_per_step_profiled": ms_prof,
         "step_ms_dist": step_dist,
         "gpu_launches": launches,

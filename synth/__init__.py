@@ -69,6 +69,22 @@ def make_weights(d, f, E, seed, layer=0, device="cpu", dtype=torch.bfloat16):
     }
 
 
+# SURVEY 8(d) optional skew variant: x = z + mu with mu along router row 0, so expert 0's
+# logit gains SKEW_ALPHA (the other logits move by ~cos(W_g rows) ~ 1/64) and expert 0 is
+# picked ~4x as often as each other expert. SKEW_ALPHA from a Monte-Carlo of top-2 over 8
+# iid N(0,1) logits (the recipe's logit distribution): P(expert 0 in the top 2) = 8/11
+# <=> a 4:1 popularity ratio at alpha ~ 1.43 (1.4 -> 3.91, 1.5 -> 4.18).
+SKEW_ALPHA = 1.43
+
+
+def make_tokens_skewed(T, d, wg, seed, layer=0, device="cpu", dtype=torch.bfloat16, alpha=SKEW_ALPHA):
+    """Tokens of the 4:1 expert-popularity workload (expert 0 popular): N(0,1) tokens plus
+    alpha * g / |g|^2, g = router row 0 (bf16 router weights as given)."""
+    z = _randn((T, d), 1.0, seed * 1000 + 100 * layer + 0, device, torch.float32)
+    g = wg[0].to(device=device, dtype=torch.float32)
+    return (z + alpha * g / g.dot(g)).to(dtype)
+
+
 def make_inputs(shape: MoEShape, seed, layer=0, device="cpu", dtype=torch.bfloat16):
     w = make_weights(shape.d, shape.f, shape.E, seed, layer, device, dtype)
     w["x"] = make_tokens(shape.T, shape.d, seed, layer, device, dtype)

@@ -335,6 +335,24 @@ def test_c2_decode_full(moe, mixtral_weights, seed):
     blk.close()
 
 
+@pytest.mark.parametrize("T", [64, 575])
+def test_skewed_routing(moe, mixtral_weights, T):
+    """SURVEY 8(d) optional skew variant: tokens with a 4:1 popularity of expert 0
+    (synth.make_tokens_skewed) at Mixtral size, decode (T=64) and the stack batch (T=575,
+    where the popular expert overflows the statistical 192-row token tile and runs
+    several token tiles): routing exact, every output vs the oracle."""
+    w, host = mixtral_weights
+    x = synth.make_tokens_skewed(T, 4096, w["wg"], seed=400 + T, device="cuda")
+    blk = moe.MoEBlock(w["wg"], w["w1"], w["w3"], w["w2"], top_k=2, max_tokens=T)
+    run = GpuRun(blk, x)
+    counts = run.np("expert_counts")
+    assert counts[0] > 2.5 * np.mean(counts[1:]), counts
+    toks = np.arange(T) if T <= 64 else np.unique(np.concatenate([[0, T - 1], np.random.default_rng(T).choice(T, 48, replace=False)]))
+    st = check_forward(run, dict(host, x=synth.bf16_bits(x)), 2, tokens=toks, literal_bf16=T <= 64)
+    print("skewed", T, counts.tolist(), st)
+    blk.close()
+
+
 def test_c2_speculative_prefetch_bit_identical(moe, mixtral_weights):
     """The speculative L2 prefetch (tuning spec_l2) changes only timing: 64-token decode
     outputs are bit-identical with it off and at two depths."""
