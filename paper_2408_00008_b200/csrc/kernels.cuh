@@ -624,6 +624,8 @@ struct CombineParams {
     uint8_t* const* peers;
     int64_t peer_off;
     int32_t G, my_rank, shard_max;
+    unsigned int* p2p_ticket;  // P2P: this exchange's completion ticket (p2p_signal_last_block)
+    int64_t p2p_sig_off;       // P2P: the exchange counter in every region
 };
 
 // K5 (a9): out[t] = bf16_rne( sum_j w_j * (sum_s y_s[pos_j]) (+ x[t]) ), fixed order:
@@ -695,6 +697,7 @@ __global__ void __launch_bounds__(256) moe_combine_kernel(const CombineParams p)
             *reinterpret_cast<uint2*>(p.out + (int64_t)t * p.d + c) = ov;
         }
     }
+    if (p.peers) p2p_signal_last_block(p.p2p_ticket, p.peers, p.G, p.p2p_sig_off);  // TP reduce-scatter done
     ptx::pdl_launch_dependents();
 }
 
@@ -705,7 +708,7 @@ __global__ void __launch_bounds__(256) moe_combine_kernel(const CombineParams p)
 __global__ void __launch_bounds__(256) moe_ep_gather_kernel(const float* y, int64_t split_stride, int splits,
                                                             const int32_t* pos, int nslots, int d, float* ysend,
                                                             uint8_t* const* peers, int64_t peer_off, int cap,
-                                                            int my_rank) {
+                                                            int my_rank, int G, unsigned int* ticket, int64_t sig_off) {
     const int nxb = (d + 1023) / 1024;  // 1-D grid: block b -> slot b / nxb
     const int slot = blockIdx.x / nxb;
     const int c = (blockIdx.x % nxb) * 1024 + threadIdx.x * 4;
@@ -728,6 +731,7 @@ __global__ void __launch_bounds__(256) moe_ep_gather_kernel(const float* y, int6
             *reinterpret_cast<float4*>(dst) = s;
         }
     }
+    if (peers) p2p_signal_last_block(ticket, peers, G, sig_off);  // EP return exchange done
     ptx::pdl_launch_dependents();
 }
 

@@ -341,6 +341,7 @@ struct moe_ctx {
     } so;
     int tp_shard_max = 0;
     uint8_t** d_peers = nullptr;  // device [p2p_world] region bases (own included)
+    unsigned int* p2p_tickets = nullptr;  // device [4] last-block tickets of the producing kernels
     std::vector<void*> p2p_opened;  // IPC mappings to close at destroy
     // TMA descriptors: workspace operands
     CUtensorMap tm_x_tiled{}, tm_h_tiled{};
@@ -990,7 +991,7 @@ struct StepTimer {
 // P2P exchange completion: counter `idx` of every rank's region += 1 after the
 // producing kernel (device-side release), then this rank's stream waits until all
 // G ranks have arrived for this epoch (no SM is held while waiting).
-moe_status p2p_arrive_and_wait(moe_ctx* c, int idx, cudaStream_t st);
+moe_status p2p_wait(moe_ctx* c, int idx, cudaStream_t st);
 
 #define NCCL_TRY(ctx, expr)                                                                          \
     do {                                                                                             \
@@ -1227,17 +1228,15 @@ moe_status check_ready(moe_ctx* c) {
     return MOE_OK;
 }
 
-// The counter of exchange idx collects exactly G arrivals per forward; after the wait
+// The counter of exchange idx collects exactly G arrivals per forward (one from the last
+// block of every rank's producing kernel, p2p.cuh p2p_signal_last_block); after the wait
 // this rank resets it to 0 (a stream memory op), so every forward waits for the SAME
 // value and the P2P forward can be captured into a CUDA graph. The reset cannot race
 // with the next forward's arrivals: a peer signals exchange idx of forward n+1 only
 // after it has received data this rank produces after the reset (the EP return / the
 // TP finished rows of forward n, or this rank's next dispatch), i.e. causally later.
-moe_status p2p_arrive_and_wait(moe_ctx* c, int idx, cudaStream_t st) {
+moe_status p2p_wait(moe_ctx* c, int idx, cudaStream_t st) {
     const int64_t sig_off = c->so.sig + 8 * idx;
-    moe_status s = launch(c, kSlotExchange, moe_p2p_signal_kernel, dim3(1), dim3(32), 0, st,
-                          static_cast<uint8_t* const*>(c->d_peers), c->p2p_world, sig_off);
-    if (s) return s;
     const CUdeviceptr ctr = reinterpret_cast<CUdeviceptr>(c->sym + sig_off);
     CUresult r = get_wait64_fn()(reinterpret_cast<CUstream>(st), ctr, (uint64_t)c->p2p_world, CU_STREAM_WAIT_VALUE_GEQ);
     if (r != CUDA_SUCCESS) return fail(c, MOE_ERR_CUDA, "cuStreamWaitValue64 failed (%d)", (int)r);
@@ -1456,6 +1455,8 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
         ALLOC(c->sym, c->sym_bytes);
         if ((e = cudaMemset(c->sym, 0, c->sym_bytes)) != cudaSuccess) return fail_init("memset", e);
         ALLOC(c->d_peers, sizeof(uint8_t*) * c->p2p_world);
+        ALLOC(c->p2p_tickets, sizeof(unsigned int) * 4);
+        if ((e = cudaMemset(c->p2p_tickets, 0, sizeof(unsigned int) * 4)) != cudaSuccess) return fail_init("memset", e);
     }
 #undef ALLOC
     if (cfg->flags & MOE_FLAG_NVLS) {
@@ -1521,7 +1522,7 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
             reinterpret_cast<const void*>(moe_router_kernel<32, 2>), reinterpret_cast<const void*>(moe_permute_kernel),
             reinterpret_cast<const void*>(moe_combine_kernel), reinterpret_cast<const void*>(moe_ep_gather_kernel),
             reinterpret_cast<const void*>(moe_tp_finish_kernel), reinterpret_cast<const void*>(moe_loopback_add_kernel),
-            reinterpret_cast<const void*>(moe_p2p_signal_kernel), reinterpret_cast<const void*>(moe_ep_p2p_fill_kernel),
+reinterpret_cast<const void*>(moe_ep_p2p_fill_kernel),
             reinterpret_cast<const void*>(moe_tp_p2p_finish_kernel), reinterpret_cast<const void*>(moe_tp_p2p_pull_kernel),
             reinterpret_cast<const void*>(moe_gemm_kernel<kG1Tiled, 256>), reinterpret_cast<const void*>(moe_gemm_kernel<kG2Tiled, 256>),
             reinterpret_cast<const void*>(moe_gemm_kernel<kG1Swap, 32>), reinterpret_cast<const void*>(moe_gemm_kernel<kG2Swap, 32>),
@@ -1551,7 +1552,7 @@ moe_status moe_destroy(moe_ctx* c) {
     void* bufs[] = {c->topk_idx, c->topk_w, c->pos, c->blockcount, c->blockoff, c->counts, c->offsets, c->done,
                     c->x_perm, c->h, c->y, c->stage_in, c->stage_out, c->tp_partial, c->tp_scatter, c->ep_send,
                     c->ep_recv, c->ep_ysend, c->ep_yrecv, c->ep_meta_send, c->ep_meta_recv,
-                    c->ep_ridx, c->ep_rpos, c->ep_rw, c->ep_rcounts, c->lb_scratch, c->d_peers, c->src_row,
+                    c->ep_ridx, c->ep_rpos, c->ep_rw, c->ep_rcounts, c->lb_scratch, c->d_peers, c->p2p_tickets, c->src_row,
                     c->tok_scale, c->h8, c->h_sf};
     for (void* p : c->p2p_opened) cudaIpcCloseMemHandle(p);
     if (c->nvls) {
@@ -1951,6 +1952,7 @@ moe_status forward_impl(moe_ctx* c, const void* tokens, int32_t T, const void* r
         cp.out_f32 = nullptr;
         cp.peers = c->d_peers; cp.peer_off = c->so.tp_slots;
         cp.G = c->tp_world; cp.my_rank = c->tp_rank; cp.shard_max = c->tp_shard_max;
+        cp.p2p_ticket = c->p2p_tickets + 2; cp.p2p_sig_off = c->so.sig + 8 * 2;
     }
     if ((s = launch(c, kSlotCombine, moe_combine_kernel, dim3((unsigned)((c->d + 4095) / 4096 * (int64_t)T)), dim3(256), 0, st, cp)))
         return s;
@@ -1959,17 +1961,18 @@ moe_status forward_impl(moe_ctx* c, const void* tokens, int32_t T, const void* r
         const int t0 = (int)((int64_t)r * T / G), n = (int)((int64_t)(r + 1) * T / G) - t0;
         float* of32 = aux ? aux->out_f32 : nullptr;
         StepTimer t1(c, kSlotExchange, st);
-        if ((s = p2p_arrive_and_wait(c, 2, st))) return s;
+        if ((s = p2p_wait(c, 2, st))) return s;
         t1.done();
         const int fb = (int)std::max<int64_t>(1, std::min<int64_t>(4 * c->num_sms, ((int64_t)n * c->d / 4 + 255) / 256));
         if ((s = launch(c, kSlotCombine, moe_tp_p2p_finish_kernel, dim3(fb), dim3(256), 0, st,
                         reinterpret_cast<const float*>(c->sym + c->so.tp_slots), G, c->tp_shard_max, t0, n, c->d,
                         residual ? static_cast<const __nv_bfloat16*>(tokens) : nullptr,
                         static_cast<__nv_bfloat16*>(out), of32, reinterpret_cast<__nv_bfloat16*>(c->sym + c->so.tp_keep16),
-                        reinterpret_cast<float*>(c->sym + c->so.tp_keep32))))
+                        reinterpret_cast<float*>(c->sym + c->so.tp_keep32), static_cast<uint8_t* const*>(c->d_peers),
+                        c->p2p_tickets + 3, c->so.sig + 8 * 3)))
             return s;
         StepTimer t2(c, kSlotExchange, st);
-        if ((s = p2p_arrive_and_wait(c, 3, st))) return s;
+        if ((s = p2p_wait(c, 3, st))) return s;
         const int pb = (int)std::max<int64_t>(1, std::min<int64_t>(4 * c->num_sms, ((int64_t)T * c->d / 8 + 255) / 256));
         if ((s = launch(c, kSlotExchange, moe_tp_p2p_pull_kernel, dim3(pb), dim3(256), 0, st,
                         static_cast<uint8_t* const*>(c->d_peers), c->so.tp_keep16, c->so.tp_keep32, G, r, T, c->d,
@@ -2034,9 +2037,10 @@ moe_status forward_ep_p2p(moe_ctx* c, const void* tokens, int32_t T, const void*
     // this rank's unused slots in every destination's receive buffer -> -1
     const int fbx = std::max(1, std::min(64, (cap + 255) / 256));
     if ((s = launch(c, kSlotDispatch, moe_ep_p2p_fill_kernel, dim3(fbx, G), dim3(256), 0, st, peers, c->so.ep_meta,
-                    T > 0 ? static_cast<const int32_t*>(c->counts) : nullptr, G, cap, me)))
+                    T > 0 ? static_cast<const int32_t*>(c->counts) : nullptr, G, cap, me, c->p2p_tickets + 0,
+                    c->so.sig + 8 * 0)))
         return s;
-    if ((s = p2p_arrive_and_wait(c, 0, st))) return s;
+    if ((s = p2p_wait(c, 0, st))) return s;
     t1.done();
     // receive side: as the NCCL path, over this rank's region
     RouteSpec r2;
@@ -2056,9 +2060,9 @@ moe_status forward_ep_p2p(moe_ctx* c, const void* tokens, int32_t T, const void*
     if ((s = launch(c, kSlotExchange, moe_ep_gather_kernel, dim3((unsigned)((c->d + 1023) / 1024 * R)), dim3(256), 0,
                     st, static_cast<const float*>(c->y), c->split_stride, splits,
                     static_cast<const int32_t*>(c->ep_rpos), (int)R, c->d, static_cast<float*>(nullptr), peers,
-                    c->so.ep_yret, cap, me)))
+                    c->so.ep_yret, cap, me, G, c->p2p_tickets + 1, c->so.sig + 8 * 1)))
         return s;
-    if ((s = p2p_arrive_and_wait(c, 1, st))) return s;
+    if ((s = p2p_wait(c, 1, st))) return s;
     t2.done();
     if (T == 0) return MOE_OK;
     CombineParams cp{};
@@ -2146,7 +2150,8 @@ moe_status forward_ep(moe_ctx* c, const void* tokens, int32_t T, const void* rou
     if ((s = launch(c, kSlotExchange, moe_ep_gather_kernel, dim3((unsigned)((c->d + 1023) / 1024 * R)), dim3(256), 0,
                     st, static_cast<const float*>(c->y), c->split_stride, splits,
                     static_cast<const int32_t*>(c->ep_rpos), (int)R, c->d, c->ep_ysend,
-                    static_cast<uint8_t* const*>(nullptr), (int64_t)0, 0, 0)))
+                    static_cast<uint8_t* const*>(nullptr), (int64_t)0, 0, 0, 0, static_cast<unsigned int*>(nullptr),
+                    (int64_t)0)))
         return s;
     StepTimer t2(c, kSlotExchange, st);
     if (c->tp_world > 1) {

@@ -16,10 +16,11 @@
 //                 owner sums the G slots in rank order, rounds once to bf16 (R7),
 //                 and the other ranks pull the finished rows (all-gather by loads)
 //
-// Completion: after a producing kernel, moe_p2p_signal_kernel adds 1 to counter
-// `sig` of every rank's region (release, system scope); each rank's stream then
-// waits (cuStreamWaitValue64, GEQ, no SM spinning) until its own counter reaches
-// epoch * G. Kernel completion + the release fence order the data before the count.
+// Completion (round 2: inside the producing kernel): every block of the producing kernel
+// fences its peer stores (system scope) and takes a ticket; the LAST block adds 1 to
+// counter `sig` of every rank's region (release, system scope) -- p2p_signal_last_block.
+// Each rank's stream then waits (cuStreamWaitValue64 >= G, no SM spinning) and resets its
+// counter for the next forward (moe.cu p2p_wait). No separate signal kernel.
 #pragma once
 #include "sm100.cuh"
 
@@ -29,26 +30,45 @@ __device__ __forceinline__ void red_release_sys_add_u64(uint64_t* p, uint64_t v)
     asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-// One thread per peer: counter `sig_off` of every region += 1.
-__global__ void moe_p2p_signal_kernel(uint8_t* const* peers, int G, int64_t sig_off) {
-    ptx::pdl_wait();  // the producing kernel has completed and its stores are performed
-    if ((int)threadIdx.x < G) {
+// Exchange completion from inside a producing kernel, called by EVERY thread of EVERY
+// block at its end (no early returns before it). Each thread's stores (local or peer) are
+// fenced at system scope before its block takes a ticket (classic last-block pattern); the
+// block that takes the last ticket resets it and signals counter `sig_off` of every
+// region with a release at system scope, which (cumulatively) orders all blocks' fenced
+// stores before the count the peers wait for. ticket: this rank's, zero between launches.
+__device__ __forceinline__ void p2p_signal_last_block(unsigned int* ticket, uint8_t* const* peers, int G,
+                                                      int64_t sig_off) {
+    __shared__ int s_last;
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned int nblk = gridDim.x * gridDim.y * gridDim.z;
+        s_last = atomicAdd(ticket, 1u) == nblk - 1;
+    }
+    __syncthreads();
+    if (s_last) {
+        if (threadIdx.x == 0) *ticket = 0u;
         __threadfence_system();
-        red_release_sys_add_u64(reinterpret_cast<uint64_t*>(peers[threadIdx.x] + sig_off), 1ull);
+        for (int g = threadIdx.x; g < G; g += blockDim.x)
+            red_release_sys_add_u64(reinterpret_cast<uint64_t*>(peers[g] + sig_off), 1ull);
     }
 }
 
 // EP dispatch, empty slots: this rank's meta entries [count_e, cap) in the receive
 // buffer of every destination e are set to -1 (count_e from the router; counts ==
 // nullptr: no rows at all, every slot empty).
+// The dispatch exchange completes here (the permute kernel, which stored the occupied
+// slots, has finished before this grid passes its griddepcontrol.wait).
 __global__ void moe_ep_p2p_fill_kernel(uint8_t* const* peers, int64_t meta_off, const int32_t* counts, int G,
-                                       int cap, int my_rank) {
+                                       int cap, int my_rank, unsigned int* ticket, int64_t sig_off) {
     ptx::pdl_wait();
     const int e = blockIdx.y;
-    if (e >= G) return;
-    const int n0 = counts ? counts[e] : 0;
-    int32_t* meta = reinterpret_cast<int32_t*>(peers[e] + meta_off) + (int64_t)my_rank * cap;
-    for (int i = n0 + blockIdx.x * blockDim.x + threadIdx.x; i < cap; i += gridDim.x * blockDim.x) meta[i] = -1;
+    if (e < G) {
+        const int n0 = counts ? counts[e] : 0;
+        int32_t* meta = reinterpret_cast<int32_t*>(peers[e] + meta_off) + (int64_t)my_rank * cap;
+        for (int i = n0 + blockIdx.x * blockDim.x + threadIdx.x; i < cap; i += gridDim.x * blockDim.x) meta[i] = -1;
+    }
+    p2p_signal_last_block(ticket, peers, G, sig_off);
     ptx::pdl_launch_dependents();
 }
 
@@ -64,7 +84,9 @@ __device__ __forceinline__ int tp_row0(int r, int T, int G) { return (int)(((int
 __global__ void __launch_bounds__(256) moe_tp_p2p_finish_kernel(const float* slots, int G, int shard_max, int t0,
                                                                 int n, int d, const __nv_bfloat16* x,
                                                                 __nv_bfloat16* out, float* out_f32,
-                                                                __nv_bfloat16* keep16, float* keep32) {
+                                                                __nv_bfloat16* keep16, float* keep32,
+                                                                uint8_t* const* peers, unsigned int* ticket,
+                                                                int64_t sig_off) {
     ptx::pdl_wait();
     const int64_t total = (int64_t)n * d;
     for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * 4; i < total;
@@ -89,6 +111,7 @@ __global__ void __launch_bounds__(256) moe_tp_p2p_finish_kernel(const float* slo
         *reinterpret_cast<float4*>(keep32 + o) = r;
         if (out_f32) *reinterpret_cast<float4*>(out_f32 + o) = r;
     }
+    p2p_signal_last_block(ticket, peers, G, sig_off);  // the finished rows may be pulled
     ptx::pdl_launch_dependents();
 }
 
