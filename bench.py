@@ -612,9 +612,11 @@ def run_stack(args, world, rank, local):
         "data": "synthetic (seeded Gaussian tokens, random-init Mixtral-shaped weights per layer; DESIGN.md input recipe)",
         "config": cfg,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                     "frac": achieved / peaks["hbm_gbs"], "traffic": None,
+                     "frac": achieved / peaks["hbm_gbs"], "traffic": load_traffic("stack")[0] if par == "none" else None,
+                     "algorithmic": g1_bytes,
                      "kernel": "moe_gemm_kernel w1/w3 + SwiGLU (mean over the 32 layers)",
-                     "peak_src": peaks["src"] + " (MEASURED_PEAKS.json hbm_gbs)"},
+                     "peak_src": peaks["src"] + " (MEASURED_PEAKS.json hbm_gbs)",
+                     "traffic_src": load_traffic("stack")[1] if par == "none" else None},
         "step_roofline_frac": STACK_LAYERS * bytes_layer / (ms * 1e-3) / 1e9 / peaks["hbm_gbs"],
         "kernel_ms_per_launch": {n: round(per[n], 5) for n in per if kt[n][1]},
         "kernel_share": {n: round(kt[n][0] / args.steps / ms_prof, 4) for n in kt if kt[n][1]},
