@@ -207,6 +207,15 @@ def dist_setup(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1 and os.environ.get("BENCH_ONE_DEVICE") == "1":
+        # TEST MODE (scripts/gpu_multirank_one_gpu.sh): every rank on cuda:0, gloo for the host
+        # process group -- exercises the multi-rank bench flow (sharding, P2P transport over
+        # CUDA IPC, max-over-ranks timing, parity reduction) on a one-GPU box. Only --p2p
+        # transports work (NCCL refuses two ranks on one device); the timings are not results.
+        import torch.distributed as dist
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo")
+        return world, rank, 0
     if world > 1:
         import torch.distributed as dist
         torch.cuda.set_device(local)
