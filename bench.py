@@ -544,7 +544,8 @@ def run_stack(args, world, rank, local):
         del lw
     torch.cuda.empty_cache()
     nbuf = 4
-    xs = [synth.make_tokens(Tg, d, seed=args.seed + 1 + i, device=dev) for i in range(nbuf)]
+    xs = [synth.make_tokens_skewed(Tg, d, st.router_w[0], seed=args.seed + 1 + i, device=dev) if args.skew
+          else synth.make_tokens(Tg, d, seed=args.seed + 1 + i, device=dev) for i in range(nbuf)]
     xs = [x[rank * T:(rank + 1) * T] if par == "ep" else x for x in xs]
     out = torch.empty(T, d, dtype=torch.bfloat16, device=dev)
     stream = torch.cuda.current_stream()
