@@ -41,6 +41,16 @@ CONFIGS = {
     "stack": (575, 4096, 14336, 8, 2, 4),
 }
 STACK_LAYERS = 32
+# C5 batches: M0 = 64 decode tokens, M1 = 63 decode + one 512-token prefill
+# chunk (the steady state of 64 closed-loop requests with 512-token prompts: one admission
+# every 8 iterations), M2 = 56 decode + 8 x 512 prefill; "cycle" = the closed-loop period,
+# 7 x M0 + 1 x M1 per step (1023 tokens)
+STACK_BATCHES = {"M0": 64, "M1": 575, "M2": 4152}
+CYCLE = (("M0", 7), ("M1", 1))
+
+
+def stack_T(args):
+    return 7 * 64 + 575 if args.stack_batch == "cycle" else STACK_BATCHES[args.stack_batch]
 
 
 METRIC = "MoE-block tokens/sec (Mixtral-8x7B shape, 64-req decode) + % HBM / tensor-pipe peak"
@@ -50,12 +60,18 @@ def workload_config(args, world):
     """The `config` object both arms print (same workload, same keys)."""
     Tg, d, f, E, k, ci = CONFIGS[args.config]
     stack = args.config == "stack"
+    if stack:
+        Tg = stack_T(args)
     par = args.par or (("tp" if stack else "ep") if world > 1 else "none")
     T = Tg // world if par == "ep" else (Tg // (world // args.tp) if par == "hybrid" else Tg)
     what = {"decode": "Mixtral-8x7B single MoE layer, 64-request decode",
             "prefill": "Mixtral-8x7B single MoE layer, 32k-token prefill",
             "stack": f"Mixtral-8x7B {STACK_LAYERS}-layer MoE stack (x + MoE(x) per layer), 64 concurrent "
-                     f"requests, mixed batch 63 decode + 1x512 prefill"}[args.config]
+                     + {"M0": "requests, 64 decode tokens (M0)",
+                        "M1": "requests, mixed batch 63 decode + 1x512 prefill (M1)",
+                        "M2": "requests, mixed batch 56 decode + 8x512 prefill (M2)",
+                        "cycle": "closed-loop requests, one cycle = 7 decode batches (M0) + 1 mixed batch (M1)"}[
+                         getattr(args, "stack_batch", "M1")]}[args.config]
     return par, T, {
         "workload": f"BASELINE.json configs[{ci if stack else (3 if world > 1 else ci)}]: {what}, "
                     f"global batch T={Tg}, d={d}, f={f}, E={E}, top-{k}, bf16",
@@ -98,6 +114,9 @@ def parse():
                          "the global batch routes to them, or its f/G ffn slice): per-kernel roofline of the "
                          "per-rank shapes of the 2/4/8-GPU runs (--config decode|prefill)")
     ap.add_argument("--split-k", type=int, default=0, help="moe_config.split_k of the decode w2 GEMM (0 = auto)")
+    ap.add_argument("--stack-batch", default="M1", choices=["M0", "M1", "M2", "cycle"],
+                    help="--config stack batch (SURVEY 8(d)): M0 64, M1 575 (default), M2 4152 tokens, or the "
+                         "closed-loop cycle 7 x M0 + M1")
     ap.add_argument("--skew", action="store_true",
                     help="4:1 expert-popularity tokens (SURVEY 8(d) optional skew variant; synth.make_tokens_skewed)")
     ap.add_argument("--no-parity", action="store_true", help="skip the sampled per-rank oracle check")
@@ -526,31 +545,48 @@ def run_stack(args, world, rank, local):
     import torch
     import synth
     import paper_2408_00008_b200 as moe
-    Tg, d, f, E, k, ci = CONFIGS["stack"]
+    _, d, f, E, k, ci = CONFIGS["stack"]
     par, T, cfg = workload_config(args, world)
+    Tg = stack_T(args)
+    cycle = args.stack_batch == "cycle"
+    # the forwards of one step: (tokens per forward, count); per-rank token counts under EP
+    fwd = [(STACK_BATCHES[b], n) for b, n in CYCLE] if cycle else [(Tg, 1)]
+    shard = lambda t: t // world if par == "ep" else t
+    T = max(shard(t) for t, _ in fwd)  # workspace bound
     dev = torch.device("cuda", local)
     pmap = {"none": moe.MOE_PAR_NONE, "ep": moe.MOE_PAR_EP, "tp": moe.MOE_PAR_TP}
     comm = None
     if par != "none":
         comm = moe.nccl_comm_from_process_group(world, rank, local) if world > 1 else \
             moe.moe_nccl_comm_init(moe.moe_nccl_unique_id(), 1, 0, local)
-    first = synth.make_weights(d, f, E, seed=args.seed, layer=0, device=dev)
+    first = synth.make_weights(d, f, E, seed=args.seed, layer=0, device=dev, w2_scale=synth.STACK_W2_SCALE)
     st = moe.MoEStack([first], top_k=k, max_tokens=T, par=pmap[par], world_size=world if par != "none" else 1,
                       rank=rank if par != "none" else 0, nccl_comm=comm, flags=args.flags)
     del first
     for l in range(1, STACK_LAYERS):
-        lw = synth.make_weights(d, f, E, seed=args.seed, layer=l, device=dev)
+        lw = synth.make_weights(d, f, E, seed=args.seed, layer=l, device=dev, w2_scale=synth.STACK_W2_SCALE)
         st.add_layer(lw)
         del lw
     torch.cuda.empty_cache()
     nbuf = 4
-    xs = [synth.make_tokens_skewed(Tg, d, st.router_w[0], seed=args.seed + 1 + i, device=dev) if args.skew
-          else synth.make_tokens(Tg, d, seed=args.seed + 1 + i, device=dev) for i in range(nbuf)]
-    xs = [x[rank * T:(rank + 1) * T] if par == "ep" else x for x in xs]
+
+    def tokens(tg, i):
+        x = synth.make_tokens_skewed(tg, d, st.router_w[0], seed=args.seed + 1 + i, device=dev) if args.skew \
+            else synth.make_tokens(tg, d, seed=args.seed + 1 + i, device=dev)
+        t = shard(tg)
+        return x[rank * t:(rank + 1) * t] if par == "ep" else x
+
+    # xs[i] = the token batches of step i's forwards
+    xs = [[tokens(tg, i) for tg, n in fwd for _ in range(n)] for i in range(nbuf)]
     out = torch.empty(T, d, dtype=torch.bfloat16, device=dev)
     stream = torch.cuda.current_stream()
+
+    def step(i):
+        for x in xs[i % nbuf]:
+            st.forward(x, out[:x.shape[0]], stream)
+
     for i in range(max(3, args.warmup)):
-        st.forward(xs[i % nbuf], out, stream)
+        step(i)
     torch.cuda.synchronize()
 
     def barrier():
@@ -568,7 +604,7 @@ def run_stack(args, world, rank, local):
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
     for i in range(args.steps):
-        st.forward(xs[i % nbuf], out, stream)
+        step(i)
     ev1.record(stream)
     torch.cuda.synchronize()
     barrier()
@@ -580,23 +616,25 @@ def run_stack(args, world, rank, local):
     torch.cuda.synchronize()
     ev0.record(stream)
     for i in range(args.steps):
-        st.forward(xs[i % nbuf], out, stream)
+        step(i)
     ev1.record(stream)
     torch.cuda.synchronize()
     barrier()
     clk = clocks.stop()
     ms = ev0.elapsed_time(ev1) / args.steps
     # e2e: host tokens -> 32 layers -> host output
-    xh = [x.cpu().pin_memory() for x in xs]
+    xh = [[x.cpu().pin_memory() for x in xi] for xi in xs]
     oh = torch.empty(T, d, dtype=torch.bfloat16).pin_memory()
     xd = torch.empty(T, d, dtype=torch.bfloat16, device=dev)
     barrier()
     torch.cuda.synchronize()
     ev0.record(stream)
     for i in range(args.steps):
-        xd.copy_(xh[i % nbuf], non_blocking=True)
-        st.forward(xd, out, stream)
-        oh.copy_(out, non_blocking=True)
+        for x in xh[i % nbuf]:
+            t = x.shape[0]
+            xd[:t].copy_(x, non_blocking=True)
+            st.forward(xd[:t], out[:t], stream)
+            oh[:t].copy_(out[:t], non_blocking=True)
     ev1.record(stream)
     torch.cuda.synchronize()
     barrier()
@@ -609,11 +647,14 @@ def run_stack(args, world, rank, local):
     peaks = load_peaks()
     f_l = f // world if par == "tp" else f
     E_l = E // world if par == "ep" else E
-    # every expert is touched at T = 575 (P(untouched) ~ 0.75^575): weights stream once per layer
-    bytes_layer = E_l * 3 * d * f_l * 2 + E * d * 2 + 2 * T * d * 2
+    # every expert is touched at T >= 64 (P(untouched) ~ 0.75^T): weights stream once per
+    # layer and forward; tokens in/out per forward
+    fwd_T = [shard(t) for t, n in fwd for _ in range(n)]
+    step_bytes = sum(STACK_LAYERS * (E_l * 3 * d * f_l * 2 + E * d * 2 + 2 * t * d * 2) for t in fwd_T)
+    step_flops = sum(STACK_LAYERS * (2 * t * k * 3 * d * f_l + 2 * t * d * E) for t in fwd_T)
     per = {n: (v[0] / v[1] if v[1] else 0.0) for n, v in kt.items()}
     g1_ms = kt["gemm1_w13_swiglu"][0] / max(1, kt["gemm1_w13_swiglu"][1])
-    g1_bytes = E_l * 2 * f_l * d * 2 + T * k * d * 2 + T * k * f_l * 2
+    g1_bytes = sum(E_l * 2 * f_l * d * 2 + t * k * d * 2 + t * k * f_l * 2 for t in fwd_T) / len(fwd_T)
     achieved = g1_bytes / (g1_ms * 1e-3) / 1e9
     line = {
         "metric": METRIC, "value": Tg / (ms * 1e-3), "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
@@ -627,12 +668,14 @@ def run_stack(args, world, rank, local):
                      "kernel": "moe_gemm_kernel w1/w3 + SwiGLU (mean over the 32 layers)",
                      "peak_src": peaks["src"] + " (MEASURED_PEAKS.json hbm_gbs)",
                      "traffic_src": load_traffic("stack")[1] if par == "none" else None},
-        "step_roofline_frac": STACK_LAYERS * bytes_layer / (ms * 1e-3) / 1e9 / peaks["hbm_gbs"],
+        "step_roofline_frac": step_bytes / (ms * 1e-3) / 1e9 / peaks["hbm_gbs"],
+        "step_tensor_frac": step_flops / (ms * 1e-3) / 1e12 / peaks["bf16_tflops_sustained"],
+        "forwards_per_step": len(fwd_T),
         "kernel_ms_per_launch": {n: round(per[n], 5) for n in per if kt[n][1]},
         "kernel_share": {n: round(kt[n][0] / args.steps / ms_prof, 4) for n in kt if kt[n][1]},
         "ms_per_step_profiled": ms_prof, "gpu_launches": launches, "clocks": clk,
         "e2e": {"value": Tg / (ms_e2e * 1e-3), "unit": "tokens/s", "ms_per_step": ms_e2e,
-                "h2d_bytes_per_step": T * d * 2, "d2h_bytes_per_step": T * d * 2,
+                "h2d_bytes_per_step": sum(fwd_T) * d * 2, "d2h_bytes_per_step": sum(fwd_T) * d * 2,
                 "api": "MoEStack.forward (host tokens copied in, 32 x moe_forward, output copied out)"},
     }
     if rank == 0:

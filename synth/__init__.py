@@ -58,14 +58,24 @@ def make_tokens(T, d, seed, layer=0, device="cpu", dtype=torch.bfloat16):
     return _randn((T, d), 1.0, seed * 1000 + 100 * layer + 0, device, dtype)
 
 
-def make_weights(d, f, E, seed, layer=0, device="cpu", dtype=torch.bfloat16):
-    """Return dict wg [E,d], w1 [E,f,d], w3 [E,f,d], w2 [E,d,f] (HF layout)."""
+# C5 stack recipe (R12): x_{l+1} = x_l + MoE_l(x_l) with the single-layer recipe
+# diverges -- the SwiGLU block's output grows with the square of its input (rms 0.44 at
+# input rms 1), so the residual stream reaches rms 1e5 by layer 8 and NaN by layer 16 at
+# T = 64, and the NaN rows all route to experts 0 and 1 (scripts/exp/stack_counts.py).
+# The stack therefore draws W2 with std STACK_W2_SCALE / sqrt(f): the block's gain drops to
+# ~0.11 at rms 1 and the stream stays near rms 1-2 over 32 layers with every expert used.
+STACK_W2_SCALE = 0.25
+
+
+def make_weights(d, f, E, seed, layer=0, device="cpu", dtype=torch.bfloat16, w2_scale=1.0):
+    """Return dict wg [E,d], w1 [E,f,d], w3 [E,f,d], w2 [E,d,f] (HF layout). w2_scale scales
+    the std of W2 (STACK_W2_SCALE for the C5 stack)."""
     base = seed * 1000 + 100 * layer
     return {
         "wg": _randn((E, d), 1.0 / math.sqrt(d), base + 1, device, dtype),
         "w1": _randn((E, f, d), 1.0 / math.sqrt(d), base + 2, device, dtype),
         "w3": _randn((E, f, d), 1.0 / math.sqrt(d), base + 3, device, dtype),
-        "w2": _randn((E, d, f), 1.0 / math.sqrt(f), base + 4, device, dtype),
+        "w2": _randn((E, d, f), w2_scale / math.sqrt(f), base + 4, device, dtype),
     }
 
 
