@@ -561,7 +561,8 @@ def run_stack(args, world, rank, local):
             moe.moe_nccl_comm_init(moe.moe_nccl_unique_id(), 1, 0, local)
     first = synth.make_weights(d, f, E, seed=args.seed, layer=0, device=dev, w2_scale=synth.STACK_W2_SCALE)
     st = moe.MoEStack([first], top_k=k, max_tokens=T, par=pmap[par], world_size=world if par != "none" else 1,
-                      rank=rank if par != "none" else 0, nccl_comm=comm, flags=args.flags)
+                      rank=rank if par != "none" else 0, nccl_comm=comm, flags=args.flags, split_k=args.split_k,
+                      tuning=parse_tuning(args.tuning))
     del first
     for l in range(1, STACK_LAYERS):
         lw = synth.make_weights(d, f, E, seed=args.seed, layer=l, device=dev, w2_scale=synth.STACK_W2_SCALE)
