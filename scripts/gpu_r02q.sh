@@ -1,6 +1,6 @@
 # honest C5 stack (W2 x0.25): M1 path / tile variants, interleaved
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1
-for r in 1 2; do for t in "" "--tuning g1_swap_rows=100,g2_swap_rows=100" "--tuning g2_swap_rows=100" "--tuning g1_swap_rows=100" "--tuning g1_nb=128,g2_nb=256" "--split-k 2" "--tuning g1_nb=128"; do
+for r in 1 2 3; do for t in "" "--tuning g1_grid=148" "--tuning g2_grid=148" "--tuning g1_grid=148,g2_grid=148" "--tuning g1_grid=128"; do
   timeout -s KILL 600 python bench.py --config stack --stack-batch M1 --steps 5 --warmup 3 --no-cpu-baseline $t 2>&1 | grep "^{" | python -c "
 import json,sys
 for l in sys.stdin:
