@@ -133,7 +133,10 @@ typedef struct moe_tuning {
     int32_t pair_hints;     /* prefill CTA-pair L2 policies, 2 bits each (0 evict-normal, 1 evict-first,
                                2 evict-last): bits 0-1 w1/w3 tokens, 2-3 w1/w3 weights, 4-5 w2 h,
                                6-7 w2 weights (0: all evict-normal)                          */
-    int32_t reserved[10];   /* must be zero                                                  */
+    int32_t swap_pair;      /* swap-AB GEMMs on CTA pairs (cta_group::2, token tile split over
+                               the pair): 0 auto (token tiles >= 128 rows), 1 off, 2 always
+                               where the shape allows (w1/w3 needs ffn/tp_world % 256 == 0) */
+    int32_t reserved[9];    /* must be zero                                                  */
 } moe_tuning;
 
 typedef struct {

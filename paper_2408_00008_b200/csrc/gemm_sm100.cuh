@@ -1029,6 +1029,290 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
 }
 
+// ============================================================================
+// Swap-AB GEMMs on CTA pairs (cta_group::2) for mid-size batches: tens to a few hundred
+// rows per expert (the T = 575 stack of BASELINE configs[4]). The single-CTA swap tile
+// stages its NB token rows next to every K block of its weight tile; at NB = 192 the
+// token operand takes 43 % of the stage ring (4 stages, ~96 KB of weights in flight per
+// SM) and the weight stream is latency-bound (ncu r02, one T = 575 layer: DRAM 70 % of
+// peak, tensor pipe 58 %, L2->SM 31 %). Here a cluster of 2 CTAs computes M = 256 weight
+// rows x N tokens with tcgen05.mma.cta_group::2: CTA r stages ITS weight tile (the A
+// half) and token rows [r N/2, (r+1) N/2) of the tile (the B half); each CTA's TMEM
+// receives its 128 weight rows x all N token columns, so the epilogue is the single-CTA
+// swap epilogue. Per SM the token bytes halve: 5 stages at NB = 192 for w1/w3, 8 for w2,
+// and the w1/w3 tile can take NB = 256 (one token tile per expert up to 256 rows).
+//   kG1Swap: pair unit = W13 tiles 2j (CTA 0) and 2j+1 (CTA 1) -- needs f / 128 even.
+//   kG2Swap: pair unit = W2 128-row tiles 2j and 2j+1 (rows are padded to 256).
+// N of the MMA = the tile's valid tokens rounded up to 16 (8-row swizzle atoms per CTA); CTA 1's half
+// starts at token N/2 of the tile, so the fixed NB/2-row TMA box may run past the tile
+// (rows of the next expert, or zero fill past the buffer: never read by the MMA).
+#ifndef MOE_SPAIR_STAGES
+#define MOE_SPAIR_STAGES 8  // stage cap of the pair swap kernels (A/B knob)
+#endif
+template <int KIND, int NB>
+struct SwapPairCfg {
+    static constexpr bool kG1 = KIND == kG1Swap;
+    static constexpr int kABytes = (kG1 ? 256 : 128) * 128;
+    static constexpr int kBRows = NB / 2;
+    static constexpr int kBBytes = kBRows * 128;
+    static constexpr int kStageBytes = kABytes + kBBytes;
+    static constexpr int kStagesRaw = (kSmemBudget - 2048) / kStageBytes;
+    static constexpr int kStagesCap = MOE_SPAIR_STAGES;
+    static constexpr int kStages = kStagesRaw > kStagesCap ? kStagesCap : kStagesRaw;
+    static constexpr int kSmemBytes = kStages * kStageBytes + 2048;
+    static constexpr bool kWide = kG1 && NB > 128;  // a and b accumulators of > 128 columns
+    static constexpr int kAccStages = kWide ? 1 : 2;
+    static constexpr int kAccCols = kWide ? 512 : 256;
+    static constexpr int kBOff = kWide ? 256 : 128;
+    static_assert(KIND == kG1Swap || KIND == kG2Swap, "swap kinds only");
+    static_assert(NB % 32 == 0 && NB >= 32 && NB <= 256, "bad NB");
+    static_assert(kBBytes % 1024 == 0, "B halves keep the 1024-byte swizzle-atom alignment");
+};
+
+template <int KIND, int NB>
+__device__ __forceinline__ int spair_tiles_of(int n_e, const GemmParams& p) {
+    if (n_e <= 0) return 0;
+    const int nt = (n_e + NB - 1) / NB;
+    return KIND == kG1Swap ? nt * (p.f / 256) : nt * ((p.d + 255) / 256) * p.splits;
+}
+
+// Tile t of the pair grid, seen from CTA `crank` (token tiles fastest, then weight pairs,
+// then K splits); m_idx / a_row are this CTA's weight tile.
+template <int KIND, int NB>
+__device__ __forceinline__ void spair_decode(int t, const GemmParams& p, const int32_t* s_counts,
+                                             const int32_t* s_offsets, uint32_t crank, TileInfo& ti) {
+    int e = 0;
+    for (; e < p.E; ++e) {
+        const int n = spair_tiles_of<KIND, NB>(s_counts[e], p);
+        if (t < n) break;
+        t -= n;
+    }
+    ti.e = e;
+    ti.seg = s_offsets[e];
+    ti.rows = s_counts[e];
+    const int nt = (ti.rows + NB - 1) / NB;
+    ti.n_idx = t % nt;
+    const int rest = t / nt;
+    const int wp = KIND == kG1Swap ? p.f / 256 : (p.d + 255) / 256;
+    ti.split = rest / wp;
+    ti.m_idx = 2 * (rest % wp) + (int)crank;
+    ti.a_row = ti.m_idx * (KIND == kG1Swap ? 256 : 128);
+    ti.b_row = ti.seg + ti.n_idx * NB;
+    const int nkb_all = (KIND == kG1Swap ? p.d : p.f) / kBK;
+    const int S = KIND == kG2Swap ? p.splits : 1;
+    ti.kb0 = (nkb_all * ti.split) / S;
+    ti.nkb = (nkb_all * (ti.split + 1)) / S - ti.kb0;
+    const int rem = ti.rows - ti.n_idx * NB;
+    ti.n_valid = rem < NB ? rem : NB;
+}
+
+template <int KIND, int NB>
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    moe_gemm_swap_pair_kernel(const GemmParams p, const __grid_constant__ CUtensorMap tmA,
+                              const __grid_constant__ CUtensorMap tmB) {
+    using C = SwapPairCfg<KIND, NB>;
+    constexpr int S = C::kStages;
+    constexpr uint32_t kTx = 2u * C::kStageBytes;  // both CTAs' weight tile + token half per stage
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* smem_a = smem;
+    uint8_t* smem_b = smem + S * C::kABytes;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * C::kStageBytes);
+    uint64_t* full = bars;            // leader's: both CTAs' loads complete here
+    uint64_t* empty = bars + S;       // each CTA's (multicast commit)
+    uint64_t* tmem_full = bars + 2 * S;
+    uint64_t* tmem_empty = bars + 2 * S + 2;  // leader's: 4 epilogue warps x 2 CTAs
+    uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 4);
+    int32_t* s_counts = reinterpret_cast<int32_t*>(bars + 2 * S + 5);
+    int32_t* s_offsets = s_counts + 32;
+
+    const int warp = threadIdx.x / 32;
+    const int lane = threadIdx.x % 32;
+    const uint32_t crank = ptx::cluster_ctarank();
+    const bool leader = crank == 0;
+
+    if (warp == 0 && lane == 0) {
+        ptx::prefetch_tmap(&tmA);
+        ptx::prefetch_tmap(&tmB);
+        for (int i = 0; i < S; ++i) {
+            ptx::mbar_init(&full[i], 1);
+            ptx::mbar_init(&empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            ptx::mbar_init(&tmem_full[i], 1);
+            ptx::mbar_init(&tmem_empty[i], 8);
+        }
+        ptx::fence_mbar_init();
+    }
+    if (warp == 1) {
+        ptx::tmem_alloc_pair(tmem_base_slot, C::kAccStages * C::kAccCols);
+        ptx::tmem_relinquish_pair();
+    }
+    // The routing counts come from the router, complete before this grid can start (see
+    // moe_gemm_kernel); the producer issues its first weight stages before waiting for the
+    // previous kernel's tokens / activations.
+    if (MOE_PDL_PREFETCH == 0) ptx::pdl_wait();
+    if (threadIdx.x < 32) {
+        for (int e = threadIdx.x; e < p.E; e += 32) {
+            s_counts[e] = p.counts[e];
+            s_offsets[e] = p.offsets[e];
+        }
+    }
+    ptx::tc_fence_before();
+    ptx::cluster_sync();  // barriers of both CTAs initialised, TMEM allocated
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = *tmem_base_slot;
+
+    int total = 0;
+    for (int e = 0; e < p.E; ++e) total += spair_tiles_of<KIND, NB>(s_counts[e], p);
+    const int cid = blockIdx.x / 2, ncl = gridDim.x / 2;
+    const uint64_t w_hint = p.hint_a ? p.hint_a : ptx::kEvictFirst;
+
+    if (warp == 0) {
+        // ---------------------------------------------------------------- TMA producer (both CTAs)
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            int pre = 0;  // k-blocks of the first tile whose weight loads precede the wait
+            if (MOE_PDL_PREFETCH > 0) {
+                if (cid < total) {
+                    TileInfo t0;
+                    spair_decode<KIND, NB>(cid, p, s_counts, s_offsets, crank, t0);
+                    pre = min(S, t0.nkb);
+                    for (int kb = 0; kb < pre; ++kb) {  // fresh stages: no empty-wait needed
+                        const uint32_t fb = ptx::map_cluster(&full[kb], 0);
+                        if (leader) ptx::mbar_arrive_expect_tx(&full[kb], kTx);
+                        const WCoord w = wcoord(p, (t0.kb0 + kb) * kBK, t0.a_row, t0.e);
+                        ptx::tma_load_4d_pair(&tmA, fb, smem_a + kb * C::kABytes, 0, w.c1, w.c2, w.c3, w_hint);
+                    }
+                }
+                ptx::pdl_wait();
+            }
+            bool first = true;
+            for (int t = cid; t < total; t += ncl) {
+                TileInfo ti;
+                spair_decode<KIND, NB>(t, p, s_counts, s_offsets, crank, ti);
+                const int half = (ti.n_valid + 15) / 16 * 8;  // N / 2 of this tile's MMAs
+                const int tok_row = ti.b_row + (int)crank * half;
+                for (int kb = 0; kb < ti.nkb; ++kb) {
+                    const int kc = (ti.kb0 + kb) * kBK;
+                    const uint32_t fb = ptx::map_cluster(&full[stage], 0);
+                    if (!(first && kb < pre)) {
+                        ptx::mbar_wait(&empty[stage], phase ^ 1);
+                        if (leader) ptx::mbar_arrive_expect_tx(&full[stage], kTx);
+                        const WCoord w = wcoord(p, kc, ti.a_row, ti.e);
+                        ptx::tma_load_4d_pair(&tmA, fb, smem_a + stage * C::kABytes, 0, w.c1, w.c2, w.c3, w_hint);
+                    }
+                    ptx::tma_load_2d_pair(&tmB, fb, smem_b + stage * C::kBBytes, kc, tok_row, ptx::kEvictLast);
+                    if (++stage == S) { stage = 0; phase ^= 1; }
+                }
+                first = false;
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------------------------------------------------------- MMA issuer (leader CTA)
+        if (leader && lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            for (int t = cid; t < total; t += ncl) {
+                TileInfo ti;
+                spair_decode<KIND, NB>(t, p, s_counts, s_offsets, 0, ti);
+                const uint32_t idesc = ptx::make_idesc_bf16(256, (uint32_t)((ti.n_valid + 15) / 16 * 16));
+                const uint32_t d_tmem = tmem_base + acc * C::kAccCols;
+                ptx::mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
+                ptx::tc_fence_after();
+                for (int kb = 0; kb < ti.nkb; ++kb) {
+                    ptx::mbar_wait(&full[stage], phase);
+                    ptx::tc_fence_after();
+                    const uint32_t sa = ptx::smem_u32(smem_a + stage * C::kABytes);
+                    const uint64_t adesc = ptx::make_smem_desc_sw128(sa);
+                    const uint64_t bdesc = ptx::make_smem_desc_sw128(ptx::smem_u32(smem_b + stage * C::kBBytes));
+#pragma unroll
+                    for (int kk = 0; kk < kBK / 16; ++kk) {
+                        const uint32_t accum = (kb | kk) ? 1u : 0u;
+                        ptx::mma_bf16_pair(d_tmem, adesc + 2 * kk, bdesc + 2 * kk, idesc, accum);
+                        if (KIND == kG1Swap) {  // w3 half of each CTA's 256-row tile (+16 KB)
+                            const uint64_t adesc3 = ptx::make_smem_desc_sw128(sa + 128 * 128);
+                            ptx::mma_bf16_pair(d_tmem + C::kBOff, adesc3 + 2 * kk, bdesc + 2 * kk, idesc, accum);
+                        }
+                    }
+                    ptx::mma_commit_pair(&empty[stage], 0x3);  // frees this stage in both CTAs
+                    if (++stage == S) { stage = 0; phase ^= 1; }
+                }
+                ptx::mma_commit_pair(&tmem_full[acc], 0x3);
+                if (++acc == C::kAccStages) { acc = 0; acc_phase ^= 1; }
+            }
+        }
+    } else {
+        // ---------------------------------------------------------------- epilogue (warps 2..5, both CTAs)
+        const int q = warp & 3;
+        const int r = q * 32 + lane;  // weight row of this CTA's tile (= TMEM lane)
+        const uint32_t leader_empty0 = ptx::map_cluster(&tmem_empty[0], 0);
+        const uint32_t leader_empty1 = ptx::map_cluster(&tmem_empty[1], 0);
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int t = cid; t < total; t += ncl) {
+            TileInfo ti;
+            spair_decode<KIND, NB>(t, p, s_counts, s_offsets, crank, ti);
+            ptx::mbar_wait(&tmem_full[acc], acc_phase);
+            ptx::tc_fence_after();
+            const uint32_t tbase = tmem_base + acc * C::kAccCols + (static_cast<uint32_t>(q * 32) << 16);
+            const int nchunks = (ti.n_valid + 15) / 16;
+            if (KIND == kG1Swap) {
+                // row r = ffn index m*128 + r (a at cols [0,N), b at [kBOff, kBOff+N)); col n = token
+                __nv_bfloat16* h = static_cast<__nv_bfloat16*>(p.out) + static_cast<int64_t>(ti.b_row) * p.f +
+                                   ti.m_idx * 128 + r;
+#pragma unroll 1
+                for (int c = 0; c < nchunks; ++c) {
+                    uint32_t a[16], b[16];
+                    ptx::tmem_ld16(tbase + c * 16, a);
+                    ptx::tmem_ld16(tbase + C::kBOff + c * 16, b);
+                    ptx::tmem_wait_ld();
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        const int n = c * 16 + i;
+                        if (n < ti.n_valid)
+                            h[static_cast<int64_t>(n) * p.f] =
+                                __float2bfloat16_rn(silu_f32(__uint_as_float(a[i])) * __uint_as_float(b[i]));
+                    }
+                }
+            } else {
+                // row r = hidden index m*128 + r; col n = token; fp32 partial of split s
+                const int drow = ti.m_idx * 128 + r;
+                float* y = static_cast<float*>(p.out) + p.out_split_stride * ti.split +
+                           static_cast<int64_t>(ti.b_row) * p.d + drow;
+#pragma unroll 1
+                for (int c = 0; c < nchunks; ++c) {
+                    uint32_t v[16];
+                    ptx::tmem_ld16(tbase + c * 16, v);
+                    ptx::tmem_wait_ld();
+                    if (drow < p.d) {
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) {
+                            const int n = c * 16 + i;
+                            if (n < ti.n_valid) y[static_cast<int64_t>(n) * p.d] = __uint_as_float(v[i]);
+                        }
+                    }
+                }
+            }
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive_cluster(acc == 0 ? leader_empty0 : leader_empty1);
+            if (++acc == C::kAccStages) { acc = 0; acc_phase ^= 1; }
+        }
+    }
+    ptx::pdl_launch_dependents();
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::cluster_sync();  // the leader's MMAs wrote both CTAs' TMEM; the peer's arrives target the leader
+    if (warp == 1) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc_pair(tmem_base, C::kAccStages * C::kAccCols);
+    }
+}
+
 
 // ============================================================================
 // FP8-weight decode GEMMs ("8-bit (fp8) floating point"),

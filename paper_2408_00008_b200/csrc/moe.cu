@@ -314,6 +314,7 @@ struct moe_ctx {
     int host_slot = 0;
     uint64_t swap_w_hint = 0;    // L2 policy of the decode GEMMs' weight stream (set per forward)
     int swap_hint_mode = 0;      // tuning.weight_hint: 0 auto, 1 evict-first, 2 normal, 3 evict-last
+    int swap_pair_mode = 0;      // tuning.swap_pair: 0 auto, 1 off, 2 on where the shape allows
     bool host_zero_copy = true;  // moe_forward_host: combine writes pinned output directly (tuning.host_stage: copy)
     moe_nvls::State* nvls = nullptr;  // MOE_FLAG_NVLS: symmetric window + device communicator (nvls.cu)
     int nvls_blocks = 0;              // grid bound of the fused TP combine (its LSA barrier count)
@@ -346,7 +347,7 @@ struct moe_ctx {
     // TMA descriptors: workspace operands
     CUtensorMap tm_x_tiled{}, tm_h_tiled{};
     CUtensorMap tm_h_store{}, tm_y_store{};       // CTA-pair epilogue TMA stores
-    CUtensorMap tm_x_swap[5]{}, tm_h_swap[5]{};  // NB = 32, 64, 128, 256, 192
+    CUtensorMap tm_x_swap[6]{}, tm_h_swap[6]{};  // box rows 32, 64, 128, 256, 192, 96 (96: CTA-pair NB 192)
     // weight descriptor cache (keyed by pointer)
     struct WeightMaps {
         const void* w13 = nullptr;
@@ -454,6 +455,15 @@ moe_status set_pair_attr(moe_ctx* c) {
     return MOE_OK;
 }
 
+template <int NB>
+moe_status set_spair_attr(moe_ctx* c) {
+    CUDA_TRY(c, cudaFuncSetAttribute(moe_gemm_swap_pair_kernel<kG1Swap, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     SwapPairCfg<kG1Swap, NB>::kSmemBytes));
+    CUDA_TRY(c, cudaFuncSetAttribute(moe_gemm_swap_pair_kernel<kG2Swap, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     SwapPairCfg<kG2Swap, NB>::kSmemBytes));
+    return MOE_OK;
+}
+
 template <int KIND, int NB>
 moe_status set_gemm_attr(moe_ctx* c) {
     CUDA_TRY(c, cudaFuncSetAttribute(moe_gemm_kernel<KIND, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -486,6 +496,41 @@ moe_status launch_gemm_pair(moe_ctx* c, int slot, const GemmParams& p, const CUt
     cfg.numAttrs = 2;
     cudaError_t e = cudaLaunchKernelEx(&cfg, moe_gemm_pair_kernel<KIND, NBLK>, p, a, b, out);
     if (e != cudaSuccess) return fail(c, MOE_ERR_CUDA, "pair kernel launch (slot %d) failed: %s", slot, cudaGetErrorString(e));
+    c->launch_count++;
+    if (c->profiling) {
+        cudaEventRecord(eb, st);
+        c->pending.push_back({slot, ea, eb});
+    }
+    return MOE_OK;
+}
+
+// Swap-AB GEMM on CTA pairs: `nclusters` clusters of 2 CTAs
+template <int KIND, int NB>
+moe_status launch_swap_pair(moe_ctx* c, int slot, const GemmParams& p, const CUtensorMap& a, const CUtensorMap& b,
+                            int nclusters, cudaStream_t st) {
+    cudaEvent_t ea = nullptr, eb = nullptr;
+    if (c->profiling) {
+        ea = take_event(c);
+        eb = take_event(c);
+        cudaEventRecord(ea, st);
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(2 * nclusters);
+    cfg.blockDim = dim3(kGemmThreads);
+    cfg.dynamicSmemBytes = SwapPairCfg<KIND, NB>::kSmemBytes;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = (c->cfg.flags & MOE_FLAG_NO_PDL) ? 0 : 1;
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = 2;
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 2;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, moe_gemm_swap_pair_kernel<KIND, NB>, p, a, b);
+    if (e != cudaSuccess)
+        return fail(c, MOE_ERR_CUDA, "swap pair kernel launch (slot %d) failed: %s", slot, cudaGetErrorString(e));
     c->launch_count++;
     if (c->profiling) {
         cudaEventRecord(eb, st);
@@ -567,12 +612,13 @@ moe_status validate_cfg(const moe_config* cfg, moe_ctx* c) {
     for (int i = 0; i < 2; ++i)
         if (cfg->reserved[i]) return fail(c, MOE_ERR_INVALID, "reserved fields must be zero");
     if (const moe_tuning* tu = cfg->tuning) {
-        for (int i = 0; i < 10; ++i)
+        for (int i = 0; i < 9; ++i)
             if (tu->reserved[i]) return fail(c, MOE_ERR_INVALID, "tuning.reserved fields must be zero");
         if (tu->g1_swap_rows < 0 || tu->g2_swap_rows < 0 || tu->g1_grid < 0 || tu->g2_grid < 0 ||
             tu->swap_nb_cap < 0 || tu->router_cc_max_T < 0 || tu->pair_order < 0)
             return fail(c, MOE_ERR_INVALID, "tuning fields must be >= 0 (spec_l2 may be < 0: off)");
         if (tu->pair_nblk < 0 || tu->pair_nblk > 2) return fail(c, MOE_ERR_INVALID, "tuning.pair_nblk must be 0, 1 or 2");
+        if (tu->swap_pair < 0 || tu->swap_pair > 2) return fail(c, MOE_ERR_INVALID, "tuning.swap_pair must be 0, 1 or 2");
         if (tu->weight_hint < 0 || tu->weight_hint > 3) return fail(c, MOE_ERR_INVALID, "tuning.weight_hint must be 0..3");
         if (tu->swap_nb_cap && tu->swap_nb_cap != 32 && tu->swap_nb_cap != 64 && tu->swap_nb_cap != 128)
             return fail(c, MOE_ERR_INVALID, "tuning.swap_nb_cap must be 0, 32, 64 or 128");
@@ -669,6 +715,26 @@ moe_status run_swap_g2(moe_ctx* c, int nbi, const moe_expert_weights* w, int spl
         }
     return launch_gemm<kG2Swap, NB>(c, kSlotGemm2, p2, c->tm_w2_swap, c->tm_h_swap[nbi],
                                     c->g2_grid_now, st);
+}
+
+// Swap-AB GEMMs on CTA pairs (moe_gemm_swap_pair_kernel): token map with NB/2-row boxes
+int half_box_index(int nb) { return nb == 128 ? 1 : nb == 192 ? 5 : 2; }  // 64 / 96 / 128 rows
+template <int NB>
+moe_status run_spair_g1(moe_ctx* c, int nclusters, cudaStream_t st) {
+    GemmParams p1{c->counts, c->offsets, c->E_local, c->d, c->f_local, 1, c->h, 0};
+    p1.hint_a = c->swap_w_hint;
+    p1.w_tr = 256;
+    p1.w_nt = c->w13_nt;
+    return launch_swap_pair<kG1Swap, NB>(c, kSlotGemm1, p1, c->tm_w13, c->tm_x_swap[half_box_index(NB)], nclusters, st);
+}
+template <int NB>
+moe_status run_spair_g2(moe_ctx* c, int splits, int nclusters, cudaStream_t st) {
+    GemmParams p2{c->counts, c->offsets, c->E_local, c->d, c->f_local, splits, c->y, c->split_stride};
+    p2.hint_a = c->swap_w_hint;
+    p2.w_tr = 128;
+    p2.w_nt = c->w2_nt;
+    return launch_swap_pair<kG2Swap, NB>(c, kSlotGemm2, p2, c->tm_w2_swap, c->tm_h_swap[half_box_index(NB)], nclusters,
+                                         st);
 }
 
 // One routing + permutation pass (K1 + K2) over `T` rows of `x`.
@@ -838,6 +904,20 @@ moe_status run_gemms(moe_ctx* c, GemmPaths gp, int64_t rows_bound, int64_t rows_
                    : c->swap_hint_mode == 3 ? ptx::kEvictLast
                    : (need > nb1 ? ptx::kEvictNormal : ptx::kEvictFirst);
     const bool pair = !(c->cfg.flags & MOE_FLAG_NO_PAIR);
+    // Swap-AB tiles on CTA pairs (token tile split over the pair) for token tiles of >= 128
+    // rows -- the mid-size batches where the token operand crowds the single-CTA stage ring
+    // (tuning.swap_pair: 1 off, 2 also forced tiles). bf16 only, not in gather mode; the
+    // w1/w3 pair unit is two 256-row W13 tiles (f_local % 256 == 0). The w1/w3 tile then
+    // takes up to 256 token rows (a and b accumulators of 256 columns in the pair's TMEM).
+    const bool sp_ok = pair && !c->fp8 && !c->gather_now && !c->spec_now && c->swap_pair_mode != 1;
+    bool sp1 = sp_ok && gp.swap1 && c->f_local % 256 == 0 && (nb1 >= 128 || c->swap_pair_mode == 2);
+    bool sp2 = sp_ok && gp.swap2 && (nb2 >= 128 || c->swap_pair_mode == 2);
+    if (sp1 && !c->tune_g1_nb && rows_bound > 128) {
+        nb1 = swap_nb_ceil((int)std::min<int64_t>(need, 256), true);
+        if (c->swap_nb_cap >= 32) nb1 = std::min(nb1, c->swap_nb_cap);
+    }
+    sp1 = sp1 && nb1 >= 128;
+    sp2 = sp2 && nb2 >= 128;
     // CTA-pair (cta_group::2) 256x256 tiles, one cluster of 2 CTAs per TPC; tile order
     // per GEMM (see pair_decode); env MOE_PAIR_TUNE overrides for experiments:
     // bits 0-1 G1 order, 2-3 G2 order, 4-9 G1 band, 10-15 G2 band
@@ -866,7 +946,18 @@ moe_status run_gemms(moe_ctx* c, GemmPaths gp, int64_t rows_bound, int64_t rows_
             c->g1_grid_now = (int)std::min<int64_t>(ns, (U1 + w1 - 1) / w1);
         }
     }
-    if (gp.swap1) {
+    if (sp1) {
+        // equal waves over the pair units (E_l x f_l/256 x token tiles) on <= SMs/2 clusters
+        const int64_t U = (int64_t)c->E_local * (c->f_local / 256) * std::max<int64_t>(1, (need + nb1 - 1) / nb1);
+        const int64_t waves = (U + ncl - 1) / ncl;
+        const int g = c->g1_grid > 0 ? std::max(1, std::min(c->g1_grid, c->num_sms) / 2)
+                                     : (int)std::min<int64_t>(ncl, (U + waves - 1) / waves);
+        c->g1_grid_now = 2 * g;
+        if (nb1 == 128) s = run_spair_g1<128>(c, g, st);
+        else if (nb1 == 192) s = run_spair_g1<192>(c, g, st);
+        else s = run_spair_g1<256>(c, g, st);
+        if (s) return s;
+    } else if (gp.swap1) {
         const int i1 = nb1 == 32 ? 0 : nb1 == 64 ? 1 : nb1 == 128 ? 2 : 4;
         if (nb1 == 32) s = run_swap_g1<32>(c, i1, &c->cur_w, st);
         else if (nb1 == 64) s = run_swap_g1<64>(c, i1, &c->cur_w, st);
@@ -924,7 +1015,16 @@ moe_status run_gemms(moe_ctx* c, GemmPaths gp, int64_t rows_bound, int64_t rows_
             c->g2_grid_now = c->g2_grid > 0 ? std::min(c->g2_grid, ns)
                            : (!c->fp8 && need <= nb2) ? (int)std::min<int64_t>(ns, (U + waves - 1) / waves) : ns;
         }
-        if (nb2 == 32) s = run_swap_g2<32>(c, 0, &c->cur_w, splits, st);
+        if (sp2) {
+            const int64_t U = (int64_t)c->E_local * ((c->d + 255) / 256) * splits;
+            const int64_t waves = (U + ncl - 1) / ncl;
+            const int g = c->g2_grid > 0 ? std::max(1, std::min(c->g2_grid, c->num_sms) / 2)
+                                         : (int)std::min<int64_t>(ncl, (U + waves - 1) / waves);
+            c->g2_grid_now = 2 * g;
+            if (nb2 == 128) s = run_spair_g2<128>(c, splits, g, st);
+            else if (nb2 == 192) s = run_spair_g2<192>(c, splits, g, st);
+            else s = run_spair_g2<256>(c, splits, g, st);
+        } else if (nb2 == 32) s = run_swap_g2<32>(c, 0, &c->cur_w, splits, st);
         else if (nb2 == 64) s = run_swap_g2<64>(c, 1, &c->cur_w, splits, st);
         else if (nb2 == 128) s = run_swap_g2<128>(c, 2, &c->cur_w, splits, st);
         else if (nb2 == 192) s = run_swap_g2<192>(c, 4, &c->cur_w, splits, st);
@@ -1344,6 +1444,7 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
         c->g2_grid = tu->g2_grid;
         c->host_zero_copy = tu->host_stage == 0;
         c->swap_hint_mode = tu->weight_hint;
+        c->swap_pair_mode = tu->swap_pair;
     }
     if (cfg->flags & MOE_FLAG_GATHER) c->gather = true;
     // EP: a rank may receive up to every token of every peer (dropless, reading R6).
@@ -1484,8 +1585,8 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
               encode_map(&c->tm_h_tiled, c->h, 2, c->f_local, c->cap, 1, 128) &&
               encode_store_map(&c->tm_h_store, c->h, false, c->f_local, c->cap) &&
               encode_store_map(&c->tm_y_store, c->y, true, c->d, c->y_elems / c->d);
-    const uint32_t nbs[5] = {32, 64, 128, 256, 192};
-    for (int i = 0; i < 5 && ok; ++i)
+    const uint32_t nbs[6] = {32, 64, 128, 256, 192, 96};
+    for (int i = 0; i < 6 && ok; ++i)
         ok = encode_map(&c->tm_x_swap[i], c->x_perm, 2, c->d, c->cap, 1, nbs[i]) &&
              encode_map(&c->tm_h_swap[i], c->h, 2, c->f_local, c->cap, 1, nbs[i]);
     for (int i = 0; i < 3 && ok && c->fp8; ++i)
@@ -1502,6 +1603,7 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
         (as = set_gemm_attr<kG1Swap, 128>(c)) || (as = set_gemm_attr<kG2Swap, 128>(c)) ||
         (as = set_gemm_attr<kG2Swap, 256>(c)) || (as = set_gemm_attr<kG1Swap, 192>(c)) ||
         (as = set_gemm_attr<kG2Swap, 192>(c)) ||
+        (as = set_spair_attr<128>(c)) || (as = set_spair_attr<192>(c)) || (as = set_spair_attr<256>(c)) ||
         (as = set_pair_attr<kG1Pair, 1>(c)) || (as = set_pair_attr<kG2Pair, 1>(c)) ||
         (as = set_pair_attr<kG1Pair, 2>(c)) || (as = set_pair_attr<kG2Pair, 2>(c)) ||
         (as = set_fp8x_attr<32>(c)) || (as = set_fp8x_attr<64>(c)) || (as = set_fp8x_attr<128>(c))) {
@@ -1532,6 +1634,12 @@ reinterpret_cast<const void*>(moe_ep_p2p_fill_kernel),
             reinterpret_cast<const void*>(moe_gemm_kernel<kG1Swap, 192>), reinterpret_cast<const void*>(moe_gemm_kernel<kG2Swap, 192>),
             reinterpret_cast<const void*>(moe_gemm_pair_kernel<kG2Pair, 1>), reinterpret_cast<const void*>(moe_gemm_pair_kernel<kG1Pair, 2>),
             reinterpret_cast<const void*>(moe_gemm_pair_kernel<kG2Pair, 2>),
+            reinterpret_cast<const void*>(moe_gemm_swap_pair_kernel<kG1Swap, 128>),
+            reinterpret_cast<const void*>(moe_gemm_swap_pair_kernel<kG1Swap, 192>),
+            reinterpret_cast<const void*>(moe_gemm_swap_pair_kernel<kG1Swap, 256>),
+            reinterpret_cast<const void*>(moe_gemm_swap_pair_kernel<kG2Swap, 128>),
+            reinterpret_cast<const void*>(moe_gemm_swap_pair_kernel<kG2Swap, 192>),
+            reinterpret_cast<const void*>(moe_gemm_swap_pair_kernel<kG2Swap, 256>),
             reinterpret_cast<const void*>(moe_gemm_fp8x_kernel<kG1Swap, 32>),
             reinterpret_cast<const void*>(moe_gemm_fp8x_kernel<kG1Swap, 64>),
             reinterpret_cast<const void*>(moe_gemm_fp8x_kernel<kG1Swap, 128>),

@@ -174,6 +174,51 @@ def test_pair_wide_tiles(moe, T, d, f, E, k):
     assert np.array_equal(outs[0].view(np.int32), outs[1].view(np.int32))
 
 
+@pytest.mark.parametrize("T,d,f,E,k,split_k", [
+    (300, 256, 512, 8, 2, 0),     # ~75 rows / expert: token tile 128 on the pair (64 rows per CTA)
+    (575, 512, 1024, 8, 2, 0),    # the stack batch: token tile 192 (96 per CTA)
+    (1000, 512, 1024, 8, 2, 0),   # ~250 rows / expert: tile 256, busy experts run a 2nd token tile
+    (400, 320, 384, 4, 2, 3),     # f/128 odd: w1/w3 on single CTAs, w2 pairs over d = 320 (a padding tile), 3 K splits
+    (130, 256, 512, 8, 1, 0),     # top-1, small experts: N = 32 tiles with a few valid tokens
+    (700, 768, 256, 6, 2, 2)])
+def test_swap_pair(moe, T, d, f, E, k, split_k):
+    """Swap-AB GEMMs on CTA pairs (moe_gemm_swap_pair_kernel, tuning swap_pair): each CTA
+    streams its own weight tile and stages half of the token tile, the pair's M = 256 MMA
+    fills both CTAs' TMEM. Oracle parity with the pair kernels forced (2) and off (1),
+    and the two runs bit-identical (same MMAs per output element, same K order)."""
+    shape = synth.MoEShape(T=T, d=d, f=f, E=E, k=k)
+    inp = _inputs(shape, 6100 + T + d)
+    host = to_host_inputs(inp)
+    outs = []
+    for mode in (2, 1):
+        blk = _block(moe, inp, k, T, moe.MOE_FLAG_FORCE_SWAP, split_k=split_k, tuning={"swap_pair": mode})
+        run = GpuRun(blk, inp["x"])
+        check_forward(run, host, k)
+        outs.append(run.np("out_f32").copy())
+        out2 = blk.forward(inp["x"])  # second forward: barrier phases carried across calls
+        torch.cuda.synchronize()
+        assert torch.equal(out2.view(torch.int16), run.out.view(torch.int16))
+        blk.close()
+    assert np.array_equal(outs[0].view(np.int32), outs[1].view(np.int32))
+
+
+@pytest.mark.parametrize("n", [129, 256, 300])
+def test_swap_pair_pathological(moe, n):
+    """Forced routing of every token to experts (0, 1) of 4 with the pair kernels: the
+    token tile is sized for the expected n/2 rows per expert, so each of the two busy
+    experts runs two token tiles (129 rows: a 1-token tail tile)."""
+    shape = synth.MoEShape(T=n, d=256, f=512, E=4, k=2)
+    inp = _inputs(shape, 6200 + n)
+    host = to_host_inputs(inp)
+    idx = np.tile(np.array([[0, 1]], np.int32), (n, 1))
+    gw = _forced_gates(host, idx)
+    blk = _block(moe, inp, 2, n, moe.MOE_FLAG_FORCE_SWAP, tuning={"swap_pair": 2})
+    run = GpuRun(blk, inp["x"], routed=(torch.from_numpy(idx).cuda(), torch.from_numpy(gw).cuda()))
+    check_forward(run, host, 2, routed=True)
+    assert run.np("expert_counts").tolist() == [n, n, 0, 0]
+    blk.close()
+
+
 @pytest.mark.parametrize("fp8", [False, True])
 @pytest.mark.parametrize("T,d,f,E", [(64, 512, 1024, 8), (300, 256, 512, 8), (100, 256, 512, 2)])
 def test_swap_nb_cap(moe, T, d, f, E, fp8):
