@@ -243,6 +243,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
     const int warp = threadIdx.x / 32;
     const int lane = threadIdx.x % 32;
+    constexpr int kTlSlot = C::kG1 ? 2 : 3;
+    MOE_TL(kTlSlot, 0);
 
     if (warp == 0 && lane == 0) {
         ptx::prefetch_tmap(&tmA);
@@ -320,16 +322,18 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 TileInfo t0;
                 decode_tile<KIND, NB>(blockIdx.x, p, s_counts, s_offsets, t0);
                 pre = min(S, t0.nkb);
-                if (lane == 0)
+                if (lane == 0) {
                     for (int kb = 0; kb < pre; ++kb) {  // fresh stages: no empty-wait needed
                         ptx::mbar_arrive_expect_tx(&full[kb], C::kStageBytes);
                         const WCoord w = wcoord(p, (t0.kb0 + kb) * kBK, t0.a_row, t0.e);
                         ptx::tma_load_4d(&tmA, &full[kb], smem_a + kb * C::kABytes, 0, w.c1, w.c2, w.c3,
                                          w_hint);
                     }
+                }
             }
             ptx::pdl_wait();
         }
+        MOE_TL(kTlSlot, 1);
         bool first = true;
         for (int t = blockIdx.x; t < total; t += gridDim.x) {
             TileInfo ti;
@@ -521,6 +525,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     ptx::pdl_launch_dependents();
     ptx::tc_fence_before();
     __syncthreads();
+    MOE_TL(kTlSlot, 2);
     if (warp == 1) {
         ptx::tc_fence_after();
         ptx::tmem_dealloc(tmem_base, C::kAccStages * C::kAccCols);
@@ -1056,10 +1061,15 @@ struct SwapPairCfg {
     static constexpr int kBRows = NB / 2;
     static constexpr int kBBytes = kBRows * 128;
     static constexpr int kStageBytes = kABytes + kBBytes;
-    static constexpr int kStagesRaw = (kSmemBudget - 2048) / kStageBytes;
+    // w1/w3: h of the tile ([NB tokens][128 ffn columns] bf16) is staged in shared memory
+    // and leaves with one bulk copy per token row, so the TMEM accumulator is released
+    // right after its last tcgen05.ld (direct 2-byte global stores held the single-buffered
+    // accumulator for ~6 us per tile: 14 % of the kernel, r02 timing probe MOE_SPAIR_PROBE=3)
+    static constexpr int kHBytes = kG1 ? NB * 256 : 0;
+    static constexpr int kStagesRaw = (kSmemBudget - 2048 - kHBytes) / kStageBytes;
     static constexpr int kStagesCap = MOE_SPAIR_STAGES;
     static constexpr int kStages = kStagesRaw > kStagesCap ? kStagesCap : kStagesRaw;
-    static constexpr int kSmemBytes = kStages * kStageBytes + 2048;
+    static constexpr int kSmemBytes = kStages * kStageBytes + kHBytes + 2048;
     static constexpr bool kWide = kG1 && NB > 128;  // a and b accumulators of > 128 columns
     static constexpr int kAccStages = kWide ? 1 : 2;
     static constexpr int kAccCols = kWide ? 512 : 256;
@@ -1112,12 +1122,16 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                               const __grid_constant__ CUtensorMap tmB) {
     using C = SwapPairCfg<KIND, NB>;
     constexpr int S = C::kStages;
-    constexpr uint32_t kTx = 2u * C::kStageBytes;  // both CTAs' weight tile + token half per stage
+#ifndef MOE_SPAIR_PROBE
+#define MOE_SPAIR_PROBE 0  // timing probes (wrong results): 1 no MMAs, 2 no token loads, 3 no h/y stores
+#endif
+    constexpr uint32_t kTx = MOE_SPAIR_PROBE == 2 ? 2u * C::kABytes : 2u * C::kStageBytes;  // both CTAs' weight tile + token half per stage
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* smem_a = smem;
     uint8_t* smem_b = smem + S * C::kABytes;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * C::kStageBytes);
+    uint8_t* smem_h = smem + S * C::kStageBytes;  // w1/w3: [NB][128] bf16 h staging
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * C::kStageBytes + C::kHBytes);
     uint64_t* full = bars;            // leader's: both CTAs' loads complete here
     uint64_t* empty = bars + S;       // each CTA's (multicast commit)
     uint64_t* tmem_full = bars + 2 * S;
@@ -1130,6 +1144,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const int lane = threadIdx.x % 32;
     const uint32_t crank = ptx::cluster_ctarank();
     const bool leader = crank == 0;
+    constexpr int kTlSlot = C::kG1 ? 2 : 3;
+    MOE_TL(kTlSlot, 0);
 
     if (warp == 0 && lane == 0) {
         ptx::prefetch_tmap(&tmA);
@@ -1188,6 +1204,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 }
                 ptx::pdl_wait();
             }
+            MOE_TL(kTlSlot, 1);
             bool first = true;
             for (int t = cid; t < total; t += ncl) {
                 TileInfo ti;
@@ -1203,7 +1220,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                         const WCoord w = wcoord(p, kc, ti.a_row, ti.e);
                         ptx::tma_load_4d_pair(&tmA, fb, smem_a + stage * C::kABytes, 0, w.c1, w.c2, w.c3, w_hint);
                     }
-                    ptx::tma_load_2d_pair(&tmB, fb, smem_b + stage * C::kBBytes, kc, tok_row, ptx::kEvictLast);
+                    if (MOE_SPAIR_PROBE != 2)
+                        ptx::tma_load_2d_pair(&tmB, fb, smem_b + stage * C::kBBytes, kc, tok_row, ptx::kEvictLast);
                     if (++stage == S) { stage = 0; phase ^= 1; }
                 }
                 first = false;
@@ -1232,6 +1250,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
                     for (int kk = 0; kk < kBK / 16; ++kk) {
                         const uint32_t accum = (kb | kk) ? 1u : 0u;
+                        if (MOE_SPAIR_PROBE == 1 && kb > 0) break;
                         ptx::mma_bf16_pair(d_tmem, adesc + 2 * kk, bdesc + 2 * kk, idesc, accum);
                         if (KIND == kG1Swap) {  // w3 half of each CTA's 256-row tile (+16 KB)
                             const uint64_t adesc3 = ptx::make_smem_desc_sw128(sa + 128 * 128);
@@ -1261,9 +1280,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             const uint32_t tbase = tmem_base + acc * C::kAccCols + (static_cast<uint32_t>(q * 32) << 16);
             const int nchunks = (ti.n_valid + 15) / 16;
             if (KIND == kG1Swap) {
-                // row r = ffn index m*128 + r (a at cols [0,N), b at [kBOff, kBOff+N)); col n = token
-                __nv_bfloat16* h = static_cast<__nv_bfloat16*>(p.out) + static_cast<int64_t>(ti.b_row) * p.f +
-                                   ti.m_idx * 128 + r;
+                // row r = ffn index m*128 + r (a at cols [0,N), b at [kBOff, kBOff+N)); col n = token.
+                // h[n][r] -> smem row n (256 B per token: one warp writes 64 contiguous bytes per
+                // token), TMEM released, then warp q == 0 copies the valid token rows to global.
+                const uint32_t hs = ptx::smem_u32(smem_h) + 2u * (uint32_t)r;
+                if (q == 0) ptx::bulk_wait_read<0>();  // the previous tile's rows have left smem
+                ptx::named_bar_sync(1, 128);
 #pragma unroll 1
                 for (int c = 0; c < nchunks; ++c) {
                     uint32_t a[16], b[16];
@@ -1272,12 +1294,24 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                     ptx::tmem_wait_ld();
 #pragma unroll
                     for (int i = 0; i < 16; ++i) {
-                        const int n = c * 16 + i;
-                        if (n < ti.n_valid)
-                            h[static_cast<int64_t>(n) * p.f] =
-                                __float2bfloat16_rn(silu_f32(__uint_as_float(a[i])) * __uint_as_float(b[i]));
+                        const __nv_bfloat16 hv = __float2bfloat16_rn(silu_f32(__uint_as_float(a[i])) * __uint_as_float(b[i]));
+                        ptx::sts16(hs + (uint32_t)(c * 16 + i) * 256u, __bfloat16_as_ushort(hv));
                     }
                 }
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive_cluster(acc == 0 ? leader_empty0 : leader_empty1);
+                ptx::fence_proxy_async();  // this thread's h bytes -> visible to the bulk copies
+                ptx::named_bar_sync(1, 128);
+                if (q == 0 && MOE_SPAIR_PROBE != 3) {
+                    __nv_bfloat16* h = static_cast<__nv_bfloat16*>(p.out) + static_cast<int64_t>(ti.b_row) * p.f +
+                                       ti.m_idx * 128;
+                    for (int n = lane; n < ti.n_valid; n += 32)
+                        ptx::bulk_store(h + static_cast<int64_t>(n) * p.f, ptx::smem_u32(smem_h) + (uint32_t)n * 256u, 256);
+                    ptx::bulk_commit();
+                }
+                if (++acc == C::kAccStages) { acc = 0; acc_phase ^= 1; }
+                continue;
             } else {
                 // row r = hidden index m*128 + r; col n = token; fp32 partial of split s
                 const int drow = ti.m_idx * 128 + r;
@@ -1292,7 +1326,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
                         for (int i = 0; i < 16; ++i) {
                             const int n = c * 16 + i;
-                            if (n < ti.n_valid) y[static_cast<int64_t>(n) * p.d] = __uint_as_float(v[i]);
+                            if (n < ti.n_valid && MOE_SPAIR_PROBE != 3) y[static_cast<int64_t>(n) * p.d] = __uint_as_float(v[i]);
                         }
                     }
                 }
@@ -1302,11 +1336,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             if (lane == 0) ptx::mbar_arrive_cluster(acc == 0 ? leader_empty0 : leader_empty1);
             if (++acc == C::kAccStages) { acc = 0; acc_phase ^= 1; }
         }
+        if (KIND == kG1Swap && q == 0) ptx::bulk_wait<0>();  // h rows written before the grid completes
     }
     ptx::pdl_launch_dependents();
     ptx::tc_fence_before();
     __syncthreads();
     ptx::cluster_sync();  // the leader's MMAs wrote both CTAs' TMEM; the peer's arrives target the leader
+    MOE_TL(kTlSlot, 2);
     if (warp == 1) {
         ptx::tc_fence_after();
         ptx::tmem_dealloc_pair(tmem_base, C::kAccStages * C::kAccCols);

@@ -320,7 +320,9 @@ __global__ void __launch_bounds__(256) moe_router_mma_kernel(const RouteParams p
     const int g = warp / KS, kp = warp % KS;
     const int gid = lane >> 2, q = lane & 3;
 
+    MOE_TL(0, 0);
     ptx::pdl_wait();
+    MOE_TL(0, 1);
     if (p.early_trigger) ptx::pdl_launch_dependents();
 
     const int r0 = min(tok0 + g * 16 + gid, p.T - 1), r1 = min(tok0 + g * 16 + gid + 8, p.T - 1);
@@ -407,6 +409,7 @@ __global__ void __launch_bounds__(256) moe_router_mma_kernel(const RouteParams p
         s_idx[tb][1] = i1;
     }
     __syncthreads();
+    MOE_TL(0, 2);
     route_block_finish<256>(p, s_idx, ntok, tok0);
 }
 
@@ -527,8 +530,10 @@ __global__ void __launch_bounds__(kPermuteThreads) moe_permute_kernel(const Perm
     __shared__ int32_t s_pos[8][2];
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int tok0 = blockIdx.x * p.PT;
+    MOE_TL(1, 0);
     if (p.early_trigger) ptx::pdl_launch_dependents();
     ptx::pdl_wait();
+    MOE_TL(1, 1);
 #ifndef MOE_PERMUTE_EARLY_TRIGGER
 #define MOE_PERMUTE_EARLY_TRIGGER 1  // r01 A/B: 0.4522 -> 0.4510 ms per decode step
 #endif
@@ -606,6 +611,7 @@ __global__ void __launch_bounds__(kPermuteThreads) moe_permute_kernel(const Perm
                 }
         }
     }
+    MOE_TL(1, 2);
     ptx::pdl_launch_dependents();
 }
 
@@ -638,7 +644,9 @@ __global__ void __launch_bounds__(256) moe_combine_kernel(const CombineParams p)
     const int nxb = (p.d + 1024 * kCombineVec - 1) / (1024 * kCombineVec);
     const int t = blockIdx.x / nxb;
     const int c0 = (blockIdx.x % nxb) * 1024 * kCombineVec + threadIdx.x * 4;
+    MOE_TL(4, 0);
     ptx::pdl_wait();
+    MOE_TL(4, 1);
     int32_t pr[2];
     float w[2];
 #pragma unroll
@@ -698,6 +706,7 @@ __global__ void __launch_bounds__(256) moe_combine_kernel(const CombineParams p)
         }
     }
     if (p.peers) p2p_signal_last_block(p.p2p_ticket, p.peers, p.G, p.p2p_sig_off);  // TP reduce-scatter done
+    MOE_TL(4, 2);
     ptx::pdl_launch_dependents();
 }
 

@@ -1969,6 +1969,17 @@ moe_status moe_nccl_comm_destroy(void* comm) {
     return MOE_OK;
 }
 
+#if MOE_TIMELINE
+// Probe builds only (not declared in include/moe.h): copies the per-block timestamps of
+// the last forward ([5 slots][3 stamps][kTlBlocks] u64 ns) to `out` and clears them.
+MOE_API int moe_debug_timeline(unsigned long long* out) {
+    using moe::ptx::g_moe_tl;
+    if (cudaMemcpyFromSymbol(out, g_moe_tl, sizeof(g_moe_tl)) != cudaSuccess) return -1;
+    static unsigned long long zero[5 * 3 * moe::ptx::kTlBlocks];
+    return cudaMemcpyToSymbol(g_moe_tl, zero, sizeof(zero)) == cudaSuccess ? 0 : -1;
+}
+#endif
+
 }  // extern "C"
 
 namespace {

@@ -102,6 +102,19 @@ template <int N>
 __device__ __forceinline__ void bulk_wait() {
     asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
 }
+// plain bulk copy shared -> global of `bytes` (multiple of 16, both 16-byte aligned)
+__device__ __forceinline__ void bulk_store(void* gdst, uint32_t ssrc, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(reinterpret_cast<uint64_t>(gdst)),
+                 "r"(ssrc), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void sts16(uint32_t addr, uint16_t v) {
+    asm volatile("st.shared.u16 [%0], %1;" ::"r"(addr), "h"(v) : "memory");
+}
+// named barrier `id` over `n` threads (multiple of 32)
+__device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t n) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
 __device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
     asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
 }
@@ -401,6 +414,31 @@ __device__ __forceinline__ void mma_commit_pair(uint64_t* bar, uint16_t mask) {
         "h"(mask)
         : "memory");
 }
+
+// ------------------------------------------------------------------ timeline probe (debug builds)
+// MOE_TIMELINE=1 (scripts/exp/timeline.py, never the product build): thread 0 of each
+// block records %globaltimer at kernel entry (0), after its griddepcontrol.wait (1) and at
+// exit (2) for slot 0 router, 1 permute, 2 w1/w3 GEMM, 3 w2 GEMM, 4 combine; read back
+// with the probe-only export moe_debug_timeline (moe.cu).
+#ifndef MOE_TIMELINE
+#define MOE_TIMELINE 0
+#endif
+#if MOE_TIMELINE
+constexpr int kTlBlocks = 4096;
+__device__ unsigned long long g_moe_tl[5][3][kTlBlocks];
+#define MOE_TL(slot, what)                                                                     \
+    do {                                                                                       \
+        if (threadIdx.x == 0 && blockIdx.x < ::moe::ptx::kTlBlocks) {                          \
+            unsigned long long t_;                                                             \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                             \
+            ::moe::ptx::g_moe_tl[slot][what][blockIdx.x] = t_;                                 \
+        }                                                                                      \
+    } while (0)
+#else
+#define MOE_TL(slot, what) \
+    do {                   \
+    } while (0)
+#endif
 
 // ------------------------------------------------------------------ PDL
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }

@@ -1,0 +1,91 @@
+"""Per-block kernel timeline of one graph-replayed MoE forward (probe build only).
+
+Build:  python paper_2408_00008_b200/_build.py --force --out build_ab/libmoe_tl.so -DMOE_TIMELINE=1
+Run:    MOE_LIB=build_ab/libmoe_tl.so python scripts/exp/timeline.py T [tuning k=v,...] [--residual]
+
+The probe build stamps %globaltimer (ns) in thread 0 of every block at kernel entry,
+after griddepcontrol.wait and at exit (csrc/sm100.cuh MOE_TL). After back-to-back graph
+replays of one layer forward the last replay's stamps are read back and summarised per
+kernel: first/last entry, first/last post-wait, first/last exit, relative to the router's
+first entry -- where the step's time goes between and inside the kernels (PDL overlap,
+tails, waves). Synthetic Mixtral 8x7B layer (synth recipe), inputs resident in HBM.
+"""
+import ctypes
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, ROOT)
+import paper_2408_00008_b200 as moe  # noqa: E402
+import synth  # noqa: E402
+
+SLOTS = ["router", "permute", "gemm1", "gemm2", "combine"]
+TL_BLOCKS = 4096
+
+
+def main():
+    T = int(sys.argv[1]) if len(sys.argv) > 1 else 575
+    tuning = None
+    if len(sys.argv) > 2 and sys.argv[2] != "-":
+        tuning = {k: int(v) for k, v in (kv.split("=") for kv in sys.argv[2].split(","))}
+    flags = moe.MOE_FLAG_RESIDUAL if "--residual" in sys.argv else 0
+    lib = moe._lib
+    if not hasattr(lib, "moe_debug_timeline"):
+        raise SystemExit("not a MOE_TIMELINE build (set MOE_LIB=build_ab/libmoe_tl.so)")
+    lib.moe_debug_timeline.argtypes = [ctypes.c_void_p]
+    lib.moe_debug_timeline.restype = ctypes.c_int
+    d, f, E = 4096, 14336, 8
+    w = synth.make_weights(d, f, E, 1, 0, device="cuda", w2_scale=synth.STACK_W2_SCALE)
+    x = synth.make_tokens(T, d, 1, 0, device="cuda")
+    blk = moe.MoEBlock(w["wg"], w["w1"], w["w3"], w["w2"], top_k=2, max_tokens=T, flags=flags, tuning=tuning)
+    del w
+    out = torch.empty_like(x)
+
+    def step():
+        moe.moe_forward(blk.ctx, x, T, blk.router_w, blk.w13, blk.w2, out, None, torch.cuda.current_stream())
+
+    for _ in range(3):
+        step()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        step()
+    for _ in range(20):
+        g.replay()
+    torch.cuda.synchronize()
+    buf = np.zeros(5 * 3 * TL_BLOCKS, np.uint64)
+    lib.moe_debug_timeline(buf.ctypes.data)  # clears the stamps
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    for _ in range(20):
+        g.replay()
+    ev1.record()
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1) / 20
+    assert lib.moe_debug_timeline(buf.ctypes.data) == 0
+    tl = buf.reshape(5, 3, TL_BLOCKS).astype(np.int64)
+    t0 = tl[0, 0][tl[0, 0] > 0].min()
+    print(f"T={T} tuning={tuning} graph step {ms * 1000:.1f} us (20 replays); stamps of the last replay, us from router entry")
+    print(f"{'kernel':8s} {'blocks':>6s} {'entry first..last':>20s} {'waited first..last':>20s} {'exit first..last':>20s}")
+    ends = {}
+    for s, name in enumerate(SLOTS):
+        ent, wt, ex = tl[s]
+        m = ent > 0
+        if not m.any():
+            continue
+        r = lambda a: (a[a > 0] - t0) / 1000.0  # noqa: E731
+        e, w_, x_ = r(ent), r(wt), r(ex)
+        fmt = lambda a: f"{a.min():8.1f}..{a.max():8.1f}" if a.size else " " * 20  # noqa: E731
+        print(f"{name:8s} {int(m.sum()):6d} {fmt(e)} {fmt(w_)} {fmt(x_)}")
+        ends[name] = x_
+        if name in ("gemm1", "gemm2") and x_.size:
+            q = np.percentile(x_, [0, 10, 50, 90, 100])
+            print(f"         exit percentiles 0/10/50/90/100: " + " ".join(f"{v:.1f}" for v in q))
+    blk.close()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,4 @@
+# kernel timeline probe (MOE_TIMELINE build): decode T=64 and the stack layer T=575
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1
+export MOE_LIB=build_ab/libmoe_tl.so
+for a in "64 -" "575 -" "575 swap_pair=1" "575 - --residual"; do timeout -s KILL 300 python scripts/exp/timeline.py $a 2>&1 | tail -12; done
