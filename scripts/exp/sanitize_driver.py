@@ -74,7 +74,10 @@ if __name__ == "__main__":
     single(synth.MoEShape(T=64, d=1024, f=2560, E=8, k=2), 0x2)  # speculative L2 prefetch, auto grids
     single(synth.MoEShape(T=32, d=256, f=512, E=4, k=2), moe.MOE_FLAG_FP8_WEIGHTS)   # FP8, block-scaled w2
     single(synth.MoEShape(T=200, d=256, f=512, E=4, k=2), moe.MOE_FLAG_FP8_WEIGHTS, {"swap_nb_cap": 32})
-    single(synth.MoEShape(T=600, d=256, f=512, E=8, k=2), 0x2)   # statistical token tile 192 (T=575-like)
+    single(synth.MoEShape(T=600, d=256, f=512, E=8, k=2), 0x2)   # token tile 192 (T=575-like): CTA-pair swap
+    single(synth.MoEShape(T=600, d=256, f=512, E=8, k=2), 0x2, {"swap_pair": 1})  # same on single-CTA swap tiles
+    single(synth.MoEShape(T=300, d=256, f=512, E=8, k=2), 0x2)   # CTA-pair swap, token tile 128
+    single(synth.MoEShape(T=1000, d=320, f=512, E=8, k=2), 0x2, {"swap_pair": 2})  # pair tile 256 + 2nd tiles, padded d
     for par in ("ep", "tp"):
         for p2p in (False, True):
             group(par, 2, p2p)
