@@ -666,7 +666,7 @@ def run_stack(args, world, rank, local):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                      "frac": achieved / peaks["hbm_gbs"], "traffic": load_traffic("stack")[0] if par == "none" else None,
                      "algorithmic": g1_bytes,
-                     "kernel": "moe_gemm_kernel w1/w3 + SwiGLU (mean over the 32 layers)",
+                     "kernel": "w1/w3 + SwiGLU GEMM, mean over the 32 layers (T >= 256: moe_gemm_swap_pair_kernel<kG1Swap,192> on CTA pairs)",
                      "peak_src": peaks["src"] + " (MEASURED_PEAKS.json hbm_gbs)",
                      "traffic_src": load_traffic("stack")[1] if par == "none" else None},
         "step_roofline_frac": step_bytes / (ms * 1e-3) / 1e9 / peaks["hbm_gbs"],
