@@ -1433,6 +1433,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const int warp = threadIdx.x / 32;
     const int lane = threadIdx.x % 32;
     const int w_tiles = kG1 ? (2 * p.f) / 256 : p.d / 128;  // weight tiles per expert
+    MOE_TL(kG1 ? 2 : 3, 0);
     if (warp == 0 && lane == 0) {
         ptx::prefetch_tmap(&tmA8);
         ptx::prefetch_tmap(&tmB8);
@@ -1483,6 +1484,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     __syncthreads();
     ptx::tc_fence_after();
     ptx::pdl_wait();
+    MOE_TL(kG1 ? 2 : 3, 1);
     const uint32_t tmem_base = *tmem_base_slot;
     int total = 0;
     for (int e = 0; e < p.E; ++e) total += tiles_of<KIND, NB>(s_counts[e], p);
@@ -1656,6 +1658,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     ptx::pdl_launch_dependents();
     ptx::tc_fence_before();
     __syncthreads();
+    MOE_TL(kG1 ? 2 : 3, 2);
     if (warp == 1) {
         ptx::tc_fence_after();
         ptx::tmem_dealloc(tmem_base, 512);

@@ -1,7 +1,7 @@
 """Per-block kernel timeline of one graph-replayed MoE forward (probe build only).
 
 Build:  python paper_2408_00008_b200/_build.py --force --out build_ab/libmoe_tl.so -DMOE_TIMELINE=1
-Run:    MOE_LIB=build_ab/libmoe_tl.so python scripts/exp/timeline.py T [tuning k=v,...] [--residual]
+Run:    MOE_LIB=build_ab/libmoe_tl.so python scripts/exp/timeline.py T [tuning k=v,...|-] [--residual] [--fp8]
 
 The probe build stamps %globaltimer (ns) in thread 0 of every block at kernel entry,
 after griddepcontrol.wait and at exit (csrc/sm100.cuh MOE_TL). After back-to-back graph
@@ -32,6 +32,7 @@ def main():
     if len(sys.argv) > 2 and sys.argv[2] != "-":
         tuning = {k: int(v) for k, v in (kv.split("=") for kv in sys.argv[2].split(","))}
     flags = moe.MOE_FLAG_RESIDUAL if "--residual" in sys.argv else 0
+    fp8 = "--fp8" in sys.argv
     lib = moe._lib
     if not hasattr(lib, "moe_debug_timeline"):
         raise SystemExit("not a MOE_TIMELINE build (set MOE_LIB=build_ab/libmoe_tl.so)")
@@ -39,13 +40,17 @@ def main():
     lib.moe_debug_timeline.restype = ctypes.c_int
     d, f, E = 4096, 14336, 8
     w = synth.make_weights(d, f, E, 1, 0, device="cuda", w2_scale=synth.STACK_W2_SCALE)
+    if fp8:  # E4M3 weights with per-row scales (bench.py --fp8)
+        flags |= moe.MOE_FLAG_FP8_WEIGHTS
+        for n in ("w1", "w3", "w2"):
+            w[n] = synth.quantize_fp8_rows(w[n])
     x = synth.make_tokens(T, d, 1, 0, device="cuda")
     blk = moe.MoEBlock(w["wg"], w["w1"], w["w3"], w["w2"], top_k=2, max_tokens=T, flags=flags, tuning=tuning)
     del w
     out = torch.empty_like(x)
 
     def step():
-        moe.moe_forward(blk.ctx, x, T, blk.router_w, blk.w13, blk.w2, out, None, torch.cuda.current_stream())
+        blk.forward(x, out, stream=torch.cuda.current_stream())
 
     for _ in range(3):
         step()

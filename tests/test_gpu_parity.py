@@ -1064,6 +1064,22 @@ def test_fp8_weights(moe, T, d, f, E):
     blk.close()
 
 
+@pytest.mark.parametrize("T", [16, 64, 128])
+def test_fp8_skewed(moe, T):
+    """FP8 decode under skewed routing (expert 0 ~4x as popular, synth.make_tokens_skewed):
+    uneven token tiles per expert on the 8-bit GEMMs, parity against the exact-dequant
+    oracle."""
+    shape = synth.MoEShape(T=T, d=512, f=1024, E=8, k=2)
+    inp, qs, host = _fp8_inputs(shape, 900 + T)
+    x = synth.make_tokens_skewed(T, shape.d, inp["wg"], seed=901 + T, device="cuda")
+    host["x"] = x.float().cpu().numpy()
+    blk = moe.MoEBlock(inp["wg"], qs["w1"], qs["w3"], qs["w2"], top_k=2, max_tokens=T,
+                       flags=moe.MOE_FLAG_FP8_WEIGHTS)
+    run = GpuRun(blk, x)
+    check_forward(run, host, 2)
+    blk.close()
+
+
 @pytest.mark.parametrize("T", [64, 300])
 def test_fp8_two_term_tokens(moe, T):
     """FP8 weights, both GEMMs on 8-bit MMAs: tokens split into two E4M3 terms with a
