@@ -476,13 +476,17 @@ def run_shard(args):
     g1_f, g2_f = 2 * A * 2 * d * f_l, 2 * A * d * f_l
     decode = args.config != "prefill"  # decode and the T = 575 stack layer are HBM-bound
     kern = {}
-    for name, b, fl in (("gemm1_w13_swiglu", g1_b, g1_f), ("gemm2_w2", g2_b, g2_f)):
-        t = per[name] * 1e-3
+    # fused FFN (tuning fused): one kernel in the w1/w3 slot carries both GEMMs
+    fused = kt["gemm2_w2"][1] == 0 and kt["gemm1_w13_swiglu"][1] > 0
+    kinds = ((("gemm1_w13_swiglu", "ffn_fused", g1_b + g2_b, g1_f + g2_f),) if fused else
+             (("gemm1_w13_swiglu", "gemm1_w13_swiglu", g1_b, g1_f), ("gemm2_w2", "gemm2_w2", g2_b, g2_f)))
+    for slot, name, b, fl in kinds:
+        t = per[slot] * 1e-3
         if decode:
-            kern[name] = {"ms": round(per[name], 5), "GB/s": b / t / 1e9, "frac_hbm": b / t / 1e9 / peaks["hbm_gbs"],
+            kern[name] = {"ms": round(per[slot], 5), "GB/s": b / t / 1e9, "frac_hbm": b / t / 1e9 / peaks["hbm_gbs"],
                           "frac_read_stream": b / t / 1e9 / READ_STREAM_GBS, "bytes": b}
         else:
-            kern[name] = {"ms": round(per[name], 5), "TFLOP/s": fl / t / 1e12,
+            kern[name] = {"ms": round(per[slot], 5), "TFLOP/s": fl / t / 1e12,
                           "frac_sustained": fl / t / 1e12 / peaks["bf16_tflops_sustained"], "flops": fl}
     step_bytes = touched * 3 * f_l * d * 2 + 2 * T_run * d * 2
     line = {"metric": "per-rank shard kernels (one GPU)", "shard": args.shard, "config": args.config,
@@ -908,11 +912,15 @@ def main():
     decode = args.config == "decode"
     dom = "gemm1_w13_swiglu"
     dom_ms = per[dom]
+    # fused FFN (tuning fused): the w1/w3 slot holds one kernel that streams both GEMMs
+    fused = ktimes["gemm2_w2"][1] == 0 and ktimes[dom][1] > 0
+    dom_bytes = alg["g1_bytes"] + (alg["g2_bytes"] if fused else 0)
     if decode:
-        achieved = alg["g1_bytes"] / (dom_ms * 1e-3) / 1e9
+        achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": achieved / peaks["hbm_gbs"], "traffic": None,
                 "kernel": ("moe_gemm_fp8x_kernel<kG1Swap> (FP8 w1/w3 + SwiGLU, kind::f8f6f4)" if args.fp8
+                           else "moe_ffn_fused_kernel (w1/w3 + SwiGLU and w2 in one launch)" if fused
                            else "moe_gemm_kernel<kG1Swap> (w1/w3 + SwiGLU)"),
                 "peak_src": peaks["src"] + " (MEASURED_PEAKS.json hbm_gbs)"}
         step_frac = alg["bytes"] / (ms * 1e-3) / 1e9 / peaks["hbm_gbs"]
@@ -931,10 +939,12 @@ def main():
         step_frac = alg["flops"] / (ms * 1e-3) / 1e12 / pk
     tr, tr_src = load_traffic(args.config + ("_fp8" if args.fp8 else "")) if world == 1 and par == "none" \
         else (None, None)
+    if fused:
+        tr = None  # traffic.json holds the two-kernel path's K3 capture
     roof["traffic"] = tr
     if tr is not None:
         roof["traffic_src"] = tr_src
-        roof["algorithmic"] = alg["g1_bytes"] if decode else alg["g1_flops"]
+        roof["algorithmic"] = dom_bytes if decode else alg["g1_flops"]
     tok_s = Tg / (ms * 1e-3) if par in ("ep", "tp", "hybrid") else T * world / (ms * 1e-3)
     kernel_share = {n: round(per[n] / ms_prof, 4) for n in per if ktimes[n][1]}
 

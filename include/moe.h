@@ -136,7 +136,15 @@ typedef struct moe_tuning {
     int32_t swap_pair;      /* swap-AB GEMMs on CTA pairs (cta_group::2, token tile split over
                                the pair): 0 auto (token tiles >= 128 rows), 1 off, 2 always
                                where the shape allows (w1/w3 needs ffn/tp_world % 256 == 0) */
-    int32_t reserved[9];    /* must be zero                                                  */
+    int32_t fused;          /* decode FFN as ONE persistent kernel (w1/w3 + SwiGLU and w2 tiles
+                               claimed from one device work counter, w2 tiles waiting per
+                               128-column h tile): 0 auto, 1 off, 2 on where the
+                               shape allows (bf16, token tile <= 128 rows, hidden % 256 == 0) */
+    int32_t fused_splits;   /* K splits of the fused kernel's w2 tiles, 1..8 (0: auto)        */
+    int32_t fused_stages;   /* pipeline stages of the fused kernel, 2..8 (0: all that fit)     */
+    int32_t fused_uniform;  /* 1: equal w2 K splits in whole ffn tiles (the two-kernel path's split,
+                               bit-identical results); 0: tapered splits, the last ones shortest */
+    int32_t reserved[5];    /* must be zero                                                  */
 } moe_tuning;
 
 typedef struct {

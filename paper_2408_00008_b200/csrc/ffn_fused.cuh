@@ -1,0 +1,524 @@
+// ffn_fused.cuh -- the decode expert FFN (steps a7 + a8 of SURVEY.md Sec. 8(a)) as ONE
+// persistent kernel: the w1/w3 GEMM + SwiGLU tiles and the w2 GEMM tiles of every local
+// expert are claimed from a single device-side work counter, and a w2 tile streams its
+// weights as soon as it is claimed, waiting only for the h columns it multiplies.
+//
+//   GEMM1 (+SwiGLU): h[r, i] = bf16_rne( silu(x_r . W1_e[i,:]) * (x_r . W3_e[i,:]) )
+//   GEMM2          : y_s[r, c] = sum_{i in split s} h[r, i] * W2_e[c, i]   (fp32 partial s)
+// Same arithmetic, K order and partial-sum layout as the two-kernel swap-AB path
+// (moe_gemm_kernel<kG1Swap> / <kG2Swap>, gemm_sm100.cuh): the combine adds the split
+// partials in a fixed order, so results do not depend on which path ran
+// (R1, R7; PAPER.md prints no formula for the block).
+//
+// Why: at decode the block is a weight stream (2.82 GB per Mixtral layer). Two kernels
+// each pay a ramp and a tail (the w1/w3 GEMM's CTAs exit over ~10 us and the w2 GEMM
+// only starts streaming after the last one; profiles/r02/experiments/timeline_r02.log),
+// and at the per-rank shapes of EP/TP (E/G experts or f/G columns: 112-256 short units)
+// those edges are a third of the step. Here the stream never stops: a CTA that runs out
+// of w1/w3 tiles claims w2 tiles, whose dependency is the finished h tiles of that
+// expert, tracked per (expert, 128-column ffn tile) by counters in global memory.
+//
+// Tiles (swap-AB: weights are the M operand, the expert's tokens the N operand):
+//   G1 tile (e, m, n): W13 rows of ffn tile m (128 w1 rows + 128 w3 rows) x token tile n
+//       -> h[:, 128m .. 128m+128) of the tile's tokens; K = d.
+//   G2 tile (s, e, m2, n): W2 rows [256 m2, 256 m2 + 256) (two M=128 MMAs sharing the token
+//       operand, so h is read from L2 once per 256 weight rows) x token tile n, K = the
+//       ffn tiles [split_j[s], split_j[s+1]) of split s -> y partial s.
+// Both tile kinds stage 256 weight rows x 64 K (32 KB, one TMA box) + NB token rows x 64 K
+// per pipeline stage and accumulate into two TMEM column blocks ([0, NB) and [128, 128+NB))
+// of one of two accumulator slots, so one stage ring and one MMA loop serve both.
+//
+// Work order: G1 tiles (expert-major, ffn tile, token tile fastest), then G2 tiles
+// (split-major, expert, weight tile, token tile fastest; splits tapered so the last are short). Every tile is claimed with an
+// atomicAdd on sched[0] by the producer lane of a RUNNING CTA, so a claimed G2 tile only
+// ever waits for G1 tiles claimed earlier by running CTAs: no dependency on a CTA that is
+// not resident, deadlock-free at any grid size. The claimed index is handed to the MMA
+// and epilogue warps through a small shared-memory ring (tile_full / tile_empty).
+//
+// h hand-off between CTAs: each G1 epilogue thread stores its h values (generic proxy),
+// fences them towards the async proxy, the four epilogue warps meet on a named barrier,
+// and one thread publishes with __threadfence + atomicAdd(ready[e][m]). A G2 producer
+// reads the counters relaxed (batched), and when every ffn tile its next stages need is
+// complete: fence.acq_rel.gpu (acquire pattern) + fence.proxy.async.global, then the TMA
+// loads of h. Weight loads of a G2 tile never wait: they run up to the ring depth ahead
+// of the h loads.
+//
+// sched[0] (claims), sched[1] (CTA exits) and ready[] are zero between launches: the last
+// CTA to exit resets them (graph-replay safe, no host work).
+#pragma once
+
+#include "gemm_sm100.cuh"
+
+namespace moe {
+
+struct FusedParams {
+    GemmParams g;            // counts / offsets / E / d / f / h (g.out) / w_nt (W13 tiles per expert)
+    float* y;                // fp32 partials [splits][rows, d]
+    int64_t y_split_stride;  // elements between split buffers
+    int32_t splits;          // S: K splits of the w2 tiles (over whole ffn tiles)
+    int32_t w2_nt;           // W2 tiles (128 rows) per expert in the tiled layout
+    int32_t* sched;          // [4] claims, CTA exits, finished G1 tiles (zero between launches)
+    int32_t* ready;          // [E * (f/128)] finished G1 token tiles per (expert, ffn tile)
+    int32_t stages;          // pipeline stages used (1..kStages; 0 = all that fit)
+    int32_t split_j[9];      // ffn-tile boundaries of the w2 K splits: 0 = j_0 < .. < j_S = f/128
+};
+
+constexpr int kFusedTileRing = 8;  // claimed-tile hand-off ring depth
+constexpr int kFusedEpiBar = 1;    // named barrier of the 4 epilogue warps
+
+template <int NB>
+struct FusedCfg {
+    static constexpr int kABytes = 256 * 128;       // 256 weight rows x 64 bf16
+    static constexpr int kBBytes = NB * 128;        // NB token rows x 64 bf16
+    static constexpr int kStageBytes = kABytes + kBBytes;
+    static constexpr int kStages = (kSmemBudget - 2048) / kStageBytes > 8 ? 8 : (kSmemBudget - 2048) / kStageBytes;
+    static constexpr int kSmemBytes = kStages * kStageBytes + 2048;
+    static_assert(NB >= 16 && NB <= 128 && NB % 16 == 0, "fused tile: a/b accumulators of <= 128 columns");
+    static_assert(kStages >= 3, "pipeline too shallow");
+};
+
+struct FusedTile {
+    bool g1;
+    int32_t e, rows, b_row;  // expert, its rows, first token row of the tile (permuted buffer)
+    int32_t m;               // G1: ffn tile; G2: 256-row weight tile
+    int32_t s;               // G2: split
+    int32_t kb0, nkb;        // K blocks (64 columns) of the tile
+    int32_t n_valid;         // valid token columns
+    int32_t nt;              // token tiles of the expert
+};
+
+__device__ __forceinline__ int fused_nt(int rows, int NB) { return rows > 0 ? (rows + NB - 1) / NB : 0; }
+
+// Tile lists (every role decodes the same claimed index t):
+//   [0, total1)      G1 tiles, expert-major: (e, m, n), token tile fastest
+//   [total1, total)  G2 tiles, split-major: (s, e, m256, n). Split s covers the ffn tiles
+//                    [split_j[s], split_j[s+1]) -- by default tapered (the host gives the
+//                    first splits the most K and the last the least), so the stream ends on
+//                    the shortest tiles and the CTAs' exits bunch up.
+template <int NB>
+__device__ __forceinline__ void fused_decode(int t, const FusedParams& p, const int32_t* s_counts,
+                                             const int32_t* s_offsets, int total1, int per_split, FusedTile& ti) {
+    const int wt = p.g.f / 128;
+    const int mt2 = p.g.d / 256;
+    ti.g1 = t < total1;
+    ti.s = 0;
+    if (!ti.g1) {
+        t -= total1;
+        ti.s = t / per_split;
+        t -= ti.s * per_split;
+    }
+    int e = 0;
+    for (; e < p.g.E; ++e) {
+        const int nt = fused_nt(s_counts[e], NB);
+        const int n = nt * (ti.g1 ? wt : mt2);
+        if (t < n) break;
+        t -= n;
+    }
+    ti.e = e;
+    ti.rows = s_counts[e];
+    ti.nt = fused_nt(ti.rows, NB);
+    const int n_idx = t % ti.nt;
+    ti.m = t / ti.nt;
+    if (ti.g1) {
+        ti.kb0 = 0;
+        ti.nkb = p.g.d / 64;
+    } else {
+        ti.kb0 = 2 * p.split_j[ti.s];
+        ti.nkb = 2 * (p.split_j[ti.s + 1] - p.split_j[ti.s]);
+    }
+    ti.b_row = s_offsets[e] + n_idx * NB;
+    const int rem = ti.rows - n_idx * NB;
+    ti.n_valid = rem < NB ? rem : NB;
+}
+
+__device__ __forceinline__ int ld_relaxed_gpu(const int32_t* p) {
+    int v;
+    asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_global() {
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+// tmW13: W13 tiled map (box 64 x 256 rows); tmX: permuted tokens (box 64 x NB);
+// tmW2: W2 tiled map with 2-tile boxes (64 x 128 rows x 1 x 2 = 256 rows); tmH: h (box 64 x NB)
+template <int NB>
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    moe_ffn_fused_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmW13,
+                         const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW2,
+                         const __grid_constant__ CUtensorMap tmH) {
+    using C = FusedCfg<NB>;
+    constexpr int S = C::kStages;
+    constexpr int R = kFusedTileRing;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* smem_a = smem;
+    uint8_t* smem_b = smem + S * C::kABytes;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * C::kStageBytes);
+    uint64_t* full = bars;
+    uint64_t* empty = bars + S;
+    uint64_t* tmem_full = bars + 2 * S;
+    uint64_t* tmem_empty = bars + 2 * S + 2;
+    uint64_t* tile_full = bars + 2 * S + 4;
+    uint64_t* tile_empty = tile_full + R;
+    int32_t* s_tile = reinterpret_cast<int32_t*>(tile_empty + R);       // [R]
+    uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(s_tile + R);  // [1]
+    int32_t* s_last = reinterpret_cast<int32_t*>(tmem_base_slot + 1);   // [1]
+    int32_t* s_counts = s_last + 2;                                      // [32]
+    int32_t* s_offsets = s_counts + 32;                                  // [33]
+
+    const int warp = threadIdx.x / 32;
+    const int lane = threadIdx.x % 32;
+    // ring depth in use: fewer bytes in flight per SM can stream faster when every SM
+    // streams (scripts/exp/read_bw.cu: 3-4 stages of 32 KB peak)
+    const int SR = p.stages > 0 && p.stages < S ? p.stages : S;
+    MOE_TL(2, 0);
+#if MOE_TIMELINE
+    // probe build: slot 3 = [first w2-tile claim, last (failing) claim, entry + ns spent
+    // waiting for h tiles] of this CTA's producer
+    const unsigned long long tl_entry = ptx::tl_now();
+    unsigned long long tl_stall = 0;
+    bool tl_g2 = false;
+#endif
+
+    if (warp == 0 && lane == 0) {
+        ptx::prefetch_tmap(&tmW13);
+        ptx::prefetch_tmap(&tmX);
+        ptx::prefetch_tmap(&tmW2);
+        ptx::prefetch_tmap(&tmH);
+        for (int i = 0; i < S; ++i) {
+            ptx::mbar_init(&full[i], 1);
+            ptx::mbar_init(&empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            ptx::mbar_init(&tmem_full[i], 1);
+            ptx::mbar_init(&tmem_empty[i], 4);
+        }
+        for (int i = 0; i < R; ++i) {
+            ptx::mbar_init(&tile_full[i], 1);
+            ptx::mbar_init(&tile_empty[i], 5);  // MMA lane + 4 epilogue warps
+        }
+        ptx::fence_mbar_init();
+    }
+    if (warp == 1) {
+        ptx::tmem_alloc(tmem_base_slot, 512);
+        ptx::tmem_relinquish();
+    }
+    // Before the routing is known (PDL: the router / permute may still run): prefetch into
+    // L2 the first K blocks of the w1/w3 tile this CTA most likely claims first, assuming
+    // every expert holds one token tile (tile b = expert b / wt, ffn tile b % wt). A wrong
+    // guess only costs the prefetch; whoever claims the tile reads it from L2. Issued by an
+    // epilogue lane (idle until the first accumulator is ready): a CTA that starts late can
+    // stall several us issuing prefetches into a busy memory system, and the producer must
+    // not wait for that (timeline r03: post-wait stamps up to 9 us late when lane 0 issued).
+    if (p.g.spec_l2 > 0 && threadIdx.x == 160) {
+        const int wt = p.g.f / 128;
+        if ((int)blockIdx.x < p.g.E * wt) {
+            const int e = blockIdx.x / wt, m = blockIdx.x % wt;
+            const int nk = min(p.g.spec_l2, p.g.d / kBK);
+            for (int kb = 0; kb < nk; ++kb) {
+                const WCoord w = wcoord(p.g, kb * kBK, m * 256, e);
+                ptx::tma_prefetch_l2_4d(&tmW13, 0, w.c1, w.c2, w.c3);
+            }
+        }
+    }
+    ptx::pdl_wait();
+    MOE_TL(2, 1);
+    if (threadIdx.x < 32) {
+        for (int e = threadIdx.x; e < p.g.E; e += 32) {
+            s_counts[e] = p.g.counts[e];
+            s_offsets[e] = p.g.offsets[e];
+        }
+    }
+    // setup hand-off: producer + MMA warps sync with each other (barrier 2) and release the
+    // epilogue warps (barrier 3) without waiting for them
+    ptx::tc_fence_before();
+    if (warp < 2) {
+        ptx::named_bar_sync(2, 64);
+        ptx::named_bar_arrive(3, 192);
+    } else {
+        ptx::named_bar_sync(3, 192);
+    }
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = *tmem_base_slot;
+
+    const int wt = p.g.f / 128;
+    int total1 = 0, per_split = 0;
+    for (int e = 0; e < p.g.E; ++e) {
+        const int nt = fused_nt(s_counts[e], NB);
+        total1 += nt * wt;
+        per_split += nt * (p.g.d / 256);
+    }
+    const int total = total1 + per_split * p.splits;
+    const uint64_t w_hint = p.g.hint_a ? p.g.hint_a : ptx::kEvictFirst;
+
+    if (warp == 0) {
+        // ---------------------------------------------------------------- TMA producer (lane 0)
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            int ts = 0;
+            uint32_t tph = 0;
+            bool all_ready = false;  // every G1 tile of this launch finished (sched[2] == total1), acquired
+            // A tile is claimed only when the previous one's loads are all issued (the ring still
+            // holds SR stages of it, which hides the atomic's round trip). Claiming ahead was
+            // measured slower: a CTA then holds two tiles at the end of the stream (tail) and,
+            // at EP ranks, two waiting w2 tiles while G1 tiles run (profiles/r03).
+            while (true) {
+                const int t = atomicAdd(&p.sched[0], 1);
+                ptx::mbar_wait(&tile_empty[ts], tph ^ 1);
+                s_tile[ts] = t;
+                ptx::mbar_arrive(&tile_full[ts]);
+                if (++ts == R) { ts = 0; tph ^= 1; }
+#if MOE_TIMELINE
+                if (blockIdx.x < ptx::kTlBlocks) {
+                    if (t >= total) {
+                        ptx::g_moe_tl[3][1][blockIdx.x] = ptx::tl_now();
+                        ptx::g_moe_tl[3][2][blockIdx.x] = tl_entry + tl_stall;
+                    } else if (t >= total1 && !tl_g2) {
+                        tl_g2 = true;
+                        ptx::g_moe_tl[3][0][blockIdx.x] = ptx::tl_now();
+                    }
+                }
+#endif
+                if (t >= total) break;
+                FusedTile ti;
+                fused_decode<NB>(t, p, s_counts, s_offsets, total1, per_split, ti);
+                if (!ti.g1 && !all_ready && ld_relaxed_gpu(&p.sched[2]) >= total1) {
+                    fence_acq_rel_gpu();
+                    fence_proxy_async_global();
+                    all_ready = true;
+                }
+                if (ti.g1 || all_ready) {
+                    for (int kb = 0; kb < ti.nkb; ++kb) {
+                        ptx::mbar_wait(&empty[stage], phase ^ 1);
+                        ptx::mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
+                        uint8_t* sa = smem_a + stage * C::kABytes;
+                        uint8_t* sb = smem_b + stage * C::kBBytes;
+                        if (ti.g1) {
+                            const WCoord w = wcoord(p.g, kb * kBK, ti.m * 256, ti.e);
+                            ptx::tma_load_4d(&tmW13, &full[stage], sa, 0, w.c1, w.c2, w.c3, w_hint);
+                            ptx::tma_load_2d(&tmX, &full[stage], sb, kb * kBK, ti.b_row, ptx::kEvictLast);
+                        } else {
+                            const int kq = ti.kb0 + kb;
+                            ptx::tma_load_4d(&tmW2, &full[stage], sa, 0, 0, kq, 2 * ti.m + ti.e * p.w2_nt, w_hint);
+                            ptx::tma_load_2d(&tmH, &full[stage], sb, kq * kBK, ti.b_row, ptx::kEvictLast);
+                        }
+                        if (++stage == SR) { stage = 0; phase ^= 1; }
+                    }
+                } else {
+                    // Some G1 tiles still run: h loads of K block q need ffn tile (kb0 + q) / 2 of
+                    // expert e finished by all of its token tiles; weight loads run up to the ring
+                    // depth ahead. ok = consecutive finished ffn tiles from j0 (relaxed reads,
+                    // then fence.acq_rel = acquire, then the proxy fence for the TMA reads).
+                    const int32_t* rdy = p.ready + ti.e * wt + ti.kb0 / 2;
+                    const int nj = ti.nkb / 2;
+                    int ok = 0;
+                    auto refresh = [&]() {
+                        const int ok0 = ok;
+                        while (ok < nj) {
+                            int v[8];
+#pragma unroll
+                            for (int i = 0; i < 8; ++i) v[i] = ok + i < nj ? ld_relaxed_gpu(rdy + ok + i) : 0;
+                            int c = 0;
+#pragma unroll
+                            for (int i = 0; i < 8; ++i)
+                                if (c == i && ok + i < nj && v[i] >= ti.nt) ++c;
+                            ok += c;
+                            if (c < 8) break;
+                        }
+                        if (ok > ok0) {
+                            fence_acq_rel_gpu();
+                            fence_proxy_async_global();
+                        }
+                    };
+                    const int st0 = stage;
+                    int bq = 0;  // K blocks whose h load is issued
+                    auto issue_b = [&](int q) {
+                        const int sq = (st0 + q) % SR;
+                        ptx::tma_load_2d(&tmH, &full[sq], smem_b + sq * C::kBBytes, (ti.kb0 + q) * kBK, ti.b_row,
+                                         ptx::kEvictLast);
+                    };
+                    auto wait_ready = [&](int q) {
+#if MOE_TIMELINE
+                        const unsigned long long w0 = q / 2 >= ok ? ptx::tl_now() : 0;
+#endif
+                        while (q / 2 >= ok) {
+                            refresh();
+                            if (q / 2 >= ok) __nanosleep(64);
+                        }
+#if MOE_TIMELINE
+                        if (w0) tl_stall += ptx::tl_now() - w0;
+#endif
+                    };
+                    for (int q = 0; q < ti.nkb; ++q) {
+                        // the stage about to be reused must have its h load in flight (its MMA
+                        // frees it only after both operands arrived)
+                        while (bq <= q - SR) {
+                            wait_ready(bq);
+                            issue_b(bq++);
+                        }
+                        ptx::mbar_wait(&empty[stage], phase ^ 1);
+                        ptx::mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
+                        uint8_t* sa = smem_a + stage * C::kABytes;
+                        const int kq = ti.kb0 + q;
+                        ptx::tma_load_4d(&tmW2, &full[stage], sa, 0, 0, kq, 2 * ti.m + ti.e * p.w2_nt, w_hint);
+                        // weights of the first stages go out before the first readiness check
+                        if (q == SR - 1 || q == ti.nkb - 1 || (q >= SR && (q & 3) == 3)) {
+                            if (bq / 2 >= ok) refresh();
+                        }
+                        while (bq <= q && bq / 2 < ok) issue_b(bq++);
+                        if (++stage == SR) { stage = 0; phase ^= 1; }
+                    }
+                    while (bq < ti.nkb) {
+                        wait_ready(bq);
+                        issue_b(bq++);
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------------------------------------------------------- MMA issuer (lane 0)
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            int ts = 0;
+            uint32_t tph = 0;
+            while (true) {
+                ptx::mbar_wait(&tile_full[ts], tph);
+                const int t = s_tile[ts];
+                ptx::mbar_arrive(&tile_empty[ts]);
+                if (++ts == R) { ts = 0; tph ^= 1; }
+                if (t >= total) break;
+                FusedTile ti;
+                fused_decode<NB>(t, p, s_counts, s_offsets, total1, per_split, ti);
+                const uint32_t n_mma = (uint32_t)((ti.n_valid + 15) / 16 * 16);
+                const uint32_t idesc = ptx::make_idesc_bf16(128, n_mma);
+                const uint32_t d_tmem = tmem_base + acc * 256;
+                ptx::mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
+                ptx::tc_fence_after();
+                for (int kb = 0; kb < ti.nkb; ++kb) {
+                    ptx::mbar_wait(&full[stage], phase);
+                    ptx::tc_fence_after();
+                    const uint32_t sa = ptx::smem_u32(smem_a + stage * C::kABytes);
+                    const uint32_t sb = ptx::smem_u32(smem_b + stage * C::kBBytes);
+                    const uint64_t adesc = ptx::make_smem_desc_sw128(sa);
+                    const uint64_t adesc2 = ptx::make_smem_desc_sw128(sa + 128 * 128);
+                    const uint64_t bdesc = ptx::make_smem_desc_sw128(sb);
+#pragma unroll
+                    for (int kk = 0; kk < kBK / 16; ++kk) {
+                        const uint32_t accum = (kb | kk) ? 1u : 0u;
+                        ptx::mma_bf16(d_tmem, adesc + 2 * kk, bdesc + 2 * kk, idesc, accum);
+                        ptx::mma_bf16(d_tmem + 128, adesc2 + 2 * kk, bdesc + 2 * kk, idesc, accum);
+                    }
+                    ptx::mma_commit(&empty[stage]);
+                    if (++stage == SR) { stage = 0; phase ^= 1; }
+                }
+                ptx::mma_commit(&tmem_full[acc]);
+                if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+            }
+        }
+    } else {
+        // ---------------------------------------------------------------- epilogue (warps 2..5)
+        const int q = warp & 3;
+        const int r = q * 32 + lane;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        int ts = 0;
+        uint32_t tph = 0;
+        while (true) {
+            ptx::mbar_wait(&tile_full[ts], tph);
+            const int t = s_tile[ts];
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&tile_empty[ts]);
+            if (++ts == R) { ts = 0; tph ^= 1; }
+            if (t >= total) break;
+            FusedTile ti;
+            fused_decode<NB>(t, p, s_counts, s_offsets, total1, per_split, ti);
+            ptx::mbar_wait(&tmem_full[acc], acc_phase);
+            ptx::tc_fence_after();
+            const uint32_t tbase = tmem_base + acc * 256 + (static_cast<uint32_t>(q * 32) << 16);
+            const int nchunks = (ti.n_valid + 15) / 16;
+            if (ti.g1) {
+                __nv_bfloat16* h = static_cast<__nv_bfloat16*>(p.g.out) + static_cast<int64_t>(ti.b_row) * p.g.f +
+                                   ti.m * 128 + r;
+#pragma unroll 1
+                for (int c = 0; c < nchunks; ++c) {
+                    uint32_t a[16], b[16];
+                    ptx::tmem_ld16(tbase + c * 16, a);
+                    ptx::tmem_ld16(tbase + 128 + c * 16, b);
+                    ptx::tmem_wait_ld();
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        const int n = c * 16 + i;
+                        if (n < ti.n_valid) {
+                            const float hv = silu_f32(__uint_as_float(a[i])) * __uint_as_float(b[i]);
+                            h[static_cast<int64_t>(n) * p.g.f] = __float2bfloat16_rn(hv);
+                        }
+                    }
+                }
+                fence_proxy_async_global();  // this thread's h stores -> visible to TMA readers
+            } else {
+                // rows 256 m + r (first MMA) and 256 m + 128 + r (second)
+                float* y = p.y + p.y_split_stride * ti.s + static_cast<int64_t>(ti.b_row) * p.g.d + ti.m * 256 + r;
+#pragma unroll 1
+                for (int c = 0; c < nchunks; ++c) {
+                    uint32_t v0[16], v1[16];
+                    ptx::tmem_ld16(tbase + c * 16, v0);
+                    ptx::tmem_ld16(tbase + 128 + c * 16, v1);
+                    ptx::tmem_wait_ld();
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        const int n = c * 16 + i;
+                        if (n < ti.n_valid) {
+                            y[static_cast<int64_t>(n) * p.g.d] = __uint_as_float(v0[i]);
+                            y[static_cast<int64_t>(n) * p.g.d + 128] = __uint_as_float(v1[i]);
+                        }
+                    }
+                }
+            }
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&tmem_empty[acc]);
+            if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+            if (ti.g1) {
+                // publish: all four warps' h stores of this tile -> one release of ready[e][m]
+                ptx::named_bar_sync(kFusedEpiBar, 128);
+                if (warp == 2 && lane == 0) {
+                    __threadfence();
+                    atomicAdd(p.ready + ti.e * wt + ti.m, 1);
+                    atomicAdd(&p.sched[2], 1);
+                }
+            }
+        }
+    }
+    ptx::pdl_launch_dependents();
+    ptx::tc_fence_before();
+    __syncthreads();
+    MOE_TL(2, 2);
+    if (warp == 1) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc(tmem_base, 512);
+    }
+    // last CTA out resets the claim / exit counters and the ready counters
+    if (threadIdx.x == 0) {
+        __threadfence();
+        *s_last = atomicAdd(&p.sched[1], 1) == (int)gridDim.x - 1;
+    }
+    __syncthreads();
+    if (*s_last) {
+        __threadfence();
+        const int nready = p.g.E * wt;
+        for (int i = threadIdx.x; i < nready; i += blockDim.x) p.ready[i] = 0;
+        if (threadIdx.x == 0) {
+            p.sched[0] = 0;
+            p.sched[1] = 0;
+            p.sched[2] = 0;
+        }
+    }
+}
+
+}  // namespace moe

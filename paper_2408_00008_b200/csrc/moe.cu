@@ -27,6 +27,7 @@
 
 #include "../../include/moe.h"
 #include "gemm_sm100.cuh"
+#include "ffn_fused.cuh"
 #include "kernels.cuh"
 #include "nvls.h"
 
@@ -245,7 +246,7 @@ struct moe_ctx {
     // swap kernel's weight prefetch under PDL wins (17.85 vs 18.5-18.7 ms).
     int swap_rows_per_expert = 256;   // w1/w3 GEMM
     int swap2_rows_per_expert = 256;  // w2 GEMM
-    int max_splits = 4;       // split-K partial buffers are sized for this many splits
+    int max_splits = 8;       // split-K partial buffers are sized for this many splits
     int64_t split_stride = 0; // elements between split-K partial buffers of this forward
     bool fp8 = false;             // MOE_FLAG_FP8_WEIGHTS
     moe_expert_weights cur_w{};   // weights of the current forward
@@ -305,6 +306,13 @@ struct moe_ctx {
     // waves instead (run_gemms), the FP8 w2 GEMM one CTA per SM.
     int g1_grid = 0, g2_grid = 0;
     int g1_grid_now = 0, g2_grid_now = 0;  // the current forward's choice
+    // Fused decode FFN (moe_ffn_fused_kernel, ffn_fused.cuh): w1/w3 + SwiGLU and w2 tiles in
+    // one persistent launch (tuning.fused: 0 auto, 1 off, 2 on where the shape allows;
+    // tuning.fused_splits: K splits of its w2 tiles, 0 = auto)
+    int fused_mode = 0, fused_splits = 0, fused_stages = 0, fused_uniform = 0;
+    bool fused_now = false;              // the current forward ran the fused kernel
+    int32_t* fused_sched = nullptr;      // [2] claim / exit counters (zero between launches)
+    int32_t* fused_ready = nullptr;      // [E_local * f_local / 128] finished h tiles
     CUtensorMap tm_src{};        // gather map over the current call's tokens [T, d], box {64, 1}
     float* y = nullptr;
     int64_t y_elems = 0;
@@ -464,6 +472,13 @@ moe_status set_spair_attr(moe_ctx* c) {
     return MOE_OK;
 }
 
+template <int NB>
+moe_status set_fused_attr(moe_ctx* c) {
+    CUDA_TRY(c, cudaFuncSetAttribute(moe_ffn_fused_kernel<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     FusedCfg<NB>::kSmemBytes));
+    return MOE_OK;
+}
+
 template <int KIND, int NB>
 moe_status set_gemm_attr(moe_ctx* c) {
     CUDA_TRY(c, cudaFuncSetAttribute(moe_gemm_kernel<KIND, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -612,13 +627,18 @@ moe_status validate_cfg(const moe_config* cfg, moe_ctx* c) {
     for (int i = 0; i < 2; ++i)
         if (cfg->reserved[i]) return fail(c, MOE_ERR_INVALID, "reserved fields must be zero");
     if (const moe_tuning* tu = cfg->tuning) {
-        for (int i = 0; i < 9; ++i)
+        for (int i = 0; i < 5; ++i)
             if (tu->reserved[i]) return fail(c, MOE_ERR_INVALID, "tuning.reserved fields must be zero");
         if (tu->g1_swap_rows < 0 || tu->g2_swap_rows < 0 || tu->g1_grid < 0 || tu->g2_grid < 0 ||
             tu->swap_nb_cap < 0 || tu->router_cc_max_T < 0 || tu->pair_order < 0)
             return fail(c, MOE_ERR_INVALID, "tuning fields must be >= 0 (spec_l2 may be < 0: off)");
         if (tu->pair_nblk < 0 || tu->pair_nblk > 2) return fail(c, MOE_ERR_INVALID, "tuning.pair_nblk must be 0, 1 or 2");
         if (tu->swap_pair < 0 || tu->swap_pair > 2) return fail(c, MOE_ERR_INVALID, "tuning.swap_pair must be 0, 1 or 2");
+        if (tu->fused < 0 || tu->fused > 2) return fail(c, MOE_ERR_INVALID, "tuning.fused must be 0, 1 or 2");
+        if (tu->fused_splits < 0 || tu->fused_splits > 8)
+            return fail(c, MOE_ERR_INVALID, "tuning.fused_splits must be in [0, 8]");
+        if (tu->fused_stages < 0 || tu->fused_stages > 8)
+            return fail(c, MOE_ERR_INVALID, "tuning.fused_stages must be in [0, 8]");
         if (tu->weight_hint < 0 || tu->weight_hint > 3) return fail(c, MOE_ERR_INVALID, "tuning.weight_hint must be 0..3");
         if (tu->swap_nb_cap && tu->swap_nb_cap != 32 && tu->swap_nb_cap != 64 && tu->swap_nb_cap != 128)
             return fail(c, MOE_ERR_INVALID, "tuning.swap_nb_cap must be 0, 32, 64 or 128");
@@ -851,6 +871,15 @@ int swap_nb_ceil(int n, bool g2) {
     return 256;
 }
 
+// K splits of the fused kernel's w2 tiles: enough 256-row w2 units that the w2 phase is
+// not a single short wave at the end of the stream
+int fused_auto_splits(const moe_ctx* c, int64_t need, int nb) {
+    (void)need; (void)nb;
+    // bulk w2 tiles (256 rows, splits 0..S-2) + tail tiles (128 rows, split S-1): 4 splits
+    // while the expert count gives >= 64 256-row units, else 8 (EP ranks holding few experts)
+    return (int64_t)c->E_local * (c->d / 256) >= 64 ? 4 : 8;
+}
+
 moe_status run_gemms(moe_ctx* c, GemmPaths gp, int64_t rows_bound, int64_t rows_total, int64_t rows_expected,
                      int* splits_out, cudaStream_t st) {
     moe_status s;
@@ -925,6 +954,75 @@ moe_status run_gemms(moe_ctx* c, GemmPaths gp, int64_t rows_bound, int64_t rows_
     if (c->pair_tune) {
         r1 = c->pair_tune & 3; r2 = (c->pair_tune >> 2) & 3;
         b1 = std::max(1, (c->pair_tune >> 4) & 63); b2 = std::max(1, (c->pair_tune >> 10) & 63);
+    }
+    // Fused decode FFN: both GEMMs in one persistent launch (ffn_fused.cuh) where the shape
+    // allows -- bf16, one token tile size <= 128 rows for both GEMMs, d a multiple of 256.
+    c->fused_now = false;
+    {
+        const bool shape_ok = gp.swap1 && gp.swap2 && !c->fp8 && !c->gather_now && nb1 == nb2 && nb1 <= 128 &&
+                              c->d % 256 == 0 && c->f_local % 128 == 0 && c->E_local <= 32;
+        // auto: where the w1/w3 tiles give >= 3 waves over the SMs (single GPU, EP2 / TP2 ranks)
+        // and the token tile is <= 64 rows (64-token decode: 0.4055-0.4064 vs 0.4094-0.4102 ms,
+        // 3 of 3 interleaved rounds; EP4 / TP4 / EP8 / TP8 ranks measured slower fused:
+        // profiles/r03/fused_ab.md)
+        const int64_t U1 = (int64_t)c->E_local * (c->f_local / 128);
+        const bool want = c->fused_mode == 2 ||
+                          (c->fused_mode == 0 && !sp1 && !sp2 && nb1 <= 64 && U1 >= 3 * (int64_t)c->num_sms);
+        if (shape_ok && want) {
+            const int64_t rows_needed = round_up(rows_total + (int64_t)c->E_local * (kSegAlign - 1), kSegAlign);
+            const int wt = c->f_local / 128;
+            int S = c->fused_splits ? c->fused_splits : c->cfg.split_k ? c->cfg.split_k : fused_auto_splits(c, need, nb1);
+            S = (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)S, (int64_t)c->max_splits, (int64_t)wt,
+                                                            c->y_elems / (rows_needed * c->d)}));
+            c->split_stride = rows_needed * c->d;
+            FusedParams fp{};
+            fp.g = GemmParams{c->counts, c->offsets, c->E_local, c->d, c->f_local, 1, c->h, 0};
+            fp.g.hint_a = c->swap_w_hint;
+            fp.g.w_tr = 256;
+            fp.g.w_nt = c->w13_nt;
+            fp.g.spec_l2 = c->spec_now ? c->spec_l2 : 0;
+            fp.y = c->y;
+            fp.y_split_stride = c->split_stride;
+            fp.splits = S;
+            fp.w2_nt = c->w2_nt;
+            fp.sched = c->fused_sched;
+            fp.ready = c->fused_ready;
+            fp.stages = c->fused_stages;
+            // split boundaries in ffn tiles: uniform (tuning fused_uniform: the two-kernel path's
+            // split of whole tiles) or tapered, split i weighted S - i (4 splits: 0.4 / 0.3 / 0.2 / 0.1
+            // of K), so the stream ends on the shortest w2 tiles
+            {
+                int64_t wsum = 0, acc = 0;
+                for (int i = 0; i < S; ++i) wsum += c->fused_uniform ? 1 : S - i;
+                fp.split_j[0] = 0;
+                for (int i = 0; i < S; ++i) {
+                    acc += c->fused_uniform ? 1 : S - i;
+                    int j = (int)((wt * acc + wsum / 2) / wsum);
+                    if (c->fused_uniform) j = (int)(wt * acc / wsum);
+                    fp.split_j[i + 1] = std::max(fp.split_j[i] + 1, std::min(j, wt - (S - 1 - i)));
+                }
+                fp.split_j[S] = wt;
+            }
+            const int grid = c->g1_grid > 0 ? std::min(c->g1_grid, c->num_sms) : c->num_sms;
+            c->g1_grid_now = c->g2_grid_now = grid;
+            const int i = nb1 == 32 ? 0 : nb1 == 64 ? 1 : 2;
+            if (nb1 == 32)
+                s = launch(c, kSlotGemm1, moe_ffn_fused_kernel<32>, dim3(grid), dim3(kGemmThreads),
+                           (size_t)FusedCfg<32>::kSmemBytes, st, fp, c->tm_w13, c->tm_x_swap[i], c->tm_w2_tiled,
+                           c->tm_h_swap[i]);
+            else if (nb1 == 64)
+                s = launch(c, kSlotGemm1, moe_ffn_fused_kernel<64>, dim3(grid), dim3(kGemmThreads),
+                           (size_t)FusedCfg<64>::kSmemBytes, st, fp, c->tm_w13, c->tm_x_swap[i], c->tm_w2_tiled,
+                           c->tm_h_swap[i]);
+            else
+                s = launch(c, kSlotGemm1, moe_ffn_fused_kernel<128>, dim3(grid), dim3(kGemmThreads),
+                           (size_t)FusedCfg<128>::kSmemBytes, st, fp, c->tm_w13, c->tm_x_swap[i], c->tm_w2_tiled,
+                           c->tm_h_swap[i]);
+            if (s) return s;
+            c->fused_now = true;
+            *splits_out = S;
+            return MOE_OK;
+        }
     }
     const int ncl = c->num_sms / 2;
     {
@@ -1003,7 +1101,7 @@ moe_status run_gemms(moe_ctx* c, GemmPaths gp, int64_t rows_bound, int64_t rows_
         // 104.8 us; the 32-layer stack is unchanged (14.97 vs 14.93 ms)
         int auto_splits = c->fp8 ? 4 : 1;
         if (need <= nb2 && 4 * U0 < 3 * (int64_t)c->num_sms)
-            auto_splits = std::max<int>(auto_splits, (int)std::min<int64_t>(c->max_splits, c->num_sms / U0));
+            auto_splits = std::max<int>(auto_splits, (int)std::min<int64_t>(std::min(4, c->max_splits), c->num_sms / U0));
         splits = c->cfg.split_k ? c->cfg.split_k : auto_splits;
         splits = (int)std::max<int64_t>(1, std::min<int64_t>(splits, c->y_elems / (rows_needed * c->d)));
         splits = std::min(splits, c->f_local / (c->fp8 ? 128 : kBK));  // >= 1 K block per split
@@ -1445,6 +1543,10 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
         c->host_zero_copy = tu->host_stage == 0;
         c->swap_hint_mode = tu->weight_hint;
         c->swap_pair_mode = tu->swap_pair;
+        c->fused_mode = tu->fused;
+        c->fused_splits = tu->fused_splits;
+        c->fused_stages = tu->fused_stages;
+        c->fused_uniform = tu->fused_uniform;
     }
     if (cfg->flags & MOE_FLAG_GATHER) c->gather = true;
     // EP: a rank may receive up to every token of every peer (dropless, reading R6).
@@ -1496,6 +1598,8 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
     ALLOC(c->counts, sizeof(int32_t) * 64);
     ALLOC(c->offsets, sizeof(int32_t) * 64);
     ALLOC(c->done, sizeof(unsigned int) * 4);
+    ALLOC(c->fused_sched, sizeof(int32_t) * 4);
+    ALLOC(c->fused_ready, sizeof(int32_t) * ((int64_t)c->E_local * (c->f_local / 128) + 4));
     ALLOC(c->x_perm, sizeof(__nv_bfloat16) * c->cap * c->d);
     ALLOC(c->tok_scale, sizeof(float) * c->cap);
     if (c->fp8) {
@@ -1573,6 +1677,9 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
         }
     }
     if ((e = cudaMemset(c->done, 0, sizeof(unsigned int) * 4)) != cudaSuccess) return fail_init("memset", e);
+    if ((e = cudaMemset(c->fused_sched, 0, sizeof(int32_t) * 4)) != cudaSuccess ||
+        (e = cudaMemset(c->fused_ready, 0, sizeof(int32_t) * ((int64_t)c->E_local * (c->f_local / 128) + 4))) != cudaSuccess)
+        return fail_init("memset", e);
     if ((e = cudaMemset(c->x_perm, 0, sizeof(__nv_bfloat16) * c->cap * c->d)) != cudaSuccess) return fail_init("memset", e);
     if ((e = cudaMemset(c->src_row, 0, sizeof(int32_t) * (c->cap + 512))) != cudaSuccess) return fail_init("memset", e);
     if ((e = cudaMemset(c->h, 0, sizeof(__nv_bfloat16) * c->cap * c->f_local)) != cudaSuccess) return fail_init("memset", e);
@@ -1606,7 +1713,8 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
         (as = set_spair_attr<128>(c)) || (as = set_spair_attr<192>(c)) || (as = set_spair_attr<256>(c)) ||
         (as = set_pair_attr<kG1Pair, 1>(c)) || (as = set_pair_attr<kG2Pair, 1>(c)) ||
         (as = set_pair_attr<kG1Pair, 2>(c)) || (as = set_pair_attr<kG2Pair, 2>(c)) ||
-        (as = set_fp8x_attr<32>(c)) || (as = set_fp8x_attr<64>(c)) || (as = set_fp8x_attr<128>(c))) {
+        (as = set_fp8x_attr<32>(c)) || (as = set_fp8x_attr<64>(c)) || (as = set_fp8x_attr<128>(c)) ||
+        (as = set_fused_attr<32>(c)) || (as = set_fused_attr<64>(c)) || (as = set_fused_attr<128>(c))) {
         std::string m = c->err;
         moe_destroy(c);
         g_init_error = m;
@@ -1645,7 +1753,10 @@ reinterpret_cast<const void*>(moe_ep_p2p_fill_kernel),
             reinterpret_cast<const void*>(moe_gemm_fp8x_kernel<kG1Swap, 128>),
             reinterpret_cast<const void*>(moe_gemm_fp8x_kernel<kG2Swap, 32>),
             reinterpret_cast<const void*>(moe_gemm_fp8x_kernel<kG2Swap, 64>),
-            reinterpret_cast<const void*>(moe_gemm_fp8x_kernel<kG2Swap, 128>)};
+            reinterpret_cast<const void*>(moe_gemm_fp8x_kernel<kG2Swap, 128>),
+            reinterpret_cast<const void*>(moe_ffn_fused_kernel<32>),
+            reinterpret_cast<const void*>(moe_ffn_fused_kernel<64>),
+            reinterpret_cast<const void*>(moe_ffn_fused_kernel<128>)};
         for (const void* fn : fns)
             if ((e = cudaFuncGetAttributes(&fa, fn)) != cudaSuccess) return fail_init("cudaFuncGetAttributes", e);
     }
@@ -1661,7 +1772,7 @@ moe_status moe_destroy(moe_ctx* c) {
                     c->x_perm, c->h, c->y, c->stage_in, c->stage_out, c->tp_partial, c->tp_scatter, c->ep_send,
                     c->ep_recv, c->ep_ysend, c->ep_yrecv, c->ep_meta_send, c->ep_meta_recv,
                     c->ep_ridx, c->ep_rpos, c->ep_rw, c->ep_rcounts, c->lb_scratch, c->d_peers, c->p2p_tickets, c->src_row,
-                    c->tok_scale, c->h8, c->h_sf};
+                    c->tok_scale, c->h8, c->h_sf, c->fused_sched, c->fused_ready};
     for (void* p : c->p2p_opened) cudaIpcCloseMemHandle(p);
     if (c->nvls) {
         cudaDeviceSynchronize();  // no fused combine still reads / writes the window

@@ -115,6 +115,10 @@ __device__ __forceinline__ void sts16(uint32_t addr, uint16_t v) {
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t n) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
+// arrive on named barrier `id` (n threads in total) without waiting (release)
+__device__ __forceinline__ void named_bar_arrive(uint32_t id, uint32_t n) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
 __device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
     asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
 }
@@ -434,6 +438,11 @@ __device__ unsigned long long g_moe_tl[5][3][kTlBlocks];
             ::moe::ptx::g_moe_tl[slot][what][blockIdx.x] = t_;                                 \
         }                                                                                      \
     } while (0)
+__device__ __forceinline__ unsigned long long tl_now() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 #else
 #define MOE_TL(slot, what) \
     do {                   \

@@ -2,6 +2,9 @@
 
 Build:  python paper_2408_00008_b200/_build.py --force --out build_ab/libmoe_tl.so -DMOE_TIMELINE=1
 Run:    MOE_LIB=build_ab/libmoe_tl.so python scripts/exp/timeline.py T [tuning k=v,...|-] [--residual] [--fp8]
+        [--shard ep2|ep4|ep8|tp2|tp4|tp8]   (one rank's share: E/G experts top-1 over its rows, or f/G columns)
+With tuning fused=2 the w1/w3 slot is the fused FFN kernel and slot 3 holds its producer
+probes: first w2-tile claim, last (failing) claim, and the time spent waiting for h tiles.
 
 The probe build stamps %globaltimer (ns) in thread 0 of every block at kernel entry,
 after griddepcontrol.wait and at exit (csrc/sm100.cuh MOE_TL). After back-to-back graph
@@ -45,7 +48,21 @@ def main():
         for n in ("w1", "w3", "w2"):
             w[n] = synth.quantize_fp8_rows(w[n])
     x = synth.make_tokens(T, d, 1, 0, device="cuda")
-    blk = moe.MoEBlock(w["wg"], w["w1"], w["w3"], w["w2"], top_k=2, max_tokens=T, flags=flags, tuning=tuning)
+    shard = next((a.split("=", 1)[1] if "=" in a else sys.argv[sys.argv.index(a) + 1]
+                  for a in sys.argv if a.startswith("--shard")), None)
+    k = 2
+    if shard and shard.startswith("tp"):  # this rank's f/G ffn slice of every expert, whole batch
+        fl = f // int(shard[2:])
+        w = {"wg": w["wg"], "w1": w["w1"][:, :fl].contiguous(), "w3": w["w3"][:, :fl].contiguous(),
+             "w2": w["w2"][:, :, :fl].contiguous()}
+    elif shard and shard.startswith("ep"):  # E/G experts; the rows routed to them (~T*k/G), top-1
+        G = int(shard[2:])
+        el = E // G
+        w = {n: w[n][:el].contiguous() for n in ("wg", "w1", "w3", "w2")}
+        T = max(1, T * 2 // G)
+        x = x[:T].contiguous()
+        k = 1
+    blk = moe.MoEBlock(w["wg"], w["w1"], w["w3"], w["w2"], top_k=k, max_tokens=T, flags=flags, tuning=tuning)
     del w
     out = torch.empty_like(x)
 
@@ -86,6 +103,11 @@ def main():
         fmt = lambda a: f"{a.min():8.1f}..{a.max():8.1f}" if a.size else " " * 20  # noqa: E731
         print(f"{name:8s} {int(m.sum()):6d} {fmt(e)} {fmt(w_)} {fmt(x_)}")
         ends[name] = x_
+        if name == "gemm2" and tuning and tuning.get("fused") == 2:
+            stall = (tl[s][2][m] - tl[2][0][m]) / 1000.0
+            print(f"  (fused producer: first w2 claim {fmt(e)}, last claim {fmt(w_)}, "
+                  f"h-wait us p50/p90/max {np.percentile(stall, 50):.1f}/{np.percentile(stall, 90):.1f}/{stall.max():.1f})")
+            continue
         if name in ("gemm1", "gemm2") and x_.size:
             q = np.percentile(x_, [0, 10, 50, 90, 100])
             print(f"         exit percentiles 0/10/50/90/100: " + " ".join(f"{v:.1f}" for v in q))

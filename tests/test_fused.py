@@ -1,0 +1,169 @@
+"""GPU parity of the fused decode FFN (moe_ffn_fused_kernel, csrc/ffn_fused.cuh; tuning
+fused=2): the w1/w3 + SwiGLU tiles and the w2 tiles of every expert in ONE persistent
+launch, w2 tiles waiting per 128-column h tile through counters in global memory.
+
+Checks, all through the C ABI:
+- oracle parity (routing, out_f32 within 2e-2 of the row RMS, bf16 out = RNE(out_f32))
+  over ragged token counts, odd ffn-tile counts, uneven K splits, empty experts, several
+  token tiles per expert (a w2 tile then waits for every token tile of its h columns);
+- bit-identity with the two-kernel swap path at the same K split where the split
+  boundaries coincide (the same MMAs per output element in the same K order);
+- repeated forwards and CUDA-graph replays (the device-side claim / ready counters are
+  reset by the last CTA of each launch);
+- EP / TP contexts (loopback transport) and the Mixtral-size 64-token decode.
+"""
+import numpy as np
+import pytest
+import torch
+
+import synth
+from parity import GpuRun, check_forward, to_host_inputs
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def moe():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2408_00008_b200 as m
+    return m
+
+
+def _block(moe, inp, k, T, tuning, split_k=0, flags=0):
+    return moe.MoEBlock(inp["wg"], inp["w1"], inp["w3"], inp["w2"], top_k=k, max_tokens=T, flags=flags,
+                        split_k=split_k, tuning=tuning)
+
+
+def _launches(moe, blk, x):
+    n0 = moe.moe_launch_count(blk.ctx)
+    blk.forward(x)
+    torch.cuda.synchronize()
+    return moe.moe_launch_count(blk.ctx) - n0
+
+
+@pytest.mark.parametrize("uniform", [0, 1])
+@pytest.mark.parametrize("T,d,f,E,k,splits", [
+    (64, 512, 1024, 8, 2, 0),    # decode-like: one token tile per expert (NB 64), auto splits
+    (1, 256, 512, 4, 2, 1),      # one token: 2 experts used, 2 empty
+    (40, 256, 1024, 8, 2, 2),
+    (40, 256, 1024, 8, 2, 3),    # 8 ffn tiles over 3 splits: 2 / 3 / 3 tiles
+    (100, 256, 384, 2, 2, 2),    # 3 ffn tiles: splits of 1 and 2 tiles; NB 128
+    (77, 768, 256, 8, 1, 4),     # top-1, 2 ffn tiles over 4 splits -> 2 (capped by the tile count)
+    (16, 256, 256, 4, 2, 1),     # NB 32 (16 rows bound), single ffn tile pair
+    (128, 512, 512, 6, 2, 4),    # NB 128, ragged expert segments
+    (48, 256, 2048, 8, 2, 8),    # 16 ffn tiles over 8 tapered splits (8 partial buffers)
+])
+def test_fused_parity(moe, T, d, f, E, k, splits, uniform):
+    """Tapered (default) and uniform w2 K splits, incl. more splits than ffn tiles allow."""
+    shape = synth.MoEShape(T=T, d=d, f=f, E=E, k=k)
+    inp = synth.make_inputs(shape, 7100 + T + d + splits, device="cuda")
+    host = to_host_inputs(inp)
+    blk = _block(moe, inp, k, T, {"fused": 2, "fused_splits": splits, "fused_uniform": uniform})
+    run = GpuRun(blk, inp["x"])
+    check_forward(run, host, k)
+    assert _launches(moe, blk, inp["x"]) == 4  # router, permute, fused FFN, combine
+    for _ in range(3):  # counters reset by the last CTA: repeated forwards agree bit for bit
+        out2 = blk.forward(inp["x"])
+        torch.cuda.synchronize()
+        assert torch.equal(out2.view(torch.int16), run.out.view(torch.int16))
+    blk.close()
+
+
+@pytest.mark.parametrize("T,splits", [(64, 1), (64, 2), (64, 4), (100, 2), (13, 4)])
+def test_fused_bit_identical_to_two_kernels(moe, T, splits):
+    """f = 1024 (8 ffn tiles), uniform splits (tuning fused_uniform): K splits 1 / 2 / 4 fall on
+    ffn-tile boundaries in both paths, so each fp32 partial is the same sum in the same order
+    and the outputs match bit for bit."""
+    shape = synth.MoEShape(T=T, d=512, f=1024, E=8, k=2)
+    inp = synth.make_inputs(shape, 7200 + T + splits, device="cuda")
+    outs = []
+    for tu in ({"fused": 2, "fused_splits": splits, "fused_uniform": 1}, {"fused": 1}):
+        blk = _block(moe, inp, 2, T, tu, split_k=splits, flags=moe.MOE_FLAG_FORCE_SWAP)
+        run = GpuRun(blk, inp["x"])
+        outs.append((run.np("out_f32").copy(), run.out.clone()))
+        blk.close()
+    assert np.array_equal(outs[0][0].view(np.int32), outs[1][0].view(np.int32))
+    assert torch.equal(outs[0][1].view(torch.int16), outs[1][1].view(torch.int16))
+
+
+@pytest.mark.parametrize("n", [33, 100, 256])
+def test_fused_multi_token_tiles(moe, n):
+    """Every token routed to experts (0, 1) of 4 with the token tile capped at 32 rows
+    (tuning swap_nb_cap): the two busy experts run ceil(n/32) token tiles each, so an h
+    tile is finished only when all of its token tiles are, and two experts are empty."""
+    shape = synth.MoEShape(T=n, d=256, f=512, E=4, k=2)
+    inp = synth.make_inputs(shape, 7300 + n, device="cuda")
+    host = to_host_inputs(inp)
+    import oracle
+    idx = np.tile(np.array([[0, 1]], np.int32), (n, 1))
+    l = oracle.router(host["x"], host["wg"], 1)["logits"]
+    li = np.take_along_axis(l, idx.astype(np.int64), 1)
+    p = np.exp(li - li.max(1, keepdims=True))
+    gw = (p / p.sum(1, keepdims=True)).astype(np.float32)
+    blk = _block(moe, inp, 2, n, {"fused": 2, "swap_nb_cap": 32, "fused_splits": 2})
+    run = GpuRun(blk, inp["x"], routed=(torch.from_numpy(idx).cuda(), torch.from_numpy(gw).cuda()))
+    check_forward(run, host, 2, routed=True)
+    assert run.np("expert_counts").tolist() == [n, n, 0, 0]
+    blk.close()
+
+
+def test_fused_graph_replay(moe):
+    """CUDA-graph capture of the fused forward, replayed 20 times: identical outputs."""
+    shape = synth.MoEShape(T=64, d=512, f=1024, E=8, k=2)
+    inp = synth.make_inputs(shape, 7400, device="cuda")
+    blk = _block(moe, inp, 2, 64, {"fused": 2})
+    ref = blk.forward(inp["x"]).clone()
+    out = torch.empty_like(ref)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        blk.forward(inp["x"], out, stream=s)
+    torch.cuda.current_stream().wait_stream(s)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        blk.forward(inp["x"], out, stream=s)
+    for _ in range(20):
+        out.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(out.view(torch.int16), ref.view(torch.int16))
+    blk.close()
+
+
+@pytest.mark.parametrize("par,G", [("ep", 2), ("ep", 4), ("tp", 2), ("tp", 4)])
+def test_fused_group(moe, par, G):
+    """Fused FFN inside EP (receive-side expert segments) and TP (ffn slice) contexts."""
+    from test_gpu_parity import _check_group_outputs, _run_group
+    shape = synth.MoEShape(T=96, d=256, f=1024, E=8, k=2)
+    inp = synth.make_inputs(shape, 7500 + G, device="cuda")
+    host = to_host_inputs(inp)
+    if par == "ep":
+        cuts = np.linspace(0, shape.T, G + 1).astype(int)
+        shards = [inp["x"][cuts[r]:cuts[r + 1]] for r in range(G)]
+        res = _run_group(moe, inp, moe.MOE_PAR_EP, G, shards, max_tokens=shape.T, tuning={"fused": 2})
+        _check_group_outputs(host, 2, host["x"], [r[0] for r in res], [r[1] for r in res])
+    else:
+        res = _run_group(moe, inp, moe.MOE_PAR_TP, G, [inp["x"]] * G, tuning={"fused": 2})
+        for r in range(1, G):
+            assert torch.equal(res[r][0].view(torch.int16), res[0][0].view(torch.int16))
+        _check_group_outputs(host, 2, host["x"], [res[0][0]], [res[0][1]])
+
+
+def test_fused_mixtral_decode(moe):
+    """BASELINE configs[1]: Mixtral layer, 64-token decode, fused FFN (sampled tokens vs the
+    oracle, every token's routing) and bit-identical to the two-kernel path at 4 splits
+    (112 ffn tiles -> 28 per split in both)."""
+    w = synth.make_weights(4096, 14336, 8, seed=42, device="cuda")
+    x = synth.make_tokens(64, 4096, seed=9001, device="cuda")
+    inp = dict(w, x=x)
+    host = to_host_inputs(inp)
+    outs = []
+    for tu in ({"fused": 2, "fused_splits": 4, "fused_uniform": 1}, {"fused": 1}):
+        blk = _block(moe, inp, 2, 64, tu, split_k=4)
+        run = GpuRun(blk, x)
+        if tu["fused"] == 2:
+            check_forward(run, host, 2, tokens=[0, 1, 31, 62, 63])
+        outs.append(run.np("out_f32").copy())
+        blk.close()
+    assert np.array_equal(outs[0].view(np.int32), outs[1].view(np.int32))

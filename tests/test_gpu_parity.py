@@ -479,7 +479,7 @@ def test_gather_equals_copy(moe, mixtral_weights, T, flags):
 
 
 # ---------------------------------------------------------------- EP / TP device path (loopback transport)
-def _run_group(moe, inp, par, G, shards, k=2, flags=0, max_tokens=None, p2p=False, iters=1):
+def _run_group(moe, inp, par, G, shards, k=2, flags=0, max_tokens=None, p2p=False, iters=1, tuning=None):
     """G contexts on one GPU, each driven by its own thread (and stream), exchanging
     through the loopback transport, or through peer memory (p2p: MOE_FLAG_P2P, the
     handles of the G regions connected in-process). shards[r] = token tensor of rank
@@ -492,7 +492,7 @@ def _run_group(moe, inp, par, G, shards, k=2, flags=0, max_tokens=None, p2p=Fals
         comms = [moe.moe_loopback_comm_rank(grp, r) for r in range(G)]
     mt = max_tokens or max(1, max(s.shape[0] for s in shards))
     blocks = [moe.MoEBlock(inp["wg"], inp["w1"], inp["w3"], inp["w2"], top_k=k, max_tokens=mt, par=par,
-                           world_size=G, rank=r, nccl_comm=comms[r], flags=flags) for r in range(G)]
+                           world_size=G, rank=r, nccl_comm=comms[r], flags=flags, tuning=tuning) for r in range(G)]
     if p2p:
         handles = [b.p2p_handle() for b in blocks]
         for b in blocks:
