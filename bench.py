@@ -937,10 +937,8 @@ def main():
                 "kernel": "moe_gemm_pair_kernel<kG1Pair,2> (w1/w3 + SwiGLU, 256x512 CTA-pair tiles)",
                 "peak_src": peaks["src"] + " (MEASURED_PEAKS.json bf16_tflops_sustained)"}
         step_frac = alg["flops"] / (ms * 1e-3) / 1e12 / pk
-    tr, tr_src = load_traffic(args.config + ("_fp8" if args.fp8 else "")) if world == 1 and par == "none" \
-        else (None, None)
-    if fused:
-        tr = None  # traffic.json holds the two-kernel path's K3 capture
+    tr, tr_src = load_traffic(args.config + ("_fp8" if args.fp8 else "") + ("_fused" if fused else "")) \
+        if world == 1 and par == "none" else (None, None)
     roof["traffic"] = tr
     if tr is not None:
         roof["traffic_src"] = tr_src

@@ -471,7 +471,9 @@ def test_gather_equals_copy(moe, mixtral_weights, T, flags):
     x = synth.make_tokens(T, 4096, seed=300 + T, device="cuda")
     outs = []
     for extra in (0, moe.MOE_FLAG_GATHER):
-        blk = moe.MoEBlock(w["wg"], w["w1"], w["w3"], w["w2"], top_k=2, max_tokens=T, flags=flags | extra)
+        # two-kernel GEMM path for both (the fused decode FFN has no gather variant)
+        blk = moe.MoEBlock(w["wg"], w["w1"], w["w3"], w["w2"], top_k=2, max_tokens=T, flags=flags | extra,
+                           tuning={"fused": 1})
         outs.append(blk.forward(x).clone())
         torch.cuda.synchronize()
         blk.close()
