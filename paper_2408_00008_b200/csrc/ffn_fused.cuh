@@ -61,6 +61,20 @@ struct FusedParams {
     int32_t* ready;          // [E * (f/128)] finished G1 token tiles per (expert, ffn tile)
     int32_t stages;          // pipeline stages used (1..kStages; 0 = all that fit)
     int32_t split_j[9];      // ffn-tile boundaries of the w2 K splits: 0 = j_0 < .. < j_S = f/128
+    // In-kernel combine (single GPU, step a9; combine_T = 0: off, moe_combine_kernel runs
+    // after): once every w2 tile of a 256-column slice m has stored its partial (arrive[m]),
+    // "combine tasks" (slice m, comb_chunk tokens), one per CTA after the GEMM tiles, compute
+    // out[t, slice] = bf16_rne(sum_j w_j * sum_s y_s[pos_j] (+ x[t])) in moe_combine_kernel's
+    // exact order, so the results are bit-identical to the separate combine.
+    int32_t combine_T;
+    int32_t k;
+    const int32_t* pos;          // [T, k] permuted row of each (token, choice), < 0: none
+    const float* topk_w;         // [T, k]
+    const __nv_bfloat16* x_res;  // residual rows (nullable)
+    __nv_bfloat16* out;          // [T, d]
+    float* out_f32;              // [T, d] (nullable)
+    int32_t* arrive;             // [d / 256] finished w2 tiles per slice (zero between launches)
+    int32_t comb_chunk;          // tokens per combine task; the host keeps the task count <= the grid
 };
 
 constexpr int kFusedTileRing = 8;  // claimed-tile hand-off ring depth
@@ -251,6 +265,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         per_split += nt * (p.g.d / 256);
     }
     const int total = total1 + per_split * p.splits;
+    // combine tasks after the GEMM tiles; a slice is complete after S * sum_e nt_e w2 tiles
+    // Each CTA takes at most ONE combine task (sched[3]), after its producer found no GEMM tile
+    // left: tasks queued behind each other in one CTA's epilogue would run back to back after
+    // the last w2 tile (measured: +46 us at the 64-token decode with 8-token tasks claimed
+    // like tiles). The host sizes the chunks so that ncomb <= gridDim.x.
+    const int nchunk = p.combine_T > 0 ? (p.combine_T + p.comb_chunk - 1) / p.comb_chunk : 0;
+    const int ncomb = (p.g.d / 256) * nchunk;
+    const int total_all = total + ncomb;
+    const int slice_need = p.splits * (per_split / (p.g.d / 256));
     const uint64_t w_hint = p.g.hint_a ? p.g.hint_a : ptx::kEvictFirst;
 
     if (warp == 0) {
@@ -265,15 +288,21 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             // holds SR stages of it, which hides the atomic's round trip). Claiming ahead was
             // measured slower: a CTA then holds two tiles at the end of the stream (tail) and,
             // at EP ranks, two waiting w2 tiles while G1 tiles run (profiles/r03).
+            bool comb_taken = false;
             while (true) {
-                const int t = atomicAdd(&p.sched[0], 1);
+                int t = atomicAdd(&p.sched[0], 1);
+                if (t >= total) {
+                    const int cidx = (ncomb > 0 && !comb_taken) ? atomicAdd(&p.sched[3], 1) : ncomb;
+                    comb_taken = true;
+                    t = cidx < ncomb ? total + cidx : total_all;
+                }
                 ptx::mbar_wait(&tile_empty[ts], tph ^ 1);
                 s_tile[ts] = t;
                 ptx::mbar_arrive(&tile_full[ts]);
                 if (++ts == R) { ts = 0; tph ^= 1; }
 #if MOE_TIMELINE
                 if (blockIdx.x < ptx::kTlBlocks) {
-                    if (t >= total) {
+                    if (t >= total_all) {
                         ptx::g_moe_tl[3][1][blockIdx.x] = ptx::tl_now();
                         ptx::g_moe_tl[3][2][blockIdx.x] = tl_entry + tl_stall;
                     } else if (t >= total1 && !tl_g2) {
@@ -282,7 +311,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                     }
                 }
 #endif
-                if (t >= total) break;
+                if (t >= total_all) break;
+                if (t >= total) continue;  // combine task: the epilogue warps only
                 FusedTile ti;
                 fused_decode<NB>(t, p, s_counts, s_offsets, total1, per_split, ti);
                 if (!ti.g1 && !all_ready && ld_relaxed_gpu(&p.sched[2]) >= total1) {
@@ -392,7 +422,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 const int t = s_tile[ts];
                 ptx::mbar_arrive(&tile_empty[ts]);
                 if (++ts == R) { ts = 0; tph ^= 1; }
-                if (t >= total) break;
+                if (t >= total_all) break;
+                if (t >= total) continue;
                 FusedTile ti;
                 fused_decode<NB>(t, p, s_counts, s_offsets, total1, per_split, ti);
                 const uint32_t n_mma = (uint32_t)((ti.n_valid + 15) / 16 * 16);
@@ -435,7 +466,60 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(&tile_empty[ts]);
             if (++ts == R) { ts = 0; tph ^= 1; }
-            if (t >= total) break;
+            if (t >= total_all) break;
+            if (t >= total) {
+                // ---- combine task: slice m = 256 columns, tokens [t0, t0 + comb_chunk)
+                const int m = (t - total) / nchunk;
+                const int t0 = ((t - total) % nchunk) * p.comb_chunk;
+                if (lane == 0) {
+                    while (ld_relaxed_gpu(p.arrive + m) < slice_need) __nanosleep(64);
+                    fence_acq_rel_gpu();
+                }
+                __syncwarp();
+                const int tid = (warp - 2) * 32 + lane;  // 0..127
+                const int c = m * 256 + (tid & 63) * 4;
+                for (int tt = t0 + (tid >> 6); tt < min(t0 + p.comb_chunk, p.combine_T); tt += 2) {
+                    int32_t pr[2];
+                    float w[2];
+#pragma unroll
+                    for (int j = 0; j < 2; ++j) {
+                        pr[j] = j < p.k ? p.pos[(int64_t)tt * p.k + j] : -1;
+                        w[j] = j < p.k ? p.topk_w[(int64_t)tt * p.k + j] : 0.f;
+                    }
+                    float4 sj[2];
+#pragma unroll
+                    for (int j = 0; j < 2; ++j) {
+                        sj[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+                        if (pr[j] >= 0) sj[j] = __ldcg(reinterpret_cast<const float4*>(p.y + (int64_t)pr[j] * p.g.d + c));
+                    }
+                    for (int sp = 1; sp < p.splits; ++sp)
+#pragma unroll
+                        for (int j = 0; j < 2; ++j)
+                            if (pr[j] >= 0) {
+                                const float4 u = __ldcg(reinterpret_cast<const float4*>(
+                                    p.y + sp * p.y_split_stride + (int64_t)pr[j] * p.g.d + c));
+                                sj[j].x += u.x; sj[j].y += u.y; sj[j].z += u.z; sj[j].w += u.w;
+                            }
+                    float4 rr = make_float4(0.f, 0.f, 0.f, 0.f);
+                    if (pr[0] >= 0) rr = make_float4(w[0] * sj[0].x, w[0] * sj[0].y, w[0] * sj[0].z, w[0] * sj[0].w);
+                    if (pr[1] >= 0) {
+                        rr.x = fmaf(w[1], sj[1].x, rr.x); rr.y = fmaf(w[1], sj[1].y, rr.y);
+                        rr.z = fmaf(w[1], sj[1].z, rr.z); rr.w = fmaf(w[1], sj[1].w, rr.w);
+                    }
+                    if (p.x_res) {
+                        const __nv_bfloat162* xs = reinterpret_cast<const __nv_bfloat162*>(p.x_res + (int64_t)tt * p.g.d + c);
+                        const float2 a = __bfloat1622float2(xs[0]), b = __bfloat1622float2(xs[1]);
+                        rr.x += a.x; rr.y += a.y; rr.z += b.x; rr.w += b.y;
+                    }
+                    if (p.out_f32) __stcs(reinterpret_cast<float4*>(p.out_f32 + (int64_t)tt * p.g.d + c), rr);
+                    __nv_bfloat162 o0 = __floats2bfloat162_rn(rr.x, rr.y), o1 = __floats2bfloat162_rn(rr.z, rr.w);
+                    uint2 ov;
+                    ov.x = *reinterpret_cast<uint32_t*>(&o0);
+                    ov.y = *reinterpret_cast<uint32_t*>(&o1);
+                    *reinterpret_cast<uint2*>(p.out + (int64_t)tt * p.g.d + c) = ov;
+                }
+                continue;
+            }
             FusedTile ti;
             fused_decode<NB>(t, p, s_counts, s_offsets, total1, per_split, ti);
             ptx::mbar_wait(&tmem_full[acc], acc_phase);
@@ -484,6 +568,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(&tmem_empty[acc]);
             if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+            if (!ti.g1 && p.combine_T > 0) {
+                // publish this tile's partial for the combine tasks of slice m
+                ptx::named_bar_sync(kFusedEpiBar, 128);
+                if (warp == 2 && lane == 0) {
+                    __threadfence();
+                    atomicAdd(p.arrive + ti.m, 1);
+                }
+            }
             if (ti.g1) {
                 // publish: all four warps' h stores of this tile -> one release of ready[e][m]
                 ptx::named_bar_sync(kFusedEpiBar, 128);
@@ -513,10 +605,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         __threadfence();
         const int nready = p.g.E * wt;
         for (int i = threadIdx.x; i < nready; i += blockDim.x) p.ready[i] = 0;
+        if (p.combine_T > 0)
+            for (int i = threadIdx.x; i < p.g.d / 256; i += blockDim.x) p.arrive[i] = 0;
         if (threadIdx.x == 0) {
             p.sched[0] = 0;
             p.sched[1] = 0;
             p.sched[2] = 0;
+            p.sched[3] = 0;
         }
     }
 }

@@ -313,6 +313,18 @@ struct moe_ctx {
     bool fused_now = false;              // the current forward ran the fused kernel
     int32_t* fused_sched = nullptr;      // [2] claim / exit counters (zero between launches)
     int32_t* fused_ready = nullptr;      // [E_local * f_local / 128] finished h tiles
+    int32_t* fused_arrive = nullptr;     // [d / 256] finished w2 tiles per slice (in-kernel combine)
+    // in-kernel combine of the fused FFN (single GPU, no TP / EP; tuning.fused_combine 1 = on):
+    // set by forward_impl before run_gemms, taken by the fused launch (fcomb_done)
+    struct FusedCombine {
+        bool on = false;
+        int T = 0;
+        const void* x = nullptr;
+        void* out = nullptr;
+        float* out_f32 = nullptr;
+    } fcomb;
+    bool fcomb_done = false;
+    int fused_combine_mode = 0;
     CUtensorMap tm_src{};        // gather map over the current call's tokens [T, d], box {64, 1}
     float* y = nullptr;
     int64_t y_elems = 0;
@@ -627,7 +639,7 @@ moe_status validate_cfg(const moe_config* cfg, moe_ctx* c) {
     for (int i = 0; i < 2; ++i)
         if (cfg->reserved[i]) return fail(c, MOE_ERR_INVALID, "reserved fields must be zero");
     if (const moe_tuning* tu = cfg->tuning) {
-        for (int i = 0; i < 5; ++i)
+        for (int i = 0; i < 4; ++i)
             if (tu->reserved[i]) return fail(c, MOE_ERR_INVALID, "tuning.reserved fields must be zero");
         if (tu->g1_swap_rows < 0 || tu->g2_swap_rows < 0 || tu->g1_grid < 0 || tu->g2_grid < 0 ||
             tu->swap_nb_cap < 0 || tu->router_cc_max_T < 0 || tu->pair_order < 0)
@@ -637,6 +649,8 @@ moe_status validate_cfg(const moe_config* cfg, moe_ctx* c) {
         if (tu->fused < 0 || tu->fused > 2) return fail(c, MOE_ERR_INVALID, "tuning.fused must be 0, 1 or 2");
         if (tu->fused_splits < 0 || tu->fused_splits > 8)
             return fail(c, MOE_ERR_INVALID, "tuning.fused_splits must be in [0, 8]");
+        if (tu->fused_combine < 0 || tu->fused_combine > 1)
+            return fail(c, MOE_ERR_INVALID, "tuning.fused_combine must be 0 or 1");
         if (tu->fused_stages < 0 || tu->fused_stages > 8)
             return fail(c, MOE_ERR_INVALID, "tuning.fused_stages must be in [0, 8]");
         if (tu->weight_hint < 0 || tu->weight_hint > 3) return fail(c, MOE_ERR_INVALID, "tuning.weight_hint must be 0..3");
@@ -975,6 +989,7 @@ moe_status run_gemms(moe_ctx* c, GemmPaths gp, int64_t rows_bound, int64_t rows_
             S = (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)S, (int64_t)c->max_splits, (int64_t)wt,
                                                             c->y_elems / (rows_needed * c->d)}));
             c->split_stride = rows_needed * c->d;
+            const int grid = c->g1_grid > 0 ? std::min(c->g1_grid, c->num_sms) : c->num_sms;
             FusedParams fp{};
             fp.g = GemmParams{c->counts, c->offsets, c->E_local, c->d, c->f_local, 1, c->h, 0};
             fp.g.hint_a = c->swap_w_hint;
@@ -988,6 +1003,20 @@ moe_status run_gemms(moe_ctx* c, GemmPaths gp, int64_t rows_bound, int64_t rows_
             fp.sched = c->fused_sched;
             fp.ready = c->fused_ready;
             fp.stages = c->fused_stages;
+            const bool comb = c->fcomb.on && c->d / 256 <= grid;  // every combine task claimed by some CTA
+            if (comb) {
+                fp.combine_T = c->fcomb.T;
+                fp.k = c->k;
+                fp.pos = c->pos;
+                fp.topk_w = c->topk_w;
+                fp.x_res = static_cast<const __nv_bfloat16*>(c->fcomb.x);
+                fp.out = static_cast<__nv_bfloat16*>(c->fcomb.out);
+                fp.out_f32 = c->fcomb.out_f32;
+                fp.arrive = c->fused_arrive;
+                // tokens per combine task: at most one task per CTA (grid / (d/256) chunks per slice)
+                const int per_slice = std::max(1, grid / (c->d / 256));
+                fp.comb_chunk = (c->fcomb.T + per_slice - 1) / per_slice;
+            }
             // split boundaries in ffn tiles: uniform (tuning fused_uniform: the two-kernel path's
             // split of whole tiles) or tapered, split i weighted S - i (4 splits: 0.4 / 0.3 / 0.2 / 0.1
             // of K), so the stream ends on the shortest w2 tiles
@@ -1003,7 +1032,6 @@ moe_status run_gemms(moe_ctx* c, GemmPaths gp, int64_t rows_bound, int64_t rows_
                 }
                 fp.split_j[S] = wt;
             }
-            const int grid = c->g1_grid > 0 ? std::min(c->g1_grid, c->num_sms) : c->num_sms;
             c->g1_grid_now = c->g2_grid_now = grid;
             const int i = nb1 == 32 ? 0 : nb1 == 64 ? 1 : 2;
             if (nb1 == 32)
@@ -1020,6 +1048,7 @@ moe_status run_gemms(moe_ctx* c, GemmPaths gp, int64_t rows_bound, int64_t rows_
                            c->tm_h_swap[i]);
             if (s) return s;
             c->fused_now = true;
+            c->fcomb_done = comb;
             *splits_out = S;
             return MOE_OK;
         }
@@ -1547,6 +1576,7 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
         c->fused_splits = tu->fused_splits;
         c->fused_stages = tu->fused_stages;
         c->fused_uniform = tu->fused_uniform;
+        c->fused_combine_mode = tu->fused_combine;
     }
     if (cfg->flags & MOE_FLAG_GATHER) c->gather = true;
     // EP: a rank may receive up to every token of every peer (dropless, reading R6).
@@ -1600,6 +1630,7 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
     ALLOC(c->done, sizeof(unsigned int) * 4);
     ALLOC(c->fused_sched, sizeof(int32_t) * 4);
     ALLOC(c->fused_ready, sizeof(int32_t) * ((int64_t)c->E_local * (c->f_local / 128) + 4));
+    ALLOC(c->fused_arrive, sizeof(int32_t) * (c->d / 256 + 4));
     ALLOC(c->x_perm, sizeof(__nv_bfloat16) * c->cap * c->d);
     ALLOC(c->tok_scale, sizeof(float) * c->cap);
     if (c->fp8) {
@@ -1678,7 +1709,8 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
     }
     if ((e = cudaMemset(c->done, 0, sizeof(unsigned int) * 4)) != cudaSuccess) return fail_init("memset", e);
     if ((e = cudaMemset(c->fused_sched, 0, sizeof(int32_t) * 4)) != cudaSuccess ||
-        (e = cudaMemset(c->fused_ready, 0, sizeof(int32_t) * ((int64_t)c->E_local * (c->f_local / 128) + 4))) != cudaSuccess)
+        (e = cudaMemset(c->fused_ready, 0, sizeof(int32_t) * ((int64_t)c->E_local * (c->f_local / 128) + 4))) != cudaSuccess ||
+        (e = cudaMemset(c->fused_arrive, 0, sizeof(int32_t) * (c->d / 256 + 4))) != cudaSuccess)
         return fail_init("memset", e);
     if ((e = cudaMemset(c->x_perm, 0, sizeof(__nv_bfloat16) * c->cap * c->d)) != cudaSuccess) return fail_init("memset", e);
     if ((e = cudaMemset(c->src_row, 0, sizeof(int32_t) * (c->cap + 512))) != cudaSuccess) return fail_init("memset", e);
@@ -1772,7 +1804,7 @@ moe_status moe_destroy(moe_ctx* c) {
                     c->x_perm, c->h, c->y, c->stage_in, c->stage_out, c->tp_partial, c->tp_scatter, c->ep_send,
                     c->ep_recv, c->ep_ysend, c->ep_yrecv, c->ep_meta_send, c->ep_meta_recv,
                     c->ep_ridx, c->ep_rpos, c->ep_rw, c->ep_rcounts, c->lb_scratch, c->d_peers, c->p2p_tickets, c->src_row,
-                    c->tok_scale, c->h8, c->h_sf, c->fused_sched, c->fused_ready};
+                    c->tok_scale, c->h8, c->h_sf, c->fused_sched, c->fused_ready, c->fused_arrive};
     for (void* p : c->p2p_opened) cudaIpcCloseMemHandle(p);
     if (c->nvls) {
         cudaDeviceSynchronize();  // no fused combine still reads / writes the window
@@ -2139,10 +2171,26 @@ moe_status forward_impl(moe_ctx* c, const void* tokens, int32_t T, const void* r
     c->spec_now = c->spec_now && s2 == MOE_OK;
     if ((s = s2)) return s;
     int splits = 1;
+    const bool residual = (c->cfg.flags & MOE_FLAG_RESIDUAL) != 0;
+    // in-kernel combine by the fused FFN (tuning.fused_combine = 1; single GPU, one combine task
+    // per CTA). Off by default: graph-replayed 64-token decode 0.4066-0.4073 ms with it vs
+    // 0.4029-0.4036 ms with the combine kernel after the fused FFN (3 of 3 interleaved rounds,
+    // profiles/r03/fused_ab.md), although the eager kernel times favour it (402.8 vs 397.0 + 9.5 us)
+    c->fcomb = moe_ctx::FusedCombine{};
+    c->fcomb_done = false;
+    if (!tp && c->fused_combine_mode == 1 && T <= 256) {
+        c->fcomb.on = true;
+        c->fcomb.T = T;
+        c->fcomb.x = residual ? tokens : nullptr;
+        c->fcomb.out = out;
+        c->fcomb.out_f32 = aux ? aux->out_f32 : nullptr;
+    }
     s = run_gemms(c, gpaths, T, (int64_t)T * c->k, (int64_t)T * c->k, &splits, st);
     c->spec_now = false;
+    c->fcomb.on = false;
     if (s) return s;
     if ((s = copy_aux(c, aux, T, st)) || (s = copy_aux_segments(c, aux, st))) return s;
+    if (c->fcomb_done) return MOE_OK;  // the fused FFN wrote out / out_f32
 
     CombineParams cp{};
     cp.y = c->y;
@@ -2151,7 +2199,6 @@ moe_status forward_impl(moe_ctx* c, const void* tokens, int32_t T, const void* r
     cp.pos = c->pos;
     cp.topk_w = c->topk_w;
     cp.T = T; cp.d = c->d; cp.k = c->k;
-    const bool residual = (c->cfg.flags & MOE_FLAG_RESIDUAL) != 0;
     if (!tp) {
         cp.x = residual ? static_cast<const __nv_bfloat16*>(tokens) : nullptr;
         cp.out = static_cast<__nv_bfloat16*>(out);

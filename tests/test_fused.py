@@ -167,3 +167,29 @@ def test_fused_mixtral_decode(moe):
         outs.append(run.np("out_f32").copy())
         blk.close()
     assert np.array_equal(outs[0].view(np.int32), outs[1].view(np.int32))
+
+
+@pytest.mark.parametrize("T,residual", [(64, False), (64, True), (1, False), (37, True), (256, False)])
+def test_fused_combine_bit_identical(moe, T, residual):
+    """In-kernel combine (tuning fused_combine=1: step a9 inside the fused FFN, one combine task
+    of 256 columns x a token chunk per CTA, each waiting for every w2 tile of its slice) vs the
+    combine kernel: the same sums in the same order -> bf16 out and out_f32 bit for bit, with
+    and without the residual; and oracle parity."""
+    shape = synth.MoEShape(T=T, d=512, f=1024, E=8, k=2)
+    inp = synth.make_inputs(shape, 7600 + T, device="cuda")
+    flags = moe.MOE_FLAG_RESIDUAL if residual else 0
+    res = []
+    for fc in (1, 0):
+        blk = _block(moe, inp, 2, T, {"fused": 2, "fused_combine": fc}, flags=flags)
+        run = GpuRun(blk, inp["x"])
+        if fc == 1 and not residual:
+            check_forward(run, to_host_inputs(inp), 2)
+        n = _launches(moe, blk, inp["x"])
+        assert n == (3 if fc == 1 else 4), n  # router, permute, fused FFN (+ combine)
+        out_noaux = blk.forward(inp["x"])  # no aux: out only
+        torch.cuda.synchronize()
+        assert torch.equal(out_noaux.view(torch.int16), run.out.view(torch.int16))
+        res.append((run.np("out_f32").copy(), run.out.clone()))
+        blk.close()
+    assert np.array_equal(res[0][0].view(np.int32), res[1][0].view(np.int32))
+    assert torch.equal(res[0][1].view(torch.int16), res[1][1].view(torch.int16))
