@@ -147,7 +147,10 @@ typedef struct moe_tuning {
     int32_t fused_combine;  /* 1: single-GPU forwards of <= 256 tokens run step a9 inside the fused
                                FFN (combine tasks after the last w2 tiles; bit-identical); 0: the
                                combine kernel runs after it (default: faster under graph replay) */
-    int32_t reserved[4];    /* must be zero                                                  */
+    int32_t fused_chain;    /* 1: the fused FFN's w2 tile of split s adds into buffer 0 after split
+                               s-1 of the same output tile stored (same sums, same order; the
+                               combine reads one partial); 0: S partial buffers the combine adds */
+    int32_t reserved[3];    /* must be zero                                                  */
 } moe_tuning;
 
 typedef struct {

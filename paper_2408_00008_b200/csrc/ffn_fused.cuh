@@ -75,6 +75,12 @@ struct FusedParams {
     float* out_f32;              // [T, d] (nullable)
     int32_t* arrive;             // [d / 256] finished w2 tiles per slice (zero between launches)
     int32_t comb_chunk;          // tokens per combine task; the host keeps the task count <= the grid
+    // Split chaining (chain != nullptr): the w2 tile of split s > 0 waits until split s-1 of the
+    // same output tile (e, m, n) has stored, then stores y = y + acc into the split-0 buffer, so
+    // ((acc_0 + acc_1) + acc_2) + .. lands in one buffer -- the same sums in the same order as
+    // the combine kernel adding S partial buffers, and the combine then reads one partial.
+    // chain[i] = splits stored so far for output tile i (the tile's index within its split).
+    int32_t* chain;
 };
 
 constexpr int kFusedTileRing = 8;  // claimed-tile hand-off ring depth
@@ -98,6 +104,7 @@ struct FusedTile {
     int32_t s;               // G2: split
     int32_t kb0, nkb;        // K blocks (64 columns) of the tile
     int32_t n_valid;         // valid token columns
+    int32_t pidx;            // G2: index of the output tile (e, m, n) within its split
     int32_t nt;              // token tiles of the expert
 };
 
@@ -121,6 +128,7 @@ __device__ __forceinline__ void fused_decode(int t, const FusedParams& p, const 
         ti.s = t / per_split;
         t -= ti.s * per_split;
     }
+    ti.pidx = t;
     int e = 0;
     for (; e < p.g.E; ++e) {
         const int nt = fused_nt(s_counts[e], NB);
@@ -492,7 +500,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                         sj[j] = make_float4(0.f, 0.f, 0.f, 0.f);
                         if (pr[j] >= 0) sj[j] = __ldcg(reinterpret_cast<const float4*>(p.y + (int64_t)pr[j] * p.g.d + c));
                     }
-                    for (int sp = 1; sp < p.splits; ++sp)
+                    for (int sp = 1; sp < (p.chain ? 1 : p.splits); ++sp)
 #pragma unroll
                         for (int j = 0; j < 2; ++j)
                             if (pr[j] >= 0) {
@@ -547,7 +555,17 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 fence_proxy_async_global();  // this thread's h stores -> visible to TMA readers
             } else {
                 // rows 256 m + r (first MMA) and 256 m + 128 + r (second)
-                float* y = p.y + p.y_split_stride * ti.s + static_cast<int64_t>(ti.b_row) * p.g.d + ti.m * 256 + r;
+                const bool chained = p.chain != nullptr;
+                float* y = p.y + (chained ? 0 : p.y_split_stride * ti.s) + static_cast<int64_t>(ti.b_row) * p.g.d +
+                           ti.m * 256 + r;
+                const bool add = chained && ti.s > 0;
+                if (add) {  // split s-1 of this output tile stored (acquire), then y += acc
+                    if (lane == 0) {
+                        while (ld_relaxed_gpu(p.chain + ti.pidx) < ti.s) __nanosleep(32);
+                        fence_acq_rel_gpu();
+                    }
+                    __syncwarp();
+                }
 #pragma unroll 1
                 for (int c = 0; c < nchunks; ++c) {
                     uint32_t v0[16], v1[16];
@@ -558,8 +576,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                     for (int i = 0; i < 16; ++i) {
                         const int n = c * 16 + i;
                         if (n < ti.n_valid) {
-                            y[static_cast<int64_t>(n) * p.g.d] = __uint_as_float(v0[i]);
-                            y[static_cast<int64_t>(n) * p.g.d + 128] = __uint_as_float(v1[i]);
+                            float* yn = y + static_cast<int64_t>(n) * p.g.d;
+                            if (add) {
+                                yn[0] = __ldcg(yn) + __uint_as_float(v0[i]);
+                                yn[128] = __ldcg(yn + 128) + __uint_as_float(v1[i]);
+                            } else {
+                                yn[0] = __uint_as_float(v0[i]);
+                                yn[128] = __uint_as_float(v1[i]);
+                            }
                         }
                     }
                 }
@@ -568,12 +592,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(&tmem_empty[acc]);
             if (++acc == 2) { acc = 0; acc_phase ^= 1; }
-            if (!ti.g1 && p.combine_T > 0) {
-                // publish this tile's partial for the combine tasks of slice m
+            if (!ti.g1 && (p.combine_T > 0 || p.chain)) {
+                // publish this tile's partial: the next split of the output tile (chain) and the
+                // combine tasks of slice m
                 ptx::named_bar_sync(kFusedEpiBar, 128);
                 if (warp == 2 && lane == 0) {
                     __threadfence();
-                    atomicAdd(p.arrive + ti.m, 1);
+                    if (p.chain) atomicExch(p.chain + ti.pidx, ti.s + 1);
+                    if (p.combine_T > 0) atomicAdd(p.arrive + ti.m, 1);
                 }
             }
             if (ti.g1) {
@@ -607,6 +633,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         for (int i = threadIdx.x; i < nready; i += blockDim.x) p.ready[i] = 0;
         if (p.combine_T > 0)
             for (int i = threadIdx.x; i < p.g.d / 256; i += blockDim.x) p.arrive[i] = 0;
+        if (p.chain)
+            for (int i = threadIdx.x; i < per_split; i += blockDim.x) p.chain[i] = 0;
         if (threadIdx.x == 0) {
             p.sched[0] = 0;
             p.sched[1] = 0;

@@ -314,6 +314,9 @@ struct moe_ctx {
     int32_t* fused_sched = nullptr;      // [2] claim / exit counters (zero between launches)
     int32_t* fused_ready = nullptr;      // [E_local * f_local / 128] finished h tiles
     int32_t* fused_arrive = nullptr;     // [d / 256] finished w2 tiles per slice (in-kernel combine)
+    int32_t* fused_chain = nullptr;      // [fused_chain_n] splits stored per w2 output tile (split chaining)
+    int64_t fused_chain_n = 0;
+    int fused_chain_mode = 0;            // tuning.fused_chain: 1 on, 0 off (S partial buffers, default)
     // in-kernel combine of the fused FFN (single GPU, no TP / EP; tuning.fused_combine 1 = on):
     // set by forward_impl before run_gemms, taken by the fused launch (fcomb_done)
     struct FusedCombine {
@@ -639,7 +642,7 @@ moe_status validate_cfg(const moe_config* cfg, moe_ctx* c) {
     for (int i = 0; i < 2; ++i)
         if (cfg->reserved[i]) return fail(c, MOE_ERR_INVALID, "reserved fields must be zero");
     if (const moe_tuning* tu = cfg->tuning) {
-        for (int i = 0; i < 4; ++i)
+        for (int i = 0; i < 3; ++i)
             if (tu->reserved[i]) return fail(c, MOE_ERR_INVALID, "tuning.reserved fields must be zero");
         if (tu->g1_swap_rows < 0 || tu->g2_swap_rows < 0 || tu->g1_grid < 0 || tu->g2_grid < 0 ||
             tu->swap_nb_cap < 0 || tu->router_cc_max_T < 0 || tu->pair_order < 0)
@@ -649,6 +652,8 @@ moe_status validate_cfg(const moe_config* cfg, moe_ctx* c) {
         if (tu->fused < 0 || tu->fused > 2) return fail(c, MOE_ERR_INVALID, "tuning.fused must be 0, 1 or 2");
         if (tu->fused_splits < 0 || tu->fused_splits > 8)
             return fail(c, MOE_ERR_INVALID, "tuning.fused_splits must be in [0, 8]");
+        if (tu->fused_chain < 0 || tu->fused_chain > 1)
+            return fail(c, MOE_ERR_INVALID, "tuning.fused_chain must be 0 or 1");
         if (tu->fused_combine < 0 || tu->fused_combine > 1)
             return fail(c, MOE_ERR_INVALID, "tuning.fused_combine must be 0 or 1");
         if (tu->fused_stages < 0 || tu->fused_stages > 8)
@@ -1003,6 +1008,17 @@ moe_status run_gemms(moe_ctx* c, GemmPaths gp, int64_t rows_bound, int64_t rows_
             fp.sched = c->fused_sched;
             fp.ready = c->fused_ready;
             fp.stages = c->fused_stages;
+            // split chaining (tuning.fused_chain = 1): needs room for every output tile of one split.
+            // Off by default: the combine gets cheaper (8.0 vs 10.2-10.7 us eager) but the fused
+            // kernel slower (411 vs 402-404 us; step 0.4149-0.4156 vs 0.4076-0.4108 ms, 3 of 3
+            // interleaved rounds, profiles/r03/fused_ab.md): the last split's tiles wait for the
+            // previous split of their output tile
+            {
+                int64_t nt_sum = c->E_local;
+                nt_sum += (rows_total + nb1 - 1) / nb1;
+                if (c->fused_chain_mode == 1 && S > 1 && nt_sum * (c->d / 256) <= c->fused_chain_n)
+                    fp.chain = c->fused_chain;
+            }
             const bool comb = c->fcomb.on && c->d / 256 <= grid;  // every combine task claimed by some CTA
             if (comb) {
                 fp.combine_T = c->fcomb.T;
@@ -1049,7 +1065,7 @@ moe_status run_gemms(moe_ctx* c, GemmPaths gp, int64_t rows_bound, int64_t rows_
             if (s) return s;
             c->fused_now = true;
             c->fcomb_done = comb;
-            *splits_out = S;
+            *splits_out = fp.chain ? 1 : S;  // chained: the w2 tiles summed the splits into buffer 0
             return MOE_OK;
         }
     }
@@ -1577,6 +1593,7 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
         c->fused_stages = tu->fused_stages;
         c->fused_uniform = tu->fused_uniform;
         c->fused_combine_mode = tu->fused_combine;
+        c->fused_chain_mode = tu->fused_chain;
     }
     if (cfg->flags & MOE_FLAG_GATHER) c->gather = true;
     // EP: a rank may receive up to every token of every peer (dropless, reading R6).
@@ -1631,6 +1648,9 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
     ALLOC(c->fused_sched, sizeof(int32_t) * 4);
     ALLOC(c->fused_ready, sizeof(int32_t) * ((int64_t)c->E_local * (c->f_local / 128) + 4));
     ALLOC(c->fused_arrive, sizeof(int32_t) * (c->d / 256 + 4));
+    // output tiles of one split: sum_e ceil(rows_e / NB) * d/256 <= (rows / 16 + E_local) * d/256
+    c->fused_chain_n = ((int64_t)c->cap_swap / 16 + c->E_local + 1) * std::max(1, c->d / 256);
+    ALLOC(c->fused_chain, sizeof(int32_t) * c->fused_chain_n);
     ALLOC(c->x_perm, sizeof(__nv_bfloat16) * c->cap * c->d);
     ALLOC(c->tok_scale, sizeof(float) * c->cap);
     if (c->fp8) {
@@ -1710,7 +1730,8 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
     if ((e = cudaMemset(c->done, 0, sizeof(unsigned int) * 4)) != cudaSuccess) return fail_init("memset", e);
     if ((e = cudaMemset(c->fused_sched, 0, sizeof(int32_t) * 4)) != cudaSuccess ||
         (e = cudaMemset(c->fused_ready, 0, sizeof(int32_t) * ((int64_t)c->E_local * (c->f_local / 128) + 4))) != cudaSuccess ||
-        (e = cudaMemset(c->fused_arrive, 0, sizeof(int32_t) * (c->d / 256 + 4))) != cudaSuccess)
+        (e = cudaMemset(c->fused_arrive, 0, sizeof(int32_t) * (c->d / 256 + 4))) != cudaSuccess ||
+        (e = cudaMemset(c->fused_chain, 0, sizeof(int32_t) * c->fused_chain_n)) != cudaSuccess)
         return fail_init("memset", e);
     if ((e = cudaMemset(c->x_perm, 0, sizeof(__nv_bfloat16) * c->cap * c->d)) != cudaSuccess) return fail_init("memset", e);
     if ((e = cudaMemset(c->src_row, 0, sizeof(int32_t) * (c->cap + 512))) != cudaSuccess) return fail_init("memset", e);
@@ -1804,7 +1825,7 @@ moe_status moe_destroy(moe_ctx* c) {
                     c->x_perm, c->h, c->y, c->stage_in, c->stage_out, c->tp_partial, c->tp_scatter, c->ep_send,
                     c->ep_recv, c->ep_ysend, c->ep_yrecv, c->ep_meta_send, c->ep_meta_recv,
                     c->ep_ridx, c->ep_rpos, c->ep_rw, c->ep_rcounts, c->lb_scratch, c->d_peers, c->p2p_tickets, c->src_row,
-                    c->tok_scale, c->h8, c->h_sf, c->fused_sched, c->fused_ready, c->fused_arrive};
+                    c->tok_scale, c->h8, c->h_sf, c->fused_sched, c->fused_ready, c->fused_arrive, c->fused_chain};
     for (void* p : c->p2p_opened) cudaIpcCloseMemHandle(p);
     if (c->nvls) {
         cudaDeviceSynchronize();  // no fused combine still reads / writes the window

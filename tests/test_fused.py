@@ -42,7 +42,7 @@ def _launches(moe, blk, x):
     return moe.moe_launch_count(blk.ctx) - n0
 
 
-@pytest.mark.parametrize("uniform", [0, 1])
+@pytest.mark.parametrize("uniform,chain", [(0, 0), (1, 0), (0, 1), (1, 1)])
 @pytest.mark.parametrize("T,d,f,E,k,splits", [
     (64, 512, 1024, 8, 2, 0),    # decode-like: one token tile per expert (NB 64), auto splits
     (1, 256, 512, 4, 2, 1),      # one token: 2 experts used, 2 empty
@@ -54,12 +54,12 @@ def _launches(moe, blk, x):
     (128, 512, 512, 6, 2, 4),    # NB 128, ragged expert segments
     (48, 256, 2048, 8, 2, 8),    # 16 ffn tiles over 8 tapered splits (8 partial buffers)
 ])
-def test_fused_parity(moe, T, d, f, E, k, splits, uniform):
+def test_fused_parity(moe, T, d, f, E, k, splits, uniform, chain):
     """Tapered (default) and uniform w2 K splits, incl. more splits than ffn tiles allow."""
     shape = synth.MoEShape(T=T, d=d, f=f, E=E, k=k)
     inp = synth.make_inputs(shape, 7100 + T + d + splits, device="cuda")
     host = to_host_inputs(inp)
-    blk = _block(moe, inp, k, T, {"fused": 2, "fused_splits": splits, "fused_uniform": uniform})
+    blk = _block(moe, inp, k, T, {"fused": 2, "fused_splits": splits, "fused_uniform": uniform, "fused_chain": chain})
     run = GpuRun(blk, inp["x"])
     check_forward(run, host, k)
     assert _launches(moe, blk, inp["x"]) == 4  # router, permute, fused FFN, combine
@@ -70,15 +70,16 @@ def test_fused_parity(moe, T, d, f, E, k, splits, uniform):
     blk.close()
 
 
+@pytest.mark.parametrize("chain", [0, 1])
 @pytest.mark.parametrize("T,splits", [(64, 1), (64, 2), (64, 4), (100, 2), (13, 4)])
-def test_fused_bit_identical_to_two_kernels(moe, T, splits):
+def test_fused_bit_identical_to_two_kernels(moe, T, splits, chain):
     """f = 1024 (8 ffn tiles), uniform splits (tuning fused_uniform): K splits 1 / 2 / 4 fall on
     ffn-tile boundaries in both paths, so each fp32 partial is the same sum in the same order
     and the outputs match bit for bit."""
     shape = synth.MoEShape(T=T, d=512, f=1024, E=8, k=2)
     inp = synth.make_inputs(shape, 7200 + T + splits, device="cuda")
     outs = []
-    for tu in ({"fused": 2, "fused_splits": splits, "fused_uniform": 1}, {"fused": 1}):
+    for tu in ({"fused": 2, "fused_splits": splits, "fused_uniform": 1, "fused_chain": chain}, {"fused": 1}):
         blk = _block(moe, inp, 2, T, tu, split_k=splits, flags=moe.MOE_FLAG_FORCE_SWAP)
         run = GpuRun(blk, inp["x"])
         outs.append((run.np("out_f32").copy(), run.out.clone()))
@@ -101,7 +102,7 @@ def test_fused_multi_token_tiles(moe, n):
     li = np.take_along_axis(l, idx.astype(np.int64), 1)
     p = np.exp(li - li.max(1, keepdims=True))
     gw = (p / p.sum(1, keepdims=True)).astype(np.float32)
-    blk = _block(moe, inp, 2, n, {"fused": 2, "swap_nb_cap": 32, "fused_splits": 2})
+    blk = _block(moe, inp, 2, n, {"fused": 2, "swap_nb_cap": 32, "fused_splits": 4})
     run = GpuRun(blk, inp["x"], routed=(torch.from_numpy(idx).cuda(), torch.from_numpy(gw).cuda()))
     check_forward(run, host, 2, routed=True)
     assert run.np("expert_counts").tolist() == [n, n, 0, 0]
@@ -169,8 +170,9 @@ def test_fused_mixtral_decode(moe):
     assert np.array_equal(outs[0].view(np.int32), outs[1].view(np.int32))
 
 
+@pytest.mark.parametrize("chain", [0, 1])
 @pytest.mark.parametrize("T,residual", [(64, False), (64, True), (1, False), (37, True), (256, False)])
-def test_fused_combine_bit_identical(moe, T, residual):
+def test_fused_combine_bit_identical(moe, T, residual, chain):
     """In-kernel combine (tuning fused_combine=1: step a9 inside the fused FFN, one combine task
     of 256 columns x a token chunk per CTA, each waiting for every w2 tile of its slice) vs the
     combine kernel: the same sums in the same order -> bf16 out and out_f32 bit for bit, with
@@ -180,7 +182,7 @@ def test_fused_combine_bit_identical(moe, T, residual):
     flags = moe.MOE_FLAG_RESIDUAL if residual else 0
     res = []
     for fc in (1, 0):
-        blk = _block(moe, inp, 2, T, {"fused": 2, "fused_combine": fc}, flags=flags)
+        blk = _block(moe, inp, 2, T, {"fused": 2, "fused_combine": fc, "fused_chain": chain}, flags=flags)
         run = GpuRun(blk, inp["x"])
         if fc == 1 and not residual:
             check_forward(run, to_host_inputs(inp), 2)
