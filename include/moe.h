@@ -150,7 +150,10 @@ typedef struct moe_tuning {
     int32_t fused_chain;    /* 1: the fused FFN's w2 tile of split s adds into buffer 0 after split
                                s-1 of the same output tile stored (same sums, same order; the
                                combine reads one partial); 0: S partial buffers the combine adds */
-    int32_t reserved[3];    /* must be zero                                                  */
+    int32_t fused_half;     /* fused FFN w1/w3 tiles of 128 rows (64 w1 + 64 w3 rows, a/b paired
+                               through shared memory): 0 auto (where the 256-row tiles do not
+                               fill the SMs), 1 off, 2 on                                      */
+    int32_t reserved[2];    /* must be zero                                                  */
 } moe_tuning;
 
 typedef struct {

@@ -58,7 +58,7 @@ struct FusedParams {
     int32_t splits;          // S: K splits of the w2 tiles (over whole ffn tiles)
     int32_t w2_nt;           // W2 tiles (128 rows) per expert in the tiled layout
     int32_t* sched;          // [4] claims, CTA exits, finished G1 tiles (zero between launches)
-    int32_t* ready;          // [E * (f/128)] finished G1 token tiles per (expert, ffn tile)
+    int32_t* ready;          // [E * (f/64)] finished G1 token tiles per (expert, 64 h columns)
     int32_t stages;          // pipeline stages used (1..kStages; 0 = all that fit)
     int32_t split_j[9];      // ffn-tile boundaries of the w2 K splits: 0 = j_0 < .. < j_S = f/128
     // In-kernel combine (single GPU, step a9; combine_T = 0: off, moe_combine_kernel runs
@@ -86,13 +86,21 @@ struct FusedParams {
 constexpr int kFusedTileRing = 8;  // claimed-tile hand-off ring depth
 constexpr int kFusedEpiBar = 1;    // named barrier of the 4 epilogue warps
 
-template <int NB>
+// HALF (small per-rank shapes, round 3): w1/w3 tiles of 128 rows -- 64 w1 + 64 w3 rows of
+// one 64-column h tile, two 64-row TMA boxes per K block -- so the first wave of w1/w3 work
+// spreads over twice as many CTAs; a stage then carries two K blocks of such a tile (32 KB
+// of weights + 2 x NB token rows), and the epilogue pairs a (TMEM lanes 0-63) with b (lanes
+// 64-127) through a shared-memory exchange buffer. w2 tiles are the same in both variants.
+template <int NB, bool HALF = false>
 struct FusedCfg {
-    static constexpr int kABytes = 256 * 128;       // 256 weight rows x 64 bf16
-    static constexpr int kBBytes = NB * 128;        // NB token rows x 64 bf16
+    static constexpr int kABytes = 256 * 128;       // 256 weight rows x 64 bf16 (HALF G1: 2 x 128 rows x 64)
+    static constexpr int kBBytes = (HALF ? 2 : 1) * NB * 128;  // token rows x 64 bf16 (x 2 K blocks)
     static constexpr int kStageBytes = kABytes + kBBytes;
-    static constexpr int kStages = (kSmemBudget - 2048) / kStageBytes > 8 ? 8 : (kSmemBudget - 2048) / kStageBytes;
-    static constexpr int kSmemBytes = kStages * kStageBytes + 2048;
+    static constexpr int kXPitch = NB + 1;          // exchange row pitch in floats (bank-conflict free)
+    static constexpr int kXBytes = HALF ? 64 * kXPitch * 4 : 0;
+    static constexpr int kStagesRaw = (kSmemBudget - 2048 - kXBytes) / kStageBytes;
+    static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
+    static constexpr int kSmemBytes = kStages * kStageBytes + kXBytes + 2048;
     static_assert(NB >= 16 && NB <= 128 && NB % 16 == 0, "fused tile: a/b accumulators of <= 128 columns");
     static_assert(kStages >= 3, "pipeline too shallow");
 };
@@ -101,6 +109,7 @@ struct FusedTile {
     bool g1;
     int32_t e, rows, b_row;  // expert, its rows, first token row of the tile (permuted buffer)
     int32_t m;               // G1: ffn tile; G2: 256-row weight tile
+    int32_t hf;              // HALF G1: which 64 columns of ffn tile m
     int32_t s;               // G2: split
     int32_t kb0, nkb;        // K blocks (64 columns) of the tile
     int32_t n_valid;         // valid token columns
@@ -116,10 +125,10 @@ __device__ __forceinline__ int fused_nt(int rows, int NB) { return rows > 0 ? (r
 //                    [split_j[s], split_j[s+1]) -- by default tapered (the host gives the
 //                    first splits the most K and the last the least), so the stream ends on
 //                    the shortest tiles and the CTAs' exits bunch up.
-template <int NB>
+template <int NB, bool HALF>
 __device__ __forceinline__ void fused_decode(int t, const FusedParams& p, const int32_t* s_counts,
                                              const int32_t* s_offsets, int total1, int per_split, FusedTile& ti) {
-    const int wt = p.g.f / 128;
+    const int wt = p.g.f / 128 * (HALF ? 2 : 1);  // w1/w3 tiles per expert and token tile
     const int mt2 = p.g.d / 256;
     ti.g1 = t < total1;
     ti.s = 0;
@@ -141,6 +150,11 @@ __device__ __forceinline__ void fused_decode(int t, const FusedParams& p, const 
     ti.nt = fused_nt(ti.rows, NB);
     const int n_idx = t % ti.nt;
     ti.m = t / ti.nt;
+    ti.hf = 0;
+    if (ti.g1 && HALF) {
+        ti.hf = ti.m & 1;
+        ti.m >>= 1;
+    }
     if (ti.g1) {
         ti.kb0 = 0;
         ti.nkb = p.g.d / 64;
@@ -163,21 +177,23 @@ __device__ __forceinline__ void fence_proxy_async_global() {
     asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
-// tmW13: W13 tiled map (box 64 x 256 rows); tmX: permuted tokens (box 64 x NB);
-// tmW2: W2 tiled map with 2-tile boxes (64 x 128 rows x 1 x 2 = 256 rows); tmH: h (box 64 x NB)
-template <int NB>
+// tmW13: W13 tiled map (box 64 x 256 rows; HALF: 64 x 64 rows); tmX: permuted tokens (box
+// 64 x NB); tmW2: W2 tiled map with 2-tile boxes (64 x 128 rows x 1 x 2 = 256 rows); tmH: h
+// (box 64 x NB)
+template <int NB, bool HALF>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     moe_ffn_fused_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmW13,
                          const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW2,
                          const __grid_constant__ CUtensorMap tmH) {
-    using C = FusedCfg<NB>;
+    using C = FusedCfg<NB, HALF>;
     constexpr int S = C::kStages;
     constexpr int R = kFusedTileRing;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* smem_a = smem;
     uint8_t* smem_b = smem + S * C::kABytes;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * C::kStageBytes);
+    float* smem_x = reinterpret_cast<float*>(smem + S * C::kStageBytes);  // HALF: [64][kXPitch] b values
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * C::kStageBytes + C::kXBytes);
     uint64_t* full = bars;
     uint64_t* empty = bars + S;
     uint64_t* tmem_full = bars + 2 * S;
@@ -235,13 +251,17 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     // stall several us issuing prefetches into a busy memory system, and the producer must
     // not wait for that (timeline r03: post-wait stamps up to 9 us late when lane 0 issued).
     if (p.g.spec_l2 > 0 && threadIdx.x == 160) {
-        const int wt = p.g.f / 128;
+        const int wt = p.g.f / 128 * (HALF ? 2 : 1);
         if ((int)blockIdx.x < p.g.E * wt) {
-            const int e = blockIdx.x / wt, m = blockIdx.x % wt;
+            const int e = blockIdx.x / wt, m = (blockIdx.x % wt) / (HALF ? 2 : 1), hf = HALF ? blockIdx.x % 2 : 0;
             const int nk = min(p.g.spec_l2, p.g.d / kBK);
             for (int kb = 0; kb < nk; ++kb) {
-                const WCoord w = wcoord(p.g, kb * kBK, m * 256, e);
+                const WCoord w = wcoord(p.g, kb * kBK, m * 256 + 64 * hf, e);
                 ptx::tma_prefetch_l2_4d(&tmW13, 0, w.c1, w.c2, w.c3);
+                if (HALF) {  // the w3 rows of the same 64 columns
+                    const WCoord w3 = wcoord(p.g, kb * kBK, m * 256 + 128 + 64 * hf, e);
+                    ptx::tma_prefetch_l2_4d(&tmW13, 0, w3.c1, w3.c2, w3.c3);
+                }
             }
         }
     }
@@ -266,10 +286,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const uint32_t tmem_base = *tmem_base_slot;
 
     const int wt = p.g.f / 128;
+    const int wq = p.g.f / 64;  // 64-column h tiles per expert (readiness granularity)
     int total1 = 0, per_split = 0;
     for (int e = 0; e < p.g.E; ++e) {
         const int nt = fused_nt(s_counts[e], NB);
-        total1 += nt * wt;
+        total1 += nt * wt * (HALF ? 2 : 1);
         per_split += nt * (p.g.d / 256);
     }
     const int total = total1 + per_split * p.splits;
@@ -322,16 +343,35 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 if (t >= total_all) break;
                 if (t >= total) continue;  // combine task: the epilogue warps only
                 FusedTile ti;
-                fused_decode<NB>(t, p, s_counts, s_offsets, total1, per_split, ti);
+                fused_decode<NB, HALF>(t, p, s_counts, s_offsets, total1, per_split, ti);
                 if (!ti.g1 && !all_ready && ld_relaxed_gpu(&p.sched[2]) >= total1) {
                     fence_acq_rel_gpu();
                     fence_proxy_async_global();
                     all_ready = true;
                 }
-                if (ti.g1 || all_ready) {
-                    for (int kb = 0; kb < ti.nkb; ++kb) {
+                if (HALF && ti.g1) {
+                    // two K blocks per stage: [kb: 64 w1 rows | 64 w3 rows][kb+1: ...] + 2 x NB tokens
+                    for (int kb = 0; kb < ti.nkb; kb += 2) {
                         ptx::mbar_wait(&empty[stage], phase ^ 1);
                         ptx::mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
+                        uint8_t* sa = smem_a + stage * C::kABytes;
+                        uint8_t* sb = smem_b + stage * C::kBBytes;
+#pragma unroll
+                        for (int u = 0; u < 2; ++u) {
+                            const WCoord w1c = wcoord(p.g, (kb + u) * kBK, ti.m * 256 + 64 * ti.hf, ti.e);
+                            const WCoord w3c = wcoord(p.g, (kb + u) * kBK, ti.m * 256 + 128 + 64 * ti.hf, ti.e);
+                            ptx::tma_load_4d(&tmW13, &full[stage], sa + u * 16384, 0, w1c.c1, w1c.c2, w1c.c3, w_hint);
+                            ptx::tma_load_4d(&tmW13, &full[stage], sa + u * 16384 + 8192, 0, w3c.c1, w3c.c2, w3c.c3,
+                                             w_hint);
+                            ptx::tma_load_2d(&tmX, &full[stage], sb + u * NB * 128, (kb + u) * kBK, ti.b_row,
+                                             ptx::kEvictLast);
+                        }
+                        if (++stage == SR) { stage = 0; phase ^= 1; }
+                    }
+                } else if (ti.g1 || all_ready) {
+                    for (int kb = 0; kb < ti.nkb; ++kb) {
+                        ptx::mbar_wait(&empty[stage], phase ^ 1);
+                        ptx::mbar_arrive_expect_tx(&full[stage], C::kABytes + NB * 128);
                         uint8_t* sa = smem_a + stage * C::kABytes;
                         uint8_t* sb = smem_b + stage * C::kBBytes;
                         if (ti.g1) {
@@ -346,12 +386,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                         if (++stage == SR) { stage = 0; phase ^= 1; }
                     }
                 } else {
-                    // Some G1 tiles still run: h loads of K block q need ffn tile (kb0 + q) / 2 of
-                    // expert e finished by all of its token tiles; weight loads run up to the ring
-                    // depth ahead. ok = consecutive finished ffn tiles from j0 (relaxed reads,
-                    // then fence.acq_rel = acquire, then the proxy fence for the TMA reads).
-                    const int32_t* rdy = p.ready + ti.e * wt + ti.kb0 / 2;
-                    const int nj = ti.nkb / 2;
+                    // Some G1 tiles still run: h loads of K block q need the 64 h columns of K block
+                    // kb0 + q of expert e finished by all of its token tiles; weight loads run up to
+                    // the ring depth ahead. ok = consecutive finished K blocks from kb0 (relaxed
+                    // reads, then fence.acq_rel = acquire, then the proxy fence for the TMA reads).
+                    const int32_t* rdy = p.ready + ti.e * wq + ti.kb0;
+                    const int nj = ti.nkb;
                     int ok = 0;
                     auto refresh = [&]() {
                         const int ok0 = ok;
@@ -380,11 +420,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                     };
                     auto wait_ready = [&](int q) {
 #if MOE_TIMELINE
-                        const unsigned long long w0 = q / 2 >= ok ? ptx::tl_now() : 0;
+                        const unsigned long long w0 = q >= ok ? ptx::tl_now() : 0;
 #endif
-                        while (q / 2 >= ok) {
+                        while (q >= ok) {
                             refresh();
-                            if (q / 2 >= ok) __nanosleep(64);
+                            if (q >= ok) __nanosleep(64);
                         }
 #if MOE_TIMELINE
                         if (w0) tl_stall += ptx::tl_now() - w0;
@@ -398,15 +438,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                             issue_b(bq++);
                         }
                         ptx::mbar_wait(&empty[stage], phase ^ 1);
-                        ptx::mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
+                        ptx::mbar_arrive_expect_tx(&full[stage], C::kABytes + NB * 128);
                         uint8_t* sa = smem_a + stage * C::kABytes;
                         const int kq = ti.kb0 + q;
                         ptx::tma_load_4d(&tmW2, &full[stage], sa, 0, 0, kq, 2 * ti.m + ti.e * p.w2_nt, w_hint);
                         // weights of the first stages go out before the first readiness check
                         if (q == SR - 1 || q == ti.nkb - 1 || (q >= SR && (q & 3) == 3)) {
-                            if (bq / 2 >= ok) refresh();
+                            if (bq >= ok) refresh();
                         }
-                        while (bq <= q && bq / 2 < ok) issue_b(bq++);
+                        while (bq <= q && bq < ok) issue_b(bq++);
                         if (++stage == SR) { stage = 0; phase ^= 1; }
                     }
                     while (bq < ti.nkb) {
@@ -433,25 +473,41 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 if (t >= total_all) break;
                 if (t >= total) continue;
                 FusedTile ti;
-                fused_decode<NB>(t, p, s_counts, s_offsets, total1, per_split, ti);
+                fused_decode<NB, HALF>(t, p, s_counts, s_offsets, total1, per_split, ti);
                 const uint32_t n_mma = (uint32_t)((ti.n_valid + 15) / 16 * 16);
                 const uint32_t idesc = ptx::make_idesc_bf16(128, n_mma);
                 const uint32_t d_tmem = tmem_base + acc * 256;
                 ptx::mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
                 ptx::tc_fence_after();
-                for (int kb = 0; kb < ti.nkb; ++kb) {
+                const bool half_g1 = HALF && ti.g1;
+                for (int kb = 0; kb < ti.nkb; kb += half_g1 ? 2 : 1) {
                     ptx::mbar_wait(&full[stage], phase);
                     ptx::tc_fence_after();
                     const uint32_t sa = ptx::smem_u32(smem_a + stage * C::kABytes);
                     const uint32_t sb = ptx::smem_u32(smem_b + stage * C::kBBytes);
-                    const uint64_t adesc = ptx::make_smem_desc_sw128(sa);
-                    const uint64_t adesc2 = ptx::make_smem_desc_sw128(sa + 128 * 128);
-                    const uint64_t bdesc = ptx::make_smem_desc_sw128(sb);
+                    if (half_g1) {
+                        // A = [K block kb: 64 w1 + 64 w3 rows][K block kb+1], one M = 128 MMA per k16:
+                        // a lands in TMEM lanes 0-63, b in lanes 64-127
 #pragma unroll
-                    for (int kk = 0; kk < kBK / 16; ++kk) {
-                        const uint32_t accum = (kb | kk) ? 1u : 0u;
-                        ptx::mma_bf16(d_tmem, adesc + 2 * kk, bdesc + 2 * kk, idesc, accum);
-                        ptx::mma_bf16(d_tmem + 128, adesc2 + 2 * kk, bdesc + 2 * kk, idesc, accum);
+                        for (int u = 0; u < 2; ++u) {
+                            const uint64_t adesc = ptx::make_smem_desc_sw128(sa + u * 16384);
+                            const uint64_t bdesc = ptx::make_smem_desc_sw128(sb + u * NB * 128);
+#pragma unroll
+                            for (int kk = 0; kk < kBK / 16; ++kk) {
+                                const uint32_t accum = (kb | u | kk) ? 1u : 0u;
+                                ptx::mma_bf16(d_tmem, adesc + 2 * kk, bdesc + 2 * kk, idesc, accum);
+                            }
+                        }
+                    } else {
+                        const uint64_t adesc = ptx::make_smem_desc_sw128(sa);
+                        const uint64_t adesc2 = ptx::make_smem_desc_sw128(sa + 128 * 128);
+                        const uint64_t bdesc = ptx::make_smem_desc_sw128(sb);
+#pragma unroll
+                        for (int kk = 0; kk < kBK / 16; ++kk) {
+                            const uint32_t accum = (kb | kk) ? 1u : 0u;
+                            ptx::mma_bf16(d_tmem, adesc + 2 * kk, bdesc + 2 * kk, idesc, accum);
+                            ptx::mma_bf16(d_tmem + 128, adesc2 + 2 * kk, bdesc + 2 * kk, idesc, accum);
+                        }
                     }
                     ptx::mma_commit(&empty[stage]);
                     if (++stage == SR) { stage = 0; phase ^= 1; }
@@ -529,12 +585,47 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 continue;
             }
             FusedTile ti;
-            fused_decode<NB>(t, p, s_counts, s_offsets, total1, per_split, ti);
+            fused_decode<NB, HALF>(t, p, s_counts, s_offsets, total1, per_split, ti);
             ptx::mbar_wait(&tmem_full[acc], acc_phase);
             ptx::tc_fence_after();
             const uint32_t tbase = tmem_base + acc * 256 + (static_cast<uint32_t>(q * 32) << 16);
             const int nchunks = (ti.n_valid + 15) / 16;
-            if (ti.g1) {
+            if (HALF && ti.g1) {
+                // a of h column j (64 per tile) in TMEM lane j (warps q = 0, 1), b in lane 64 + j
+                // (warps q = 2, 3): b goes through shared memory, warps 0 / 1 finish h
+                if (q >= 2) {
+                    float* xr = smem_x + (r - 64) * C::kXPitch;
+#pragma unroll 1
+                    for (int c = 0; c < nchunks; ++c) {
+                        uint32_t b[16];
+                        ptx::tmem_ld16(tbase + c * 16, b);
+                        ptx::tmem_wait_ld();
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) xr[c * 16 + i] = __uint_as_float(b[i]);
+                    }
+                }
+                ptx::named_bar_sync(kFusedEpiBar, 128);
+                if (q < 2) {
+                    const float* xr = smem_x + r * C::kXPitch;
+                    __nv_bfloat16* h = static_cast<__nv_bfloat16*>(p.g.out) +
+                                       static_cast<int64_t>(ti.b_row) * p.g.f + ti.m * 128 + 64 * ti.hf + r;
+#pragma unroll 1
+                    for (int c = 0; c < nchunks; ++c) {
+                        uint32_t a[16];
+                        ptx::tmem_ld16(tbase + c * 16, a);
+                        ptx::tmem_wait_ld();
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) {
+                            const int n = c * 16 + i;
+                            if (n < ti.n_valid) {
+                                const float hv = silu_f32(__uint_as_float(a[i])) * xr[n];
+                                h[static_cast<int64_t>(n) * p.g.f] = __float2bfloat16_rn(hv);
+                            }
+                        }
+                    }
+                    fence_proxy_async_global();
+                }
+            } else if (ti.g1) {
                 __nv_bfloat16* h = static_cast<__nv_bfloat16*>(p.g.out) + static_cast<int64_t>(ti.b_row) * p.g.f +
                                    ti.m * 128 + r;
 #pragma unroll 1
@@ -607,7 +698,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 ptx::named_bar_sync(kFusedEpiBar, 128);
                 if (warp == 2 && lane == 0) {
                     __threadfence();
-                    atomicAdd(p.ready + ti.e * wt + ti.m, 1);
+                    if (HALF) {
+                        atomicAdd(p.ready + ti.e * wq + 2 * ti.m + ti.hf, 1);
+                    } else {
+                        atomicAdd(p.ready + ti.e * wq + 2 * ti.m, 1);
+                        atomicAdd(p.ready + ti.e * wq + 2 * ti.m + 1, 1);
+                    }
                     atomicAdd(&p.sched[2], 1);
                 }
             }
@@ -629,7 +725,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     __syncthreads();
     if (*s_last) {
         __threadfence();
-        const int nready = p.g.E * wt;
+        const int nready = p.g.E * wq;
         for (int i = threadIdx.x; i < nready; i += blockDim.x) p.ready[i] = 0;
         if (p.combine_T > 0)
             for (int i = threadIdx.x; i < p.g.d / 256; i += blockDim.x) p.arrive[i] = 0;

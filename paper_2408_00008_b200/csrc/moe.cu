@@ -317,6 +317,8 @@ struct moe_ctx {
     int32_t* fused_chain = nullptr;      // [fused_chain_n] splits stored per w2 output tile (split chaining)
     int64_t fused_chain_n = 0;
     int fused_chain_mode = 0;            // tuning.fused_chain: 1 on, 0 off (S partial buffers, default)
+    int fused_half_mode = 0;             // tuning.fused_half: 0 auto, 1 off, 2 on (128-row w1/w3 tiles)
+    bool fused_half_now = false;
     // in-kernel combine of the fused FFN (single GPU, no TP / EP; tuning.fused_combine 1 = on):
     // set by forward_impl before run_gemms, taken by the fused launch (fcomb_done)
     struct FusedCombine {
@@ -376,12 +378,12 @@ struct moe_ctx {
         const void* w13 = nullptr;
         const void* w2 = nullptr;
         uint64_t tick = 0;
-        CUtensorMap tm_w13{}, tm_w13_pair{}, tm_w2_tiled{}, tm_w2_swap{};
+        CUtensorMap tm_w13{}, tm_w13_pair{}, tm_w2_tiled{}, tm_w2_swap{}, tm_w13_h{};
     };
     static constexpr size_t kWeightMapCache = 64;
     std::vector<WeightMaps> wmaps;
     uint64_t use_tick = 0;
-    CUtensorMap tm_w13{}, tm_w13_pair{}, tm_w2_tiled{}, tm_w2_swap{};  // maps of the current call
+    CUtensorMap tm_w13{}, tm_w13_pair{}, tm_w2_tiled{}, tm_w2_swap{}, tm_w13_h{};  // maps of the current call
     // instrumentation
     bool profiling = false;
     struct Ev { int slot; cudaEvent_t a, b; };
@@ -489,8 +491,10 @@ moe_status set_spair_attr(moe_ctx* c) {
 
 template <int NB>
 moe_status set_fused_attr(moe_ctx* c) {
-    CUDA_TRY(c, cudaFuncSetAttribute(moe_ffn_fused_kernel<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     FusedCfg<NB>::kSmemBytes));
+    CUDA_TRY(c, cudaFuncSetAttribute(moe_ffn_fused_kernel<NB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     FusedCfg<NB, false>::kSmemBytes));
+    CUDA_TRY(c, cudaFuncSetAttribute(moe_ffn_fused_kernel<NB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     FusedCfg<NB, true>::kSmemBytes));
     return MOE_OK;
 }
 
@@ -642,7 +646,7 @@ moe_status validate_cfg(const moe_config* cfg, moe_ctx* c) {
     for (int i = 0; i < 2; ++i)
         if (cfg->reserved[i]) return fail(c, MOE_ERR_INVALID, "reserved fields must be zero");
     if (const moe_tuning* tu = cfg->tuning) {
-        for (int i = 0; i < 3; ++i)
+        for (int i = 0; i < 2; ++i)
             if (tu->reserved[i]) return fail(c, MOE_ERR_INVALID, "tuning.reserved fields must be zero");
         if (tu->g1_swap_rows < 0 || tu->g2_swap_rows < 0 || tu->g1_grid < 0 || tu->g2_grid < 0 ||
             tu->swap_nb_cap < 0 || tu->router_cc_max_T < 0 || tu->pair_order < 0)
@@ -652,6 +656,8 @@ moe_status validate_cfg(const moe_config* cfg, moe_ctx* c) {
         if (tu->fused < 0 || tu->fused > 2) return fail(c, MOE_ERR_INVALID, "tuning.fused must be 0, 1 or 2");
         if (tu->fused_splits < 0 || tu->fused_splits > 8)
             return fail(c, MOE_ERR_INVALID, "tuning.fused_splits must be in [0, 8]");
+        if (tu->fused_half < 0 || tu->fused_half > 2)
+            return fail(c, MOE_ERR_INVALID, "tuning.fused_half must be 0, 1 or 2");
         if (tu->fused_chain < 0 || tu->fused_chain > 1)
             return fail(c, MOE_ERR_INVALID, "tuning.fused_chain must be 0 or 1");
         if (tu->fused_combine < 0 || tu->fused_combine > 1)
@@ -676,7 +682,7 @@ moe_status ensure_weight_maps(moe_ctx* c, const moe_expert_weights* w) {
         if (m.w13 == w->w13 && m.w2 == w->w2) {
             m.tick = c->use_tick;
             c->tm_w13 = m.tm_w13; c->tm_w13_pair = m.tm_w13_pair;
-            c->tm_w2_tiled = m.tm_w2_tiled; c->tm_w2_swap = m.tm_w2_swap;
+            c->tm_w2_tiled = m.tm_w2_tiled; c->tm_w2_swap = m.tm_w2_swap; c->tm_w13_h = m.tm_w13_h;
             return MOE_OK;
         }
     moe_ctx::WeightMaps m;
@@ -691,7 +697,8 @@ moe_status ensure_weight_maps(moe_ctx* c, const moe_expert_weights* w) {
         // tiled layout: W13 in 256-row tiles, W2 in 128-row tiles (rows padded to 256)
         const uint64_t nt13 = (uint64_t)c->E_local * c->w13_nt, nt2 = (uint64_t)c->E_local * c->w2_nt;
         if (!encode_wmap(&m.tm_w13, w->w13, c->d, 256, nt13, 256, 1) ||
-            !encode_wmap(&m.tm_w13_pair, w->w13, c->d, 256, nt13, 128, 1))
+            !encode_wmap(&m.tm_w13_pair, w->w13, c->d, 256, nt13, 128, 1) ||
+            !encode_wmap(&m.tm_w13_h, w->w13, c->d, 256, nt13, 64, 1))
             return fail(c, MOE_ERR_CUDA, "cuTensorMapEncodeTiled(w13) failed");
         if (!encode_wmap(&m.tm_w2_tiled, w->w2, c->f_local, 128, nt2, 128, 2) ||
             !encode_wmap(&m.tm_w2_swap, w->w2, c->f_local, 128, nt2, 128, 1))
@@ -706,7 +713,7 @@ moe_status ensure_weight_maps(moe_ctx* c, const moe_expert_weights* w) {
         c->wmaps.push_back(m);
     }
     c->tm_w13 = m.tm_w13; c->tm_w13_pair = m.tm_w13_pair;
-    c->tm_w2_tiled = m.tm_w2_tiled; c->tm_w2_swap = m.tm_w2_swap;
+    c->tm_w2_tiled = m.tm_w2_tiled; c->tm_w2_swap = m.tm_w2_swap; c->tm_w13_h = m.tm_w13_h;
     return MOE_OK;
 }
 
@@ -1050,18 +1057,23 @@ moe_status run_gemms(moe_ctx* c, GemmPaths gp, int64_t rows_bound, int64_t rows_
             }
             c->g1_grid_now = c->g2_grid_now = grid;
             const int i = nb1 == 32 ? 0 : nb1 == 64 ? 1 : 2;
+            // 128-row w1/w3 tiles where the 256-row ones do not fill the SMs (tuning.fused_half)
+            const bool half = c->fused_half_mode == 2 || (c->fused_half_mode == 0 && U1 < (int64_t)c->num_sms);
+            c->fused_half_now = half;
+            const CUtensorMap& tw = half ? c->tm_w13_h : c->tm_w13;
+            auto go = [&](auto kern, size_t smem) {
+                return launch(c, kSlotGemm1, kern, dim3(grid), dim3(kGemmThreads), smem, st, fp, tw, c->tm_x_swap[i],
+                              c->tm_w2_tiled, c->tm_h_swap[i]);
+            };
             if (nb1 == 32)
-                s = launch(c, kSlotGemm1, moe_ffn_fused_kernel<32>, dim3(grid), dim3(kGemmThreads),
-                           (size_t)FusedCfg<32>::kSmemBytes, st, fp, c->tm_w13, c->tm_x_swap[i], c->tm_w2_tiled,
-                           c->tm_h_swap[i]);
+                s = half ? go(moe_ffn_fused_kernel<32, true>, (size_t)FusedCfg<32, true>::kSmemBytes)
+                         : go(moe_ffn_fused_kernel<32, false>, (size_t)FusedCfg<32, false>::kSmemBytes);
             else if (nb1 == 64)
-                s = launch(c, kSlotGemm1, moe_ffn_fused_kernel<64>, dim3(grid), dim3(kGemmThreads),
-                           (size_t)FusedCfg<64>::kSmemBytes, st, fp, c->tm_w13, c->tm_x_swap[i], c->tm_w2_tiled,
-                           c->tm_h_swap[i]);
+                s = half ? go(moe_ffn_fused_kernel<64, true>, (size_t)FusedCfg<64, true>::kSmemBytes)
+                         : go(moe_ffn_fused_kernel<64, false>, (size_t)FusedCfg<64, false>::kSmemBytes);
             else
-                s = launch(c, kSlotGemm1, moe_ffn_fused_kernel<128>, dim3(grid), dim3(kGemmThreads),
-                           (size_t)FusedCfg<128>::kSmemBytes, st, fp, c->tm_w13, c->tm_x_swap[i], c->tm_w2_tiled,
-                           c->tm_h_swap[i]);
+                s = half ? go(moe_ffn_fused_kernel<128, true>, (size_t)FusedCfg<128, true>::kSmemBytes)
+                         : go(moe_ffn_fused_kernel<128, false>, (size_t)FusedCfg<128, false>::kSmemBytes);
             if (s) return s;
             c->fused_now = true;
             c->fcomb_done = comb;
@@ -1594,6 +1606,7 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
         c->fused_uniform = tu->fused_uniform;
         c->fused_combine_mode = tu->fused_combine;
         c->fused_chain_mode = tu->fused_chain;
+        c->fused_half_mode = tu->fused_half;
     }
     if (cfg->flags & MOE_FLAG_GATHER) c->gather = true;
     // EP: a rank may receive up to every token of every peer (dropless, reading R6).
@@ -1646,7 +1659,7 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
     ALLOC(c->offsets, sizeof(int32_t) * 64);
     ALLOC(c->done, sizeof(unsigned int) * 4);
     ALLOC(c->fused_sched, sizeof(int32_t) * 4);
-    ALLOC(c->fused_ready, sizeof(int32_t) * ((int64_t)c->E_local * (c->f_local / 128) + 4));
+    ALLOC(c->fused_ready, sizeof(int32_t) * ((int64_t)c->E_local * (c->f_local / 64) + 4));
     ALLOC(c->fused_arrive, sizeof(int32_t) * (c->d / 256 + 4));
     // output tiles of one split: sum_e ceil(rows_e / NB) * d/256 <= (rows / 16 + E_local) * d/256
     c->fused_chain_n = ((int64_t)c->cap_swap / 16 + c->E_local + 1) * std::max(1, c->d / 256);
@@ -1729,7 +1742,7 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
     }
     if ((e = cudaMemset(c->done, 0, sizeof(unsigned int) * 4)) != cudaSuccess) return fail_init("memset", e);
     if ((e = cudaMemset(c->fused_sched, 0, sizeof(int32_t) * 4)) != cudaSuccess ||
-        (e = cudaMemset(c->fused_ready, 0, sizeof(int32_t) * ((int64_t)c->E_local * (c->f_local / 128) + 4))) != cudaSuccess ||
+        (e = cudaMemset(c->fused_ready, 0, sizeof(int32_t) * ((int64_t)c->E_local * (c->f_local / 64) + 4))) != cudaSuccess ||
         (e = cudaMemset(c->fused_arrive, 0, sizeof(int32_t) * (c->d / 256 + 4))) != cudaSuccess ||
         (e = cudaMemset(c->fused_chain, 0, sizeof(int32_t) * c->fused_chain_n)) != cudaSuccess)
         return fail_init("memset", e);
@@ -1807,9 +1820,12 @@ reinterpret_cast<const void*>(moe_ep_p2p_fill_kernel),
             reinterpret_cast<const void*>(moe_gemm_fp8x_kernel<kG2Swap, 32>),
             reinterpret_cast<const void*>(moe_gemm_fp8x_kernel<kG2Swap, 64>),
             reinterpret_cast<const void*>(moe_gemm_fp8x_kernel<kG2Swap, 128>),
-            reinterpret_cast<const void*>(moe_ffn_fused_kernel<32>),
-            reinterpret_cast<const void*>(moe_ffn_fused_kernel<64>),
-            reinterpret_cast<const void*>(moe_ffn_fused_kernel<128>)};
+            reinterpret_cast<const void*>(moe_ffn_fused_kernel<32, false>),
+            reinterpret_cast<const void*>(moe_ffn_fused_kernel<64, false>),
+            reinterpret_cast<const void*>(moe_ffn_fused_kernel<128, false>),
+            reinterpret_cast<const void*>(moe_ffn_fused_kernel<32, true>),
+            reinterpret_cast<const void*>(moe_ffn_fused_kernel<64, true>),
+            reinterpret_cast<const void*>(moe_ffn_fused_kernel<128, true>)};
         for (const void* fn : fns)
             if ((e = cudaFuncGetAttributes(&fa, fn)) != cudaSuccess) return fail_init("cudaFuncGetAttributes", e);
     }

@@ -42,6 +42,7 @@ def _launches(moe, blk, x):
     return moe.moe_launch_count(blk.ctx) - n0
 
 
+@pytest.mark.parametrize("half", [1, 2])
 @pytest.mark.parametrize("uniform,chain", [(0, 0), (1, 0), (0, 1), (1, 1)])
 @pytest.mark.parametrize("T,d,f,E,k,splits", [
     (64, 512, 1024, 8, 2, 0),    # decode-like: one token tile per expert (NB 64), auto splits
@@ -54,12 +55,15 @@ def _launches(moe, blk, x):
     (128, 512, 512, 6, 2, 4),    # NB 128, ragged expert segments
     (48, 256, 2048, 8, 2, 8),    # 16 ffn tiles over 8 tapered splits (8 partial buffers)
 ])
-def test_fused_parity(moe, T, d, f, E, k, splits, uniform, chain):
-    """Tapered (default) and uniform w2 K splits, incl. more splits than ffn tiles allow."""
+def test_fused_parity(moe, T, d, f, E, k, splits, uniform, chain, half):
+    """Tapered (default) and uniform w2 K splits, incl. more splits than ffn tiles allow;
+    256-row w1/w3 tiles (fused_half 1) and 128-row ones (2: 64 w1 + 64 w3 rows, a/b paired
+    through shared memory)."""
     shape = synth.MoEShape(T=T, d=d, f=f, E=E, k=k)
     inp = synth.make_inputs(shape, 7100 + T + d + splits, device="cuda")
     host = to_host_inputs(inp)
-    blk = _block(moe, inp, k, T, {"fused": 2, "fused_splits": splits, "fused_uniform": uniform, "fused_chain": chain})
+    blk = _block(moe, inp, k, T, {"fused": 2, "fused_splits": splits, "fused_uniform": uniform, "fused_chain": chain,
+                                  "fused_half": half})
     run = GpuRun(blk, inp["x"])
     check_forward(run, host, k)
     assert _launches(moe, blk, inp["x"]) == 4  # router, permute, fused FFN, combine
@@ -70,16 +74,18 @@ def test_fused_parity(moe, T, d, f, E, k, splits, uniform, chain):
     blk.close()
 
 
+@pytest.mark.parametrize("half", [1, 2])
 @pytest.mark.parametrize("chain", [0, 1])
 @pytest.mark.parametrize("T,splits", [(64, 1), (64, 2), (64, 4), (100, 2), (13, 4)])
-def test_fused_bit_identical_to_two_kernels(moe, T, splits, chain):
+def test_fused_bit_identical_to_two_kernels(moe, T, splits, chain, half):
     """f = 1024 (8 ffn tiles), uniform splits (tuning fused_uniform): K splits 1 / 2 / 4 fall on
     ffn-tile boundaries in both paths, so each fp32 partial is the same sum in the same order
     and the outputs match bit for bit."""
     shape = synth.MoEShape(T=T, d=512, f=1024, E=8, k=2)
     inp = synth.make_inputs(shape, 7200 + T + splits, device="cuda")
     outs = []
-    for tu in ({"fused": 2, "fused_splits": splits, "fused_uniform": 1, "fused_chain": chain}, {"fused": 1}):
+    for tu in ({"fused": 2, "fused_splits": splits, "fused_uniform": 1, "fused_chain": chain, "fused_half": half},
+               {"fused": 1}):
         blk = _block(moe, inp, 2, T, tu, split_k=splits, flags=moe.MOE_FLAG_FORCE_SWAP)
         run = GpuRun(blk, inp["x"])
         outs.append((run.np("out_f32").copy(), run.out.clone()))
@@ -102,7 +108,7 @@ def test_fused_multi_token_tiles(moe, n):
     li = np.take_along_axis(l, idx.astype(np.int64), 1)
     p = np.exp(li - li.max(1, keepdims=True))
     gw = (p / p.sum(1, keepdims=True)).astype(np.float32)
-    blk = _block(moe, inp, 2, n, {"fused": 2, "swap_nb_cap": 32, "fused_splits": 4})
+    blk = _block(moe, inp, 2, n, {"fused": 2, "swap_nb_cap": 32, "fused_splits": 4, "fused_half": 2})
     run = GpuRun(blk, inp["x"], routed=(torch.from_numpy(idx).cuda(), torch.from_numpy(gw).cuda()))
     check_forward(run, host, 2, routed=True)
     assert run.np("expert_counts").tolist() == [n, n, 0, 0]
@@ -132,8 +138,9 @@ def test_fused_graph_replay(moe):
     blk.close()
 
 
+@pytest.mark.parametrize("half", [1, 2])
 @pytest.mark.parametrize("par,G", [("ep", 2), ("ep", 4), ("tp", 2), ("tp", 4)])
-def test_fused_group(moe, par, G):
+def test_fused_group(moe, par, G, half):
     """Fused FFN inside EP (receive-side expert segments) and TP (ffn slice) contexts."""
     from test_gpu_parity import _check_group_outputs, _run_group
     shape = synth.MoEShape(T=96, d=256, f=1024, E=8, k=2)
@@ -142,10 +149,10 @@ def test_fused_group(moe, par, G):
     if par == "ep":
         cuts = np.linspace(0, shape.T, G + 1).astype(int)
         shards = [inp["x"][cuts[r]:cuts[r + 1]] for r in range(G)]
-        res = _run_group(moe, inp, moe.MOE_PAR_EP, G, shards, max_tokens=shape.T, tuning={"fused": 2})
+        res = _run_group(moe, inp, moe.MOE_PAR_EP, G, shards, max_tokens=shape.T, tuning={"fused": 2, "fused_half": half})
         _check_group_outputs(host, 2, host["x"], [r[0] for r in res], [r[1] for r in res])
     else:
-        res = _run_group(moe, inp, moe.MOE_PAR_TP, G, [inp["x"]] * G, tuning={"fused": 2})
+        res = _run_group(moe, inp, moe.MOE_PAR_TP, G, [inp["x"]] * G, tuning={"fused": 2, "fused_half": half})
         for r in range(1, G):
             assert torch.equal(res[r][0].view(torch.int16), res[0][0].view(torch.int16))
         _check_group_outputs(host, 2, host["x"], [res[0][0]], [res[0][1]])
@@ -195,3 +202,31 @@ def test_fused_combine_bit_identical(moe, T, residual, chain):
         blk.close()
     assert np.array_equal(res[0][0].view(np.int32), res[1][0].view(np.int32))
     assert torch.equal(res[0][1].view(torch.int16), res[1][1].view(torch.int16))
+
+
+@pytest.mark.parametrize("par,G", [("ep", 8), ("tp", 8)])
+def test_fused_half_mixtral_ranks(moe, par, G):
+    """Mixtral-size EP8 / TP8 rank shapes with the fused FFN on 128-row w1/w3 tiles (the
+    per-rank shapes it is meant for) vs the two-kernel path: routing and outputs bit-identical
+    (uniform splits), and oracle parity on sampled tokens."""
+    w = synth.make_weights(4096, 14336, 8, seed=42, device="cuda")
+    x = synth.make_tokens(64, 4096, seed=9100 + G, device="cuda")
+    if par == "tp":
+        f_l = 14336 // G
+        ws = {"wg": w["wg"], "w1": w["w1"][:, :f_l].contiguous(), "w3": w["w3"][:, :f_l].contiguous(),
+              "w2": w["w2"][:, :, :f_l].contiguous()}
+        k, xs = 2, x
+    else:  # one expert, the rows it receives (top-1 over a single expert)
+        ws = {n: w[n][:1].contiguous() for n in ("wg", "w1", "w3", "w2")}
+        k, xs = 1, x[:21].contiguous()
+    inp = dict(ws, x=xs)
+    outs = []
+    S = 2 if par == "tp" else 4  # split boundaries on whole ffn tiles in both paths (f/G = 1792: 14 tiles)
+    for tu in ({"fused": 2, "fused_half": 2, "fused_uniform": 1, "fused_splits": S}, {"fused": 1}):
+        blk = _block(moe, inp, k, xs.shape[0], tu, split_k=S)
+        run = GpuRun(blk, xs)
+        if tu["fused"] == 2:
+            check_forward(run, to_host_inputs(inp), k, tokens=[0, 5, xs.shape[0] - 1])
+        outs.append(run.np("out_f32").copy())
+        blk.close()
+    assert np.array_equal(outs[0].view(np.int32), outs[1].view(np.int32))
