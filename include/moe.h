@@ -153,7 +153,9 @@ typedef struct moe_tuning {
     int32_t fused_half;     /* fused FFN w1/w3 tiles of 128 rows (64 w1 + 64 w3 rows, a/b paired
                                through shared memory): 0 auto (where the 256-row tiles do not
                                fill the SMs), 1 off, 2 on                                      */
-    int32_t reserved[2];    /* must be zero                                                  */
+    int32_t combine_vec;    /* combine kernel: 4-column groups per thread, 1 or 4 (0: 1 up to 256
+                               tokens -- more blocks for the latency-bound decode combine -- else 4) */
+    int32_t reserved[1];    /* must be zero                                                  */
 } moe_tuning;
 
 typedef struct {

@@ -638,7 +638,10 @@ struct CombineParams {
 // splits ascending, then r = w_0*s_0, r = fma(w_1, s_1, r), then + x.
 // grid = T * ceil(d/4096) blocks: each thread owns 4 float4 column groups of one token
 // (strided by 1024 columns), so 8 independent 16-byte loads per thread are in flight.
-constexpr int kCombineVec = 4;
+// VEC = column groups per thread: 4 for large batches; 1 for small ones (T <= 256), so a
+// 64-token decode spreads over 4x more blocks (the combine runs after the last GEMM tile:
+// its latency is on the step's critical path).
+template <int kCombineVec>
 __global__ void __launch_bounds__(256) moe_combine_kernel(const CombineParams p) {
     // 1-D grid (T may exceed the 65535 limit of gridDim.y): block b -> token b / nxb
     const int nxb = (p.d + 1024 * kCombineVec - 1) / (1024 * kCombineVec);

@@ -319,6 +319,7 @@ struct moe_ctx {
     int fused_chain_mode = 0;            // tuning.fused_chain: 1 on, 0 off (S partial buffers, default)
     int fused_half_mode = 0;             // tuning.fused_half: 0 auto, 1 off, 2 on (128-row w1/w3 tiles)
     bool fused_half_now = false;
+    int combine_vec = 0;                 // tuning.combine_vec: K5 column groups per thread (0 auto, 1, 4)
     // in-kernel combine of the fused FFN (single GPU, no TP / EP; tuning.fused_combine 1 = on):
     // set by forward_impl before run_gemms, taken by the fused launch (fcomb_done)
     struct FusedCombine {
@@ -646,7 +647,7 @@ moe_status validate_cfg(const moe_config* cfg, moe_ctx* c) {
     for (int i = 0; i < 2; ++i)
         if (cfg->reserved[i]) return fail(c, MOE_ERR_INVALID, "reserved fields must be zero");
     if (const moe_tuning* tu = cfg->tuning) {
-        for (int i = 0; i < 2; ++i)
+        for (int i = 0; i < 1; ++i)
             if (tu->reserved[i]) return fail(c, MOE_ERR_INVALID, "tuning.reserved fields must be zero");
         if (tu->g1_swap_rows < 0 || tu->g2_swap_rows < 0 || tu->g1_grid < 0 || tu->g2_grid < 0 ||
             tu->swap_nb_cap < 0 || tu->router_cc_max_T < 0 || tu->pair_order < 0)
@@ -656,6 +657,8 @@ moe_status validate_cfg(const moe_config* cfg, moe_ctx* c) {
         if (tu->fused < 0 || tu->fused > 2) return fail(c, MOE_ERR_INVALID, "tuning.fused must be 0, 1 or 2");
         if (tu->fused_splits < 0 || tu->fused_splits > 8)
             return fail(c, MOE_ERR_INVALID, "tuning.fused_splits must be in [0, 8]");
+        if (tu->combine_vec != 0 && tu->combine_vec != 1 && tu->combine_vec != 4)
+            return fail(c, MOE_ERR_INVALID, "tuning.combine_vec must be 0, 1 or 4");
         if (tu->fused_half < 0 || tu->fused_half > 2)
             return fail(c, MOE_ERR_INVALID, "tuning.fused_half must be 0, 1 or 2");
         if (tu->fused_chain < 0 || tu->fused_chain > 1)
@@ -1209,6 +1212,17 @@ moe_status run_gemms(moe_ctx* c, GemmPaths gp, int64_t rows_bound, int64_t rows_
     return MOE_OK;
 }
 
+// K5 launch: 1 column group per thread below 256 tokens (4x the blocks), 4 above
+// (tuning.combine_vec overrides: 1 or 4)
+moe_status launch_combine(moe_ctx* c, const CombineParams& cp, int T, cudaStream_t st) {
+    const int vec = c->combine_vec ? c->combine_vec : (T <= 256 ? 1 : 4);
+    if (vec == 1)
+        return launch(c, kSlotCombine, moe_combine_kernel<1>, dim3((unsigned)((c->d + 1023) / 1024 * (int64_t)T)),
+                      dim3(256), 0, st, cp);
+    return launch(c, kSlotCombine, moe_combine_kernel<4>, dim3((unsigned)((c->d + 4095) / 4096 * (int64_t)T)),
+                  dim3(256), 0, st, cp);
+}
+
 moe_status copy_aux(moe_ctx* c, const moe_aux* aux, int T, cudaStream_t st) {
     if (!aux || T <= 0) return MOE_OK;
     if (aux->topk_idx)
@@ -1607,6 +1621,7 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
         c->fused_combine_mode = tu->fused_combine;
         c->fused_chain_mode = tu->fused_chain;
         c->fused_half_mode = tu->fused_half;
+        c->combine_vec = tu->combine_vec;
     }
     if (cfg->flags & MOE_FLAG_GATHER) c->gather = true;
     // EP: a rank may receive up to every token of every peer (dropless, reading R6).
@@ -1796,7 +1811,8 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
             reinterpret_cast<const void*>(moe_router_mma_kernel<1>), reinterpret_cast<const void*>(moe_router_mma_kernel<8>),
             reinterpret_cast<const void*>(moe_router_kernel<8, 2>), reinterpret_cast<const void*>(moe_router_kernel<16, 2>),
             reinterpret_cast<const void*>(moe_router_kernel<32, 2>), reinterpret_cast<const void*>(moe_permute_kernel),
-            reinterpret_cast<const void*>(moe_combine_kernel), reinterpret_cast<const void*>(moe_ep_gather_kernel),
+            reinterpret_cast<const void*>(moe_combine_kernel<4>), reinterpret_cast<const void*>(moe_combine_kernel<1>),
+            reinterpret_cast<const void*>(moe_ep_gather_kernel),
             reinterpret_cast<const void*>(moe_tp_finish_kernel), reinterpret_cast<const void*>(moe_loopback_add_kernel),
 reinterpret_cast<const void*>(moe_ep_p2p_fill_kernel),
             reinterpret_cast<const void*>(moe_tp_p2p_finish_kernel), reinterpret_cast<const void*>(moe_tp_p2p_pull_kernel),
@@ -2240,7 +2256,7 @@ moe_status forward_impl(moe_ctx* c, const void* tokens, int32_t T, const void* r
         cp.x = residual ? static_cast<const __nv_bfloat16*>(tokens) : nullptr;
         cp.out = static_cast<__nv_bfloat16*>(out);
         cp.out_f32 = aux ? aux->out_f32 : nullptr;
-        return launch(c, kSlotCombine, moe_combine_kernel, dim3((unsigned)((c->d + 4095) / 4096 * (int64_t)T)), dim3(256), 0, st, cp);
+        return launch_combine(c, cp, T, st);
     }
     if (c->nvls) {
         // ---- TP over NVLink SHARP (MOE_FLAG_NVLS, nvls.cu): combine, switch-side fp32 sum,
@@ -2268,7 +2284,7 @@ moe_status forward_impl(moe_ctx* c, const void* tokens, int32_t T, const void* r
         cp.G = c->tp_world; cp.my_rank = c->tp_rank; cp.shard_max = c->tp_shard_max;
         cp.p2p_ticket = c->p2p_tickets + 2; cp.p2p_sig_off = c->so.sig + 8 * 2;
     }
-    if ((s = launch(c, kSlotCombine, moe_combine_kernel, dim3((unsigned)((c->d + 4095) / 4096 * (int64_t)T)), dim3(256), 0, st, cp)))
+    if ((s = launch_combine(c, cp, T, st)))
         return s;
     if (c->p2p) {
         const int G = c->tp_world, r = c->tp_rank;
@@ -2389,7 +2405,7 @@ moe_status forward_ep_p2p(moe_ctx* c, const void* tokens, int32_t T, const void*
     cp.T = T; cp.d = c->d; cp.k = c->k;
     cp.out = static_cast<__nv_bfloat16*>(out);
     cp.out_f32 = aux ? aux->out_f32 : nullptr;
-    return launch(c, kSlotCombine, moe_combine_kernel, dim3((unsigned)((c->d + 4095) / 4096 * (int64_t)T)), dim3(256), 0, st, cp);
+    return launch_combine(c, cp, T, st);
 }
 
 moe_status forward_ep(moe_ctx* c, const void* tokens, int32_t T, const void* router_w, void* out,
@@ -2501,7 +2517,7 @@ moe_status forward_ep(moe_ctx* c, const void* tokens, int32_t T, const void* rou
     cp.T = T; cp.d = c->d; cp.k = c->k;
     cp.out = static_cast<__nv_bfloat16*>(out);
     cp.out_f32 = aux ? aux->out_f32 : nullptr;
-    return launch(c, kSlotCombine, moe_combine_kernel, dim3((unsigned)((c->d + 4095) / 4096 * (int64_t)T)), dim3(256), 0, st, cp);
+    return launch_combine(c, cp, T, st);
 }
 
 }  // namespace
