@@ -27,7 +27,7 @@ def single(shape, flags, tuning=None):
     print("ok", shape, hex(flags), tuning, flush=True)
 
 
-def group(par, G, p2p):
+def group(par, G, p2p, tuning=None):
     shape = synth.MoEShape(T=48, d=256, f=512, E=4, k=2)
     inp = synth.make_inputs(shape, 6, device="cuda")
     flags = moe.MOE_FLAG_P2P if p2p else 0
@@ -35,7 +35,7 @@ def group(par, G, p2p):
     comms = [None] * G if p2p else [moe.moe_loopback_comm_rank(grp, r) for r in range(G)]
     pm = moe.MOE_PAR_EP if par == "ep" else moe.MOE_PAR_TP
     blocks = [moe.MoEBlock(inp["wg"], inp["w1"], inp["w3"], inp["w2"], max_tokens=48, par=pm, world_size=G, rank=r,
-                           nccl_comm=comms[r], flags=flags) for r in range(G)]
+                           nccl_comm=comms[r], flags=flags, tuning=tuning) for r in range(G)]
     if p2p:
         hs = [b.p2p_handle() for b in blocks]
         for b in blocks:
@@ -61,7 +61,7 @@ def group(par, G, p2p):
         for c in comms:
             moe.moe_loopback_comm_destroy(c)
         moe.moe_loopback_comm_destroy(grp)
-    print("ok", par, G, "p2p" if p2p else "loopback", flush=True)
+    print("ok", par, G, "p2p" if p2p else "loopback", tuning, flush=True)
 
 
 if __name__ == "__main__":
@@ -78,6 +78,14 @@ if __name__ == "__main__":
     single(synth.MoEShape(T=600, d=256, f=512, E=8, k=2), 0x2, {"swap_pair": 1})  # same on single-CTA swap tiles
     single(synth.MoEShape(T=300, d=256, f=512, E=8, k=2), 0x2)   # CTA-pair swap, token tile 128
     single(synth.MoEShape(T=1000, d=320, f=512, E=8, k=2), 0x2, {"swap_pair": 2})  # pair tile 256 + 2nd tiles, padded d
+    # fused decode FFN (ffn_fused.cuh): cross-CTA h readiness / tile claims / counter resets
+    fz = synth.MoEShape(T=64, d=1024, f=2560, E=8, k=2)
+    single(fz, 0, {"fused": 2})                                   # tapered splits, 256-row w1/w3 tiles
+    single(fz, 0, {"fused": 2, "fused_half": 2})                  # 128-row w1/w3 tiles (smem a/b exchange)
+    single(fz, 0, {"fused": 2, "fused_chain": 1, "fused_splits": 8})  # split chaining
+    single(fz, moe.MOE_FLAG_RESIDUAL, {"fused": 2, "fused_combine": 1})  # in-kernel combine
+    single(synth.MoEShape(T=100, d=512, f=1024, E=4, k=2), 0, {"fused": 2, "swap_nb_cap": 32})  # several token tiles
     for par in ("ep", "tp"):
         for p2p in (False, True):
             group(par, 2, p2p)
+    group("tp", 2, False, {"fused": 2})
