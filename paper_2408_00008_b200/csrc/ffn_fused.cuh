@@ -81,6 +81,11 @@ struct FusedParams {
     // the combine kernel adding S partial buffers, and the combine then reads one partial.
     // chain[i] = splits stored so far for output tile i (the tile's index within its split).
     int32_t* chain;
+    // FP8 weights (FP8 instantiation; GemmParams h_sf / plane_rows / sf_nb as the two-kernel
+    // FP8 path): per-row weight scales and per-token scales of the two-term E4M3 tokens
+    const float* w13_scale;  // [E][2 f] (w1 rows then w3 rows of each 128-row block pair)
+    const float* w2_scale;   // [E][d]
+    const float* tok_scale;  // [rows] 2^-s of each permuted row
 };
 
 constexpr int kFusedTileRing = 8;  // claimed-tile hand-off ring depth
@@ -91,17 +96,28 @@ constexpr int kFusedEpiBar = 1;    // named barrier of the 4 epilogue warps
 // spreads over twice as many CTAs; a stage then carries two K blocks of such a tile (32 KB
 // of weights + 2 x NB token rows), and the epilogue pairs a (TMEM lanes 0-63) with b (lanes
 // 64-127) through a shared-memory exchange buffer. w2 tiles are the same in both variants.
-template <int NB, bool HALF = false>
+// FP8 (E4M3 weights, round 3): the two-kernel FP8 path's tiles (moe_gemm_fp8x_kernel) in the
+// fused schedule. A stage = one 128-byte K chunk: 256 weight rows (G1: a W13 tile; G2: W2 tiles
+// 2m and 2m+1) + the hi and lo E4M3 terms of the NB token / h rows (stacked, N = 2 NB) + for G2
+// the tile's UE8M0 B-scale block; G1 runs kind::f8f6f4 MMAs, G2 the block-scaled
+// kind::mxf8f6f4 ones (B scales copied into TMEM per stage, A scales a constant 2^0 atom).
+// Accumulator stage = 4 NB columns (two M=128 MMAs x hi/lo halves); NB = 32 only.
+template <int NB, bool HALF = false, bool FP8 = false>
 struct FusedCfg {
-    static constexpr int kABytes = 256 * 128;       // 256 weight rows x 64 bf16 (HALF G1: 2 x 128 rows x 64)
-    static constexpr int kBBytes = (HALF ? 2 : 1) * NB * 128;  // token rows x 64 bf16 (x 2 K blocks)
-    static constexpr int kStageBytes = kABytes + kBBytes;
+    static constexpr int kABytes = 256 * 128;       // 256 weight rows x 64 bf16 (HALF G1: 2 x 128 rows x 64; FP8: x 128 E4M3)
+    static constexpr int kBBytes = FP8 ? 2 * NB * 128 : (HALF ? 2 : 1) * NB * 128;  // token rows x 128 B (x 2 K blocks / terms)
+    static constexpr int kSFBytes = FP8 ? 512 : 0;  // FP8 G2: the tile's B scale block per K chunk
+    static constexpr int kStageBytes = kABytes + kBBytes + kSFBytes;
     static constexpr int kXPitch = NB + 1;          // exchange row pitch in floats (bank-conflict free)
     static constexpr int kXBytes = HALF ? 64 * kXPitch * 4 : 0;
-    static constexpr int kStagesRaw = (kSmemBudget - 2048 - kXBytes) / kStageBytes;
+    static constexpr int kSfaBytes = FP8 ? 512 : 0;  // FP8: the constant A scale atom (UE8M0 127)
+    static constexpr int kStagesRaw = (kSmemBudget - 2048 - kXBytes - kSfaBytes) / kStageBytes;
     static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
-    static constexpr int kSmemBytes = kStages * kStageBytes + kXBytes + 2048;
+    static constexpr int kSmemBytes = kStages * kStageBytes + kXBytes + kSfaBytes + 2048;
+    static constexpr int kAccStride = FP8 ? 4 * NB : 256;  // TMEM columns per accumulator stage
+    static constexpr uint32_t kSfaCol = 480, kSfbCol = 488;  // FP8 scale columns in TMEM
     static_assert(NB >= 16 && NB <= 128 && NB % 16 == 0, "fused tile: a/b accumulators of <= 128 columns");
+    static_assert(!FP8 || (!HALF && NB == 32), "FP8 fused tiles: 32-row token tiles, 256-row w1/w3 tiles");
     static_assert(kStages >= 3, "pipeline too shallow");
 };
 
@@ -125,7 +141,7 @@ __device__ __forceinline__ int fused_nt(int rows, int NB) { return rows > 0 ? (r
 //                    [split_j[s], split_j[s+1]) -- by default tapered (the host gives the
 //                    first splits the most K and the last the least), so the stream ends on
 //                    the shortest tiles and the CTAs' exits bunch up.
-template <int NB, bool HALF>
+template <int NB, bool HALF, bool FP8>
 __device__ __forceinline__ void fused_decode(int t, const FusedParams& p, const int32_t* s_counts,
                                              const int32_t* s_offsets, int total1, int per_split, FusedTile& ti) {
     const int wt = p.g.f / 128 * (HALF ? 2 : 1);  // w1/w3 tiles per expert and token tile
@@ -155,12 +171,13 @@ __device__ __forceinline__ void fused_decode(int t, const FusedParams& p, const 
         ti.hf = ti.m & 1;
         ti.m >>= 1;
     }
+    // K units: 64 bf16 (K block) or 128 E4M3 (FP8 K chunk = one ffn tile of h)
     if (ti.g1) {
         ti.kb0 = 0;
-        ti.nkb = p.g.d / 64;
+        ti.nkb = p.g.d / (FP8 ? 128 : 64);
     } else {
-        ti.kb0 = 2 * p.split_j[ti.s];
-        ti.nkb = 2 * (p.split_j[ti.s + 1] - p.split_j[ti.s]);
+        ti.kb0 = (FP8 ? 1 : 2) * p.split_j[ti.s];
+        ti.nkb = (FP8 ? 1 : 2) * (p.split_j[ti.s + 1] - p.split_j[ti.s]);
     }
     ti.b_row = s_offsets[e] + n_idx * NB;
     const int rem = ti.rows - n_idx * NB;
@@ -180,20 +197,22 @@ __device__ __forceinline__ void fence_proxy_async_global() {
 // tmW13: W13 tiled map (box 64 x 256 rows; HALF: 64 x 64 rows); tmX: permuted tokens (box
 // 64 x NB); tmW2: W2 tiled map with 2-tile boxes (64 x 128 rows x 1 x 2 = 256 rows); tmH: h
 // (box 64 x NB)
-template <int NB, bool HALF>
+template <int NB, bool HALF, bool FP8 = false>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     moe_ffn_fused_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmW13,
                          const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW2,
                          const __grid_constant__ CUtensorMap tmH) {
-    using C = FusedCfg<NB, HALF>;
+    using C = FusedCfg<NB, HALF, FP8>;
     constexpr int S = C::kStages;
     constexpr int R = kFusedTileRing;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* smem_a = smem;
     uint8_t* smem_b = smem + S * C::kABytes;
+    uint8_t* smem_sf = smem_b + S * C::kBBytes;                            // FP8: per-stage B scale blocks
     float* smem_x = reinterpret_cast<float*>(smem + S * C::kStageBytes);  // HALF: [64][kXPitch] b values
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * C::kStageBytes + C::kXBytes);
+    uint8_t* smem_sfa = smem + S * C::kStageBytes + C::kXBytes;             // FP8: A scale atom
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * C::kStageBytes + C::kXBytes + C::kSfaBytes);
     uint64_t* full = bars;
     uint64_t* empty = bars + S;
     uint64_t* tmem_full = bars + 2 * S;
@@ -242,6 +261,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     if (warp == 1) {
         ptx::tmem_alloc(tmem_base_slot, 512);
         ptx::tmem_relinquish();
+        if (FP8) {  // A scales of the block-scaled w2 MMAs: UE8M0 127 = 2^0 for every row and K block
+            reinterpret_cast<uint4*>(smem_sfa)[lane] = make_uint4(0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu);
+            ptx::fence_proxy_async();  // generic-proxy stores visible to tcgen05.cp
+        }
     }
     // Before the routing is known (PDL: the router / permute may still run): prefetch into
     // L2 the first K blocks of the w1/w3 tile this CTA most likely claims first, assuming
@@ -250,7 +273,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     // epilogue lane (idle until the first accumulator is ready): a CTA that starts late can
     // stall several us issuing prefetches into a busy memory system, and the producer must
     // not wait for that (timeline r03: post-wait stamps up to 9 us late when lane 0 issued).
-    if (p.g.spec_l2 > 0 && threadIdx.x == 160) {
+    if (!FP8 && p.g.spec_l2 > 0 && threadIdx.x == 160) {
         const int wt = p.g.f / 128 * (HALF ? 2 : 1);
         if ((int)blockIdx.x < p.g.E * wt) {
             const int e = blockIdx.x / wt, m = (blockIdx.x % wt) / (HALF ? 2 : 1), hf = HALF ? blockIdx.x % 2 : 0;
@@ -343,13 +366,37 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 if (t >= total_all) break;
                 if (t >= total) continue;  // combine task: the epilogue warps only
                 FusedTile ti;
-                fused_decode<NB, HALF>(t, p, s_counts, s_offsets, total1, per_split, ti);
+                fused_decode<NB, HALF, FP8>(t, p, s_counts, s_offsets, total1, per_split, ti);
                 if (!ti.g1 && !all_ready && ld_relaxed_gpu(&p.sched[2]) >= total1) {
                     fence_acq_rel_gpu();
                     fence_proxy_async_global();
                     all_ready = true;
                 }
-                if (HALF && ti.g1) {
+                if (FP8 && (ti.g1 || all_ready)) {
+                    // one 128-byte K chunk per stage: 256 weight rows, hi / lo token (h) rows, (G2) scales
+                    const int d128 = p.g.d / 128;
+                    for (int kb = 0; kb < ti.nkb; ++kb) {
+                        const int kq = ti.kb0 + kb;
+                        ptx::mbar_wait(&empty[stage], phase ^ 1);
+                        ptx::mbar_arrive_expect_tx(&full[stage], ti.g1 ? C::kABytes + C::kBBytes : C::kStageBytes);
+                        uint8_t* sa = smem_a + stage * C::kABytes;
+                        uint8_t* sb = smem_b + stage * C::kBBytes;
+                        if (ti.g1) {
+                            ptx::tma_load_4d(&tmW13, &full[stage], sa, 0, 0, kq, ti.m + ti.e * wt, w_hint);
+                            ptx::tma_load_3d(&tmX, &full[stage], sb, kq * 128, ti.b_row, 0, ptx::kEvictLast);
+                            ptx::tma_load_3d(&tmX, &full[stage], sb + NB * 128, kq * 128, ti.b_row, 1, ptx::kEvictLast);
+                        } else {
+                            ptx::tma_load_4d(&tmW2, &full[stage], sa, 0, 0, kq, 2 * ti.m + ti.e * d128, w_hint);
+                            ptx::tma_load_4d(&tmW2, &full[stage], sa + 16384, 0, 0, kq, 2 * ti.m + 1 + ti.e * d128, w_hint);
+                            ptx::tma_load_3d(&tmH, &full[stage], sb, kq * 128, ti.b_row, 0, ptx::kEvictLast);
+                            ptx::tma_load_3d(&tmH, &full[stage], sb + NB * 128, kq * 128, ti.b_row, 1, ptx::kEvictLast);
+                            ptx::bulk_load(smem_sf + stage * C::kSFBytes,
+                                           p.g.h_sf + ((int64_t)(ti.b_row / NB) * wt + kq) * C::kSFBytes, C::kSFBytes,
+                                           &full[stage]);
+                        }
+                        if (++stage == SR) { stage = 0; phase ^= 1; }
+                    }
+                } else if (HALF && ti.g1) {
                     // two K blocks per stage: [kb: 64 w1 rows | 64 w3 rows][kb+1: ...] + 2 x NB tokens
                     for (int kb = 0; kb < ti.nkb; kb += 2) {
                         ptx::mbar_wait(&empty[stage], phase ^ 1);
@@ -390,8 +437,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                     // kb0 + q of expert e finished by all of its token tiles; weight loads run up to
                     // the ring depth ahead. ok = consecutive finished K blocks from kb0 (relaxed
                     // reads, then fence.acq_rel = acquire, then the proxy fence for the TMA reads).
-                    const int32_t* rdy = p.ready + ti.e * wq + ti.kb0;
-                    const int nj = ti.nkb;
+                    constexpr int fpq = FP8 ? 2 : 1;  // 64-column readiness flags per K unit
+                    const int32_t* rdy = p.ready + ti.e * wq + ti.kb0 * fpq;
+                    const int nj = ti.nkb * fpq;
                     int ok = 0;
                     auto refresh = [&]() {
                         const int ok0 = ok;
@@ -415,16 +463,27 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                     int bq = 0;  // K blocks whose h load is issued
                     auto issue_b = [&](int q) {
                         const int sq = (st0 + q) % SR;
-                        ptx::tma_load_2d(&tmH, &full[sq], smem_b + sq * C::kBBytes, (ti.kb0 + q) * kBK, ti.b_row,
-                                         ptx::kEvictLast);
+                        if (FP8) {
+                            const int kq = ti.kb0 + q;
+                            uint8_t* sb = smem_b + sq * C::kBBytes;
+                            ptx::tma_load_3d(&tmH, &full[sq], sb, kq * 128, ti.b_row, 0, ptx::kEvictLast);
+                            ptx::tma_load_3d(&tmH, &full[sq], sb + NB * 128, kq * 128, ti.b_row, 1, ptx::kEvictLast);
+                            ptx::bulk_load(smem_sf + sq * C::kSFBytes,
+                                           p.g.h_sf + ((int64_t)(ti.b_row / NB) * wt + kq) * C::kSFBytes, C::kSFBytes,
+                                           &full[sq]);
+                        } else {
+                            ptx::tma_load_2d(&tmH, &full[sq], smem_b + sq * C::kBBytes, (ti.kb0 + q) * kBK, ti.b_row,
+                                             ptx::kEvictLast);
+                        }
                     };
+                    auto unit_ok = [&](int q) { return (q + 1) * fpq <= ok; };  // K unit q's h is ready
                     auto wait_ready = [&](int q) {
 #if MOE_TIMELINE
-                        const unsigned long long w0 = q >= ok ? ptx::tl_now() : 0;
+                        const unsigned long long w0 = !unit_ok(q) ? ptx::tl_now() : 0;
 #endif
-                        while (q >= ok) {
+                        while (!unit_ok(q)) {
                             refresh();
-                            if (q >= ok) __nanosleep(64);
+                            if (!unit_ok(q)) __nanosleep(64);
                         }
 #if MOE_TIMELINE
                         if (w0) tl_stall += ptx::tl_now() - w0;
@@ -438,15 +497,21 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                             issue_b(bq++);
                         }
                         ptx::mbar_wait(&empty[stage], phase ^ 1);
-                        ptx::mbar_arrive_expect_tx(&full[stage], C::kABytes + NB * 128);
+                        ptx::mbar_arrive_expect_tx(&full[stage], FP8 ? C::kStageBytes : C::kABytes + NB * 128);
                         uint8_t* sa = smem_a + stage * C::kABytes;
                         const int kq = ti.kb0 + q;
-                        ptx::tma_load_4d(&tmW2, &full[stage], sa, 0, 0, kq, 2 * ti.m + ti.e * p.w2_nt, w_hint);
+                        if (FP8) {
+                            const int d128 = p.g.d / 128;
+                            ptx::tma_load_4d(&tmW2, &full[stage], sa, 0, 0, kq, 2 * ti.m + ti.e * d128, w_hint);
+                            ptx::tma_load_4d(&tmW2, &full[stage], sa + 16384, 0, 0, kq, 2 * ti.m + 1 + ti.e * d128, w_hint);
+                        } else {
+                            ptx::tma_load_4d(&tmW2, &full[stage], sa, 0, 0, kq, 2 * ti.m + ti.e * p.w2_nt, w_hint);
+                        }
                         // weights of the first stages go out before the first readiness check
                         if (q == SR - 1 || q == ti.nkb - 1 || (q >= SR && (q & 3) == 3)) {
-                            if (bq >= ok) refresh();
+                            if (!unit_ok(bq)) refresh();
                         }
-                        while (bq <= q && bq < ok) issue_b(bq++);
+                        while (bq <= q && unit_ok(bq)) issue_b(bq++);
                         if (++stage == SR) { stage = 0; phase ^= 1; }
                     }
                     while (bq < ti.nkb) {
@@ -465,6 +530,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             uint32_t acc_phase = 0;
             int ts = 0;
             uint32_t tph = 0;
+            const uint32_t sfa = tmem_base + C::kSfaCol, sfb = tmem_base + C::kSfbCol;
+            if (FP8) ptx::tmem_cp_32x128b_x4(sfa, ptx::make_smem_desc_rows16(ptx::smem_u32(smem_sfa)));
             while (true) {
                 ptx::mbar_wait(&tile_full[ts], tph);
                 const int t = s_tile[ts];
@@ -473,10 +540,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 if (t >= total_all) break;
                 if (t >= total) continue;
                 FusedTile ti;
-                fused_decode<NB, HALF>(t, p, s_counts, s_offsets, total1, per_split, ti);
+                fused_decode<NB, HALF, FP8>(t, p, s_counts, s_offsets, total1, per_split, ti);
                 const uint32_t n_mma = (uint32_t)((ti.n_valid + 15) / 16 * 16);
                 const uint32_t idesc = ptx::make_idesc_bf16(128, n_mma);
-                const uint32_t d_tmem = tmem_base + acc * 256;
+                const uint32_t d_tmem = tmem_base + acc * C::kAccStride;
                 ptx::mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
                 ptx::tc_fence_after();
                 const bool half_g1 = HALF && ti.g1;
@@ -485,7 +552,30 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                     ptx::tc_fence_after();
                     const uint32_t sa = ptx::smem_u32(smem_a + stage * C::kABytes);
                     const uint32_t sb = ptx::smem_u32(smem_b + stage * C::kBBytes);
-                    if (half_g1) {
+                    if (FP8) {
+                        // hi and lo terms stacked: N = 2 NB; 32 bytes of K per MMA (+2 in the descriptor)
+                        constexpr uint32_t N2 = 2 * NB;
+                        const uint64_t a1 = ptx::make_smem_desc_sw128(sa);
+                        const uint64_t b0 = ptx::make_smem_desc_sw128(sb);
+                        if (!ti.g1) {  // this stage's B scales -> TMEM (in order before the MMAs below)
+                            ptx::tmem_cp_32x128b_x4(sfb, ptx::make_smem_desc_rows16(ptx::smem_u32(smem_sf + stage * C::kSFBytes)));
+                        }
+#pragma unroll
+                        for (int kk = 0; kk < 4; ++kk) {
+                            const uint32_t acc_in = (kb | kk) ? 1u : 0u;
+                            if (ti.g1) {
+                                const uint32_t id8 = (1u << 4) | ((N2 >> 3) << 17) | ((128u >> 4) << 24);  // D f32, E4M3
+                                ptx::mma_e4m3(d_tmem, a1 + 2 * kk, b0 + 2 * kk, id8, acc_in);
+                                ptx::mma_e4m3(d_tmem + N2, a1 + (16384 >> 4) + 2 * kk, b0 + 2 * kk, id8, acc_in);
+                            } else {
+                                const uint32_t sel = static_cast<uint32_t>(kk) << 30;  // K block kk of the chunk
+                                const uint32_t idmx = ptx::make_idesc_mx_e4m3(128, N2, kk, kk);
+                                ptx::mma_mx_e4m3(d_tmem, a1 + 2 * kk, b0 + 2 * kk, idmx, acc_in, sfa | sel, sfb | sel);
+                                ptx::mma_mx_e4m3(d_tmem + N2, a1 + (16384 >> 4) + 2 * kk, b0 + 2 * kk, idmx, acc_in,
+                                                 sfa | sel, sfb | sel);
+                            }
+                        }
+                    } else if (half_g1) {
                         // A = [K block kb: 64 w1 + 64 w3 rows][K block kb+1], one M = 128 MMA per k16:
                         // a lands in TMEM lanes 0-63, b in lanes 64-127
 #pragma unroll
@@ -585,12 +675,88 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 continue;
             }
             FusedTile ti;
-            fused_decode<NB, HALF>(t, p, s_counts, s_offsets, total1, per_split, ti);
+            fused_decode<NB, HALF, FP8>(t, p, s_counts, s_offsets, total1, per_split, ti);
             ptx::mbar_wait(&tmem_full[acc], acc_phase);
             ptx::tc_fence_after();
-            const uint32_t tbase = tmem_base + acc * 256 + (static_cast<uint32_t>(q * 32) << 16);
+            const uint32_t tbase = tmem_base + acc * C::kAccStride + (static_cast<uint32_t>(q * 32) << 16);
             const int nchunks = (ti.n_valid + 15) / 16;
-            if (HALF && ti.g1) {
+            if (FP8 && ti.g1) {
+                // columns [0, NB): w1 hi term, [NB, 2 NB): w1 lo, then the w3 accumulator (moe_gemm_fp8x_kernel's
+                // epilogue): dequantise, SwiGLU, h -> two E4M3 planes + UE8M0 scales per 32 ffn columns
+                // token scales of the tile's NB = 32 rows: one per lane, broadcast with shuffles (no
+                // dependent global load per token inside the warp-synchronous loop below)
+                const float ts_lane = lane < ti.n_valid ? p.tok_scale[ti.b_row + lane] : 0.f;
+                const float* sc = p.w13_scale + (int64_t)ti.e * 2 * p.g.f + ti.m * 256;
+                const float s1v = sc[r], s3v = sc[128 + r];
+                const int64_t plane = p.g.plane_rows * p.g.f;
+                uint8_t* hp = static_cast<uint8_t*>(p.g.out) + static_cast<int64_t>(ti.b_row) * p.g.f + ti.m * 128 + r;
+                constexpr int snb = NB;
+                constexpr int sfbytes = 512;
+#pragma unroll 1
+                for (int cc = 0; cc < nchunks; ++cc) {
+                    uint32_t a0[16], a1[16], b0[16], b1[16];
+                    ptx::tmem_ld16(tbase + cc * 16, a0);
+                    ptx::tmem_ld16(tbase + NB + cc * 16, a1);
+                    ptx::tmem_ld16(tbase + 2 * NB + cc * 16, b0);
+                    ptx::tmem_ld16(tbase + 3 * NB + cc * 16, b1);
+                    ptx::tmem_wait_ld();
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        const int n = cc * 16 + i;
+                        const float tsn = __shfl_sync(0xffffffffu, ts_lane, n & 31);
+                        if (n < ti.n_valid) {  // warp-uniform
+                            const float av = __uint_as_float(a0[i]) + __uint_as_float(a1[i]);
+                            const float bv = __uint_as_float(b0[i]) + __uint_as_float(b1[i]);
+                            const float hv = silu_f32(av * (s1v * tsn)) * (bv * (s3v * tsn));
+                            const uint32_t mbits = __reduce_max_sync(0xffffffffu, __float_as_uint(hv) & 0x7FFFFFFFu);
+                            const float mx = __uint_as_float(mbits);
+                            int u = 0;
+                            if (mx > 0.f) {
+                                const float ratio = 448.f / mx;
+                                u = isinf(ratio) ? 120 : ((__float_as_int(ratio) >> 23) & 0xFF) - 127;
+                                u = max(-120, min(120, u));
+                            }
+                            const float v = hv * __int_as_float((u + 127) << 23);
+                            const uint8_t hi = f32_to_e4m3(v);
+                            const uint8_t lo = f32_to_e4m3((v - e4m3_to_f32(hi)) * 16.f);
+                            hp[static_cast<int64_t>(n) * p.g.f] = hi;
+                            hp[static_cast<int64_t>(n) * p.g.f + plane] = lo;
+                            if (lane < 2) {
+                                const int64_t row = ti.b_row + n;
+                                const int v_row = static_cast<int>(row % snb) + lane * snb;
+                                const int64_t o = ((row / snb) * (p.g.f / 128) + ti.m) * sfbytes + 512 * (v_row / 128) +
+                                                  16 * (v_row % 32) + 4 * ((v_row % 128) / 32) + q;
+                                p.g.h_sf[o] = static_cast<uint8_t>((lane ? 123 : 127) - u);
+                            }
+                        }
+                    }
+                }
+                fence_proxy_async_global();  // h planes + scales -> visible to the w2 tiles' TMA / bulk loads
+            } else if (FP8) {
+                // rows 256 m + r (first MMA: columns [0, 2 NB)) and 256 m + 128 + r ([2 NB, 4 NB)); hi + lo
+                const int drow = ti.m * 256 + r;
+                const float s2a = p.w2_scale[(int64_t)ti.e * p.g.d + drow];
+                const float s2b = p.w2_scale[(int64_t)ti.e * p.g.d + drow + 128];
+                float* y = p.y + p.y_split_stride * ti.s + static_cast<int64_t>(ti.b_row) * p.g.d + drow;
+#pragma unroll 1
+                for (int cc = 0; cc < nchunks; ++cc) {
+                    uint32_t v0[16], v1[16], w0[16], w1[16];
+                    ptx::tmem_ld16(tbase + cc * 16, v0);
+                    ptx::tmem_ld16(tbase + NB + cc * 16, v1);
+                    ptx::tmem_ld16(tbase + 2 * NB + cc * 16, w0);
+                    ptx::tmem_ld16(tbase + 3 * NB + cc * 16, w1);
+                    ptx::tmem_wait_ld();
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        const int n = cc * 16 + i;
+                        if (n < ti.n_valid) {
+                            y[static_cast<int64_t>(n) * p.g.d] = (__uint_as_float(v0[i]) + __uint_as_float(v1[i])) * s2a;
+                            y[static_cast<int64_t>(n) * p.g.d + 128] =
+                                (__uint_as_float(w0[i]) + __uint_as_float(w1[i])) * s2b;
+                        }
+                    }
+                }
+            } else if (HALF && ti.g1) {
                 // a of h column j (64 per tile) in TMEM lane j (warps q = 0, 1), b in lane 64 + j
                 // (warps q = 2, 3): b goes through shared memory, warps 0 / 1 finish h
                 if (q >= 2) {

@@ -496,6 +496,9 @@ moe_status set_fused_attr(moe_ctx* c) {
                                      FusedCfg<NB, false>::kSmemBytes));
     CUDA_TRY(c, cudaFuncSetAttribute(moe_ffn_fused_kernel<NB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      FusedCfg<NB, true>::kSmemBytes));
+    if constexpr (NB == 32)
+        CUDA_TRY(c, cudaFuncSetAttribute(moe_ffn_fused_kernel<32, false, true>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, FusedCfg<32, false, true>::kSmemBytes));
     return MOE_OK;
 }
 
@@ -988,15 +991,21 @@ moe_status run_gemms(moe_ctx* c, GemmPaths gp, int64_t rows_bound, int64_t rows_
     // allows -- bf16, one token tile size <= 128 rows for both GEMMs, d a multiple of 256.
     c->fused_now = false;
     {
-        const bool shape_ok = gp.swap1 && gp.swap2 && !c->fp8 && !c->gather_now && nb1 == nb2 && nb1 <= 128 &&
-                              c->d % 256 == 0 && c->f_local % 128 == 0 && c->E_local <= 32;
+        // FP8 weights: the 32-row token tile of the FP8 decode only (moe_gemm_fp8x_kernel's tiles)
+        const bool shape_ok = gp.swap1 && gp.swap2 && !c->gather_now && nb1 == nb2 && nb1 <= 128 &&
+                              (!c->fp8 || nb1 == 32) && c->d % 256 == 0 && c->f_local % 128 == 0 &&
+                              c->E_local <= 32;
         // auto: where the w1/w3 tiles give >= 3 waves over the SMs (single GPU, EP2 / TP2 ranks)
         // and the token tile is <= 64 rows (64-token decode: 0.4055-0.4064 vs 0.4094-0.4102 ms,
         // 3 of 3 interleaved rounds; EP4 / TP4 / EP8 / TP8 ranks measured slower fused:
         // profiles/r03/fused_ab.md)
         const int64_t U1 = (int64_t)c->E_local * (c->f_local / 128);
         const bool want = c->fused_mode == 2 ||
-                          (c->fused_mode == 0 && !sp1 && !sp2 && nb1 <= 64 && U1 >= 3 * (int64_t)c->num_sms);
+                          (c->fused_mode == 0 && !c->fp8 && !sp1 && !sp2 && nb1 <= 64 && U1 >= 3 * (int64_t)c->num_sms);
+        // FP8 weights: parity-tested (tuning fused=2) but slower than the two FP8 kernels:
+        // 0.2591-0.2657 vs 0.2291-0.2316 ms at the 64-token decode, ncu 254.9 us vs 152.0 + 80.7 us
+        // (DRAM 68.7 % vs 76 / 73 % of peak); its w1/w3 phase streams ~25 % slower than
+        // moe_gemm_fp8x_kernel's (profiles/r03/fused_ab.md) -- not understood yet
         if (shape_ok && want) {
             const int64_t rows_needed = round_up(rows_total + (int64_t)c->E_local * (kSegAlign - 1), kSegAlign);
             const int wt = c->f_local / 128;
@@ -1010,7 +1019,16 @@ moe_status run_gemms(moe_ctx* c, GemmPaths gp, int64_t rows_bound, int64_t rows_
             fp.g.hint_a = c->swap_w_hint;
             fp.g.w_tr = 256;
             fp.g.w_nt = c->w13_nt;
-            fp.g.spec_l2 = c->spec_now ? c->spec_l2 : 0;
+            fp.g.spec_l2 = c->spec_now && !c->fp8 ? c->spec_l2 : 0;
+            if (c->fp8) {  // two E4M3 h planes + UE8M0 block scales (the FP8 w2 tiles' B operand)
+                fp.g.out = c->h8;
+                fp.g.h_sf = c->h_sf;
+                fp.g.plane_rows = c->cap;
+                fp.g.sf_nb = 32;
+                fp.w13_scale = static_cast<const float*>(c->cur_w.w13_scale);
+                fp.w2_scale = static_cast<const float*>(c->cur_w.w2_scale);
+                fp.tok_scale = c->tok_scale;
+            }
             fp.y = c->y;
             fp.y_split_stride = c->split_stride;
             fp.splits = S;
@@ -1026,7 +1044,7 @@ moe_status run_gemms(moe_ctx* c, GemmPaths gp, int64_t rows_bound, int64_t rows_
             {
                 int64_t nt_sum = c->E_local;
                 nt_sum += (rows_total + nb1 - 1) / nb1;
-                if (c->fused_chain_mode == 1 && S > 1 && nt_sum * (c->d / 256) <= c->fused_chain_n)
+                if (c->fused_chain_mode == 1 && !c->fp8 && S > 1 && nt_sum * (c->d / 256) <= c->fused_chain_n)
                     fp.chain = c->fused_chain;
             }
             const bool comb = c->fcomb.on && c->d / 256 <= grid;  // every combine task claimed by some CTA
@@ -1061,14 +1079,18 @@ moe_status run_gemms(moe_ctx* c, GemmPaths gp, int64_t rows_bound, int64_t rows_
             c->g1_grid_now = c->g2_grid_now = grid;
             const int i = nb1 == 32 ? 0 : nb1 == 64 ? 1 : 2;
             // 128-row w1/w3 tiles where the 256-row ones do not fill the SMs (tuning.fused_half)
-            const bool half = c->fused_half_mode == 2 || (c->fused_half_mode == 0 && U1 < (int64_t)c->num_sms);
+            const bool half = !c->fp8 && (c->fused_half_mode == 2 || (c->fused_half_mode == 0 && U1 < (int64_t)c->num_sms));
             c->fused_half_now = half;
             const CUtensorMap& tw = half ? c->tm_w13_h : c->tm_w13;
             auto go = [&](auto kern, size_t smem) {
                 return launch(c, kSlotGemm1, kern, dim3(grid), dim3(kGemmThreads), smem, st, fp, tw, c->tm_x_swap[i],
                               c->tm_w2_tiled, c->tm_h_swap[i]);
             };
-            if (nb1 == 32)
+            if (c->fp8)
+                s = launch(c, kSlotGemm1, moe_ffn_fused_kernel<32, false, true>, dim3(grid), dim3(kGemmThreads),
+                           (size_t)FusedCfg<32, false, true>::kSmemBytes, st, fp, c->tm_w13, c->tm_x8[0], c->tm_w2_swap,
+                           c->tm_h8[0]);
+            else if (nb1 == 32)
                 s = half ? go(moe_ffn_fused_kernel<32, true>, (size_t)FusedCfg<32, true>::kSmemBytes)
                          : go(moe_ffn_fused_kernel<32, false>, (size_t)FusedCfg<32, false>::kSmemBytes);
             else if (nb1 == 64)
@@ -1841,7 +1863,8 @@ reinterpret_cast<const void*>(moe_ep_p2p_fill_kernel),
             reinterpret_cast<const void*>(moe_ffn_fused_kernel<128, false>),
             reinterpret_cast<const void*>(moe_ffn_fused_kernel<32, true>),
             reinterpret_cast<const void*>(moe_ffn_fused_kernel<64, true>),
-            reinterpret_cast<const void*>(moe_ffn_fused_kernel<128, true>)};
+            reinterpret_cast<const void*>(moe_ffn_fused_kernel<128, true>),
+            reinterpret_cast<const void*>(moe_ffn_fused_kernel<32, false, true>)};
         for (const void* fn : fns)
             if ((e = cudaFuncGetAttributes(&fa, fn)) != cudaSuccess) return fail_init("cudaFuncGetAttributes", e);
     }

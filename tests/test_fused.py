@@ -230,3 +230,56 @@ def test_fused_half_mixtral_ranks(moe, par, G):
         outs.append(run.np("out_f32").copy())
         blk.close()
     assert np.array_equal(outs[0].view(np.int32), outs[1].view(np.int32))
+
+
+def _fp8_block_inputs(shape, seed):
+    """bf16 inputs + their E4M3 row-quantised weights and the oracle's exact-dequant host copy
+    (tests/test_gpu_parity.py _fp8_inputs)."""
+    from test_gpu_parity import _fp8_inputs
+    return _fp8_inputs(shape, seed)
+
+
+@pytest.mark.parametrize("T,d,f,E", [(64, 512, 1024, 8), (37, 256, 1024, 8), (64, 1024, 2560, 8), (16, 256, 512, 4)])
+def test_fused_fp8(moe, T, d, f, E):
+    """FP8 E4M3 weights through the fused FFN (FusedCfg FP8: kind::f8f6f4 w1/w3 tiles, block-scaled
+    w2 tiles with the B scales copied into TMEM per stage): oracle parity on the exact-dequant
+    weights, and bit-identity with the two-kernel FP8 path at uniform splits (same MMAs, same
+    K-chunk order, same scale placement)."""
+    shape = synth.MoEShape(T=T, d=d, f=f, E=E, k=2)
+    inp, qs, host = _fp8_block_inputs(shape, 7700 + T + d)
+    outs = []
+    for tu in ({"fused": 2, "fused_uniform": 1, "fused_splits": 4}, {"fused": 1}):
+        blk = moe.MoEBlock(inp["wg"], qs["w1"], qs["w3"], qs["w2"], top_k=2, max_tokens=T,
+                           flags=moe.MOE_FLAG_FP8_WEIGHTS, split_k=4, tuning=tu)
+        run = GpuRun(blk, inp["x"])
+        check_forward(run, host, 2)
+        if tu["fused"] == 2:
+            assert _launches(moe, blk, inp["x"]) == 4
+            out2 = blk.forward(inp["x"])
+            torch.cuda.synchronize()
+            assert torch.equal(out2.view(torch.int16), run.out.view(torch.int16))
+        outs.append(run.np("out_f32").copy())
+        blk.close()
+    assert np.array_equal(outs[0].view(np.int32), outs[1].view(np.int32))
+
+
+def test_fused_fp8_mixtral(moe):
+    """FP8 Mixtral-size 64-token decode: the fused FFN (uniform 4 splits) bit-identical to the
+    two-kernel FP8 path, and oracle parity on sampled tokens (exact-dequant weights); the default
+    tapered splits against the oracle too (tests/test_gpu_parity.py test_fp8_mixtral_decode
+    checks every token of the default path)."""
+    w = synth.make_weights(4096, 14336, 8, seed=42, device="cuda")
+    x = synth.make_tokens(64, 4096, seed=9200, device="cuda")
+    qs = {n: synth.quantize_fp8_rows(w[n]) for n in ("w1", "w3", "w2")}
+    host = {n: synth.dequantize_fp8_rows(*qs[n]).cpu().numpy() for n in qs}
+    host["x"] = x.float().cpu().numpy()
+    host["wg"] = w["wg"].float().cpu().numpy()
+    outs = []
+    for tu in ({"fused": 2, "fused_uniform": 1, "fused_splits": 4}, {"fused": 1}, {"fused": 2}):
+        blk = moe.MoEBlock(w["wg"], qs["w1"], qs["w3"], qs["w2"], top_k=2, max_tokens=64,
+                           flags=moe.MOE_FLAG_FP8_WEIGHTS, split_k=4, tuning=tu)
+        run = GpuRun(blk, x)
+        check_forward(run, host, 2, tokens=[0, 1, 33, 62, 63])
+        outs.append(run.np("out_f32").copy())
+        blk.close()
+    assert np.array_equal(outs[0].view(np.int32), outs[1].view(np.int32))
