@@ -30,7 +30,10 @@
  *     asynchronous; an asynchronous device fault surfaces as MOE_ERR_CUDA on a
  *     later call and is sticky (MOE_ERR_STATE thereafter for that context).
  *   - No exception crosses the ABI; the library never calls exit().
- *   - One host thread per context at a time.
+ *   - One host thread per context at a time, and the forwards of one context must be
+ *     ordered on the device (one stream, or streams ordered by events): they share the
+ *     context's workspace (permuted rows, h, fp32 partials) and, for the fused decode FFN,
+ *     its device-side tile-claim / readiness counters, which each launch's last CTA resets.
  *   - There is no CPU fallback: every step of the forward runs in libmoe's own
  *     CUDA kernels on the device (sm_100a). A machine without an sm_100 GPU
  *     gets MOE_ERR_UNSUPPORTED from moe_init.
