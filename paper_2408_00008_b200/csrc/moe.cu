@@ -973,6 +973,11 @@ moe_status run_gemms(moe_ctx* c, GemmPaths gp, int64_t rows_bound, int64_t rows_
     const bool sp_ok = pair && !c->fp8 && !c->gather_now && !c->spec_now && c->swap_pair_mode != 1;
     bool sp1 = sp_ok && gp.swap1 && c->f_local % 256 == 0 && (nb1 >= 128 || c->swap_pair_mode == 2);
     bool sp2 = sp_ok && gp.swap2 && (nb2 >= 128 || c->swap_pair_mode == 2);
+    // w1/w3 on CTA pairs only where the pair units (E_l x f_l/256) fill the clusters: below one
+    // wave (EP8 / TP8 ranks of the T=575 layer, 56 units on 74 clusters) the single-CTA tiles run
+    // 112 units on 148 SMs (TP8 rank 51.6 vs 53.3 us, profiles/r03/experiments/ab_tp8_stack_rank.txt;
+    // r02 shards_stack_pair.md: EP8 50.9 vs 51.9 us); the w2 GEMM stays on pairs there
+    if (sp1 && c->swap_pair_mode != 2 && (int64_t)c->E_local * (c->f_local / 256) < c->num_sms / 2) sp1 = false;
     if (sp1 && !c->tune_g1_nb && rows_bound > 128) {
         nb1 = swap_nb_ceil((int)std::min<int64_t>(need, 256), true);
         if (c->swap_nb_cap >= 32) nb1 = std::min(nb1, c->swap_nb_cap);
