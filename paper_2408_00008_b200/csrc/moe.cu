@@ -1026,6 +1026,10 @@ moe_status run_gemms(moe_ctx* c, GemmPaths gp, int64_t rows_bound, int64_t rows_
             fp.g.w_nt = c->w13_nt;
             fp.g.spec_l2 = c->spec_now && !c->fp8 ? c->spec_l2 : 0;
             if (c->fp8) {  // two E4M3 h planes + UE8M0 block scales (the FP8 w2 tiles' B operand)
+                // weights evict-first, as moe_gemm_fp8x_kernel: the 32-row token tile is below the
+                // 64-row bound, so the auto rule would pick evict-normal, and the weight stream then
+                // pushes the token planes (re-read by every w1/w3 tile) out of L2
+                fp.g.hint_a = c->swap_hint_mode ? c->swap_w_hint : ptx::kEvictFirst;
                 fp.g.out = c->h8;
                 fp.g.h_sf = c->h_sf;
                 fp.g.plane_rows = c->cap;
