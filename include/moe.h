@@ -158,7 +158,10 @@ typedef struct moe_tuning {
                                fill the SMs), 1 off, 2 on                                      */
     int32_t combine_vec;    /* combine kernel: 4-column groups per thread, 1 or 4 (0: 1 up to 256
                                tokens -- more blocks for the latency-bound decode combine -- else 4) */
-    int32_t reserved[1];    /* must be zero                                                  */
+    int32_t ep_fold;        /* EP over peer memory, T <= 64: 2 = the router's blocks dispatch the rows
+                               themselves after the scan (no permute / fill launch; bit-identical);
+                               0 / 1 = the permute kernel dispatches (default: faster measured)  */
+    int32_t reserved[8];    /* must be zero                                                  */
 } moe_tuning;
 
 typedef struct {

@@ -50,12 +50,12 @@ EXPORTED = ("moe_init", "moe_packed_sizes", "moe_pack_weights", "moe_forward", "
 
 TUNING_FIELDS = ("g1_swap_rows", "g2_swap_rows", "g1_grid", "g2_grid", "spec_l2", "swap_nb_cap", "pair_nblk",
                  "pair_order", "router_cc_max_T", "weight_hint", "host_stage", "g1_nb", "g2_nb",
-                 "pair_hints", "swap_pair", "fused", "fused_splits", "fused_stages", "fused_uniform", "fused_combine", "fused_chain", "fused_half", "combine_vec")
+                 "pair_hints", "swap_pair", "fused", "fused_splits", "fused_stages", "fused_uniform", "fused_combine", "fused_chain", "fused_half", "combine_vec", "ep_fold")
 
 
 class moe_tuning(ctypes.Structure):
     """include/moe.h moe_tuning: kernel-variant / grid overrides (0 = default)."""
-    _fields_ = [(n, ctypes.c_int32) for n in TUNING_FIELDS] + [("reserved", ctypes.c_int32 * 1)]
+    _fields_ = [(n, ctypes.c_int32) for n in TUNING_FIELDS] + [("reserved", ctypes.c_int32 * 8)]
 
 
 class moe_config(ctypes.Structure):

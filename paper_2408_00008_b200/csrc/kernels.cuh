@@ -48,6 +48,17 @@ struct RouteParams {
     // decode speculative weight prefetch (moe.cu spec_l2): let the permute kernel (and
     // through it the w1/w3 GEMM) launch while this grid still runs
     int32_t early_trigger;
+    // EP dispatch folded into the router (peer-memory transport, small batches; nullable
+    // scan_epoch = off): the last block bumps scan_epoch after the scan; every block waits for
+    // it and then does the permute kernel's dispatch for its own tokens -- positions, the rows
+    // into the destination ranks' receive buffers, the meta entries -- fills its share of the
+    // unused slots and takes part in the exchange's completion signal (p2p_signal_last_block).
+    unsigned int* scan_epoch;
+    uint8_t* const* peers;
+    int64_t peer_rows_off, peer_meta_off, sig_off;
+    int32_t cap, my_rank;
+    int32_t* pos_aux;           // [T, k] optional copy of the positions
+    unsigned int* p2p_ticket;
 };
 
 __device__ __forceinline__ int hist_key(int e, int key_lo, int key_div, int nkeys) {
@@ -167,7 +178,66 @@ __device__ __forceinline__ void route_block_finish(const RouteParams& p, const i
             p.offsets[e + 1] = off;
         }
         *p.done = 0u;  // ready for the next forward (kernel boundary orders it)
+        if (p.scan_epoch) {  // folded dispatch: the other blocks may read the offsets now
+            __threadfence();
+            atomicAdd(p.scan_epoch, 1u);
+        }
     }
+}
+
+// Folded EP dispatch (RouteParams::scan_epoch): after route_block_finish, in every block of a
+// router grid whose blocks are all resident (small batches). ep0 = scan_epoch read at kernel
+// start (before this block's completion ticket, so before the scan can be published).
+template <int NTHREADS, int TB>
+__device__ __forceinline__ void route_fold_dispatch(const RouteParams& p, const int32_t (*s_idx)[2], int ntok,
+                                                    int tok0, unsigned int ep0) {
+    __shared__ int32_t s_ps[TB][2];
+    if (threadIdx.x == 0) {
+        unsigned int v;
+        do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p.scan_epoch) : "memory");
+            if (v == ep0) __nanosleep(32);
+        } while (v == ep0);
+    }
+    __syncthreads();
+    // positions: destination rank e (the histogram key), slot r = block offset + in-block rank
+    if (threadIdx.x < ntok * p.k) {
+        const int tl = threadIdx.x / p.k, j = threadIdx.x % p.k;
+        const int t = tok0 + tl;
+        const int ex = s_idx[tl][j];
+        const int e = ex >= 0 ? hist_key(ex, p.key_lo, p.key_div, p.nkeys) : -1;
+        int32_t ps = -1;
+        if (e >= 0) {
+            const int32_t r = __ldcg(&p.blockoff[(int64_t)blockIdx.x * p.nkeys + e]) + __ldcg(&p.rank[(int64_t)t * p.k + j]);
+            ps = e * p.cap + r;
+            int32_t* meta = reinterpret_cast<int32_t*>(p.peers[e] + p.peer_meta_off) + (int64_t)p.my_rank * p.cap + r;
+            *meta = ex - e * p.key_div;  // expert index local to the destination
+        }
+        p.rank[(int64_t)t * p.k + j] = ps;  // rank[] doubles as the positions array (c->pos)
+        if (p.pos_aux) p.pos_aux[(int64_t)t * p.k + j] = ps;
+        s_ps[tl][j] = ps;
+    }
+    __syncthreads();
+    // rows: 16-byte vectors of each routed token row into its slots of the destinations' buffers
+    const int nvec = p.d / 8;
+    for (int tl = 0; tl < ntok; ++tl) {
+        const uint4* src = reinterpret_cast<const uint4*>(p.x + (int64_t)(tok0 + tl) * p.d);
+        for (int j = 0; j < p.k; ++j) {
+            const int32_t ps = s_ps[tl][j];
+            if (ps < 0) continue;
+            const int e = ps / p.cap, r = ps - e * p.cap;
+            uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.peers[e] + p.peer_rows_off) +
+                                                  ((int64_t)p.my_rank * p.cap + r) * p.d);
+            for (int v = threadIdx.x; v < nvec; v += NTHREADS) dst[v] = __ldg(src + v);
+        }
+    }
+    // this rank's unused slots [count_e, cap) of every destination's meta -> -1 (grid-stride)
+    for (int e = 0; e < p.nkeys; ++e) {
+        const int n0 = __ldcg(&p.counts[e]);
+        int32_t* meta = reinterpret_cast<int32_t*>(p.peers[e] + p.peer_meta_off) + (int64_t)p.my_rank * p.cap;
+        for (int i = n0 + blockIdx.x * NTHREADS + threadIdx.x; i < p.cap; i += gridDim.x * NTHREADS) meta[i] = -1;
+    }
+    p2p_signal_last_block(p.p2p_ticket, p.peers, p.nkeys, p.sig_off);  // the dispatch exchange is complete
 }
 
 // K1: router (a2, a3) + histogram / ranks (a4) + last-block exclusive scan (a5).
@@ -186,6 +256,7 @@ __global__ void __launch_bounds__(kRouteThreads) moe_router_kernel(const RoutePa
 
     ptx::pdl_wait();
     if (p.early_trigger) ptx::pdl_launch_dependents();
+    const unsigned int ep0 = p.scan_epoch ? *reinterpret_cast<volatile unsigned int*>(p.scan_epoch) : 0u;
 
     if (p.in_idx == nullptr) {
         float acc[TB][E_MAX];
@@ -288,6 +359,7 @@ __global__ void __launch_bounds__(kRouteThreads) moe_router_kernel(const RoutePa
     }
     __syncthreads();
     route_block_finish<kRouteThreads>(p, s_idx, ntok, tok0);
+    if (p.scan_epoch) route_fold_dispatch<kRouteThreads, TB>(p, s_idx, ntok, tok0, ep0);
 }
 
 
@@ -324,6 +396,7 @@ __global__ void __launch_bounds__(256) moe_router_mma_kernel(const RouteParams p
     ptx::pdl_wait();
     MOE_TL(0, 1);
     if (p.early_trigger) ptx::pdl_launch_dependents();
+    const unsigned int ep0 = p.scan_epoch ? *reinterpret_cast<volatile unsigned int*>(p.scan_epoch) : 0u;
 
     const int r0 = min(tok0 + g * 16 + gid, p.T - 1), r1 = min(tok0 + g * 16 + gid + 8, p.T - 1);
     const uint4* xa = reinterpret_cast<const uint4*>(p.x + (int64_t)r0 * p.d);
@@ -411,6 +484,7 @@ __global__ void __launch_bounds__(256) moe_router_mma_kernel(const RouteParams p
     __syncthreads();
     MOE_TL(0, 2);
     route_block_finish<256>(p, s_idx, ntok, tok0);
+    if (p.scan_epoch) route_fold_dispatch<256, TOK>(p, s_idx, ntok, tok0, ep0);
 }
 
 struct PermuteParams {

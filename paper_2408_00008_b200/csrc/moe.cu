@@ -279,6 +279,8 @@ struct moe_ctx {
     int32_t *counts = nullptr, *offsets = nullptr;
     float* topk_w = nullptr;
     unsigned int* done = nullptr;
+    unsigned int* fold_epoch = nullptr;   // folded EP dispatch: scan publications (monotonic)
+    int ep_fold_mode = 0;                 // tuning.ep_fold: 2 on (EP P2P, T <= 64), 0 / 1 off
     __nv_bfloat16 *x_perm = nullptr, *h = nullptr;
     int32_t* src_row = nullptr;  // gather mode: [cap + 512] token of each permuted row
     int w13_nt = 0, w2_nt = 0;   // tiles per expert of the tiled bf16 weight layout (256 / 128 rows)
@@ -650,7 +652,7 @@ moe_status validate_cfg(const moe_config* cfg, moe_ctx* c) {
     for (int i = 0; i < 2; ++i)
         if (cfg->reserved[i]) return fail(c, MOE_ERR_INVALID, "reserved fields must be zero");
     if (const moe_tuning* tu = cfg->tuning) {
-        for (int i = 0; i < 1; ++i)
+        for (int i = 0; i < 8; ++i)
             if (tu->reserved[i]) return fail(c, MOE_ERR_INVALID, "tuning.reserved fields must be zero");
         if (tu->g1_swap_rows < 0 || tu->g2_swap_rows < 0 || tu->g1_grid < 0 || tu->g2_grid < 0 ||
             tu->swap_nb_cap < 0 || tu->router_cc_max_T < 0 || tu->pair_order < 0)
@@ -660,6 +662,7 @@ moe_status validate_cfg(const moe_config* cfg, moe_ctx* c) {
         if (tu->fused < 0 || tu->fused > 2) return fail(c, MOE_ERR_INVALID, "tuning.fused must be 0, 1 or 2");
         if (tu->fused_splits < 0 || tu->fused_splits > 8)
             return fail(c, MOE_ERR_INVALID, "tuning.fused_splits must be in [0, 8]");
+        if (tu->ep_fold < 0 || tu->ep_fold > 2) return fail(c, MOE_ERR_INVALID, "tuning.ep_fold must be 0, 1 or 2");
         if (tu->combine_vec != 0 && tu->combine_vec != 1 && tu->combine_vec != 4)
             return fail(c, MOE_ERR_INVALID, "tuning.combine_vec must be 0, 1 or 4");
         if (tu->fused_half < 0 || tu->fused_half > 2)
@@ -811,6 +814,12 @@ struct RouteSpec {
     int64_t peer_rows_off = 0, peer_meta_off = 0;
     int my_rank = 0;
     bool early = false;          // spec_l2: router and permute trigger their dependents early
+    // EP P2P dispatch folded into the router (CUDA-core router, every block does the permute's
+    // work for its tokens after the scan, no permute / fill launch): peers + cap + my_rank above,
+    // completion through ticket / sig like moe_ep_p2p_fill_kernel
+    bool fold = false;
+    unsigned int* fold_ticket = nullptr;
+    int64_t fold_sig_off = 0;
 };
 
 moe_status route_and_permute(moe_ctx* c, const RouteSpec& r, cudaStream_t st) {
@@ -836,6 +845,17 @@ moe_status route_and_permute(moe_ctx* c, const RouteSpec& r, cudaStream_t st) {
     rp.blockcount = c->blockcount; rp.blockoff = c->blockoff;
     rp.counts = c->counts; rp.offsets = c->offsets; rp.done = c->done;
     rp.early_trigger = r.early;
+    if (r.fold) {
+        rp.scan_epoch = c->fold_epoch;
+        rp.peers = r.peers;
+        rp.peer_rows_off = r.peer_rows_off;
+        rp.peer_meta_off = r.peer_meta_off;
+        rp.sig_off = r.fold_sig_off;
+        rp.cap = r.cap;
+        rp.my_rank = r.my_rank;
+        rp.pos_aux = r.pos_aux;
+        rp.p2p_ticket = r.fold_ticket;
+    }
     moe_status s;
     const dim3 rg(nblk);
     if (mma && KS == 1) s = launch(c, kSlotRouter, moe_router_mma_kernel<1>, rg, dim3(256), 0, st, rp);
@@ -844,6 +864,7 @@ moe_status route_and_permute(moe_ctx* c, const RouteSpec& r, cudaStream_t st) {
     else if (c->E <= 16) s = launch(c, kSlotRouter, moe_router_kernel<16, 2>, rg, dim3(kRouteThreads), 0, st, rp);
     else s = launch(c, kSlotRouter, moe_router_kernel<32, 2>, rg, dim3(kRouteThreads), 0, st, rp);
     if (s) return s;
+    if (r.fold) return MOE_OK;  // the router blocks did the dispatch
 
     PermuteParams pp{};
     pp.x = rp.x; pp.topk_idx = r.topk_idx; pp.blockoff = c->blockoff; pp.offsets = c->offsets;
@@ -1653,6 +1674,7 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
         c->fused_chain_mode = tu->fused_chain;
         c->fused_half_mode = tu->fused_half;
         c->combine_vec = tu->combine_vec;
+        c->ep_fold_mode = tu->ep_fold;
     }
     if (cfg->flags & MOE_FLAG_GATHER) c->gather = true;
     // EP: a rank may receive up to every token of every peer (dropless, reading R6).
@@ -1704,6 +1726,7 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
     ALLOC(c->counts, sizeof(int32_t) * 64);
     ALLOC(c->offsets, sizeof(int32_t) * 64);
     ALLOC(c->done, sizeof(unsigned int) * 4);
+    ALLOC(c->fold_epoch, sizeof(unsigned int) * 4);
     ALLOC(c->fused_sched, sizeof(int32_t) * 4);
     ALLOC(c->fused_ready, sizeof(int32_t) * ((int64_t)c->E_local * (c->f_local / 64) + 4));
     ALLOC(c->fused_arrive, sizeof(int32_t) * (c->d / 256 + 4));
@@ -1786,7 +1809,9 @@ moe_status moe_init(const moe_config* cfg, moe_ctx** out) {
             return fail(nullptr, MOE_ERR_UNSUPPORTED, "%s", nerr);
         }
     }
-    if ((e = cudaMemset(c->done, 0, sizeof(unsigned int) * 4)) != cudaSuccess) return fail_init("memset", e);
+    if ((e = cudaMemset(c->done, 0, sizeof(unsigned int) * 4)) != cudaSuccess ||
+        (e = cudaMemset(c->fold_epoch, 0, sizeof(unsigned int) * 4)) != cudaSuccess)
+        return fail_init("memset", e);
     if ((e = cudaMemset(c->fused_sched, 0, sizeof(int32_t) * 4)) != cudaSuccess ||
         (e = cudaMemset(c->fused_ready, 0, sizeof(int32_t) * ((int64_t)c->E_local * (c->f_local / 64) + 4))) != cudaSuccess ||
         (e = cudaMemset(c->fused_arrive, 0, sizeof(int32_t) * (c->d / 256 + 4))) != cudaSuccess ||
@@ -1889,7 +1914,7 @@ moe_status moe_destroy(moe_ctx* c) {
                     c->x_perm, c->h, c->y, c->stage_in, c->stage_out, c->tp_partial, c->tp_scatter, c->ep_send,
                     c->ep_recv, c->ep_ysend, c->ep_yrecv, c->ep_meta_send, c->ep_meta_recv,
                     c->ep_ridx, c->ep_rpos, c->ep_rw, c->ep_rcounts, c->lb_scratch, c->d_peers, c->p2p_tickets, c->src_row,
-                    c->tok_scale, c->h8, c->h_sf, c->fused_sched, c->fused_ready, c->fused_arrive, c->fused_chain};
+                    c->tok_scale, c->h8, c->h_sf, c->fused_sched, c->fused_ready, c->fused_arrive, c->fused_chain, c->fold_epoch};
     for (void* p : c->p2p_opened) cudaIpcCloseMemHandle(p);
     if (c->nvls) {
         cudaDeviceSynchronize();  // no fused combine still reads / writes the window
@@ -2384,6 +2409,12 @@ moe_status forward_ep_p2p(moe_ctx* c, const void* tokens, int32_t T, const void*
     const int64_t R = (int64_t)cap * G;
     uint8_t* const* peers = c->d_peers;
     StepTimer t1(c, kSlotDispatch, st);
+    // folded dispatch: T <= 64 (the router's blocks -- 16 tokens each on the tensor-core router,
+    // 2 on the CUDA-core one -- are all resident while they wait for the scan)
+    // Opt-in (tuning.ep_fold = 2): on one GPU shared by two P2P ranks the folded dispatch measured
+    // 0.768-0.774 vs 0.748 ms per EP step (the router's 1-4 blocks copy the rows where the
+    // permute spreads them over T/2 blocks; profiles/r03/experiments/ab_ep_fold_one_gpu.txt)
+    const bool fold = T > 0 && T <= 64 && c->ep_fold_mode == 2;
     if (T > 0) {
         RouteSpec r;
         r.x = tokens; r.T = T; r.k = c->k; r.router_w = router_w;
@@ -2393,15 +2424,22 @@ moe_status forward_ep_p2p(moe_ctx* c, const void* tokens, int32_t T, const void*
         r.pos = c->pos; r.pos_aux = aux ? aux->pos : nullptr;
         r.dst_rows = nullptr; r.cap = cap; r.meta = nullptr;
         r.peers = peers; r.peer_rows_off = c->so.ep_rows; r.peer_meta_off = c->so.ep_meta; r.my_rank = me;
+        // small batches: the router's blocks (<= 32, all resident) dispatch their own rows after
+        // the scan (EP dispatch issued by the router; no permute / fill launch)
+        r.fold = fold;
+        r.fold_ticket = c->p2p_tickets + 0;
+        r.fold_sig_off = c->so.sig + 8 * 0;
         if ((s = route_and_permute(c, r, st))) return s;
         if ((s = copy_aux(c, aux, T, st))) return s;
     }
-    // this rank's unused slots in every destination's receive buffer -> -1
-    const int fbx = std::max(1, std::min(64, (cap + 255) / 256));
-    if ((s = launch(c, kSlotDispatch, moe_ep_p2p_fill_kernel, dim3(fbx, G), dim3(256), 0, st, peers, c->so.ep_meta,
-                    T > 0 ? static_cast<const int32_t*>(c->counts) : nullptr, G, cap, me, c->p2p_tickets + 0,
-                    c->so.sig + 8 * 0)))
-        return s;
+    if (!fold) {
+        // this rank's unused slots in every destination's receive buffer -> -1
+        const int fbx = std::max(1, std::min(64, (cap + 255) / 256));
+        if ((s = launch(c, kSlotDispatch, moe_ep_p2p_fill_kernel, dim3(fbx, G), dim3(256), 0, st, peers, c->so.ep_meta,
+                        T > 0 ? static_cast<const int32_t*>(c->counts) : nullptr, G, cap, me, c->p2p_tickets + 0,
+                        c->so.sig + 8 * 0)))
+            return s;
+    }
     if ((s = p2p_wait(c, 0, st))) return s;
     t1.done();
     // receive side: as the NCCL path, over this rank's region

@@ -511,6 +511,7 @@ def _run_group(moe, inp, par, G, shards, k=2, flags=0, max_tokens=None, p2p=Fals
             x = shards[r]
             T = x.shape[0]
             aux = {"topk_idx": torch.empty(max(T, 1), k, dtype=torch.int32, device="cuda"),
+                   "pos": torch.empty(max(T, 1), k, dtype=torch.int32, device="cuda"),
                    "out_f32": torch.empty(max(T, 1), d, dtype=torch.float32, device="cuda")}
             out = torch.empty(max(T, 1), d, dtype=torch.bfloat16, device="cuda")
             first = None
@@ -633,6 +634,30 @@ def test_p2p_equals_collectives(moe, G, par, mode):
         for r in range(1, G):
             assert torch.equal(got[0][0], got[r][0])
         _check_group_outputs(host, 2, host["x"], [got[0][0]], [got[0][1]])
+
+
+@pytest.mark.parametrize("G", [2, 4, 8])
+def test_ep_router_dispatch(moe, G):
+    """EP over peer memory with the dispatch folded into the router (tuning ep_fold = 2, T <= 64
+    per rank): the router's blocks wait for the scan and store their rows and meta into the
+    destinations' buffers themselves (no permute / fill launch). Bit-identical to the
+    permute-kernel dispatch (ep_fold = 1) over 3 forwards, an empty rank and a 64-token rank
+    included, and the oracle within tolerance."""
+    shape = synth.MoEShape(T=64 * G // 2, d=256, f=512, E=8, k=2)
+    inp = _inputs(shape, 7800 + G)
+    host = to_host_inputs(inp)
+    cuts = np.linspace(0, shape.T, G + 1).astype(int)
+    cuts[1] = 0  # rank 0: no tokens; the others up to 64
+    shards = [inp["x"][cuts[r]:cuts[r + 1]] for r in range(G)]
+    outs = []
+    for tu in ({"ep_fold": 2}, {"ep_fold": 1}):
+        res = _run_group(moe, inp, moe.MOE_PAR_EP, G, shards, max_tokens=64, p2p=True, iters=3, tuning=tu)
+        outs.append(res)
+    for r in range(G):
+        assert torch.equal(outs[0][r][0].view(torch.int16), outs[1][r][0].view(torch.int16)), r
+        assert torch.equal(outs[0][r][1]["out_f32"], outs[1][r][1]["out_f32"]), r
+        assert torch.equal(outs[0][r][1]["pos"], outs[1][r][1]["pos"]), r
+    _check_group_outputs(host, 2, host["x"], [g[0] for g in outs[0]], [g[1] for g in outs[0]])
 
 
 @pytest.mark.parametrize("par", ["ep", "tp"])
