@@ -158,6 +158,28 @@ def test_fused_group(moe, par, G, half):
         _check_group_outputs(host, 2, host["x"], [res[0][0]], [res[0][1]])
 
 
+@pytest.mark.parametrize("par,G", [("ep", 2), ("tp", 2), ("tp", 4)])
+def test_fused_p2p_equals_collectives(moe, par, G):
+    """Fused FFN inside EP / TP over peer memory (MOE_FLAG_P2P): bit-identical to the same
+    contexts over the loopback collectives, over 3 back-to-back forwards."""
+    from test_gpu_parity import _run_group
+    shape = synth.MoEShape(T=64, d=256, f=1024, E=8, k=2)
+    inp = synth.make_inputs(shape, 7900 + G, device="cuda")
+    if par == "ep":
+        cuts = np.linspace(0, shape.T, G + 1).astype(int)
+        shards = [inp["x"][cuts[r]:cuts[r + 1]] for r in range(G)]
+        pm = moe.MOE_PAR_EP
+    else:
+        shards = [inp["x"]] * G
+        pm = moe.MOE_PAR_TP
+    tu = {"fused": 2}
+    ref = _run_group(moe, inp, pm, G, shards, max_tokens=shape.T, tuning=tu)
+    got = _run_group(moe, inp, pm, G, shards, max_tokens=shape.T, p2p=True, iters=3, tuning=tu)
+    for r in range(G):
+        assert torch.equal(ref[r][0].view(torch.int16), got[r][0].view(torch.int16)), r
+        assert torch.equal(ref[r][1]["out_f32"], got[r][1]["out_f32"]), r
+
+
 def test_fused_mixtral_decode(moe):
     """BASELINE configs[1]: Mixtral layer, 64-token decode, fused FFN (sampled tokens vs the
     oracle, every token's routing) and bit-identical to the two-kernel path at 4 splits
