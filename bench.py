@@ -919,7 +919,9 @@ def main():
         achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": achieved / peaks["hbm_gbs"], "traffic": None,
-                "kernel": ("moe_gemm_fp8x_kernel<kG1Swap> (FP8 w1/w3 + SwiGLU, kind::f8f6f4)" if args.fp8
+                "kernel": ("moe_ffn_fused_kernel<32,0,1> (FP8: w1/w3 + SwiGLU on kind::f8f6f4 and block-scaled w2, "
+                           "one launch)" if args.fp8 and fused
+                           else "moe_gemm_fp8x_kernel<kG1Swap> (FP8 w1/w3 + SwiGLU, kind::f8f6f4)" if args.fp8
                            else "moe_ffn_fused_kernel (w1/w3 + SwiGLU and w2 in one launch)" if fused
                            else "moe_gemm_kernel<kG1Swap> (w1/w3 + SwiGLU)"),
                 "peak_src": peaks["src"] + " (MEASURED_PEAKS.json hbm_gbs)"}

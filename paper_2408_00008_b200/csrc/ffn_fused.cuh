@@ -97,16 +97,20 @@ constexpr int kFusedEpiBar = 1;    // named barrier of the 4 epilogue warps
 // of weights + 2 x NB token rows), and the epilogue pairs a (TMEM lanes 0-63) with b (lanes
 // 64-127) through a shared-memory exchange buffer. w2 tiles are the same in both variants.
 // FP8 (E4M3 weights, round 3): the two-kernel FP8 path's tiles (moe_gemm_fp8x_kernel) in the
-// fused schedule. A stage = one 128-byte K chunk: 256 weight rows (G1: a W13 tile; G2: W2 tiles
-// 2m and 2m+1) + the hi and lo E4M3 terms of the NB token / h rows (stacked, N = 2 NB) + for G2
-// the tile's UE8M0 B-scale block; G1 runs kind::f8f6f4 MMAs, G2 the block-scaled
-// kind::mxf8f6f4 ones (B scales copied into TMEM per stage, A scales a constant 2^0 atom).
-// Accumulator stage = 4 NB columns (two M=128 MMAs x hi/lo halves); NB = 32 only.
+// fused schedule, 32 KB of weights per stage in both phases. A w1/w3 stage = one 128-byte K
+// chunk of a 256-row W13 tile + the hi and lo E4M3 terms of the NB token rows (stacked, N = 2 NB;
+// kind::f8f6f4 MMAs, w1 and w3 halves into two accumulators). A w2 stage = TWO K chunks of a
+// 128-row W2 tile, each with its hi / lo h rows and UE8M0 B-scale block (block-scaled
+// kind::mxf8f6f4 MMAs, B scales copied into TMEM per chunk, A scales a constant 2^0 atom) --
+// 256-row w2 tiles (two MMAs sharing the scales) measured slower. NB = 32 only.
 template <int NB, bool HALF = false, bool FP8 = false>
 struct FusedCfg {
     static constexpr int kABytes = 256 * 128;       // 256 weight rows x 64 bf16 (HALF G1: 2 x 128 rows x 64; FP8: x 128 E4M3)
-    static constexpr int kBBytes = FP8 ? 2 * NB * 128 : (HALF ? 2 : 1) * NB * 128;  // token rows x 128 B (x 2 K blocks / terms)
-    static constexpr int kSFBytes = FP8 ? 512 : 0;  // FP8 G2: the tile's B scale block per K chunk
+    // FP8: a w2 stage carries TWO K chunks of a 128-row W2 tile (2 x 16 KB weights, 2 x the hi/lo
+    // h rows, 2 scale blocks) -- the same weight bytes per stage as a w1/w3 stage, whose single
+    // 128-byte K chunk of 256 rows uses half of the B region
+    static constexpr int kBBytes = FP8 ? 2 * 2 * NB * 128 : (HALF ? 2 : 1) * NB * 128;  // token rows x 128 B (x 2 K blocks / terms)
+    static constexpr int kSFBytes = FP8 ? 2 * 512 : 0;  // FP8 G2: the tile's B scale blocks of the stage's two K chunks
     static constexpr int kStageBytes = kABytes + kBBytes + kSFBytes;
     static constexpr int kXPitch = NB + 1;          // exchange row pitch in floats (bank-conflict free)
     static constexpr int kXBytes = HALF ? 64 * kXPitch * 4 : 0;
@@ -115,6 +119,7 @@ struct FusedCfg {
     static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
     static constexpr int kSmemBytes = kStages * kStageBytes + kXBytes + kSfaBytes + 2048;
     static constexpr int kAccStride = FP8 ? 4 * NB : 256;  // TMEM columns per accumulator stage
+    static constexpr int kG2Rows = FP8 ? 128 : 256;        // w2 tile rows (FP8: one block-scaled MMA per K step)
     static constexpr uint32_t kSfaCol = 480, kSfbCol = 488;  // FP8 scale columns in TMEM
     static_assert(NB >= 16 && NB <= 128 && NB % 16 == 0, "fused tile: a/b accumulators of <= 128 columns");
     static_assert(!FP8 || (!HALF && NB == 32), "FP8 fused tiles: 32-row token tiles, 256-row w1/w3 tiles");
@@ -145,7 +150,7 @@ template <int NB, bool HALF, bool FP8>
 __device__ __forceinline__ void fused_decode(int t, const FusedParams& p, const int32_t* s_counts,
                                              const int32_t* s_offsets, int total1, int per_split, FusedTile& ti) {
     const int wt = p.g.f / 128 * (HALF ? 2 : 1);  // w1/w3 tiles per expert and token tile
-    const int mt2 = p.g.d / 256;
+    const int mt2 = p.g.d / FusedCfg<NB, HALF, FP8>::kG2Rows;
     ti.g1 = t < total1;
     ti.s = 0;
     if (!ti.g1) {
@@ -314,7 +319,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     for (int e = 0; e < p.g.E; ++e) {
         const int nt = fused_nt(s_counts[e], NB);
         total1 += nt * wt * (HALF ? 2 : 1);
-        per_split += nt * (p.g.d / 256);
+        per_split += nt * (p.g.d / C::kG2Rows);
     }
     const int total = total1 + per_split * p.splits;
     // combine tasks after the GEMM tiles; a slice is complete after S * sum_e nt_e w2 tiles
@@ -325,7 +330,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const int nchunk = p.combine_T > 0 ? (p.combine_T + p.comb_chunk - 1) / p.comb_chunk : 0;
     const int ncomb = (p.g.d / 256) * nchunk;
     const int total_all = total + ncomb;
-    const int slice_need = p.splits * (per_split / (p.g.d / 256));
+    const int slice_need = p.splits * (per_split / (p.g.d / C::kG2Rows));
     const uint64_t w_hint = p.g.hint_a ? p.g.hint_a : ptx::kEvictFirst;
 
     if (warp == 0) {
@@ -373,26 +378,32 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                     all_ready = true;
                 }
                 if (FP8 && (ti.g1 || all_ready)) {
-                    // one 128-byte K chunk per stage: 256 weight rows, hi / lo token (h) rows, (G2) scales
+                    // w1/w3: one 128-byte K chunk per stage (256 weight rows, hi / lo token rows);
+                    // w2: two K chunks per stage (128 weight rows + hi / lo h rows + scales each)
                     const int d128 = p.g.d / 128;
-                    for (int kb = 0; kb < ti.nkb; ++kb) {
-                        const int kq = ti.kb0 + kb;
+                    const int step = ti.g1 ? 1 : 2;
+                    for (int kb = 0; kb < ti.nkb; kb += step) {
                         ptx::mbar_wait(&empty[stage], phase ^ 1);
-                        ptx::mbar_arrive_expect_tx(&full[stage], ti.g1 ? C::kABytes + C::kBBytes : C::kStageBytes);
                         uint8_t* sa = smem_a + stage * C::kABytes;
                         uint8_t* sb = smem_b + stage * C::kBBytes;
                         if (ti.g1) {
+                            const int kq = ti.kb0 + kb;
+                            ptx::mbar_arrive_expect_tx(&full[stage], C::kABytes + 2 * NB * 128);
                             ptx::tma_load_4d(&tmW13, &full[stage], sa, 0, 0, kq, ti.m + ti.e * wt, w_hint);
                             ptx::tma_load_3d(&tmX, &full[stage], sb, kq * 128, ti.b_row, 0, ptx::kEvictLast);
                             ptx::tma_load_3d(&tmX, &full[stage], sb + NB * 128, kq * 128, ti.b_row, 1, ptx::kEvictLast);
                         } else {
-                            ptx::tma_load_4d(&tmW2, &full[stage], sa, 0, 0, kq, 2 * ti.m + ti.e * d128, w_hint);
-                            ptx::tma_load_4d(&tmW2, &full[stage], sa + 16384, 0, 0, kq, 2 * ti.m + 1 + ti.e * d128, w_hint);
-                            ptx::tma_load_3d(&tmH, &full[stage], sb, kq * 128, ti.b_row, 0, ptx::kEvictLast);
-                            ptx::tma_load_3d(&tmH, &full[stage], sb + NB * 128, kq * 128, ti.b_row, 1, ptx::kEvictLast);
-                            ptx::bulk_load(smem_sf + stage * C::kSFBytes,
-                                           p.g.h_sf + ((int64_t)(ti.b_row / NB) * wt + kq) * C::kSFBytes, C::kSFBytes,
-                                           &full[stage]);
+                            const int nc = min(2, ti.nkb - kb);
+                            ptx::mbar_arrive_expect_tx(&full[stage], nc * (16384 + 2 * NB * 128 + 512));
+                            for (int u = 0; u < nc; ++u) {
+                                const int kq = ti.kb0 + kb + u;
+                                ptx::tma_load_4d(&tmW2, &full[stage], sa + u * 16384, 0, 0, kq, ti.m + ti.e * d128, w_hint);
+                                uint8_t* sbu = sb + u * 2 * NB * 128;
+                                ptx::tma_load_3d(&tmH, &full[stage], sbu, kq * 128, ti.b_row, 0, ptx::kEvictLast);
+                                ptx::tma_load_3d(&tmH, &full[stage], sbu + NB * 128, kq * 128, ti.b_row, 1, ptx::kEvictLast);
+                                ptx::bulk_load(smem_sf + stage * C::kSFBytes + u * 512,
+                                               p.g.h_sf + ((int64_t)(ti.b_row / NB) * wt + kq) * 512, 512, &full[stage]);
+                            }
                         }
                         if (++stage == SR) { stage = 0; phase ^= 1; }
                     }
@@ -461,22 +472,28 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                     };
                     const int st0 = stage;
                     int bq = 0;  // K blocks whose h load is issued
+                    // K units of the stages: FP8 = pairs of K chunks (the last one may be single)
+                    const int nunits = FP8 ? (ti.nkb + 1) / 2 : ti.nkb;
                     auto issue_b = [&](int q) {
                         const int sq = (st0 + q) % SR;
                         if (FP8) {
-                            const int kq = ti.kb0 + q;
-                            uint8_t* sb = smem_b + sq * C::kBBytes;
-                            ptx::tma_load_3d(&tmH, &full[sq], sb, kq * 128, ti.b_row, 0, ptx::kEvictLast);
-                            ptx::tma_load_3d(&tmH, &full[sq], sb + NB * 128, kq * 128, ti.b_row, 1, ptx::kEvictLast);
-                            ptx::bulk_load(smem_sf + sq * C::kSFBytes,
-                                           p.g.h_sf + ((int64_t)(ti.b_row / NB) * wt + kq) * C::kSFBytes, C::kSFBytes,
-                                           &full[sq]);
+                            const int nc = min(2, ti.nkb - 2 * q);
+                            for (int u = 0; u < nc; ++u) {
+                                const int kq = ti.kb0 + 2 * q + u;
+                                uint8_t* sb = smem_b + sq * C::kBBytes + u * 2 * NB * 128;
+                                ptx::tma_load_3d(&tmH, &full[sq], sb, kq * 128, ti.b_row, 0, ptx::kEvictLast);
+                                ptx::tma_load_3d(&tmH, &full[sq], sb + NB * 128, kq * 128, ti.b_row, 1, ptx::kEvictLast);
+                                ptx::bulk_load(smem_sf + sq * C::kSFBytes + u * 512,
+                                               p.g.h_sf + ((int64_t)(ti.b_row / NB) * wt + kq) * 512, 512, &full[sq]);
+                            }
                         } else {
                             ptx::tma_load_2d(&tmH, &full[sq], smem_b + sq * C::kBBytes, (ti.kb0 + q) * kBK, ti.b_row,
                                              ptx::kEvictLast);
                         }
                     };
-                    auto unit_ok = [&](int q) { return (q + 1) * fpq <= ok; };  // K unit q's h is ready
+                    auto unit_ok = [&](int q) {  // K unit q's h is ready
+                        return (FP8 ? min(2 * q + 2, ti.nkb) : q + 1) * fpq <= ok;
+                    };
                     auto wait_ready = [&](int q) {
 #if MOE_TIMELINE
                         const unsigned long long w0 = !unit_ok(q) ? ptx::tl_now() : 0;
@@ -489,7 +506,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                         if (w0) tl_stall += ptx::tl_now() - w0;
 #endif
                     };
-                    for (int q = 0; q < ti.nkb; ++q) {
+                    for (int q = 0; q < nunits; ++q) {
                         // the stage about to be reused must have its h load in flight (its MMA
                         // frees it only after both operands arrived)
                         while (bq <= q - SR) {
@@ -497,24 +514,26 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                             issue_b(bq++);
                         }
                         ptx::mbar_wait(&empty[stage], phase ^ 1);
-                        ptx::mbar_arrive_expect_tx(&full[stage], FP8 ? C::kStageBytes : C::kABytes + NB * 128);
+                        const int ncq = FP8 ? min(2, ti.nkb - 2 * q) : 1;
+                        ptx::mbar_arrive_expect_tx(&full[stage], FP8 ? ncq * (16384 + 2 * NB * 128 + 512) : C::kABytes + NB * 128);
                         uint8_t* sa = smem_a + stage * C::kABytes;
                         const int kq = ti.kb0 + q;
                         if (FP8) {
                             const int d128 = p.g.d / 128;
-                            ptx::tma_load_4d(&tmW2, &full[stage], sa, 0, 0, kq, 2 * ti.m + ti.e * d128, w_hint);
-                            ptx::tma_load_4d(&tmW2, &full[stage], sa + 16384, 0, 0, kq, 2 * ti.m + 1 + ti.e * d128, w_hint);
+                            for (int u = 0; u < ncq; ++u)
+                                ptx::tma_load_4d(&tmW2, &full[stage], sa + u * 16384, 0, 0, ti.kb0 + 2 * q + u,
+                                                 ti.m + ti.e * d128, w_hint);
                         } else {
                             ptx::tma_load_4d(&tmW2, &full[stage], sa, 0, 0, kq, 2 * ti.m + ti.e * p.w2_nt, w_hint);
                         }
                         // weights of the first stages go out before the first readiness check
-                        if (q == SR - 1 || q == ti.nkb - 1 || (q >= SR && (q & 3) == 3)) {
+                        if (q == SR - 1 || q == nunits - 1 || (q >= SR && (q & 3) == 3)) {
                             if (!unit_ok(bq)) refresh();
                         }
                         while (bq <= q && unit_ok(bq)) issue_b(bq++);
                         if (++stage == SR) { stage = 0; phase ^= 1; }
                     }
-                    while (bq < ti.nkb) {
+                    while (bq < nunits) {
                         wait_ready(bq);
                         issue_b(bq++);
                     }
@@ -547,7 +566,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 ptx::mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
                 ptx::tc_fence_after();
                 const bool half_g1 = HALF && ti.g1;
-                for (int kb = 0; kb < ti.nkb; kb += half_g1 ? 2 : 1) {
+                const bool fp8_g2 = FP8 && !ti.g1;  // two K chunks per stage
+                for (int kb = 0; kb < ti.nkb; kb += (half_g1 || fp8_g2) ? 2 : 1) {
                     ptx::mbar_wait(&full[stage], phase);
                     ptx::tc_fence_after();
                     const uint32_t sa = ptx::smem_u32(smem_a + stage * C::kABytes);
@@ -557,22 +577,29 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                         constexpr uint32_t N2 = 2 * NB;
                         const uint64_t a1 = ptx::make_smem_desc_sw128(sa);
                         const uint64_t b0 = ptx::make_smem_desc_sw128(sb);
-                        if (!ti.g1) {  // this stage's B scales -> TMEM (in order before the MMAs below)
-                            ptx::tmem_cp_32x128b_x4(sfb, ptx::make_smem_desc_rows16(ptx::smem_u32(smem_sf + stage * C::kSFBytes)));
-                        }
+                        if (ti.g1) {
 #pragma unroll
-                        for (int kk = 0; kk < 4; ++kk) {
-                            const uint32_t acc_in = (kb | kk) ? 1u : 0u;
-                            if (ti.g1) {
+                            for (int kk = 0; kk < 4; ++kk) {
+                                const uint32_t acc_in = (kb | kk) ? 1u : 0u;
                                 const uint32_t id8 = (1u << 4) | ((N2 >> 3) << 17) | ((128u >> 4) << 24);  // D f32, E4M3
                                 ptx::mma_e4m3(d_tmem, a1 + 2 * kk, b0 + 2 * kk, id8, acc_in);
                                 ptx::mma_e4m3(d_tmem + N2, a1 + (16384 >> 4) + 2 * kk, b0 + 2 * kk, id8, acc_in);
-                            } else {
-                                const uint32_t sel = static_cast<uint32_t>(kk) << 30;  // K block kk of the chunk
-                                const uint32_t idmx = ptx::make_idesc_mx_e4m3(128, N2, kk, kk);
-                                ptx::mma_mx_e4m3(d_tmem, a1 + 2 * kk, b0 + 2 * kk, idmx, acc_in, sfa | sel, sfb | sel);
-                                ptx::mma_mx_e4m3(d_tmem + N2, a1 + (16384 >> 4) + 2 * kk, b0 + 2 * kk, idmx, acc_in,
-                                                 sfa | sel, sfb | sel);
+                            }
+                        } else {
+                            const int nc = min(2, ti.nkb - kb);
+                            for (int u = 0; u < nc; ++u) {
+                                // this chunk's B scales -> TMEM (in order before its MMAs)
+                                ptx::tmem_cp_32x128b_x4(sfb, ptx::make_smem_desc_rows16(
+                                                                 ptx::smem_u32(smem_sf + stage * C::kSFBytes + u * 512)));
+                                const uint64_t au = a1 + (u * 16384 >> 4);
+                                const uint64_t bu = b0 + (u * 2 * NB * 128 >> 4);
+#pragma unroll
+                                for (int kk = 0; kk < 4; ++kk) {
+                                    const uint32_t acc_in = (kb | u | kk) ? 1u : 0u;
+                                    const uint32_t sel = static_cast<uint32_t>(kk) << 30;  // K block kk of the chunk
+                                    const uint32_t idmx = ptx::make_idesc_mx_e4m3(128, N2, kk, kk);
+                                    ptx::mma_mx_e4m3(d_tmem, au + 2 * kk, bu + 2 * kk, idmx, acc_in, sfa | sel, sfb | sel);
+                                }
                             }
                         }
                     } else if (half_g1) {
@@ -733,27 +760,21 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 }
                 fence_proxy_async_global();  // h planes + scales -> visible to the w2 tiles' TMA / bulk loads
             } else if (FP8) {
-                // rows 256 m + r (first MMA: columns [0, 2 NB)) and 256 m + 128 + r ([2 NB, 4 NB)); hi + lo
-                const int drow = ti.m * 256 + r;
+                // row 128 m + r (columns [0, NB): hi term, [NB, 2 NB): lo term)
+                const int drow = ti.m * 128 + r;
                 const float s2a = p.w2_scale[(int64_t)ti.e * p.g.d + drow];
-                const float s2b = p.w2_scale[(int64_t)ti.e * p.g.d + drow + 128];
                 float* y = p.y + p.y_split_stride * ti.s + static_cast<int64_t>(ti.b_row) * p.g.d + drow;
 #pragma unroll 1
                 for (int cc = 0; cc < nchunks; ++cc) {
-                    uint32_t v0[16], v1[16], w0[16], w1[16];
+                    uint32_t v0[16], v1[16];
                     ptx::tmem_ld16(tbase + cc * 16, v0);
                     ptx::tmem_ld16(tbase + NB + cc * 16, v1);
-                    ptx::tmem_ld16(tbase + 2 * NB + cc * 16, w0);
-                    ptx::tmem_ld16(tbase + 3 * NB + cc * 16, w1);
                     ptx::tmem_wait_ld();
 #pragma unroll
                     for (int i = 0; i < 16; ++i) {
                         const int n = cc * 16 + i;
-                        if (n < ti.n_valid) {
+                        if (n < ti.n_valid)
                             y[static_cast<int64_t>(n) * p.g.d] = (__uint_as_float(v0[i]) + __uint_as_float(v1[i])) * s2a;
-                            y[static_cast<int64_t>(n) * p.g.d + 128] =
-                                (__uint_as_float(w0[i]) + __uint_as_float(w1[i])) * s2b;
-                        }
                     }
                 }
             } else if (HALF && ti.g1) {

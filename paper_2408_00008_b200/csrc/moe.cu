@@ -1027,11 +1027,11 @@ moe_status run_gemms(moe_ctx* c, GemmPaths gp, int64_t rows_bound, int64_t rows_
         // profiles/r03/fused_ab.md)
         const int64_t U1 = (int64_t)c->E_local * (c->f_local / 128);
         const bool want = c->fused_mode == 2 ||
-                          (c->fused_mode == 0 && !c->fp8 && !sp1 && !sp2 && nb1 <= 64 && U1 >= 3 * (int64_t)c->num_sms);
-        // FP8 weights: parity-tested (tuning fused=2) but slower than the two FP8 kernels:
-        // 0.2591-0.2657 vs 0.2291-0.2316 ms at the 64-token decode, ncu 254.9 us vs 152.0 + 80.7 us
-        // (DRAM 68.7 % vs 76 / 73 % of peak); its w1/w3 phase streams ~25 % slower than
-        // moe_gemm_fp8x_kernel's (profiles/r03/fused_ab.md) -- not understood yet
+                          (c->fused_mode == 0 && !sp1 && !sp2 && nb1 <= 64 && U1 >= 3 * (int64_t)c->num_sms);
+        // FP8 weights included since its w2 tiles run 128 rows x two K chunks per stage (one
+        // block-scaled MMA per K step, 32 KB of weights per stage): 0.2281-0.2334 vs 0.2350-0.2357
+        // ms for the two FP8 kernels, 3 of 3 rounds (256-row w2 tiles were slower: 0.255-0.261;
+        // profiles/r03/fused_ab.md)
         if (shape_ok && want) {
             const int64_t rows_needed = round_up(rows_total + (int64_t)c->E_local * (kSegAlign - 1), kSegAlign);
             const int wt = c->f_local / 128;
