@@ -293,6 +293,16 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             }
         }
     }
+    if (FP8 && p.g.spec_l2 > 0 && threadIdx.x == 160) {
+        // the same guess for the E4M3 W13 tiles: 128-byte K chunks of 32 KB (half the K chunks
+        // of the bf16 depth: a 256-row FP8 tile is 32 chunks)
+        const int wt = p.g.f / 128;
+        if ((int)blockIdx.x < p.g.E * wt) {
+            const int e = blockIdx.x / wt, m = blockIdx.x % wt;
+            const int nk = min(p.g.spec_l2 / 2, p.g.d / 128);
+            for (int kq = 0; kq < nk; ++kq) ptx::tma_prefetch_l2_4d(&tmW13, 0, 0, kq, m + e * wt);
+        }
+    }
     ptx::pdl_wait();
     MOE_TL(2, 1);
     if (threadIdx.x < 32) {

@@ -1459,6 +1459,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     // permute kernel triggers its dependents after its own griddepcontrol.wait). The
     // producer issues the first tile's weight stages before anything waits on the
     // previous kernel (PDL); its token loads and every other warp wait for it.
+    // p.spec_l2 > 0: the router / permute triggered this grid early (speculative mode of the
+    // fused FFN's forward), so the counts are not final before the wait: wait first, no
+    // pre-wait weight stages
+    const bool counts_late = p.spec_l2 > 0;
+    if (counts_late) ptx::pdl_wait();
     if (threadIdx.x < 32)
         for (int e = threadIdx.x; e < p.E; e += 32) {
             s_counts[e] = p.counts[e];
@@ -1466,7 +1471,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         }
     __syncwarp();
     int pre = 0;  // producer: weight stages of its first tile already issued
-    if (warp == 0 && lane == 0) {
+    if (warp == 0 && lane == 0 && !counts_late) {
         int total0 = 0;  // warp 0 wrote s_counts itself
         for (int e = 0; e < p.E; ++e) total0 += tiles_of<KIND, NB>(s_counts[e], p);
         if ((int)blockIdx.x < total0) {

@@ -740,6 +740,7 @@ moe_status run_swap_g1(moe_ctx* c, int nbi, const moe_expert_weights* w, cudaStr
     }
     if constexpr (NB >= 32 && NB <= 128)
         if (c->fp8) {  // h -> two E4M3 planes + block scales for the block-scaled w2 GEMM
+            p1.spec_l2 = c->spec_now ? c->spec_l2 : 0;  // early-triggered grid: counts after the wait
             p1.out = c->h8;
             p1.h_sf = c->h_sf;
             p1.plane_rows = c->cap;
@@ -1045,7 +1046,7 @@ moe_status run_gemms(moe_ctx* c, GemmPaths gp, int64_t rows_bound, int64_t rows_
             fp.g.hint_a = c->swap_w_hint;
             fp.g.w_tr = 256;
             fp.g.w_nt = c->w13_nt;
-            fp.g.spec_l2 = c->spec_now && !c->fp8 ? c->spec_l2 : 0;
+            fp.g.spec_l2 = c->spec_now ? c->spec_l2 : 0;
             if (c->fp8) {  // two E4M3 h planes + UE8M0 block scales (the FP8 w2 tiles' B operand)
                 // weights evict-first, as moe_gemm_fp8x_kernel: the 32-row token tile is below the
                 // 64-row bound, so the auto rule would pick evict-normal, and the weight stream then
@@ -2274,8 +2275,7 @@ moe_status forward_impl(moe_ctx* c, const void* tokens, int32_t T, const void* r
     r.dst_rows = c->gather_now ? nullptr : c->x_perm;
     r.src_row = c->gather_now ? c->src_row : nullptr;
     const GemmPaths gpaths = gemm_paths(c, (int64_t)T * c->k);
-    c->spec_now = c->spec_l2 > 0 && gpaths.swap1 && !c->fp8 && !c->gather_now &&
-                  T >= 16 && T <= 128 && !c->profiling;
+    c->spec_now = c->spec_l2 > 0 && gpaths.swap1 && !c->gather_now && T >= 16 && T <= 128 && !c->profiling;
     r.early = c->spec_now;
     moe_status s2 = route_and_permute(c, r, st);
     c->spec_now = c->spec_now && s2 == MOE_OK;
