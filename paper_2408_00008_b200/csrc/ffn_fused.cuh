@@ -49,6 +49,10 @@
 
 #include "gemm_sm100.cuh"
 
+#ifndef MOE_FUSED_BF16_G2_128
+#define MOE_FUSED_BF16_G2_128 0  // bf16 w2 tiles of 128 rows x two K blocks per stage (A/B knob)
+#endif
+
 namespace moe {
 
 struct FusedParams {
@@ -109,7 +113,8 @@ struct FusedCfg {
     // FP8: a w2 stage carries TWO K chunks of a 128-row W2 tile (2 x 16 KB weights, 2 x the hi/lo
     // h rows, 2 scale blocks) -- the same weight bytes per stage as a w1/w3 stage, whose single
     // 128-byte K chunk of 256 rows uses half of the B region
-    static constexpr int kBBytes = FP8 ? 2 * 2 * NB * 128 : (HALF ? 2 : 1) * NB * 128;  // token rows x 128 B (x 2 K blocks / terms)
+    static constexpr bool kG2Pair = FP8 || (MOE_FUSED_BF16_G2_128 && !HALF);  // w2: 128-row tiles, 2 K units / stage
+    static constexpr int kBBytes = FP8 ? 2 * 2 * NB * 128 : (HALF || kG2Pair ? 2 : 1) * NB * 128;  // token rows x 128 B (x 2 K blocks / terms)
     static constexpr int kSFBytes = FP8 ? 2 * 512 : 0;  // FP8 G2: the tile's B scale blocks of the stage's two K chunks
     static constexpr int kStageBytes = kABytes + kBBytes + kSFBytes;
     static constexpr int kXPitch = NB + 1;          // exchange row pitch in floats (bank-conflict free)
@@ -119,7 +124,7 @@ struct FusedCfg {
     static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
     static constexpr int kSmemBytes = kStages * kStageBytes + kXBytes + kSfaBytes + 2048;
     static constexpr int kAccStride = FP8 ? 4 * NB : 256;  // TMEM columns per accumulator stage
-    static constexpr int kG2Rows = FP8 ? 128 : 256;        // w2 tile rows (FP8: one block-scaled MMA per K step)
+    static constexpr int kG2Rows = kG2Pair ? 128 : 256;    // w2 tile rows (128: one MMA per K step)
     static constexpr uint32_t kSfaCol = 480, kSfbCol = 488;  // FP8 scale columns in TMEM
     static_assert(NB >= 16 && NB <= 128 && NB % 16 == 0, "fused tile: a/b accumulators of <= 128 columns");
     static_assert(!FP8 || (!HALF && NB == 32), "FP8 fused tiles: 32-row token tiles, 256-row w1/w3 tiles");
@@ -340,7 +345,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const int nchunk = p.combine_T > 0 ? (p.combine_T + p.comb_chunk - 1) / p.comb_chunk : 0;
     const int ncomb = (p.g.d / 256) * nchunk;
     const int total_all = total + ncomb;
-    const int slice_need = p.splits * (per_split / (p.g.d / C::kG2Rows));
+    // (each w2 tile row range of kG2Rows columns counts towards its 256-column slice)
+    const int slice_need = p.splits * (per_split / (p.g.d / C::kG2Rows)) * (256 / C::kG2Rows);
     const uint64_t w_hint = p.g.hint_a ? p.g.hint_a : ptx::kEvictFirst;
 
     if (warp == 0) {
@@ -436,6 +442,21 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                         }
                         if (++stage == SR) { stage = 0; phase ^= 1; }
                     }
+                } else if (C::kG2Pair && !ti.g1 && all_ready) {
+                    // bf16 w2: two K blocks of a 128-row W2 tile per stage (2 x 16 KB + 2 x NB h rows)
+                    for (int kb = 0; kb < ti.nkb; kb += 2) {
+                        ptx::mbar_wait(&empty[stage], phase ^ 1);
+                        ptx::mbar_arrive_expect_tx(&full[stage], 2 * (16384 + NB * 128));
+                        uint8_t* sa = smem_a + stage * C::kABytes;
+                        uint8_t* sb = smem_b + stage * C::kBBytes;
+#pragma unroll
+                        for (int u = 0; u < 2; ++u) {
+                            const int kq = ti.kb0 + kb + u;
+                            ptx::tma_load_4d(&tmW2, &full[stage], sa + u * 16384, 0, 0, kq, ti.m + ti.e * p.w2_nt, w_hint);
+                            ptx::tma_load_2d(&tmH, &full[stage], sb + u * NB * 128, kq * kBK, ti.b_row, ptx::kEvictLast);
+                        }
+                        if (++stage == SR) { stage = 0; phase ^= 1; }
+                    }
                 } else if (ti.g1 || all_ready) {
                     for (int kb = 0; kb < ti.nkb; ++kb) {
                         ptx::mbar_wait(&empty[stage], phase ^ 1);
@@ -483,7 +504,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                     const int st0 = stage;
                     int bq = 0;  // K blocks whose h load is issued
                     // K units of the stages: FP8 = pairs of K chunks (the last one may be single)
-                    const int nunits = FP8 ? (ti.nkb + 1) / 2 : ti.nkb;
+                    const int nunits = C::kG2Pair ? (ti.nkb + 1) / 2 : ti.nkb;
                     auto issue_b = [&](int q) {
                         const int sq = (st0 + q) % SR;
                         if (FP8) {
@@ -496,13 +517,18 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                                 ptx::bulk_load(smem_sf + sq * C::kSFBytes + u * 512,
                                                p.g.h_sf + ((int64_t)(ti.b_row / NB) * wt + kq) * 512, 512, &full[sq]);
                             }
+                        } else if (C::kG2Pair) {
+                            const int nc = min(2, ti.nkb - 2 * q);
+                            for (int u = 0; u < nc; ++u)
+                                ptx::tma_load_2d(&tmH, &full[sq], smem_b + sq * C::kBBytes + u * NB * 128,
+                                                 (ti.kb0 + 2 * q + u) * kBK, ti.b_row, ptx::kEvictLast);
                         } else {
                             ptx::tma_load_2d(&tmH, &full[sq], smem_b + sq * C::kBBytes, (ti.kb0 + q) * kBK, ti.b_row,
                                              ptx::kEvictLast);
                         }
                     };
                     auto unit_ok = [&](int q) {  // K unit q's h is ready
-                        return (FP8 ? min(2 * q + 2, ti.nkb) : q + 1) * fpq <= ok;
+                        return (C::kG2Pair ? min(2 * q + 2, ti.nkb) : q + 1) * fpq <= ok;
                     };
                     auto wait_ready = [&](int q) {
 #if MOE_TIMELINE
@@ -524,8 +550,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                             issue_b(bq++);
                         }
                         ptx::mbar_wait(&empty[stage], phase ^ 1);
-                        const int ncq = FP8 ? min(2, ti.nkb - 2 * q) : 1;
-                        ptx::mbar_arrive_expect_tx(&full[stage], FP8 ? ncq * (16384 + 2 * NB * 128 + 512) : C::kABytes + NB * 128);
+                        const int ncq = C::kG2Pair ? min(2, ti.nkb - 2 * q) : 1;
+                        ptx::mbar_arrive_expect_tx(&full[stage], FP8 ? ncq * (16384 + 2 * NB * 128 + 512)
+                                                                 : C::kG2Pair ? ncq * (16384 + NB * 128)
+                                                                              : C::kABytes + NB * 128);
                         uint8_t* sa = smem_a + stage * C::kABytes;
                         const int kq = ti.kb0 + q;
                         if (FP8) {
@@ -533,6 +561,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                             for (int u = 0; u < ncq; ++u)
                                 ptx::tma_load_4d(&tmW2, &full[stage], sa + u * 16384, 0, 0, ti.kb0 + 2 * q + u,
                                                  ti.m + ti.e * d128, w_hint);
+                        } else if (C::kG2Pair) {
+                            for (int u = 0; u < ncq; ++u)
+                                ptx::tma_load_4d(&tmW2, &full[stage], sa + u * 16384, 0, 0, ti.kb0 + 2 * q + u,
+                                                 ti.m + ti.e * p.w2_nt, w_hint);
                         } else {
                             ptx::tma_load_4d(&tmW2, &full[stage], sa, 0, 0, kq, 2 * ti.m + ti.e * p.w2_nt, w_hint);
                         }
@@ -576,8 +608,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 ptx::mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
                 ptx::tc_fence_after();
                 const bool half_g1 = HALF && ti.g1;
-                const bool fp8_g2 = FP8 && !ti.g1;  // two K chunks per stage
-                for (int kb = 0; kb < ti.nkb; kb += (half_g1 || fp8_g2) ? 2 : 1) {
+                const bool pair_g2 = C::kG2Pair && !ti.g1;  // two K units per stage
+                for (int kb = 0; kb < ti.nkb; kb += (half_g1 || pair_g2) ? 2 : 1) {
                     ptx::mbar_wait(&full[stage], phase);
                     ptx::tc_fence_after();
                     const uint32_t sa = ptx::smem_u32(smem_a + stage * C::kABytes);
@@ -610,6 +642,17 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                                     const uint32_t idmx = ptx::make_idesc_mx_e4m3(128, N2, kk, kk);
                                     ptx::mma_mx_e4m3(d_tmem, au + 2 * kk, bu + 2 * kk, idmx, acc_in, sfa | sel, sfb | sel);
                                 }
+                            }
+                        }
+                    } else if (pair_g2) {
+                        const int nc = min(2, ti.nkb - kb);
+                        for (int u = 0; u < nc; ++u) {
+                            const uint64_t adesc = ptx::make_smem_desc_sw128(sa + u * 16384);
+                            const uint64_t bdesc = ptx::make_smem_desc_sw128(sb + u * NB * 128);
+#pragma unroll
+                            for (int kk = 0; kk < kBK / 16; ++kk) {
+                                const uint32_t accum = (kb | u | kk) ? 1u : 0u;
+                                ptx::mma_bf16(d_tmem, adesc + 2 * kk, bdesc + 2 * kk, idesc, accum);
                             }
                         }
                     } else if (half_g1) {
@@ -842,10 +885,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 }
                 fence_proxy_async_global();  // this thread's h stores -> visible to TMA readers
             } else {
-                // rows 256 m + r (first MMA) and 256 m + 128 + r (second)
+                // rows 256 m + r (first MMA) and 256 m + 128 + r (second); 128-row tiles: 128 m + r
                 const bool chained = p.chain != nullptr;
                 float* y = p.y + (chained ? 0 : p.y_split_stride * ti.s) + static_cast<int64_t>(ti.b_row) * p.g.d +
-                           ti.m * 256 + r;
+                           ti.m * C::kG2Rows + r;
                 const bool add = chained && ti.s > 0;
                 if (add) {  // split s-1 of this output tile stored (acquire), then y += acc
                     if (lane == 0) {
@@ -858,7 +901,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 for (int c = 0; c < nchunks; ++c) {
                     uint32_t v0[16], v1[16];
                     ptx::tmem_ld16(tbase + c * 16, v0);
-                    ptx::tmem_ld16(tbase + 128 + c * 16, v1);
+                    if (C::kG2Rows == 256) ptx::tmem_ld16(tbase + 128 + c * 16, v1);
                     ptx::tmem_wait_ld();
 #pragma unroll
                     for (int i = 0; i < 16; ++i) {
@@ -867,10 +910,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                             float* yn = y + static_cast<int64_t>(n) * p.g.d;
                             if (add) {
                                 yn[0] = __ldcg(yn) + __uint_as_float(v0[i]);
-                                yn[128] = __ldcg(yn + 128) + __uint_as_float(v1[i]);
+                                if (C::kG2Rows == 256) yn[128] = __ldcg(yn + 128) + __uint_as_float(v1[i]);
                             } else {
                                 yn[0] = __uint_as_float(v0[i]);
-                                yn[128] = __uint_as_float(v1[i]);
+                                if (C::kG2Rows == 256) yn[128] = __uint_as_float(v1[i]);
                             }
                         }
                     }
@@ -887,7 +930,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 if (warp == 2 && lane == 0) {
                     __threadfence();
                     if (p.chain) atomicExch(p.chain + ti.pidx, ti.s + 1);
-                    if (p.combine_T > 0) atomicAdd(p.arrive + ti.m, 1);
+                    if (p.combine_T > 0) atomicAdd(p.arrive + ti.m * C::kG2Rows / 256, 1);
                 }
             }
             if (ti.g1) {

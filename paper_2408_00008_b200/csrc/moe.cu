@@ -1075,7 +1075,8 @@ moe_status run_gemms(moe_ctx* c, GemmPaths gp, int64_t rows_bound, int64_t rows_
             {
                 int64_t nt_sum = c->E_local;
                 nt_sum += (rows_total + nb1 - 1) / nb1;
-                if (c->fused_chain_mode == 1 && !c->fp8 && S > 1 && nt_sum * (c->d / 256) <= c->fused_chain_n)
+                if (c->fused_chain_mode == 1 && !c->fp8 && !MOE_FUSED_BF16_G2_128 && S > 1 &&
+                    nt_sum * (c->d / 256) <= c->fused_chain_n)
                     fp.chain = c->fused_chain;
             }
             const bool comb = c->fcomb.on && c->d / 256 <= grid;  // every combine task claimed by some CTA
@@ -1115,7 +1116,7 @@ moe_status run_gemms(moe_ctx* c, GemmPaths gp, int64_t rows_bound, int64_t rows_
             const CUtensorMap& tw = half ? c->tm_w13_h : c->tm_w13;
             auto go = [&](auto kern, size_t smem) {
                 return launch(c, kSlotGemm1, kern, dim3(grid), dim3(kGemmThreads), smem, st, fp, tw, c->tm_x_swap[i],
-                              c->tm_w2_tiled, c->tm_h_swap[i]);
+                              (MOE_FUSED_BF16_G2_128 && !half) ? c->tm_w2_swap : c->tm_w2_tiled, c->tm_h_swap[i]);
             };
             if (c->fp8)
                 s = launch(c, kSlotGemm1, moe_ffn_fused_kernel<32, false, true>, dim3(grid), dim3(kGemmThreads),

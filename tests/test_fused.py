@@ -285,6 +285,28 @@ def test_fused_fp8(moe, T, d, f, E):
     assert np.array_equal(outs[0].view(np.int32), outs[1].view(np.int32))
 
 
+@pytest.mark.parametrize("T,residual", [(64, False), (37, True)])
+def test_fused_fp8_combine_bit_identical(moe, T, residual):
+    """FP8 fused FFN with the in-kernel combine: its w2 tiles are 128 rows, two per 256-column
+    combine slice, so a slice's combine task must wait for both (arrive[m * 128 / 256]);
+    bit-identical to the combine kernel after the same fused FFN, and oracle parity."""
+    shape = synth.MoEShape(T=T, d=512, f=1024, E=8, k=2)
+    inp, qs, host = _fp8_block_inputs(shape, 7800 + T)
+    flags = moe.MOE_FLAG_FP8_WEIGHTS | (moe.MOE_FLAG_RESIDUAL if residual else 0)
+    res = []
+    for fc in (1, 0):
+        blk = moe.MoEBlock(inp["wg"], qs["w1"], qs["w3"], qs["w2"], top_k=2, max_tokens=T, flags=flags,
+                           split_k=4, tuning={"fused": 2, "fused_combine": fc})
+        run = GpuRun(blk, inp["x"])
+        if not residual:
+            check_forward(run, host, 2)
+        assert _launches(moe, blk, inp["x"]) == (3 if fc == 1 else 4)
+        res.append((run.np("out_f32").copy(), run.out.clone()))
+        blk.close()
+    assert np.array_equal(res[0][0].view(np.int32), res[1][0].view(np.int32))
+    assert torch.equal(res[0][1].view(torch.int16), res[1][1].view(torch.int16))
+
+
 def test_fused_fp8_mixtral(moe):
     """FP8 Mixtral-size 64-token decode: the fused FFN (uniform 4 splits) bit-identical to the
     two-kernel FP8 path, and oracle parity on sampled tokens (exact-dequant weights); the default
