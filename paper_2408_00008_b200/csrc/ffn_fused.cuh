@@ -373,7 +373,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 s_tile[ts] = t;
                 ptx::mbar_arrive(&tile_full[ts]);
                 if (++ts == R) { ts = 0; tph ^= 1; }
-#if MOE_TIMELINE
+#if MOE_TIMELINE && !MOE_TL_TEARDOWN
                 if (blockIdx.x < ptx::kTlBlocks) {
                     if (t >= total_all) {
                         ptx::g_moe_tl[3][1][blockIdx.x] = ptx::tl_now();
@@ -952,7 +952,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     ptx::pdl_launch_dependents();
     ptx::tc_fence_before();
     __syncthreads();
+#if !MOE_TL_LATE_EXIT
     MOE_TL(2, 2);
+#endif
     if (warp == 1) {
         ptx::tc_fence_after();
         ptx::tmem_dealloc(tmem_base, 512);
@@ -960,13 +962,24 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     // last CTA out resets the claim / exit counters and the ready counters
     if (threadIdx.x == 0) {
         __threadfence();
+#if MOE_TL_TEARDOWN
+        ptx::g_moe_tl[3][0][blockIdx.x] = ptx::tl_now();
+#endif
         *s_last = atomicAdd(&p.sched[1], 1) == (int)gridDim.x - 1;
+#if MOE_TL_TEARDOWN
+        ptx::g_moe_tl[3][1][blockIdx.x] = ptx::tl_now();
+#endif
     }
     __syncthreads();
+#if MOE_TL_TEARDOWN
+    if (threadIdx.x == 0) ptx::g_moe_tl[3][2][blockIdx.x] = ptx::tl_now();
+#endif
     if (*s_last) {
         __threadfence();
-        const int nready = p.g.E * wq;
-        for (int i = threadIdx.x; i < nready; i += blockDim.x) p.ready[i] = 0;
+        const int nready = p.g.E * wq;  // 16-byte stores (cudaMalloc'd, 16-B aligned) + a tail
+        for (int i = threadIdx.x; i < nready / 4; i += blockDim.x)
+            reinterpret_cast<int4*>(p.ready)[i] = make_int4(0, 0, 0, 0);
+        if (threadIdx.x < (nready & 3)) p.ready[(nready & ~3) + threadIdx.x] = 0;
         if (p.combine_T > 0)
             for (int i = threadIdx.x; i < p.g.d / 256; i += blockDim.x) p.arrive[i] = 0;
         if (p.chain)
@@ -978,6 +991,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             p.sched[3] = 0;
         }
     }
+#if MOE_TL_LATE_EXIT
+    MOE_TL(2, 2);  // probe: exit stamp after the counter hand-off (every CTA)
+#endif
 }
 
 }  // namespace moe

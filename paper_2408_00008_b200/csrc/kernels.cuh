@@ -482,9 +482,14 @@ __global__ void __launch_bounds__(256) moe_router_mma_kernel(const RouteParams p
         s_idx[tb][1] = i1;
     }
     __syncthreads();
+#if !MOE_TL_LATE_EXIT
     MOE_TL(0, 2);
+#endif
     route_block_finish<256>(p, s_idx, ntok, tok0);
     if (p.scan_epoch) route_fold_dispatch<256, TOK>(p, s_idx, ntok, tok0, ep0);
+#if MOE_TL_LATE_EXIT
+    MOE_TL(0, 2);  // probe: exit stamp after the histogram / scan hand-off
+#endif
 }
 
 struct PermuteParams {

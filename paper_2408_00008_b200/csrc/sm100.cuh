@@ -427,6 +427,12 @@ __device__ __forceinline__ void mma_commit_pair(uint64_t* bar, uint16_t mask) {
 #ifndef MOE_TIMELINE
 #define MOE_TIMELINE 0
 #endif
+#ifndef MOE_TL_LATE_EXIT
+#define MOE_TL_LATE_EXIT 0  // probe: router / fused FFN exit stamps after their hand-off code
+#endif
+#ifndef MOE_TL_TEARDOWN
+#define MOE_TL_TEARDOWN 0  // probe: fused FFN slot 3 = [after exit fence, after exit atomic, after barrier]
+#endif
 #if MOE_TIMELINE
 constexpr int kTlBlocks = 4096;
 __device__ unsigned long long g_moe_tl[5][3][kTlBlocks];

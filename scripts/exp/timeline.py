@@ -111,6 +111,17 @@ def main():
         if name in ("gemm1", "gemm2") and x_.size:
             q = np.percentile(x_, [0, 10, 50, 90, 100])
             print(f"         exit percentiles 0/10/50/90/100: " + " ".join(f"{v:.1f}" for v in q))
+    if "--teardown" in sys.argv:  # MOE_TL_TEARDOWN build: slot 3 = fused FFN exit hand-off stamps
+        a, b, c = tl[3]
+        x = tl[2][2]
+        m = (a > 0) & (x > 0)
+        last = np.argmax(np.where(m, x, 0))
+        us = lambda v: (v - t0) / 1000.0  # noqa: E731
+        print(f"fused exit hand-off, last CTA {last}: fence done {us(a[last]):.1f}, atomic back {us(b[last]):.1f}, "
+              f"barrier {us(c[last]):.1f}, exit {us(x[last]):.1f}")
+        for lbl, v in (("fence->atomic", b - a), ("atomic->barrier", c - b), ("barrier->exit", x - c)):
+            q = np.percentile(v[m] / 1000.0, [50, 90, 100])
+            print(f"  {lbl:16s} p50/p90/max us {q[0]:.2f}/{q[1]:.2f}/{q[2]:.2f}")
     blk.close()
 
 
