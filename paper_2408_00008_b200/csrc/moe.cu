@@ -671,6 +671,8 @@ moe_status validate_cfg(const moe_config* cfg, moe_ctx* c) {
             return fail(c, MOE_ERR_INVALID, "tuning.fused_chain must be 0 or 1");
         if (tu->fused_combine < 0 || tu->fused_combine > 1)
             return fail(c, MOE_ERR_INVALID, "tuning.fused_combine must be 0 or 1");
+        if (tu->fused_uniform < 0 || tu->fused_uniform > 3)
+            return fail(c, MOE_ERR_INVALID, "tuning.fused_uniform must be 0..3");
         if (tu->fused_stages < 0 || tu->fused_stages > 8)
             return fail(c, MOE_ERR_INVALID, "tuning.fused_stages must be in [0, 8]");
         if (tu->weight_hint < 0 || tu->weight_hint > 3) return fail(c, MOE_ERR_INVALID, "tuning.weight_hint must be 0..3");
@@ -1093,17 +1095,26 @@ moe_status run_gemms(moe_ctx* c, GemmPaths gp, int64_t rows_bound, int64_t rows_
                 const int per_slice = std::max(1, grid / (c->d / 256));
                 fp.comb_chunk = (c->fcomb.T + per_slice - 1) / per_slice;
             }
-            // split boundaries in ffn tiles: uniform (tuning fused_uniform: the two-kernel path's
-            // split of whole tiles) or tapered, split i weighted S - i (4 splits: 0.4 / 0.3 / 0.2 / 0.1
-            // of K), so the stream ends on the shortest w2 tiles
+            // split boundaries in ffn tiles: uniform (tuning fused_uniform 1: the two-kernel path's
+            // split of whole tiles) or tapered so the stream ends on the shortest w2 tiles: split i
+            // weighted 2^(S-1-i) (4 splits: 8/15, 4/15, 2/15, 1/15 of K), S - i (fused_uniform 2) or
+            // (S-i)^2 (3); default (0): geometric for bf16, linear for FP8. 64-token decode: 0.4052-
+            // 0.4054 ms geometric vs 0.4063-0.4071 linear vs 0.4065-0.4070 quadratic (4 of 4
+            // interleaved rounds); FP8: 0.2250 linear vs 0.2255-0.2268 geometric (3 of 3;
+            // profiles/r03/fused_ab.md)
             {
+                const int mode = c->fused_uniform ? c->fused_uniform : c->fp8 ? 2 : 0;
+                auto weight = [&](int i) -> int64_t {
+                    return mode == 1 ? 1 : mode == 2 ? S - i : mode == 3 ? (int64_t)(S - i) * (S - i)
+                                                                         : (int64_t)1 << (S - 1 - i);
+                };
                 int64_t wsum = 0, acc = 0;
-                for (int i = 0; i < S; ++i) wsum += c->fused_uniform ? 1 : S - i;
+                for (int i = 0; i < S; ++i) wsum += weight(i);
                 fp.split_j[0] = 0;
                 for (int i = 0; i < S; ++i) {
-                    acc += c->fused_uniform ? 1 : S - i;
+                    acc += weight(i);
                     int j = (int)((wt * acc + wsum / 2) / wsum);
-                    if (c->fused_uniform) j = (int)(wt * acc / wsum);
+                    if (mode == 1) j = (int)(wt * acc / wsum);
                     fp.split_j[i + 1] = std::max(fp.split_j[i] + 1, std::min(j, wt - (S - 1 - i)));
                 }
                 fp.split_j[S] = wt;
