@@ -147,7 +147,8 @@ typedef struct moe_tuning {
     int32_t fused_stages;   /* pipeline stages of the fused kernel, 2..8 (0: all that fit)     */
     int32_t fused_uniform;  /* 1: equal w2 K splits in whole ffn tiles (the two-kernel path's split,
                                bit-identical results); 0: tapered splits, the last ones shortest
-                               (split i weighted 2^(S-1-i), FP8 weights: S-i); 2: weighted S-i;
+                               (split i weighted 2^(S-1-i) where one split's w2 tiles cover half
+                               the grid, else and for FP8 weights S-i); 2: weighted S-i;
                                3: weighted (S-i)^2                                              */
     int32_t fused_combine;  /* 1: single-GPU forwards of <= 256 tokens run step a9 inside the fused
                                FFN (combine tasks after the last w2 tiles; bit-identical); 0: the

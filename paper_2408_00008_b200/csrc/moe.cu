@@ -1098,12 +1098,15 @@ moe_status run_gemms(moe_ctx* c, GemmPaths gp, int64_t rows_bound, int64_t rows_
             // split boundaries in ffn tiles: uniform (tuning fused_uniform 1: the two-kernel path's
             // split of whole tiles) or tapered so the stream ends on the shortest w2 tiles: split i
             // weighted 2^(S-1-i) (4 splits: 8/15, 4/15, 2/15, 1/15 of K), S - i (fused_uniform 2) or
-            // (S-i)^2 (3); default (0): geometric for bf16, linear for FP8. 64-token decode: 0.4052-
-            // 0.4054 ms geometric vs 0.4063-0.4071 linear vs 0.4065-0.4070 quadratic (4 of 4
-            // interleaved rounds); FP8: 0.2250 linear vs 0.2255-0.2268 geometric (3 of 3;
-            // profiles/r03/fused_ab.md)
+            // (S-i)^2 (3); default (0): geometric for bf16 where one split's w2 tiles (at least
+            // E_local * d/256) cover half the grid, else linear -- with few tiles per split the
+            // first split's long tiles run on a few CTAs (EP8 rank, forced fused: 99.7 vs 73 us).
+            // 64-token decode: 0.4052-0.4054 ms geometric vs 0.4063-0.4071 linear vs 0.4065-0.4070
+            // quadratic (4 of 4 interleaved rounds); FP8: 0.2250 linear vs 0.2255-0.2268 geometric
+            // (3 of 3; profiles/r03/fused_ab.md)
             {
-                const int mode = c->fused_uniform ? c->fused_uniform : c->fp8 ? 2 : 0;
+                const bool geo = !c->fp8 && 2LL * c->E_local * (c->d / 256) >= grid;
+                const int mode = c->fused_uniform ? c->fused_uniform : geo ? 0 : 2;
                 auto weight = [&](int i) -> int64_t {
                     return mode == 1 ? 1 : mode == 2 ? S - i : mode == 3 ? (int64_t)(S - i) * (S - i)
                                                                          : (int64_t)1 << (S - 1 - i);
