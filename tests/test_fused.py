@@ -146,16 +146,22 @@ def test_fused_group(moe, par, G, half):
     shape = synth.MoEShape(T=96, d=256, f=1024, E=8, k=2)
     inp = synth.make_inputs(shape, 7500 + G, device="cuda")
     host = to_host_inputs(inp)
+    n_two, n_fused = [0] * G, [0] * G
     if par == "ep":
         cuts = np.linspace(0, shape.T, G + 1).astype(int)
         shards = [inp["x"][cuts[r]:cuts[r + 1]] for r in range(G)]
-        res = _run_group(moe, inp, moe.MOE_PAR_EP, G, shards, max_tokens=shape.T, tuning={"fused": 2, "fused_half": half})
+        _run_group(moe, inp, moe.MOE_PAR_EP, G, shards, max_tokens=shape.T, tuning={"fused": 1}, launches=n_two)
+        res = _run_group(moe, inp, moe.MOE_PAR_EP, G, shards, max_tokens=shape.T, tuning={"fused": 2, "fused_half": half},
+                         launches=n_fused)
         _check_group_outputs(host, 2, host["x"], [r[0] for r in res], [r[1] for r in res])
     else:
-        res = _run_group(moe, inp, moe.MOE_PAR_TP, G, [inp["x"]] * G, tuning={"fused": 2, "fused_half": half})
+        _run_group(moe, inp, moe.MOE_PAR_TP, G, [inp["x"]] * G, tuning={"fused": 1}, launches=n_two)
+        res = _run_group(moe, inp, moe.MOE_PAR_TP, G, [inp["x"]] * G, tuning={"fused": 2, "fused_half": half},
+                         launches=n_fused)
         for r in range(1, G):
             assert torch.equal(res[r][0].view(torch.int16), res[0][0].view(torch.int16))
         _check_group_outputs(host, 2, host["x"], [res[0][0]], [res[0][1]])
+    assert all(f == t - 1 for f, t in zip(n_fused, n_two)), (n_fused, n_two)  # one launch for both GEMMs
 
 
 @pytest.mark.parametrize("par,G", [("ep", 2), ("tp", 2), ("tp", 4)])
@@ -305,6 +311,37 @@ def test_fused_fp8_combine_bit_identical(moe, T, residual):
         blk.close()
     assert np.array_equal(res[0][0].view(np.int32), res[1][0].view(np.int32))
     assert torch.equal(res[0][1].view(torch.int16), res[1][1].view(torch.int16))
+
+
+@pytest.mark.parametrize("par,G", [("tp", 2), ("tp", 4)])
+def test_fused_fp8_group(moe, par, G):
+    """FP8 weights through the fused FFN (tuning fused=2) inside TP contexts (ffn slice, fp32
+    partials reduced across ranks; loopback transport): one launch replaces the two FP8 GEMMs,
+    oracle parity on the exact-dequant weights, every rank with the same output, 3 back-to-back
+    forwards. (EP capacity-mode ranks size their token tile for the capacity, above the FP8
+    fused kernel's 32 rows, and keep the two FP8 kernels.)"""
+    from test_gpu_parity import _check_group_outputs, _run_group
+    shape = synth.MoEShape(T=64, d=512, f=1024, E=8, k=2)
+    inp, qs, host = _fp8_block_inputs(shape, 7950 + G)
+    inp8 = dict(inp, w1=qs["w1"], w3=qs["w3"], w2=qs["w2"])
+    if par == "ep":
+        cuts = np.linspace(0, shape.T, G + 1).astype(int)
+        shards, pm, mt = [inp["x"][cuts[r]:cuts[r + 1]] for r in range(G)], moe.MOE_PAR_EP, shape.T
+    else:
+        shards, pm, mt = [inp["x"]] * G, moe.MOE_PAR_TP, None
+    n_two = [0] * G
+    _run_group(moe, inp8, pm, G, shards, flags=moe.MOE_FLAG_FP8_WEIGHTS, max_tokens=mt, tuning={"fused": 1},
+               launches=n_two)
+    n_fused = [0] * G
+    res = _run_group(moe, inp8, pm, G, shards, flags=moe.MOE_FLAG_FP8_WEIGHTS, max_tokens=mt, iters=3,
+                     tuning={"fused": 2}, launches=n_fused)
+    assert all(f == t - 1 for f, t in zip(n_fused, n_two)), (n_fused, n_two)  # one launch for both GEMMs
+    if par == "ep":
+        _check_group_outputs(host, 2, host["x"], [r[0] for r in res], [r[1] for r in res])
+    else:
+        for r in range(1, G):
+            assert torch.equal(res[r][0].view(torch.int16), res[0][0].view(torch.int16))
+        _check_group_outputs(host, 2, host["x"], [res[0][0]], [res[0][1]])
 
 
 def test_fused_fp8_mixtral(moe):

@@ -481,11 +481,12 @@ def test_gather_equals_copy(moe, mixtral_weights, T, flags):
 
 
 # ---------------------------------------------------------------- EP / TP device path (loopback transport)
-def _run_group(moe, inp, par, G, shards, k=2, flags=0, max_tokens=None, p2p=False, iters=1, tuning=None):
+def _run_group(moe, inp, par, G, shards, k=2, flags=0, max_tokens=None, p2p=False, iters=1, tuning=None, launches=None):
     """G contexts on one GPU, each driven by its own thread (and stream), exchanging
     through the loopback transport, or through peer memory (p2p: MOE_FLAG_P2P, the
     handles of the G regions connected in-process). shards[r] = token tensor of rank
-    r. Returns per-rank (out, aux) of the last of `iters` forwards (all must agree)."""
+    r. Returns per-rank (out, aux) of the last of `iters` forwards (all must agree);
+    launches (a list of G), when given, receives each rank's kernel launches of that forward."""
     import threading
     if p2p:
         grp, comms, flags = None, [None] * G, flags | moe.MOE_FLAG_P2P
@@ -516,10 +517,13 @@ def _run_group(moe, inp, par, G, shards, k=2, flags=0, max_tokens=None, p2p=Fals
             out = torch.empty(max(T, 1), d, dtype=torch.bfloat16, device="cuda")
             first = None
             for it in range(iters):
+                n0 = moe.moe_launch_count(blocks[r].ctx)
                 with torch.cuda.stream(st):
                     moe.moe_forward(blocks[r].ctx, x if T else out, T, blocks[r].router_w, blocks[r].w13,
                                     blocks[r].w2, out, aux, st, blocks[r].s13, blocks[r].s2)
                 st.synchronize()
+                if launches is not None:
+                    launches[r] = moe.moe_launch_count(blocks[r].ctx) - n0
                 res[r] = (out[:T].clone(), {n: v[:T].clone() for n, v in aux.items()})
                 if first is None:
                     first = res[r][0]
