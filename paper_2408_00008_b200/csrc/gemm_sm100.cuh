@@ -243,7 +243,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
     const int warp = threadIdx.x / 32;
     const int lane = threadIdx.x % 32;
-    constexpr int kTlSlot = C::kG1 ? 2 : 3;
+    [[maybe_unused]] constexpr int kTlSlot = C::kG1 ? 2 : 3;
     MOE_TL(kTlSlot, 0);
 
     if (warp == 0 && lane == 0) {
@@ -1144,7 +1144,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const int lane = threadIdx.x % 32;
     const uint32_t crank = ptx::cluster_ctarank();
     const bool leader = crank == 0;
-    constexpr int kTlSlot = C::kG1 ? 2 : 3;
+    [[maybe_unused]] constexpr int kTlSlot = C::kG1 ? 2 : 3;
     MOE_TL(kTlSlot, 0);
 
     if (warp == 0 && lane == 0) {
