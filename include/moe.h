@@ -149,7 +149,7 @@ typedef struct moe_tuning {
                                bit-identical results); 0: tapered splits, the last ones shortest
                                (split i weighted 2^(S-1-i) where one split's w2 tiles cover half
                                the grid, else and for FP8 weights S-i); 2: weighted S-i;
-                               3: weighted (S-i)^2                                              */
+                               3: weighted (S-i)^2; 4: weighted 2^(S-1-i)                       */
     int32_t fused_combine;  /* 1: single-GPU forwards of <= 256 tokens run step a9 inside the fused
                                FFN (combine tasks after the last w2 tiles; bit-identical); 0: the
                                combine kernel runs after it (default: faster under graph replay) */

@@ -671,8 +671,8 @@ moe_status validate_cfg(const moe_config* cfg, moe_ctx* c) {
             return fail(c, MOE_ERR_INVALID, "tuning.fused_chain must be 0 or 1");
         if (tu->fused_combine < 0 || tu->fused_combine > 1)
             return fail(c, MOE_ERR_INVALID, "tuning.fused_combine must be 0 or 1");
-        if (tu->fused_uniform < 0 || tu->fused_uniform > 3)
-            return fail(c, MOE_ERR_INVALID, "tuning.fused_uniform must be 0..3");
+        if (tu->fused_uniform < 0 || tu->fused_uniform > 4)
+            return fail(c, MOE_ERR_INVALID, "tuning.fused_uniform must be 0..4");
         if (tu->fused_stages < 0 || tu->fused_stages > 8)
             return fail(c, MOE_ERR_INVALID, "tuning.fused_stages must be in [0, 8]");
         if (tu->weight_hint < 0 || tu->weight_hint > 3) return fail(c, MOE_ERR_INVALID, "tuning.weight_hint must be 0..3");
@@ -1097,8 +1097,8 @@ moe_status run_gemms(moe_ctx* c, GemmPaths gp, int64_t rows_bound, int64_t rows_
             }
             // split boundaries in ffn tiles: uniform (tuning fused_uniform 1: the two-kernel path's
             // split of whole tiles) or tapered so the stream ends on the shortest w2 tiles: split i
-            // weighted 2^(S-1-i) (4 splits: 8/15, 4/15, 2/15, 1/15 of K), S - i (fused_uniform 2) or
-            // (S-i)^2 (3); default (0): geometric for bf16 where one split's w2 tiles (at least
+            // weighted 2^(S-1-i) (fused_uniform 4; 4 splits: 8/15, 4/15, 2/15, 1/15 of K), S - i (2)
+            // or (S-i)^2 (3); default (0): geometric for bf16 where one split's w2 tiles (at least
             // E_local * d/256) cover half the grid, else linear -- with few tiles per split the
             // first split's long tiles run on a few CTAs (EP8 rank, forced fused: 99.7 vs 73 us).
             // 64-token decode: 0.4052-0.4054 ms geometric vs 0.4063-0.4071 linear vs 0.4065-0.4070
@@ -1106,7 +1106,7 @@ moe_status run_gemms(moe_ctx* c, GemmPaths gp, int64_t rows_bound, int64_t rows_
             // (3 of 3; profiles/r03/fused_ab.md)
             {
                 const bool geo = !c->fp8 && 2LL * c->E_local * (c->d / 256) >= grid;
-                const int mode = c->fused_uniform ? c->fused_uniform : geo ? 0 : 2;
+                const int mode = c->fused_uniform ? c->fused_uniform : geo ? 4 : 2;
                 auto weight = [&](int i) -> int64_t {
                     return mode == 1 ? 1 : mode == 2 ? S - i : mode == 3 ? (int64_t)(S - i) * (S - i)
                                                                          : (int64_t)1 << (S - 1 - i);

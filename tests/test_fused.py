@@ -43,7 +43,7 @@ def _launches(moe, blk, x):
 
 
 @pytest.mark.parametrize("half", [1, 2])
-@pytest.mark.parametrize("uniform,chain", [(0, 0), (1, 0), (0, 1), (1, 1)])
+@pytest.mark.parametrize("uniform,chain", [(0, 0), (1, 0), (0, 1), (1, 1), (4, 0), (2, 0)])
 @pytest.mark.parametrize("T,d,f,E,k,splits", [
     (64, 512, 1024, 8, 2, 0),    # decode-like: one token tile per expert (NB 64), auto splits
     (1, 256, 512, 4, 2, 1),      # one token: 2 experts used, 2 empty
@@ -56,7 +56,8 @@ def _launches(moe, blk, x):
     (48, 256, 2048, 8, 2, 8),    # 16 ffn tiles over 8 tapered splits (8 partial buffers)
 ])
 def test_fused_parity(moe, T, d, f, E, k, splits, uniform, chain, half):
-    """Tapered (default) and uniform w2 K splits, incl. more splits than ffn tiles allow;
+    """Tapered (default: geometric or linear by shape; 4 / 2 forced), uniform and chained w2 K
+    splits, incl. more splits than ffn tiles allow;
     256-row w1/w3 tiles (fused_half 1) and 128-row ones (2: 64 w1 + 64 w3 rows, a/b paired
     through shared memory)."""
     shape = synth.MoEShape(T=T, d=d, f=f, E=E, k=k)
