@@ -151,8 +151,9 @@ typedef struct moe_tuning {
                                the grid, else and for FP8 weights S-i); 2: weighted S-i;
                                3: weighted (S-i)^2; 4: weighted 2^(S-1-i)                       */
     int32_t fused_combine;  /* 1: single-GPU forwards of <= 256 tokens run step a9 inside the fused
-                               FFN (combine tasks after the last w2 tiles; bit-identical); 0: the
-                               combine kernel runs after it (default: faster under graph replay) */
+                               FFN (combine tasks after the last w2 tiles; bit-identical); 2: the
+                               combine kernel runs after it (faster into device memory); 0 (auto):
+                               in-kernel where moe_forward_host writes mapped host memory, else 2 */
     int32_t fused_chain;    /* 1: the fused FFN's w2 tile of split s adds into buffer 0 after split
                                s-1 of the same output tile stored (same sums, same order; the
                                combine reads one partial); 0: S partial buffers the combine adds */

@@ -332,7 +332,8 @@ struct moe_ctx {
         float* out_f32 = nullptr;
     } fcomb;
     bool fcomb_done = false;
-    int fused_combine_mode = 0;
+    int fused_combine_mode = 0;  // tuning.fused_combine: 0 auto (host output), 1 always, 2 never
+    bool host_out_now = false;   // moe_forward_host: this forward's output is mapped host memory
     CUtensorMap tm_src{};        // gather map over the current call's tokens [T, d], box {64, 1}
     float* y = nullptr;
     int64_t y_elems = 0;
@@ -669,8 +670,8 @@ moe_status validate_cfg(const moe_config* cfg, moe_ctx* c) {
             return fail(c, MOE_ERR_INVALID, "tuning.fused_half must be 0, 1 or 2");
         if (tu->fused_chain < 0 || tu->fused_chain > 1)
             return fail(c, MOE_ERR_INVALID, "tuning.fused_chain must be 0 or 1");
-        if (tu->fused_combine < 0 || tu->fused_combine > 1)
-            return fail(c, MOE_ERR_INVALID, "tuning.fused_combine must be 0 or 1");
+        if (tu->fused_combine < 0 || tu->fused_combine > 2)
+            return fail(c, MOE_ERR_INVALID, "tuning.fused_combine must be 0, 1 or 2");
         if (tu->fused_uniform < 0 || tu->fused_uniform > 4)
             return fail(c, MOE_ERR_INVALID, "tuning.fused_uniform must be 0..4");
         if (tu->fused_stages < 0 || tu->fused_stages > 8)
@@ -2057,7 +2058,10 @@ moe_status moe_forward_host(moe_ctx* c, const void* tokens_host, int32_t T, cons
             out_dev = pa.devicePointer;
         cudaGetLastError();  // pageable memory: not an error
     }
-    if ((s = moe_forward(c, in, T, router_w, w, out_dev ? out_dev : c->stage_out, nullptr, stream))) return s;
+    c->host_out_now = out_dev != nullptr;
+    s = moe_forward(c, in, T, router_w, w, out_dev ? out_dev : c->stage_out, nullptr, stream);
+    c->host_out_now = false;
+    if (s) return s;
     if (T > 0) {
         CUDA_TRY(c, cudaEventRecord(c->slot_free[slot], st));
         if (!out_dev) CUDA_TRY(c, cudaMemcpyAsync(out_host, c->stage_out, bytes, cudaMemcpyDeviceToHost, st));
@@ -2297,13 +2301,17 @@ moe_status forward_impl(moe_ctx* c, const void* tokens, int32_t T, const void* r
     if ((s = s2)) return s;
     int splits = 1;
     const bool residual = (c->cfg.flags & MOE_FLAG_RESIDUAL) != 0;
-    // in-kernel combine by the fused FFN (tuning.fused_combine = 1; single GPU, one combine task
-    // per CTA). Off by default: graph-replayed 64-token decode 0.4066-0.4073 ms with it vs
-    // 0.4029-0.4036 ms with the combine kernel after the fused FFN (3 of 3 interleaved rounds,
-    // profiles/r03/fused_ab.md), although the eager kernel times favour it (402.8 vs 397.0 + 9.5 us)
+    // in-kernel combine by the fused FFN (tuning.fused_combine; single GPU, one combine task
+    // per CTA). Into device memory the combine kernel after the fused FFN is faster: graph-
+    // replayed 64-token decode 0.4066-0.4073 ms in-kernel vs 0.4029-0.4036 ms (3 of 3
+    // interleaved rounds, profiles/r03/fused_ab.md). Into mapped host memory (moe_forward_host,
+    // the default auto mode) the in-kernel combine wins: each 256-column slice crosses the
+    // host link as soon as its w2 tiles are done instead of the whole output after the last
+    // tile -- e2e 0.4155-0.4156 vs 0.4183-0.4184 ms (3 of 3)
     c->fcomb = moe_ctx::FusedCombine{};
     c->fcomb_done = false;
-    if (!tp && c->fused_combine_mode == 1 && T <= 256) {
+    const bool fcomb_want = c->fused_combine_mode == 1 || (c->fused_combine_mode == 0 && c->host_out_now);
+    if (!tp && fcomb_want && T <= 256) {
         c->fcomb.on = true;
         c->fcomb.T = T;
         c->fcomb.x = residual ? tokens : nullptr;

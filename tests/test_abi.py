@@ -84,7 +84,7 @@ def test_tuning_validation():
                                                         "swap_nb_cap": 32, "weight_hint": 3})
     moe.moe_packed_sizes(ok)
     for bad in ({"pair_nblk": 3}, {"swap_pair": 3}, {"weight_hint": 4}, {"swap_nb_cap": 48}, {"g1_grid": -1}, {"g2_swap_rows": -5},
-                {"fused": 3}, {"fused_splits": 9}, {"fused_stages": -1}, {"fused_combine": 2}, {"fused_chain": 2},
+                {"fused": 3}, {"fused_splits": 9}, {"fused_stages": -1}, {"fused_combine": 3}, {"fused_chain": 2},
                 {"fused_uniform": 5}):
         with pytest.raises(moe.MoEError) as ei:
             moe.moe_packed_sizes(moe.make_config(4096, 14336, 8, 2, 64, tuning=bad))

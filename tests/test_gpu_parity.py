@@ -357,6 +357,38 @@ def test_host_entry_point(moe):
     blk.close()
 
 
+@pytest.mark.parametrize("residual", [False, True])
+def test_host_entry_point_fused_combine(moe, residual):
+    """moe_forward_host into pinned (mapped) host memory with the fused FFN: the auto mode of
+    tuning fused_combine runs step a9 inside the fused kernel there (one launch fewer, each
+    output slice crossing the host link as its w2 tiles finish) -- bit-identical to the device
+    forward with the combine kernel; pageable output keeps the combine kernel."""
+    shape = synth.MoEShape(T=64, d=512, f=1024, E=8, k=2)
+    inp = synth.make_inputs(shape, 8100 + residual, device="cuda")
+    flags = moe.MOE_FLAG_RESIDUAL if residual else 0
+    blk = _block(moe, inp, 2, 64, flags=flags, tuning={"fused": 2})
+    n0 = moe.moe_launch_count(blk.ctx)
+    ref = blk.forward(inp["x"]).cpu()
+    torch.cuda.synchronize()
+    n_dev = moe.moe_launch_count(blk.ctx) - n0
+    xh = inp["x"].cpu().pin_memory()
+    oh = torch.empty_like(xh).pin_memory()
+    for _ in range(3):
+        n0 = moe.moe_launch_count(blk.ctx)
+        moe.moe_forward_host(blk.ctx, xh, 64, blk.router_w, blk.w13, blk.w2, oh)
+        torch.cuda.synchronize()
+        n_host = moe.moe_launch_count(blk.ctx) - n0
+        assert torch.equal(oh.view(torch.int16), ref.view(torch.int16))
+    assert n_dev == 4 and n_host == 3, (n_dev, n_host)  # router, permute, fused FFN (+ combine kernel)
+    op = torch.zeros_like(inp["x"].cpu())  # pageable: staging buffer + copy, combine kernel
+    n0 = moe.moe_launch_count(blk.ctx)
+    moe.moe_forward_host(blk.ctx, inp["x"].cpu(), 64, blk.router_w, blk.w13, blk.w2, op)
+    torch.cuda.synchronize()
+    assert moe.moe_launch_count(blk.ctx) - n0 == 4
+    assert torch.equal(op.view(torch.int16), ref.view(torch.int16))
+    blk.close()
+
+
 # ---------------------------------------------------------------- full size (BASELINE configs[1], [2])
 @pytest.fixture(scope="module")
 def mixtral_weights():
