@@ -399,6 +399,24 @@ def mixtral_weights():
     return w, host
 
 
+def test_c2_host_entry_point(moe, mixtral_weights):
+    """The e2e call bench.py times (moe_forward_host, pinned host buffers) at Mixtral size in the
+    bench's default configuration (fused FFN; in-kernel combine for the mapped host output):
+    bit-identical to the device-resident forward over back-to-back calls."""
+    w, _ = mixtral_weights
+    x = synth.make_tokens(64, 4096, seed=8200, device="cuda")
+    blk = moe.MoEBlock(w["wg"], w["w1"], w["w3"], w["w2"], top_k=2, max_tokens=64)
+    ref = blk.forward(x).cpu()
+    xh = x.cpu().pin_memory()
+    oh = torch.empty_like(xh).pin_memory()
+    for _ in range(4):
+        oh.zero_()
+        moe.moe_forward_host(blk.ctx, xh, 64, blk.router_w, blk.w13, blk.w2, oh)
+        torch.cuda.synchronize()
+        assert torch.equal(oh.view(torch.int16), ref.view(torch.int16))
+    blk.close()
+
+
 @pytest.mark.parametrize("seed", [0, 1, 2, 3, 4])  # SURVEY 8(d): C2 x 5 parity seeds
 def test_c2_decode_full(moe, mixtral_weights, seed):
     """64-token decode at Mixtral size, all tokens checked against the oracle."""
